@@ -276,7 +276,7 @@ def register(x, y, *, omega=0.7, beta=2.0, lambda_reg=10.0, iterations=100,
     trace = np.zeros(max(iterations, 1))
     it = C.c_int()
     s0 = C.c_double()
-    timing = np.zeros(6)
+    timing = np.zeros(7)
     diag = np.zeros(2, dtype=np.int64)
     bu = bl = None
     brank = 0
@@ -290,7 +290,7 @@ def register(x, y, *, omega=0.7, beta=2.0, lambda_reg=10.0, iterations=100,
                               int(early_stop), _ptr(bu), _ptr(bl), _I64(brank), _ptr(out_x),
                               _ptr(out_w), _ptr(trace), C.byref(it), C.byref(s0),
                               _ptr(timing), diag.ctypes.data_as(C.POINTER(C.c_int64))))
-    keys = ["t_c", "t_eig", "t_iter", "t_f", "t_o", "t_total"]
+    keys = ["t_c", "t_eig", "t_iter", "t_f", "t_o", "t_total", "t_loop"]
     return Result(np.ascontiguousarray(out_x), np.ascontiguousarray(out_w),
                   trace[: it.value].copy(), s0.value, dict(zip(keys, timing.tolist())),
                   int(diag[0]), int(diag[1]))

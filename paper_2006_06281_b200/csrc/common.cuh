@@ -1,0 +1,93 @@
+// common.cuh — shared device helpers for the B200 Fast-CPD hot path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "fcpd_capi.h"
+
+namespace fcpd {
+
+// Error carried from the engine to the C-ABI boundary; `code` is one of the
+// FCPD_ERR_* values of include/fcpd_capi.h.
+struct Failure : std::runtime_error {
+  int code;
+  Failure(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define FCPD_CUDA(call)                                                         \
+  do {                                                                          \
+    cudaError_t e_ = (call);                                                    \
+    if (e_ != cudaSuccess)                                                      \
+      throw ::fcpd::Failure(e_ == cudaErrorMemoryAllocation ? FCPD_ERR_OOM       \
+                                                            : FCPD_ERR_CUDA,     \
+                            std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define FCPD_LAUNCH_CHECK() FCPD_CUDA(cudaGetLastError())
+
+constexpr double kSigma2Floor = 1e-10;      // correspondence.hpp:12
+constexpr double kLog2e = 1.4426950408889634;
+// log2(1e-300): rows whose raw posterior mass is below 1e-300 fall back to
+// the uniform row (correspondence.hpp:89).
+constexpr double kLog2DegenerateRow = -996.5784284662087;
+
+// Device error slots (first error wins).  Codes mirror the reference's
+// NumericError sites so the host can rebuild the reference message.
+enum DevErr : int {
+  kDevOk = 0,
+  kDevSolveDiag = 1,    // solvers.hpp:68-69
+  kDevNegVariance = 2,  // solvers.hpp:173-174
+};
+
+// Per-iteration scalars living in device memory so a captured CUDA graph can
+// replay iterations without host round trips.
+struct IterState {
+  double sigma2;        // σ² entering this iteration (unclamped, as the reference)
+  double sigma2_e;      // max(σ², 1e-10): the value the E-step uses
+  double log2c;         // outlier constant in log2 units (only if ω>0)
+  float sx;             // sqrt(log2e / (2 σ²_e)): coordinate pre-scale
+  float pad0;
+  int32_t active;       // 0 after early stop → kernels return immediately
+  int32_t iter;         // iteration index
+  int32_t err_code;
+  int32_t err_iter;
+  double err_value;
+  int64_t degenerate_rows;  // cumulative
+  int64_t sigma2_clamps;    // cumulative
+  int32_t iters_run;
+  int32_t pad1;
+};
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void set_error(IterState* st, int code, double value) {
+  if (atomicCAS(&st->err_code, 0, code) == 0) {
+    st->err_iter = st->iter;
+    st->err_value = value;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace fcpd

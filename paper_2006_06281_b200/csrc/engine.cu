@@ -1,0 +1,909 @@
+// engine.cu — host orchestration + C ABI (include/fcpd_capi.h).
+//
+// register_pointsets (registration.hpp:79-175) as a device-resident loop:
+//   validate → normalize_pair (host, fp64, O(M+N)) → upload →
+//   spectral setup (cached per context) → init_sigma2 → one CUDA graph per
+//   EM iteration, replayed `iterations` times with no host round trip →
+//   one read-back (σ² trace, x̃, W, diagnostics, device phase timestamps).
+
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "estep.cuh"
+#include "mstep.cuh"
+#include "setup.cuh"
+
+namespace fcpd {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t0) {
+  return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    FCPD_CUDA(cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)));
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+uint64_t fnv1a(const void* data, size_t bytes, uint64_t h = 1469598103934665603ull) {
+  const unsigned char* c = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < bytes; ++i) {
+    h ^= c[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+// ------------------------------------------------------------- small kernels
+
+// Dense materialisation of the last E-step's P (or row-constrained P̃) in fp64,
+// from the per-column normalisers and per-row masses (debug / small M·N).
+__global__ void dense_posterior_kernel(const double* __restrict__ xt64, int64_t m,
+                                       const double* __restrict__ y64, int64_t n,
+                                       const double* __restrict__ b2,
+                                       const double* __restrict__ log2p1,
+                                       const int32_t* __restrict__ degenerate, int row_constrain,
+                                       const IterState* __restrict__ st, double* __restrict__ p) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t j = blockIdx.y;
+  if (i >= m) return;
+  if (row_constrain && degenerate[i]) {
+    p[j * m + i] = 1.0 / static_cast<double>(n);
+    return;
+  }
+  double d2 = 0.0;
+  for (int c = 0; c < 3; ++c) {
+    const double t = y64[c * n + j] - xt64[c * m + i];
+    d2 += t * t;
+  }
+  const double k2 = kLog2e / (2.0 * st->sigma2_e);
+  double e = b2[j] - d2 * k2;
+  if (row_constrain) e -= log2p1[i];
+  p[j * m + i] = exp2(e);
+}
+
+// W = Q c (coefficients), fp64 accumulation over the fp32 basis.
+__global__ void coef_kernel(const float* __restrict__ qt, int64_t mpad, int64_t m, int64_t k,
+                            const double* __restrict__ coef, double* __restrict__ w) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double a0 = 0, a1 = 0, a2 = 0;
+  for (int64_t j = 0; j < k; ++j) {
+    const double q = qt[j * mpad + i];
+    a0 += q * coef[j];
+    a1 += q * coef[k + j];
+    a2 += q * coef[2 * k + j];
+  }
+  w[i] = a0;
+  w[m + i] = a1;
+  w[2 * m + i] = a2;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ Session
+
+struct Session {
+  int64_t m = 0, n = 0;
+  int d = 0;
+  fcpd_config cfg{};
+  int capacity = 0;  // trace slots
+  int launched = 0;  // iterations enqueued since session_begin
+  int64_t h2d = 0, d2h = 0;  // bytes copied by the current call
+  bool ready = false;
+  // normalisation record (pointset.hpp:31-43)
+  double center[3] = {0, 0, 0};
+  double scale = 1.0;
+  double sigma2_initial = 0.0;
+  double t_setup_host = 0.0, t_eig = 0.0, t_gram = 0.0;
+  bool basis_reused = false;
+
+  DevBuf<double> x0, xt64, xt_prev, y64;
+  DevBuf<float4> xt4, y4b, resid4, g4;
+  DevBuf<double> b2, pt1, col_part, row_part, ptilde_y, var, log2p1, zpart, vpart, coef,
+      sig_part, trace;
+  DevBuf<int32_t> col_flags, row_flags, flags_count, degenerate;
+  DevBuf<uint64_t> stamps;
+  DevBuf<IterState> st;
+
+  YStats ystats{};
+  EStepPlan ep;
+  ColsumPlan zp, vp;
+  cudaGraphExec_t graph = nullptr;
+
+  void release_graph() {
+    if (graph) cudaGraphExecDestroy(graph);
+    graph = nullptr;
+  }
+  void release() {
+    release_graph();
+    for (auto* b : {&x0, &xt64, &xt_prev, &y64, &b2, &pt1, &col_part, &row_part, &ptilde_y,
+                    &var, &log2p1, &zpart, &vpart, &coef, &sig_part, &trace})
+      b->release();
+    for (auto* b : {&xt4, &y4b, &resid4, &g4}) b->release();
+    for (auto* b : {&col_flags, &row_flags, &flags_count, &degenerate}) b->release();
+    stamps.release();
+    st.release();
+  }
+};
+
+}  // namespace fcpd
+
+struct fcpd_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  std::string err;
+  fcpd::Basis basis;
+  fcpd::Session sess;
+};
+
+namespace fcpd {
+namespace {
+
+int fail(fcpd_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+template <typename F>
+int guarded(fcpd_ctx* ctx, F&& f) {
+  if (!ctx) return FCPD_ERR_PARAMETER;
+  try {
+    FCPD_CUDA(cudaSetDevice(ctx->device));
+    f();
+    ctx->err.clear();
+    return FCPD_OK;
+  } catch (const Failure& e) {
+    return fail(ctx, e.code, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(ctx, FCPD_ERR_OOM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(ctx, FCPD_ERR_CUDA, e.what());
+  }
+}
+
+// pack a column-major M×D fp64 host point set into fp64 SoA(3) + float4
+void pack_points(const double* src, int64_t cnt, int d, std::vector<double>& soa3,
+                 std::vector<float4>& f4) {
+  soa3.assign(3 * cnt, 0.0);
+  f4.resize(cnt);
+  for (int c = 0; c < d; ++c) std::memcpy(&soa3[c * cnt], src + c * cnt, sizeof(double) * cnt);
+  for (int64_t i = 0; i < cnt; ++i)
+    f4[i] = make_float4(static_cast<float>(soa3[i]), static_cast<float>(soa3[cnt + i]),
+                        static_cast<float>(soa3[2 * cnt + i]), 0.f);
+}
+
+void validate_register(const double* x, int64_t m, const double* y, int64_t n, int d,
+                       const fcpd_config& cfg) {
+  // registration.hpp:82-86
+  if (m <= 0 || n <= 0 || !x || !y) throw Failure(FCPD_ERR_PARAMETER, "register: empty point set");
+  if (d < 1) throw Failure(FCPD_ERR_DIMENSION, "register: model and scene dimension mismatch");
+  if (cfg.iterations < 0) throw Failure(FCPD_ERR_PARAMETER, "register: negative iterations");
+  if (d > 3)
+    throw Failure(FCPD_ERR_DIMENSION, "register: the B200 path supports D <= 3, got D=" +
+                                          std::to_string(d));
+  if (cfg.variant != FCPD_VARIANT_FAST && cfg.variant != FCPD_VARIANT_FAST_LOWRANK)
+    throw Failure(FCPD_ERR_PARAMETER,
+                  "register: only the fast / fast_lowrank variants run on the B200 path");
+  if (m > INT32_MAX || n > INT32_MAX) throw Failure(FCPD_ERR_PARAMETER, "register: too many points");
+}
+
+int64_t lowrank_rank(double fraction, int64_t m) {  // solvers.hpp:46-54
+  if (fraction <= 0.0 || fraction > 1.0)
+    throw Failure(FCPD_ERR_PARAMETER, "rank_fraction must lie in (0, 1]");
+  int64_t k = std::llround(fraction * static_cast<double>(m));
+  return std::max<int64_t>(1, std::min<int64_t>(k, m));
+}
+
+void ensure_basis(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa) {
+  const bool lowrank = s.cfg.variant == FCPD_VARIANT_FAST_LOWRANK;
+  const int64_t rank = lowrank ? lowrank_rank(s.cfg.rank_fraction, s.m) : s.m;
+  if (!(s.cfg.beta > 0.0)) throw Failure(FCPD_ERR_PARAMETER, "build_gram: beta must be positive");
+  uint64_t h = fnv1a(x_soa.data(), sizeof(double) * x_soa.size());
+  h = fnv1a(&s.m, sizeof s.m, h);
+  h = fnv1a(&rank, sizeof rank, h);
+  Basis& b = ctx->basis;
+  if (b.q && b.key_hash == h && b.key_beta == s.cfg.beta && b.m == s.m && b.k == rank &&
+      b.key_variant == s.cfg.variant) {
+    s.basis_reused = true;
+    s.t_eig = 0.0;
+    s.t_gram = 0.0;
+    return;
+  }
+  s.basis_reused = false;
+  b.release();
+  if (s.m > 46000)
+    throw Failure(FCPD_ERR_PARAMETER,
+                  "eigendecompose: dense device eigensolver limited to M <= 46000 "
+                  "(top-K on-the-fly setup not built yet)");
+  double* phi = nullptr;
+  FCPD_CUDA(cudaMalloc(&phi, sizeof(double) * s.m * s.m));
+  try {
+    const auto t0 = Clock::now();
+    build_gram_device(s.x0.p, s.m, s.d, s.cfg.beta, phi, s.m, ctx->stream);
+    FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
+    s.t_gram = since(t0);
+    const auto t1 = Clock::now();
+    dense_eigensolve(ctx->solver, phi, s.m, rank, b, nullptr, ctx->stream);
+    upload_lambda(b, !lowrank, ctx->stream);
+    s.t_eig = since(t1);
+  } catch (...) {
+    cudaFree(phi);
+    throw;
+  }
+  cudaFree(phi);
+  b.key_hash = h;
+  b.key_beta = s.cfg.beta;
+  b.key_variant = s.cfg.variant;
+  b.t_gram = s.t_gram;
+  b.t_eig = s.t_eig;
+}
+
+// ev (optional, 7 events): recorded before the iteration and after each of
+// pass 1, pass 2, Qᵀ·R, z-reduce/filter, Q·g, transform/σ² (eager profiling).
+void enqueue_iteration(fcpd_ctx* ctx, Session& s, cudaEvent_t* ev = nullptr) {
+  Basis& b = ctx->basis;
+  IterState* st = s.st.p;
+  cudaStream_t str = ctx->stream;
+  EStepBuffers eb{};
+  eb.xt4 = s.xt4.p;
+  eb.xt64 = s.xt64.p;
+  eb.y4b = s.y4b.p;
+  eb.b2 = s.b2.p;
+  eb.pt1 = nullptr;
+  eb.col_part = s.col_part.p;
+  eb.row_part = s.row_part.p;
+  eb.col_flags = s.col_flags.p;
+  eb.row_flags = s.row_flags.p;
+  eb.flags_count = s.flags_count.p;
+  eb.out = RowOut{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p, s.resid4.p, s.x0.p};
+  eb.ystats = s.ystats;
+  auto rec = [&](int i) {
+    if (ev) FCPD_CUDA(cudaEventRecord(ev[i], str));
+  };
+  rec(0);
+  launch_estep(s.ep, eb, s.m, s.n, s.d, s.cfg.omega, st, s.stamps.p, str, ev ? ev[1] : nullptr);
+  rec(2);
+  launch_colsum(s.zp, b.q, b.kpad, s.m, s.resid4.p, s.zpart.p, b.kpad, st, s.stamps.p, 1, str);
+  rec(3);
+  launch_zreduce(s.zpart.p, s.zp.row_blocks, b.k, b.kpad, b.lam, b.lam + b.k, s.cfg.lambda_reg,
+                 s.coef.p, s.g4.p, st, str);
+  rec(4);
+  launch_colsum(s.vp, b.qt, b.mpad, b.k, s.g4.p, s.vpart.p, b.mpad, st, nullptr, 0, str);
+  rec(5);
+  launch_transform_sigma(s.vpart.p, s.vp.row_blocks, s.m, b.mpad, s.x0.p, s.xt64.p,
+                         s.xt_prev.p, s.xt4.p, s.ptilde_y.p, s.var.p, s.sig_part.p, s.d,
+                         s.cfg.early_stop, s.trace.p, st, s.stamps.p, str);
+  rec(6);
+}
+
+}  // namespace
+}  // namespace fcpd
+
+namespace fcpd {
+namespace {
+
+// Upload points, plan kernels, allocate per-session device buffers.
+// x_soa/y_soa are fp64 SoA(3) host arrays already normalised.
+void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa,
+                     const std::vector<double>& y_soa, int capacity, bool need_mstep) {
+  const int64_t m = s.m, n = s.n;
+  cudaStream_t str = ctx->stream;
+  s.release_graph();
+  s.x0.ensure(3 * m);
+  s.xt64.ensure(3 * m);
+  s.xt_prev.ensure(3 * m);
+  s.y64.ensure(3 * n);
+  s.xt4.ensure(m);
+  s.y4b.ensure(n);
+  s.resid4.ensure(m);
+  s.b2.ensure(n);
+  s.pt1.ensure(n);
+  s.ptilde_y.ensure(3 * m);
+  s.var.ensure(m);
+  s.log2p1.ensure(m);
+  s.degenerate.ensure(m);
+  s.col_flags.ensure(n);
+  s.row_flags.ensure(m);
+  s.flags_count.ensure(2);
+  s.st.ensure(1);
+  s.capacity = std::max(capacity, 1);
+  s.trace.ensure(s.capacity);
+  s.stamps.ensure(4 * static_cast<size_t>(s.capacity));
+  s.ep = make_estep_plan(m, n, ctx->sm_count);
+  s.col_part.ensure(static_cast<size_t>(s.ep.col_splits) * n);
+  s.row_part.ensure(static_cast<size_t>(s.ep.row_splits) * 5 * m);
+  s.sig_part.ensure(ceil_div(m, 256));
+
+  std::vector<float4> x4(m), y4(n);
+  for (int64_t i = 0; i < m; ++i)
+    x4[i] = make_float4(static_cast<float>(x_soa[i]), static_cast<float>(x_soa[m + i]),
+                        static_cast<float>(x_soa[2 * m + i]), 0.f);
+  for (int64_t i = 0; i < n; ++i)
+    y4[i] = make_float4(static_cast<float>(y_soa[i]), static_cast<float>(y_soa[n + i]),
+                        static_cast<float>(y_soa[2 * n + i]), 0.f);
+  FCPD_CUDA(cudaMemcpyAsync(s.x0.p, x_soa.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, str));
+  FCPD_CUDA(cudaMemcpyAsync(s.xt64.p, s.x0.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, str));
+  FCPD_CUDA(cudaMemcpyAsync(s.xt_prev.p, s.x0.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, str));
+  FCPD_CUDA(cudaMemcpyAsync(s.y64.p, y_soa.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice, str));
+  FCPD_CUDA(cudaMemcpyAsync(s.xt4.p, x4.data(), sizeof(float4) * m, cudaMemcpyHostToDevice, str));
+  FCPD_CUDA(cudaMemcpyAsync(s.y4b.p, y4.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, str));
+  s.h2d += (sizeof(double) * 3 + sizeof(float4)) * (m + n);
+
+  // scene statistics for the uniform-row fallback (fp64, fixed order)
+  YStats ys{};
+  for (int c = 0; c < 3; ++c) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) acc += y_soa[c * n + i];
+    ys.mean[c] = acc / static_cast<double>(n);
+  }
+  double sq = 0.0;
+  for (int64_t i = 0; i < n; ++i)
+    sq += y_soa[i] * y_soa[i] + y_soa[n + i] * y_soa[n + i] + y_soa[2 * n + i] * y_soa[2 * n + i];
+  ys.sq_mean = sq / static_cast<double>(n);
+  s.ystats = ys;
+
+  if (need_mstep) {
+    Basis& b = ctx->basis;
+    s.zp = make_colsum_plan(m, b.k, ctx->sm_count);
+    s.vp = make_colsum_plan(b.k, m, ctx->sm_count);
+    s.zpart.ensure(static_cast<size_t>(s.zp.row_blocks) * 3 * b.kpad);
+    s.vpart.ensure(static_cast<size_t>(s.vp.row_blocks) * 3 * b.mpad);
+    s.coef.ensure(3 * b.k);
+    s.g4.ensure(b.k);
+  }
+}
+
+void reset_state(fcpd_ctx* ctx, Session& s, double sigma2) {
+  IterState h{};
+  h.sigma2 = sigma2;
+  h.sigma2_e = sigma2;
+  h.active = 1;
+  FCPD_CUDA(cudaMemcpyAsync(s.st.p, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
+  FCPD_CUDA(cudaMemsetAsync(s.degenerate.p, 0, sizeof(int32_t) * s.m, ctx->stream));
+}
+
+// registration.hpp:59-69 (host, fp64, same formula)
+double init_sigma2_host(const std::vector<double>& x, int64_t m, const std::vector<double>& y,
+                        int64_t n, int d) {
+  double fx = 0.0, fy = 0.0, dot = 0.0;
+  for (int c = 0; c < d; ++c) {
+    double sx = 0.0, sy = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+      fx += x[c * m + i] * x[c * m + i];
+      sx += x[c * m + i];
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      fy += y[c * n + i] * y[c * n + i];
+      sy += y[c * n + i];
+    }
+    dot += sx * sy;
+  }
+  const double md = static_cast<double>(m), nd = static_cast<double>(n);
+  return std::max((md * fy + nd * fx - 2.0 * dot) / (static_cast<double>(d) * md * nd), 0.0);
+}
+
+void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n, int d,
+                   const fcpd_config& cfg) {
+  validate_register(x, m, y, n, d, cfg);
+  const auto t0 = Clock::now();
+  Session& s = ctx->sess;
+  s.ready = false;
+  s.h2d = s.d2h = 0;
+  s.m = m;
+  s.n = n;
+  s.d = d;
+  s.cfg = cfg;
+  // normalize_pair (pointset.hpp:124-148), fp64 on the host: O(M+N)
+  std::vector<double> xs(3 * m, 0.0), ys(3 * n, 0.0);
+  s.center[0] = s.center[1] = s.center[2] = 0.0;
+  s.scale = 1.0;
+  if (cfg.normalize) {
+    const double total = static_cast<double>(m + n);
+    for (int c = 0; c < d; ++c) {
+      double sx = 0.0, sy = 0.0;
+      for (int64_t i = 0; i < m; ++i) sx += x[c * m + i];
+      for (int64_t i = 0; i < n; ++i) sy += y[c * n + i];
+      s.center[c] = (sx + sy) / total;
+    }
+    double sc = 0.0;
+    for (int c = 0; c < d; ++c) {
+      for (int64_t i = 0; i < m; ++i) sc = std::max(sc, std::fabs(x[c * m + i] - s.center[c]));
+      for (int64_t i = 0; i < n; ++i) sc = std::max(sc, std::fabs(y[c * n + i] - s.center[c]));
+    }
+    if (sc <= 0.0) sc = 1.0;
+    s.scale = sc;
+    for (int c = 0; c < d; ++c) {
+      for (int64_t i = 0; i < m; ++i) xs[c * m + i] = (x[c * m + i] - s.center[c]) / sc;
+      for (int64_t i = 0; i < n; ++i) ys[c * n + i] = (y[c * n + i] - s.center[c]) / sc;
+    }
+  } else {
+    for (int c = 0; c < d; ++c) {
+      std::memcpy(&xs[c * m], x + c * m, sizeof(double) * m);
+      std::memcpy(&ys[c * n], y + c * n, sizeof(double) * n);
+    }
+  }
+  // x0 must be on the device before the Gram build
+  s.x0.ensure(3 * m);
+  FCPD_CUDA(cudaMemcpyAsync(s.x0.p, xs.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice,
+                            ctx->stream));
+  ensure_basis(ctx, s, xs);
+  prepare_buffers(ctx, s, xs, ys, cfg.iterations, true);
+  s.sigma2_initial = init_sigma2_host(xs, m, ys, n, d);
+  if (cfg.iterations > 0 && !(cfg.omega >= 0.0 && cfg.omega < 1.0))
+    throw Failure(FCPD_ERR_NUMERIC,
+                  "register: iteration 0: posterior: omega must lie in [0, 1)");
+  reset_state(ctx, s, s.sigma2_initial);
+  FCPD_CUDA(cudaMemsetAsync(s.coef.p, 0, sizeof(double) * 3 * ctx->basis.k, ctx->stream));
+
+  // capture one EM iteration as a CUDA graph
+  cudaGraph_t g = nullptr;
+  FCPD_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    enqueue_iteration(ctx, s);
+  } catch (...) {
+    cudaStreamEndCapture(ctx->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  FCPD_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  FCPD_CUDA(ie);
+  s.graph = exec;
+  FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
+  s.t_setup_host = since(t0);
+  s.launched = 0;
+  s.ready = true;
+}
+
+void session_run(fcpd_ctx* ctx, int iters) {
+  Session& s = ctx->sess;
+  if (!s.ready) throw Failure(FCPD_ERR_PARAMETER, "session: not started");
+  if (iters < 0 || s.launched + iters > s.capacity)
+    throw Failure(FCPD_ERR_PARAMETER, "session: more iterations than cfg.iterations");
+  s.launched += iters;
+  for (int i = 0; i < iters; ++i) FCPD_CUDA(cudaGraphLaunch(s.graph, ctx->stream));
+}
+
+void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
+  Session& s = ctx->sess;
+  Basis& b = ctx->basis;
+  cudaStream_t str = ctx->stream;
+  IterState h{};
+  FCPD_CUDA(cudaMemcpyAsync(&h, s.st.p, sizeof h, cudaMemcpyDeviceToHost, str));
+  FCPD_CUDA(cudaStreamSynchronize(str));
+  s.d2h += sizeof h;
+  if (h.err_code != 0) {
+    std::string what;
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%f", h.err_value);
+    if (h.err_code == kDevSolveDiag) what = "solve_fast: lambda_i + lambda*sigma2 not positive";
+    else what = std::string("update_sigma2: negative variance ") + buf;
+    throw Failure(FCPD_ERR_NUMERIC, "register: iteration " + std::to_string(h.err_iter) + ": " + what);
+  }
+  const int64_t m = s.m, n = s.n;
+  const int d = s.d;
+  const int run = h.iters_run;
+  if (!out) return;
+  out->iterations_run = run;
+  out->basis_reused = s.basis_reused ? 1 : 0;
+  out->sigma2_initial = s.sigma2_initial;
+  out->degenerate_rows = h.degenerate_rows;
+  out->sigma2_clamps = h.sigma2_clamps;
+  if (out->sigma2_trace && run > 0)
+    FCPD_CUDA(cudaMemcpyAsync(out->sigma2_trace, s.trace.p, sizeof(double) * run,
+                              cudaMemcpyDeviceToHost, str));
+  s.d2h += sizeof(double) * (run + 3 * m);
+  std::vector<double> xt(3 * m);
+  FCPD_CUDA(cudaMemcpyAsync(xt.data(), s.xt64.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, str));
+  if (out->coefficients) {
+    DevBuf<double> w;
+    w.ensure(3 * m);
+    coef_kernel<<<ceil_div(m, 128), 128, 0, str>>>(b.qt, b.mpad, m, b.k, s.coef.p, w.p);
+    FCPD_LAUNCH_CHECK();
+    FCPD_CUDA(cudaMemcpyAsync(out->coefficients, w.p, sizeof(double) * d * m,
+                              cudaMemcpyDeviceToHost, str));
+    s.d2h += sizeof(double) * d * m;
+    FCPD_CUDA(cudaStreamSynchronize(str));
+    w.release();
+  }
+  if (out->correspondence && run > 0) {
+    DevBuf<double> p;
+    p.ensure(static_cast<size_t>(m) * n);
+    dense_posterior_kernel<<<dim3(ceil_div(m, 128), static_cast<unsigned>(n)), 128, 0, str>>>(
+        s.xt_prev.p, m, s.y64.p, n, s.b2.p, s.log2p1.p, s.degenerate.p, 1, s.st.p, p.p);
+    FCPD_LAUNCH_CHECK();
+    FCPD_CUDA(cudaMemcpyAsync(out->correspondence, p.p, sizeof(double) * m * n,
+                              cudaMemcpyDeviceToHost, str));
+    s.d2h += sizeof(double) * m * n;
+    FCPD_CUDA(cudaStreamSynchronize(str));
+    p.release();
+  }
+  if (out->degenerate_mask)
+    FCPD_CUDA(cudaMemcpyAsync(out->degenerate_mask, s.degenerate.p, sizeof(int32_t) * m,
+                              cudaMemcpyDeviceToHost, str));
+  if (out->degenerate_mask) s.d2h += sizeof(int32_t) * m;
+  std::vector<uint64_t> stamps(4 * static_cast<size_t>(std::max(run, 1)));
+  if (run > 0)
+    FCPD_CUDA(cudaMemcpyAsync(stamps.data(), s.stamps.p, sizeof(uint64_t) * 4 * run,
+                              cudaMemcpyDeviceToHost, str));
+  s.d2h += sizeof(uint64_t) * 4 * run;
+  FCPD_CUDA(cudaStreamSynchronize(str));
+  if (out->transformed) {
+    for (int c = 0; c < d; ++c)
+      for (int64_t i = 0; i < m; ++i)
+        out->transformed[c * m + i] =
+            s.cfg.normalize ? xt[c * m + i] * s.scale + s.center[c] : xt[c * m + i];
+  }
+  // phases (registration.hpp:120-147): t_c = E-step; t_iter = residual +
+  // solve (Qᵀ R, filter, Q g); t_o = transform epilogue + σ² + everything else
+  double tc = 0.0, ti = 0.0;
+  for (int it = 0; it < run; ++it) {
+    const uint64_t* st4 = &stamps[4 * it];
+    tc += 1e-9 * static_cast<double>(st4[1] - st4[0]);
+    ti += 1e-9 * static_cast<double>(st4[2] - st4[1]);
+  }
+  fcpd_timing& t = out->timing;
+  t.t_c = tc;
+  t.t_eig = s.t_eig;
+  t.t_iter = ti;
+  t.t_f = t.t_eig + t.t_iter;
+  t.t_o = std::max(wall - t.t_c - t.t_f, 0.0);
+  t.t_total = t.t_c + t.t_f + t.t_o;
+  t.t_setup = s.t_gram + s.t_eig;
+  out->h2d_bytes = s.h2d;
+  out->d2h_bytes = s.d2h;
+}
+
+}  // namespace
+}  // namespace fcpd
+
+// ============================================================== C ABI
+
+using namespace fcpd;
+
+extern "C" {
+
+void fcpd_config_default(fcpd_config* cfg) {
+  if (!cfg) return;
+  cfg->omega = 0.7;
+  cfg->beta = 2.0;
+  cfg->lambda_reg = 10.0;
+  cfg->iterations = 100;
+  cfg->variant = FCPD_VARIANT_FAST;
+  cfg->rank_fraction = 0.1;
+  cfg->seed = 0;
+  cfg->normalize = 1;
+  cfg->early_stop = 0;
+}
+
+const char* fcpd_version(void) { return "fcpd-b200 0.1 (sm_100a)"; }
+
+int fcpd_create(fcpd_ctx** out, int device) {
+  if (!out) return FCPD_ERR_PARAMETER;
+  *out = nullptr;
+  auto* ctx = new (std::nothrow) fcpd_ctx();
+  if (!ctx) return FCPD_ERR_OOM;
+  ctx->device = device;
+  try {
+    FCPD_CUDA(cudaSetDevice(device));
+    int sms = 0;
+    FCPD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    ctx->sm_count = sms;
+    FCPD_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    if (cusolverDnCreate(&ctx->solver) != CUSOLVER_STATUS_SUCCESS)
+      throw Failure(FCPD_ERR_CUDA, "cusolverDnCreate failed");
+  } catch (const Failure& e) {
+    static thread_local std::string last;
+    last = e.what();
+    delete ctx;
+    return e.code;
+  }
+  *out = ctx;
+  return FCPD_OK;
+}
+
+void fcpd_destroy(fcpd_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  ctx->sess.release();
+  ctx->basis.release();
+  if (ctx->solver) cusolverDnDestroy(ctx->solver);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* fcpd_last_error(const fcpd_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void* fcpd_stream(fcpd_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int32_t fcpd_kernels_per_iteration(const fcpd_ctx*) {
+  // prologue, col, col-combine, col-fallback, row, row-combine,
+  // row-fallback, Qᵀ·R, z-reduce/filter, Q·g, transform/σ²-rows, σ²-final
+  return 12;
+}
+
+int fcpd_register(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n,
+                  int32_t d, const fcpd_config* cfg, fcpd_result* out) {
+  return guarded(ctx, [&] {
+    if (!cfg) throw Failure(FCPD_ERR_PARAMETER, "register: null config");
+    const auto t0 = Clock::now();
+    session_begin(ctx, x, m, y, n, d, *cfg);
+    session_run(ctx, cfg->iterations);
+    FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
+    session_read(ctx, out, since(t0));
+  });
+}
+
+int fcpd_session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n,
+                       int32_t d, const fcpd_config* cfg) {
+  return guarded(ctx, [&] {
+    if (!cfg) throw Failure(FCPD_ERR_PARAMETER, "session: null config");
+    session_begin(ctx, x, m, y, n, d, *cfg);
+  });
+}
+
+int fcpd_session_run(fcpd_ctx* ctx, int32_t iterations) {
+  return guarded(ctx, [&] { session_run(ctx, iterations); });
+}
+
+int fcpd_session_sync(fcpd_ctx* ctx) {
+  return guarded(ctx, [&] { FCPD_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int fcpd_session_read(fcpd_ctx* ctx, fcpd_result* out) {
+  return guarded(ctx, [&] { session_read(ctx, out, 0.0); });
+}
+
+int fcpd_session_profile(fcpd_ctx* ctx, int32_t iterations, double* ms_per_phase) {
+  return guarded(ctx, [&] {
+    Session& s = ctx->sess;
+    if (!s.ready) throw Failure(FCPD_ERR_PARAMETER, "session: not started");
+    if (iterations < 1 || s.launched + iterations > s.capacity)
+      throw Failure(FCPD_ERR_PARAMETER, "session: more iterations than cfg.iterations");
+    cudaEvent_t ev[7];
+    for (auto& e : ev) FCPD_CUDA(cudaEventCreate(&e));
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    for (int it = 0; it < iterations; ++it) {
+      enqueue_iteration(ctx, s, ev);
+      ++s.launched;
+      FCPD_CUDA(cudaEventSynchronize(ev[6]));
+      for (int p = 0; p < 6; ++p) {
+        float ms = 0.f;
+        FCPD_CUDA(cudaEventElapsedTime(&ms, ev[p], ev[p + 1]));
+        acc[p] += ms;
+      }
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    for (int p = 0; p < 6; ++p) ms_per_phase[p] = acc[p] / iterations;
+  });
+}
+
+int fcpd_estep(fcpd_ctx* ctx, const double* xt, int64_t m, const double* y, int64_t n,
+               int32_t d, double omega, double sigma2, double* ptilde_y, double* p1, double* var,
+               int32_t* degenerate, double* pt1, int32_t* clamped) {
+  return guarded(ctx, [&] {
+    if (m <= 0 || n <= 0) throw Failure(FCPD_ERR_PARAMETER, "posterior: empty point set");
+    if (d < 1 || d > 3) throw Failure(FCPD_ERR_DIMENSION, "posterior: the B200 path supports D <= 3");
+    if (!(omega >= 0.0 && omega < 1.0))
+      throw Failure(FCPD_ERR_PARAMETER, "posterior: omega must lie in [0, 1)");
+    Session& s = ctx->sess;
+    s.ready = false;
+    s.m = m;
+    s.n = n;
+    s.d = d;
+    fcpd_config_default(&s.cfg);
+    s.cfg.omega = omega;
+    std::vector<double> xs(3 * m, 0.0), ys(3 * n, 0.0);
+    for (int c = 0; c < d; ++c) {
+      std::memcpy(&xs[c * m], xt + c * m, sizeof(double) * m);
+      std::memcpy(&ys[c * n], y + c * n, sizeof(double) * n);
+    }
+    prepare_buffers(ctx, s, xs, ys, 1, false);
+    reset_state(ctx, s, sigma2);
+    EStepBuffers eb{};
+    eb.xt4 = s.xt4.p;
+    eb.xt64 = s.xt64.p;
+    eb.y4b = s.y4b.p;
+    eb.b2 = s.b2.p;
+    eb.pt1 = s.pt1.p;
+    eb.col_part = s.col_part.p;
+    eb.row_part = s.row_part.p;
+    eb.col_flags = s.col_flags.p;
+    eb.row_flags = s.row_flags.p;
+    eb.flags_count = s.flags_count.p;
+    eb.out = RowOut{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p, nullptr, nullptr};
+    eb.ystats = s.ystats;
+    launch_estep(s.ep, eb, m, n, d, omega, s.st.p, nullptr, ctx->stream);
+    std::vector<double> pty(3 * m), lp(m);
+    FCPD_CUDA(cudaMemcpyAsync(pty.data(), s.ptilde_y.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, ctx->stream));
+    FCPD_CUDA(cudaMemcpyAsync(lp.data(), s.log2p1.p, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    if (var) FCPD_CUDA(cudaMemcpyAsync(var, s.var.p, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    if (degenerate) FCPD_CUDA(cudaMemcpyAsync(degenerate, s.degenerate.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    if (pt1) FCPD_CUDA(cudaMemcpyAsync(pt1, s.pt1.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ptilde_y) std::memcpy(ptilde_y, pty.data(), sizeof(double) * d * m);
+    if (p1)
+      for (int64_t i = 0; i < m; ++i) p1[i] = std::exp2(lp[i]);
+    if (clamped) *clamped = sigma2 < kSigma2Floor ? 1 : 0;
+  });
+}
+
+int fcpd_posterior_dense(fcpd_ctx* ctx, const double* xt, int64_t m, const double* y, int64_t n,
+                         int32_t d, double omega, double sigma2, int32_t row_constrain, double* p,
+                         int32_t* clamped, int64_t* degenerate_rows, int64_t* n_degenerate) {
+  std::vector<int32_t> deg(m > 0 ? m : 1);
+  int rc = fcpd_estep(ctx, xt, m, y, n, d, omega, sigma2, nullptr, nullptr, nullptr, deg.data(),
+                      nullptr, clamped);
+  if (rc) return rc;
+  return guarded(ctx, [&] {
+    Session& s = ctx->sess;
+    DevBuf<double> dp;
+    dp.ensure(static_cast<size_t>(m) * n);
+    dense_posterior_kernel<<<dim3(ceil_div(m, 128), static_cast<unsigned>(n)), 128, 0,
+                             ctx->stream>>>(s.xt64.p, m, s.y64.p, n, s.b2.p, s.log2p1.p,
+                                            s.degenerate.p, row_constrain, s.st.p, dp.p);
+    FCPD_LAUNCH_CHECK();
+    FCPD_CUDA(cudaMemcpyAsync(p, dp.p, sizeof(double) * m * n, cudaMemcpyDeviceToHost, ctx->stream));
+    FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
+    dp.release();
+    int64_t nd = 0;
+    if (row_constrain)
+      for (int64_t i = 0; i < m; ++i)
+        if (deg[i]) {
+          if (degenerate_rows) degenerate_rows[nd] = i;
+          ++nd;
+        }
+    if (n_degenerate) *n_degenerate = nd;
+  });
+}
+
+int fcpd_build_gram(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d, double beta,
+                    double* phi) {
+  return guarded(ctx, [&] {
+    if (m <= 0 || m > 46000) throw Failure(FCPD_ERR_PARAMETER, "build_gram: M out of range for the dense path");
+    DevBuf<double> xd, g;
+    xd.ensure(static_cast<size_t>(d) * m);
+    g.ensure(static_cast<size_t>(m) * m);
+    FCPD_CUDA(cudaMemcpyAsync(xd.p, x, sizeof(double) * d * m, cudaMemcpyHostToDevice, ctx->stream));
+    build_gram_device(xd.p, m, d, beta, g.p, m, ctx->stream);
+    FCPD_CUDA(cudaMemcpyAsync(phi, g.p, sizeof(double) * m * m, cudaMemcpyDeviceToHost, ctx->stream));
+    FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
+    xd.release();
+    g.release();
+  });
+}
+
+int fcpd_build_basis(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d, double beta,
+                     int64_t rank, double* u, double* lambda, double* lambda_raw) {
+  return guarded(ctx, [&] {
+    if (m <= 0 || m > 46000) throw Failure(FCPD_ERR_PARAMETER, "eigendecompose: M out of range for the dense path");
+    if (rank < 1 || rank > m) throw Failure(FCPD_ERR_PARAMETER, "eigendecompose: rank out of [1, M]");
+    DevBuf<double> xd, g;
+    xd.ensure(static_cast<size_t>(d) * m);
+    g.ensure(static_cast<size_t>(m) * m);
+    FCPD_CUDA(cudaMemcpyAsync(xd.p, x, sizeof(double) * d * m, cudaMemcpyHostToDevice, ctx->stream));
+    build_gram_device(xd.p, m, d, beta, g.p, m, ctx->stream);
+    Basis b;
+    dense_eigensolve(ctx->solver, g.p, m, rank, b, u, ctx->stream);
+    if (lambda) std::copy(b.lam_host.begin(), b.lam_host.end(), lambda);
+    if (lambda_raw) std::copy(b.lam_raw_host.begin(), b.lam_raw_host.end(), lambda_raw);
+    b.release();
+    xd.release();
+    g.release();
+  });
+}
+
+namespace {
+// shared by solve_fast_lowrank / apply_transform_lowrank: run z = Qᵀ v,
+// filter, and either W = Q c or out = X + Q g.
+void lowrank_apply(fcpd_ctx* ctx, const double* u, const double* lambda, int64_t m, int64_t k,
+                   const double* rhs, int d, double lambda_reg, double sigma2, bool transform,
+                   const double* x, double* out) {
+  if (m <= 0 || k <= 0 || k > m) throw Failure(FCPD_ERR_PARAMETER, "solve_fast: bad basis shape");
+  if (d < 1 || d > 3) throw Failure(FCPD_ERR_DIMENSION, "solve_fast: the B200 path supports D <= 3");
+  cudaStream_t str = ctx->stream;
+  Basis b;
+  basis_from_host(b, u, lambda, m, k, str);
+  // lam buffer: [0,k) solver diagonal λ, [k,2k) numerator
+  std::vector<double> lh(2 * k);
+  for (int64_t i = 0; i < k; ++i) {
+    lh[i] = transform ? 1.0 : lambda[i];
+    lh[k + i] = transform ? lambda[i] : 1.0;
+  }
+  FCPD_CUDA(cudaMemcpyAsync(b.lam, lh.data(), sizeof(double) * 2 * k, cudaMemcpyHostToDevice, str));
+  std::vector<float4> v4(m);
+  for (int64_t i = 0; i < m; ++i) {
+    float c[3] = {0.f, 0.f, 0.f};
+    for (int j = 0; j < d; ++j) c[j] = static_cast<float>(rhs[j * m + i]);
+    v4[i] = make_float4(c[0], c[1], c[2], 0.f);
+  }
+  DevBuf<float4> v, g;
+  DevBuf<double> zpart, vpart, coef, xd, res;
+  DevBuf<IterState> st;
+  v.ensure(m);
+  g.ensure(k);
+  coef.ensure(3 * k);
+  st.ensure(1);
+  FCPD_CUDA(cudaMemcpyAsync(v.p, v4.data(), sizeof(float4) * m, cudaMemcpyHostToDevice, str));
+  IterState h{};
+  h.sigma2 = transform ? 0.0 : sigma2;
+  h.active = 1;
+  FCPD_CUDA(cudaMemcpyAsync(st.p, &h, sizeof h, cudaMemcpyHostToDevice, str));
+  const ColsumPlan zp = make_colsum_plan(m, k, ctx->sm_count);
+  zpart.ensure(static_cast<size_t>(zp.row_blocks) * 3 * b.kpad);
+  launch_colsum(zp, b.q, b.kpad, m, v.p, zpart.p, b.kpad, st.p, nullptr, 0, str);
+  launch_zreduce(zpart.p, zp.row_blocks, k, b.kpad, b.lam, b.lam + k,
+                 transform ? 0.0 : lambda_reg, coef.p, g.p, st.p, str);
+  res.ensure(3 * m);
+  if (transform) {
+    const ColsumPlan vp = make_colsum_plan(k, m, ctx->sm_count);
+    vpart.ensure(static_cast<size_t>(vp.row_blocks) * 3 * b.mpad);
+    launch_colsum(vp, b.qt, b.mpad, k, g.p, vpart.p, b.mpad, st.p, nullptr, 0, str);
+    xd.ensure(3 * m);
+    FCPD_CUDA(cudaMemcpyAsync(xd.p, x, sizeof(double) * d * m, cudaMemcpyHostToDevice, str));
+    launch_vreduce_add(vpart.p, vp.row_blocks, m, b.mpad, xd.p, d, res.p, str);
+  } else {
+    coef_kernel<<<ceil_div(m, 128), 128, 0, str>>>(b.qt, b.mpad, m, k, coef.p, res.p);
+    FCPD_LAUNCH_CHECK();
+  }
+  IterState hs{};
+  FCPD_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof hs, cudaMemcpyDeviceToHost, str));
+  FCPD_CUDA(cudaMemcpyAsync(out, res.p, sizeof(double) * d * m, cudaMemcpyDeviceToHost, str));
+  FCPD_CUDA(cudaStreamSynchronize(str));
+  for (auto* p : {&zpart, &vpart, &coef, &xd, &res}) p->release();
+  v.release();
+  g.release();
+  st.release();
+  b.release();
+  if (hs.err_code == kDevSolveDiag)
+    throw Failure(FCPD_ERR_NUMERIC, "solve_fast: lambda_i + lambda*sigma2 not positive");
+}
+}  // namespace
+
+int fcpd_solve_fast_lowrank(fcpd_ctx* ctx, const double* u, const double* lambda, int64_t m,
+                            int64_t k, double lambda_reg, double sigma2, const double* residual,
+                            int32_t d, double* w) {
+  return guarded(ctx, [&] {
+    lowrank_apply(ctx, u, lambda, m, k, residual, d, lambda_reg, sigma2, false, nullptr, w);
+  });
+}
+
+int fcpd_apply_transform_lowrank(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d,
+                                 const double* u, const double* lambda, int64_t k, const double* w,
+                                 double* out) {
+  return guarded(ctx, [&] {
+    lowrank_apply(ctx, u, lambda, m, k, w, d, 0.0, 0.0, true, x, out);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,59 @@
+// estep.cuh — E-step launch interface (see estep.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace fcpd {
+
+constexpr int kColsPerThread = 4;
+constexpr int kRowsPerThread = 4;
+
+// Fallback-path per-row outputs (all device pointers; SoA fp64 M×3).
+struct RowOut {
+  double* ptilde_y;   // (P̃Y)_m
+  double* var;        // Σ_n P̃_mn ‖y_n − x̃_m‖²
+  double* log2p1;     // log2 of the raw row mass Σ_n P_mn
+  int32_t* degenerate;
+  float4* resid4;     // optional: R = P̃Y − X for the M-step (fp32)
+  const double* x0;   // X (normalised model) when resid4 is set
+};
+
+// Statistics of the scene for the uniform-row fallback (fp64).
+struct YStats {
+  double mean[3];
+  double sq_mean;
+};
+
+struct EStepPlan {
+  int col_blocks = 0, col_splits = 0;
+  int64_t m_per_split = 0;
+  int row_blocks = 0, row_splits = 0;
+  int64_t n_per_split = 0;
+};
+
+struct EStepBuffers {
+  const float4* xt4;   // x̃ fp32 (x,y,z,0), M
+  const double* xt64;  // x̃ fp64 SoA M×3
+  float4* y4b;         // y fp32 (x,y,z,b2), N — .w written by pass 1
+  double* b2;          // b_n fp64 (log2 units), N
+  double* pt1;         // optional Σ_m P_mn, N
+  double* col_part;    // [col_splits][N]
+  double* row_part;    // [row_splits][5][M]
+  int32_t* col_flags;  // N
+  int32_t* row_flags;  // M
+  int32_t* flags_count;  // 2
+  RowOut out;
+  YStats ystats;
+};
+
+EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count);
+void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n, int d,
+                  double omega, IterState* st, uint64_t* stamps, cudaStream_t stream,
+                  cudaEvent_t mid = nullptr);
+
+}  // namespace fcpd

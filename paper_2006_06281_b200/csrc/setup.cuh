@@ -1,0 +1,39 @@
+// setup.cuh — spectral basis setup interface (see setup.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+#include <stdint.h>
+
+#include <vector>
+
+namespace fcpd {
+
+// Device-resident spectral basis, packed for the streaming M-step.
+struct Basis {
+  int64_t m = 0, k = 0, kpad = 0, mpad = 0;
+  float* q = nullptr;    // M×kpad row-major fp32
+  float* qt = nullptr;   // K×mpad row-major fp32
+  double* lam = nullptr; // [0,k): clamped λ ; [k,2k): transform numerator
+  bool full_rank = false;
+  std::vector<double> lam_raw_host, lam_host;
+  // cache key
+  uint64_t key_hash = 0;
+  double key_beta = 0.0;
+  int key_variant = -1;
+  double t_gram = 0.0, t_eig = 0.0;
+  void release();
+};
+
+void build_gram_device(const double* x_dev, int64_t m, int d, double beta, double* phi,
+                       int64_t ld, cudaStream_t stream);
+// In-place eigensolve of phi (M×M col-major, overwritten with eigenvectors);
+// packs the top `rank` into b.  Optionally returns U (M×rank) to the host.
+void dense_eigensolve(cusolverDnHandle_t h, double* phi, int64_t m, int64_t rank, Basis& b,
+                      double* u_out_host, cudaStream_t stream);
+void basis_from_host(Basis& b, const double* u_host, const double* lam_host, int64_t m,
+                     int64_t k, cudaStream_t stream);
+void clamp_lambda(Basis& b);
+void upload_lambda(Basis& b, bool full_rank, cudaStream_t stream);
+
+}  // namespace fcpd

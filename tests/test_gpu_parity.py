@@ -1,0 +1,275 @@
+"""GPU parity: the CUDA product path (through the C ABI) against the oracle.
+
+Tolerances: the device E-step evaluates pair terms in fp32 (MUFU ex2) with
+fp64 accumulation and the M-step streams an fp32 copy of the fp64 basis, so
+single-step quantities match the fp64 oracle to ~1e-7..1e-6 relative; the
+north-star bar for full registrations is σ² within 1e-5 relative per
+iteration and final points within 1e-4 of the scene bounding-box diagonal.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SIGMA_RTOL = 1e-5   # north_star: per-iteration σ²
+POINT_FRAC = 1e-4   # north_star: final points / bbox diagonal
+
+
+@pytest.fixture(scope="module")
+def fc():
+    import paper_2006_06281_b200 as f
+    return f
+
+
+@pytest.fixture(scope="module")
+def ctx(fc):
+    c = fc.Context(0)
+    yield c
+    c.close()
+
+
+def bbox_diag(y):
+    return float(np.linalg.norm(y.max(0) - y.min(0)))
+
+
+# ------------------------------------------------------------ E-step (L2)
+
+
+def test_posterior_kats(ctx, orc):  # test_correspondence.cpp:10-35
+    p, _, _ = ctx.posterior(np.array([[0.0, 0.0]]), orc.make_cloud(5, 2, 1), 0.0, 0.5)
+    assert np.allclose(p, 1.0, rtol=1e-6, atol=0)
+    p, _, _ = ctx.posterior(np.array([[-1.0, 0.0], [1.0, 0.0]]), np.array([[0.0, 0.3]]), 0.0, 0.25)
+    assert np.allclose(p[:, 0], 0.5, rtol=1e-6)
+    p, _, _ = ctx.posterior(np.array([[0.0]]), np.array([[1.0]]), 0.5, 1.0)
+    e = math.exp(-0.5)
+    assert p[0, 0] == pytest.approx(e / (e + math.sqrt(2 * math.pi)), rel=1e-6)
+
+
+def test_posterior_parameter_errors(ctx, fc, orc):  # test_correspondence.cpp:37-45
+    x, y = orc.make_cloud(3, 2, 2), orc.make_cloud(4, 2, 3)
+    for om in (1.0, -0.1):
+        with pytest.raises(fc.ParameterError):
+            ctx.posterior(x, y, om, 1.0)
+    _, clamped, _ = ctx.posterior(x, y, 0.5, 1e-30)
+    assert clamped
+
+
+@pytest.mark.parametrize("omega,s2", [(0.0, 0.3), (0.7, 0.2), (0.2, 1e-3), (0.0, 2e-5)])
+def test_dense_posterior_matches_oracle(ctx, orc, omega, s2):
+    x = orc.make_cloud(37, 3, 14) * 0.5
+    y = orc.make_cloud(53, 3, 15) * 0.5
+    ref, _ = orc.posterior(x, y, omega, s2)
+    got, _, _ = ctx.posterior(x, y, omega, s2)
+    assert np.abs(got - ref).max() <= 2e-6
+    refc, deg = orc.enforce_row_constraint(ref)
+    gotc, _, gdeg = ctx.posterior(x, y, omega, s2, row_constrain=True)
+    assert gdeg == deg
+    assert np.abs(gotc - refc).max() <= 2e-6
+
+
+@pytest.mark.parametrize("m,n,d,omega,s2", [
+    (1, 3, 2, 0.7, 0.5),        # test_registration.cpp:85-97 sizes
+    (300, 360, 3, 0.0, 0.3),
+    (777, 1001, 3, 0.2, 1e-3),  # ragged: not multiples of any tile
+    (500, 400, 2, 0.7, 2e-5),
+    (256, 257, 1, 0.1, 1e-4),
+    (2000, 2400, 3, 0.3, 5e-6),
+])
+def test_estep_matches_oracle(ctx, orc, m, n, d, omega, s2):
+    xt = orc.make_cloud(m, d, 100 + m) * 0.6
+    y = orc.make_cloud(n, d, 200 + n) * 0.6
+    ref = orc.estep_stream(xt, y, omega, s2)
+    got = ctx.estep(xt, y, omega, s2)
+    assert np.array_equal(got["degenerate"], ref.degenerate)
+    ok = ~ref.degenerate
+    scale = math.sqrt(s2)
+    # P̃Y: fp32 pair terms → error ≲ 1e-6 of the kernel width + coordinate ulp
+    assert np.abs(got["ptilde_y"] - ref.ptilde_y).max() <= 1e-6 + 2e-5 * scale
+    assert np.allclose(got["var"][ok], ref.var[ok], rtol=2e-5, atol=0)
+    assert np.allclose(got["p1"][ok], ref.p1[ok], rtol=2e-5, atol=1e-300)
+    if ref.pt1 is not None:
+        assert np.allclose(got["pt1"], ref.pt1, rtol=2e-5, atol=1e-12)
+
+
+def test_estep_degenerate_rows(ctx, orc):
+    """Rows with raw mass < 1e-300 become uniform (correspondence.hpp:89-91)."""
+    y = orc.make_cloud(64, 3, 7) * 0.1
+    xt = np.vstack([orc.make_cloud(16, 3, 8) * 0.1, np.full((4, 3), 0.9)])
+    s2 = 2e-4  # far rows: d² ≈ 2 → log P ≈ -5000
+    ref = orc.estep_stream(xt, y, 0.0, s2)
+    got = ctx.estep(xt, y, 0.0, s2)
+    assert ref.degenerate[-4:].all() and not ref.degenerate[:16].any()
+    assert np.array_equal(got["degenerate"], ref.degenerate)
+    assert np.allclose(got["ptilde_y"][-4:], y.mean(0), rtol=1e-12, atol=1e-14)
+    assert np.allclose(got["var"], ref.var, rtol=2e-5)
+
+
+def test_estep_far_rows_not_degenerate(ctx, orc):
+    """Rows whose mass is tiny but above 1e-300 take the exact fallback."""
+    y = orc.make_cloud(200, 3, 9) * 0.2
+    xt = np.vstack([orc.make_cloud(50, 3, 10) * 0.2, np.full((3, 3), 0.45)])
+    s2 = 4e-3
+    ref = orc.estep_stream(xt, y, 0.0, s2)
+    assert (ref.p1[-3:] < 1e-40).all() and not ref.degenerate.any()
+    got = ctx.estep(xt, y, 0.0, s2)
+    assert not got["degenerate"].any()
+    assert np.allclose(got["ptilde_y"], ref.ptilde_y, rtol=0, atol=1e-6)
+    assert np.allclose(got["p1"], ref.p1, rtol=2e-5, atol=0)
+
+
+# ------------------------------------------------------ setup + M-step (L2)
+
+
+def test_build_gram_matches_oracle(ctx, orc):  # kernel.hpp:31-47
+    x = orc.make_cloud(60, 3, 11)
+    g = ctx.build_gram(x, 2.0)
+    ref = orc.build_gram(x, 2.0)
+    assert np.abs(g - g.T).max() == 0.0 and np.diag(g).min() == 1.0
+    assert np.abs(g - ref).max() <= 1e-14
+
+
+def test_build_basis_matches_oracle(ctx, orc):  # kernel.hpp:49-72
+    x = orc.make_cloud(400, 3, 3)
+    u, lam, raw = ctx.build_basis(x, 2.0, 400)
+    _, rlam, rraw = orc.eigendecompose(orc.build_gram(x, 2.0), 400)
+    assert np.all(np.diff(lam) <= 0)
+    assert np.abs(raw - rraw).max() <= 1e-10 * rraw[0]
+    assert np.abs(u.T @ u - np.eye(400)).max() <= 1e-8
+    phi = orc.build_gram(x, 2.0)
+    assert np.linalg.norm(u @ np.diag(raw) @ u.T - phi) <= 1e-8 * np.linalg.norm(phi)
+    # the clamp: λ < 1e-12·λ_max → 0, exactly as the oracle
+    assert np.array_equal(lam == 0.0, rlam == 0.0)
+
+
+def test_solve_and_transform_lowrank(ctx, orc):  # solvers.hpp:61-73, :147-155
+    x = orc.make_cloud(300, 3, 21)
+    y = orc.make_cloud(280, 3, 22)
+    phi = orc.build_gram(x, 2.0)
+    u, lam, _ = orc.eigendecompose(phi, 300)
+    p = orc.random_row_constrained(300, 280, 23)
+    r = p @ y - x
+    for k in (300, 30):
+        w_ref = orc.solve_fast_lowrank(u[:, :k], lam[:k], 10.0, 0.3, r)
+        w = ctx.solve_fast_lowrank(u[:, :k], lam[:k], 10.0, 0.3, r)
+        assert np.linalg.norm(w - w_ref) <= 1e-5 * np.linalg.norm(w_ref)
+        t_ref = orc.apply_transform_lowrank(x, u[:, :k], lam[:k], w_ref)
+        t = ctx.apply_transform_lowrank(x, u[:, :k], lam[:k], w_ref)
+        assert np.abs(t - t_ref).max() <= 1e-5 * np.abs(t_ref - x).max() + 1e-12
+    # solve_fast stationarity (test_solvers.cpp:51-68), fp32-basis tolerance
+    w = ctx.solve_fast(u, lam, 10.0, 0.3, r)
+    a = phi + 3.0 * np.eye(300)
+    assert np.linalg.norm(a @ w - r) <= 1e-5 * np.linalg.norm(r)
+
+
+def test_solve_fast_nonpositive_diag(ctx, fc):  # solvers.hpp:68-69
+    u = np.eye(2)
+    with pytest.raises(fc.NumericError):
+        ctx.solve_fast(u, np.array([1.0, -5.0]), 1.0, 0.1, np.ones((2, 1)))
+
+
+# ------------------------------------------------- register_pointsets (L3)
+
+
+def test_self_registration(ctx, fc, orc):  # test_registration.cpp:29-42
+    x = orc.make_torus(120, 52)
+    res = ctx.register(x, x, fc.RegistrationConfig(iterations=50))
+    assert len(res.sigma2_trace) == 50
+    assert math.sqrt(((res.transformed - x) ** 2).sum(1).mean()) <= 1e-3
+    assert np.all(np.diff(res.sigma2_trace) <= 1e-12)
+
+
+def test_zero_iterations_identity(ctx, fc, orc):  # test_registration.cpp:44-53
+    x, y = orc.make_cloud(20, 2, 53), orc.make_cloud(25, 2, 54)
+    res = ctx.register(x, y, fc.RegistrationConfig(iterations=0))
+    assert np.abs(res.transformed - x).max() <= 1e-12
+    assert np.abs(res.coefficients).max() == 0.0
+    assert len(res.sigma2_trace) == 0
+
+
+def test_timing_identities(ctx, fc, orc):  # test_registration.cpp:55-70
+    x, y = orc.make_cloud(60, 3, 55), orc.make_cloud(60, 3, 56)
+    for v in ("fast", "fast_lowrank"):
+        t = ctx.register(x, y, fc.RegistrationConfig(iterations=5, variant=v)).timing
+        assert t.t_f == t.t_eig + t.t_iter
+        assert t.t_total == t.t_c + t.t_f + t.t_o
+        assert t.t_c > 0 and t.t_iter > 0
+
+
+def test_bitwise_determinism(ctx, fc, orc):  # test_registration.cpp:72-83
+    x, y = orc.make_torus(80, 57), orc.make_torus(90, 58)
+    cfg = fc.RegistrationConfig(iterations=15)
+    a = ctx.register(x, y, cfg)
+    b = ctx.register(x, y, cfg)
+    assert b.basis_reused
+    assert np.array_equal(a.sigma2_trace, b.sigma2_trace)
+    assert np.array_equal(a.transformed, b.transformed)
+    with fc.Context(0) as other:  # fresh context recomputes the basis
+        c = other.register(x, y, cfg)
+    assert np.array_equal(a.sigma2_trace, c.sigma2_trace)
+
+
+def test_degenerate_sizes(ctx, fc):  # test_registration.cpp:85-97
+    x = np.array([[0.2, 0.1]])
+    y = np.array([[0, 0], [1, 0], [0, 1.0]])
+    for v in ("fast", "fast_lowrank"):
+        res = ctx.register(x, y, fc.RegistrationConfig(iterations=3, variant=v))
+        assert res.transformed.shape == (1, 2) and len(res.sigma2_trace) == 3
+
+
+def test_register_validation(ctx, fc, orc):  # test_registration.cpp:99-106
+    x = orc.make_cloud(5, 2, 59)
+    with pytest.raises(fc.DimensionError):
+        ctx.register(x, orc.make_cloud(5, 3, 60))
+    with pytest.raises(fc.ParameterError):
+        ctx.register(x, x, fc.RegistrationConfig(iterations=-1))
+    with pytest.raises(fc.ParameterError):
+        ctx.register(np.zeros((0, 2)), x)
+    with pytest.raises(fc.NumericError, match="iteration 0"):  # posterior rethrown
+        ctx.register(x, x, fc.RegistrationConfig(omega=1.0, iterations=2))
+    with pytest.raises(fc.ParameterError):
+        ctx.register(x, x, fc.RegistrationConfig(beta=0.0))
+    with pytest.raises(fc.ParameterError):
+        ctx.register(x, x, fc.RegistrationConfig(variant="fast_lowrank", rank_fraction=0.0))
+
+
+@pytest.mark.parametrize("variant,omega", [("fast", 0.7), ("fast_lowrank", 0.7), ("fast", 0.0)])
+def test_register_matches_oracle_small(ctx, fc, orc, variant, omega):
+    x = orc.make_torus(400, 61)
+    y = orc.make_torus(450, 62) * np.array([1.1, 0.9, 1.0]) + 0.05
+    cfg = fc.RegistrationConfig(omega=omega, iterations=40, variant=variant)
+    got = ctx.register(x, y, cfg, want_correspondence=True)
+    ref = orc.register(x, y, omega=omega, iterations=40, variant=variant)
+    assert np.abs(got.sigma2_trace / ref.sigma2_trace - 1).max() <= SIGMA_RTOL
+    assert np.abs(got.transformed - ref.transformed).max() <= POINT_FRAC * bbox_diag(y)
+    assert got.sigma2_initial == pytest.approx(ref.sigma2_initial, rel=1e-13)
+    assert got.degenerate_rows == ref.degenerate_rows
+    assert got.sigma2_clamps == ref.sigma2_clamps
+    # final correspondence is row-stochastic
+    assert np.abs(got.correspondence.sum(1) - 1).max() <= 1e-6
+
+
+def test_c0_parity(ctx, fc, orc):
+    """BASELINE.json configs[0] at full size: M=N=2000, ω=0, β=2, λ=3, 50 it."""
+    from paper_2006_06281_b200 import datagen
+    x, y, w = datagen.generate("c0")
+    got = ctx.register(x, y, datagen.config_for(w))
+    ref = orc.register(x, y, omega=w.omega, beta=w.beta, lambda_reg=w.lambda_reg,
+                       iterations=w.iterations)
+    rel = np.abs(got.sigma2_trace / ref.sigma2_trace - 1)
+    assert rel.max() <= SIGMA_RTOL, f"worst sigma2 rel {rel.max():.3g} at it {rel.argmax()}"
+    err = np.abs(got.transformed - ref.transformed).max() / bbox_diag(y)
+    assert err <= POINT_FRAC, err
+
+
+def test_c1_reduced_parity(ctx, fc, orc):
+    """configs[1]'s generator (outliers, ω=0.2) at M=3000 against the oracle."""
+    from paper_2006_06281_b200 import datagen
+    x, y, w = datagen.generate("c1", m=3000)
+    got = ctx.register(x, y, datagen.config_for(w, iterations=60))
+    ref = orc.register(x, y, omega=w.omega, beta=w.beta, lambda_reg=w.lambda_reg,
+                       iterations=60)
+    rel = np.abs(got.sigma2_trace / ref.sigma2_trace - 1)
+    assert rel.max() <= SIGMA_RTOL, f"worst sigma2 rel {rel.max():.3g} at it {rel.argmax()}"
+    assert np.abs(got.transformed - ref.transformed).max() <= POINT_FRAC * bbox_diag(y)
