@@ -61,30 +61,78 @@ uint64_t fnv1a(const void* data, size_t bytes, uint64_t h = 1469598103934665603u
 
 // ------------------------------------------------------------- small kernels
 
-// Dense materialisation of the last E-step's P (or row-constrained P̃) in fp64,
-// from the per-column normalisers and per-row masses (debug / small M·N).
+// Dense materialisation (small problems, tests, RegistrationResult::
+// correspondence): the reference algorithm itself in fp64 on the device —
+// posterior (correspondence.hpp:35-79), one warp per scene column with the
+// per-column max shift incl. log c; then enforce_row_constraint (:83-98),
+// one thread per model row.  Independent of the streaming fp32 hot path.
 __global__ void dense_posterior_kernel(const double* __restrict__ xt64, int64_t m,
-                                       const double* __restrict__ y64, int64_t n,
-                                       const double* __restrict__ b2,
-                                       const double* __restrict__ log2p1,
-                                       const int32_t* __restrict__ degenerate, int row_constrain,
-                                       const IterState* __restrict__ st, double* __restrict__ p) {
+                                       const double* __restrict__ y64, int64_t n, int d,
+                                       double omega, const IterState* __restrict__ st,
+                                       double* __restrict__ p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= n) return;
+  const double sigma2 = st->sigma2_e;
+  const double inv = 1.0 / (2.0 * sigma2);
+  const bool has_outlier = omega > 0.0;
+  const double log_c = has_outlier ? 0.5 * d * log(2.0 * M_PI * sigma2) +
+                                         log(omega / (1.0 - omega)) +
+                                         log(static_cast<double>(m) / static_cast<double>(n))
+                                   : 0.0;
+  double* col = p + j * m;
+  double shift = -INFINITY;
+  for (int64_t i = lane; i < m; i += 32) {
+    double s = 0.0;
+    for (int c = 0; c < d; ++c) {
+      const double t = y64[c * n + j] - xt64[c * m + i];
+      s += t * t;
+    }
+    col[i] = -s * inv;
+    shift = fmax(shift, col[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) shift = fmax(shift, __shfl_xor_sync(0xffffffffu, shift, o));
+  if (has_outlier && log_c > shift) shift = log_c;
+  double denom = 0.0;
+  for (int64_t i = lane; i < m; i += 32) {
+    col[i] = exp(col[i] - shift);
+    denom += col[i];
+  }
+  denom = warp_sum(denom);
+  if (has_outlier) denom += exp(log_c - shift);
+  for (int64_t i = lane; i < m; i += 32) col[i] /= denom;
+}
+
+__global__ void dense_row_constraint_kernel(double* __restrict__ p, int64_t m, int64_t n,
+                                            int32_t* __restrict__ degenerate) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t j = blockIdx.y;
   if (i >= m) return;
-  if (row_constrain && degenerate[i]) {
-    p[j * m + i] = 1.0 / static_cast<double>(n);
-    return;
+  double s = 0.0;
+  for (int64_t j = 0; j < n; ++j) s += p[j * m + i];
+  const bool deg = s < 1e-300;
+  degenerate[i] = deg ? 1 : 0;
+  for (int64_t j = 0; j < n; ++j) p[j * m + i] = deg ? 1.0 / static_cast<double>(n) : p[j * m + i] / s;
+}
+
+void launch_dense_posterior(const double* xt64, int64_t m, const double* y64, int64_t n, int d,
+                            double omega, const IterState* st, int row_constrain,
+                            int32_t* degenerate, double* p, cudaStream_t str) {
+  dense_posterior_kernel<<<ceil_div(n, 8), 256, 0, str>>>(xt64, m, y64, n, d, omega, st, p);
+  FCPD_LAUNCH_CHECK();
+  if (row_constrain) {
+    dense_row_constraint_kernel<<<ceil_div(m, 128), 128, 0, str>>>(p, m, n, degenerate);
+    FCPD_LAUNCH_CHECK();
   }
-  double d2 = 0.0;
-  for (int c = 0; c < 3; ++c) {
-    const double t = y64[c * n + j] - xt64[c * m + i];
-    d2 += t * t;
-  }
-  const double k2 = kLog2e / (2.0 * st->sigma2_e);
-  double e = b2[j] - d2 * k2;
-  if (row_constrain) e -= log2p1[i];
-  p[j * m + i] = exp2(e);
+}
+
+// coefficients c (fp64 SoA 3×K) → float4 rows for the Qᵀ-row stream.
+__global__ void pack_coef_kernel(const double* __restrict__ coef, int64_t k,
+                                 float4* __restrict__ c4) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < k)
+    c4[i] = make_float4(static_cast<float>(coef[i]), static_cast<float>(coef[k + i]),
+                        static_cast<float>(coef[2 * k + i]), 0.f);
 }
 
 // W = Q c (coefficients), fp64 accumulation over the fp32 basis.
@@ -291,16 +339,16 @@ void enqueue_iteration(fcpd_ctx* ctx, Session& s, cudaEvent_t* ev = nullptr) {
   rec(0);
   launch_estep(s.ep, eb, s.m, s.n, s.d, s.cfg.omega, st, s.stamps.p, str, ev ? ev[1] : nullptr);
   rec(2);
-  launch_colsum(s.zp, b.q, b.kpad, s.m, s.resid4.p, s.zpart.p, b.kpad, st, s.stamps.p, 1, str);
+  launch_colsum(s.zp, b.q, b.kpad, s.resid4.p, s.zpart.p, st, s.stamps.p, 1, str);
   rec(3);
-  launch_zreduce(s.zpart.p, s.zp.row_blocks, b.k, b.kpad, b.lam, b.lam + b.k, s.cfg.lambda_reg,
-                 s.coef.p, s.g4.p, st, str);
+  launch_zreduce(s.zp, s.zpart.p, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.coef.p, s.g4.p, st,
+                 str);
   rec(4);
-  launch_colsum(s.vp, b.qt, b.mpad, b.k, s.g4.p, s.vpart.p, b.mpad, st, nullptr, 0, str);
+  launch_colsum(s.vp, b.qt, b.mpad, s.g4.p, s.vpart.p, st, nullptr, 0, str);
   rec(5);
-  launch_transform_sigma(s.vpart.p, s.vp.row_blocks, s.m, b.mpad, s.x0.p, s.xt64.p,
-                         s.xt_prev.p, s.xt4.p, s.ptilde_y.p, s.var.p, s.sig_part.p, s.d,
-                         s.cfg.early_stop, s.trace.p, st, s.stamps.p, str);
+  launch_transform_sigma(s.vp, s.vpart.p, s.x0.p, s.xt64.p, s.xt_prev.p, s.xt4.p, s.ptilde_y.p,
+                         s.var.p, s.sig_part.p, s.d, s.cfg.early_stop, s.trace.p, st,
+                         s.stamps.p, str);
   rec(6);
 }
 
@@ -374,8 +422,8 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
     Basis& b = ctx->basis;
     s.zp = make_colsum_plan(m, b.k, ctx->sm_count);
     s.vp = make_colsum_plan(b.k, m, ctx->sm_count);
-    s.zpart.ensure(static_cast<size_t>(s.zp.row_blocks) * 3 * b.kpad);
-    s.vpart.ensure(static_cast<size_t>(s.vp.row_blocks) * 3 * b.mpad);
+    s.zpart.ensure(s.zp.part_doubles());
+    s.vpart.ensure(s.vp.part_doubles());
     s.coef.ensure(3 * b.k);
     s.g4.ensure(b.k);
   }
@@ -526,27 +574,29 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
   std::vector<double> xt(3 * m);
   FCPD_CUDA(cudaMemcpyAsync(xt.data(), s.xt64.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, str));
   if (out->coefficients) {
-    DevBuf<double> w;
-    w.ensure(3 * m);
-    coef_kernel<<<ceil_div(m, 128), 128, 0, str>>>(b.qt, b.mpad, m, b.k, s.coef.p, w.p);
+    // W = Q c (the last iteration's coefficients): one more Qᵀ-row stream
+    pack_coef_kernel<<<ceil_div(b.k, 256), 256, 0, str>>>(s.coef.p, b.k, s.g4.p);
     FCPD_LAUNCH_CHECK();
-    FCPD_CUDA(cudaMemcpyAsync(out->coefficients, w.p, sizeof(double) * d * m,
+    launch_colsum(s.vp, b.qt, b.mpad, s.g4.p, s.vpart.p, nullptr, nullptr, 0, str);
+    launch_vreduce_add(s.vp, s.vpart.p, nullptr, d, s.ptilde_y.p, str);
+    FCPD_CUDA(cudaMemcpyAsync(out->coefficients, s.ptilde_y.p, sizeof(double) * d * m,
                               cudaMemcpyDeviceToHost, str));
     s.d2h += sizeof(double) * d * m;
-    FCPD_CUDA(cudaStreamSynchronize(str));
-    w.release();
   }
   if (out->correspondence && run > 0) {
     DevBuf<double> p;
     p.ensure(static_cast<size_t>(m) * n);
-    dense_posterior_kernel<<<dim3(ceil_div(m, 128), static_cast<unsigned>(n)), 128, 0, str>>>(
-        s.xt_prev.p, m, s.y64.p, n, s.b2.p, s.log2p1.p, s.degenerate.p, 1, s.st.p, p.p);
-    FCPD_LAUNCH_CHECK();
+    // the last E-step's P̃ (x̃ before the last transform, σ² it used)
+    DevBuf<int32_t> deg;
+    deg.ensure(m);
+    launch_dense_posterior(s.xt_prev.p, m, s.y64.p, n, d, s.cfg.omega, s.st.p, 1, deg.p, p.p,
+                           str);
     FCPD_CUDA(cudaMemcpyAsync(out->correspondence, p.p, sizeof(double) * m * n,
                               cudaMemcpyDeviceToHost, str));
     s.d2h += sizeof(double) * m * n;
     FCPD_CUDA(cudaStreamSynchronize(str));
     p.release();
+    deg.release();
   }
   if (out->degenerate_mask)
     FCPD_CUDA(cudaMemcpyAsync(out->degenerate_mask, s.degenerate.p, sizeof(int32_t) * m,
@@ -762,20 +812,37 @@ int fcpd_posterior_dense(fcpd_ctx* ctx, const double* xt, int64_t m, const doubl
                          int32_t d, double omega, double sigma2, int32_t row_constrain, double* p,
                          int32_t* clamped, int64_t* degenerate_rows, int64_t* n_degenerate) {
   std::vector<int32_t> deg(m > 0 ? m : 1);
-  int rc = fcpd_estep(ctx, xt, m, y, n, d, omega, sigma2, nullptr, nullptr, nullptr, deg.data(),
-                      nullptr, clamped);
-  if (rc) return rc;
   return guarded(ctx, [&] {
-    Session& s = ctx->sess;
-    DevBuf<double> dp;
+    if (m <= 0 || n <= 0) throw Failure(FCPD_ERR_PARAMETER, "posterior: empty point set");
+    if (d < 1 || d > 3) throw Failure(FCPD_ERR_DIMENSION, "posterior: the B200 path supports D <= 3");
+    if (!(omega >= 0.0 && omega < 1.0))
+      throw Failure(FCPD_ERR_PARAMETER, "posterior: omega must lie in [0, 1)");
+    if (static_cast<double>(m) * static_cast<double>(n) > 4e9)
+      throw Failure(FCPD_ERR_PARAMETER, "posterior: dense output limited to M*N <= 4e9");
+    cudaStream_t str = ctx->stream;
+    DevBuf<double> xd, yd, dp;
+    DevBuf<int32_t> dg;
+    DevBuf<IterState> st;
+    xd.ensure(3 * m);
+    yd.ensure(3 * n);
     dp.ensure(static_cast<size_t>(m) * n);
-    dense_posterior_kernel<<<dim3(ceil_div(m, 128), static_cast<unsigned>(n)), 128, 0,
-                             ctx->stream>>>(s.xt64.p, m, s.y64.p, n, s.b2.p, s.log2p1.p,
-                                            s.degenerate.p, row_constrain, s.st.p, dp.p);
-    FCPD_LAUNCH_CHECK();
-    FCPD_CUDA(cudaMemcpyAsync(p, dp.p, sizeof(double) * m * n, cudaMemcpyDeviceToHost, ctx->stream));
-    FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
-    dp.release();
+    dg.ensure(m);
+    st.ensure(1);
+    IterState h{};
+    h.sigma2 = sigma2;
+    h.sigma2_e = std::max(sigma2, kSigma2Floor);  // correspondence.hpp:43-47
+    FCPD_CUDA(cudaMemcpyAsync(xd.p, xt, sizeof(double) * d * m, cudaMemcpyHostToDevice, str));
+    FCPD_CUDA(cudaMemcpyAsync(yd.p, y, sizeof(double) * d * n, cudaMemcpyHostToDevice, str));
+    FCPD_CUDA(cudaMemcpyAsync(st.p, &h, sizeof h, cudaMemcpyHostToDevice, str));
+    FCPD_CUDA(cudaMemsetAsync(dg.p, 0, sizeof(int32_t) * m, str));
+    launch_dense_posterior(xd.p, m, yd.p, n, d, omega, st.p, row_constrain, dg.p, dp.p, str);
+    FCPD_CUDA(cudaMemcpyAsync(p, dp.p, sizeof(double) * m * n, cudaMemcpyDeviceToHost, str));
+    FCPD_CUDA(cudaMemcpyAsync(deg.data(), dg.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, str));
+    FCPD_CUDA(cudaStreamSynchronize(str));
+    if (clamped) *clamped = sigma2 < kSigma2Floor ? 1 : 0;
+    for (auto* b : {&xd, &yd, &dp}) b->release();
+    dg.release();
+    st.release();
     int64_t nd = 0;
     if (row_constrain)
       for (int64_t i = 0; i < m; ++i)
@@ -860,18 +927,18 @@ void lowrank_apply(fcpd_ctx* ctx, const double* u, const double* lambda, int64_t
   h.active = 1;
   FCPD_CUDA(cudaMemcpyAsync(st.p, &h, sizeof h, cudaMemcpyHostToDevice, str));
   const ColsumPlan zp = make_colsum_plan(m, k, ctx->sm_count);
-  zpart.ensure(static_cast<size_t>(zp.row_blocks) * 3 * b.kpad);
-  launch_colsum(zp, b.q, b.kpad, m, v.p, zpart.p, b.kpad, st.p, nullptr, 0, str);
-  launch_zreduce(zpart.p, zp.row_blocks, k, b.kpad, b.lam, b.lam + k,
-                 transform ? 0.0 : lambda_reg, coef.p, g.p, st.p, str);
+  zpart.ensure(zp.part_doubles());
+  launch_colsum(zp, b.q, b.kpad, v.p, zpart.p, st.p, nullptr, 0, str);
+  launch_zreduce(zp, zpart.p, b.lam, b.lam + k, transform ? 0.0 : lambda_reg, coef.p, g.p, st.p,
+                 str);
   res.ensure(3 * m);
   if (transform) {
     const ColsumPlan vp = make_colsum_plan(k, m, ctx->sm_count);
-    vpart.ensure(static_cast<size_t>(vp.row_blocks) * 3 * b.mpad);
-    launch_colsum(vp, b.qt, b.mpad, k, g.p, vpart.p, b.mpad, st.p, nullptr, 0, str);
+    vpart.ensure(vp.part_doubles());
+    launch_colsum(vp, b.qt, b.mpad, g.p, vpart.p, st.p, nullptr, 0, str);
     xd.ensure(3 * m);
     FCPD_CUDA(cudaMemcpyAsync(xd.p, x, sizeof(double) * d * m, cudaMemcpyHostToDevice, str));
-    launch_vreduce_add(vpart.p, vp.row_blocks, m, b.mpad, xd.p, d, res.p, str);
+    launch_vreduce_add(vp, vpart.p, xd.p, d, res.p, str);
   } else {
     coef_kernel<<<ceil_div(m, 128), 128, 0, str>>>(b.qt, b.mpad, m, k, coef.p, res.p);
     FCPD_LAUNCH_CHECK();

@@ -84,53 +84,85 @@ __global__ void estep_prologue_kernel(IterState* st, int64_t m, int64_t n, int d
 
 // ---------------------------------------------------------------------------
 // Pass 1: per-column partial sums Σ_m 2^{−t_mn} over one M-split.
-template <int CPT>
+//
+// f32x2 packing (FADD2/FMUL2/FFMA2, sm_100): each thread owns CP column
+// pairs; every packed op evaluates two (m, n) pairs in one issue slot, so
+// per pair the pass costs 3.5 issue slots of FP32 work + 1 MUFU.EX2 and is
+// bound by the 16 ex2/clk/SM SFU rate.  Each lane of a packed op rounds
+// exactly like the scalar op, so t_mn is bitwise identical to sqdist() used
+// by pass 2 and the fallbacks.  Shared memory holds each model point as
+// (−x,−x,−y,−y),(−z,−z) so a broadcast LDS yields the packed operand.
+template <int CP>
 __global__ void __launch_bounds__(128)
     estep_col_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4,
                      int64_t n, int64_t m_per_split, const IterState* __restrict__ st,
                      double* __restrict__ part) {
   if (!st->active) return;
-  __shared__ float4 xs[kTile];
+  __shared__ float4 xa[kTile];  // (−x, −x, −y, −y)
+  __shared__ float2 xb[kTile];  // (−z, −z)
   const float s = st->sx;
-  const int64_t col0 = static_cast<int64_t>(blockIdx.x) * (128 * CPT) + threadIdx.x;
-  float4 yv[CPT];
+  // column pair p of this thread: cols c, c+1 with c = base + p·256 + 2·tid
+  const int64_t cbase = static_cast<int64_t>(blockIdx.x) * (256 * CP) + 2 * threadIdx.x;
+  float2 yx[CP], yy[CP], yz[CP];
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) {
-    const int64_t col = col0 + c * 128;
-    yv[c] = col < n ? scale_pt(y4[col], s) : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int p = 0; p < CP; ++p) {
+    const int64_t c = cbase + p * 256;
+    const float4 a = c < n ? scale_pt(y4[c], s) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 b = c + 1 < n ? scale_pt(y4[c + 1], s) : make_float4(0.f, 0.f, 0.f, 0.f);
+    yx[p] = make_float2(a.x, b.x);
+    yy[p] = make_float2(a.y, b.y);
+    yz[p] = make_float2(a.z, b.z);
   }
   const int64_t m_begin = static_cast<int64_t>(blockIdx.y) * m_per_split;
   const int64_t m_end = min(m, m_begin + m_per_split);
-  double dsum[CPT];
+  double dsum[CP][2];
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) dsum[c] = 0.0;
+  for (int p = 0; p < CP; ++p) dsum[p][0] = dsum[p][1] = 0.0;
 
   for (int64_t base = m_begin; base < m_end; base += kTile) {
     const int cnt = static_cast<int>(min(static_cast<int64_t>(kTile), m_end - base));
     __syncthreads();
-    for (int i = threadIdx.x; i < kTile; i += 128)
-      xs[i] = i < cnt ? scale_pt(xt4[base + i], s)
-                      : make_float4(kPadCoord, kPadCoord, kPadCoord, 0.f);
+    for (int i = threadIdx.x; i < kTile; i += 128) {
+      const float4 v = i < cnt ? scale_pt(xt4[base + i], s)
+                               : make_float4(kPadCoord, kPadCoord, kPadCoord, 0.f);
+      xa[i] = make_float4(-v.x, -v.x, -v.y, -v.y);
+      xb[i] = make_float2(-v.z, -v.z);
+    }
     __syncthreads();
-    float fsum[CPT];
+    float2 fsum[CP];
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) fsum[c] = 0.f;
+    for (int p = 0; p < CP; ++p) fsum[p] = make_float2(0.f, 0.f);
     const int cnt8 = (cnt + 7) & ~7;
     for (int j = 0; j < cnt8; j += 8) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const float4 xv = xs[j + u];
+        const float4 a = xa[j + u];
+        const float2 nx = make_float2(a.x, a.y), ny = make_float2(a.z, a.w);
+        const float2 nz = xb[j + u];
 #pragma unroll
-        for (int c = 0; c < CPT; ++c) fsum[c] += ex2_approx(-sqdist(yv[c], xv));
+        for (int p = 0; p < CP; ++p) {
+          const float2 dx = __fadd2_rn(yx[p], nx);
+          const float2 dy = __fadd2_rn(yy[p], ny);
+          const float2 dz = __fadd2_rn(yz[p], nz);
+          float2 t = __fmul2_rn(dx, dx);
+          t = __ffma2_rn(dy, dy, t);
+          t = __ffma2_rn(dz, dz, t);
+          fsum[p] = __fadd2_rn(fsum[p], make_float2(ex2_approx(-t.x), ex2_approx(-t.y)));
+        }
       }
     }
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) dsum[c] += static_cast<double>(fsum[c]);
+    for (int p = 0; p < CP; ++p) {
+      dsum[p][0] += static_cast<double>(fsum[p].x);
+      dsum[p][1] += static_cast<double>(fsum[p].y);
+    }
   }
+  double* out = part + static_cast<int64_t>(blockIdx.y) * n;
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) {
-    const int64_t col = col0 + c * 128;
-    if (col < n) part[static_cast<int64_t>(blockIdx.y) * n + col] = dsum[c];
+  for (int p = 0; p < CP; ++p) {
+    const int64_t c = cbase + p * 256;
+    if (c < n) out[c] = dsum[p][0];
+    if (c + 1 < n) out[c + 1] = dsum[p][1];
   }
 }
 
@@ -205,77 +237,110 @@ __global__ void estep_col_fallback_kernel(const float4* __restrict__ xt4, int64_
 
 // ---------------------------------------------------------------------------
 // Pass 2: per-row partial sums over one N-split: S0, Sy (3), SV.
-template <int RPT>
+//
+// f32x2 packing over row pairs: per pair 6 packed FP32 issue slots (12
+// lane-ops: the FP32 pipe bound) + 1 MUFU.EX2.  Shared memory holds each
+// scene point as (y,y,y',y'),(z,z,b,b) so a broadcast LDS yields the packed
+// operands; the weight is w = 2^{b − t} (b − t = FFMA2(t, −1, b)).
+template <int RP>
 __global__ void __launch_bounds__(128)
     estep_row_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4b,
                      int64_t n, int64_t n_per_split, const IterState* __restrict__ st,
                      double* __restrict__ part /* [split][5][m] */) {
   if (!st->active) return;
-  __shared__ float4 ys[kTile];
+  __shared__ float4 ya[kTile];  // (yx, yx, yy, yy)
+  __shared__ float4 yb[kTile];  // (yz, yz, b, b)
   const float s = st->sx;
-  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * (128 * RPT) + threadIdx.x;
-  float4 xv[RPT];
+  const int64_t rbase = static_cast<int64_t>(blockIdx.x) * (256 * RP) + 2 * threadIdx.x;
+  float2 nx[RP], ny[RP], nz[RP];
 #pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    const int64_t row = row0 + r * 128;
-    xv[r] = row < m ? scale_pt(xt4[row], s) : make_float4(kPadCoord, kPadCoord, kPadCoord, 0.f);
+  for (int p = 0; p < RP; ++p) {
+    const int64_t r = rbase + p * 256;
+    const float4 pad = make_float4(kPadCoord, kPadCoord, kPadCoord, 0.f);
+    const float4 a = r < m ? scale_pt(xt4[r], s) : pad;
+    const float4 b = r + 1 < m ? scale_pt(xt4[r + 1], s) : pad;
+    nx[p] = make_float2(-a.x, -b.x);
+    ny[p] = make_float2(-a.y, -b.y);
+    nz[p] = make_float2(-a.z, -b.z);
   }
   const int64_t n_begin = static_cast<int64_t>(blockIdx.y) * n_per_split;
   const int64_t n_end = min(n, n_begin + n_per_split);
-  double d0[RPT], dx[RPT], dy[RPT], dz[RPT], dv[RPT];
+  double d0[RP][2], dx[RP][2], dy[RP][2], dz[RP][2], dv[RP][2];
 #pragma unroll
-  for (int r = 0; r < RPT; ++r) d0[r] = dx[r] = dy[r] = dz[r] = dv[r] = 0.0;
+  for (int p = 0; p < RP; ++p)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) d0[p][h] = dx[p][h] = dy[p][h] = dz[p][h] = dv[p][h] = 0.0;
+  const float2 minus1 = make_float2(-1.f, -1.f);
 
   for (int64_t base = n_begin; base < n_end; base += kTile) {
     const int cnt = static_cast<int>(min(static_cast<int64_t>(kTile), n_end - base));
     __syncthreads();
     for (int i = threadIdx.x; i < kTile; i += 128) {
-      // padding column: far away and b = -inf → weight exactly 0
-      ys[i] = i < cnt ? scale_pt(y4b[base + i], s)
-                      : make_float4(kPadCoord, kPadCoord, kPadCoord, -INFINITY);
+      // padding column: far away and b = −inf → weight exactly 0
+      const float4 v = i < cnt ? scale_pt(y4b[base + i], s)
+                               : make_float4(kPadCoord, kPadCoord, kPadCoord, -INFINITY);
+      ya[i] = make_float4(v.x, v.x, v.y, v.y);
+      yb[i] = make_float4(v.z, v.z, v.w, v.w);
     }
     __syncthreads();
-    float f0[RPT], fx[RPT], fy[RPT], fz[RPT], fv[RPT];
+    float2 f0[RP], fx[RP], fy[RP], fz[RP], fv[RP];
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) f0[r] = fx[r] = fy[r] = fz[r] = fv[r] = 0.f;
+    for (int p = 0; p < RP; ++p)
+      f0[p] = fx[p] = fy[p] = fz[p] = fv[p] = make_float2(0.f, 0.f);
     const int cnt8 = (cnt + 7) & ~7;
     for (int j = 0; j < cnt8; j += 8) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const float4 yv = ys[j + u];
+        const float4 a = ya[j + u];
+        const float4 c = yb[j + u];
+        const float2 Yx = make_float2(a.x, a.y), Yy = make_float2(a.z, a.w);
+        const float2 Yz = make_float2(c.x, c.y), B = make_float2(c.z, c.w);
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          const float t = sqdist(yv, xv[r]);
-          const float w = ex2_approx(yv.w - t);
-          f0[r] += w;
-          fx[r] = __fmaf_rn(w, yv.x, fx[r]);
-          fy[r] = __fmaf_rn(w, yv.y, fy[r]);
-          fz[r] = __fmaf_rn(w, yv.z, fz[r]);
-          fv[r] = __fmaf_rn(w, t, fv[r]);
+        for (int p = 0; p < RP; ++p) {
+          const float2 ddx = __fadd2_rn(Yx, nx[p]);
+          const float2 ddy = __fadd2_rn(Yy, ny[p]);
+          const float2 ddz = __fadd2_rn(Yz, nz[p]);
+          float2 t = __fmul2_rn(ddx, ddx);
+          t = __ffma2_rn(ddy, ddy, t);
+          t = __ffma2_rn(ddz, ddz, t);
+          const float2 L = __ffma2_rn(t, minus1, B);
+          const float2 w = make_float2(ex2_approx(L.x), ex2_approx(L.y));
+          f0[p] = __fadd2_rn(f0[p], w);
+          fx[p] = __ffma2_rn(w, Yx, fx[p]);
+          fy[p] = __ffma2_rn(w, Yy, fy[p]);
+          fz[p] = __ffma2_rn(w, Yz, fz[p]);
+          fv[p] = __ffma2_rn(w, t, fv[p]);
         }
       }
     }
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-      d0[r] += f0[r];
-      dx[r] += fx[r];
-      dy[r] += fy[r];
-      dz[r] += fz[r];
-      dv[r] += fv[r];
+    for (int p = 0; p < RP; ++p) {
+      d0[p][0] += f0[p].x;
+      d0[p][1] += f0[p].y;
+      dx[p][0] += fx[p].x;
+      dx[p][1] += fx[p].y;
+      dy[p][0] += fy[p].x;
+      dy[p][1] += fy[p].y;
+      dz[p][0] += fz[p].x;
+      dz[p][1] += fz[p].y;
+      dv[p][0] += fv[p].x;
+      dv[p][1] += fv[p].y;
     }
   }
   const int64_t sp = static_cast<int64_t>(blockIdx.y) * 5 * m;
 #pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    const int64_t row = row0 + r * 128;
-    if (row < m) {
-      part[sp + 0 * m + row] = d0[r];
-      part[sp + 1 * m + row] = dx[r];
-      part[sp + 2 * m + row] = dy[r];
-      part[sp + 3 * m + row] = dz[r];
-      part[sp + 4 * m + row] = dv[r];
+  for (int p = 0; p < RP; ++p)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t row = rbase + p * 256 + h;
+      if (row < m) {
+        part[sp + 0 * m + row] = d0[p][h];
+        part[sp + 1 * m + row] = dx[p][h];
+        part[sp + 2 * m + row] = dy[p][h];
+        part[sp + 3 * m + row] = dz[p][h];
+        part[sp + 4 * m + row] = dv[p][h];
+      }
     }
-  }
 }
 
 // Row finalisation shared by the combine and the fallback.
@@ -391,17 +456,43 @@ __global__ void estep_row_fallback_kernel(const float4* __restrict__ xt4, int64_
 // ---------------------------------------------------------------------------
 // Host-side launcher.
 
+// Split the reduction axis so the grid fills whole waves: CTAs are uniform,
+// so wave efficiency = T / (ceil(T/slots)·slots) with T = blocks × splits.
+// Take the fewest splits reaching ≥ 96 % (or the best found), keeping ≥ 128
+// reduction points per split.
+static int choose_splits(int blocks, int64_t len, int slots) {
+  const int max_s = static_cast<int>(std::max<int64_t>(1, len / 128));
+  int best = 1;
+  double best_eff = -1.0;
+  for (int s = 1; s <= max_s; ++s) {
+    const int64_t per = ceil_div(len, s);
+    const int real = ceil_div(len, per);  // splits actually produced
+    const int64_t t = static_cast<int64_t>(blocks) * real;
+    const double waves = std::ceil(static_cast<double>(t) / slots);
+    const double eff = static_cast<double>(t) / (waves * slots);
+    if (t < slots && s < max_s) continue;  // want at least one full wave
+    if (eff >= 0.96) return s;
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
+}
+
 EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
   EStepPlan p;
-  const int target = sm_count * 8;
+  int occ_col = 0, occ_row = 0;
+  FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &occ_col, estep_col_kernel<kColsPerThread / 2>, 128, 0));
+  FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &occ_row, estep_row_kernel<kRowsPerThread / 2>, 128, 0));
   p.col_blocks = ceil_div(n, 128 * kColsPerThread);
-  int s1 = ceil_div(target, p.col_blocks);
-  s1 = static_cast<int>(std::min<int64_t>(s1, std::max<int64_t>(1, ceil_div(m, 256))));
+  const int s1 = choose_splits(p.col_blocks, m, sm_count * std::max(occ_col, 1));
   p.m_per_split = ceil_div(m, s1);
   p.col_splits = ceil_div(m, p.m_per_split);
   p.row_blocks = ceil_div(m, 128 * kRowsPerThread);
-  int s2 = ceil_div(target, p.row_blocks);
-  s2 = static_cast<int>(std::min<int64_t>(s2, std::max<int64_t>(1, ceil_div(n, 256))));
+  const int s2 = choose_splits(p.row_blocks, n, sm_count * std::max(occ_row, 1));
   p.n_per_split = ceil_div(n, s2);
   p.row_splits = ceil_div(n, p.n_per_split);
   return p;
@@ -412,7 +503,7 @@ void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t 
                   cudaEvent_t mid) {
   estep_prologue_kernel<<<1, 1, 0, stream>>>(st, m, n, d, omega, b.flags_count, stamps);
   FCPD_LAUNCH_CHECK();
-  estep_col_kernel<kColsPerThread>
+  estep_col_kernel<kColsPerThread / 2>
       <<<dim3(p.col_blocks, p.col_splits), 128, 0, stream>>>(b.xt4, m, b.y4b, n, p.m_per_split,
                                                              st, b.col_part);
   FCPD_LAUNCH_CHECK();
@@ -423,7 +514,7 @@ void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t 
                                                      b.flags_count, st);
   FCPD_LAUNCH_CHECK();
   if (mid) FCPD_CUDA(cudaEventRecord(mid, stream));
-  estep_row_kernel<kRowsPerThread>
+  estep_row_kernel<kRowsPerThread / 2>
       <<<dim3(p.row_blocks, p.row_splits), 128, 0, stream>>>(b.xt4, m, b.y4b, n, p.n_per_split,
                                                              st, b.row_part);
   FCPD_LAUNCH_CHECK();

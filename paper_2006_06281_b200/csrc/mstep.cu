@@ -12,9 +12,12 @@
 //     V = Q (f ⊙ z)   (colsum over Qᵀ, K×M row-major fp32)
 // Both are "column sums of a row-major matrix weighted by a per-row 3-vector"
 // — the same kernel.  Storing Q and Qᵀ (2× the basis, ≤ 3.2 GB at M=20k)
-// makes both passes fully coalesced single reads of HBM.  fp32 products,
-// fp32 accumulation over 16-row groups, fp64 accumulation above that, and a
-// fixed-order fp64 reduction across row blocks (bitwise reproducible).
+// makes both passes fully coalesced single reads of HBM.  The kernel is
+// stream-K: a persistent grid (one wave of resident CTAs) splits the
+// (row × 1024-column block) units evenly, so there is no tail wave and each
+// CTA emits one partial per column block it touched.  fp32 products, fp32
+// accumulation over 16-row groups, fp64 above that, and a fixed-order fp64
+// reduction over partials (bitwise reproducible).
 //
 // σ² uses the cancellation-free per-row form: with
 // Δ̄_m = (P̃Y)_m − x̃old_m, V_m = Σ_n P̃_mn‖y_n − x̃old_m‖², δ = x̃new − x̃old,
@@ -24,103 +27,136 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "mstep.cuh"
 
 namespace fcpd {
 
 namespace {
-constexpr int kColsumThreads = 256;
-constexpr int kRowGroup = 16;  // rows per fp32 sub-accumulation
-}  // namespace
+constexpr int kRowGroup = 16;  // rows per fp32 sub-accumulation / loads in flight
 
-// partial[rb][d][c] = Σ_{r in block rb} A[r][c] · v[r].d   (d < 3)
-__global__ void __launch_bounds__(kColsumThreads)
-    colsum_kernel(const float* __restrict__ A, int64_t lda, int64_t rows, int64_t cols4,
-                  const float4* __restrict__ v, int64_t rows_per_block,
-                  double* __restrict__ part, int64_t part_ld, const IterState* __restrict__ st,
-                  uint64_t* stamps, int stamp_slot) {
-  if (st && !st->active) return;
-  if (stamps && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
-    stamps[4 * st->iter + stamp_slot] = globaltimer();
-  extern __shared__ float4 vs[];
-  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_block;
-  const int64_t r1 = min(rows, r0 + rows_per_block);
-  const int nr = static_cast<int>(r1 - r0);
-  for (int i = threadIdx.x; i < nr; i += kColsumThreads) vs[i] = v[r0 + i];
-  __syncthreads();
-  const int64_t c4 = static_cast<int64_t>(blockIdx.x) * kColsumThreads + threadIdx.x;
-  if (c4 >= cols4) return;
-  const float4* a = reinterpret_cast<const float4*>(A + r0 * lda) + c4;
-  const int64_t ld4 = lda >> 2;
-  double acc[4][3];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = 0.0;
+struct SkGeom {
+  int64_t rows, cols4, units;
+  int grid, kmax;
+};
 
-  int r = 0;
-  for (; r + kRowGroup <= nr; r += kRowGroup) {
-    float4 q[kRowGroup];
-#pragma unroll
-    for (int u = 0; u < kRowGroup; ++u) q[u] = __ldcs(a + static_cast<int64_t>(r + u) * ld4);
-    float f[4][3];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) f[i][0] = f[i][1] = f[i][2] = 0.f;
-#pragma unroll
-    for (int u = 0; u < kRowGroup; ++u) {
-      const float4 w = vs[r + u];
-      const float qq[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        f[i][0] = __fmaf_rn(qq[i], w.x, f[i][0]);
-        f[i][1] = __fmaf_rn(qq[i], w.y, f[i][1]);
-        f[i][2] = __fmaf_rn(qq[i], w.z, f[i][2]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      acc[i][0] += f[i][0];
-      acc[i][1] += f[i][1];
-      acc[i][2] += f[i][2];
-    }
-  }
-  for (; r < nr; ++r) {
-    const float4 q = __ldcs(a + static_cast<int64_t>(r) * ld4);
-    const float4 w = vs[r];
-    const float qq[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      acc[i][0] += static_cast<double>(qq[i] * w.x);
-      acc[i][1] += static_cast<double>(qq[i] * w.y);
-      acc[i][2] += static_cast<double>(qq[i] * w.z);
-    }
-  }
-  double* out = part + static_cast<int64_t>(blockIdx.y) * 3 * part_ld + 4 * c4;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    double2* o = reinterpret_cast<double2*>(out + d * part_ld);
-    o[0] = make_double2(acc[0][d], acc[1][d]);
-    o[1] = make_double2(acc[2][d], acc[3][d]);
+__host__ __device__ __forceinline__ int64_t sk_begin(const SkGeom& g, int64_t cta) {
+  return cta * g.units / g.grid;
+}
+// CTA owning work unit u: the g with begin(g) ≤ u < begin(g+1)
+__device__ __forceinline__ int64_t sk_owner(const SkGeom& g, int64_t u) {
+  return ((u + 1) * g.grid - 1) / g.units;
+}
+
+// Fixed-order sum of the partials covering column c.
+__device__ __forceinline__ void sk_sum(const double* __restrict__ part, const SkGeom& g,
+                                       int64_t c, double& s0, double& s1, double& s2) {
+  const int64_t cb = c / kColsPerBlock;
+  const int64_t cc = c - cb * kColsPerBlock;
+  const int64_t g_lo = sk_owner(g, cb * g.rows);
+  const int64_t g_hi = sk_owner(g, (cb + 1) * g.rows - 1);
+  s0 = s1 = s2 = 0.0;
+  for (int64_t cta = g_lo; cta <= g_hi; ++cta) {
+    const int64_t k = cb - sk_begin(g, cta) / g.rows;
+    const double* p = part + ((cta * g.kmax + k) * 3) * kColsPerBlock + cc;
+    s0 += p[0];
+    s1 += p[kColsPerBlock];
+    s2 += p[2 * kColsPerBlock];
   }
 }
 
-// z_k = Σ_rb partial; solve + filter (solvers.hpp:66-72):
+SkGeom geom(const ColsumPlan& p) {
+  return SkGeom{p.rows, p.cols4, p.units, p.grid, p.kmax};
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kColsumThreads)
+    colsum_kernel(const float* __restrict__ A, int64_t lda, const float4* __restrict__ v,
+                  SkGeom g, double* __restrict__ part, const IterState* __restrict__ st,
+                  uint64_t* stamps, int stamp_slot) {
+  if (st && !st->active) return;
+  if (stamps && blockIdx.x == 0 && threadIdx.x == 0)
+    stamps[4 * st->iter + stamp_slot] = globaltimer();
+  const int64_t ld4 = lda >> 2;
+  int64_t u = sk_begin(g, blockIdx.x);
+  const int64_t u_end = sk_begin(g, blockIdx.x + 1);
+  int slot = 0;
+  while (u < u_end) {
+    const int64_t cb = u / g.rows;
+    const int64_t r0 = u - cb * g.rows;
+    const int64_t r1 = min(g.rows, r0 + (u_end - u));
+    const int64_t c4 = cb * kColsumThreads + threadIdx.x;
+    double acc[4][3];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = 0.0;
+    if (c4 < g.cols4) {
+      const float4* a = reinterpret_cast<const float4*>(A) + c4;
+      int64_t r = r0;
+      for (; r + kRowGroup <= r1; r += kRowGroup) {
+        float4 q[kRowGroup];
+#pragma unroll
+        for (int w = 0; w < kRowGroup; ++w) q[w] = __ldcs(a + (r + w) * ld4);
+        float f[4][3];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) f[i][0] = f[i][1] = f[i][2] = 0.f;
+#pragma unroll
+        for (int w = 0; w < kRowGroup; ++w) {
+          const float4 vv = __ldg(v + r + w);
+          const float qq[4] = {q[w].x, q[w].y, q[w].z, q[w].w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            f[i][0] = __fmaf_rn(qq[i], vv.x, f[i][0]);
+            f[i][1] = __fmaf_rn(qq[i], vv.y, f[i][1]);
+            f[i][2] = __fmaf_rn(qq[i], vv.z, f[i][2]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[i][0] += f[i][0];
+          acc[i][1] += f[i][1];
+          acc[i][2] += f[i][2];
+        }
+      }
+      for (; r < r1; ++r) {
+        const float4 qv = __ldcs(a + r * ld4);
+        const float4 vv = __ldg(v + r);
+        const float qq[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[i][0] += static_cast<double>(qq[i] * vv.x);
+          acc[i][1] += static_cast<double>(qq[i] * vv.y);
+          acc[i][2] += static_cast<double>(qq[i] * vv.z);
+        }
+      }
+    }
+    double* out = part + ((static_cast<int64_t>(blockIdx.x) * g.kmax + slot) * 3) * kColsPerBlock +
+                  4 * threadIdx.x;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double2* o = reinterpret_cast<double2*>(out + d * kColsPerBlock);
+      o[0] = make_double2(acc[0][d], acc[1][d]);
+      o[1] = make_double2(acc[2][d], acc[3][d]);
+    }
+    u += r1 - r0;
+    ++slot;
+  }
+}
+
+// z_k = Σ partials; solve + filter (solvers.hpp:66-72):
 //   c_k = z_k / (λ_k + λ_reg σ²)   (W = Q c, kept for `coefficients`)
 //   g_k = λnum_k · c_k             (ΦW = Q g)
-__global__ void zreduce_filter_kernel(const double* __restrict__ part, int blocks, int64_t k,
-                                      int64_t part_ld, const double* __restrict__ lam,
+__global__ void zreduce_filter_kernel(const double* __restrict__ part, SkGeom g, int64_t k,
+                                      const double* __restrict__ lam,
                                       const double* __restrict__ lam_num, double lambda_reg,
                                       double* __restrict__ coef, float4* __restrict__ g4,
                                       IterState* st) {
   if (!st->active) return;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= k) return;
-  double z0 = 0, z1 = 0, z2 = 0;
-  for (int b = 0; b < blocks; ++b) {
-    const double* p = part + static_cast<int64_t>(b) * 3 * part_ld;
-    z0 += p[i];
-    z1 += p[part_ld + i];
-    z2 += p[2 * part_ld + i];
-  }
+  double z0, z1, z2;
+  sk_sum(part, g, i, z0, z1, z2);
   // σ² of this iteration's E-step, unclamped (registration.hpp:137)
   const double diag = lam[i] + lambda_reg * st->sigma2;
   if (!(diag > 0.0)) set_error(st, kDevSolveDiag, diag);
@@ -135,8 +171,8 @@ __global__ void zreduce_filter_kernel(const double* __restrict__ part, int block
 
 // x̃new = X + V; per-row σ² terms; block partial sums (fixed order).
 __global__ void __launch_bounds__(256)
-    transform_sigma_kernel(const double* __restrict__ part, int blocks, int64_t m,
-                           int64_t part_ld, const double* __restrict__ x0, double* xt64,
+    transform_sigma_kernel(const double* __restrict__ part, SkGeom g, int64_t m,
+                           const double* __restrict__ x0, double* xt64,
                            double* __restrict__ xt_prev, float4* __restrict__ xt4,
                            const double* __restrict__ ptilde_y, const double* __restrict__ var,
                            double* __restrict__ sig_part, IterState* st, uint64_t* stamps) {
@@ -145,13 +181,8 @@ __global__ void __launch_bounds__(256)
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   double term = 0.0;
   if (i < m) {
-    double v0 = 0, v1 = 0, v2 = 0;
-    for (int b = 0; b < blocks; ++b) {
-      const double* p = part + static_cast<int64_t>(b) * 3 * part_ld;
-      v0 += p[i];
-      v1 += p[part_ld + i];
-      v2 += p[2 * part_ld + i];
-    }
+    double v0, v1, v2;
+    sk_sum(part, g, i, v0, v1, v2);
     const double o0 = xt64[i], o1 = xt64[m + i], o2 = xt64[2 * m + i];
     const double n0 = x0[i] + v0, n1 = x0[m + i] + v1, n2 = x0[2 * m + i] + v2;
     const double d0 = n0 - o0, d1 = n1 - o1, d2 = n2 - o2;
@@ -209,73 +240,69 @@ __global__ void sigma_final_kernel(const double* __restrict__ sig_part, int bloc
   if (early_stop && delta < 1e-10) st->active = 0;
 }
 
+// out = X + Σ partials  (apply_transform_lowrank epilogue, no σ² terms)
+__global__ void vreduce_add_kernel(const double* __restrict__ part, SkGeom g, int64_t m,
+                                   const double* __restrict__ x0, int d,
+                                   double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double v[3];
+  sk_sum(part, g, i, v[0], v[1], v[2]);
+  for (int c = 0; c < d; ++c) out[c * m + i] = (x0 ? x0[c * m + i] : 0.0) + v[c];
+}
+
 // ---------------------------------------------------------------------------
 
 ColsumPlan make_colsum_plan(int64_t rows, int64_t cols, int sm_count) {
   ColsumPlan p;
+  p.rows = rows;
+  p.cols = cols;
   p.cols4 = (cols + 3) / 4;
   p.col_blocks = ceil_div(p.cols4, kColsumThreads);
-  // aim for ~4 resident waves; at least 64 rows per block, at most 2048
-  const int64_t target = static_cast<int64_t>(sm_count) * 8;
-  int64_t row_blocks = std::max<int64_t>(1, target / p.col_blocks);
-  int64_t rpb = (rows + row_blocks - 1) / row_blocks;
-  rpb = std::max<int64_t>(64, std::min<int64_t>(2048, rpb));
-  rpb = (rpb + kRowGroup - 1) / kRowGroup * kRowGroup;
-  p.rows_per_block = rpb;
-  p.row_blocks = ceil_div(rows, rpb);
+  p.units = p.rows * p.col_blocks;
+  int occ = 0;
+  FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, colsum_kernel, kColsumThreads, 0));
+  const int64_t slots = static_cast<int64_t>(sm_count) * std::max(occ, 1);
+  p.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(slots, p.units)));
+  const int64_t per = (p.units + p.grid - 1) / p.grid;
+  p.kmax = static_cast<int>((per + rows - 1) / rows + 1);
   return p;
 }
 
-void launch_colsum(const ColsumPlan& p, const float* A, int64_t lda, int64_t rows,
-                   const float4* v, double* part, int64_t part_ld, const IterState* st,
-                   uint64_t* stamps, int stamp_slot, cudaStream_t stream) {
-  const size_t smem = sizeof(float4) * p.rows_per_block;
-  colsum_kernel<<<dim3(p.col_blocks, p.row_blocks), kColsumThreads, smem, stream>>>(
-      A, lda, rows, p.cols4, v, p.rows_per_block, part, part_ld, st, stamps, stamp_slot);
+void launch_colsum(const ColsumPlan& p, const float* A, int64_t lda, const float4* v,
+                   double* part, const IterState* st, uint64_t* stamps, int stamp_slot,
+                   cudaStream_t stream) {
+  colsum_kernel<<<p.grid, kColsumThreads, 0, stream>>>(A, lda, v, geom(p), part, st, stamps,
+                                                       stamp_slot);
   FCPD_LAUNCH_CHECK();
 }
 
-void launch_zreduce(const double* part, int blocks, int64_t k, int64_t part_ld,
-                    const double* lam, const double* lam_num, double lambda_reg, double* coef,
-                    float4* g4, IterState* st, cudaStream_t stream) {
-  zreduce_filter_kernel<<<ceil_div(k, 256), 256, 0, stream>>>(part, blocks, k, part_ld, lam,
-                                                              lam_num, lambda_reg, coef, g4, st);
+void launch_zreduce(const ColsumPlan& p, const double* part, const double* lam,
+                    const double* lam_num, double lambda_reg, double* coef, float4* g4,
+                    IterState* st, cudaStream_t stream) {
+  zreduce_filter_kernel<<<ceil_div(p.cols, 256), 256, 0, stream>>>(
+      part, geom(p), p.cols, lam, lam_num, lambda_reg, coef, g4, st);
   FCPD_LAUNCH_CHECK();
 }
 
-void launch_transform_sigma(const double* part, int blocks, int64_t m, int64_t part_ld,
-                            const double* x0, double* xt64, double* xt_prev, float4* xt4,
+void launch_transform_sigma(const ColsumPlan& p, const double* part, const double* x0,
+                            double* xt64, double* xt_prev, float4* xt4,
                             const double* ptilde_y, const double* var, double* sig_part,
                             int d, int early_stop, double* trace, IterState* st,
                             uint64_t* stamps, cudaStream_t stream) {
+  const int64_t m = p.cols;
   const int nb = ceil_div(m, 256);
-  transform_sigma_kernel<<<nb, 256, 0, stream>>>(part, blocks, m, part_ld, x0, xt64, xt_prev,
-                                                 xt4, ptilde_y, var, sig_part, st, stamps);
+  transform_sigma_kernel<<<nb, 256, 0, stream>>>(part, geom(p), m, x0, xt64, xt_prev, xt4,
+                                                 ptilde_y, var, sig_part, st, stamps);
   FCPD_LAUNCH_CHECK();
   sigma_final_kernel<<<1, 256, 0, stream>>>(sig_part, nb, m, d, early_stop, trace, st, stamps);
   FCPD_LAUNCH_CHECK();
 }
 
-}  // namespace fcpd
-
-namespace fcpd {
-
-// out = X + Σ_b part[b]  (apply_transform_lowrank epilogue, no σ² terms)
-__global__ void vreduce_add_kernel(const double* __restrict__ part, int blocks, int64_t m,
-                                   int64_t part_ld, const double* __restrict__ x0, int d,
-                                   double* __restrict__ out) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  for (int c = 0; c < d; ++c) {
-    double v = 0.0;
-    for (int b = 0; b < blocks; ++b) v += part[(static_cast<int64_t>(b) * 3 + c) * part_ld + i];
-    out[c * m + i] = x0[c * m + i] + v;
-  }
-}
-
-void launch_vreduce_add(const double* part, int blocks, int64_t m, int64_t part_ld,
-                        const double* x0, int d, double* out, cudaStream_t stream) {
-  vreduce_add_kernel<<<ceil_div(m, 256), 256, 0, stream>>>(part, blocks, m, part_ld, x0, d, out);
+void launch_vreduce_add(const ColsumPlan& p, const double* part, const double* x0, int d,
+                        double* out, cudaStream_t stream) {
+  vreduce_add_kernel<<<ceil_div(p.cols, 256), 256, 0, stream>>>(part, geom(p), p.cols, x0, d,
+                                                                out);
   FCPD_LAUNCH_CHECK();
 }
 

@@ -8,34 +8,45 @@
 
 namespace fcpd {
 
+constexpr int kColsumThreads = 256;
+constexpr int kColsPerBlock = 4 * kColsumThreads;  // 1024 columns per column block
+
+// Stream-K plan for "column sums of a row-major matrix weighted by a per-row
+// 3-vector": the rows × column-blocks work units (one 4 KB row segment each)
+// are split evenly over `grid` persistent CTAs; CTA g writes one fp64
+// partial per column block it touches (slot k < kmax).
 struct ColsumPlan {
-  int64_t cols4 = 0;
+  int64_t rows = 0, cols = 0, cols4 = 0;
   int col_blocks = 0;
-  int row_blocks = 0;
-  int64_t rows_per_block = 0;
+  int64_t units = 0;
+  int grid = 0;
+  int kmax = 0;
+  size_t part_doubles() const {
+    return static_cast<size_t>(grid) * kmax * 3 * kColsPerBlock;
+  }
 };
 
 ColsumPlan make_colsum_plan(int64_t rows, int64_t cols, int sm_count);
 
-// part[rb][d][c] (d<3, leading dimension part_ld ≥ 4·cols4) =
-//   Σ_{r∈rb} A[r][c]·v[r].d ;  A row-major fp32 with lda % 4 == 0.
-void launch_colsum(const ColsumPlan& p, const float* A, int64_t lda, int64_t rows,
-                   const float4* v, double* part, int64_t part_ld, const IterState* st,
-                   uint64_t* stamps, int stamp_slot, cudaStream_t stream);
+// part ← partials of Σ_r A[r][c]·v[r].d (d < 3); A row-major fp32, lda % 4 == 0.
+void launch_colsum(const ColsumPlan& p, const float* A, int64_t lda, const float4* v,
+                   double* part, const IterState* st, uint64_t* stamps, int stamp_slot,
+                   cudaStream_t stream);
 
-void launch_zreduce(const double* part, int blocks, int64_t k, int64_t part_ld,
-                    const double* lam, const double* lam_num, double lambda_reg, double* coef,
-                    float4* g4, IterState* st, cudaStream_t stream);
+// z = Σ partials (column c ↔ basis index k); c = z/(λ + λ_reg σ²); g = λnum·c.
+void launch_zreduce(const ColsumPlan& p, const double* part, const double* lam,
+                    const double* lam_num, double lambda_reg, double* coef, float4* g4,
+                    IterState* st, cudaStream_t stream);
 
-void launch_transform_sigma(const double* part, int blocks, int64_t m, int64_t part_ld,
-                            const double* x0, double* xt64, double* xt_prev, float4* xt4,
+// x̃new = X + Σ partials (column c ↔ model point m); per-row σ² terms; σ².
+void launch_transform_sigma(const ColsumPlan& p, const double* part, const double* x0,
+                            double* xt64, double* xt_prev, float4* xt4,
                             const double* ptilde_y, const double* var, double* sig_part,
                             int d, int early_stop, double* trace, IterState* st,
                             uint64_t* stamps, cudaStream_t stream);
 
-}  // namespace fcpd
+// out = (x0 or 0) + Σ partials, D columns.
+void launch_vreduce_add(const ColsumPlan& p, const double* part, const double* x0, int d,
+                        double* out, cudaStream_t stream);
 
-namespace fcpd {
-void launch_vreduce_add(const double* part, int blocks, int64_t m, int64_t part_ld,
-                        const double* x0, int d, double* out, cudaStream_t stream);
 }  // namespace fcpd
