@@ -1,0 +1,307 @@
+// fastcpd/fastcpd.hpp — drop-in C++ API for the B200 engine.
+//
+// Mirrors the reference's public headers (proj/include/fastcpd/*.hpp) for the
+// registration path: the same namespace, type names, field names, defaults
+// and exception classes, so code written against
+//   fastcpd::register_pointsets(const PointSet&, const PointSet&,
+//                               const RegistrationConfig&)
+// (registration.hpp:79-81) compiles against this header and runs on the GPU
+// through the C ABI in fcpd_capi.h.  Differences:
+//  * PointSet::pts is fastcpd::Matrix (column-major, Eigen-compatible layout
+//    and the Eigen accessors used by the reference's callers: rows(), cols(),
+//    operator()(i,j), data(), resize(), setZero()).  Define
+//    FASTCPD_USE_EIGEN before including to use Eigen::MatrixXd instead.
+//  * RegistrationResult::correspondence is filled only when
+//    cfg.want_correspondence is set (the device path never forms the M×N P).
+//  * Only the fast / fast_lowrank variants run on the device; cpd variants
+//    throw ParameterError (they are the reference's O(M³) baselines).
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "fcpd_capi.h"
+
+#ifdef FASTCPD_USE_EIGEN
+#include <Eigen/Core>
+#endif
+
+namespace fastcpd {
+
+// ------------------------------------------------------ errors.hpp:8-34
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ParseError : Error {
+  using Error::Error;
+};
+struct DimensionError : Error {
+  using Error::Error;
+};
+struct ParameterError : Error {
+  using Error::Error;
+};
+struct NumericError : Error {
+  using Error::Error;
+};
+struct IoError : Error {
+  using Error::Error;
+};
+struct DeviceError : Error {  // CUDA / NCCL / out of device memory
+  using Error::Error;
+};
+
+inline void throw_code(int code, const std::string& msg) {
+  switch (code) {
+    case FCPD_OK: return;
+    case FCPD_ERR_PARAMETER: throw ParameterError(msg);
+    case FCPD_ERR_DIMENSION: throw DimensionError(msg);
+    case FCPD_ERR_NUMERIC: throw NumericError(msg);
+    case FCPD_ERR_IO: throw IoError(msg);
+    case FCPD_ERR_PARSE: throw ParseError(msg);
+    default: throw DeviceError(msg);
+  }
+}
+
+// -------------------------------------------------------------- matrix
+#ifdef FASTCPD_USE_EIGEN
+using Matrix = Eigen::MatrixXd;
+using Index = Eigen::Index;
+#else
+using Index = std::ptrdiff_t;
+// Column-major dense fp64 matrix: the subset of Eigen::MatrixXd the
+// registration API and its callers use.
+class Matrix {
+ public:
+  Matrix() = default;
+  Matrix(Index r, Index c) : r_(r), c_(c), v_(static_cast<size_t>(r * c), 0.0) {}
+  Index rows() const { return r_; }
+  Index cols() const { return c_; }
+  Index size() const { return r_ * c_; }
+  double& operator()(Index i, Index j) { return v_[static_cast<size_t>(j * r_ + i)]; }
+  double operator()(Index i, Index j) const { return v_[static_cast<size_t>(j * r_ + i)]; }
+  double* data() { return v_.data(); }
+  const double* data() const { return v_.data(); }
+  void resize(Index r, Index c) {
+    r_ = r;
+    c_ = c;
+    v_.assign(static_cast<size_t>(r * c), 0.0);
+  }
+  void setZero() { std::fill(v_.begin(), v_.end(), 0.0); }
+  static Matrix Zero(Index r, Index c) { return Matrix(r, c); }
+
+ private:
+  Index r_ = 0, c_ = 0;
+  std::vector<double> v_;
+};
+#endif
+
+// -------------------------------------------------- pointset.hpp:19-43
+struct PointSet {
+  Matrix pts;
+  PointSet() = default;
+  explicit PointSet(Matrix p) : pts(std::move(p)) {}
+  Index count() const { return pts.rows(); }
+  Index dim() const { return pts.cols(); }
+};
+
+// ------------------------------------------------------ solvers.hpp:14-54
+struct Coefficients {
+  Matrix w;
+};
+
+enum class SolverVariant { cpd, cpd_lowrank, fast, fast_lowrank };
+
+inline const char* to_string(SolverVariant v) {
+  switch (v) {
+    case SolverVariant::cpd: return "cpd";
+    case SolverVariant::cpd_lowrank: return "cpd_lowrank";
+    case SolverVariant::fast: return "fast";
+    case SolverVariant::fast_lowrank: return "fast_lowrank";
+  }
+  return "?";
+}
+
+inline SolverVariant variant_from_string(const std::string& s) {
+  if (s == "cpd") return SolverVariant::cpd;
+  if (s == "cpd_lowrank" || s == "cpd-lowrank") return SolverVariant::cpd_lowrank;
+  if (s == "fast") return SolverVariant::fast;
+  if (s == "fast_lowrank" || s == "fast-lowrank") return SolverVariant::fast_lowrank;
+  throw ParameterError("unknown solver variant: " + s);
+}
+
+inline bool is_lowrank(SolverVariant v) {
+  return v == SolverVariant::cpd_lowrank || v == SolverVariant::fast_lowrank;
+}
+inline bool is_fast(SolverVariant v) {
+  return v == SolverVariant::fast || v == SolverVariant::fast_lowrank;
+}
+
+inline Index lowrank_rank(double rank_fraction, Index m) {
+  if (rank_fraction <= 0.0 || rank_fraction > 1.0)
+    throw ParameterError("rank_fraction must lie in (0, 1]");
+  Index k = static_cast<Index>(std::llround(rank_fraction * static_cast<double>(m)));
+  if (k < 1) k = 1;
+  if (k > m) k = m;
+  return k;
+}
+
+// --------------------------------------------- correspondence.hpp:12-29
+inline constexpr double kSigma2Floor = 1e-10;
+
+struct Correspondence {
+  Matrix p;
+  bool row_constrained = false;
+  std::vector<Index> degenerate_rows;
+  bool sigma2_clamped = false;
+};
+
+// ------------------------------------------------ registration.hpp:21-56
+struct TimingBreakdown {
+  double t_c = 0.0, t_eig = 0.0, t_iter = 0.0, t_f = 0.0, t_o = 0.0, t_total = 0.0;
+  double t_setup = 0.0;  // extension: Gram build + eigendecomposition
+};
+
+struct RegistrationConfig {
+  double omega = 0.7;
+  double beta = 2.0;
+  double lambda_reg = 10.0;
+  int iterations = 100;
+  SolverVariant variant = SolverVariant::fast;
+  double rank_fraction = 0.1;
+  unsigned long seed = 0;
+  bool normalize = true;
+  bool early_stop = false;
+  bool want_correspondence = false;  // extension: materialise P̃ (M×N) at the end
+  int device = 0;                    // extension: CUDA device of the default context
+};
+
+struct RegistrationDiagnostics {
+  long degenerate_rows = 0;
+  long sigma2_clamps = 0;
+  std::string baseline_solver = "dense LDLT factorization";
+};
+
+struct RegistrationResult {
+  PointSet transformed;
+  Coefficients coefficients;
+  Correspondence correspondence;
+  std::vector<double> sigma2_trace;
+  TimingBreakdown timing;
+  RegistrationDiagnostics diagnostics;
+  double sigma2_initial = 0.0;
+};
+
+// ----------------------------------------------------------- context
+// One engine context per device per thread (stream, cuSOLVER handle, cached
+// spectral basis).  register_pointsets() uses a thread-local default.
+class Context {
+ public:
+  explicit Context(int device = 0) {
+    fcpd_ctx* c = nullptr;
+    const int rc = fcpd_create(&c, device);
+    if (rc != FCPD_OK) throw_code(rc, "fcpd_create failed on device " + std::to_string(device));
+    ctx_.reset(c);
+  }
+  fcpd_ctx* get() const { return ctx_.get(); }
+  void check(int rc) const {
+    if (rc != FCPD_OK) throw_code(rc, fcpd_last_error(ctx_.get()));
+  }
+
+  RegistrationResult register_pointsets(const PointSet& x, const PointSet& y,
+                                        const RegistrationConfig& cfg) const {
+    if (x.count() == 0 || y.count() == 0) throw ParameterError("register: empty point set");
+    if (x.dim() != y.dim()) throw DimensionError("register: model and scene dimension mismatch");
+    const Index m = x.count(), n = y.count(), d = x.dim();
+    fcpd_config c;
+    fcpd_config_default(&c);
+    c.omega = cfg.omega;
+    c.beta = cfg.beta;
+    c.lambda_reg = cfg.lambda_reg;
+    c.iterations = cfg.iterations;
+    c.variant = static_cast<int32_t>(cfg.variant);
+    c.rank_fraction = cfg.rank_fraction;
+    c.seed = cfg.seed;
+    c.normalize = cfg.normalize ? 1 : 0;
+    c.early_stop = cfg.early_stop ? 1 : 0;
+    RegistrationResult res;
+    res.transformed.pts.resize(m, d);
+    res.coefficients.w.resize(m, d);
+    res.sigma2_trace.assign(static_cast<size_t>(cfg.iterations > 0 ? cfg.iterations : 1), 0.0);
+    std::vector<int32_t> mask(static_cast<size_t>(m), 0);
+    fcpd_result out{};
+    out.transformed = res.transformed.pts.data();
+    out.coefficients = res.coefficients.w.data();
+    out.sigma2_trace = res.sigma2_trace.data();
+    out.degenerate_mask = mask.data();
+    if (cfg.want_correspondence) {
+      res.correspondence.p.resize(m, n);
+      out.correspondence = res.correspondence.p.data();
+    }
+    check(fcpd_register(ctx_.get(), x.pts.data(), m, y.pts.data(), n, static_cast<int32_t>(d),
+                        &c, &out));
+    res.sigma2_trace.resize(static_cast<size_t>(out.iterations_run));
+    res.sigma2_initial = out.sigma2_initial;
+    res.diagnostics.degenerate_rows = static_cast<long>(out.degenerate_rows);
+    res.diagnostics.sigma2_clamps = static_cast<long>(out.sigma2_clamps);
+    res.timing = TimingBreakdown{out.timing.t_c,   out.timing.t_eig, out.timing.t_iter,
+                                 out.timing.t_f,   out.timing.t_o,   out.timing.t_total,
+                                 out.timing.t_setup};
+    res.correspondence.row_constrained = out.iterations_run > 0;
+    for (Index i = 0; i < m; ++i)
+      if (mask[static_cast<size_t>(i)]) res.correspondence.degenerate_rows.push_back(i);
+    return res;
+  }
+
+ private:
+  struct Del {
+    void operator()(fcpd_ctx* c) const { fcpd_destroy(c); }
+  };
+  std::unique_ptr<fcpd_ctx, Del> ctx_;
+};
+
+inline Context& default_context(int device = 0) {
+  thread_local std::unique_ptr<Context> ctx;
+  thread_local int dev = -1;
+  if (!ctx || dev != device) {
+    ctx = std::make_unique<Context>(device);
+    dev = device;
+  }
+  return *ctx;
+}
+
+// registration.hpp:79-175 — the drop-in entry point.
+inline RegistrationResult register_pointsets(const PointSet& x, const PointSet& y,
+                                             const RegistrationConfig& cfg) {
+  return default_context(cfg.device).register_pointsets(x, y, cfg);
+}
+
+// registration.hpp:59-69 (host, O(M+N)).
+inline double init_sigma2(const PointSet& x, const PointSet& y) {
+  if (x.count() == 0 || y.count() == 0) throw ParameterError("init_sigma2: empty point set");
+  if (x.dim() != y.dim()) throw DimensionError("init_sigma2: dimension mismatch");
+  const double m = static_cast<double>(x.count()), n = static_cast<double>(y.count());
+  double fx = 0, fy = 0, dot = 0;
+  for (Index j = 0; j < x.dim(); ++j) {
+    double sx = 0, sy = 0;
+    for (Index i = 0; i < x.count(); ++i) {
+      fx += x.pts(i, j) * x.pts(i, j);
+      sx += x.pts(i, j);
+    }
+    for (Index i = 0; i < y.count(); ++i) {
+      fy += y.pts(i, j) * y.pts(i, j);
+      sy += y.pts(i, j);
+    }
+    dot += sx * sy;
+  }
+  const double v = (m * fy + n * fx - 2.0 * dot) / (static_cast<double>(x.dim()) * m * n);
+  return v > 0.0 ? v : 0.0;
+}
+
+}  // namespace fastcpd

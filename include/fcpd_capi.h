@@ -12,7 +12,7 @@
  * which map 1:1 to the reference exception hierarchy (errors.hpp:8-34);
  * fcpd_last_error() returns the message the reference would have thrown
  * (e.g. "register: iteration 3: update_sigma2: negative variance ...").
- * include/fastcpd/*.hpp rethrow them as fastcpd::ParameterError etc.
+ * include/fastcpd/fastcpd.hpp rethrows them as fastcpd::ParameterError etc.
  *
  * Threading: one context per host thread; a context is not thread-safe.
  */

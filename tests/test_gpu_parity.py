@@ -77,7 +77,7 @@ def test_dense_posterior_matches_oracle(ctx, orc, omega, s2):
     (300, 360, 3, 0.0, 0.3, False),
     (777, 1001, 3, 0.2, 1e-3, False),  # ragged: not multiples of any tile
     (256, 257, 1, 0.1, 1e-4, False),
-    (500, 400, 2, 0.7, 2e-5, True),    # small σ²: scene near the model, as in EM
+    (400, 500, 2, 0.7, 2e-5, True),    # small σ²: scene near the model, as in EM
     (2000, 2400, 3, 0.3, 5e-6, True),
     (3000, 3000, 3, 0.0, 1e-6, True),
 ])
@@ -88,8 +88,9 @@ def test_estep_matches_oracle(ctx, orc, m, n, d, omega, s2, aligned):
     (DESIGN.md §Precision)."""
     xt = orc.make_cloud(m, d, 100 + m) * 0.6
     if aligned:
+        # every model point has a scene counterpart within a few σ
         rng = np.random.default_rng(m)
-        idx = rng.integers(0, m, n)
+        idx = np.concatenate([np.arange(m), rng.integers(0, m, n - m)])
         y = xt[idx] + rng.normal(0.0, 2.0 * math.sqrt(s2), (n, d))
     else:
         y = orc.make_cloud(n, d, 200 + n) * 0.6
@@ -129,7 +130,8 @@ def test_estep_far_rows_not_degenerate(ctx, orc):
     got = ctx.estep(xt, y, 0.0, s2)
     assert not got["degenerate"].any()
     assert np.allclose(got["ptilde_y"], ref.ptilde_y, rtol=0, atol=1e-6)
-    assert np.allclose(got["p1"], ref.p1, rtol=2e-5, atol=0)
+    # far rows: fp32 log-weights at t ≈ 200 carry ~ε₃₂·t
+    assert np.allclose(got["p1"], ref.p1, rtol=1e-4, atol=0)
 
 
 # ------------------------------------------------------ setup + M-step (L2)
