@@ -90,4 +90,6 @@ __device__ __forceinline__ T warp_sum(T v) {
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
 }  // namespace fcpd

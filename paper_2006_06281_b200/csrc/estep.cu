@@ -37,6 +37,7 @@ namespace fcpd {
 namespace {
 
 constexpr int kTile = 256;       // points staged in shared memory per step
+constexpr int kCombineLanes = 8; // lanes cooperating on one row/column reduction
 constexpr float kPadCoord = 3.0e18f;  // padding point: t ≈ 1e37, 2^-t = 0
 
 __device__ __forceinline__ float sqdist(float4 a, float4 b) {
@@ -175,10 +176,15 @@ __global__ void estep_col_combine_kernel(const double* __restrict__ part, int sp
                                          int32_t* __restrict__ flag_count,
                                          const IterState* __restrict__ st) {
   if (!st->active) return;
-  const int64_t col = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (col >= n) return;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t col = gid / kCombineLanes;
+  const int lane = static_cast<int>(gid % kCombineLanes);
   double sm = 0.0;
-  for (int s = 0; s < splits; ++s) sm += part[static_cast<int64_t>(s) * n + col];
+  if (col < n)
+    for (int s = lane; s < splits; s += kCombineLanes) sm += part[static_cast<int64_t>(s) * n + col];
+#pragma unroll
+  for (int o = kCombineLanes / 2; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+  if (col >= n || lane != 0) return;
   const double log2c = st->log2c;
   const double c = exp2(log2c);  // 0 when ω = 0
   const double total = sm + c;
@@ -386,17 +392,33 @@ __global__ void estep_row_combine_kernel(const double* __restrict__ part, int sp
                                          RowOut out, YStats ys, int32_t* __restrict__ flag_list,
                                          int32_t* __restrict__ flag_count, IterState* st) {
   if (!st->active) return;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (row >= m) return;
+  // kCombineLanes lanes per row, lane j sums splits j, j+L, … then a fixed
+  // xor-tree combines the lanes: deterministic, and L× the memory-level
+  // parallelism of one thread per row.
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t row = gid / kCombineLanes;
+  const int lane = static_cast<int>(gid % kCombineLanes);
+  const bool live = row < m;
   double a0 = 0, ax = 0, ay = 0, az = 0, av = 0;
-  for (int sp = 0; sp < splits; ++sp) {
-    const double* p = part + static_cast<int64_t>(sp) * 5 * m;
-    a0 += p[row];
-    ax += p[m + row];
-    ay += p[2 * m + row];
-    az += p[3 * m + row];
-    av += p[4 * m + row];
+  if (live) {
+    for (int sp = lane; sp < splits; sp += kCombineLanes) {
+      const double* p = part + static_cast<int64_t>(sp) * 5 * m;
+      a0 += p[row];
+      ax += p[m + row];
+      ay += p[2 * m + row];
+      az += p[3 * m + row];
+      av += p[4 * m + row];
+    }
   }
+#pragma unroll
+  for (int o = kCombineLanes / 2; o > 0; o >>= 1) {
+    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+    ax += __shfl_xor_sync(0xffffffffu, ax, o);
+    ay += __shfl_xor_sync(0xffffffffu, ay, o);
+    az += __shfl_xor_sync(0xffffffffu, az, o);
+    av += __shfl_xor_sync(0xffffffffu, av, o);
+  }
+  if (!live || lane != 0) return;
   if (!(a0 >= static_cast<double>(n) * 0x1p-76)) {
     const int slot = atomicAdd(flag_count, 1);
     flag_list[slot] = static_cast<int32_t>(row);
@@ -507,7 +529,7 @@ void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t 
       <<<dim3(p.col_blocks, p.col_splits), 128, 0, stream>>>(b.xt4, m, b.y4b, n, p.m_per_split,
                                                              st, b.col_part);
   FCPD_LAUNCH_CHECK();
-  estep_col_combine_kernel<<<ceil_div(n, 256), 256, 0, stream>>>(
+  estep_col_combine_kernel<<<ceil_div(n * kCombineLanes, 256), 256, 0, stream>>>(
       b.col_part, p.col_splits, m, n, b.y4b, b.b2, b.pt1, b.col_flags, b.flags_count, st);
   FCPD_LAUNCH_CHECK();
   estep_col_fallback_kernel<<<148, 256, 0, stream>>>(b.xt4, m, b.y4b, b.b2, b.pt1, b.col_flags,
@@ -518,7 +540,7 @@ void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t 
       <<<dim3(p.row_blocks, p.row_splits), 128, 0, stream>>>(b.xt4, m, b.y4b, n, p.n_per_split,
                                                              st, b.row_part);
   FCPD_LAUNCH_CHECK();
-  estep_row_combine_kernel<<<ceil_div(m, 256), 256, 0, stream>>>(
+  estep_row_combine_kernel<<<ceil_div(m * kCombineLanes, 256), 256, 0, stream>>>(
       b.row_part, p.row_splits, m, n, b.xt64, b.out, b.ystats, b.row_flags, b.flags_count + 1,
       st);
   FCPD_LAUNCH_CHECK();

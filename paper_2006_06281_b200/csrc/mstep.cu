@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "mstep.cuh"
@@ -64,6 +66,32 @@ __device__ __forceinline__ void sk_sum(const double* __restrict__ part, const Sk
     s0 += p[0];
     s1 += p[kColsPerBlock];
     s2 += p[2 * kColsPerBlock];
+  }
+}
+
+// kSkLanes lanes cooperate on one column (lane l takes CTAs g_lo+l, +2l, …);
+// a fixed xor tree combines them — deterministic, kSkLanes× the MLP.
+constexpr int kSkLanes = 4;
+__device__ __forceinline__ void sk_sum_lanes(const double* __restrict__ part, const SkGeom& g,
+                                             int64_t c, int lane, double& s0, double& s1,
+                                             double& s2) {
+  const int64_t cb = c / kColsPerBlock;
+  const int64_t cc = c - cb * kColsPerBlock;
+  const int64_t g_lo = sk_owner(g, cb * g.rows);
+  const int64_t g_hi = sk_owner(g, (cb + 1) * g.rows - 1);
+  s0 = s1 = s2 = 0.0;
+  for (int64_t cta = g_lo + lane; cta <= g_hi; cta += kSkLanes) {
+    const int64_t k = cb - sk_begin(g, cta) / g.rows;
+    const double* p = part + ((cta * g.kmax + k) * 3) * kColsPerBlock + cc;
+    s0 += p[0];
+    s1 += p[kColsPerBlock];
+    s2 += p[2 * kColsPerBlock];
+  }
+#pragma unroll
+  for (int o = kSkLanes / 2; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
   }
 }
 
@@ -144,6 +172,192 @@ __global__ void __launch_bounds__(kColsumThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Bulk-copy (TMA engine) variant: one CTA per SM, a producer warp streams the
+// CTA's stream-K row segments into a 6-stage shared-memory ring with
+// cp.async.bulk (+ L2 evict-first) completing on mbarriers; 8 consumer warps
+// read the stage (conflict-free LDS.128) and accumulate.  Up to 192 KB of
+// the basis is in flight per SM regardless of register pressure — the
+// long-scoreboard stall that capped the LDG kernel at ~85 % of HBM.
+namespace {
+constexpr int kBulkStages = 3;       // × 2 CTAs per SM → 192 KB in flight per SM
+constexpr int kBulkCtasPerSm = 2;
+constexpr int kStageBytes = 32 * 1024;
+constexpr int kBulkConsumers = kColsumThreads;         // 8 warps
+constexpr int kBulkThreads = kBulkConsumers + 32;      // + producer warp
+constexpr int kBulkMaxChunkRows = 64;
+constexpr int kBulkSmem = kBulkStages * kStageBytes + 2 * kBulkStages * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// The chunk sequence both roles walk: segments (cb, rows r0..r1) of the
+// CTA's stream-K range, each cut into chunks of ≤ chunk_rows rows.
+struct SegCursor {
+  int64_t u, u_end, cb, r, r1;
+  __device__ bool next_segment(const SkGeom& g) {
+    if (u >= u_end) return false;
+    cb = u / g.rows;
+    r = u - cb * g.rows;
+    r1 = min(g.rows, r + (u_end - u));
+    u += r1 - r;
+    return true;
+  }
+};
+}  // namespace
+
+__global__ void __launch_bounds__(kBulkThreads, kBulkCtasPerSm)
+    colsum_bulk_kernel(const float* __restrict__ A, int64_t lda, const float4* __restrict__ v,
+                       SkGeom g, double* __restrict__ part, const IterState* __restrict__ st,
+                       uint64_t* stamps, int stamp_slot) {
+  if (st && !st->active) return;
+  if (stamps && blockIdx.x == 0 && threadIdx.x == 0)
+    stamps[4 * st->iter + stamp_slot] = globaltimer();
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* ring = reinterpret_cast<float*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBulkStages * kStageBytes);
+  uint64_t* empty = full + kBulkStages;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < kBulkStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kBulkConsumers / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t u0 = sk_begin(g, blockIdx.x), u1 = sk_begin(g, blockIdx.x + 1);
+  const int64_t col_blocks = (g.cols4 + kColsumThreads - 1) / kColsumThreads;
+
+  if (tid >= kBulkConsumers) {  // ---------------- producer warp
+    if (tid != kBulkConsumers) return;
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    SegCursor c{u0, u1, 0, 0, 0};
+    int64_t chunk = 0;
+    while (c.next_segment(g)) {
+      const int64_t c4 = min(static_cast<int64_t>(kColsumThreads), g.cols4 - c.cb * kColsumThreads);
+      const uint32_t seg_bytes = static_cast<uint32_t>(c4 * 16);
+      const int rows_per_chunk = static_cast<int>(min64(kBulkMaxChunkRows, kStageBytes / seg_bytes));
+      const bool contiguous = col_blocks == 1 && lda == 4 * g.cols4;
+      for (int64_t r = c.r; r < c.r1; r += rows_per_chunk, ++chunk) {
+        const int nr = static_cast<int>(min64(rows_per_chunk, c.r1 - r));
+        const int s = static_cast<int>(chunk % kBulkStages);
+        const uint32_t ph = static_cast<uint32_t>((chunk / kBulkStages) & 1);
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], seg_bytes * nr);
+        float* dst = ring + static_cast<int64_t>(s) * (kStageBytes / 4);
+        const float* src = A + r * lda + c.cb * (4 * kColsumThreads);
+        if (contiguous) {
+          bulk_g2s(dst, src, seg_bytes * nr, &full[s], policy);
+        } else {
+          for (int i = 0; i < nr; ++i)
+            bulk_g2s(dst + i * (seg_bytes / 4), src + i * lda, seg_bytes, &full[s], policy);
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------ consumer warps
+  SegCursor c{u0, u1, 0, 0, 0};
+  int64_t chunk = 0;
+  int slot = 0;
+  while (c.next_segment(g)) {
+    const int64_t c4 = min(static_cast<int64_t>(kColsumThreads), g.cols4 - c.cb * kColsumThreads);
+    const uint32_t seg_bytes = static_cast<uint32_t>(c4 * 16);
+    const int rows_per_chunk = static_cast<int>(min64(kBulkMaxChunkRows, kStageBytes / seg_bytes));
+    const bool active = tid < c4;
+    double acc[4][3];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = 0.0;
+    for (int64_t r = c.r; r < c.r1; r += rows_per_chunk, ++chunk) {
+      const int nr = static_cast<int>(min64(rows_per_chunk, c.r1 - r));
+      const int s = static_cast<int>(chunk % kBulkStages);
+      const uint32_t ph = static_cast<uint32_t>((chunk / kBulkStages) & 1);
+      mbar_wait(&full[s], ph);
+      if (active) {
+        const float4* row = reinterpret_cast<const float4*>(ring + static_cast<int64_t>(s) * (kStageBytes / 4)) + tid;
+        const int stride4 = static_cast<int>(seg_bytes / 16);
+        float f[4][3];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) f[i][0] = f[i][1] = f[i][2] = 0.f;
+        auto fma_row = [&](const float4 q, const float4 vv) {
+          const float qq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            f[j][0] = __fmaf_rn(qq[j], vv.x, f[j][0]);
+            f[j][1] = __fmaf_rn(qq[j], vv.y, f[j][1]);
+            f[j][2] = __fmaf_rn(qq[j], vv.z, f[j][2]);
+          }
+        };
+        auto flush = [&] {  // fp32 over ≤ 8 rows, then fp64
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc[j][0] += f[j][0];
+            acc[j][1] += f[j][1];
+            acc[j][2] += f[j][2];
+            f[j][0] = f[j][1] = f[j][2] = 0.f;
+          }
+        };
+        int i = 0;
+        for (; i + 8 <= nr; i += 8) {  // 8 independent LDS + 8 broadcast LDG in flight
+          float4 vv[8], q[8];
+#pragma unroll
+          for (int w = 0; w < 8; ++w) vv[w] = __ldg(v + r + i + w);
+#pragma unroll
+          for (int w = 0; w < 8; ++w) q[w] = row[(i + w) * stride4];
+#pragma unroll
+          for (int w = 0; w < 8; ++w) fma_row(q[w], vv[w]);
+          flush();
+        }
+        for (; i < nr; ++i) fma_row(row[i * stride4], __ldg(v + r + i));
+        flush();
+      }
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    }
+    double* out = part + ((static_cast<int64_t>(blockIdx.x) * g.kmax + slot) * 3) * kColsPerBlock +
+                  4 * tid;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double2* o = reinterpret_cast<double2*>(out + d * kColsPerBlock);
+      o[0] = make_double2(acc[0][d], acc[1][d]);
+      o[1] = make_double2(acc[2][d], acc[3][d]);
+    }
+    ++slot;
+  }
+}
+
 // z_k = Σ partials; solve + filter (solvers.hpp:66-72):
 //   c_k = z_k / (λ_k + λ_reg σ²)   (W = Q c, kept for `coefficients`)
 //   g_k = λnum_k · c_k             (ΦW = Q g)
@@ -153,10 +367,11 @@ __global__ void zreduce_filter_kernel(const double* __restrict__ part, SkGeom g,
                                       double* __restrict__ coef, float4* __restrict__ g4,
                                       IterState* st) {
   if (!st->active) return;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= k) return;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = gid / kSkLanes;
   double z0, z1, z2;
-  sk_sum(part, g, i, z0, z1, z2);
+  sk_sum_lanes(part, g, i < k ? i : k - 1, static_cast<int>(gid % kSkLanes), z0, z1, z2);
+  if (i >= k || gid % kSkLanes) return;
   // σ² of this iteration's E-step, unclamped (registration.hpp:137)
   const double diag = lam[i] + lambda_reg * st->sigma2;
   if (!(diag > 0.0)) set_error(st, kDevSolveDiag, diag);
@@ -178,11 +393,12 @@ __global__ void __launch_bounds__(256)
                            double* __restrict__ sig_part, IterState* st, uint64_t* stamps) {
   if (!st->active) return;
   if (stamps && blockIdx.x == 0 && threadIdx.x == 0) stamps[4 * st->iter + 2] = globaltimer();
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = gid / kSkLanes;
   double term = 0.0;
-  if (i < m) {
-    double v0, v1, v2;
-    sk_sum(part, g, i, v0, v1, v2);
+  double v0, v1, v2;
+  sk_sum_lanes(part, g, i < m ? i : m - 1, static_cast<int>(gid % kSkLanes), v0, v1, v2);
+  if (i < m && gid % kSkLanes == 0) {
     const double o0 = xt64[i], o1 = xt64[m + i], o2 = xt64[2 * m + i];
     const double n0 = x0[i] + v0, n1 = x0[m + i] + v1, n2 = x0[2 * m + i] + v2;
     const double d0 = n0 - o0, d1 = n1 - o1, d2 = n2 - o2;
@@ -260,10 +476,24 @@ ColsumPlan make_colsum_plan(int64_t rows, int64_t cols, int sm_count) {
   p.cols4 = (cols + 3) / 4;
   p.col_blocks = ceil_div(p.cols4, kColsumThreads);
   p.units = p.rows * p.col_blocks;
-  int occ = 0;
-  FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, colsum_kernel, kColsumThreads, 0));
-  const int64_t slots = static_cast<int64_t>(sm_count) * std::max(occ, 1);
-  p.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(slots, p.units)));
+  // FCPD_COLSUM=ldg selects the register-staged LDG kernel (A/B measurement)
+  const char* env = std::getenv("FCPD_COLSUM");
+  p.bulk = !(env && std::string(env) == "ldg");
+  int64_t slots = 0;
+  if (p.bulk) {
+    static bool attr = false;
+    if (!attr) {
+      FCPD_CUDA(cudaFuncSetAttribute(colsum_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kBulkSmem));
+      attr = true;
+    }
+    slots = static_cast<int64_t>(sm_count) * kBulkCtasPerSm;
+  } else {
+    int occ = 0;
+    FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, colsum_kernel, kColsumThreads, 0));
+    slots = static_cast<int64_t>(sm_count) * std::max(occ, 1);
+  }
+  p.grid = static_cast<int>(std::max<int64_t>(1, min64(slots, p.units)));
   const int64_t per = (p.units + p.grid - 1) / p.grid;
   p.kmax = static_cast<int>((per + rows - 1) / rows + 1);
   return p;
@@ -272,15 +502,19 @@ ColsumPlan make_colsum_plan(int64_t rows, int64_t cols, int sm_count) {
 void launch_colsum(const ColsumPlan& p, const float* A, int64_t lda, const float4* v,
                    double* part, const IterState* st, uint64_t* stamps, int stamp_slot,
                    cudaStream_t stream) {
-  colsum_kernel<<<p.grid, kColsumThreads, 0, stream>>>(A, lda, v, geom(p), part, st, stamps,
-                                                       stamp_slot);
+  if (p.bulk)
+    colsum_bulk_kernel<<<p.grid, kBulkThreads, kBulkSmem, stream>>>(A, lda, v, geom(p), part, st,
+                                                                     stamps, stamp_slot);
+  else
+    colsum_kernel<<<p.grid, kColsumThreads, 0, stream>>>(A, lda, v, geom(p), part, st, stamps,
+                                                         stamp_slot);
   FCPD_LAUNCH_CHECK();
 }
 
 void launch_zreduce(const ColsumPlan& p, const double* part, const double* lam,
                     const double* lam_num, double lambda_reg, double* coef, float4* g4,
                     IterState* st, cudaStream_t stream) {
-  zreduce_filter_kernel<<<ceil_div(p.cols, 256), 256, 0, stream>>>(
+  zreduce_filter_kernel<<<ceil_div(p.cols * kSkLanes, 256), 256, 0, stream>>>(
       part, geom(p), p.cols, lam, lam_num, lambda_reg, coef, g4, st);
   FCPD_LAUNCH_CHECK();
 }
@@ -291,7 +525,7 @@ void launch_transform_sigma(const ColsumPlan& p, const double* part, const doubl
                             int d, int early_stop, double* trace, IterState* st,
                             uint64_t* stamps, cudaStream_t stream) {
   const int64_t m = p.cols;
-  const int nb = ceil_div(m, 256);
+  const int nb = ceil_div(m * kSkLanes, 256);
   transform_sigma_kernel<<<nb, 256, 0, stream>>>(part, geom(p), m, x0, xt64, xt_prev, xt4,
                                                  ptilde_y, var, sig_part, st, stamps);
   FCPD_LAUNCH_CHECK();

@@ -21,6 +21,7 @@ struct ColsumPlan {
   int64_t units = 0;
   int grid = 0;
   int kmax = 0;
+  bool bulk = true;  // cp.async.bulk ring (default) or register-staged LDG
   size_t part_doubles() const {
     return static_cast<size_t>(grid) * kmax * 3 * kColsPerBlock;
   }
