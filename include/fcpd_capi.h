@@ -153,6 +153,14 @@ FCPD_API int fcpd_posterior_dense(fcpd_ctx* ctx, const double* xt, int64_t m, co
 FCPD_API int fcpd_build_basis(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d, double beta,
                      int64_t rank, double* u, double* lambda, double* lambda_raw);
 
+/* Top-K eigenpairs of Φ without forming it (configs 2–4): randomized block
+ * subspace iteration with on-the-fly fp64 Φ·V products + Rayleigh–Ritz,
+ * `iterations` power steps (0 → default 4).  Same outputs and clamp as
+ * fcpd_build_basis. */
+FCPD_API int fcpd_build_basis_topk(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d,
+                                   double beta, int64_t rank, int32_t iterations, double* u,
+                                   double* lambda, double* lambda_raw);
+
 /* build_gram — kernel.hpp:31-47 — M×M column-major fp64. */
 FCPD_API int fcpd_build_gram(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d, double beta,
                     double* phi);

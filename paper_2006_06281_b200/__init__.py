@@ -143,6 +143,7 @@ def lib():
                                                PI64, PI64]),
             "fcpd_build_basis": (C.c_int, [vp, P, I64, I32, D, I64, P, P, P]),
             "fcpd_build_gram": (C.c_int, [vp, P, I64, I32, D, P]),
+            "fcpd_build_basis_topk": (C.c_int, [vp, P, I64, I32, D, I64, I32, P, P, P]),
             "fcpd_solve_fast_lowrank": (C.c_int, [vp, P, P, I64, I64, D, D, P, I32, P]),
             "fcpd_apply_transform_lowrank": (C.c_int, [vp, P, I64, I32, P, P, I64, P, P]),
         }
@@ -361,6 +362,16 @@ class Context:
         lam, raw = np.zeros(rank), np.zeros(rank)
         self._check(lib().fcpd_build_basis(self._h, _p(x), m, d, beta, int(rank), _p(u),
                                            _p(lam), _p(raw)))
+        return u, lam, raw
+
+    def build_basis_topk(self, x, beta: float, rank: int, iterations: int = 0):
+        """Top-K eigenpairs of Φ without forming it (configs 2–4 setup)."""
+        x = _colmajor(x)
+        m, d = x.shape
+        u = np.zeros((m, rank), order="F")
+        lam, raw = np.zeros(rank), np.zeros(rank)
+        self._check(lib().fcpd_build_basis_topk(self._h, _p(x), m, d, beta, int(rank),
+                                                int(iterations), _p(u), _p(lam), _p(raw)))
         return u, lam, raw
 
     def solve_fast_lowrank(self, u, lam, lambda_reg: float, sigma2: float, residual):

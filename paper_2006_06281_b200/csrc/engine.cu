@@ -207,6 +207,7 @@ struct fcpd_ctx {
   int sm_count = 148;
   cudaStream_t stream = nullptr;
   cusolverDnHandle_t solver = nullptr;
+  cublasHandle_t blas = nullptr;
   std::string err;
   fcpd::Basis basis;
   fcpd::Session sess;
@@ -270,6 +271,10 @@ int64_t lowrank_rank(double fraction, int64_t m) {  // solvers.hpp:46-54
   return std::max<int64_t>(1, std::min<int64_t>(k, m));
 }
 
+constexpr int64_t kDenseEigLimit = 46000;          // M×M fp64 + syevd workspace fit
+constexpr int64_t kDenseEigLimitLowrank = 16384;   // above: on-the-fly top-K solver
+constexpr int kTopkIterations = 4;
+
 void ensure_basis(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa) {
   const bool lowrank = s.cfg.variant == FCPD_VARIANT_FAST_LOWRANK;
   const int64_t rank = lowrank ? lowrank_rank(s.cfg.rank_fraction, s.m) : s.m;
@@ -287,10 +292,31 @@ void ensure_basis(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa) {
   }
   s.basis_reused = false;
   b.release();
-  if (s.m > 46000)
+  // Low rank beyond the dense limit: top-K eigenpairs from on-the-fly Φ·V
+  // products (topk.cu); Φ is never formed.  Small problems keep the
+  // reference's full eigensolve + truncation exactly.
+  // FCPD_TOPK_MIN_M overrides the switch-over point (tests force the top-K
+  // path at small M to compare it with the dense solver)
+  int64_t topk_min = kDenseEigLimitLowrank;
+  if (const char* e = std::getenv("FCPD_TOPK_MIN_M")) topk_min = std::atoll(e);
+  if (lowrank && s.m > topk_min) {
+    const auto t1 = Clock::now();
+    topk_eigensolve(ctx->solver, ctx->blas, s.x0.p, s.m, s.d, s.cfg.beta, rank,
+                    kTopkIterations, s.cfg.seed, b, ctx->stream);
+    upload_lambda(b, false, ctx->stream);
+    s.t_gram = 0.0;
+    s.t_eig = since(t1);
+    b.key_hash = h;
+    b.key_beta = s.cfg.beta;
+    b.key_variant = s.cfg.variant;
+    b.t_gram = s.t_gram;
+    b.t_eig = s.t_eig;
+    return;
+  }
+  if (s.m > kDenseEigLimit)
     throw Failure(FCPD_ERR_PARAMETER,
-                  "eigendecompose: dense device eigensolver limited to M <= 46000 "
-                  "(top-K on-the-fly setup not built yet)");
+                  "eigendecompose: the full-rank variant needs a dense M×M eigensolve; "
+                  "M > " + std::to_string(kDenseEigLimit) + " — use fast_lowrank");
   double* phi = nullptr;
   FCPD_CUDA(cudaMalloc(&phi, sizeof(double) * s.m * s.m));
   try {
@@ -672,6 +698,8 @@ int fcpd_create(fcpd_ctx** out, int device) {
     FCPD_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     if (cusolverDnCreate(&ctx->solver) != CUSOLVER_STATUS_SUCCESS)
       throw Failure(FCPD_ERR_CUDA, "cusolverDnCreate failed");
+    if (cublasCreate(&ctx->blas) != CUBLAS_STATUS_SUCCESS)
+      throw Failure(FCPD_ERR_CUDA, "cublasCreate failed");
   } catch (const Failure& e) {
     static thread_local std::string last;
     last = e.what();
@@ -688,6 +716,7 @@ void fcpd_destroy(fcpd_ctx* ctx) {
   ctx->sess.release();
   ctx->basis.release();
   if (ctx->solver) cusolverDnDestroy(ctx->solver);
+  if (ctx->blas) cublasDestroy(ctx->blas);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -887,6 +916,26 @@ int fcpd_build_basis(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d, doubl
     b.release();
     xd.release();
     g.release();
+  });
+}
+
+int fcpd_build_basis_topk(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d, double beta,
+                          int64_t rank, int32_t iterations, double* u, double* lambda,
+                          double* lambda_raw) {
+  return guarded(ctx, [&] {
+    if (m <= 0) throw Failure(FCPD_ERR_PARAMETER, "eigendecompose: empty point set");
+    if (d < 1 || d > 3) throw Failure(FCPD_ERR_DIMENSION, "eigendecompose: the B200 path supports D <= 3");
+    DevBuf<double> xd;
+    xd.ensure(3 * static_cast<size_t>(m));
+    FCPD_CUDA(cudaMemsetAsync(xd.p, 0, sizeof(double) * 3 * m, ctx->stream));
+    FCPD_CUDA(cudaMemcpyAsync(xd.p, x, sizeof(double) * d * m, cudaMemcpyHostToDevice, ctx->stream));
+    Basis b;
+    topk_eigensolve(ctx->solver, ctx->blas, xd.p, m, d, beta, rank,
+                    iterations > 0 ? iterations : 4, 0, b, ctx->stream, u);
+    if (lambda) std::copy(b.lam_host.begin(), b.lam_host.end(), lambda);
+    if (lambda_raw) std::copy(b.lam_raw_host.begin(), b.lam_raw_host.end(), lambda_raw);
+    b.release();
+    xd.release();
   });
 }
 

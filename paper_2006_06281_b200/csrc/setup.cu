@@ -205,6 +205,15 @@ void dense_eigensolve(cusolverDnHandle_t h, double* phi, int64_t m, int64_t rank
   cusolverDnDestroyParams(params);
 }
 
+void pack_basis_from(Basis& b, const double* u_dev, int64_t m, int64_t k, int reverse,
+                     const std::vector<double>& lam_raw, cudaStream_t stream) {
+  alloc_basis(b, m, k);
+  pack_basis(b, u_dev, m, k, reverse, stream);
+  b.lam_raw_host = lam_raw;
+  clamp_lambda(b);
+  FCPD_CUDA(cudaStreamSynchronize(stream));
+}
+
 void basis_from_host(Basis& b, const double* u_host, const double* lam_host, int64_t m,
                      int64_t k, cudaStream_t stream) {
   double* v = nullptr;

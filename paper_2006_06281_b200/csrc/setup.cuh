@@ -1,6 +1,7 @@
 // setup.cuh — spectral basis setup interface (see setup.cu).
 #pragma once
 
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 #include <stdint.h>
@@ -35,5 +36,15 @@ void basis_from_host(Basis& b, const double* u_host, const double* lam_host, int
                      int64_t k, cudaStream_t stream);
 void clamp_lambda(Basis& b);
 void upload_lambda(Basis& b, bool full_rank, cudaStream_t stream);
+// Pack device eigenvectors u (M×k col-major fp64) + λ_raw (descending) into b.
+void pack_basis_from(Basis& b, const double* u_dev, int64_t m, int64_t k, int reverse,
+                     const std::vector<double>& lam_raw, cudaStream_t stream);
+
+// topk.cu — on-the-fly Gram products and the randomized block eigensolver.
+void gram_matmul(const double* x, int64_t m, int d, double beta, const double* v, int64_t b,
+                 double* y, cudaStream_t stream);
+void topk_eigensolve(cusolverDnHandle_t solver, cublasHandle_t blas, const double* x_dev,
+                     int64_t m, int d, double beta, int64_t rank, int iterations, uint64_t seed,
+                     Basis& b_out, cudaStream_t stream, double* u_host_out = nullptr);
 
 }  // namespace fcpd
