@@ -126,10 +126,8 @@ def run_reference(args, world, rank):
         return
     from paper_2006_06281_b200 import datagen
     x, y, w = datagen.generate(args.workload)
-    warm = 1 if args.warmup > 0 else 0
-    if warm:
-        cpu_sample(x, y, w, 1)
-    # bounded sample: at most args.steps iterations, capped by a time budget
+    # one untimed warm-up iteration (also sizes the sample), then a bounded
+    # sample: at most args.steps iterations, capped by a time budget
     t_est = cpu_sample(x, y, w, 1)[2]
     k = max(1, min(args.steps, int(args.cpu_budget_s / max(t_est, 1e-9))))
     rate, threads, secs = cpu_sample(x, y, w, k)
