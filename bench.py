@@ -91,6 +91,24 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+class Watchdog:
+    """Kill the process if a collective hangs (a stuck rank must fail, not hang)."""
+
+    def __init__(self, seconds: float):
+        self._t = threading.Timer(seconds, self._fire)
+        self._t.daemon = True
+        self._t.start()
+
+    @staticmethod
+    def _fire():
+        sys.stderr.write("bench.py: watchdog expired, aborting\n")
+        sys.stderr.flush()
+        os._exit(3)
+
+    def cancel(self):
+        self._t.cancel()
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -162,11 +180,23 @@ def run_ours(args, world, rank, local):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    x, y, w = datagen.generate(args.workload)
-    prof_iters = 3
+    x, y_full, w = datagen.generate(args.workload)
+    sharded = world > 1 and not args.replicas
+    prof_iters = 0 if sharded else 3
     total = args.warmup + args.steps + prof_iters
     cfg = datagen.config_for(w, iterations=total)
-    ctx = fcpd.Context(local)
+    if sharded:
+        # scene points sharded over ranks; the engine's own NCCL
+        # communicator carries the per-iteration reductions
+        obj = [fcpd.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = fcpd.Context.distributed(local, rank, world, obj[0])
+        n = y_full.shape[0]
+        y = y_full[rank * n // world:(rank + 1) * n // world]
+    else:
+        ctx = fcpd.Context(local)
+        y = y_full
+    watchdog = Watchdog(args.watchdog_s)
     t0 = time.perf_counter()
     ctx.session_begin(x, y, cfg)
     setup_s = time.perf_counter() - t0
@@ -191,7 +221,7 @@ def run_ours(args, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
-    phases = ctx.session_profile(prof_iters)
+    phases = ctx.session_profile(prof_iters) if prof_iters else None
     state = ctx.session_read(with_points=False)
     sigma_last = float(state["sigma2_trace"][-1])
 
@@ -211,33 +241,47 @@ def run_ours(args, world, rank, local):
     if world > 1 and e2e_calls > 0:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_rate = world * e2e_calls * e2e_iters / float(t.item())
+        e2e_s = float(t.item())
+        e2e_rate = (1 if sharded else world) * e2e_calls * e2e_iters / e2e_s
+    watchdog.cancel()
 
     if rank == 0:
         peaks, peak_kind = load_peaks()
-        m, n = x.shape[0], y.shape[0]
+        m, n = x.shape[0], y_full.shape[0]
         k = m if w.variant == "fast" else fcpd.lowrank_rank(w.rank_fraction, m)
         kpad, mpad = (k + 3) // 4 * 4, (m + 3) // 4 * 4
-        value = world * args.steps / (ms / 1e3)
-        # dominant HBM kernel: the two basis streams (Qᵀ·R over Q, Q·g over Qᵀ)
+        # sharded: every iteration is the whole problem (strong scaling);
+        # replicas: each rank runs its own copy (weak scaling)
+        value = (1 if sharded or world == 1 else world) * args.steps / (ms / 1e3)
         q_bytes = 4.0 * (m * kpad + k * mpad)
-        q_ms = phases["qt_r_stream"] + phases["q_g_stream"]
-        achieved = q_bytes / (q_ms / 1e3) / 1e9
-        e_ms = phases["estep_pass1"] + phases["estep_pass2"]
         clocks = clk.summary()
         f_mhz = clocks["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)
         mufu_bound = 148 * f_mhz * 1e6 * 16 / 2  # 2 ex2 per pair, 16 ex2/clk/SM
-        pairs_s = m * n / (e_ms / 1e3)
-        traffic = None
-        prof_json = os.path.join(ROOT, "profiles", "ncu_summary.json")
-        if os.path.exists(prof_json):
-            try:
-                traffic = json.load(open(prof_json)).get("colsum_dram_bytes_per_launch")
-            except Exception:
-                traffic = None
+        roofline = estep_roof = None
+        pairs_s = None
+        if phases:
+            # dominant HBM kernel: the two basis streams (Qᵀ·R over Q, Q·g over Qᵀ)
+            q_ms = phases["qt_r_stream"] + phases["q_g_stream"]
+            achieved = q_bytes / (q_ms / 1e3) / 1e9
+            e_ms = phases["estep_pass1"] + phases["estep_pass2"]
+            pairs_s = m * n / (e_ms / 1e3)
+            traffic = None
+            prof_json = os.path.join(ROOT, "profiles", "ncu_summary.json")
+            if os.path.exists(prof_json):
+                try:
+                    traffic = json.load(open(prof_json)).get("colsum_dram_bytes_per_launch")
+                except Exception:
+                    traffic = None
+            roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                        "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                        "kernel": "colsum_bulk (Qᵀ·R and Q·g basis streams, cp.async.bulk ring)",
+                        "peak_source": peak_kind}
+            estep_roof = {"bound": "mufu", "achieved": pairs_s / 1e9, "peak": mufu_bound / 1e9,
+                          "unit": "Gpairs/s", "frac": pairs_s / mufu_bound,
+                          "note": "2 ex2/pair, 16 ex2/clk/SM at the sampled SM clock"}
         cpu = None
         if world == 1 and not args.no_cpu:
-            rate, threads, secs = cpu_sample(x, y, w, args.cpu_iters)
+            rate, threads, secs = cpu_sample(x, y_full, w, args.cpu_iters)
             cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                    "sample": f"{args.cpu_iters} dense fp64 EM iteration(s) of {args.workload} "
                              f"via the oracle restatement, identity stand-in basis, "
@@ -245,25 +289,21 @@ def run_ours(args, world, rank, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+            "vs_baseline": None,
             "dtype": "f32 pair terms + f64 accumulation; f32 basis stream",
             "data": "synthetic (seeded generator, datagen.py)",
             "config": {"workload": f"{args.workload}: {w.description}", "M": m, "N": n, "K": k,
                        "omega": w.omega, "beta": w.beta, "lambda": w.lambda_reg,
                        "variant": w.variant,
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "parallelism": (f"scene-sharded x{world} (NCCL)" if sharded else
+                                       f"replicas x{world}" if world > 1 else "single"),
                        "l2": "inputs larger than L2 (Q+Qt = %.2f GB fp32)" % (q_bytes / 1e9)},
             "setup_s": setup_s, "sigma2_last": sigma_last,
             "phase_ms": phases,
-            "estep_gpairs_per_s": pairs_s / 1e9,
-            "estep_roofline": {"bound": "mufu", "achieved": pairs_s / 1e9,
-                               "peak": mufu_bound / 1e9, "unit": "Gpairs/s",
-                               "frac": pairs_s / mufu_bound,
-                               "note": "2 ex2/pair, 16 ex2/clk/SM at the sampled SM clock"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
-                         "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                         "traffic": traffic, "kernel": "colsum (Qᵀ·R and Q·g basis streams)",
-                         "peak_source": peak_kind},
+            "estep_gpairs_per_s": pairs_s / 1e9 if pairs_s else None,
+            "estep_roofline": estep_roof,
+            "roofline": roofline,
             "clocks": clocks,
             "gpu_launches": ctx.kernels_per_iteration * args.steps,
             "e2e": {"value": e2e_rate, "unit": UNIT,
@@ -292,6 +332,9 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--cpu-budget-s", type=float, default=90.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent replicas instead of the scene-sharded NCCL path")
+    ap.add_argument("--watchdog-s", type=float, default=900.0)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: ≥ 3 warm-up steps

@@ -104,6 +104,18 @@ FCPD_API void fcpd_destroy(fcpd_ctx* ctx);
 FCPD_API const char* fcpd_last_error(const fcpd_ctx* ctx);
 FCPD_API const char* fcpd_version(void);
 
+/* Multi-GPU (one process per GPU): rank 0 calls fcpd_nccl_unique_id and
+ * shares the 128 bytes with the other ranks (e.g. torch.distributed); each
+ * rank then creates its context with fcpd_create_dist.  In such a context
+ * fcpd_register / fcpd_session_begin take the FULL model x and this rank's
+ * SHARD of the scene y (n = local count); the scene is reduced over ranks,
+ * the model rows and the basis are row-sharded, and every
+ * rank receives the full result.  Correspondence output is single-GPU only. */
+FCPD_API int fcpd_nccl_unique_id(uint8_t* out128);
+FCPD_API int fcpd_create_dist(fcpd_ctx** out, int device, int rank, int world,
+                              const uint8_t* id128);
+FCPD_API int fcpd_world(const fcpd_ctx* ctx, int32_t* rank, int32_t* world);
+
 /* register_pointsets — registration.hpp:79-175.  x: M×D model, y: N×D scene.
  * The spectral basis is cached in the context keyed by (normalised X, β,
  * rank); a repeated call on the same model reuses it (the paper's

@@ -144,6 +144,10 @@ def lib():
             "fcpd_build_basis": (C.c_int, [vp, P, I64, I32, D, I64, P, P, P]),
             "fcpd_build_gram": (C.c_int, [vp, P, I64, I32, D, P]),
             "fcpd_build_basis_topk": (C.c_int, [vp, P, I64, I32, D, I64, I32, P, P, P]),
+            "fcpd_nccl_unique_id": (C.c_int, [C.c_char_p]),
+            "fcpd_create_dist": (C.c_int, [C.POINTER(vp), C.c_int, C.c_int, C.c_int,
+                                           C.c_char_p]),
+            "fcpd_world": (C.c_int, [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
             "fcpd_solve_fast_lowrank": (C.c_int, [vp, P, P, I64, I64, D, D, P, I32, P]),
             "fcpd_apply_transform_lowrank": (C.c_int, [vp, P, I64, I32, P, P, I64, P, P]),
         }
@@ -218,12 +222,41 @@ class RegistrationResult:  # registration.hpp:48-56
 
 
 # ------------------------------------------------------------------ context
-class Context:
-    """One CUDA device: stream, cuSOLVER handle, cached basis, graphs."""
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id for fcpd_create_dist (rank 0 makes it, all ranks share it)."""
+    buf = C.create_string_buffer(128)
+    if lib().fcpd_nccl_unique_id(buf) != 0:
+        raise CudaError("ncclGetUniqueId failed")
+    return buf.raw
 
-    def __init__(self, device: int = 0):
+
+class Context:
+    """One CUDA device: stream, cuSOLVER handle, cached basis, graphs.
+
+    ``Context.distributed(device, rank, world, uid)`` joins a multi-GPU
+    group (one process per GPU): register/session calls then take the full
+    model and this rank's scene shard (see include/fcpd_capi.h)."""
+
+    def __init__(self, device: int = 0, *, _dist=None):
         self._h = C.c_void_p()
-        self._check(lib().fcpd_create(C.byref(self._h), int(device)))
+        if _dist is None:
+            self._check(lib().fcpd_create(C.byref(self._h), int(device)))
+        else:
+            rank, world, uid = _dist
+            rc = lib().fcpd_create_dist(C.byref(self._h), int(device), int(rank), int(world),
+                                        bytes(uid))
+            if rc != 0:
+                raise _CODES.get(rc, Error)(f"fcpd_create_dist failed (code {rc})")
+
+    @classmethod
+    def distributed(cls, device: int, rank: int, world: int, uid: bytes) -> "Context":
+        return cls(device, _dist=(rank, world, uid))
+
+    @property
+    def world(self):
+        r, w = C.c_int32(), C.c_int32()
+        lib().fcpd_world(self._h, C.byref(r), C.byref(w))
+        return r.value, w.value
 
     def close(self):
         if self._h:

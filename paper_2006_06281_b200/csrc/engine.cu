@@ -18,9 +18,18 @@
 #include <vector>
 
 #include "common.cuh"
+#include "dist.cuh"
 #include "estep.cuh"
 #include "mstep.cuh"
+#include "nccl_dyn.cuh"
 #include "setup.cuh"
+
+#define FCPD_NCCL(call)                                                               \
+  do {                                                                                \
+    ncclResult_t r_ = (call);                                                         \
+    if (r_ != ncclSuccess)                                                            \
+      throw ::fcpd::Failure(FCPD_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
 
 namespace fcpd {
 
@@ -184,6 +193,16 @@ struct Session {
   ColsumPlan zp, vp;
   cudaGraphExec_t graph = nullptr;
 
+  // ---- distributed (NCCL) sharding: scene N split over ranks, model rows
+  // [m0, m0+mr) owned by this rank (m_pad = world·mr ≥ M).  In this mode
+  // x0/xt64/xt_prev/ptilde_y/var/log2p1/degenerate/resid4 hold OWN rows
+  // (stride mr); xt4 holds all M_pad rows; y4b the local scene shard.
+  bool dist = false;
+  int64_t n_global = 0, m_pad = 0, mr = 0, m0 = 0, m_valid_own = 0, mr4 = 0;
+  DevBuf<double> rowsum_all, rowsum_own, fsum_all, fsum_own, zfull, sig_local, stage;
+  DevBuf<int32_t> mask_own, mask_all;
+  DevBuf<float> fmax_all, qt_own;
+
   void release_graph() {
     if (graph) cudaGraphExecDestroy(graph);
     graph = nullptr;
@@ -197,6 +216,12 @@ struct Session {
     for (auto* b : {&col_flags, &row_flags, &flags_count, &degenerate}) b->release();
     stamps.release();
     st.release();
+    for (auto* b : {&rowsum_all, &rowsum_own, &fsum_all, &fsum_own, &zfull, &sig_local, &stage})
+      b->release();
+    mask_own.release();
+    mask_all.release();
+    fmax_all.release();
+    qt_own.release();
   }
 };
 
@@ -208,6 +233,8 @@ struct fcpd_ctx {
   cudaStream_t stream = nullptr;
   cusolverDnHandle_t solver = nullptr;
   cublasHandle_t blas = nullptr;
+  ncclComm_t comm = nullptr;  // set by fcpd_create_dist: scene-sharded EM over NCCL
+  int rank = 0, world = 1;
   std::string err;
   fcpd::Basis basis;
   fcpd::Session sess;
@@ -484,12 +511,21 @@ double init_sigma2_host(const std::vector<double>& x, int64_t m, const std::vect
   return std::max((md * fy + nd * fx - 2.0 * dot) / (static_cast<double>(d) * md * nd), 0.0);
 }
 
+void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n,
+                        int d, const fcpd_config& cfg);
+void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall);
+
 void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n, int d,
                    const fcpd_config& cfg) {
+  if (ctx->comm) {
+    session_begin_dist(ctx, x, m, y, n, d, cfg);
+    return;
+  }
   validate_register(x, m, y, n, d, cfg);
   const auto t0 = Clock::now();
   Session& s = ctx->sess;
   s.ready = false;
+  s.dist = false;
   s.h2d = s.d2h = 0;
   s.m = m;
   s.n = n;
@@ -569,6 +605,10 @@ void session_run(fcpd_ctx* ctx, int iters) {
 }
 
 void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
+  if (ctx->sess.dist) {
+    session_read_dist(ctx, out, wall);
+    return;
+  }
   Session& s = ctx->sess;
   Basis& b = ctx->basis;
   cudaStream_t str = ctx->stream;
@@ -660,6 +700,336 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
   out->d2h_bytes = s.d2h;
 }
 
+// ============================================================ distributed
+// One process per GPU; ctx->comm spans the ranks.  See dist.cu for the
+// sharding.  `y` passed to the dist session is this rank's scene shard;
+// `x` is the full model on every rank.
+
+void host_allreduce(fcpd_ctx* ctx, double* vals, int count, ncclRedOp_t op) {
+  DevBuf<double> d;
+  d.ensure(count);
+  FCPD_CUDA(cudaMemcpyAsync(d.p, vals, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
+  FCPD_NCCL(ncclAllReduce(d.p, d.p, count, ncclDouble, op, ctx->comm, ctx->stream));
+  FCPD_CUDA(cudaMemcpyAsync(vals, d.p, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
+  FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
+  d.release();
+}
+
+void enqueue_iteration_dist(fcpd_ctx* ctx, Session& s) {
+  Basis& b = ctx->basis;
+  IterState* st = s.st.p;
+  cudaStream_t str = ctx->stream;
+  ncclComm_t comm = ctx->comm;
+  const int64_t m = s.m, nl = s.n;
+  EStepBuffers eb{};
+  eb.xt4 = s.xt4.p;
+  eb.y4b = s.y4b.p;
+  eb.b2 = s.b2.p;
+  eb.col_part = s.col_part.p;
+  eb.row_part = s.row_part.p;
+  eb.col_flags = s.col_flags.p;
+  eb.row_flags = s.row_flags.p;
+  eb.flags_count = s.flags_count.p;
+  eb.ystats = s.ystats;
+  launch_estep_prologue(st, m, s.n_global, s.d, s.cfg.omega, s.flags_count.p, s.stamps.p, str);
+  launch_estep_pass1(s.ep, eb, m, nl, st, str);  // column-local: no communication
+  launch_estep_pass2_partials(s.ep, eb, m, nl, st, str);
+  launch_row_split_sum(s.row_part.p, s.ep.row_splits, m, s.m_pad, s.rowsum_all.p, st, str);
+  FCPD_NCCL(ncclReduceScatter(s.rowsum_all.p, s.rowsum_own.p, s.mr * 5, ncclDouble, ncclSum,
+                              comm, str));
+  const DistRowOut o{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p, s.resid4.p, s.x0.p};
+  launch_row_finalize_own(s.rowsum_own.p, s.mr, s.m_valid_own, s.n_global, s.xt64.p, o, s.ystats,
+                          s.mask_own.p, st, str);
+  // exact fallback for rows of tiny global mass (max + shifted sums)
+  FCPD_NCCL(ncclAllGather(s.mask_own.p, s.mask_all.p, s.mr, ncclInt32, comm, str));
+  launch_fallback_max(s.mask_all.p, s.m_pad, s.xt4.p, s.y4b.p, nl, s.fmax_all.p, st, str);
+  FCPD_NCCL(ncclAllReduce(s.fmax_all.p, s.fmax_all.p, s.m_pad, ncclFloat, ncclMax, comm, str));
+  launch_fallback_sum(s.mask_all.p, s.m_pad, s.fmax_all.p, s.xt4.p, s.y4b.p, nl, s.fsum_all.p, st,
+                      str);
+  FCPD_NCCL(ncclReduceScatter(s.fsum_all.p, s.fsum_own.p, s.mr * 5, ncclDouble, ncclSum, comm,
+                              str));
+  launch_fallback_finalize_own(s.fsum_own.p, s.fmax_all.p + s.m0, s.mask_own.p, s.mr, s.xt64.p, o,
+                               s.ystats, st, str);
+  // M-step on the own row shard of the basis
+  launch_colsum(s.zp, b.q + s.m0 * b.kpad, b.kpad, s.resid4.p, s.zpart.p, st, s.stamps.p, 1, str);
+  launch_zsum(s.zp, s.zpart.p, s.zfull.p, st, str);
+  FCPD_NCCL(ncclAllReduce(s.zfull.p, s.zfull.p, 3 * b.k, ncclDouble, ncclSum, comm, str));
+  launch_zfilter(s.zfull.p, b.k, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.coef.p, s.g4.p, st, str);
+  launch_colsum(s.vp, s.qt_own.p, s.mr4, s.g4.p, s.vpart.p, st, nullptr, 0, str);
+  const int nb = launch_transform_rows(s.vp, s.vpart.p, s.m_valid_own, s.x0.p, s.xt64.p,
+                                       s.xt_prev.p, s.xt4.p + s.m0, s.ptilde_y.p, s.var.p,
+                                       s.sig_part.p, st, s.stamps.p, str);
+  launch_sigma_local_sum(s.sig_part.p, nb, s.sig_local.p, st, str);
+  FCPD_NCCL(ncclAllReduce(s.sig_local.p, s.sig_local.p, 1, ncclDouble, ncclSum, comm, str));
+  launch_sigma_final(s.sig_local.p, 1, m, s.d, s.cfg.early_stop, s.trace.p, st, s.stamps.p, str);
+  FCPD_NCCL(ncclAllGather(s.xt4.p + s.m0, s.xt4.p, s.mr * 4, ncclFloat, comm, str));
+}
+
+void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n,
+                        int d, const fcpd_config& cfg) {
+  validate_register(x, m, y, n, d, cfg);
+  const auto t0 = Clock::now();
+  Session& s = ctx->sess;
+  cudaStream_t str = ctx->stream;
+  s.ready = false;
+  s.dist = true;
+  s.h2d = s.d2h = 0;
+  s.m = m;
+  s.n = n;
+  s.d = d;
+  s.cfg = cfg;
+  const int G = ctx->world, R = ctx->rank;
+  if (m < G) throw Failure(FCPD_ERR_PARAMETER, "register: fewer model points than ranks");
+  // global scene size and normalize_pair statistics (pointset.hpp:124-148)
+  double red[5] = {static_cast<double>(n), 0, 0, 0, 0};
+  for (int c = 0; c < d; ++c)
+    for (int64_t i = 0; i < n; ++i) red[1 + c] += y[c * n + i];
+  host_allreduce(ctx, red, 4, ncclSum);
+  s.n_global = static_cast<int64_t>(red[0]);
+  std::vector<double> xs(3 * m, 0.0), ys(3 * n, 0.0);
+  s.center[0] = s.center[1] = s.center[2] = 0.0;
+  s.scale = 1.0;
+  if (cfg.normalize) {
+    const double total = static_cast<double>(m + s.n_global);
+    for (int c = 0; c < d; ++c) {
+      double sx = 0.0;
+      for (int64_t i = 0; i < m; ++i) sx += x[c * m + i];
+      s.center[c] = (sx + red[1 + c]) / total;
+    }
+    double sc = 0.0;
+    for (int c = 0; c < d; ++c) {
+      for (int64_t i = 0; i < m; ++i) sc = std::max(sc, std::fabs(x[c * m + i] - s.center[c]));
+      for (int64_t i = 0; i < n; ++i) sc = std::max(sc, std::fabs(y[c * n + i] - s.center[c]));
+    }
+    host_allreduce(ctx, &sc, 1, ncclMax);
+    if (sc <= 0.0) sc = 1.0;
+    s.scale = sc;
+    for (int c = 0; c < d; ++c) {
+      for (int64_t i = 0; i < m; ++i) xs[c * m + i] = (x[c * m + i] - s.center[c]) / sc;
+      for (int64_t i = 0; i < n; ++i) ys[c * n + i] = (y[c * n + i] - s.center[c]) / sc;
+    }
+  } else {
+    for (int c = 0; c < d; ++c) {
+      std::memcpy(&xs[c * m], x + c * m, sizeof(double) * m);
+      std::memcpy(&ys[c * n], y + c * n, sizeof(double) * n);
+    }
+  }
+  // global scene statistics of the normalised scene
+  double ystat[4] = {0, 0, 0, 0};
+  for (int c = 0; c < 3; ++c)
+    for (int64_t i = 0; i < n; ++i) ystat[c] += ys[c * n + i];
+  for (int64_t i = 0; i < n; ++i)
+    ystat[3] += ys[i] * ys[i] + ys[n + i] * ys[n + i] + ys[2 * n + i] * ys[2 * n + i];
+  host_allreduce(ctx, ystat, 4, ncclSum);
+  const double ng = static_cast<double>(s.n_global);
+  for (int c = 0; c < 3; ++c) s.ystats.mean[c] = ystat[c] / ng;
+  s.ystats.sq_mean = ystat[3] / ng;
+  // init_sigma2 (registration.hpp:59-69) from the global statistics
+  {
+    double fx = 0.0, dot = 0.0;
+    for (int c = 0; c < d; ++c) {
+      double sx = 0.0;
+      for (int64_t i = 0; i < m; ++i) {
+        fx += xs[c * m + i] * xs[c * m + i];
+        sx += xs[c * m + i];
+      }
+      dot += sx * ystat[c];
+    }
+    const double md = static_cast<double>(m);
+    s.sigma2_initial =
+        std::max((md * ystat[3] + ng * fx - 2.0 * dot) / (static_cast<double>(d) * md * ng), 0.0);
+  }
+  // spectral basis (computed redundantly per rank; each keeps its row shard)
+  s.x0.ensure(3 * m);
+  FCPD_CUDA(cudaMemcpyAsync(s.x0.p, xs.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, str));
+  ensure_basis(ctx, s, xs);
+  Basis& b = ctx->basis;
+  // shard geometry
+  s.mr = (m + G - 1) / G;
+  s.m_pad = s.mr * G;
+  s.m0 = s.mr * R;
+  s.m_valid_own = std::max<int64_t>(0, std::min<int64_t>(s.mr, m - s.m0));
+  if (s.m_valid_own < 1) throw Failure(FCPD_ERR_PARAMETER, "register: empty model shard");
+  s.mr4 = (s.mr + 3) / 4 * 4;
+  const int64_t mr = s.mr;
+  // own-row SoA arrays (stride mr)
+  std::vector<double> own(3 * mr, 0.0);
+  for (int c = 0; c < 3; ++c)
+    for (int64_t i = 0; i < s.m_valid_own; ++i) own[c * mr + i] = xs[c * m + s.m0 + i];
+  s.release_graph();
+  s.x0.ensure(3 * mr);
+  s.xt64.ensure(3 * mr);
+  s.xt_prev.ensure(3 * mr);
+  s.ptilde_y.ensure(3 * mr);
+  s.var.ensure(mr);
+  s.log2p1.ensure(mr);
+  s.degenerate.ensure(mr);
+  s.resid4.ensure(mr);
+  FCPD_CUDA(cudaMemcpyAsync(s.x0.p, own.data(), sizeof(double) * 3 * mr, cudaMemcpyHostToDevice, str));
+  FCPD_CUDA(cudaMemcpyAsync(s.xt64.p, s.x0.p, sizeof(double) * 3 * mr, cudaMemcpyDeviceToDevice, str));
+  FCPD_CUDA(cudaMemcpyAsync(s.xt_prev.p, s.x0.p, sizeof(double) * 3 * mr, cudaMemcpyDeviceToDevice, str));
+  // full model (float4, padded) and local scene
+  std::vector<float4> x4(s.m_pad, make_float4(3.0e18f, 3.0e18f, 3.0e18f, 0.f)), y4(n);
+  for (int64_t i = 0; i < m; ++i)
+    x4[i] = make_float4(static_cast<float>(xs[i]), static_cast<float>(xs[m + i]),
+                        static_cast<float>(xs[2 * m + i]), 0.f);
+  for (int64_t i = 0; i < n; ++i)
+    y4[i] = make_float4(static_cast<float>(ys[i]), static_cast<float>(ys[n + i]),
+                        static_cast<float>(ys[2 * n + i]), 0.f);
+  s.xt4.ensure(s.m_pad);
+  s.y4b.ensure(n);
+  FCPD_CUDA(cudaMemcpyAsync(s.xt4.p, x4.data(), sizeof(float4) * s.m_pad, cudaMemcpyHostToDevice, str));
+  FCPD_CUDA(cudaMemcpyAsync(s.y4b.p, y4.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, str));
+  s.h2d += (sizeof(double) * 3 + sizeof(float4)) * (m + n);
+  // E-step scratch over all M rows / local columns
+  s.ep = make_estep_plan(m, n, ctx->sm_count);
+  s.b2.ensure(n);
+  s.pt1.ensure(n);
+  s.col_part.ensure(static_cast<size_t>(s.ep.col_splits) * n);
+  s.row_part.ensure(static_cast<size_t>(s.ep.row_splits) * 5 * m);
+  s.col_flags.ensure(n);
+  s.row_flags.ensure(m);
+  s.flags_count.ensure(2);
+  s.rowsum_all.ensure(5 * s.m_pad);
+  s.rowsum_own.ensure(5 * mr);
+  s.fsum_all.ensure(5 * s.m_pad);
+  s.fsum_own.ensure(5 * mr);
+  s.mask_own.ensure(mr);
+  s.mask_all.ensure(s.m_pad);
+  s.fmax_all.ensure(s.m_pad);
+  // basis shard: Q rows [m0, m0+m_valid) in place; Qᵀ columns copied compact
+  s.qt_own.ensure(static_cast<size_t>(b.k) * s.mr4);
+  FCPD_CUDA(cudaMemsetAsync(s.qt_own.p, 0, sizeof(float) * b.k * s.mr4, str));
+  const int64_t cols = std::min<int64_t>(mr, b.mpad - s.m0);
+  if (cols > 0)
+    FCPD_CUDA(cudaMemcpy2DAsync(s.qt_own.p, sizeof(float) * s.mr4, b.qt + s.m0,
+                                sizeof(float) * b.mpad, sizeof(float) * cols, b.k,
+                                cudaMemcpyDeviceToDevice, str));
+  s.zp = make_colsum_plan(s.m_valid_own, b.k, ctx->sm_count);
+  s.vp = make_colsum_plan(b.k, mr, ctx->sm_count);
+  s.zpart.ensure(s.zp.part_doubles());
+  s.vpart.ensure(s.vp.part_doubles());
+  s.zfull.ensure(3 * b.k);
+  s.coef.ensure(3 * b.k);
+  s.g4.ensure(b.k);
+  s.sig_part.ensure(ceil_div(mr * 4, 256));
+  s.sig_local.ensure(1);
+  s.st.ensure(1);
+  s.capacity = std::max(cfg.iterations, 1);
+  s.trace.ensure(s.capacity);
+  s.stamps.ensure(4 * static_cast<size_t>(s.capacity));
+  if (cfg.iterations > 0 && !(cfg.omega >= 0.0 && cfg.omega < 1.0))
+    throw Failure(FCPD_ERR_NUMERIC, "register: iteration 0: posterior: omega must lie in [0, 1)");
+  reset_state(ctx, s, s.sigma2_initial);
+  FCPD_CUDA(cudaMemsetAsync(s.coef.p, 0, sizeof(double) * 3 * b.k, str));
+  FCPD_CUDA(cudaStreamSynchronize(str));
+
+  cudaGraph_t g = nullptr;
+  FCPD_CUDA(cudaStreamBeginCapture(str, cudaStreamCaptureModeThreadLocal));
+  try {
+    enqueue_iteration_dist(ctx, s);
+  } catch (...) {
+    cudaStreamEndCapture(str, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  FCPD_CUDA(cudaStreamEndCapture(str, &g));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  FCPD_CUDA(ie);
+  s.graph = exec;
+  s.t_setup_host = since(t0);
+  s.launched = 0;
+  s.ready = true;
+}
+
+// gather the own-row SoA blocks (stride mr) of every rank into a full SoA M×d
+void gather_rows(fcpd_ctx* ctx, Session& s, const double* own, double* out_full, int d) {
+  const int G = ctx->world;
+  s.stage.ensure(static_cast<size_t>(3) * s.mr * G);
+  FCPD_NCCL(ncclAllGather(own, s.stage.p, 3 * s.mr, ncclDouble, ctx->comm, ctx->stream));
+  std::vector<double> h(static_cast<size_t>(3) * s.mr * G);
+  FCPD_CUDA(cudaMemcpyAsync(h.data(), s.stage.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
+  s.d2h += sizeof(double) * 3 * s.mr;
+  for (int r = 0; r < G; ++r)
+    for (int c = 0; c < d; ++c)
+      for (int64_t i = 0; i < s.mr; ++i) {
+        const int64_t row = r * s.mr + i;
+        if (row < s.m) out_full[c * s.m + row] = h[(static_cast<size_t>(r) * 3 + c) * s.mr + i];
+      }
+}
+
+void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall) {
+  Session& s = ctx->sess;
+  Basis& b = ctx->basis;
+  cudaStream_t str = ctx->stream;
+  IterState h{};
+  FCPD_CUDA(cudaMemcpyAsync(&h, s.st.p, sizeof h, cudaMemcpyDeviceToHost, str));
+  FCPD_CUDA(cudaStreamSynchronize(str));
+  if (h.err_code != 0) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%f", h.err_value);
+    const std::string what = h.err_code == kDevSolveDiag
+                                 ? "solve_fast: lambda_i + lambda*sigma2 not positive"
+                                 : std::string("update_sigma2: negative variance ") + buf;
+    throw Failure(FCPD_ERR_NUMERIC, "register: iteration " + std::to_string(h.err_iter) + ": " + what);
+  }
+  double deg = static_cast<double>(h.degenerate_rows);
+  host_allreduce(ctx, &deg, 1, ncclSum);  // own-row counts → global
+  if (!out) return;
+  if (out->correspondence)
+    throw Failure(FCPD_ERR_PARAMETER, "register: correspondence output is single-GPU only");
+  const int run = h.iters_run;
+  const int d = s.d;
+  out->iterations_run = run;
+  out->basis_reused = s.basis_reused ? 1 : 0;
+  out->sigma2_initial = s.sigma2_initial;
+  out->degenerate_rows = static_cast<int64_t>(deg);
+  out->sigma2_clamps = h.sigma2_clamps;
+  if (out->sigma2_trace && run > 0)
+    FCPD_CUDA(cudaMemcpyAsync(out->sigma2_trace, s.trace.p, sizeof(double) * run,
+                              cudaMemcpyDeviceToHost, str));
+  std::vector<double> xt(3 * s.m, 0.0);
+  gather_rows(ctx, s, s.xt64.p, xt.data(), 3);
+  if (out->transformed)
+    for (int c = 0; c < d; ++c)
+      for (int64_t i = 0; i < s.m; ++i)
+        out->transformed[c * s.m + i] =
+            s.cfg.normalize ? xt[c * s.m + i] * s.scale + s.center[c] : xt[c * s.m + i];
+  if (out->coefficients) {
+    pack_coef_kernel<<<ceil_div(b.k, 256), 256, 0, str>>>(s.coef.p, b.k, s.g4.p);
+    FCPD_LAUNCH_CHECK();
+    launch_colsum(s.vp, s.qt_own.p, s.mr4, s.g4.p, s.vpart.p, nullptr, nullptr, 0, str);
+    launch_vreduce_add(s.vp, s.vpart.p, nullptr, 3, s.ptilde_y.p, str);
+    std::vector<double> w(3 * s.m, 0.0);
+    gather_rows(ctx, s, s.ptilde_y.p, w.data(), 3);
+    std::memcpy(out->coefficients, w.data(), sizeof(double) * d * s.m);
+  }
+  std::vector<uint64_t> stamps(4 * static_cast<size_t>(std::max(run, 1)));
+  if (run > 0)
+    FCPD_CUDA(cudaMemcpyAsync(stamps.data(), s.stamps.p, sizeof(uint64_t) * 4 * run,
+                              cudaMemcpyDeviceToHost, str));
+  FCPD_CUDA(cudaStreamSynchronize(str));
+  double tc = 0.0, ti = 0.0;
+  for (int it = 0; it < run; ++it) {
+    tc += 1e-9 * static_cast<double>(stamps[4 * it + 1] - stamps[4 * it]);
+    ti += 1e-9 * static_cast<double>(stamps[4 * it + 2] - stamps[4 * it + 1]);
+  }
+  fcpd_timing& t = out->timing;
+  t.t_c = tc;
+  t.t_eig = s.t_eig;
+  t.t_iter = ti;
+  t.t_f = t.t_eig + t.t_iter;
+  t.t_o = std::max(wall - t.t_c - t.t_f, 0.0);
+  t.t_total = t.t_c + t.t_f + t.t_o;
+  t.t_setup = s.t_gram + s.t_eig;
+  out->h2d_bytes = s.h2d;
+  out->d2h_bytes = s.d2h;
+}
+
 }  // namespace
 }  // namespace fcpd
 
@@ -710,11 +1080,45 @@ int fcpd_create(fcpd_ctx** out, int device) {
   return FCPD_OK;
 }
 
+int fcpd_nccl_unique_id(uint8_t* out128) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  if (!out128) return FCPD_ERR_PARAMETER;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return FCPD_ERR_NCCL;
+  std::memcpy(out128, &id, sizeof id);
+  return FCPD_OK;
+}
+
+int fcpd_create_dist(fcpd_ctx** out, int device, int rank, int world, const uint8_t* id128) {
+  if (!out || !id128 || world < 1 || rank < 0 || rank >= world) return FCPD_ERR_PARAMETER;
+  int rc = fcpd_create(out, device);
+  if (rc) return rc;
+  fcpd_ctx* ctx = *out;
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  if (ncclCommInitRank(&ctx->comm, world, id, rank) != ncclSuccess) {
+    fcpd_destroy(ctx);
+    *out = nullptr;
+    return FCPD_ERR_NCCL;
+  }
+  ctx->rank = rank;
+  ctx->world = world;
+  return FCPD_OK;
+}
+
+int fcpd_world(const fcpd_ctx* ctx, int32_t* rank, int32_t* world) {
+  if (!ctx) return FCPD_ERR_PARAMETER;
+  if (rank) *rank = ctx->rank;
+  if (world) *world = ctx->world;
+  return FCPD_OK;
+}
+
 void fcpd_destroy(fcpd_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   ctx->sess.release();
   ctx->basis.release();
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->solver) cusolverDnDestroy(ctx->solver);
   if (ctx->blas) cublasDestroy(ctx->blas);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -725,10 +1129,13 @@ const char* fcpd_last_error(const fcpd_ctx* ctx) { return ctx ? ctx->err.c_str()
 
 void* fcpd_stream(fcpd_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
-int32_t fcpd_kernels_per_iteration(const fcpd_ctx*) {
-  // prologue, col, col-combine, col-fallback, row, row-combine,
-  // row-fallback, Qᵀ·R, z-reduce/filter, Q·g, transform/σ²-rows, σ²-final
-  return 12;
+int32_t fcpd_kernels_per_iteration(const fcpd_ctx* ctx) {
+  // single GPU: prologue, col, col-combine, col-fallback, row, row-combine,
+  // row-fallback, Qᵀ·R, z-reduce/filter, Q·g, transform/σ²-rows, σ²-final.
+  // distributed: prologue, col, col-combine, col-fallback, row, row-sum,
+  // finalize-own, fb-max, fb-sum, fb-finalize, Qᵀ·R, z-sum, z-filter, Q·g,
+  // transform, σ²-local, σ²-final (+ 7 NCCL collectives)
+  return ctx && ctx->sess.dist ? 17 : 12;
 }
 
 int fcpd_register(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n,
@@ -767,6 +1174,7 @@ int fcpd_session_profile(fcpd_ctx* ctx, int32_t iterations, double* ms_per_phase
   return guarded(ctx, [&] {
     Session& s = ctx->sess;
     if (!s.ready) throw Failure(FCPD_ERR_PARAMETER, "session: not started");
+    if (s.dist) throw Failure(FCPD_ERR_PARAMETER, "session_profile: single-GPU sessions only");
     if (iterations < 1 || s.launched + iterations > s.capacity)
       throw Failure(FCPD_ERR_PARAMETER, "session: more iterations than cfg.iterations");
     cudaEvent_t ev[7];

@@ -520,6 +520,34 @@ EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
   return p;
 }
 
+void launch_estep_prologue(IterState* st, int64_t m, int64_t n_global, int d, double omega,
+                           int32_t* flags_count, uint64_t* stamps, cudaStream_t stream) {
+  estep_prologue_kernel<<<1, 1, 0, stream>>>(st, m, n_global, d, omega, flags_count, stamps);
+  FCPD_LAUNCH_CHECK();
+}
+
+void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
+                        IterState* st, cudaStream_t stream) {
+  estep_col_kernel<kColsPerThread / 2>
+      <<<dim3(p.col_blocks, p.col_splits), 128, 0, stream>>>(b.xt4, m, b.y4b, n, p.m_per_split,
+                                                             st, b.col_part);
+  FCPD_LAUNCH_CHECK();
+  estep_col_combine_kernel<<<ceil_div(n * kCombineLanes, 256), 256, 0, stream>>>(
+      b.col_part, p.col_splits, m, n, b.y4b, b.b2, b.pt1, b.col_flags, b.flags_count, st);
+  FCPD_LAUNCH_CHECK();
+  estep_col_fallback_kernel<<<148, 256, 0, stream>>>(b.xt4, m, b.y4b, b.b2, b.pt1, b.col_flags,
+                                                     b.flags_count, st);
+  FCPD_LAUNCH_CHECK();
+}
+
+void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int64_t m,
+                                 int64_t n, IterState* st, cudaStream_t stream) {
+  estep_row_kernel<kRowsPerThread / 2>
+      <<<dim3(p.row_blocks, p.row_splits), 128, 0, stream>>>(b.xt4, m, b.y4b, n, p.n_per_split,
+                                                             st, b.row_part);
+  FCPD_LAUNCH_CHECK();
+}
+
 void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n, int d,
                   double omega, IterState* st, uint64_t* stamps, cudaStream_t stream,
                   cudaEvent_t mid) {

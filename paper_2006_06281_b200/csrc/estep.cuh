@@ -52,6 +52,14 @@ struct EStepBuffers {
 };
 
 EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count);
+// Pieces of launch_estep for the distributed path (n = local scene count;
+// the prologue's outlier constant uses the global N).
+void launch_estep_prologue(IterState* st, int64_t m, int64_t n_global, int d, double omega,
+                           int32_t* flags_count, uint64_t* stamps, cudaStream_t stream);
+void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
+                        IterState* st, cudaStream_t stream);
+void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int64_t m,
+                                 int64_t n, IterState* st, cudaStream_t stream);
 void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n, int d,
                   double omega, IterState* st, uint64_t* stamps, cudaStream_t stream,
                   cudaEvent_t mid = nullptr);

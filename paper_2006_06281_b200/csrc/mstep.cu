@@ -387,10 +387,11 @@ __global__ void zreduce_filter_kernel(const double* __restrict__ part, SkGeom g,
 // x̃new = X + V; per-row σ² terms; block partial sums (fixed order).
 __global__ void __launch_bounds__(256)
     transform_sigma_kernel(const double* __restrict__ part, SkGeom g, int64_t m,
-                           const double* __restrict__ x0, double* xt64,
+                           int64_t m_valid, const double* __restrict__ x0, double* xt64,
                            double* __restrict__ xt_prev, float4* __restrict__ xt4,
                            const double* __restrict__ ptilde_y, const double* __restrict__ var,
                            double* __restrict__ sig_part, IterState* st, uint64_t* stamps) {
+  // m = row stride of the SoA arrays; rows ≥ m_valid (shard padding) are inert
   if (!st->active) return;
   if (stamps && blockIdx.x == 0 && threadIdx.x == 0) stamps[4 * st->iter + 2] = globaltimer();
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(256)
   double term = 0.0;
   double v0, v1, v2;
   sk_sum_lanes(part, g, i < m ? i : m - 1, static_cast<int>(gid % kSkLanes), v0, v1, v2);
-  if (i < m && gid % kSkLanes == 0) {
+  if (i < m_valid && gid % kSkLanes == 0) {
     const double o0 = xt64[i], o1 = xt64[m + i], o2 = xt64[2 * m + i];
     const double n0 = x0[i] + v0, n1 = x0[m + i] + v1, n2 = x0[2 * m + i] + v2;
     const double d0 = n0 - o0, d1 = n1 - o1, d2 = n2 - o2;
@@ -525,11 +526,75 @@ void launch_transform_sigma(const ColsumPlan& p, const double* part, const doubl
                             int d, int early_stop, double* trace, IterState* st,
                             uint64_t* stamps, cudaStream_t stream) {
   const int64_t m = p.cols;
+  const int nb = launch_transform_rows(p, part, m, x0, xt64, xt_prev, xt4, ptilde_y, var,
+                                       sig_part, st, stamps, stream);
+  launch_sigma_final(sig_part, nb, m, d, early_stop, trace, st, stamps, stream);
+}
+
+int launch_transform_rows(const ColsumPlan& p, const double* part, int64_t m_valid,
+                          const double* x0, double* xt64, double* xt_prev, float4* xt4,
+                          const double* ptilde_y, const double* var, double* sig_part,
+                          IterState* st, uint64_t* stamps, cudaStream_t stream) {
+  const int64_t m = p.cols;
   const int nb = ceil_div(m * kSkLanes, 256);
-  transform_sigma_kernel<<<nb, 256, 0, stream>>>(part, geom(p), m, x0, xt64, xt_prev, xt4,
-                                                 ptilde_y, var, sig_part, st, stamps);
+  transform_sigma_kernel<<<nb, 256, 0, stream>>>(part, geom(p), m, m_valid, x0, xt64, xt_prev,
+                                                 xt4, ptilde_y, var, sig_part, st, stamps);
   FCPD_LAUNCH_CHECK();
-  sigma_final_kernel<<<1, 256, 0, stream>>>(sig_part, nb, m, d, early_stop, trace, st, stamps);
+  return nb;
+}
+
+void launch_sigma_final(const double* sig_part, int blocks, int64_t m_global, int d,
+                        int early_stop, double* trace, IterState* st, uint64_t* stamps,
+                        cudaStream_t stream) {
+  sigma_final_kernel<<<1, 256, 0, stream>>>(sig_part, blocks, m_global, d, early_stop, trace, st,
+                                            stamps);
+  FCPD_LAUNCH_CHECK();
+}
+
+// z (SoA 3×K) = Σ stream-K partials, no filter (distributed path: all-reduced next)
+__global__ void zsum_kernel(const double* __restrict__ part, SkGeom g, int64_t k,
+                            double* __restrict__ z, const IterState* __restrict__ st) {
+  if (st && !st->active) return;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = gid / kSkLanes;
+  double z0, z1, z2;
+  sk_sum_lanes(part, g, i < k ? i : k - 1, static_cast<int>(gid % kSkLanes), z0, z1, z2);
+  if (i >= k || gid % kSkLanes) return;
+  z[i] = z0;
+  z[k + i] = z1;
+  z[2 * k + i] = z2;
+}
+
+__global__ void zfilter_kernel(const double* __restrict__ z, int64_t k,
+                               const double* __restrict__ lam, const double* __restrict__ lam_num,
+                               double lambda_reg, double* __restrict__ coef,
+                               float4* __restrict__ g4, IterState* st) {
+  if (!st->active) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= k) return;
+  const double diag = lam[i] + lambda_reg * st->sigma2;
+  if (!(diag > 0.0)) set_error(st, kDevSolveDiag, diag);
+  const double inv = 1.0 / diag;
+  const double z0 = z[i], z1 = z[k + i], z2 = z[2 * k + i];
+  coef[i] = z0 * inv;
+  coef[k + i] = z1 * inv;
+  coef[2 * k + i] = z2 * inv;
+  const double f = lam_num[i] * inv;
+  g4[i] = make_float4(static_cast<float>(z0 * f), static_cast<float>(z1 * f),
+                      static_cast<float>(z2 * f), 0.f);
+}
+
+void launch_zsum(const ColsumPlan& p, const double* part, double* z, const IterState* st,
+                 cudaStream_t stream) {
+  zsum_kernel<<<ceil_div(p.cols * kSkLanes, 256), 256, 0, stream>>>(part, geom(p), p.cols, z, st);
+  FCPD_LAUNCH_CHECK();
+}
+
+void launch_zfilter(const double* z, int64_t k, const double* lam, const double* lam_num,
+                    double lambda_reg, double* coef, float4* g4, IterState* st,
+                    cudaStream_t stream) {
+  zfilter_kernel<<<ceil_div(k, 256), 256, 0, stream>>>(z, k, lam, lam_num, lambda_reg, coef, g4,
+                                                       st);
   FCPD_LAUNCH_CHECK();
 }
 

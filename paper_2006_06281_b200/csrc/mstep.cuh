@@ -46,6 +46,20 @@ void launch_transform_sigma(const ColsumPlan& p, const double* part, const doubl
                             int d, int early_stop, double* trace, IterState* st,
                             uint64_t* stamps, cudaStream_t stream);
 
+// Pieces for the distributed path.
+int launch_transform_rows(const ColsumPlan& p, const double* part, int64_t m_valid,
+                          const double* x0, double* xt64, double* xt_prev, float4* xt4,
+                          const double* ptilde_y, const double* var, double* sig_part,
+                          IterState* st, uint64_t* stamps, cudaStream_t stream);
+void launch_sigma_final(const double* sig_part, int blocks, int64_t m_global, int d,
+                        int early_stop, double* trace, IterState* st, uint64_t* stamps,
+                        cudaStream_t stream);
+void launch_zsum(const ColsumPlan& p, const double* part, double* z, const IterState* st,
+                 cudaStream_t stream);
+void launch_zfilter(const double* z, int64_t k, const double* lam, const double* lam_num,
+                    double lambda_reg, double* coef, float4* g4, IterState* st,
+                    cudaStream_t stream);
+
 // out = (x0 or 0) + Σ partials, D columns.
 void launch_vreduce_add(const ColsumPlan& p, const double* part, const double* x0, int d,
                         double* out, cudaStream_t stream);

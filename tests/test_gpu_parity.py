@@ -357,3 +357,28 @@ def test_lowrank_register_via_topk_matches_dense_basis(ctx, fc, orc, monkeypatch
     rel = np.abs(topk.sigma2_trace / dense.sigma2_trace - 1).max()
     assert rel <= SIGMA_RTOL, rel
     assert np.abs(topk.transformed - dense.transformed).max() <= POINT_FRAC * bbox_diag(y)
+
+
+# ------------------------------------------ multi-GPU engine path (row e)
+
+
+@pytest.mark.parametrize("variant,omega", [("fast", 0.2), ("fast_lowrank", 0.0)])
+def test_distributed_engine_single_rank(ctx, fc, orc, variant, omega):
+    """The NCCL-sharded engine path (dist.cu kernels, reduce-scatter /
+    all-reduce / all-gather inside the CUDA graph) run as a one-rank group
+    reproduces the single-GPU path; the decomposition itself is checked
+    at world size 2 on CPU (tests/test_dist_gloo.py)."""
+    from paper_2006_06281_b200 import datagen
+    x, y, w = datagen.generate("c1", m=2500)
+    cfg = fc.RegistrationConfig(omega=omega, beta=2.0, lambda_reg=3.0, iterations=25,
+                                variant=variant, rank_fraction=0.05)
+    ref = ctx.register(x, y, cfg)
+    uid = fc.nccl_unique_id()
+    with fc.Context.distributed(0, 0, 1, uid) as dctx:
+        assert dctx.world == (0, 1)
+        got = dctx.register(x, y, cfg)
+        assert dctx.kernels_per_iteration == 17
+    rel = np.abs(got.sigma2_trace / ref.sigma2_trace - 1).max()
+    assert rel <= 1e-9, rel
+    assert np.abs(got.transformed - ref.transformed).max() <= 1e-9 * bbox_diag(y)
+    assert np.abs(got.coefficients - ref.coefficients).max() <= 1e-6 * np.abs(ref.coefficients).max()
