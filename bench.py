@@ -276,9 +276,17 @@ def run_ours(args, world, rank, local):
                         "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                         "kernel": "colsum_bulk (Qᵀ·R and Q·g basis streams, cp.async.bulk ring)",
                         "peak_source": peak_kind}
-            estep_roof = {"bound": "mufu", "achieved": pairs_s / 1e9, "peak": mufu_bound / 1e9,
-                          "unit": "Gpairs/s", "frac": pairs_s / mufu_bound,
-                          "note": "2 ex2/pair, 16 ex2/clk/SM at the sampled SM clock"}
+            # exp/FP32 roofline of the two passes (SASS-verified op counts):
+            # pass 1: 1 MUFU.EX2 + 7 FP32 lane-ops per pair → bound by MUFU (16/clk/SM)
+            # pass 2: 1 MUFU.EX2 + 12 FP32 lane-ops per pair → bound by FP32 (128/clk/SM)
+            clk_per_pair = max(1 / 16, 7 / 128) + max(1 / 16, 12 / 128)
+            roof = 148 * f_mhz * 1e6 / clk_per_pair
+            estep_roof = {"bound": "mufu+fp32", "achieved": pairs_s / 1e9, "peak": roof / 1e9,
+                          "unit": "Gpairs/s", "frac": pairs_s / roof,
+                          "mufu_only_peak": mufu_bound / 1e9,
+                          "note": "pass1 MUFU-bound (16 ex2/clk/SM), pass2 FP32-bound "
+                                  "(12 lane-ops/pair at 128/clk/SM); sampled SM clock; "
+                                  "phase times include the combine/fallback kernels"}
         cpu = None
         if world == 1 and not args.no_cpu:
             rate, threads, secs = cpu_sample(x, y_full, w, args.cpu_iters)

@@ -271,11 +271,14 @@ __global__ void __launch_bounds__(128)
   }
   const int64_t n_begin = static_cast<int64_t>(blockIdx.y) * n_per_split;
   const int64_t n_end = min(n, n_begin + n_per_split);
-  double d0[RP][2], dx[RP][2], dy[RP][2], dz[RP][2], dv[RP][2];
+  // fp64 tile accumulators live in shared memory (thread-private slots,
+  // [quantity][row][thread] → conflict-free): keeps registers for the packed
+  // pipeline and raises occupancy (the pass is FP32-pipe bound).
+  __shared__ double acc_s[5][2 * RP][128];
 #pragma unroll
-  for (int p = 0; p < RP; ++p)
+  for (int k = 0; k < 5; ++k)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) d0[p][h] = dx[p][h] = dy[p][h] = dz[p][h] = dv[p][h] = 0.0;
+    for (int r = 0; r < 2 * RP; ++r) acc_s[k][r][threadIdx.x] = 0.0;
   const float2 minus1 = make_float2(-1.f, -1.f);
 
   for (int64_t base = n_begin; base < n_end; base += kTile) {
@@ -321,16 +324,17 @@ __global__ void __launch_bounds__(128)
     }
 #pragma unroll
     for (int p = 0; p < RP; ++p) {
-      d0[p][0] += f0[p].x;
-      d0[p][1] += f0[p].y;
-      dx[p][0] += fx[p].x;
-      dx[p][1] += fx[p].y;
-      dy[p][0] += fy[p].x;
-      dy[p][1] += fy[p].y;
-      dz[p][0] += fz[p].x;
-      dz[p][1] += fz[p].y;
-      dv[p][0] += fv[p].x;
-      dv[p][1] += fv[p].y;
+      const int t = threadIdx.x;
+      acc_s[0][2 * p][t] += f0[p].x;
+      acc_s[0][2 * p + 1][t] += f0[p].y;
+      acc_s[1][2 * p][t] += fx[p].x;
+      acc_s[1][2 * p + 1][t] += fx[p].y;
+      acc_s[2][2 * p][t] += fy[p].x;
+      acc_s[2][2 * p + 1][t] += fy[p].y;
+      acc_s[3][2 * p][t] += fz[p].x;
+      acc_s[3][2 * p + 1][t] += fz[p].y;
+      acc_s[4][2 * p][t] += fv[p].x;
+      acc_s[4][2 * p + 1][t] += fv[p].y;
     }
   }
   const int64_t sp = static_cast<int64_t>(blockIdx.y) * 5 * m;
@@ -340,11 +344,8 @@ __global__ void __launch_bounds__(128)
     for (int h = 0; h < 2; ++h) {
       const int64_t row = rbase + p * 256 + h;
       if (row < m) {
-        part[sp + 0 * m + row] = d0[p][h];
-        part[sp + 1 * m + row] = dx[p][h];
-        part[sp + 2 * m + row] = dy[p][h];
-        part[sp + 3 * m + row] = dz[p][h];
-        part[sp + 4 * m + row] = dv[p][h];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) part[sp + k * m + row] = acc_s[k][2 * p + h][threadIdx.x];
       }
     }
 }
