@@ -192,6 +192,12 @@ struct Session {
   EStepPlan ep;
   ColsumPlan zp, vp;
   cudaGraphExec_t graph = nullptr;
+  // overlapped graph form: pass-2 row chunks ∥ chunked Qᵀ·R stream
+  int chunks = 1;
+  ColsumPlan zpc[kMaxRowChunks];
+  size_t zoff[kMaxRowChunks] = {};
+  cudaEvent_t ev_chunk[kMaxRowChunks] = {};
+  cudaEvent_t ev_join = nullptr;
 
   // ---- distributed (NCCL) sharding: scene N split over ranks, model rows
   // [m0, m0+mr) owned by this rank (m_pad = world·mr ≥ M).  In this mode
@@ -222,6 +228,9 @@ struct Session {
     mask_all.release();
     fmax_all.release();
     qt_own.release();
+    for (auto& e : ev_chunk)
+      if (e) cudaEventDestroy(e), e = nullptr;
+    if (ev_join) cudaEventDestroy(ev_join), ev_join = nullptr;
   }
 };
 
@@ -231,6 +240,7 @@ struct fcpd_ctx {
   int device = 0;
   int sm_count = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // second stream forked inside the iteration graph
   cusolverDnHandle_t solver = nullptr;
   cublasHandle_t blas = nullptr;
   ncclComm_t comm = nullptr;  // set by fcpd_create_dist: scene-sharded EM over NCCL
@@ -405,6 +415,53 @@ void enqueue_iteration(fcpd_ctx* ctx, Session& s, cudaEvent_t* ev = nullptr) {
   rec(6);
 }
 
+// The captured (graph) form of one iteration: pass 2 is cut into row chunks
+// and the Qᵀ·R basis stream of chunk c runs on a second stream as soon as
+// chunk c's residual rows are final, so the HBM-bound stream overlaps the
+// FP32/MUFU-bound E-step of the next chunk (fork/join with events inside the
+// graph).  Same kernels; only the stream-K partition of Qᵀ·R changes (per
+// chunk), so results equal enqueue_iteration's to fp64 rounding and are
+// bitwise reproducible run to run.
+void enqueue_iteration_overlap(fcpd_ctx* ctx, Session& s) {
+  Basis& b = ctx->basis;
+  IterState* st = s.st.p;
+  cudaStream_t str = ctx->stream, side = ctx->side;
+  EStepBuffers eb{};
+  eb.xt4 = s.xt4.p;
+  eb.xt64 = s.xt64.p;
+  eb.y4b = s.y4b.p;
+  eb.b2 = s.b2.p;
+  eb.pt1 = nullptr;
+  eb.col_part = s.col_part.p;
+  eb.row_part = s.row_part.p;
+  eb.col_flags = s.col_flags.p;
+  eb.row_flags = s.row_flags.p;
+  eb.flags_count = s.flags_count.p;
+  eb.out = RowOut{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p, s.resid4.p, s.x0.p};
+  eb.ystats = s.ystats;
+  launch_estep_prologue(st, s.m, s.n, s.d, s.cfg.omega, s.flags_count.p, s.stamps.p, str);
+  launch_estep_pass1(s.ep, eb, s.m, s.n, st, str);
+  const double* parts[kMaxRowChunks];
+  for (int c = 0; c < s.chunks; ++c) {
+    launch_estep_pass2_chunk(s.ep, eb, s.m, s.n, st, str, c, s.chunks);
+    FCPD_CUDA(cudaEventRecord(s.ev_chunk[c], str));
+    FCPD_CUDA(cudaStreamWaitEvent(side, s.ev_chunk[c], 0));
+    const RowChunk rc = row_chunk(s.ep, s.m, c, s.chunks);
+    double* part = s.zpart.p + s.zoff[c];
+    parts[c] = part;
+    launch_colsum(s.zpc[c], b.q + rc.r0 * b.kpad, b.kpad, s.resid4.p + rc.r0, part, st,
+                  c == 0 ? s.stamps.p : nullptr, 1, side);
+  }
+  FCPD_CUDA(cudaEventRecord(s.ev_join, side));
+  FCPD_CUDA(cudaStreamWaitEvent(str, s.ev_join, 0));
+  launch_zreduce_chunks(s.zpc, parts, s.chunks, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.coef.p,
+                        s.g4.p, st, str);
+  launch_colsum(s.vp, b.qt, b.mpad, s.g4.p, s.vpart.p, st, nullptr, 0, str);
+  launch_transform_sigma(s.vp, s.vpart.p, s.x0.p, s.xt64.p, s.xt_prev.p, s.xt4.p, s.ptilde_y.p,
+                         s.var.p, s.sig_part.p, s.d, s.cfg.early_stop, s.trace.p, st,
+                         s.stamps.p, str);
+}
+
 }  // namespace
 }  // namespace fcpd
 
@@ -433,7 +490,7 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
   s.degenerate.ensure(m);
   s.col_flags.ensure(n);
   s.row_flags.ensure(m);
-  s.flags_count.ensure(2);
+  s.flags_count.ensure(1 + kMaxRowChunks);
   s.st.ensure(1);
   s.capacity = std::max(capacity, 1);
   s.trace.ensure(s.capacity);
@@ -475,7 +532,34 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
     Basis& b = ctx->basis;
     s.zp = make_colsum_plan(m, b.k, ctx->sm_count);
     s.vp = make_colsum_plan(b.k, m, ctx->sm_count);
-    s.zpart.ensure(s.zp.part_doubles());
+    // overlap form: ~8 row blocks (4096 rows) per chunk, ≤ kMaxRowChunks;
+    // each chunk's stream uses one bulk CTA per SM so pass-2 CTAs co-reside
+    // Off by default: measured on B200 (C1) the chunked/concurrent form is
+    // slower (1.03 vs 0.90 ms/iteration) — the co-resident bulk stream drops
+    // below full HBM rate and pass 2 loses SMs; kept for experiments via
+    // FCPD_OVERLAP_CHUNKS=<n>.
+    int chunks = 1;
+    if (const char* e = std::getenv("FCPD_OVERLAP_CHUNKS")) chunks = std::atoi(e);
+    chunks = std::max(1, std::min(kMaxRowChunks, std::min(chunks, s.ep.row_blocks)));
+    s.chunks = chunks;
+    if (chunks > 1) {
+      plan_row_chunks(s.ep, m, n, ctx->sm_count, chunks);
+      s.row_part.ensure(static_cast<size_t>(s.ep.max_row_splits()) * 5 * m);
+    }
+    size_t ztotal = s.zp.part_doubles();
+    if (chunks > 1) {
+      ztotal = 0;
+      for (int c = 0; c < chunks; ++c) {
+        const RowChunk rc = row_chunk(s.ep, m, c, chunks);
+        s.zpc[c] = make_colsum_plan(std::max<int64_t>(1, rc.r1 - rc.r0), b.k, ctx->sm_count, 1);
+        s.zoff[c] = ztotal;
+        ztotal += s.zpc[c].part_doubles();
+        if (!s.ev_chunk[c])
+          FCPD_CUDA(cudaEventCreateWithFlags(&s.ev_chunk[c], cudaEventDisableTiming));
+      }
+      if (!s.ev_join) FCPD_CUDA(cudaEventCreateWithFlags(&s.ev_join, cudaEventDisableTiming));
+    }
+    s.zpart.ensure(std::max(ztotal, s.zp.part_doubles()));
     s.vpart.ensure(s.vp.part_doubles());
     s.coef.ensure(3 * b.k);
     s.g4.ensure(b.k);
@@ -577,7 +661,10 @@ void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, i
   cudaGraph_t g = nullptr;
   FCPD_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   try {
-    enqueue_iteration(ctx, s);
+    if (s.chunks > 1)
+      enqueue_iteration_overlap(ctx, s);
+    else
+      enqueue_iteration(ctx, s);
   } catch (...) {
     cudaStreamEndCapture(ctx->stream, &g);
     if (g) cudaGraphDestroy(g);
@@ -889,7 +976,7 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
   s.row_part.ensure(static_cast<size_t>(s.ep.row_splits) * 5 * m);
   s.col_flags.ensure(n);
   s.row_flags.ensure(m);
-  s.flags_count.ensure(2);
+  s.flags_count.ensure(1 + kMaxRowChunks);
   s.rowsum_all.ensure(5 * s.m_pad);
   s.rowsum_own.ensure(5 * mr);
   s.fsum_all.ensure(5 * s.m_pad);
@@ -1066,6 +1153,7 @@ int fcpd_create(fcpd_ctx** out, int device) {
     FCPD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     ctx->sm_count = sms;
     FCPD_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    FCPD_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     if (cusolverDnCreate(&ctx->solver) != CUSOLVER_STATUS_SUCCESS)
       throw Failure(FCPD_ERR_CUDA, "cusolverDnCreate failed");
     if (cublasCreate(&ctx->blas) != CUBLAS_STATUS_SUCCESS)
@@ -1122,6 +1210,7 @@ void fcpd_destroy(fcpd_ctx* ctx) {
   if (ctx->solver) cusolverDnDestroy(ctx->solver);
   if (ctx->blas) cublasDestroy(ctx->blas);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   delete ctx;
 }
 

@@ -65,8 +65,7 @@ __global__ void estep_prologue_kernel(IterState* st, int64_t m, int64_t n, int d
                                       double omega, int32_t* flags_count, uint64_t* stamps) {
   if (!st->active) return;
   if (stamps) stamps[4 * st->iter + 0] = globaltimer();
-  flags_count[0] = 0;
-  flags_count[1] = 0;
+  for (int i = 0; i <= kMaxRowChunks; ++i) flags_count[i] = 0;  // column + per-chunk row lists
   double s2 = st->sigma2;
   if (s2 < kSigma2Floor) {
     s2 = kSigma2Floor;
@@ -252,12 +251,13 @@ template <int RP>
 __global__ void __launch_bounds__(128)
     estep_row_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4b,
                      int64_t n, int64_t n_per_split, const IterState* __restrict__ st,
-                     double* __restrict__ part /* [split][5][m] */) {
+                     double* __restrict__ part /* [split][5][m] */, int rb_offset) {
   if (!st->active) return;
   __shared__ float4 ya[kTile];  // (yx, yx, yy, yy)
   __shared__ float4 yb[kTile];  // (yz, yz, b, b)
   const float s = st->sx;
-  const int64_t rbase = static_cast<int64_t>(blockIdx.x) * (256 * RP) + 2 * threadIdx.x;
+  const int64_t rbase =
+      static_cast<int64_t>(blockIdx.x + rb_offset) * (256 * RP) + 2 * threadIdx.x;
   float2 nx[RP], ny[RP], nz[RP];
 #pragma unroll
   for (int p = 0; p < RP; ++p) {
@@ -391,15 +391,16 @@ __device__ __forceinline__ void finalize_row(int64_t row, int64_t m, double log2
 __global__ void estep_row_combine_kernel(const double* __restrict__ part, int splits, int64_t m,
                                          int64_t n, const double* __restrict__ xt64,
                                          RowOut out, YStats ys, int32_t* __restrict__ flag_list,
-                                         int32_t* __restrict__ flag_count, IterState* st) {
+                                         int32_t* __restrict__ flag_count, IterState* st,
+                                         int64_t r0, int64_t r1) {
   if (!st->active) return;
   // kCombineLanes lanes per row, lane j sums splits j, j+L, … then a fixed
   // xor-tree combines the lanes: deterministic, and L× the memory-level
-  // parallelism of one thread per row.
+  // parallelism of one thread per row.  Rows [r0, r1) of this launch.
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t row = gid / kCombineLanes;
+  const int64_t row = r0 + gid / kCombineLanes;
   const int lane = static_cast<int>(gid % kCombineLanes);
-  const bool live = row < m;
+  const bool live = row < r1;
   double a0 = 0, ax = 0, ay = 0, az = 0, av = 0;
   if (live) {
     for (int sp = lane; sp < splits; sp += kCombineLanes) {
@@ -518,7 +519,22 @@ EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
   const int s2 = choose_splits(p.row_blocks, n, sm_count * std::max(occ_row, 1));
   p.n_per_split = ceil_div(n, s2);
   p.row_splits = ceil_div(n, p.n_per_split);
+  p.chunks = 1;
   return p;
+}
+
+void plan_row_chunks(EStepPlan& p, int64_t m, int64_t n, int sm_count, int chunks) {
+  int occ_row = 0;
+  FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &occ_row, estep_row_kernel<kRowsPerThread / 2>, 128, 0));
+  p.chunks = chunks;
+  for (int c = 0; c < chunks; ++c) {
+    const int rb = static_cast<int>(static_cast<int64_t>(p.row_blocks) * (c + 1) / chunks -
+                                    static_cast<int64_t>(p.row_blocks) * c / chunks);
+    const int s = choose_splits(std::max(rb, 1), n, sm_count * std::max(occ_row, 1));
+    p.chunk_nps[c] = ceil_div(n, s);
+    p.chunk_splits[c] = ceil_div(n, p.chunk_nps[c]);
+  }
 }
 
 void launch_estep_prologue(IterState* st, int64_t m, int64_t n_global, int d, double omega,
@@ -545,7 +561,7 @@ void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int6
                                  int64_t n, IterState* st, cudaStream_t stream) {
   estep_row_kernel<kRowsPerThread / 2>
       <<<dim3(p.row_blocks, p.row_splits), 128, 0, stream>>>(b.xt4, m, b.y4b, n, p.n_per_split,
-                                                             st, b.row_part);
+                                                             st, b.row_part, 0);
   FCPD_LAUNCH_CHECK();
 }
 
@@ -565,17 +581,39 @@ void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t 
                                                      b.flags_count, st);
   FCPD_LAUNCH_CHECK();
   if (mid) FCPD_CUDA(cudaEventRecord(mid, stream));
-  estep_row_kernel<kRowsPerThread / 2>
-      <<<dim3(p.row_blocks, p.row_splits), 128, 0, stream>>>(b.xt4, m, b.y4b, n, p.n_per_split,
-                                                             st, b.row_part);
+  launch_estep_pass2_chunk(p, b, m, n, st, stream, 0, 1);
+}
+
+RowChunk row_chunk(const EStepPlan& p, int64_t m, int c, int chunks) {
+  RowChunk r;
+  r.rb0 = static_cast<int>(static_cast<int64_t>(p.row_blocks) * c / chunks);
+  r.rb1 = static_cast<int>(static_cast<int64_t>(p.row_blocks) * (c + 1) / chunks);
+  r.r0 = std::min<int64_t>(m, static_cast<int64_t>(r.rb0) * 128 * kRowsPerThread);
+  r.r1 = std::min<int64_t>(m, static_cast<int64_t>(r.rb1) * 128 * kRowsPerThread);
+  return r;
+}
+
+// Pass 2 for the model rows of chunk c of `chunks`: partial sums, combine,
+// exact fallback for this chunk's flagged rows (its own list/counter), so
+// the rows' P̃Y / residual are final when the launch sequence returns and a
+// consumer (the Qᵀ·R stream of the same rows) can start on another stream.
+void launch_estep_pass2_chunk(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
+                              IterState* st, cudaStream_t stream, int c, int chunks) {
+  const RowChunk rc = row_chunk(p, m, c, chunks);
+  if (rc.rb1 <= rc.rb0) return;
+  const bool own = chunks > 1 && p.chunks == chunks;
+  const int splits = own ? p.chunk_splits[c] : p.row_splits;
+  const int64_t nps = own ? p.chunk_nps[c] : p.n_per_split;
+  estep_row_kernel<kRowsPerThread / 2><<<dim3(rc.rb1 - rc.rb0, splits), 128, 0, stream>>>(
+      b.xt4, m, b.y4b, n, nps, st, b.row_part, rc.rb0);
   FCPD_LAUNCH_CHECK();
-  estep_row_combine_kernel<<<ceil_div(m * kCombineLanes, 256), 256, 0, stream>>>(
-      b.row_part, p.row_splits, m, n, b.xt64, b.out, b.ystats, b.row_flags, b.flags_count + 1,
-      st);
+  int32_t* list = b.row_flags + rc.r0;
+  int32_t* count = b.flags_count + 1 + c;
+  estep_row_combine_kernel<<<ceil_div((rc.r1 - rc.r0) * kCombineLanes, 256), 256, 0, stream>>>(
+      b.row_part, splits, m, n, b.xt64, b.out, b.ystats, list, count, st, rc.r0, rc.r1);
   FCPD_LAUNCH_CHECK();
   estep_row_fallback_kernel<<<148, 256, 0, stream>>>(b.xt4, m, b.y4b, n, b.xt64, b.out,
-                                                     b.ystats, b.row_flags, b.flags_count + 1,
-                                                     st);
+                                                     b.ystats, list, count, st);
   FCPD_LAUNCH_CHECK();
 }
 

@@ -12,6 +12,7 @@ namespace fcpd {
 
 constexpr int kColsPerThread = 4;
 constexpr int kRowsPerThread = 4;
+constexpr int kMaxRowChunks = 8;  // pass-2 row chunks (overlap with the Qᵀ·R stream)
 
 // Fallback-path per-row outputs (all device pointers; SoA fp64 M×3).
 struct RowOut {
@@ -34,7 +35,18 @@ struct EStepPlan {
   int64_t m_per_split = 0;
   int row_blocks = 0, row_splits = 0;
   int64_t n_per_split = 0;
+  // per-chunk pass-2 splits when pass 2 runs as row chunks (overlap form):
+  // fewer row blocks per launch need more N-splits to fill the GPU
+  int chunks = 1;
+  int chunk_splits[kMaxRowChunks] = {};
+  int64_t chunk_nps[kMaxRowChunks] = {};
+  int max_row_splits() const {
+    int s = row_splits;
+    for (int c = 0; c < chunks; ++c) s = chunk_splits[c] > s ? chunk_splits[c] : s;
+    return s;
+  }
 };
+void plan_row_chunks(EStepPlan& p, int64_t m, int64_t n, int sm_count, int chunks);
 
 struct EStepBuffers {
   const float4* xt4;   // x̃ fp32 (x,y,z,0), M
@@ -60,6 +72,14 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
                         IterState* st, cudaStream_t stream);
 void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int64_t m,
                                  int64_t n, IterState* st, cudaStream_t stream);
+
+struct RowChunk {
+  int rb0 = 0, rb1 = 0;      // row blocks
+  int64_t r0 = 0, r1 = 0;    // model rows
+};
+RowChunk row_chunk(const EStepPlan& p, int64_t m, int c, int chunks);
+void launch_estep_pass2_chunk(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
+                              IterState* st, cudaStream_t stream, int c, int chunks);
 void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n, int d,
                   double omega, IterState* st, uint64_t* stamps, cudaStream_t stream,
                   cudaEvent_t mid = nullptr);
