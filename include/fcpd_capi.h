@@ -173,6 +173,18 @@ FCPD_API int fcpd_build_basis_topk(fcpd_ctx* ctx, const double* x, int64_t m, in
                                    double beta, int64_t rank, int32_t iterations, double* u,
                                    double* lambda, double* lambda_raw);
 
+/* Spectral cache — kernel.hpp:85-144, the reference's binary format ("FCPD",
+ * u32 version 1, u64 M, u64 K, f64 beta, U row-major f64, λ f64).  save
+ * writes the context's current basis (the one the last register/session
+ * built or reused); load installs a cached basis for the model of the
+ * (x, y, cfg) call (normalised exactly as fcpd_register will) so the next
+ * fcpd_register on them skips the eigensolve (the paper's precomputed
+ * basis).  Mismatched (M, rank, β) → FCPD_ERR_PARAMETER. */
+FCPD_API int fcpd_save_spectral_cache(fcpd_ctx* ctx, const char* path);
+FCPD_API int fcpd_load_spectral_cache(fcpd_ctx* ctx, const char* path, const double* x,
+                                      int64_t m, const double* y, int64_t n, int32_t d,
+                                      const fcpd_config* cfg);
+
 /* build_gram — kernel.hpp:31-47 — M×M column-major fp64. */
 FCPD_API int fcpd_build_gram(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d, double beta,
                     double* phi);

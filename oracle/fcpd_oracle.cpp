@@ -680,6 +680,143 @@ int orc_register(const double* x_in, int64_t m, const double* y_in, int64_t n,
 // Test fixtures restated from proj/tests/test_util.hpp:13-52 (std::mt19937_64
 // with libstdc++'s distributions, so the inputs equal the reference tests').
 // Outputs are column-major like Eigen.
+// kernel.hpp:92-110 save_spectral_cache: "FCPD", u32 1, u64 M, u64 K,
+// f64 beta, U row-major, λ.  u is column-major M×K here (Eigen layout).
+int orc_save_spectral_cache(const char* path, const double* u, const double* lambda, int64_t m,
+                            int64_t k, double beta) {
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(kIo, std::string("cannot open spectral cache for writing: ") + path);
+  const uint32_t ver = 1;
+  const uint64_t mm = m, kk = k;
+  bool ok = std::fwrite("FCPD", 1, 4, f) == 4 && std::fwrite(&ver, 4, 1, f) == 1 &&
+            std::fwrite(&mm, 8, 1, f) == 1 && std::fwrite(&kk, 8, 1, f) == 1 &&
+            std::fwrite(&beta, 8, 1, f) == 1;
+  std::vector<double> row(k);
+  for (int64_t i = 0; ok && i < m; ++i) {
+    for (int64_t j = 0; j < k; ++j) row[j] = u[j * m + i];
+    ok = std::fwrite(row.data(), 8, k, f) == static_cast<size_t>(k);
+  }
+  ok = ok && std::fwrite(lambda, 8, k, f) == static_cast<size_t>(k);
+  ok = (std::fclose(f) == 0) && ok;
+  return ok ? kOk : fail(kIo, std::string("spectral cache write failed: ") + path);
+}
+
+// kernel.hpp:112-144 load_spectral_cache.  Call with u == nullptr to read
+// the header only (m, k, beta).
+int orc_load_spectral_cache(const char* path, int64_t* m, int64_t* k, double* beta, double* u,
+                            double* lambda) {
+  FILE* f = std::fopen(path, "rb");
+  if (!f) return fail(kIo, std::string("cannot open spectral cache: ") + path);
+  char magic[4];
+  uint32_t ver = 0;
+  uint64_t mm = 0, kk = 0;
+  double b = 0.0;
+  const bool hdr = std::fread(magic, 1, 4, f) == 4 && std::fread(&ver, 4, 1, f) == 1 &&
+                   std::fread(&mm, 8, 1, f) == 1 && std::fread(&kk, 8, 1, f) == 1 &&
+                   std::fread(&b, 8, 1, f) == 1;
+  if (!hdr || std::memcmp(magic, "FCPD", 4) != 0) {
+    std::fclose(f);
+    return fail(kParse, std::string("not a spectral cache file: ") + path);
+  }
+  if (ver != 1) {
+    std::fclose(f);
+    return fail(kParse, std::string("unsupported spectral cache version in ") + path);
+  }
+  *m = static_cast<int64_t>(mm);
+  *k = static_cast<int64_t>(kk);
+  *beta = b;
+  if (!u) {
+    std::fclose(f);
+    return kOk;
+  }
+  std::vector<double> row(kk);
+  bool ok = true;
+  for (uint64_t i = 0; ok && i < mm; ++i) {
+    ok = std::fread(row.data(), 8, kk, f) == kk;
+    for (uint64_t j = 0; j < kk; ++j) u[j * mm + i] = row[j];
+  }
+  ok = ok && std::fread(lambda, 8, kk, f) == kk;
+  std::fclose(f);
+  return ok ? kOk : fail(kParse, std::string("truncated spectral cache: ") + path);
+}
+
+// register_pointsets (registration.hpp:79-175) for a GIVEN basis with the
+// streaming E-step (orc_estep_stream: no M×N matrix) — the oracle for
+// configs whose dense P (20–320 GB) does not fit.  Transform: X + U
+// diag(λ_num) Uᵀ W (λ_num = raw λ for full rank, clamped for low rank);
+// σ² by the per-row form Σ_m [V_m − 2δ·Δ̄ + ‖δ‖²]/(DM), algebraically the
+// trace form of solvers.hpp:166-172 (row sums of P̃ are 1; checked against
+// the dense oracle at small sizes in tests/test_oracle_kat.py).
+int orc_register_stream(const double* x_in, int64_t m, const double* y_in, int64_t n, int d,
+                        double omega, double lambda_reg, int iterations, int normalize,
+                        const double* u, const double* lam, const double* lam_num, int64_t k,
+                        double* out_x, double* sigma2_trace, int* iters_run,
+                        double* sigma2_initial) {
+  if (m == 0 || n == 0) return fail(kParameter, "register: empty point set");
+  std::vector<double> x(m * d), y(n * d), center(d, 0.0);
+  double scale = 1.0;
+  int degen = 0;
+  if (normalize) {
+    int rc = orc_normalize_pair(x_in, m, y_in, n, d, x.data(), y.data(), center.data(), &scale,
+                                &degen);
+    if (rc) return rc;
+  } else {
+    std::memcpy(x.data(), x_in, sizeof(double) * m * d);
+    std::memcpy(y.data(), y_in, sizeof(double) * n * d);
+  }
+  double sigma2 = 0.0;
+  orc_init_sigma2(x.data(), m, y.data(), n, d, &sigma2);
+  *sigma2_initial = sigma2;
+  std::vector<double> xt = x, pty(m * d), p1(m), var(m), resid(m * d), z(k * d), xn(m * d);
+  std::vector<int32_t> deg(m);
+  int it = 0;
+  for (; it < iterations; ++it) {
+    int clamped = 0;
+    int rc = orc_estep_stream(xt.data(), m, y.data(), n, d, omega, sigma2, pty.data(), p1.data(),
+                              var.data(), deg.data(), nullptr, &clamped);
+    if (rc) return fail(kNumeric, "register: iteration " + std::to_string(it) + ": " + g_err);
+    for (int64_t i = 0; i < m * d; ++i) resid[i] = pty[i] - x[i];
+    const double shift = lambda_reg * sigma2;
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < k; ++j)
+      for (int c = 0; c < d; ++c) {
+        double acc = 0.0;
+        for (int64_t r = 0; r < m; ++r) acc += u[j * m + r] * resid[c * m + r];
+        z[c * k + j] = acc * lam_num[j] / (lam[j] + shift);
+      }
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < m; ++r)
+      for (int c = 0; c < d; ++c) {
+        double acc = 0.0;
+        for (int64_t j = 0; j < k; ++j) acc += u[j * m + r] * z[c * k + j];
+        xn[c * m + r] = x[c * m + r] + acc;
+      }
+    double tot = 0.0;
+    for (int64_t r = 0; r < m; ++r) {
+      double dd = 0.0, da = 0.0;
+      for (int c = 0; c < d; ++c) {
+        const double dl = xn[c * m + r] - xt[c * m + r];
+        dd += dl * dl;
+        da += dl * (pty[c * m + r] - xt[c * m + r]);
+      }
+      tot += var[r] - 2.0 * da + dd;
+    }
+    const double val = tot / (static_cast<double>(d) * static_cast<double>(m));
+    if (val < -1e-8)
+      return fail(kNumeric, "register: iteration " + std::to_string(it) +
+                                ": update_sigma2: negative variance " + std::to_string(val));
+    const double next = std::max(val, kSigma2Floor);
+    sigma2_trace[it] = next;
+    sigma2 = next;
+    xt.swap(xn);
+  }
+  *iters_run = it;
+  for (int c = 0; c < d; ++c)
+    for (int64_t r = 0; r < m; ++r)
+      out_x[c * m + r] = normalize ? xt[c * m + r] * scale + center[c] : xt[c * m + r];
+  return kOk;
+}
+
 void orc_make_cloud(int64_t m, int d, uint64_t seed, double* out) {
   std::mt19937_64 rng(seed);
   std::uniform_real_distribution<double> u(-1.0, 1.0);

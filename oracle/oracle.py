@@ -315,3 +315,48 @@ def random_row_constrained(m: int, n: int, seed: int) -> np.ndarray:
     p = np.zeros((m, n), order="F")
     lib().orc_random_row_constrained(_I64(m), _I64(n), C.c_uint64(seed), _ptr(p))
     return p
+
+
+# ------------------------------------------- spectral cache + streaming register
+
+
+def save_spectral_cache(path: str, u, lam, beta: float):
+    """kernel.hpp:92-110."""
+    u = np.asfortranarray(u, dtype=np.float64)
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    _check(lib().orc_save_spectral_cache(path.encode(), _ptr(u), _ptr(lam), _I64(u.shape[0]),
+                                         _I64(u.shape[1]), C.c_double(beta)))
+
+
+def load_spectral_cache(path: str):
+    """kernel.hpp:112-144 → (u (M×K), lambda (K), beta)."""
+    m, k, beta = C.c_int64(), C.c_int64(), C.c_double()
+    _check(lib().orc_load_spectral_cache(path.encode(), C.byref(m), C.byref(k), C.byref(beta),
+                                         None, None))
+    u = np.zeros((m.value, k.value), order="F")
+    lam = np.zeros(k.value)
+    _check(lib().orc_load_spectral_cache(path.encode(), C.byref(m), C.byref(k), C.byref(beta),
+                                         _ptr(u), _ptr(lam)))
+    return u, lam, beta.value
+
+
+def register_stream(x, y, u, lam, lam_num=None, *, omega, lambda_reg, iterations,
+                    normalize=True) -> Result:
+    """Streaming-E-step restatement of register_pointsets with a given basis
+    (configs 2–4: no M×N matrix)."""
+    x, y = _col(x), _col(y)
+    u = np.asfortranarray(u, dtype=np.float64)
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    lam_num = lam if lam_num is None else np.ascontiguousarray(lam_num, dtype=np.float64)
+    m, d = x.shape
+    out_x = np.zeros((m, d), order="F")
+    trace = np.zeros(max(iterations, 1))
+    it = C.c_int()
+    s0 = C.c_double()
+    _check(lib().orc_register_stream(_ptr(x), _I64(m), _ptr(y), _I64(y.shape[0]), d,
+                                     C.c_double(omega), C.c_double(lambda_reg), int(iterations),
+                                     int(normalize), _ptr(u), _ptr(lam), _ptr(lam_num),
+                                     _I64(u.shape[1]), _ptr(out_x), _ptr(trace), C.byref(it),
+                                     C.byref(s0)))
+    return Result(np.ascontiguousarray(out_x), np.zeros_like(out_x), trace[: it.value].copy(),
+                  s0.value)

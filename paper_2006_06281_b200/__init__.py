@@ -144,6 +144,9 @@ def lib():
             "fcpd_build_basis": (C.c_int, [vp, P, I64, I32, D, I64, P, P, P]),
             "fcpd_build_gram": (C.c_int, [vp, P, I64, I32, D, P]),
             "fcpd_build_basis_topk": (C.c_int, [vp, P, I64, I32, D, I64, I32, P, P, P]),
+            "fcpd_save_spectral_cache": (C.c_int, [vp, C.c_char_p]),
+            "fcpd_load_spectral_cache": (C.c_int, [vp, C.c_char_p, P, I64, P, I64, I32,
+                                                   C.POINTER(_Config)]),
             "fcpd_nccl_unique_id": (C.c_int, [C.c_char_p]),
             "fcpd_create_dist": (C.c_int, [C.POINTER(vp), C.c_int, C.c_int, C.c_int,
                                            C.c_char_p]),
@@ -396,6 +399,17 @@ class Context:
         self._check(lib().fcpd_build_basis(self._h, _p(x), m, d, beta, int(rank), _p(u),
                                            _p(lam), _p(raw)))
         return u, lam, raw
+
+    def save_spectral_cache(self, path: str):
+        """Write the context's current basis in the reference format (kernel.hpp:92-110)."""
+        self._check(lib().fcpd_save_spectral_cache(self._h, os.fsencode(path)))
+
+    def load_spectral_cache(self, path: str, x, y, cfg: RegistrationConfig):
+        """Install a cached basis for register(x, y, cfg) (kernel.hpp:112-144)."""
+        x, y = _colmajor(x), _colmajor(y)
+        c = cfg._c()
+        self._check(lib().fcpd_load_spectral_cache(self._h, os.fsencode(path), _p(x), x.shape[0],
+                                                   _p(y), y.shape[0], x.shape[1], C.byref(c)))
 
     def build_basis_topk(self, x, beta: float, rank: int, iterations: int = 0):
         """Top-K eigenpairs of Φ without forming it (configs 2–4 setup)."""

@@ -599,6 +599,42 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
                         int d, const fcpd_config& cfg);
 void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall);
 
+// normalize_pair (pointset.hpp:124-148), fp64 on the host, O(M+N); outputs
+// fp64 SoA(3) copies (unused coordinates zero).
+void normalize_pair_host(const double* x, int64_t m, const double* y, int64_t n, int d,
+                         bool normalize, std::vector<double>& xs, std::vector<double>& ys,
+                         double* center, double* scale) {
+  xs.assign(3 * m, 0.0);
+  ys.assign(3 * n, 0.0);
+  center[0] = center[1] = center[2] = 0.0;
+  *scale = 1.0;
+  if (normalize) {
+    const double total = static_cast<double>(m + n);
+    for (int c = 0; c < d; ++c) {
+      double sx = 0.0, sy = 0.0;
+      for (int64_t i = 0; i < m; ++i) sx += x[c * m + i];
+      for (int64_t i = 0; i < n; ++i) sy += y[c * n + i];
+      center[c] = (sx + sy) / total;
+    }
+    double sc = 0.0;
+    for (int c = 0; c < d; ++c) {
+      for (int64_t i = 0; i < m; ++i) sc = std::max(sc, std::fabs(x[c * m + i] - center[c]));
+      for (int64_t i = 0; i < n; ++i) sc = std::max(sc, std::fabs(y[c * n + i] - center[c]));
+    }
+    if (sc <= 0.0) sc = 1.0;
+    *scale = sc;
+    for (int c = 0; c < d; ++c) {
+      for (int64_t i = 0; i < m; ++i) xs[c * m + i] = (x[c * m + i] - center[c]) / sc;
+      for (int64_t i = 0; i < n; ++i) ys[c * n + i] = (y[c * n + i] - center[c]) / sc;
+    }
+  } else {
+    for (int c = 0; c < d; ++c) {
+      std::memcpy(&xs[c * m], x + c * m, sizeof(double) * m);
+      std::memcpy(&ys[c * n], y + c * n, sizeof(double) * n);
+    }
+  }
+}
+
 void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n, int d,
                    const fcpd_config& cfg) {
   if (ctx->comm) {
@@ -615,35 +651,8 @@ void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, i
   s.n = n;
   s.d = d;
   s.cfg = cfg;
-  // normalize_pair (pointset.hpp:124-148), fp64 on the host: O(M+N)
-  std::vector<double> xs(3 * m, 0.0), ys(3 * n, 0.0);
-  s.center[0] = s.center[1] = s.center[2] = 0.0;
-  s.scale = 1.0;
-  if (cfg.normalize) {
-    const double total = static_cast<double>(m + n);
-    for (int c = 0; c < d; ++c) {
-      double sx = 0.0, sy = 0.0;
-      for (int64_t i = 0; i < m; ++i) sx += x[c * m + i];
-      for (int64_t i = 0; i < n; ++i) sy += y[c * n + i];
-      s.center[c] = (sx + sy) / total;
-    }
-    double sc = 0.0;
-    for (int c = 0; c < d; ++c) {
-      for (int64_t i = 0; i < m; ++i) sc = std::max(sc, std::fabs(x[c * m + i] - s.center[c]));
-      for (int64_t i = 0; i < n; ++i) sc = std::max(sc, std::fabs(y[c * n + i] - s.center[c]));
-    }
-    if (sc <= 0.0) sc = 1.0;
-    s.scale = sc;
-    for (int c = 0; c < d; ++c) {
-      for (int64_t i = 0; i < m; ++i) xs[c * m + i] = (x[c * m + i] - s.center[c]) / sc;
-      for (int64_t i = 0; i < n; ++i) ys[c * n + i] = (y[c * n + i] - s.center[c]) / sc;
-    }
-  } else {
-    for (int c = 0; c < d; ++c) {
-      std::memcpy(&xs[c * m], x + c * m, sizeof(double) * m);
-      std::memcpy(&ys[c * n], y + c * n, sizeof(double) * n);
-    }
-  }
+  std::vector<double> xs, ys;
+  normalize_pair_host(x, m, y, n, d, cfg.normalize != 0, xs, ys, s.center, &s.scale);
   // x0 must be on the device before the Gram build
   s.x0.ensure(3 * m);
   FCPD_CUDA(cudaMemcpyAsync(s.x0.p, xs.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice,
@@ -1413,6 +1422,88 @@ int fcpd_build_basis(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d, doubl
     b.release();
     xd.release();
     g.release();
+  });
+}
+
+// ---- spectral cache (kernel.hpp:85-144): "FCPD", u32 version 1, u64 M,
+// u64 K, f64 beta, U row-major f64 (M×K), λ f64 (K) — little-endian.
+
+int fcpd_save_spectral_cache(fcpd_ctx* ctx, const char* path) {
+  return guarded(ctx, [&] {
+    Basis& b = ctx->basis;
+    if (!b.u64 || b.m == 0) throw Failure(FCPD_ERR_PARAMETER, "spectral cache: no basis in context");
+    std::vector<double> u(static_cast<size_t>(b.m * b.k));
+    FCPD_CUDA(cudaMemcpyAsync(u.data(), b.u64, sizeof(double) * u.size(), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
+    FILE* f = std::fopen(path, "wb");
+    if (!f) throw Failure(FCPD_ERR_IO, std::string("cannot open spectral cache for writing: ") + path);
+    const uint32_t ver = 1;
+    const uint64_t mm = static_cast<uint64_t>(b.m), kk = static_cast<uint64_t>(b.k);
+    bool ok = std::fwrite("FCPD", 1, 4, f) == 4 && std::fwrite(&ver, 4, 1, f) == 1 &&
+              std::fwrite(&mm, 8, 1, f) == 1 && std::fwrite(&kk, 8, 1, f) == 1 &&
+              std::fwrite(&b.key_beta, 8, 1, f) == 1;
+    std::vector<double> row(b.k);
+    for (int64_t i = 0; ok && i < b.m; ++i) {
+      for (int64_t j = 0; j < b.k; ++j) row[j] = u[j * b.m + i];
+      ok = std::fwrite(row.data(), 8, b.k, f) == static_cast<size_t>(b.k);
+    }
+    ok = ok && std::fwrite(b.lam_host.data(), 8, b.k, f) == static_cast<size_t>(b.k);
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw Failure(FCPD_ERR_IO, std::string("spectral cache write failed: ") + path);
+  });
+}
+
+int fcpd_load_spectral_cache(fcpd_ctx* ctx, const char* path, const double* x, int64_t m,
+                             const double* y, int64_t n, int32_t d, const fcpd_config* cfg) {
+  return guarded(ctx, [&] {
+    if (!cfg) throw Failure(FCPD_ERR_PARAMETER, "spectral cache: null config");
+    validate_register(x, m, y, n, d, *cfg);
+    FILE* f = std::fopen(path, "rb");
+    if (!f) throw Failure(FCPD_ERR_IO, std::string("cannot open spectral cache: ") + path);
+    char magic[4];
+    uint32_t ver = 0;
+    uint64_t mm = 0, kk = 0;
+    double beta = 0.0;
+    const bool hdr = std::fread(magic, 1, 4, f) == 4 && std::fread(&ver, 4, 1, f) == 1 &&
+                     std::fread(&mm, 8, 1, f) == 1 && std::fread(&kk, 8, 1, f) == 1 &&
+                     std::fread(&beta, 8, 1, f) == 1;
+    if (!hdr || std::memcmp(magic, "FCPD", 4) != 0) {
+      std::fclose(f);
+      throw Failure(FCPD_ERR_PARSE, std::string("not a spectral cache file: ") + path);
+    }
+    if (ver != 1) {
+      std::fclose(f);
+      throw Failure(FCPD_ERR_PARSE, std::string("unsupported spectral cache version in ") + path);
+    }
+    const bool lowrank = cfg->variant == FCPD_VARIANT_FAST_LOWRANK;
+    const int64_t rank = lowrank ? lowrank_rank(cfg->rank_fraction, m) : m;
+    if (static_cast<int64_t>(mm) != m || static_cast<int64_t>(kk) != rank || beta != cfg->beta) {
+      std::fclose(f);
+      throw Failure(FCPD_ERR_PARAMETER, "spectral cache does not match (M, rank, beta) of the call");
+    }
+    std::vector<double> u(static_cast<size_t>(m * rank)), row(rank), lam(rank);
+    bool ok = true;
+    for (int64_t i = 0; ok && i < m; ++i) {
+      ok = std::fread(row.data(), 8, rank, f) == static_cast<size_t>(rank);
+      for (int64_t j = 0; j < rank; ++j) u[j * m + i] = row[j];
+    }
+    ok = ok && std::fread(lam.data(), 8, rank, f) == static_cast<size_t>(rank);
+    std::fclose(f);
+    if (!ok) throw Failure(FCPD_ERR_PARSE, std::string("truncated spectral cache: ") + path);
+    // install under the key register_pointsets will compute for (x, y, cfg)
+    std::vector<double> xs, ys;
+    double center[3], scale;
+    normalize_pair_host(x, m, y, n, d, cfg->normalize != 0, xs, ys, center, &scale);
+    uint64_t h = fnv1a(xs.data(), sizeof(double) * xs.size());
+    h = fnv1a(&m, sizeof m, h);
+    h = fnv1a(&rank, sizeof rank, h);
+    Basis& b = ctx->basis;
+    basis_from_host(b, u.data(), lam.data(), m, rank, ctx->stream);
+    upload_lambda(b, !lowrank, ctx->stream);  // cached λ are the clamped ones
+    b.key_hash = h;
+    b.key_beta = cfg->beta;
+    b.key_variant = cfg->variant;
   });
 }
 

@@ -81,8 +81,9 @@ void Basis::release() {
   if (q) cudaFree(q);
   if (qt) cudaFree(qt);
   if (lam) cudaFree(lam);
+  if (u64) cudaFree(u64);
   q = qt = nullptr;
-  lam = nullptr;
+  lam = u64 = nullptr;
   lam_raw_host.clear();
   lam_host.clear();
   m = k = 0;
@@ -106,12 +107,25 @@ static void alloc_basis(Basis& b, int64_t m, int64_t k) {
   FCPD_CUDA(cudaMalloc(&b.q, sizeof(float) * m * b.kpad));
   FCPD_CUDA(cudaMalloc(&b.qt, sizeof(float) * k * b.mpad));
   FCPD_CUDA(cudaMalloc(&b.lam, sizeof(double) * 2 * k));
+  FCPD_CUDA(cudaMalloc(&b.u64, sizeof(double) * m * k));
+}
+
+// u64[:, i] = V[:, src(i)] (fp64 copy kept for the spectral cache)
+__global__ void pack_u64_kernel(const double* __restrict__ v, int64_t ldv, int64_t m,
+                                int64_t ncols, int reverse, double* __restrict__ u) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = blockIdx.y;
+  const int64_t src = reverse ? ncols - 1 - i : i;
+  if (r < m) u[i * m + r] = v[src * ldv + r];
 }
 
 void pack_basis(Basis& b, const double* v, int64_t ldv, int64_t ncols, int reverse,
                 cudaStream_t stream) {
   pack_qt_kernel<<<dim3(ceil_div(b.mpad, 256), static_cast<unsigned>(b.k)), 256, 0, stream>>>(
       v, ldv, b.m, ncols, reverse, b.qt, b.mpad);
+  FCPD_LAUNCH_CHECK();
+  pack_u64_kernel<<<dim3(ceil_div(b.m, 256), static_cast<unsigned>(b.k)), 256, 0, stream>>>(
+      v, ldv, b.m, ncols, reverse, b.u64);
   FCPD_LAUNCH_CHECK();
   pack_q_kernel<<<dim3(ceil_div(b.m, 32), ceil_div(b.kpad, 32)), dim3(32, 8), 0, stream>>>(
       v, ldv, b.m, ncols, b.k, reverse, b.q, b.kpad);

@@ -16,6 +16,7 @@ struct Basis {
   float* q = nullptr;    // M×kpad row-major fp32
   float* qt = nullptr;   // K×mpad row-major fp32
   double* lam = nullptr; // [0,k): clamped λ ; [k,2k): transform numerator
+  double* u64 = nullptr; // M×K column-major fp64 eigenvectors (descending), for export
   bool full_rank = false;
   std::vector<double> lam_raw_host, lam_host;
   // cache key

@@ -382,3 +382,62 @@ def test_distributed_engine_single_rank(ctx, fc, orc, variant, omega):
     assert rel <= 1e-9, rel
     assert np.abs(got.transformed - ref.transformed).max() <= 1e-9 * bbox_diag(y)
     assert np.abs(got.coefficients - ref.coefficients).max() <= 1e-6 * np.abs(ref.coefficients).max()
+
+
+# ------------------------------------------------ spectral cache (§8f rank 1)
+
+
+def test_spectral_cache_interchange(ctx, fc, orc, tmp_path):
+    """Device basis → reference-format file → oracle, and oracle file →
+    device: the cached basis is reused by register (t_eig = 0) and gives the
+    oracle's registration."""
+    x = orc.make_torus(300, 71)
+    y = orc.make_torus(330, 72) * 1.07
+    cfg = fc.RegistrationConfig(omega=0.2, beta=2.0, lambda_reg=3.0, iterations=20,
+                                variant="fast_lowrank", rank_fraction=0.1)
+    ctx.register(x, y, cfg)
+    path = str(tmp_path / "dev.fcpd")
+    ctx.save_spectral_cache(path)
+    u, lam, beta = orc.load_spectral_cache(path)
+    xn, _, _, _, _ = orc.normalize_pair(x, y)
+    ur, lr, _ = orc.eigendecompose(orc.build_gram(xn, 2.0), 30)
+    assert beta == 2.0 and u.shape == (300, 30)
+    assert np.abs(lam - lr).max() <= 1e-10 * lr[0]
+    # same subspace (eigenvectors up to sign)
+    assert np.abs(np.abs((u * ur).sum(0)) - 1).max() <= 1e-8
+    # oracle-written cache → device
+    opath = str(tmp_path / "orc.fcpd")
+    orc.save_spectral_cache(opath, ur, lr, 2.0)
+    with fc.Context(0) as other:
+        other.load_spectral_cache(opath, x, y, cfg)
+        got = other.register(x, y, cfg)
+    assert got.basis_reused and got.timing.t_eig == 0.0
+    ref = orc.register(x, y, omega=0.2, beta=2.0, lambda_reg=3.0, iterations=20,
+                       variant="fast_lowrank", rank_fraction=0.1)
+    rel, pts = record_parity("cache-torus300-lowrank", got, ref, y)
+    assert rel.max() <= SIGMA_RTOL and pts <= POINT_FRAC
+    with pytest.raises(fc.ParameterError):  # rank mismatch
+        other2 = fc.Context(0)
+        other2.load_spectral_cache(opath, x, y, fc.RegistrationConfig(variant="fast"))
+
+
+@pytest.mark.parametrize("name,iters", [("c2", 3), ("c3", 2), ("c4", 1)])
+def test_full_size_parity_configs_2_4(ctx, fc, orc, tmp_path, name, iters):
+    """BASELINE configs 2–4 at FULL size: the device run (top-K on-the-fly
+    setup, fused E-step, basis streams) against the oracle's streaming
+    restatement of register_pointsets driven by the same basis (exported in
+    the reference's spectral-cache format), for the first iterations the
+    CPU can afford (C3: 1.5e10 pairs per iteration)."""
+    from paper_2006_06281_b200 import datagen
+    x, y, w = datagen.generate(name)
+    cfg = datagen.config_for(w, iterations=iters)
+    got = ctx.register(x, y, cfg)
+    path = str(tmp_path / f"{name}.fcpd")
+    ctx.save_spectral_cache(path)
+    u, lam, _ = orc.load_spectral_cache(path)
+    orc.set_threads(os.cpu_count() or 1)
+    ref = orc.register_stream(x, y, u, lam, omega=w.omega, lambda_reg=w.lambda_reg,
+                              iterations=iters)
+    rel, pts = record_parity(f"{name}-full-{iters}it", got, ref, y)
+    assert rel.max() <= SIGMA_RTOL
+    assert pts <= POINT_FRAC

@@ -407,3 +407,38 @@ def test_stream_estep_matches_dense(orc, omega, s2):
     var = (pc * d2).sum(1)
     assert np.allclose(es.var, var, rtol=1e-9, atol=1e-300)
     assert np.allclose(es.pt1, p.sum(0), rtol=1e-10, atol=1e-300)
+
+
+def test_spectral_cache_round_trip(orc, tmp_path):  # test_kernel.cpp:98-110
+    x = orc.make_cloud(20, 3, 5)
+    u, lam, _ = orc.eigendecompose(orc.build_gram(x, 2.0), 7)
+    path = str(tmp_path / "fcpd_cache.bin")
+    orc.save_spectral_cache(path, u, lam, 2.0)
+    back, blam, beta = orc.load_spectral_cache(path)
+    assert beta == 2.0 and back.shape == (20, 7)
+    assert np.abs(back - u).max() == 0.0 and np.abs(blam - lam).max() == 0.0
+    raw = open(path, "rb").read()
+    assert raw[:4] == b"FCPD" and len(raw) == 4 + 4 + 8 + 8 + 8 + 8 * (20 * 7 + 7)
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(b"XXXX" + raw[4:])
+    with pytest.raises(orc.OracleError) as ei:
+        orc.load_spectral_cache(str(bad))
+    assert ei.value.kind == "ParseError"
+
+
+@pytest.mark.parametrize("variant,omega", [("fast", 0.0), ("fast_lowrank", 0.3)])
+def test_streaming_register_equals_dense(orc, variant, omega):
+    """The streaming restatement used as the oracle for configs 2–4 (no M×N
+    matrix, per-row σ²) equals the dense faithful restatement."""
+    x = orc.make_torus(150, 3)
+    y = orc.make_torus(170, 4) * 1.05
+    xn, _, _, _, _ = orc.normalize_pair(x, y)
+    phi = orc.build_gram(xn, 2.0)
+    k = 150 if variant == "fast" else 30
+    u, lam, raw = orc.eigendecompose(phi, k)
+    ref = orc.register(x, y, omega=omega, beta=2.0, lambda_reg=3.0, iterations=20, variant=variant,
+                       rank_fraction=k / 150)
+    st = orc.register_stream(x, y, u, lam, raw if variant == "fast" else lam, omega=omega,
+                             lambda_reg=3.0, iterations=20)
+    assert np.abs(st.sigma2_trace / ref.sigma2_trace - 1).max() <= 1e-11
+    assert np.abs(st.transformed - ref.transformed).max() <= 1e-11
