@@ -498,7 +498,7 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
   s.ep = make_estep_plan(m, n, ctx->sm_count);
   s.col_part.ensure(static_cast<size_t>(s.ep.col_splits) * n);
   s.row_part.ensure(static_cast<size_t>(s.ep.row_splits) * 5 * m);
-  s.sig_part.ensure(ceil_div(m, 256));
+  s.sig_part.ensure(transform_sigma_blocks(m));  // one σ² partial per transform block
 
   std::vector<float4> x4(m), y4(n);
   for (int64_t i = 0; i < m; ++i)
@@ -1008,7 +1008,7 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
   s.zfull.ensure(3 * b.k);
   s.coef.ensure(3 * b.k);
   s.g4.ensure(b.k);
-  s.sig_part.ensure(ceil_div(mr * 4, 256));
+  s.sig_part.ensure(transform_sigma_blocks(mr));
   s.sig_local.ensure(1);
   s.st.ensure(1);
   s.capacity = std::max(cfg.iterations, 1);

@@ -581,12 +581,14 @@ void launch_transform_sigma(const ColsumPlan& p, const double* part, const doubl
   launch_sigma_final(sig_part, nb, m, d, early_stop, trace, st, stamps, stream);
 }
 
+int transform_sigma_blocks(int64_t m) { return ceil_div(m * kSkLanes, 256); }
+
 int launch_transform_rows(const ColsumPlan& p, const double* part, int64_t m_valid,
                           const double* x0, double* xt64, double* xt_prev, float4* xt4,
                           const double* ptilde_y, const double* var, double* sig_part,
                           IterState* st, uint64_t* stamps, cudaStream_t stream) {
   const int64_t m = p.cols;
-  const int nb = ceil_div(m * kSkLanes, 256);
+  const int nb = transform_sigma_blocks(m);
   transform_sigma_kernel<<<nb, 256, 0, stream>>>(part, geom(p), m, m_valid, x0, xt64, xt_prev,
                                                  xt4, ptilde_y, var, sig_part, st, stamps);
   FCPD_LAUNCH_CHECK();

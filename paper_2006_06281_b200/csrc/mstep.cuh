@@ -55,6 +55,9 @@ void launch_transform_sigma(const ColsumPlan& p, const double* part, const doubl
                             int d, int early_stop, double* trace, IterState* st,
                             uint64_t* stamps, cudaStream_t stream);
 
+// Number of blocks (= σ² partials) launch_transform_* uses for m rows.
+int transform_sigma_blocks(int64_t m);
+
 // Pieces for the distributed path.
 int launch_transform_rows(const ColsumPlan& p, const double* part, int64_t m_valid,
                           const double* x0, double* xt64, double* xt_prev, float4* xt4,
