@@ -90,6 +90,9 @@ typedef struct fcpd_result {
   fcpd_timing timing;
   int64_t h2d_bytes;        /* host→device bytes this call copied     */
   int64_t d2h_bytes;        /* device→host bytes this call copied     */
+  int64_t tiles_evaluated[2]; /* E-step tile pairs computed since the
+                                 session began (pass 1, pass 2); the rest
+                                 were culled (≤ 2^-50 of any total)     */
 } fcpd_result;
 
 typedef struct fcpd_ctx fcpd_ctx;

@@ -105,7 +105,8 @@ class _Result(C.Structure):
                 ("iterations_run", C.c_int32), ("basis_reused", C.c_int32),
                 ("sigma2_initial", C.c_double), ("degenerate_rows", C.c_int64),
                 ("sigma2_clamps", C.c_int64), ("timing", _Timing),
-                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+                ("tiles_evaluated", C.c_int64 * 2)]
 
 
 _lib = None

@@ -192,6 +192,14 @@ struct Session {
   EStepPlan ep;
   ColsumPlan zp, vp;
   cudaGraphExec_t graph = nullptr;
+  // spatial order (sorted → original index) and tile-culling buffers
+  std::vector<int64_t> perm_x, perm_y;
+  bool cull = true;
+  DevBuf<float4> xlo, xhi, ylo, yhi;
+  DevBuf<float> col_bound, row_bound;
+  DevBuf<float2> bminmax;
+  DevBuf<unsigned long long> cull_counters;  // tiles evaluated (pass 1, pass 2), cumulative
+
   // overlapped graph form: pass-2 row chunks ∥ chunked Qᵀ·R stream
   int chunks = 1;
   ColsumPlan zpc[kMaxRowChunks];
@@ -228,6 +236,11 @@ struct Session {
     mask_all.release();
     fmax_all.release();
     qt_own.release();
+    for (auto* b : {&xlo, &xhi, &ylo, &yhi}) b->release();
+    col_bound.release();
+    row_bound.release();
+    bminmax.release();
+    cull_counters.release();
     for (auto& e : ev_chunk)
       if (e) cudaEventDestroy(e), e = nullptr;
     if (ev_join) cudaEventDestroy(ev_join), ev_join = nullptr;
@@ -377,6 +390,28 @@ void ensure_basis(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa) {
   b.t_eig = s.t_eig;
 }
 
+// Wire the session's culling geometry into the E-step buffers.  margin =
+// 50 + log2(count) log2-units: skipped mass ≤ 2^-50 of any column/row total.
+void set_cull(Session& s, EStepBuffers& eb, int64_t m, int64_t n_local, int64_t n_global) {
+  CullInfo& c = eb.cull;
+  c.enabled = s.cull && s.xlo.p && s.ylo.p ? 1 : 0;
+  c.n_xtiles = ceil_div(m, 256);
+  c.n_ytiles = ceil_div(n_local, 256);
+  c.xlo = s.xlo.p;
+  c.xhi = s.xhi.p;
+  c.ylo = s.ylo.p;
+  c.yhi = s.yhi.p;
+  c.col_bound = s.col_bound.p;
+  c.row_bound = s.row_bound.p;
+  c.bminmax = s.bminmax.p;
+  c.margin1 = 50.f + static_cast<float>(std::log2(static_cast<double>(std::max<int64_t>(m, 1))));
+  c.margin2 =
+      50.f + static_cast<float>(std::log2(static_cast<double>(std::max<int64_t>(n_global, 1))));
+  c.counters = s.cull_counters.p;
+  eb.cullw = CullBuffers{s.xlo.p, s.xhi.p, s.ylo.p, s.yhi.p, s.col_bound.p, s.row_bound.p,
+                         s.bminmax.p};
+}
+
 // ev (optional, 7 events): recorded before the iteration and after each of
 // pass 1, pass 2, Qᵀ·R, z-reduce/filter, Q·g, transform/σ² (eager profiling).
 void enqueue_iteration(fcpd_ctx* ctx, Session& s, cudaEvent_t* ev = nullptr) {
@@ -396,6 +431,7 @@ void enqueue_iteration(fcpd_ctx* ctx, Session& s, cudaEvent_t* ev = nullptr) {
   eb.flags_count = s.flags_count.p;
   eb.out = RowOut{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p, s.resid4.p, s.x0.p};
   eb.ystats = s.ystats;
+  set_cull(s, eb, s.m, s.n, s.dist ? s.n_global : s.n);
   auto rec = [&](int i) {
     if (ev) FCPD_CUDA(cudaEventRecord(ev[i], str));
   };
@@ -439,6 +475,7 @@ void enqueue_iteration_overlap(fcpd_ctx* ctx, Session& s) {
   eb.flags_count = s.flags_count.p;
   eb.out = RowOut{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p, s.resid4.p, s.x0.p};
   eb.ystats = s.ystats;
+  set_cull(s, eb, s.m, s.n, s.dist ? s.n_global : s.n);
   launch_estep_prologue(st, s.m, s.n, s.d, s.cfg.omega, s.flags_count.p, s.stamps.p, str);
   launch_estep_pass1(s.ep, eb, s.m, s.n, st, str);
   const double* parts[kMaxRowChunks];
@@ -528,6 +565,21 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
   ys.sq_mean = sq / static_cast<double>(n);
   s.ystats = ys;
 
+  // tile-culling geometry: scene tiles are fixed for the session
+  s.cull = true;
+  if (const char* e = std::getenv("FCPD_CULL")) s.cull = std::atoi(e) != 0;
+  const int64_t nxt = ceil_div(m, 256), nyt = ceil_div(n, 256);
+  s.xlo.ensure(nxt);
+  s.xhi.ensure(nxt);
+  s.ylo.ensure(nyt);
+  s.yhi.ensure(nyt);
+  s.bminmax.ensure(nyt);
+  s.col_bound.ensure(s.ep.col_blocks);
+  s.row_bound.ensure(s.ep.row_blocks);
+  s.cull_counters.ensure(2);
+  FCPD_CUDA(cudaMemsetAsync(s.cull_counters.p, 0, 2 * sizeof(unsigned long long), str));
+  launch_tile_bbox(s.y4b.p, n, s.ylo.p, s.yhi.p, nullptr, str);
+
   if (need_mstep) {
     Basis& b = ctx->basis;
     s.zp = make_colsum_plan(m, b.k, ctx->sm_count);
@@ -599,6 +651,54 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
                         int d, const fcpd_config& cfg);
 void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall);
 
+// ---- spatial (Morton / Z-order) sort: makes 256-point tiles compact boxes
+// for the E-step's tile culling.  The order depends only on the point set
+// itself (its own bounding box), is deterministic (ties by index), and is
+// undone on every output.
+uint64_t morton_spread21(uint64_t v) {
+  v &= 0x1fffffull;
+  v = (v | v << 32) & 0x1f00000000ffffull;
+  v = (v | v << 16) & 0x1f0000ff0000ffull;
+  v = (v | v << 8) & 0x100f00f00f00f00full;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+  v = (v | v << 2) & 0x1249249249249249ull;
+  return v;
+}
+
+// perm[k] = original index of sorted position k; soa (SoA 3×cnt) is permuted.
+std::vector<int64_t> morton_sort(std::vector<double>& soa, int64_t cnt) {
+  double lo[3], hi[3];
+  for (int c = 0; c < 3; ++c) {
+    lo[c] = INFINITY;
+    hi[c] = -INFINITY;
+    for (int64_t i = 0; i < cnt; ++i) {
+      lo[c] = std::min(lo[c], soa[c * cnt + i]);
+      hi[c] = std::max(hi[c], soa[c * cnt + i]);
+    }
+  }
+  double span = 0.0;
+  for (int c = 0; c < 3; ++c) span = std::max(span, hi[c] - lo[c]);
+  const double q = span > 0.0 ? 2097151.0 / span : 0.0;
+  std::vector<std::pair<uint64_t, int64_t>> keys(cnt);
+  for (int64_t i = 0; i < cnt; ++i) {
+    uint64_t key = 0;
+    for (int c = 0; c < 3; ++c) {
+      const uint64_t v = static_cast<uint64_t>((soa[c * cnt + i] - lo[c]) * q);
+      key |= morton_spread21(v) << c;
+    }
+    keys[i] = {key, i};
+  }
+  std::sort(keys.begin(), keys.end());
+  std::vector<int64_t> perm(cnt);
+  std::vector<double> out(soa.size());
+  for (int64_t k = 0; k < cnt; ++k) {
+    perm[k] = keys[k].second;
+    for (int c = 0; c < 3; ++c) out[c * cnt + k] = soa[c * cnt + perm[k]];
+  }
+  soa.swap(out);
+  return perm;
+}
+
 // normalize_pair (pointset.hpp:124-148), fp64 on the host, O(M+N); outputs
 // fp64 SoA(3) copies (unused coordinates zero).
 void normalize_pair_host(const double* x, int64_t m, const double* y, int64_t n, int d,
@@ -653,11 +753,15 @@ void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, i
   s.cfg = cfg;
   std::vector<double> xs, ys;
   normalize_pair_host(x, m, y, n, d, cfg.normalize != 0, xs, ys, s.center, &s.scale);
+  // internal order: Morton-sorted model and scene (undone on output)
+  s.perm_x = morton_sort(xs, m);
+  s.perm_y = morton_sort(ys, n);
   // x0 must be on the device before the Gram build
   s.x0.ensure(3 * m);
   FCPD_CUDA(cudaMemcpyAsync(s.x0.p, xs.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice,
                             ctx->stream));
   ensure_basis(ctx, s, xs);
+  ctx->basis.perm = s.perm_x;  // basis rows are in the session's sorted order
   prepare_buffers(ctx, s, xs, ys, cfg.iterations, true);
   s.sigma2_initial = init_sigma2_host(xs, m, ys, n, d);
   if (cfg.iterations > 0 && !(cfg.omega >= 0.0 && cfg.omega < 1.0))
@@ -735,14 +839,21 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
   s.d2h += sizeof(double) * (run + 3 * m);
   std::vector<double> xt(3 * m);
   FCPD_CUDA(cudaMemcpyAsync(xt.data(), s.xt64.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, str));
+  // internal rows are Morton-sorted: sorted row k is original row perm_x[k]
+  const std::vector<int64_t>& px = s.perm_x;
+  const std::vector<int64_t>& py = s.perm_y;
   if (out->coefficients) {
     // W = Q c (the last iteration's coefficients): one more Qᵀ-row stream
     pack_coef_kernel<<<ceil_div(b.k, 256), 256, 0, str>>>(s.coef.p, b.k, s.g4.p);
     FCPD_LAUNCH_CHECK();
     launch_colsum(s.vp, b.qt, b.mpad, s.g4.p, s.vpart.p, nullptr, nullptr, 0, str);
     launch_vreduce_add(s.vp, s.vpart.p, nullptr, d, s.ptilde_y.p, str);
-    FCPD_CUDA(cudaMemcpyAsync(out->coefficients, s.ptilde_y.p, sizeof(double) * d * m,
+    std::vector<double> w(static_cast<size_t>(d) * m);
+    FCPD_CUDA(cudaMemcpyAsync(w.data(), s.ptilde_y.p, sizeof(double) * d * m,
                               cudaMemcpyDeviceToHost, str));
+    FCPD_CUDA(cudaStreamSynchronize(str));
+    for (int c = 0; c < d; ++c)
+      for (int64_t k = 0; k < m; ++k) out->coefficients[c * m + px[k]] = w[c * m + k];
     s.d2h += sizeof(double) * d * m;
   }
   if (out->correspondence && run > 0) {
@@ -753,28 +864,40 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
     deg.ensure(m);
     launch_dense_posterior(s.xt_prev.p, m, s.y64.p, n, d, s.cfg.omega, s.st.p, 1, deg.p, p.p,
                            str);
-    FCPD_CUDA(cudaMemcpyAsync(out->correspondence, p.p, sizeof(double) * m * n,
-                              cudaMemcpyDeviceToHost, str));
+    std::vector<double> ps(static_cast<size_t>(m) * n);
+    FCPD_CUDA(cudaMemcpyAsync(ps.data(), p.p, sizeof(double) * m * n, cudaMemcpyDeviceToHost,
+                              str));
     s.d2h += sizeof(double) * m * n;
     FCPD_CUDA(cudaStreamSynchronize(str));
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t k = 0; k < m; ++k) out->correspondence[py[j] * m + px[k]] = ps[j * m + k];
     p.release();
     deg.release();
   }
-  if (out->degenerate_mask)
-    FCPD_CUDA(cudaMemcpyAsync(out->degenerate_mask, s.degenerate.p, sizeof(int32_t) * m,
+  std::vector<int32_t> degm(out->degenerate_mask ? m : 0);
+  if (out->degenerate_mask) {
+    FCPD_CUDA(cudaMemcpyAsync(degm.data(), s.degenerate.p, sizeof(int32_t) * m,
                               cudaMemcpyDeviceToHost, str));
-  if (out->degenerate_mask) s.d2h += sizeof(int32_t) * m;
+    s.d2h += sizeof(int32_t) * m;
+  }
   std::vector<uint64_t> stamps(4 * static_cast<size_t>(std::max(run, 1)));
   if (run > 0)
     FCPD_CUDA(cudaMemcpyAsync(stamps.data(), s.stamps.p, sizeof(uint64_t) * 4 * run,
                               cudaMemcpyDeviceToHost, str));
   s.d2h += sizeof(uint64_t) * 4 * run;
+  unsigned long long tiles[2] = {0, 0};
+  if (s.cull_counters.p)
+    FCPD_CUDA(cudaMemcpyAsync(tiles, s.cull_counters.p, sizeof tiles, cudaMemcpyDeviceToHost, str));
   FCPD_CUDA(cudaStreamSynchronize(str));
+  out->tiles_evaluated[0] = static_cast<int64_t>(tiles[0]);
+  out->tiles_evaluated[1] = static_cast<int64_t>(tiles[1]);
+  if (out->degenerate_mask)
+    for (int64_t k = 0; k < m; ++k) out->degenerate_mask[px[k]] = degm[k];
   if (out->transformed) {
     for (int c = 0; c < d; ++c)
-      for (int64_t i = 0; i < m; ++i)
-        out->transformed[c * m + i] =
-            s.cfg.normalize ? xt[c * m + i] * s.scale + s.center[c] : xt[c * m + i];
+      for (int64_t k = 0; k < m; ++k)
+        out->transformed[c * m + px[k]] =
+            s.cfg.normalize ? xt[c * m + k] * s.scale + s.center[c] : xt[c * m + k];
   }
   // phases (registration.hpp:120-147): t_c = E-step; t_iter = residual +
   // solve (Qᵀ R, filter, Q g); t_o = transform epilogue + σ² + everything else
@@ -827,6 +950,7 @@ void enqueue_iteration_dist(fcpd_ctx* ctx, Session& s) {
   eb.row_flags = s.row_flags.p;
   eb.flags_count = s.flags_count.p;
   eb.ystats = s.ystats;
+  set_cull(s, eb, s.m, s.n, s.dist ? s.n_global : s.n);
   launch_estep_prologue(st, m, s.n_global, s.d, s.cfg.omega, s.flags_count.p, s.stamps.p, str);
   launch_estep_pass1(s.ep, eb, m, nl, st, str);  // column-local: no communication
   launch_estep_pass2_partials(s.ep, eb, m, nl, st, str);
@@ -935,10 +1059,15 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
     s.sigma2_initial =
         std::max((md * ystat[3] + ng * fx - 2.0 * dot) / (static_cast<double>(d) * md * ng), 0.0);
   }
+  // internal spatial order: the full model (identical on all ranks) and the
+  // local scene shard are Morton-sorted; row shards are spatial slabs
+  s.perm_x = morton_sort(xs, m);
+  s.perm_y = morton_sort(ys, n);
   // spectral basis (computed redundantly per rank; each keeps its row shard)
   s.x0.ensure(3 * m);
   FCPD_CUDA(cudaMemcpyAsync(s.x0.p, xs.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, str));
   ensure_basis(ctx, s, xs);
+  ctx->basis.perm = s.perm_x;  // basis rows are in the session's sorted order
   Basis& b = ctx->basis;
   // shard geometry
   s.mr = (m + G - 1) / G;
@@ -993,6 +1122,19 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
   s.mask_own.ensure(mr);
   s.mask_all.ensure(s.m_pad);
   s.fmax_all.ensure(s.m_pad);
+  // tile-culling geometry (model tiles over all M rows; local scene tiles)
+  s.cull = true;
+  if (const char* e = std::getenv("FCPD_CULL")) s.cull = std::atoi(e) != 0;
+  s.xlo.ensure(ceil_div(m, 256));
+  s.xhi.ensure(ceil_div(m, 256));
+  s.ylo.ensure(ceil_div(n, 256));
+  s.yhi.ensure(ceil_div(n, 256));
+  s.bminmax.ensure(ceil_div(n, 256));
+  s.col_bound.ensure(s.ep.col_blocks);
+  s.row_bound.ensure(s.ep.row_blocks);
+  s.cull_counters.ensure(2);
+  FCPD_CUDA(cudaMemsetAsync(s.cull_counters.p, 0, 2 * sizeof(unsigned long long), str));
+  launch_tile_bbox(s.y4b.p, n, s.ylo.p, s.yhi.p, nullptr, str);
   // basis shard: Q rows [m0, m0+m_valid) in place; Qᵀ columns copied compact
   s.qt_own.ensure(static_cast<size_t>(b.k) * s.mr4);
   FCPD_CUDA(cudaMemsetAsync(s.qt_own.p, 0, sizeof(float) * b.k * s.mr4, str));
@@ -1090,11 +1232,12 @@ void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall) {
                               cudaMemcpyDeviceToHost, str));
   std::vector<double> xt(3 * s.m, 0.0);
   gather_rows(ctx, s, s.xt64.p, xt.data(), 3);
+  const std::vector<int64_t>& px = s.perm_x;  // sorted row k ↔ original row px[k]
   if (out->transformed)
     for (int c = 0; c < d; ++c)
-      for (int64_t i = 0; i < s.m; ++i)
-        out->transformed[c * s.m + i] =
-            s.cfg.normalize ? xt[c * s.m + i] * s.scale + s.center[c] : xt[c * s.m + i];
+      for (int64_t k = 0; k < s.m; ++k)
+        out->transformed[c * s.m + px[k]] =
+            s.cfg.normalize ? xt[c * s.m + k] * s.scale + s.center[c] : xt[c * s.m + k];
   if (out->coefficients) {
     pack_coef_kernel<<<ceil_div(b.k, 256), 256, 0, str>>>(s.coef.p, b.k, s.g4.p);
     FCPD_LAUNCH_CHECK();
@@ -1102,7 +1245,8 @@ void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall) {
     launch_vreduce_add(s.vp, s.vpart.p, nullptr, 3, s.ptilde_y.p, str);
     std::vector<double> w(3 * s.m, 0.0);
     gather_rows(ctx, s, s.ptilde_y.p, w.data(), 3);
-    std::memcpy(out->coefficients, w.data(), sizeof(double) * d * s.m);
+    for (int c = 0; c < d; ++c)
+      for (int64_t k = 0; k < s.m; ++k) out->coefficients[c * s.m + px[k]] = w[c * s.m + k];
   }
   std::vector<uint64_t> stamps(4 * static_cast<size_t>(std::max(run, 1)));
   if (run > 0)
@@ -1313,6 +1457,9 @@ int fcpd_estep(fcpd_ctx* ctx, const double* xt, int64_t m, const double* y, int6
       std::memcpy(&xs[c * m], xt + c * m, sizeof(double) * m);
       std::memcpy(&ys[c * n], y + c * n, sizeof(double) * n);
     }
+    s.dist = false;
+    s.perm_x = morton_sort(xs, m);  // internal spatial order (tile culling)
+    s.perm_y = morton_sort(ys, n);
     prepare_buffers(ctx, s, xs, ys, 1, false);
     reset_state(ctx, s, sigma2);
     EStepBuffers eb{};
@@ -1328,17 +1475,29 @@ int fcpd_estep(fcpd_ctx* ctx, const double* xt, int64_t m, const double* y, int6
     eb.flags_count = s.flags_count.p;
     eb.out = RowOut{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p, nullptr, nullptr};
     eb.ystats = s.ystats;
+  set_cull(s, eb, s.m, s.n, s.dist ? s.n_global : s.n);
     launch_estep(s.ep, eb, m, n, d, omega, s.st.p, nullptr, ctx->stream);
-    std::vector<double> pty(3 * m), lp(m);
-    FCPD_CUDA(cudaMemcpyAsync(pty.data(), s.ptilde_y.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, ctx->stream));
-    FCPD_CUDA(cudaMemcpyAsync(lp.data(), s.log2p1.p, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
-    if (var) FCPD_CUDA(cudaMemcpyAsync(var, s.var.p, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
-    if (degenerate) FCPD_CUDA(cudaMemcpyAsync(degenerate, s.degenerate.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
-    if (pt1) FCPD_CUDA(cudaMemcpyAsync(pt1, s.pt1.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
-    FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (ptilde_y) std::memcpy(ptilde_y, pty.data(), sizeof(double) * d * m);
-    if (p1)
-      for (int64_t i = 0; i < m; ++i) p1[i] = std::exp2(lp[i]);
+    std::vector<double> pty(3 * m), lp(m), vr(m), pc(n);
+    std::vector<int32_t> dg(m);
+    cudaStream_t str = ctx->stream;
+    FCPD_CUDA(cudaMemcpyAsync(pty.data(), s.ptilde_y.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, str));
+    FCPD_CUDA(cudaMemcpyAsync(lp.data(), s.log2p1.p, sizeof(double) * m, cudaMemcpyDeviceToHost, str));
+    FCPD_CUDA(cudaMemcpyAsync(vr.data(), s.var.p, sizeof(double) * m, cudaMemcpyDeviceToHost, str));
+    FCPD_CUDA(cudaMemcpyAsync(dg.data(), s.degenerate.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, str));
+    FCPD_CUDA(cudaMemcpyAsync(pc.data(), s.pt1.p, sizeof(double) * n, cudaMemcpyDeviceToHost, str));
+    FCPD_CUDA(cudaStreamSynchronize(str));
+    // undo the spatial order: sorted row k ↔ original row perm_x[k]
+    const std::vector<int64_t>& px = s.perm_x;
+    for (int64_t k = 0; k < m; ++k) {
+      const int64_t i = px[k];
+      if (ptilde_y)
+        for (int c = 0; c < d; ++c) ptilde_y[c * m + i] = pty[c * m + k];
+      if (p1) p1[i] = std::exp2(lp[k]);
+      if (var) var[i] = vr[k];
+      if (degenerate) degenerate[i] = dg[k];
+    }
+    if (pt1)
+      for (int64_t j = 0; j < n; ++j) pt1[s.perm_y[j]] = pc[j];
     if (clamped) *clamped = sigma2 < kSigma2Floor ? 1 : 0;
   });
 }
@@ -1443,9 +1602,12 @@ int fcpd_save_spectral_cache(fcpd_ctx* ctx, const char* path) {
     bool ok = std::fwrite("FCPD", 1, 4, f) == 4 && std::fwrite(&ver, 4, 1, f) == 1 &&
               std::fwrite(&mm, 8, 1, f) == 1 && std::fwrite(&kk, 8, 1, f) == 1 &&
               std::fwrite(&b.key_beta, 8, 1, f) == 1;
+    // rows in the caller's point order (the device keeps them Morton-sorted)
+    std::vector<int64_t> inv(b.m);
+    for (int64_t k = 0; k < b.m; ++k) inv[b.perm.empty() ? k : b.perm[k]] = k;
     std::vector<double> row(b.k);
     for (int64_t i = 0; ok && i < b.m; ++i) {
-      for (int64_t j = 0; j < b.k; ++j) row[j] = u[j * b.m + i];
+      for (int64_t j = 0; j < b.k; ++j) row[j] = u[j * b.m + inv[i]];
       ok = std::fwrite(row.data(), 8, b.k, f) == static_cast<size_t>(b.k);
     }
     ok = ok && std::fwrite(b.lam_host.data(), 8, b.k, f) == static_cast<size_t>(b.k);
@@ -1495,11 +1657,16 @@ int fcpd_load_spectral_cache(fcpd_ctx* ctx, const char* path, const double* x, i
     std::vector<double> xs, ys;
     double center[3], scale;
     normalize_pair_host(x, m, y, n, d, cfg->normalize != 0, xs, ys, center, &scale);
+    std::vector<int64_t> perm = morton_sort(xs, m);  // the order register will use
     uint64_t h = fnv1a(xs.data(), sizeof(double) * xs.size());
     h = fnv1a(&m, sizeof m, h);
     h = fnv1a(&rank, sizeof rank, h);
+    std::vector<double> us(u.size());
+    for (int64_t j = 0; j < rank; ++j)
+      for (int64_t k = 0; k < m; ++k) us[j * m + k] = u[j * m + perm[k]];
     Basis& b = ctx->basis;
-    basis_from_host(b, u.data(), lam.data(), m, rank, ctx->stream);
+    basis_from_host(b, us.data(), lam.data(), m, rank, ctx->stream);
+    b.perm = perm;
     upload_lambda(b, !lowrank, ctx->stream);  // cached λ are the clamped ones
     b.key_hash = h;
     b.key_beta = cfg->beta;

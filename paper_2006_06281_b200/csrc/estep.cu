@@ -56,6 +56,29 @@ __device__ __forceinline__ double derived_scale(const IterState* st) {
   return sqrt(kLog2e / (2.0 * st->sigma2_e));
 }
 
+__device__ __forceinline__ float4 box_min(float4 a, float4 b) {
+  return make_float4(fminf(a.x, b.x), fminf(a.y, b.y), fminf(a.z, b.z), 0.f);
+}
+__device__ __forceinline__ float4 box_max(float4 a, float4 b) {
+  return make_float4(fmaxf(a.x, b.x), fmaxf(a.y, b.y), fmaxf(a.z, b.z), 0.f);
+}
+// smallest squared distance between two boxes (0 if they overlap)
+__device__ __forceinline__ float box_mindist2(float4 alo, float4 ahi, float4 blo, float4 bhi) {
+  const float dx = fmaxf(0.f, fmaxf(alo.x - bhi.x, blo.x - ahi.x));
+  const float dy = fmaxf(0.f, fmaxf(alo.y - bhi.y, blo.y - ahi.y));
+  const float dz = fmaxf(0.f, fmaxf(alo.z - bhi.z, blo.z - ahi.z));
+  // shrink by one part in 2^20: fp32 rounding of the bound never culls a pair
+  // the exact geometry would keep
+  return (dx * dx + dy * dy + dz * dz) * (1.f - 0x1p-20f);
+}
+// largest squared distance between points of two boxes
+__device__ __forceinline__ float box_maxdist2(float4 alo, float4 ahi, float4 blo, float4 bhi) {
+  const float dx = fmaxf(ahi.x - blo.x, bhi.x - alo.x);
+  const float dy = fmaxf(ahi.y - blo.y, bhi.y - alo.y);
+  const float dz = fmaxf(ahi.z - blo.z, bhi.z - alo.z);
+  return (dx * dx + dy * dy + dz * dz) * (1.f + 0x1p-20f);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -96,11 +119,26 @@ template <int CP>
 __global__ void __launch_bounds__(128)
     estep_col_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4,
                      int64_t n, int64_t m_per_split, const IterState* __restrict__ st,
-                     double* __restrict__ part) {
+                     double* __restrict__ part, CullInfo cull) {
   if (!st->active) return;
   __shared__ float4 xa[kTile];  // (−x, −x, −y, −y)
   __shared__ float2 xb[kTile];  // (−z, −z)
   const float s = st->sx;
+  const float s2 = s * s;
+  // tile culling: this CTA's 512 columns vs each 256-point model tile
+  float4 blo = make_float4(0.f, 0.f, 0.f, 0.f), bhi = blo;
+  float cut = INFINITY;
+  if (cull.enabled) {
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * 2;
+    blo = cull.ylo[t0];
+    bhi = cull.yhi[t0];
+    if (t0 + 1 < cull.n_ytiles) {
+      blo = box_min(blo, cull.ylo[t0 + 1]);
+      bhi = box_max(bhi, cull.yhi[t0 + 1]);
+    }
+    cut = s2 * cull.col_bound[blockIdx.x] + cull.margin1;
+  }
+  int evaluated = 0;
   // column pair p of this thread: cols c, c+1 with c = base + p·256 + 2·tid
   const int64_t cbase = static_cast<int64_t>(blockIdx.x) * (256 * CP) + 2 * threadIdx.x;
   float2 yx[CP], yy[CP], yz[CP];
@@ -121,6 +159,11 @@ __global__ void __launch_bounds__(128)
 
   for (int64_t base = m_begin; base < m_end; base += kTile) {
     const int cnt = static_cast<int>(min(static_cast<int64_t>(kTile), m_end - base));
+    if (cull.enabled) {  // uniform across the CTA (same data, same math)
+      const int64_t tj = base / kTile;  // m_per_split is a multiple of kTile
+      if (s2 * box_mindist2(blo, bhi, cull.xlo[tj], cull.xhi[tj]) > cut) continue;
+    }
+    ++evaluated;
     __syncthreads();
     for (int i = threadIdx.x; i < kTile; i += 128) {
       const float4 v = i < cnt ? scale_pt(xt4[base + i], s)
@@ -164,6 +207,7 @@ __global__ void __launch_bounds__(128)
     if (c < n) out[c] = dsum[p][0];
     if (c + 1 < n) out[c + 1] = dsum[p][1];
   }
+  if (cull.counters && threadIdx.x == 0) atomicAdd(cull.counters, (unsigned long long)evaluated);
 }
 
 // Pass 1 combine: fixed-order sum over splits; column normaliser b_n.
@@ -251,13 +295,30 @@ template <int RP>
 __global__ void __launch_bounds__(128)
     estep_row_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4b,
                      int64_t n, int64_t n_per_split, const IterState* __restrict__ st,
-                     double* __restrict__ part /* [split][5][m] */, int rb_offset) {
+                     double* __restrict__ part /* [split][5][m] */, int rb_offset,
+                     CullInfo cull) {
   if (!st->active) return;
   __shared__ float4 ya[kTile];  // (yx, yx, yy, yy)
   __shared__ float4 yb[kTile];  // (yz, yz, b, b)
   const float s = st->sx;
+  const float s2 = s * s;
   const int64_t rbase =
       static_cast<int64_t>(blockIdx.x + rb_offset) * (256 * RP) + 2 * threadIdx.x;
+  // tile culling: this CTA's 512 model rows vs each 256-point scene tile
+  float4 blo = make_float4(0.f, 0.f, 0.f, 0.f), bhi = blo;
+  float floor_l = -INFINITY;
+  if (cull.enabled) {
+    const int64_t rb = blockIdx.x + rb_offset;
+    const int64_t t0 = rb * 2;
+    blo = cull.xlo[t0];
+    bhi = cull.xhi[t0];
+    if (t0 + 1 < cull.n_xtiles) {
+      blo = box_min(blo, cull.xlo[t0 + 1]);
+      bhi = box_max(bhi, cull.xhi[t0 + 1]);
+    }
+    floor_l = cull.row_bound[rb] - cull.margin2;
+  }
+  int evaluated = 0;
   float2 nx[RP], ny[RP], nz[RP];
 #pragma unroll
   for (int p = 0; p < RP; ++p) {
@@ -283,6 +344,12 @@ __global__ void __launch_bounds__(128)
 
   for (int64_t base = n_begin; base < n_end; base += kTile) {
     const int cnt = static_cast<int>(min(static_cast<int64_t>(kTile), n_end - base));
+    if (cull.enabled) {  // L ≤ bmax − s²·mindist² < (row-max lower bound) − margin → skip
+      const int64_t tj = base / kTile;  // n_per_split is a multiple of kTile
+      const float lub = cull.bminmax[tj].y - s2 * box_mindist2(blo, bhi, cull.ylo[tj], cull.yhi[tj]);
+      if (lub < floor_l) continue;
+    }
+    ++evaluated;
     __syncthreads();
     for (int i = threadIdx.x; i < kTile; i += 128) {
       // padding column: far away and b = −inf → weight exactly 0
@@ -348,6 +415,125 @@ __global__ void __launch_bounds__(128)
         for (int k = 0; k < 5; ++k) part[sp + k * m + row] = acc_s[k][2 * p + h][threadIdx.x];
       }
     }
+  if (cull.counters && threadIdx.x == 0)
+    atomicAdd(cull.counters + 1, (unsigned long long)evaluated);
+}
+
+// ---------------------------------------------------------------------------
+// Tile geometry for culling (points are Morton-sorted by the engine, so
+// 256-point tiles are spatially compact).
+
+// per-tile axis-aligned box of the first three coordinates (unscaled)
+__global__ void tile_bbox_kernel(const float4* __restrict__ p, int64_t count,
+                                 float4* __restrict__ lo, float4* __restrict__ hi,
+                                 const IterState* __restrict__ st) {
+  if (st && !st->active) return;
+  __shared__ float red[6][8];
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kTile + threadIdx.x;
+  float v[6];
+  if (i < count) {
+    const float4 q = p[i];
+    v[0] = v[3] = q.x;
+    v[1] = v[4] = q.y;
+    v[2] = v[5] = q.z;
+  } else {
+    v[0] = v[1] = v[2] = INFINITY;
+    v[3] = v[4] = v[5] = -INFINITY;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const float w = __shfl_xor_sync(0xffffffffu, v[k], o);
+      v[k] = k < 3 ? fminf(v[k], w) : fmaxf(v[k], w);
+    }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int k = 0; k < 6; ++k) red[k][warp] = v[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float r[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) r[k] = red[k][0];
+    for (int w = 1; w < kTile / 32; ++w)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) r[k] = k < 3 ? fminf(r[k], red[k][w]) : fmaxf(r[k], red[k][w]);
+    lo[blockIdx.x] = make_float4(r[0], r[1], r[2], 0.f);
+    hi[blockIdx.x] = make_float4(r[3], r[4], r[5], 0.f);
+  }
+}
+
+// per scene tile: (min b_n, max b_n) after pass 1
+__global__ void tile_bminmax_kernel(const float4* __restrict__ y4b, int64_t n,
+                                    float2* __restrict__ out, const IterState* __restrict__ st) {
+  if (!st->active) return;
+  __shared__ float red[2][8];
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kTile + threadIdx.x;
+  float mn = INFINITY, mx = -INFINITY;
+  if (i < n) mn = mx = y4b[i].w;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = mn;
+    red[1][threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kTile / 32; ++w) {
+      mn = fminf(red[0][0], red[0][w]);
+      mx = fmaxf(red[1][0], red[1][w]);
+      red[0][0] = mn;
+      red[1][0] = mx;
+    }
+    out[blockIdx.x] = make_float2(red[0][0], red[1][0]);
+  }
+}
+
+// pass-1 bound per 512-column block: U = min over model tiles of the largest
+// possible squared distance → every column has t_min ≤ s²·U.
+__global__ void col_bound_kernel(CullInfo cull, float* __restrict__ out, int n_blocks,
+                                 const IterState* __restrict__ st) {
+  if (!st->active) return;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= n_blocks) return;
+  float4 lo = cull.ylo[2 * b], hi = cull.yhi[2 * b];
+  if (2 * b + 1 < cull.n_ytiles) {
+    lo = box_min(lo, cull.ylo[2 * b + 1]);
+    hi = box_max(hi, cull.yhi[2 * b + 1]);
+  }
+  float u = INFINITY;
+  for (int j = lane; j < cull.n_xtiles; j += 32)
+    u = fminf(u, box_maxdist2(lo, hi, cull.xlo[j], cull.xhi[j]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
+  if (lane == 0) out[b] = u;
+}
+
+// pass-2 bound per 512-row block: a lower bound on max_n L_mn for every row,
+// L_lb = max over scene tiles of (min b − s²·maxdist²).
+__global__ void row_bound_kernel(CullInfo cull, float* __restrict__ out, int n_blocks,
+                                 const IterState* __restrict__ st) {
+  if (!st->active) return;
+  const float s2 = st->sx * st->sx;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= n_blocks) return;
+  float4 lo = cull.xlo[2 * b], hi = cull.xhi[2 * b];
+  if (2 * b + 1 < cull.n_xtiles) {
+    lo = box_min(lo, cull.xlo[2 * b + 1]);
+    hi = box_max(hi, cull.xhi[2 * b + 1]);
+  }
+  float l = -INFINITY;
+  for (int j = lane; j < cull.n_ytiles; j += 32)
+    l = fmaxf(l, cull.bminmax[j].x - s2 * box_maxdist2(lo, hi, cull.ylo[j], cull.yhi[j]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) l = fmaxf(l, __shfl_xor_sync(0xffffffffu, l, o));
+  if (lane == 0) out[b] = l;
 }
 
 // Row finalisation shared by the combine and the fallback.
@@ -513,11 +699,12 @@ EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
       &occ_row, estep_row_kernel<kRowsPerThread / 2>, 128, 0));
   p.col_blocks = ceil_div(n, 128 * kColsPerThread);
   const int s1 = choose_splits(p.col_blocks, m, sm_count * std::max(occ_col, 1));
-  p.m_per_split = ceil_div(m, s1);
+  // splits on 256-point tile boundaries (culling tests whole tiles)
+  p.m_per_split = static_cast<int64_t>(ceil_div(ceil_div(m, s1), kTile)) * kTile;
   p.col_splits = ceil_div(m, p.m_per_split);
   p.row_blocks = ceil_div(m, 128 * kRowsPerThread);
   const int s2 = choose_splits(p.row_blocks, n, sm_count * std::max(occ_row, 1));
-  p.n_per_split = ceil_div(n, s2);
+  p.n_per_split = static_cast<int64_t>(ceil_div(ceil_div(n, s2), kTile)) * kTile;
   p.row_splits = ceil_div(n, p.n_per_split);
   p.chunks = 1;
   return p;
@@ -532,7 +719,7 @@ void plan_row_chunks(EStepPlan& p, int64_t m, int64_t n, int sm_count, int chunk
     const int rb = static_cast<int>(static_cast<int64_t>(p.row_blocks) * (c + 1) / chunks -
                                     static_cast<int64_t>(p.row_blocks) * c / chunks);
     const int s = choose_splits(std::max(rb, 1), n, sm_count * std::max(occ_row, 1));
-    p.chunk_nps[c] = ceil_div(n, s);
+    p.chunk_nps[c] = static_cast<int64_t>(ceil_div(ceil_div(n, s), kTile)) * kTile;
     p.chunk_splits[c] = ceil_div(n, p.chunk_nps[c]);
   }
 }
@@ -543,11 +730,27 @@ void launch_estep_prologue(IterState* st, int64_t m, int64_t n_global, int d, do
   FCPD_LAUNCH_CHECK();
 }
 
+void launch_tile_bbox(const float4* pts, int64_t count, float4* lo, float4* hi,
+                      const IterState* st, cudaStream_t stream) {
+  tile_bbox_kernel<<<ceil_div(count, kTile), kTile, 0, stream>>>(pts, count, lo, hi, st);
+  FCPD_LAUNCH_CHECK();
+}
+
+// Pass 1 (column normalisers) + the culling geometry around it: model-tile
+// boxes of this iteration's x̃ and the per-block bounds before, scene-tile
+// b ranges and row bounds after (pass 2 reads them).
 void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
                         IterState* st, cudaStream_t stream) {
+  const CullInfo& cu = b.cull;
+  if (cu.enabled) {
+    launch_tile_bbox(b.xt4, m, b.cullw.xlo, b.cullw.xhi, st, stream);
+    col_bound_kernel<<<ceil_div(p.col_blocks, 8), 256, 0, stream>>>(cu, b.cullw.col_bound,
+                                                                    p.col_blocks, st);
+    FCPD_LAUNCH_CHECK();
+  }
   estep_col_kernel<kColsPerThread / 2>
       <<<dim3(p.col_blocks, p.col_splits), 128, 0, stream>>>(b.xt4, m, b.y4b, n, p.m_per_split,
-                                                             st, b.col_part);
+                                                             st, b.col_part, cu);
   FCPD_LAUNCH_CHECK();
   estep_col_combine_kernel<<<ceil_div(n * kCombineLanes, 256), 256, 0, stream>>>(
       b.col_part, p.col_splits, m, n, b.y4b, b.b2, b.pt1, b.col_flags, b.flags_count, st);
@@ -555,13 +758,20 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
   estep_col_fallback_kernel<<<148, 256, 0, stream>>>(b.xt4, m, b.y4b, b.b2, b.pt1, b.col_flags,
                                                      b.flags_count, st);
   FCPD_LAUNCH_CHECK();
+  if (cu.enabled) {
+    tile_bminmax_kernel<<<ceil_div(n, kTile), kTile, 0, stream>>>(b.y4b, n, b.cullw.bminmax, st);
+    FCPD_LAUNCH_CHECK();
+    row_bound_kernel<<<ceil_div(p.row_blocks, 8), 256, 0, stream>>>(cu, b.cullw.row_bound,
+                                                                    p.row_blocks, st);
+    FCPD_LAUNCH_CHECK();
+  }
 }
 
 void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int64_t m,
                                  int64_t n, IterState* st, cudaStream_t stream) {
   estep_row_kernel<kRowsPerThread / 2>
       <<<dim3(p.row_blocks, p.row_splits), 128, 0, stream>>>(b.xt4, m, b.y4b, n, p.n_per_split,
-                                                             st, b.row_part, 0);
+                                                             st, b.row_part, 0, b.cull);
   FCPD_LAUNCH_CHECK();
 }
 
@@ -570,16 +780,7 @@ void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t 
                   cudaEvent_t mid) {
   estep_prologue_kernel<<<1, 1, 0, stream>>>(st, m, n, d, omega, b.flags_count, stamps);
   FCPD_LAUNCH_CHECK();
-  estep_col_kernel<kColsPerThread / 2>
-      <<<dim3(p.col_blocks, p.col_splits), 128, 0, stream>>>(b.xt4, m, b.y4b, n, p.m_per_split,
-                                                             st, b.col_part);
-  FCPD_LAUNCH_CHECK();
-  estep_col_combine_kernel<<<ceil_div(n * kCombineLanes, 256), 256, 0, stream>>>(
-      b.col_part, p.col_splits, m, n, b.y4b, b.b2, b.pt1, b.col_flags, b.flags_count, st);
-  FCPD_LAUNCH_CHECK();
-  estep_col_fallback_kernel<<<148, 256, 0, stream>>>(b.xt4, m, b.y4b, b.b2, b.pt1, b.col_flags,
-                                                     b.flags_count, st);
-  FCPD_LAUNCH_CHECK();
+  launch_estep_pass1(p, b, m, n, st, stream);
   if (mid) FCPD_CUDA(cudaEventRecord(mid, stream));
   launch_estep_pass2_chunk(p, b, m, n, st, stream, 0, 1);
 }
@@ -605,7 +806,7 @@ void launch_estep_pass2_chunk(const EStepPlan& p, const EStepBuffers& b, int64_t
   const int splits = own ? p.chunk_splits[c] : p.row_splits;
   const int64_t nps = own ? p.chunk_nps[c] : p.n_per_split;
   estep_row_kernel<kRowsPerThread / 2><<<dim3(rc.rb1 - rc.rb0, splits), 128, 0, stream>>>(
-      b.xt4, m, b.y4b, n, nps, st, b.row_part, rc.rb0);
+      b.xt4, m, b.y4b, n, nps, st, b.row_part, rc.rb0, b.cull);
   FCPD_LAUNCH_CHECK();
   int32_t* list = b.row_flags + rc.r0;
   int32_t* count = b.flags_count + 1 + c;

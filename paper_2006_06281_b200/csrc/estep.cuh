@@ -48,6 +48,31 @@ struct EStepPlan {
 };
 void plan_row_chunks(EStepPlan& p, int64_t m, int64_t n, int sm_count, int chunks);
 
+// Tile culling.  Points are Morton-sorted by the engine
+// so 256-point tiles are compact boxes; a (column block, model tile) or (row
+// block, scene tile) pair is skipped when every pair term in it is below
+// 2^-margin of the smallest possible column (row) total.  With margin =
+// 50 + log2(count) the skipped mass is ≤ 2^-50 relative: exact to fp32.
+struct CullInfo {
+  int enabled = 0;
+  int n_xtiles = 0, n_ytiles = 0;   // 256-point tiles
+  const float4* xlo = nullptr;      // model tiles (x̃ of this iteration)
+  const float4* xhi = nullptr;
+  const float4* ylo = nullptr;      // scene tiles (fixed)
+  const float4* yhi = nullptr;
+  const float* col_bound = nullptr; // per 512-column block: U (unscaled d²)
+  const float* row_bound = nullptr; // per 512-row block: lower bound of max L (log2)
+  const float2* bminmax = nullptr;  // per scene tile: (min b, max b)
+  float margin1 = 0.f, margin2 = 0.f;
+  unsigned long long* counters = nullptr;  // [0] pass-1 tiles, [1] pass-2 tiles evaluated
+};
+
+struct CullBuffers {  // writable views of the CullInfo arrays (engine-owned)
+  float4 *xlo, *xhi, *ylo, *yhi;
+  float *col_bound, *row_bound;
+  float2* bminmax;
+};
+
 struct EStepBuffers {
   const float4* xt4;   // x̃ fp32 (x,y,z,0), M
   const double* xt64;  // x̃ fp64 SoA M×3
@@ -61,7 +86,13 @@ struct EStepBuffers {
   int32_t* flags_count;  // 2
   RowOut out;
   YStats ystats;
+  CullInfo cull;      // cull.enabled = 0 → dense (every pair evaluated)
+  CullBuffers cullw;  // geometry buffers written each iteration
 };
+
+// Scene-tile boxes (once per session; Y does not move).
+void launch_tile_bbox(const float4* pts, int64_t count, float4* lo, float4* hi,
+                      const IterState* st, cudaStream_t stream);
 
 EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count);
 // Pieces of launch_estep for the distributed path (n = local scene count;

@@ -19,6 +19,7 @@ struct Basis {
   double* u64 = nullptr; // M×K column-major fp64 eigenvectors (descending), for export
   bool full_rank = false;
   std::vector<double> lam_raw_host, lam_host;
+  std::vector<int64_t> perm;  // basis row k ↔ original model point perm[k] (empty: identity)
   // cache key
   uint64_t key_hash = 0;
   double key_beta = 0.0;
