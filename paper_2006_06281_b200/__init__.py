@@ -344,7 +344,8 @@ class Context:
         self._check(lib().fcpd_session_read(self._h, C.byref(res)))
         return dict(transformed=None if out_x is None else np.ascontiguousarray(out_x),
                     sigma2_trace=trace[: res.iterations_run].copy(),
-                    iterations_run=res.iterations_run, degenerate_rows=res.degenerate_rows)
+                    iterations_run=res.iterations_run, degenerate_rows=res.degenerate_rows,
+                    tiles_evaluated=(int(res.tiles_evaluated[0]), int(res.tiles_evaluated[1])))
 
     @property
     def stream_ptr(self) -> int:

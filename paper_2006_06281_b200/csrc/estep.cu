@@ -125,17 +125,12 @@ __global__ void __launch_bounds__(128)
   __shared__ float2 xb[kTile];  // (−z, −z)
   const float s = st->sx;
   const float s2 = s * s;
-  // tile culling: this CTA's 512 columns vs each 256-point model tile
+  // tile culling: this CTA's 256 columns vs each 256-point model tile
   float4 blo = make_float4(0.f, 0.f, 0.f, 0.f), bhi = blo;
   float cut = INFINITY;
-  if (cull.enabled) {
-    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * 2;
-    blo = cull.ylo[t0];
-    bhi = cull.yhi[t0];
-    if (t0 + 1 < cull.n_ytiles) {
-      blo = box_min(blo, cull.ylo[t0 + 1]);
-      bhi = box_max(bhi, cull.yhi[t0 + 1]);
-    }
+  if (cull.enabled) {  // a column block is exactly one 256-point scene tile
+    blo = cull.ylo[blockIdx.x];
+    bhi = cull.yhi[blockIdx.x];
     cut = s2 * cull.col_bound[blockIdx.x] + cull.margin1;
   }
   int evaluated = 0;
@@ -304,18 +299,13 @@ __global__ void __launch_bounds__(128)
   const float s2 = s * s;
   const int64_t rbase =
       static_cast<int64_t>(blockIdx.x + rb_offset) * (256 * RP) + 2 * threadIdx.x;
-  // tile culling: this CTA's 512 model rows vs each 256-point scene tile
+  // tile culling: this CTA's 256 model rows vs each 256-point scene tile
   float4 blo = make_float4(0.f, 0.f, 0.f, 0.f), bhi = blo;
   float floor_l = -INFINITY;
-  if (cull.enabled) {
+  if (cull.enabled) {  // a row block is exactly one 256-point model tile
     const int64_t rb = blockIdx.x + rb_offset;
-    const int64_t t0 = rb * 2;
-    blo = cull.xlo[t0];
-    bhi = cull.xhi[t0];
-    if (t0 + 1 < cull.n_xtiles) {
-      blo = box_min(blo, cull.xlo[t0 + 1]);
-      bhi = box_max(bhi, cull.xhi[t0 + 1]);
-    }
+    blo = cull.xlo[rb];
+    bhi = cull.xhi[rb];
     floor_l = cull.row_bound[rb] - cull.margin2;
   }
   int evaluated = 0;
@@ -493,7 +483,7 @@ __global__ void tile_bminmax_kernel(const float4* __restrict__ y4b, int64_t n,
   }
 }
 
-// pass-1 bound per 512-column block: U = min over model tiles of the largest
+// pass-1 bound per scene tile: U = min over model tiles of the largest
 // possible squared distance → every column has t_min ≤ s²·U.
 __global__ void col_bound_kernel(CullInfo cull, float* __restrict__ out, int n_blocks,
                                  const IterState* __restrict__ st) {
@@ -501,11 +491,7 @@ __global__ void col_bound_kernel(CullInfo cull, float* __restrict__ out, int n_b
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (b >= n_blocks) return;
-  float4 lo = cull.ylo[2 * b], hi = cull.yhi[2 * b];
-  if (2 * b + 1 < cull.n_ytiles) {
-    lo = box_min(lo, cull.ylo[2 * b + 1]);
-    hi = box_max(hi, cull.yhi[2 * b + 1]);
-  }
+  const float4 lo = cull.ylo[b], hi = cull.yhi[b];
   float u = INFINITY;
   for (int j = lane; j < cull.n_xtiles; j += 32)
     u = fminf(u, box_maxdist2(lo, hi, cull.xlo[j], cull.xhi[j]));
@@ -514,7 +500,7 @@ __global__ void col_bound_kernel(CullInfo cull, float* __restrict__ out, int n_b
   if (lane == 0) out[b] = u;
 }
 
-// pass-2 bound per 512-row block: a lower bound on max_n L_mn for every row,
+// pass-2 bound per model tile: a lower bound on max_n L_mn for every row,
 // L_lb = max over scene tiles of (min b − s²·maxdist²).
 __global__ void row_bound_kernel(CullInfo cull, float* __restrict__ out, int n_blocks,
                                  const IterState* __restrict__ st) {
@@ -523,11 +509,7 @@ __global__ void row_bound_kernel(CullInfo cull, float* __restrict__ out, int n_b
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (b >= n_blocks) return;
-  float4 lo = cull.xlo[2 * b], hi = cull.xhi[2 * b];
-  if (2 * b + 1 < cull.n_xtiles) {
-    lo = box_min(lo, cull.xlo[2 * b + 1]);
-    hi = box_max(hi, cull.xhi[2 * b + 1]);
-  }
+  const float4 lo = cull.xlo[b], hi = cull.xhi[b];
   float l = -INFINITY;
   for (int j = lane; j < cull.n_ytiles; j += 32)
     l = fmaxf(l, cull.bminmax[j].x - s2 * box_maxdist2(lo, hi, cull.ylo[j], cull.yhi[j]));

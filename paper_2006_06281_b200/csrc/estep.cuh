@@ -10,8 +10,10 @@
 
 namespace fcpd {
 
-constexpr int kColsPerThread = 4;
-constexpr int kRowsPerThread = 4;
+// one column pair / row pair per thread: a 128-thread CTA covers exactly one
+// 256-point tile, the culling granularity
+constexpr int kColsPerThread = 2;
+constexpr int kRowsPerThread = 2;
 constexpr int kMaxRowChunks = 8;  // pass-2 row chunks (overlap with the Qᵀ·R stream)
 
 // Fallback-path per-row outputs (all device pointers; SoA fp64 M×3).
@@ -60,8 +62,8 @@ struct CullInfo {
   const float4* xhi = nullptr;
   const float4* ylo = nullptr;      // scene tiles (fixed)
   const float4* yhi = nullptr;
-  const float* col_bound = nullptr; // per 512-column block: U (unscaled d²)
-  const float* row_bound = nullptr; // per 512-row block: lower bound of max L (log2)
+  const float* col_bound = nullptr; // per scene tile: U (unscaled d²)
+  const float* row_bound = nullptr; // per model tile: lower bound of max L (log2)
   const float2* bminmax = nullptr;  // per scene tile: (min b, max b)
   float margin1 = 0.f, margin2 = 0.f;
   unsigned long long* counters = nullptr;  // [0] pass-1 tiles, [1] pass-2 tiles evaluated
