@@ -35,29 +35,6 @@ __device__ __forceinline__ float4 scale_d(float4 p, float s) {
 }  // namespace
 
 // part [splits][5][M] → out [M_pad][5] (pad rows zero), 8 lanes per row.
-__global__ void row_split_sum_kernel(const double* __restrict__ part, int splits, int64_t m,
-                                     int64_t m_pad, double* __restrict__ out,
-                                     const IterState* __restrict__ st) {
-  if (!st->active) return;
-  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t row = gid / kLanes;
-  const int lane = static_cast<int>(gid % kLanes);
-  double a[5] = {0, 0, 0, 0, 0};
-  if (row < m)
-    for (int sp = lane; sp < splits; sp += kLanes) {
-      const double* p = part + static_cast<int64_t>(sp) * 5 * m;
-#pragma unroll
-      for (int k = 0; k < 5; ++k) a[k] += p[k * m + row];
-    }
-#pragma unroll
-  for (int o = kLanes / 2; o > 0; o >>= 1)
-#pragma unroll
-    for (int k = 0; k < 5; ++k) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
-  if (row < m_pad && lane == 0)
-#pragma unroll
-    for (int k = 0; k < 5; ++k) out[row * 5 + k] = a[k];
-}
-
 __device__ __forceinline__ void finalize_own(int64_t i, int64_t mr, double log2p1, double s0,
                                              double sy0, double sy1, double sy2, double sv,
                                              const double* __restrict__ xt64_own, double s,
@@ -213,12 +190,6 @@ __global__ void sigma_local_sum_kernel(const double* __restrict__ sig_part, int 
 
 // ------------------------------------------------------------------ launchers
 
-void launch_row_split_sum(const double* part, int splits, int64_t m, int64_t m_pad, double* out,
-                          const IterState* st, cudaStream_t s) {
-  row_split_sum_kernel<<<ceil_div(m_pad * kLanes, 256), 256, 0, s>>>(part, splits, m, m_pad, out,
-                                                                     st);
-  FCPD_LAUNCH_CHECK();
-}
 void launch_row_finalize_own(const double* sums_own, int64_t mr, int64_t m_valid_own,
                              int64_t n_global, const double* xt64_own, const DistRowOut& o,
                              const YStats& ys, int32_t* mask_own, IterState* st, cudaStream_t s) {

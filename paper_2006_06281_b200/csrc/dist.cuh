@@ -19,8 +19,6 @@ struct DistRowOut {
   const double* x0_own;
 };
 
-void launch_row_split_sum(const double* part, int splits, int64_t m, int64_t m_pad, double* out,
-                          const IterState* st, cudaStream_t s);
 void launch_row_finalize_own(const double* sums_own, int64_t mr, int64_t m_valid_own,
                              int64_t n_global, const double* xt64_own, const DistRowOut& o,
                              const YStats& ys, int32_t* mask_own, IterState* st, cudaStream_t s);

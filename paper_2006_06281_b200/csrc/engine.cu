@@ -182,7 +182,7 @@ struct Session {
 
   DevBuf<double> x0, xt64, xt_prev, y64;
   DevBuf<float4> xt4, y4b, resid4, g4;
-  DevBuf<double> b2, pt1, col_part, row_part, ptilde_y, var, log2p1, zpart, vpart, coef,
+  DevBuf<double> b2, pt1, col_seg, row_seg, ptilde_y, var, log2p1, zpart, vpart, coef,
       sig_part, trace;
   DevBuf<int32_t> col_flags, row_flags, flags_count, degenerate;
   DevBuf<uint64_t> stamps;
@@ -196,16 +196,10 @@ struct Session {
   std::vector<int64_t> perm_x, perm_y;
   bool cull = true;
   DevBuf<float4> xlo, xhi, ylo, yhi;
-  DevBuf<float> col_bound, row_bound;
   DevBuf<float2> bminmax;
   DevBuf<unsigned long long> cull_counters;  // tiles evaluated (pass 1, pass 2), cumulative
-
-  // overlapped graph form: pass-2 row chunks ∥ chunked Qᵀ·R stream
-  int chunks = 1;
-  ColsumPlan zpc[kMaxRowChunks];
-  size_t zoff[kMaxRowChunks] = {};
-  cudaEvent_t ev_chunk[kMaxRowChunks] = {};
-  cudaEvent_t ev_join = nullptr;
+  // per-iteration work lists of the two passes (culled tile pairs)
+  DevBuf<int32_t> wl1_tiles, wl1_off, wl2_tiles, wl2_off, wl_done;
 
   // ---- distributed (NCCL) sharding: scene N split over ranks, model rows
   // [m0, m0+mr) owned by this rank (m_pad = world·mr ≥ M).  In this mode
@@ -223,7 +217,7 @@ struct Session {
   }
   void release() {
     release_graph();
-    for (auto* b : {&x0, &xt64, &xt_prev, &y64, &b2, &pt1, &col_part, &row_part, &ptilde_y,
+    for (auto* b : {&x0, &xt64, &xt_prev, &y64, &b2, &pt1, &col_seg, &row_seg, &ptilde_y,
                     &var, &log2p1, &zpart, &vpart, &coef, &sig_part, &trace})
       b->release();
     for (auto* b : {&xt4, &y4b, &resid4, &g4}) b->release();
@@ -237,13 +231,9 @@ struct Session {
     fmax_all.release();
     qt_own.release();
     for (auto* b : {&xlo, &xhi, &ylo, &yhi}) b->release();
-    col_bound.release();
-    row_bound.release();
     bminmax.release();
     cull_counters.release();
-    for (auto& e : ev_chunk)
-      if (e) cudaEventDestroy(e), e = nullptr;
-    if (ev_join) cudaEventDestroy(ev_join), ev_join = nullptr;
+    for (auto* b : {&wl1_tiles, &wl1_off, &wl2_tiles, &wl2_off, &wl_done}) b->release();
   }
 };
 
@@ -390,26 +380,80 @@ void ensure_basis(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa) {
   b.t_eig = s.t_eig;
 }
 
+// Culling pays once there are enough tile pairs to skip: below ~1k pairs
+// (e.g. C0, 8×8 tiles) its four geometry kernels cost more than they save.
+// FCPD_CULL=0/1 overrides.
+constexpr int64_t kCullMinTilePairs = 1024;
+bool cull_default(int64_t x_tiles, int64_t y_tiles) {
+  if (const char* e = std::getenv("FCPD_CULL")) return std::atoi(e) != 0;
+  return x_tiles * y_tiles >= kCullMinTilePairs;
+}
+
 // Wire the session's culling geometry into the E-step buffers.  margin =
 // 50 + log2(count) log2-units: skipped mass ≤ 2^-50 of any column/row total.
 void set_cull(Session& s, EStepBuffers& eb, int64_t m, int64_t n_local, int64_t n_global) {
   CullInfo& c = eb.cull;
-  c.enabled = s.cull && s.xlo.p && s.ylo.p ? 1 : 0;
+  c.enabled = s.cull && s.xlo.p && s.ylo.p && s.wl1_tiles.p && s.wl2_tiles.p ? 1 : 0;
   c.n_xtiles = ceil_div(m, 256);
   c.n_ytiles = ceil_div(n_local, 256);
   c.xlo = s.xlo.p;
   c.xhi = s.xhi.p;
   c.ylo = s.ylo.p;
   c.yhi = s.yhi.p;
-  c.col_bound = s.col_bound.p;
-  c.row_bound = s.row_bound.p;
   c.bminmax = s.bminmax.p;
   c.margin1 = 50.f + static_cast<float>(std::log2(static_cast<double>(std::max<int64_t>(m, 1))));
   c.margin2 =
       50.f + static_cast<float>(std::log2(static_cast<double>(std::max<int64_t>(n_global, 1))));
   c.counters = s.cull_counters.p;
-  eb.cullw = CullBuffers{s.xlo.p, s.xhi.p, s.ylo.p, s.yhi.p, s.col_bound.p, s.row_bound.p,
-                         s.bminmax.p};
+  eb.cullw = CullBuffers{s.xlo.p, s.xhi.p, s.ylo.p, s.yhi.p, s.bminmax.p};
+  eb.wl1 = WorkListBuffers{s.wl1_tiles.p, s.wl1_off.p, s.wl_done.p};
+  eb.wl2 = WorkListBuffers{s.wl2_tiles.p, s.wl2_off.p, s.wl_done.p ? s.wl_done.p + 1 : nullptr};
+}
+
+// E-step buffers of the session (pt1: optional Σ_m P_mn output; resid:
+// write R = P̃Y − X for the M-step).
+EStepBuffers estep_buffers(Session& s, double* pt1, bool resid) {
+  EStepBuffers eb{};
+  eb.xt4 = s.xt4.p;
+  eb.xt64 = s.xt64.p;
+  eb.y4b = s.y4b.p;
+  eb.b2 = s.b2.p;
+  eb.pt1 = pt1;
+  eb.col_seg = s.col_seg.p;
+  eb.row_seg = s.row_seg.p;
+  eb.col_flags = s.col_flags.p;
+  eb.row_flags = s.row_flags.p;
+  eb.flags_count = s.flags_count.p;
+  eb.out = RowOut{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p,
+                  resid ? s.resid4.p : nullptr, resid ? s.x0.p : nullptr};
+  eb.ystats = s.ystats;
+  set_cull(s, eb, s.m, s.n, s.dist ? s.n_global : s.n);
+  return eb;
+}
+
+// Session E-step scratch: segment partials, work lists, culling geometry.
+// m = model rows the E-step sees (all M), n = local scene points.
+void alloc_estep(Session& s, int64_t m, int64_t n, cudaStream_t str) {
+  s.col_seg.ensure(s.ep.col_seg_doubles());
+  s.row_seg.ensure(s.ep.row_seg_doubles());
+  const int64_t nxt = ceil_div(m, 256), nyt = ceil_div(n, 256);
+  s.cull = cull_default(nxt, nyt);
+  s.xlo.ensure(nxt);
+  s.xhi.ensure(nxt);
+  s.ylo.ensure(nyt);
+  s.yhi.ensure(nyt);
+  s.bminmax.ensure(nyt);
+  s.cull_counters.ensure(2);
+  FCPD_CUDA(cudaMemsetAsync(s.cull_counters.p, 0, 2 * sizeof(unsigned long long), str));
+  if (s.cull) {
+    s.wl1_tiles.ensure(static_cast<size_t>(nyt) * nxt);
+    s.wl1_off.ensure(nyt + 1);
+    s.wl2_tiles.ensure(static_cast<size_t>(nxt) * nyt);
+    s.wl2_off.ensure(nxt + 1);
+    s.wl_done.ensure(2);
+    FCPD_CUDA(cudaMemsetAsync(s.wl_done.p, 0, 2 * sizeof(int32_t), str));
+  }
+  launch_tile_bbox(s.y4b.p, n, s.ylo.p, s.yhi.p, nullptr, str);
 }
 
 // ev (optional, 7 events): recorded before the iteration and after each of
@@ -418,20 +462,7 @@ void enqueue_iteration(fcpd_ctx* ctx, Session& s, cudaEvent_t* ev = nullptr) {
   Basis& b = ctx->basis;
   IterState* st = s.st.p;
   cudaStream_t str = ctx->stream;
-  EStepBuffers eb{};
-  eb.xt4 = s.xt4.p;
-  eb.xt64 = s.xt64.p;
-  eb.y4b = s.y4b.p;
-  eb.b2 = s.b2.p;
-  eb.pt1 = nullptr;
-  eb.col_part = s.col_part.p;
-  eb.row_part = s.row_part.p;
-  eb.col_flags = s.col_flags.p;
-  eb.row_flags = s.row_flags.p;
-  eb.flags_count = s.flags_count.p;
-  eb.out = RowOut{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p, s.resid4.p, s.x0.p};
-  eb.ystats = s.ystats;
-  set_cull(s, eb, s.m, s.n, s.dist ? s.n_global : s.n);
+  const EStepBuffers eb = estep_buffers(s, nullptr, true);
   auto rec = [&](int i) {
     if (ev) FCPD_CUDA(cudaEventRecord(ev[i], str));
   };
@@ -449,54 +480,6 @@ void enqueue_iteration(fcpd_ctx* ctx, Session& s, cudaEvent_t* ev = nullptr) {
                          s.var.p, s.sig_part.p, s.d, s.cfg.early_stop, s.trace.p, st,
                          s.stamps.p, str);
   rec(6);
-}
-
-// The captured (graph) form of one iteration: pass 2 is cut into row chunks
-// and the Qᵀ·R basis stream of chunk c runs on a second stream as soon as
-// chunk c's residual rows are final, so the HBM-bound stream overlaps the
-// FP32/MUFU-bound E-step of the next chunk (fork/join with events inside the
-// graph).  Same kernels; only the stream-K partition of Qᵀ·R changes (per
-// chunk), so results equal enqueue_iteration's to fp64 rounding and are
-// bitwise reproducible run to run.
-void enqueue_iteration_overlap(fcpd_ctx* ctx, Session& s) {
-  Basis& b = ctx->basis;
-  IterState* st = s.st.p;
-  cudaStream_t str = ctx->stream, side = ctx->side;
-  EStepBuffers eb{};
-  eb.xt4 = s.xt4.p;
-  eb.xt64 = s.xt64.p;
-  eb.y4b = s.y4b.p;
-  eb.b2 = s.b2.p;
-  eb.pt1 = nullptr;
-  eb.col_part = s.col_part.p;
-  eb.row_part = s.row_part.p;
-  eb.col_flags = s.col_flags.p;
-  eb.row_flags = s.row_flags.p;
-  eb.flags_count = s.flags_count.p;
-  eb.out = RowOut{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p, s.resid4.p, s.x0.p};
-  eb.ystats = s.ystats;
-  set_cull(s, eb, s.m, s.n, s.dist ? s.n_global : s.n);
-  launch_estep_prologue(st, s.m, s.n, s.d, s.cfg.omega, s.flags_count.p, s.stamps.p, str);
-  launch_estep_pass1(s.ep, eb, s.m, s.n, st, str);
-  const double* parts[kMaxRowChunks];
-  for (int c = 0; c < s.chunks; ++c) {
-    launch_estep_pass2_chunk(s.ep, eb, s.m, s.n, st, str, c, s.chunks);
-    FCPD_CUDA(cudaEventRecord(s.ev_chunk[c], str));
-    FCPD_CUDA(cudaStreamWaitEvent(side, s.ev_chunk[c], 0));
-    const RowChunk rc = row_chunk(s.ep, s.m, c, s.chunks);
-    double* part = s.zpart.p + s.zoff[c];
-    parts[c] = part;
-    launch_colsum(s.zpc[c], b.q + rc.r0 * b.kpad, b.kpad, s.resid4.p + rc.r0, part, st,
-                  c == 0 ? s.stamps.p : nullptr, 1, side);
-  }
-  FCPD_CUDA(cudaEventRecord(s.ev_join, side));
-  FCPD_CUDA(cudaStreamWaitEvent(str, s.ev_join, 0));
-  launch_zreduce_chunks(s.zpc, parts, s.chunks, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.coef.p,
-                        s.g4.p, st, str);
-  launch_colsum(s.vp, b.qt, b.mpad, s.g4.p, s.vpart.p, st, nullptr, 0, str);
-  launch_transform_sigma(s.vp, s.vpart.p, s.x0.p, s.xt64.p, s.xt_prev.p, s.xt4.p, s.ptilde_y.p,
-                         s.var.p, s.sig_part.p, s.d, s.cfg.early_stop, s.trace.p, st,
-                         s.stamps.p, str);
 }
 
 }  // namespace
@@ -527,14 +510,12 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
   s.degenerate.ensure(m);
   s.col_flags.ensure(n);
   s.row_flags.ensure(m);
-  s.flags_count.ensure(1 + kMaxRowChunks);
+  s.flags_count.ensure(2);
   s.st.ensure(1);
   s.capacity = std::max(capacity, 1);
   s.trace.ensure(s.capacity);
   s.stamps.ensure(4 * static_cast<size_t>(s.capacity));
   s.ep = make_estep_plan(m, n, ctx->sm_count);
-  s.col_part.ensure(static_cast<size_t>(s.ep.col_splits) * n);
-  s.row_part.ensure(static_cast<size_t>(s.ep.row_splits) * 5 * m);
   s.sig_part.ensure(transform_sigma_blocks(m));  // one σ² partial per transform block
 
   std::vector<float4> x4(m), y4(n);
@@ -565,53 +546,13 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
   ys.sq_mean = sq / static_cast<double>(n);
   s.ystats = ys;
 
-  // tile-culling geometry: scene tiles are fixed for the session
-  s.cull = true;
-  if (const char* e = std::getenv("FCPD_CULL")) s.cull = std::atoi(e) != 0;
-  const int64_t nxt = ceil_div(m, 256), nyt = ceil_div(n, 256);
-  s.xlo.ensure(nxt);
-  s.xhi.ensure(nxt);
-  s.ylo.ensure(nyt);
-  s.yhi.ensure(nyt);
-  s.bminmax.ensure(nyt);
-  s.col_bound.ensure(s.ep.col_blocks);
-  s.row_bound.ensure(s.ep.row_blocks);
-  s.cull_counters.ensure(2);
-  FCPD_CUDA(cudaMemsetAsync(s.cull_counters.p, 0, 2 * sizeof(unsigned long long), str));
-  launch_tile_bbox(s.y4b.p, n, s.ylo.p, s.yhi.p, nullptr, str);
+  alloc_estep(s, m, n, str);  // scene tiles are fixed for the session
 
   if (need_mstep) {
     Basis& b = ctx->basis;
     s.zp = make_colsum_plan(m, b.k, ctx->sm_count);
     s.vp = make_colsum_plan(b.k, m, ctx->sm_count);
-    // overlap form: ~8 row blocks (4096 rows) per chunk, ≤ kMaxRowChunks;
-    // each chunk's stream uses one bulk CTA per SM so pass-2 CTAs co-reside
-    // Off by default: measured on B200 (C1) the chunked/concurrent form is
-    // slower (1.03 vs 0.90 ms/iteration) — the co-resident bulk stream drops
-    // below full HBM rate and pass 2 loses SMs; kept for experiments via
-    // FCPD_OVERLAP_CHUNKS=<n>.
-    int chunks = 1;
-    if (const char* e = std::getenv("FCPD_OVERLAP_CHUNKS")) chunks = std::atoi(e);
-    chunks = std::max(1, std::min(kMaxRowChunks, std::min(chunks, s.ep.row_blocks)));
-    s.chunks = chunks;
-    if (chunks > 1) {
-      plan_row_chunks(s.ep, m, n, ctx->sm_count, chunks);
-      s.row_part.ensure(static_cast<size_t>(s.ep.max_row_splits()) * 5 * m);
-    }
-    size_t ztotal = s.zp.part_doubles();
-    if (chunks > 1) {
-      ztotal = 0;
-      for (int c = 0; c < chunks; ++c) {
-        const RowChunk rc = row_chunk(s.ep, m, c, chunks);
-        s.zpc[c] = make_colsum_plan(std::max<int64_t>(1, rc.r1 - rc.r0), b.k, ctx->sm_count, 1);
-        s.zoff[c] = ztotal;
-        ztotal += s.zpc[c].part_doubles();
-        if (!s.ev_chunk[c])
-          FCPD_CUDA(cudaEventCreateWithFlags(&s.ev_chunk[c], cudaEventDisableTiming));
-      }
-      if (!s.ev_join) FCPD_CUDA(cudaEventCreateWithFlags(&s.ev_join, cudaEventDisableTiming));
-    }
-    s.zpart.ensure(std::max(ztotal, s.zp.part_doubles()));
+    s.zpart.ensure(s.zp.part_doubles());
     s.vpart.ensure(s.vp.part_doubles());
     s.coef.ensure(3 * b.k);
     s.g4.ensure(b.k);
@@ -774,10 +715,7 @@ void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, i
   cudaGraph_t g = nullptr;
   FCPD_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   try {
-    if (s.chunks > 1)
-      enqueue_iteration_overlap(ctx, s);
-    else
-      enqueue_iteration(ctx, s);
+    enqueue_iteration(ctx, s);
   } catch (...) {
     cudaStreamEndCapture(ctx->stream, &g);
     if (g) cudaGraphDestroy(g);
@@ -940,21 +878,11 @@ void enqueue_iteration_dist(fcpd_ctx* ctx, Session& s) {
   cudaStream_t str = ctx->stream;
   ncclComm_t comm = ctx->comm;
   const int64_t m = s.m, nl = s.n;
-  EStepBuffers eb{};
-  eb.xt4 = s.xt4.p;
-  eb.y4b = s.y4b.p;
-  eb.b2 = s.b2.p;
-  eb.col_part = s.col_part.p;
-  eb.row_part = s.row_part.p;
-  eb.col_flags = s.col_flags.p;
-  eb.row_flags = s.row_flags.p;
-  eb.flags_count = s.flags_count.p;
-  eb.ystats = s.ystats;
-  set_cull(s, eb, s.m, s.n, s.dist ? s.n_global : s.n);
+  const EStepBuffers eb = estep_buffers(s, nullptr, false);
   launch_estep_prologue(st, m, s.n_global, s.d, s.cfg.omega, s.flags_count.p, s.stamps.p, str);
   launch_estep_pass1(s.ep, eb, m, nl, st, str);  // column-local: no communication
   launch_estep_pass2_partials(s.ep, eb, m, nl, st, str);
-  launch_row_split_sum(s.row_part.p, s.ep.row_splits, m, s.m_pad, s.rowsum_all.p, st, str);
+  launch_row_seg_sum(s.ep, eb, m, nl, s.m_pad, s.rowsum_all.p, st, str);
   FCPD_NCCL(ncclReduceScatter(s.rowsum_all.p, s.rowsum_own.p, s.mr * 5, ncclDouble, ncclSum,
                               comm, str));
   const DistRowOut o{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p, s.resid4.p, s.x0.p};
@@ -1110,11 +1038,9 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
   s.ep = make_estep_plan(m, n, ctx->sm_count);
   s.b2.ensure(n);
   s.pt1.ensure(n);
-  s.col_part.ensure(static_cast<size_t>(s.ep.col_splits) * n);
-  s.row_part.ensure(static_cast<size_t>(s.ep.row_splits) * 5 * m);
   s.col_flags.ensure(n);
   s.row_flags.ensure(m);
-  s.flags_count.ensure(1 + kMaxRowChunks);
+  s.flags_count.ensure(2);
   s.rowsum_all.ensure(5 * s.m_pad);
   s.rowsum_own.ensure(5 * mr);
   s.fsum_all.ensure(5 * s.m_pad);
@@ -1122,19 +1048,9 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
   s.mask_own.ensure(mr);
   s.mask_all.ensure(s.m_pad);
   s.fmax_all.ensure(s.m_pad);
-  // tile-culling geometry (model tiles over all M rows; local scene tiles)
-  s.cull = true;
-  if (const char* e = std::getenv("FCPD_CULL")) s.cull = std::atoi(e) != 0;
-  s.xlo.ensure(ceil_div(m, 256));
-  s.xhi.ensure(ceil_div(m, 256));
-  s.ylo.ensure(ceil_div(n, 256));
-  s.yhi.ensure(ceil_div(n, 256));
-  s.bminmax.ensure(ceil_div(n, 256));
-  s.col_bound.ensure(s.ep.col_blocks);
-  s.row_bound.ensure(s.ep.row_blocks);
-  s.cull_counters.ensure(2);
-  FCPD_CUDA(cudaMemsetAsync(s.cull_counters.p, 0, 2 * sizeof(unsigned long long), str));
-  launch_tile_bbox(s.y4b.p, n, s.ylo.p, s.yhi.p, nullptr, str);
+  // segment partials, work lists, culling geometry (model tiles over all M
+  // rows; local scene tiles)
+  alloc_estep(s, m, n, str);
   // basis shard: Q rows [m0, m0+m_valid) in place; Qᵀ columns copied compact
   s.qt_own.ensure(static_cast<size_t>(b.k) * s.mr4);
   FCPD_CUDA(cudaMemsetAsync(s.qt_own.p, 0, sizeof(float) * b.k * s.mr4, str));
@@ -1376,8 +1292,13 @@ int32_t fcpd_kernels_per_iteration(const fcpd_ctx* ctx) {
   // row-fallback, Qᵀ·R, z-reduce/filter, Q·g, transform/σ²-rows, σ²-final.
   // distributed: prologue, col, col-combine, col-fallback, row, row-sum,
   // finalize-own, fb-max, fb-sum, fb-finalize, Qᵀ·R, z-sum, z-filter, Q·g,
-  // transform, σ²-local, σ²-final (+ 7 NCCL collectives)
-  return ctx && ctx->sess.dist ? 17 : 12;
+  // transform, σ²-local, σ²-final (+ 7 NCCL collectives).
+  // Tile culling adds 4: model-tile boxes, column bounds, scene-tile b range,
+  // row bounds.
+  if (!ctx) return 0;
+  const Session& s = ctx->sess;
+  const int cull = s.cull && s.xlo.p && s.ylo.p ? 4 : 0;
+  return (s.dist ? 17 : 12) + cull;
 }
 
 int fcpd_register(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n,
@@ -1462,20 +1383,7 @@ int fcpd_estep(fcpd_ctx* ctx, const double* xt, int64_t m, const double* y, int6
     s.perm_y = morton_sort(ys, n);
     prepare_buffers(ctx, s, xs, ys, 1, false);
     reset_state(ctx, s, sigma2);
-    EStepBuffers eb{};
-    eb.xt4 = s.xt4.p;
-    eb.xt64 = s.xt64.p;
-    eb.y4b = s.y4b.p;
-    eb.b2 = s.b2.p;
-    eb.pt1 = s.pt1.p;
-    eb.col_part = s.col_part.p;
-    eb.row_part = s.row_part.p;
-    eb.col_flags = s.col_flags.p;
-    eb.row_flags = s.row_flags.p;
-    eb.flags_count = s.flags_count.p;
-    eb.out = RowOut{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p, nullptr, nullptr};
-    eb.ystats = s.ystats;
-  set_cull(s, eb, s.m, s.n, s.dist ? s.n_global : s.n);
+    const EStepBuffers eb = estep_buffers(s, s.pt1.p, false);
     launch_estep(s.ep, eb, m, n, d, omega, s.st.p, nullptr, ctx->stream);
     std::vector<double> pty(3 * m), lp(m), vr(m), pc(n);
     std::vector<int32_t> dg(m);

@@ -21,13 +21,22 @@
 // reference's degenerate-row rule (row mass < 1e-300 → uniform row,
 // correspondence.hpp:89-91) bit-for-bit in the decision.
 //
-// Work split: pass 1 tiles columns over threads (CPT per thread) and splits
-// M over gridDim.y; pass 2 tiles rows over threads (RPT per thread) and
-// splits N over gridDim.y.  Partials are fp64 per (split, column|row) and
-// are reduced in a fixed order, so results are bitwise reproducible.
+// Schedule (both passes): the work is the list of (own block, other tile)
+// pairs — all of them, or the culled list (tile culling on Morton-sorted
+// points, list kernels below).  A persistent grid of exactly one CTA wave
+// splits the list's POINTS evenly (stream-K): CTA g gets the contiguous
+// range [g·P/G, (g+1)·P/G) of the P = 256·units point-units, cut into
+// segments at block boundaries.  Every CTA therefore does the same work to
+// within one point, independent of how culling thinned the list.  A segment
+// (CTA g, block b) writes its fp64 partial sums to slot g + b (slots are
+// strictly increasing along the schedule, so unique); the combine sums a
+// block's slots in CTA order: deterministic, bitwise reproducible.
 
 #include <cuda_runtime.h>
 #include <math.h>
+
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "estep.cuh"
@@ -36,12 +45,15 @@ namespace fcpd {
 
 namespace {
 
-constexpr int kTile = 256;       // points staged in shared memory per step
+constexpr int kTile = kTilePts;  // points staged in shared memory per step
 constexpr int kCombineLanes = 8; // lanes cooperating on one row/column reduction
 constexpr float kPadCoord = 3.0e18f;  // padding point: t ≈ 1e37, 2^-t = 0
+// centred form only where its fp32 rounding stays ≤ ~4e-6 in log2 units:
+// squared half-diagonal of the CTA's own box in the scaled frame
+constexpr float kCentredMaxR2 = 16.f;
 
 __device__ __forceinline__ float sqdist(float4 a, float4 b) {
-  // identical operation order in both passes (bitwise-equal t_mn)
+  // the fallbacks' pair term (difference form, as the main kernels' diff path)
   const float dx = __fsub_rn(a.x, b.x);
   const float dy = __fsub_rn(a.y, b.y);
   const float dz = __fsub_rn(a.z, b.z);
@@ -56,12 +68,6 @@ __device__ __forceinline__ double derived_scale(const IterState* st) {
   return sqrt(kLog2e / (2.0 * st->sigma2_e));
 }
 
-__device__ __forceinline__ float4 box_min(float4 a, float4 b) {
-  return make_float4(fminf(a.x, b.x), fminf(a.y, b.y), fminf(a.z, b.z), 0.f);
-}
-__device__ __forceinline__ float4 box_max(float4 a, float4 b) {
-  return make_float4(fmaxf(a.x, b.x), fmaxf(a.y, b.y), fmaxf(a.z, b.z), 0.f);
-}
 // smallest squared distance between two boxes (0 if they overlap)
 __device__ __forceinline__ float box_mindist2(float4 alo, float4 ahi, float4 blo, float4 bhi) {
   const float dx = fmaxf(0.f, fmaxf(alo.x - bhi.x, blo.x - ahi.x));
@@ -79,6 +85,78 @@ __device__ __forceinline__ float box_maxdist2(float4 alo, float4 ahi, float4 blo
   return (dx * dx + dy * dy + dz * dz) * (1.f + 0x1p-20f);
 }
 
+// stream-K geometry over P point-units and G CTAs
+__device__ __forceinline__ int64_t sk_start(int64_t g, int64_t G, int64_t P) { return g * P / G; }
+__device__ __forceinline__ int64_t sk_owner(int64_t p, int64_t G, int64_t P) {
+  return ((p + 1) * G - 1) / P;  // the CTA whose range holds point-unit p
+}
+// largest block b with off(b) ≤ u (u < total)
+__device__ __forceinline__ int wl_block_of(const WorkList& wl, int64_t u) {
+  if (wl.implicit) return static_cast<int>(u / wl.n_other);
+  int lo = 0, hi = wl.n_blocks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (wl.offset[mid] <= u) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Centre and squared half-diagonal of the CTA's points' bounding box
+// (scaled frame); blockDim = 128.  Callers separate successive calls by a
+// __syncthreads (the staging barrier).
+struct BoxCentre {
+  float3 c;
+  float r2;
+};
+__device__ __forceinline__ BoxCentre cta_box_centre(float lx, float ly, float lz, float hx,
+                                                    float hy, float hz) {
+  __shared__ float red[6][4];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lx = fminf(lx, __shfl_xor_sync(0xffffffffu, lx, o));
+    ly = fminf(ly, __shfl_xor_sync(0xffffffffu, ly, o));
+    lz = fminf(lz, __shfl_xor_sync(0xffffffffu, lz, o));
+    hx = fmaxf(hx, __shfl_xor_sync(0xffffffffu, hx, o));
+    hy = fmaxf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
+    hz = fmaxf(hz, __shfl_xor_sync(0xffffffffu, hz, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[0][w] = lx;
+    red[1][w] = ly;
+    red[2][w] = lz;
+    red[3][w] = hx;
+    red[4][w] = hy;
+    red[5][w] = hz;
+  }
+  __syncthreads();
+  float r[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) r[k] = red[k][0];
+#pragma unroll
+  for (int i = 1; i < 4; ++i) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) r[k] = fminf(r[k], red[k][i]);
+#pragma unroll
+    for (int k = 3; k < 6; ++k) r[k] = fmaxf(r[k], red[k][i]);
+  }
+  BoxCentre b;
+  if (!(r[0] <= r[3])) {  // no valid point
+    b.c = make_float3(0.f, 0.f, 0.f);
+    b.r2 = INFINITY;
+    return b;
+  }
+  b.c = make_float3(0.5f * (r[0] + r[3]), 0.5f * (r[1] + r[4]), 0.5f * (r[2] + r[5]));
+  const float ex = 0.5f * (r[3] - r[0]), ey = 0.5f * (r[4] - r[1]), ez = 0.5f * (r[5] - r[2]);
+  b.r2 = ex * ex + ey * ey + ez * ez;
+  return b;
+}
+
+__device__ __forceinline__ float2 ex2x2(float2 v) {
+  return make_float2(ex2_approx(v.x), ex2_approx(v.y));
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -88,7 +166,7 @@ __global__ void estep_prologue_kernel(IterState* st, int64_t m, int64_t n, int d
                                       double omega, int32_t* flags_count, uint64_t* stamps) {
   if (!st->active) return;
   if (stamps) stamps[4 * st->iter + 0] = globaltimer();
-  for (int i = 0; i <= kMaxRowChunks; ++i) flags_count[i] = 0;  // column + per-chunk row lists
+  flags_count[0] = flags_count[1] = 0;  // column and row fallback lists
   double s2 = st->sigma2;
   if (s2 < kSigma2Floor) {
     s2 = kSigma2Floor;
@@ -106,109 +184,174 @@ __global__ void estep_prologue_kernel(IterState* st, int64_t m, int64_t n, int d
 }
 
 // ---------------------------------------------------------------------------
-// Pass 1: per-column partial sums Σ_m 2^{−t_mn} over one M-split.
+// Pass 1: per-column sums Σ_m 2^{−t_mn}.  Own block = 256 scene points
+// (thread: column pair 2·tid, 2·tid+1); the staged tiles are model points.
 //
-// f32x2 packing (FADD2/FMUL2/FFMA2, sm_100): each thread owns CP column
-// pairs; every packed op evaluates two (m, n) pairs in one issue slot, so
-// per pair the pass costs 3.5 issue slots of FP32 work + 1 MUFU.EX2 and is
-// bound by the 16 ex2/clk/SM SFU rate.  Each lane of a packed op rounds
-// exactly like the scalar op, so t_mn is bitwise identical to sqdist() used
-// by pass 2 and the fallbacks.  Shared memory holds each model point as
-// (−x,−x,−y,−y),(−z,−z) so a broadcast LDS yields the packed operand.
-template <int CP>
+// Two pair forms, chosen per segment (uniform across the CTA):
+//  * centred (default where exact enough): with the block's box centre c,
+//    u = y' − c, v = x' − c:  −t = 2u·v − |u|² − |v|², so a packed pair of
+//    pairs costs FADD2 + 3 FFMA2 (+ FADD2 accumulate) and 2 MUFU.EX2;
+//  * difference: −t = −‖y' − x'‖² (3 FADD2 + FMUL2 + 2 FFMA2), used when
+//    the block's scaled radius makes the centred rounding (≈ 4ε·R²) too
+//    large (kCentredMaxR2).
+// f32x2 packing (FADD2/FMUL2/FFMA2, sm_100): each packed op evaluates two
+// (m, n) pairs; each lane rounds like the scalar op.
 __global__ void __launch_bounds__(128)
     estep_col_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4,
-                     int64_t n, int64_t m_per_split, const IterState* __restrict__ st,
-                     double* __restrict__ part, CullInfo cull) {
+                     int64_t n, const IterState* __restrict__ st, WorkList wl,
+                     double* __restrict__ seg, int allow_centred) {
   if (!st->active) return;
-  __shared__ float4 xa[kTile];  // (−x, −x, −y, −y)
-  __shared__ float2 xb[kTile];  // (−z, −z)
+  __shared__ float4 xa[kTile];  // centred (vx,vx,vy,vy) | diff (−x,−x,−y,−y)
+  __shared__ float4 xb[kTile];  // centred (vz,vz,−|v|²,−|v|²) | diff (−z,−z,·,·)
   const float s = st->sx;
-  const float s2 = s * s;
-  // tile culling: this CTA's 256 columns vs each 256-point model tile
-  float4 blo = make_float4(0.f, 0.f, 0.f, 0.f), bhi = blo;
-  float cut = INFINITY;
-  if (cull.enabled) {  // a column block is exactly one 256-point scene tile
-    blo = cull.ylo[blockIdx.x];
-    bhi = cull.yhi[blockIdx.x];
-    cut = s2 * cull.col_bound[blockIdx.x] + cull.margin1;
-  }
-  int evaluated = 0;
-  // column pair p of this thread: cols c, c+1 with c = base + p·256 + 2·tid
-  const int64_t cbase = static_cast<int64_t>(blockIdx.x) * (256 * CP) + 2 * threadIdx.x;
-  float2 yx[CP], yy[CP], yz[CP];
+  const int64_t G = gridDim.x, g = blockIdx.x;
+  const int64_t P = wl.off(wl.n_blocks) * kTile;
+  const int64_t p0 = sk_start(g, G, P), p1 = sk_start(g + 1, G, P);
+  if (p0 >= p1) return;
+  int rb = wl_block_of(wl, p0 / kTile);
+  for (int64_t p = p0; p < p1;) {
+    while (wl.off(rb + 1) * kTile <= p) ++rb;
+    const int64_t pe = min(p1, wl.off(rb + 1) * kTile);
+    __syncthreads();  // previous segment's readers of the shared box/tiles are done
+    // own columns of block rb
+    const int64_t c0 = static_cast<int64_t>(rb) * kTile + 2 * threadIdx.x;
+    float4 yv[2];
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-  for (int p = 0; p < CP; ++p) {
-    const int64_t c = cbase + p * 256;
-    const float4 a = c < n ? scale_pt(y4[c], s) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 b = c + 1 < n ? scale_pt(y4[c + 1], s) : make_float4(0.f, 0.f, 0.f, 0.f);
-    yx[p] = make_float2(a.x, b.x);
-    yy[p] = make_float2(a.y, b.y);
-    yz[p] = make_float2(a.z, b.z);
-  }
-  const int64_t m_begin = static_cast<int64_t>(blockIdx.y) * m_per_split;
-  const int64_t m_end = min(m, m_begin + m_per_split);
-  double dsum[CP][2];
-#pragma unroll
-  for (int p = 0; p < CP; ++p) dsum[p][0] = dsum[p][1] = 0.0;
-
-  for (int64_t base = m_begin; base < m_end; base += kTile) {
-    const int cnt = static_cast<int>(min(static_cast<int64_t>(kTile), m_end - base));
-    if (cull.enabled) {  // uniform across the CTA (same data, same math)
-      const int64_t tj = base / kTile;  // m_per_split is a multiple of kTile
-      if (s2 * box_mindist2(blo, bhi, cull.xlo[tj], cull.xhi[tj]) > cut) continue;
-    }
-    ++evaluated;
-    __syncthreads();
-    for (int i = threadIdx.x; i < kTile; i += 128) {
-      const float4 v = i < cnt ? scale_pt(xt4[base + i], s)
-                               : make_float4(kPadCoord, kPadCoord, kPadCoord, 0.f);
-      xa[i] = make_float4(-v.x, -v.x, -v.y, -v.y);
-      xb[i] = make_float2(-v.z, -v.z);
-    }
-    __syncthreads();
-    float2 fsum[CP];
-#pragma unroll
-    for (int p = 0; p < CP; ++p) fsum[p] = make_float2(0.f, 0.f);
-    const int cnt8 = (cnt + 7) & ~7;
-    for (int j = 0; j < cnt8; j += 8) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const float4 a = xa[j + u];
-        const float2 nx = make_float2(a.x, a.y), ny = make_float2(a.z, a.w);
-        const float2 nz = xb[j + u];
-#pragma unroll
-        for (int p = 0; p < CP; ++p) {
-          const float2 dx = __fadd2_rn(yx[p], nx);
-          const float2 dy = __fadd2_rn(yy[p], ny);
-          const float2 dz = __fadd2_rn(yz[p], nz);
-          float2 t = __fmul2_rn(dx, dx);
-          t = __ffma2_rn(dy, dy, t);
-          t = __ffma2_rn(dz, dz, t);
-          fsum[p] = __fadd2_rn(fsum[p], make_float2(ex2_approx(-t.x), ex2_approx(-t.y)));
-        }
+    for (int h = 0; h < 2; ++h) {
+      const int64_t c = c0 + h;
+      yv[h] = c < n ? scale_pt(y4[c], s) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c < n) {
+        lo[0] = fminf(lo[0], yv[h].x), hi[0] = fmaxf(hi[0], yv[h].x);
+        lo[1] = fminf(lo[1], yv[h].y), hi[1] = fmaxf(hi[1], yv[h].y);
+        lo[2] = fminf(lo[2], yv[h].z), hi[2] = fmaxf(hi[2], yv[h].z);
       }
     }
+    const BoxCentre bc = cta_box_centre(lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]);
+    const bool centred = allow_centred && bc.r2 <= kCentredMaxR2;
+    // per-thread operands: centred → 2u, −|u|²; diff → y'
+    float2 ox, oy, oz, on;
+    if (centred) {
+      float ux[2], uy[2], uz[2], q[2];
 #pragma unroll
-    for (int p = 0; p < CP; ++p) {
-      dsum[p][0] += static_cast<double>(fsum[p].x);
-      dsum[p][1] += static_cast<double>(fsum[p].y);
+      for (int h = 0; h < 2; ++h) {
+        ux[h] = __fsub_rn(yv[h].x, bc.c.x);
+        uy[h] = __fsub_rn(yv[h].y, bc.c.y);
+        uz[h] = __fsub_rn(yv[h].z, bc.c.z);
+        q[h] = __fmaf_rn(uz[h], uz[h], __fmaf_rn(uy[h], uy[h], __fmul_rn(ux[h], ux[h])));
+      }
+      ox = make_float2(2.f * ux[0], 2.f * ux[1]);
+      oy = make_float2(2.f * uy[0], 2.f * uy[1]);
+      oz = make_float2(2.f * uz[0], 2.f * uz[1]);
+      on = make_float2(-q[0], -q[1]);
+    } else {
+      ox = make_float2(yv[0].x, yv[1].x);
+      oy = make_float2(yv[0].y, yv[1].y);
+      oz = make_float2(yv[0].z, yv[1].z);
+      on = make_float2(0.f, 0.f);
     }
-  }
-  double* out = part + static_cast<int64_t>(blockIdx.y) * n;
+    double d0 = 0.0, d1 = 0.0;
+    for (int64_t q = p; q < pe;) {
+      const int64_t k = q / kTile - wl.off(rb);
+      const int a = static_cast<int>(q % kTile);
+      const int b = static_cast<int>(min(static_cast<int64_t>(kTile), a + (pe - q)));
+      const int64_t base = static_cast<int64_t>(wl.tile(rb, k)) * kTile + a;
+      const int cnt = static_cast<int>(max(int64_t(0), min(static_cast<int64_t>(b - a), m - base)));
+      q += b - a;
+      if (cnt == 0) continue;  // uniform
+      const int cnt8 = (cnt + 7) & ~7;
+      __syncthreads();
+      for (int i = threadIdx.x; i < cnt8; i += 128) {
+        if (centred) {
+          float4 v;
+          if (i < cnt) {
+            const float4 x = scale_pt(xt4[base + i], s);
+            v = make_float4(__fsub_rn(x.x, bc.c.x), __fsub_rn(x.y, bc.c.y),
+                            __fsub_rn(x.z, bc.c.z), 0.f);
+            v.w = -__fmaf_rn(v.z, v.z, __fmaf_rn(v.y, v.y, __fmul_rn(v.x, v.x)));
+          } else {  // padding row: −|v|² = −inf → 2^{−t} = 0 exactly
+            v = make_float4(0.f, 0.f, 0.f, -INFINITY);
+          }
+          xa[i] = make_float4(v.x, v.x, v.y, v.y);
+          xb[i] = make_float4(v.z, v.z, v.w, v.w);
+        } else {
+          const float4 v = i < cnt ? scale_pt(xt4[base + i], s)
+                                   : make_float4(kPadCoord, kPadCoord, kPadCoord, 0.f);
+          xa[i] = make_float4(-v.x, -v.x, -v.y, -v.y);
+          xb[i] = make_float4(-v.z, -v.z, 0.f, 0.f);
+        }
+      }
+      __syncthreads();
+      float2 f = make_float2(0.f, 0.f);
+      if (centred) {
+        for (int j = 0; j < cnt8; j += 8) {
 #pragma unroll
-  for (int p = 0; p < CP; ++p) {
-    const int64_t c = cbase + p * 256;
-    if (c < n) out[c] = dsum[p][0];
-    if (c + 1 < n) out[c + 1] = dsum[p][1];
+          for (int u = 0; u < 8; ++u) {
+            const float4 va = xa[j + u];
+            const float4 vb = xb[j + u];
+            float2 e = __fadd2_rn(on, make_float2(vb.z, vb.w));  // −|u|² − |v|²
+            e = __ffma2_rn(ox, make_float2(va.x, va.y), e);
+            e = __ffma2_rn(oy, make_float2(va.z, va.w), e);
+            e = __ffma2_rn(oz, make_float2(vb.x, vb.y), e);      // −t
+            f = __fadd2_rn(f, ex2x2(e));
+          }
+        }
+      } else {
+        for (int j = 0; j < cnt8; j += 8) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 va = xa[j + u];
+            const float4 vb = xb[j + u];
+            const float2 dx = __fadd2_rn(ox, make_float2(va.x, va.y));
+            const float2 dy = __fadd2_rn(oy, make_float2(va.z, va.w));
+            const float2 dz = __fadd2_rn(oz, make_float2(vb.x, vb.y));
+            float2 t = __fmul2_rn(dx, dx);
+            t = __ffma2_rn(dy, dy, t);
+            t = __ffma2_rn(dz, dz, t);
+            f = __fadd2_rn(f, ex2x2(make_float2(-t.x, -t.y)));
+          }
+        }
+      }
+      d0 += static_cast<double>(f.x);
+      d1 += static_cast<double>(f.y);
+    }
+    double* out = seg + (g + rb) * kTile;
+    out[2 * threadIdx.x] = d0;
+    out[2 * threadIdx.x + 1] = d1;
+    p = pe;
   }
-  if (cull.counters && threadIdx.x == 0) atomicAdd(cull.counters, (unsigned long long)evaluated);
 }
 
-// Pass 1 combine: fixed-order sum over splits; column normaliser b_n.
-// Flags columns whose mass is too small for the flush-to-zero fast path.
-__global__ void estep_col_combine_kernel(const double* __restrict__ part, int splits, int64_t m,
-                                         int64_t n, float4* __restrict__ y4b,
+// Sum of the segments of block b at local index li (lane-strided over the
+// block's CTAs, then a fixed xor tree): deterministic.
+template <int NQ>
+__device__ __forceinline__ void sum_segments(const WorkList& wl, int64_t G, const double* seg,
+                                             int b, int li, int lane, bool live, double (&a)[NQ]) {
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) a[k] = 0.0;
+  if (live) {
+    const int64_t P = wl.off(wl.n_blocks) * kTile;
+    const int64_t ua = wl.off(b) * kTile, ub = wl.off(b + 1) * kTile;
+    if (ua < ub) {
+      const int64_t g0 = sk_owner(ua, G, P), g1 = sk_owner(ub - 1, G, P);
+      for (int64_t g = g0 + lane; g <= g1; g += kCombineLanes) {
+        if (sk_start(g, G, P) == sk_start(g + 1, G, P)) continue;  // empty range
+        const double* sp = seg + (g + b) * NQ * kTile + li;
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) a[k] += sp[k * kTile];
+      }
+    }
+  }
+#pragma unroll
+  for (int o = kCombineLanes / 2; o > 0; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
+}
+
+// Pass 1 combine: column normaliser b_n.  Flags columns whose mass is too
+// small for the flush-to-zero fast path.
+__global__ void estep_col_combine_kernel(const double* __restrict__ seg, WorkList wl, int G,
+                                         int64_t m, int64_t n, float4* __restrict__ y4b,
                                          double* __restrict__ b2_out, double* __restrict__ pt1,
                                          int32_t* __restrict__ flag_list,
                                          int32_t* __restrict__ flag_count,
@@ -217,12 +360,11 @@ __global__ void estep_col_combine_kernel(const double* __restrict__ part, int sp
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t col = gid / kCombineLanes;
   const int lane = static_cast<int>(gid % kCombineLanes);
-  double sm = 0.0;
-  if (col < n)
-    for (int s = lane; s < splits; s += kCombineLanes) sm += part[static_cast<int64_t>(s) * n + col];
-#pragma unroll
-  for (int o = kCombineLanes / 2; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+  double a[1];
+  sum_segments<1>(wl, G, seg, static_cast<int>(col / kTile), static_cast<int>(col % kTile), lane,
+                  col < n, a);
   if (col >= n || lane != 0) return;
+  const double sm = a[0];
   const double log2c = st->log2c;
   const double c = exp2(log2c);  // 0 when ω = 0
   const double total = sm + c;
@@ -240,7 +382,7 @@ __global__ void estep_col_combine_kernel(const double* __restrict__ part, int sp
 }
 
 // Exact column normaliser for flagged columns: warp per column, max-shifted
-// log-sum-exp over all m in the same fp32 t_mn, fp64 accumulation.
+// log-sum-exp over all m in fp32 t_mn, fp64 accumulation.
 __global__ void estep_col_fallback_kernel(const float4* __restrict__ xt4, int64_t m,
                                           float4* __restrict__ y4b, double* __restrict__ b2_out,
                                           double* __restrict__ pt1,
@@ -280,138 +422,201 @@ __global__ void estep_col_fallback_kernel(const float4* __restrict__ xt4, int64_
 }
 
 // ---------------------------------------------------------------------------
-// Pass 2: per-row partial sums over one N-split: S0, Sy (3), SV.
-//
-// f32x2 packing over row pairs: per pair 6 packed FP32 issue slots (12
-// lane-ops: the FP32 pipe bound) + 1 MUFU.EX2.  Shared memory holds each
-// scene point as (y,y,y',y'),(z,z,b,b) so a broadcast LDS yields the packed
-// operands; the weight is w = 2^{b − t} (b − t = FFMA2(t, −1, b)).
-template <int RP>
-__global__ void __launch_bounds__(128)
+// Pass 2: per-row sums over n: S0, Sy (3), SV.  Own block = 256 model points
+// (thread: row pair 2·tid, 2·tid+1); the staged tiles are scene points.
+//  * centred: L = (b − |u|²) − |v|² + 2u·v with u = y' − c, v = x' − c, and
+//    the sums kept as Σw, Σw·u, Σw·|u|²; converted per segment in fp64:
+//      Σw·y' = Σw·u + c·Σw,  Σw·t = Σw·|u|² + |v|²·Σw − 2v·Σw·u.
+//    Per packed pair of pairs: FADD2 + 3 FFMA2 (L) + FADD2 + 4 FFMA2 (sums).
+//  * difference: t = ‖y' − x'‖², L = b − t; sums Σw, Σw·y', Σw·t directly.
+// The pass is bound by FP32 operand traffic (≈ one 64-bit register operand
+// per cycle per SMSP, measured: tools/loopbench.cu); the centred form needs
+// 25 operands per 2 pairs against 31.
+__global__ void __launch_bounds__(128, 8)
     estep_row_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4b,
-                     int64_t n, int64_t n_per_split, const IterState* __restrict__ st,
-                     double* __restrict__ part /* [split][5][m] */, int rb_offset,
-                     CullInfo cull) {
+                     int64_t n, const IterState* __restrict__ st, WorkList wl,
+                     double* __restrict__ seg /* [slot][5][256] */, int allow_centred) {
   if (!st->active) return;
-  __shared__ float4 ya[kTile];  // (yx, yx, yy, yy)
-  __shared__ float4 yb[kTile];  // (yz, yz, b, b)
+  __shared__ float4 ya[kTile];  // centred (ux,ux,uy,uy) | diff (y,y,y',y') scaled
+  __shared__ float4 yb[kTile];  // centred (uz,uz,b−|u|²,·) | diff (z,z,b,b)
+  __shared__ float2 yq[kTile];  // centred (|u|², |u|²)
+  // fp64 tile accumulators in shared memory (thread-private slots,
+  // [quantity][row][thread] → conflict-free): registers stay with the
+  // packed pipeline
+  __shared__ double acc_s[5][2][128];
   const float s = st->sx;
-  const float s2 = s * s;
-  const int64_t rbase =
-      static_cast<int64_t>(blockIdx.x + rb_offset) * (256 * RP) + 2 * threadIdx.x;
-  // tile culling: this CTA's 256 model rows vs each 256-point scene tile
-  float4 blo = make_float4(0.f, 0.f, 0.f, 0.f), bhi = blo;
-  float floor_l = -INFINITY;
-  if (cull.enabled) {  // a row block is exactly one 256-point model tile
-    const int64_t rb = blockIdx.x + rb_offset;
-    blo = cull.xlo[rb];
-    bhi = cull.xhi[rb];
-    floor_l = cull.row_bound[rb] - cull.margin2;
-  }
-  int evaluated = 0;
-  float2 nx[RP], ny[RP], nz[RP];
-#pragma unroll
-  for (int p = 0; p < RP; ++p) {
-    const int64_t r = rbase + p * 256;
-    const float4 pad = make_float4(kPadCoord, kPadCoord, kPadCoord, 0.f);
-    const float4 a = r < m ? scale_pt(xt4[r], s) : pad;
-    const float4 b = r + 1 < m ? scale_pt(xt4[r + 1], s) : pad;
-    nx[p] = make_float2(-a.x, -b.x);
-    ny[p] = make_float2(-a.y, -b.y);
-    nz[p] = make_float2(-a.z, -b.z);
-  }
-  const int64_t n_begin = static_cast<int64_t>(blockIdx.y) * n_per_split;
-  const int64_t n_end = min(n, n_begin + n_per_split);
-  // fp64 tile accumulators live in shared memory (thread-private slots,
-  // [quantity][row][thread] → conflict-free): keeps registers for the packed
-  // pipeline and raises occupancy (the pass is FP32-pipe bound).
-  __shared__ double acc_s[5][2 * RP][128];
-#pragma unroll
-  for (int k = 0; k < 5; ++k)
-#pragma unroll
-    for (int r = 0; r < 2 * RP; ++r) acc_s[k][r][threadIdx.x] = 0.0;
+  const int64_t G = gridDim.x, g = blockIdx.x;
+  const int64_t P = wl.off(wl.n_blocks) * kTile;
+  const int64_t p0 = sk_start(g, G, P), p1 = sk_start(g + 1, G, P);
+  if (p0 >= p1) return;
   const float2 minus1 = make_float2(-1.f, -1.f);
-
-  for (int64_t base = n_begin; base < n_end; base += kTile) {
-    const int cnt = static_cast<int>(min(static_cast<int64_t>(kTile), n_end - base));
-    if (cull.enabled) {  // L ≤ bmax − s²·mindist² < (row-max lower bound) − margin → skip
-      const int64_t tj = base / kTile;  // n_per_split is a multiple of kTile
-      const float lub = cull.bminmax[tj].y - s2 * box_mindist2(blo, bhi, cull.ylo[tj], cull.yhi[tj]);
-      if (lub < floor_l) continue;
-    }
-    ++evaluated;
-    __syncthreads();
-    for (int i = threadIdx.x; i < kTile; i += 128) {
-      // padding column: far away and b = −inf → weight exactly 0
-      const float4 v = i < cnt ? scale_pt(y4b[base + i], s)
-                               : make_float4(kPadCoord, kPadCoord, kPadCoord, -INFINITY);
-      ya[i] = make_float4(v.x, v.x, v.y, v.y);
-      yb[i] = make_float4(v.z, v.z, v.w, v.w);
-    }
-    __syncthreads();
-    float2 f0[RP], fx[RP], fy[RP], fz[RP], fv[RP];
-#pragma unroll
-    for (int p = 0; p < RP; ++p)
-      f0[p] = fx[p] = fy[p] = fz[p] = fv[p] = make_float2(0.f, 0.f);
-    const int cnt8 = (cnt + 7) & ~7;
-    for (int j = 0; j < cnt8; j += 8) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const float4 a = ya[j + u];
-        const float4 c = yb[j + u];
-        const float2 Yx = make_float2(a.x, a.y), Yy = make_float2(a.z, a.w);
-        const float2 Yz = make_float2(c.x, c.y), B = make_float2(c.z, c.w);
-#pragma unroll
-        for (int p = 0; p < RP; ++p) {
-          const float2 ddx = __fadd2_rn(Yx, nx[p]);
-          const float2 ddy = __fadd2_rn(Yy, ny[p]);
-          const float2 ddz = __fadd2_rn(Yz, nz[p]);
-          float2 t = __fmul2_rn(ddx, ddx);
-          t = __ffma2_rn(ddy, ddy, t);
-          t = __ffma2_rn(ddz, ddz, t);
-          const float2 L = __ffma2_rn(t, minus1, B);
-          const float2 w = make_float2(ex2_approx(L.x), ex2_approx(L.y));
-          f0[p] = __fadd2_rn(f0[p], w);
-          fx[p] = __ffma2_rn(w, Yx, fx[p]);
-          fy[p] = __ffma2_rn(w, Yy, fy[p]);
-          fz[p] = __ffma2_rn(w, Yz, fz[p]);
-          fv[p] = __ffma2_rn(w, t, fv[p]);
-        }
-      }
-    }
-#pragma unroll
-    for (int p = 0; p < RP; ++p) {
-      const int t = threadIdx.x;
-      acc_s[0][2 * p][t] += f0[p].x;
-      acc_s[0][2 * p + 1][t] += f0[p].y;
-      acc_s[1][2 * p][t] += fx[p].x;
-      acc_s[1][2 * p + 1][t] += fx[p].y;
-      acc_s[2][2 * p][t] += fy[p].x;
-      acc_s[2][2 * p + 1][t] += fy[p].y;
-      acc_s[3][2 * p][t] += fz[p].x;
-      acc_s[3][2 * p + 1][t] += fz[p].y;
-      acc_s[4][2 * p][t] += fv[p].x;
-      acc_s[4][2 * p + 1][t] += fv[p].y;
-    }
-  }
-  const int64_t sp = static_cast<int64_t>(blockIdx.y) * 5 * m;
-#pragma unroll
-  for (int p = 0; p < RP; ++p)
+  const int t = threadIdx.x;
+  int rb = wl_block_of(wl, p0 / kTile);
+  for (int64_t p = p0; p < p1;) {
+    while (wl.off(rb + 1) * kTile <= p) ++rb;
+    const int64_t pe = min(p1, wl.off(rb + 1) * kTile);
+    __syncthreads();  // previous segment's readers of the shared box/tiles are done
+    const int64_t r0 = static_cast<int64_t>(rb) * kTile + 2 * t;
+    float4 xv[2];
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int64_t row = rbase + p * 256 + h;
-      if (row < m) {
-#pragma unroll
-        for (int k = 0; k < 5; ++k) part[sp + k * m + row] = acc_s[k][2 * p + h][threadIdx.x];
+      const int64_t r = r0 + h;
+      xv[h] = r < m ? scale_pt(xt4[r], s) : make_float4(kPadCoord, kPadCoord, kPadCoord, 0.f);
+      if (r < m) {
+        lo[0] = fminf(lo[0], xv[h].x), hi[0] = fmaxf(hi[0], xv[h].x);
+        lo[1] = fminf(lo[1], xv[h].y), hi[1] = fmaxf(hi[1], xv[h].y);
+        lo[2] = fminf(lo[2], xv[h].z), hi[2] = fmaxf(hi[2], xv[h].z);
       }
     }
-  if (cull.counters && threadIdx.x == 0)
-    atomicAdd(cull.counters + 1, (unsigned long long)evaluated);
+    const BoxCentre bc = cta_box_centre(lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]);
+    const bool centred = allow_centred && bc.r2 <= kCentredMaxR2;
+    // per-thread operands: centred → 2v, −|v|² (and v, |v|² for the
+    // conversion); diff → −x'
+    float v[2][4];
+    float2 ox, oy, oz, on;
+    if (centred) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool ok = r0 + h < m;
+        v[h][0] = ok ? __fsub_rn(xv[h].x, bc.c.x) : 0.f;
+        v[h][1] = ok ? __fsub_rn(xv[h].y, bc.c.y) : 0.f;
+        v[h][2] = ok ? __fsub_rn(xv[h].z, bc.c.z) : 0.f;
+        v[h][3] = __fmaf_rn(v[h][2], v[h][2], __fmaf_rn(v[h][1], v[h][1], __fmul_rn(v[h][0], v[h][0])));
+      }
+      ox = make_float2(2.f * v[0][0], 2.f * v[1][0]);
+      oy = make_float2(2.f * v[0][1], 2.f * v[1][1]);
+      oz = make_float2(2.f * v[0][2], 2.f * v[1][2]);
+      on = make_float2(-v[0][3], -v[1][3]);
+    } else {
+      ox = make_float2(-xv[0].x, -xv[1].x);
+      oy = make_float2(-xv[0].y, -xv[1].y);
+      oz = make_float2(-xv[0].z, -xv[1].z);
+      on = make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k) acc_s[k][0][t] = acc_s[k][1][t] = 0.0;
+    for (int64_t q = p; q < pe;) {
+      const int64_t k = q / kTile - wl.off(rb);
+      const int a = static_cast<int>(q % kTile);
+      const int b = static_cast<int>(min(static_cast<int64_t>(kTile), a + (pe - q)));
+      const int64_t base = static_cast<int64_t>(wl.tile(rb, k)) * kTile + a;
+      const int cnt = static_cast<int>(max(int64_t(0), min(static_cast<int64_t>(b - a), n - base)));
+      q += b - a;
+      if (cnt == 0) continue;  // uniform
+      const int cnt8 = (cnt + 7) & ~7;
+      __syncthreads();
+      for (int i = t; i < cnt8; i += 128) {
+        if (centred) {
+          float4 u;
+          float uq;
+          if (i < cnt) {
+            const float4 y = scale_pt(y4b[base + i], s);
+            u = make_float4(__fsub_rn(y.x, bc.c.x), __fsub_rn(y.y, bc.c.y),
+                            __fsub_rn(y.z, bc.c.z), 0.f);
+            uq = __fmaf_rn(u.z, u.z, __fmaf_rn(u.y, u.y, __fmul_rn(u.x, u.x)));
+            u.w = __fsub_rn(y.w, uq);  // b − |u|²
+          } else {  // padding column: b = −inf → weight exactly 0
+            u = make_float4(0.f, 0.f, 0.f, -INFINITY);
+            uq = 0.f;
+          }
+          ya[i] = make_float4(u.x, u.x, u.y, u.y);
+          yb[i] = make_float4(u.z, u.z, u.w, u.w);
+          yq[i] = make_float2(uq, uq);
+        } else {
+          const float4 y = i < cnt ? scale_pt(y4b[base + i], s)
+                                   : make_float4(kPadCoord, kPadCoord, kPadCoord, -INFINITY);
+          ya[i] = make_float4(y.x, y.x, y.y, y.y);
+          yb[i] = make_float4(y.z, y.z, y.w, y.w);
+        }
+      }
+      __syncthreads();
+      float2 f0 = make_float2(0.f, 0.f), fx = f0, fy = f0, fz = f0, fv = f0;
+      if (centred) {
+        for (int j = 0; j < cnt8; j += 8) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 A = ya[j + u];
+            const float4 B = yb[j + u];
+            const float2 Q = yq[j + u];
+            const float2 Ux = make_float2(A.x, A.y), Uy = make_float2(A.z, A.w);
+            const float2 Uz = make_float2(B.x, B.y);
+            float2 L = __fadd2_rn(make_float2(B.z, B.w), on);  // b − |u|² − |v|²
+            L = __ffma2_rn(Ux, ox, L);
+            L = __ffma2_rn(Uy, oy, L);
+            L = __ffma2_rn(Uz, oz, L);                          // b − t
+            const float2 w = ex2x2(L);
+            f0 = __fadd2_rn(f0, w);
+            fx = __ffma2_rn(w, Ux, fx);
+            fy = __ffma2_rn(w, Uy, fy);
+            fz = __ffma2_rn(w, Uz, fz);
+            fv = __ffma2_rn(w, Q, fv);
+          }
+        }
+      } else {
+        for (int j = 0; j < cnt8; j += 8) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 A = ya[j + u];
+            const float4 B = yb[j + u];
+            const float2 Yx = make_float2(A.x, A.y), Yy = make_float2(A.z, A.w);
+            const float2 Yz = make_float2(B.x, B.y), Bn = make_float2(B.z, B.w);
+            const float2 ddx = __fadd2_rn(Yx, ox);
+            const float2 ddy = __fadd2_rn(Yy, oy);
+            const float2 ddz = __fadd2_rn(Yz, oz);
+            float2 tt = __fmul2_rn(ddx, ddx);
+            tt = __ffma2_rn(ddy, ddy, tt);
+            tt = __ffma2_rn(ddz, ddz, tt);
+            const float2 L = __ffma2_rn(tt, minus1, Bn);
+            const float2 w = ex2x2(L);
+            f0 = __fadd2_rn(f0, w);
+            fx = __ffma2_rn(w, Yx, fx);
+            fy = __ffma2_rn(w, Yy, fy);
+            fz = __ffma2_rn(w, Yz, fz);
+            fv = __ffma2_rn(w, tt, fv);
+          }
+        }
+      }
+      acc_s[0][0][t] += f0.x;
+      acc_s[0][1][t] += f0.y;
+      acc_s[1][0][t] += fx.x;
+      acc_s[1][1][t] += fx.y;
+      acc_s[2][0][t] += fy.x;
+      acc_s[2][1][t] += fy.y;
+      acc_s[3][0][t] += fz.x;
+      acc_s[3][1][t] += fz.y;
+      acc_s[4][0][t] += fv.x;
+      acc_s[4][1][t] += fv.y;
+    }
+    // segment out: S0, Σw·y', Σw·t per own row
+    double* out = seg + (g + rb) * 5 * kTile;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int li = 2 * t + h;
+      const double s0 = acc_s[0][h][t], s1 = acc_s[1][h][t], s2v = acc_s[2][h][t],
+                   s3 = acc_s[3][h][t], s4 = acc_s[4][h][t];
+      if (centred) {
+        const double vx = v[h][0], vy = v[h][1], vz = v[h][2], vq = v[h][3];
+        out[li] = s0;
+        out[kTile + li] = s1 + static_cast<double>(bc.c.x) * s0;
+        out[2 * kTile + li] = s2v + static_cast<double>(bc.c.y) * s0;
+        out[3 * kTile + li] = s3 + static_cast<double>(bc.c.z) * s0;
+        out[4 * kTile + li] = s4 + vq * s0 - 2.0 * (vx * s1 + vy * s2v + vz * s3);
+      } else {
+        out[li] = s0;
+        out[kTile + li] = s1;
+        out[2 * kTile + li] = s2v;
+        out[3 * kTile + li] = s3;
+        out[4 * kTile + li] = s4;
+      }
+    }
+    p = pe;
+  }
 }
 
 // ---------------------------------------------------------------------------
-// Tile geometry for culling (points are Morton-sorted by the engine, so
-// 256-point tiles are spatially compact).
+// Tile geometry and work lists for culling (points are Morton-sorted by the
+// engine, so 256-point tiles are spatially compact).
 
 // per-tile axis-aligned box of the first three coordinates (unscaled)
 __global__ void tile_bbox_kernel(const float4* __restrict__ p, int64_t count,
@@ -483,41 +688,115 @@ __global__ void tile_bminmax_kernel(const float4* __restrict__ y4b, int64_t n,
   }
 }
 
-// pass-1 bound per scene tile: U = min over model tiles of the largest
-// possible squared distance → every column has t_min ≤ s²·U.
-__global__ void col_bound_kernel(CullInfo cull, float* __restrict__ out, int n_blocks,
-                                 const IterState* __restrict__ st) {
-  if (!st->active) return;
-  const int lane = threadIdx.x & 31;
-  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (b >= n_blocks) return;
-  const float4 lo = cull.ylo[b], hi = cull.yhi[b];
-  float u = INFINITY;
-  for (int j = lane; j < cull.n_xtiles; j += 32)
-    u = fminf(u, box_maxdist2(lo, hi, cull.xlo[j], cull.xhi[j]));
+// The last CTA of a list kernel turns the per-block counts (offset[b+1])
+// into the exclusive prefix (in place), resets the done counter for the next
+// graph replay and adds the total to the evaluated-pairs counter.
+__device__ void last_cta_scan(int32_t* offset, int n_blocks, int32_t* done,
+                              unsigned long long* counter) {
+  __shared__ int is_last;
+  __shared__ int wsum[32];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(done, 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int carry = 0;
+  for (int base = 0; base < n_blocks; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    int v = i < n_blocks ? __ldcg(offset + i + 1) : 0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
-  if (lane == 0) out[b] = u;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane == 31) wsum[warp] = v;
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < nw; ++w) {
+      if (w < warp) before += wsum[w];
+      total += wsum[w];
+    }
+    if (i < n_blocks) offset[i + 1] = carry + before + v;
+    carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    offset[0] = 0;
+    *done = 0;
+    if (counter) *counter += static_cast<unsigned long long>(carry);
+  }
 }
 
-// pass-2 bound per model tile: a lower bound on max_n L_mn for every row,
-// L_lb = max over scene tiles of (min b − s²·maxdist²).
-__global__ void row_bound_kernel(CullInfo cull, float* __restrict__ out, int n_blocks,
-                                 const IterState* __restrict__ st) {
+// Pass-1 list: per scene tile b, U = min over model tiles of the largest
+// squared distance (every column has t_min ≤ s²·U, so its total is
+// ≥ 2^{−s²U}); keep model tile j unless s²·mindist²(b, j) > s²U + margin.
+__global__ void col_list_kernel(CullInfo cull, int32_t* __restrict__ tiles,
+                                int32_t* __restrict__ offset, int n_blocks,
+                                int32_t* __restrict__ done, const IterState* __restrict__ st) {
   if (!st->active) return;
   const float s2 = st->sx * st->sx;
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (b >= n_blocks) return;
-  const float4 lo = cull.xlo[b], hi = cull.xhi[b];
-  float l = -INFINITY;
-  for (int j = lane; j < cull.n_ytiles; j += 32)
-    l = fmaxf(l, cull.bminmax[j].x - s2 * box_maxdist2(lo, hi, cull.ylo[j], cull.yhi[j]));
+  if (b < n_blocks) {
+    const float4 lo = cull.ylo[b], hi = cull.yhi[b];
+    float u = INFINITY;
+    for (int j = lane; j < cull.n_xtiles; j += 32)
+      u = fminf(u, box_maxdist2(lo, hi, cull.xlo[j], cull.xhi[j]));
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) l = fmaxf(l, __shfl_xor_sync(0xffffffffu, l, o));
-  if (lane == 0) out[b] = l;
+    for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
+    const float cut = s2 * u + cull.margin1;
+    int count = 0;
+    int32_t* out = tiles + static_cast<int64_t>(b) * cull.n_xtiles;
+    for (int j0 = 0; j0 < cull.n_xtiles; j0 += 32) {
+      const int j = j0 + lane;
+      const bool keep =
+          j < cull.n_xtiles && !(s2 * box_mindist2(lo, hi, cull.xlo[j], cull.xhi[j]) > cut);
+      const unsigned mask = __ballot_sync(0xffffffffu, keep);
+      if (keep) out[count + __popc(mask & ((1u << lane) - 1))] = j;
+      count += __popc(mask);
+    }
+    if (lane == 0) offset[b + 1] = count;
+  }
+  last_cta_scan(offset, n_blocks, done, cull.counters);
 }
 
+// Pass-2 list: per model tile b, a lower bound on max_n L_mn of every row,
+// L_lb = max over scene tiles of (min b − s²·maxdist²); keep scene tile j
+// unless its largest possible L (max b − s²·mindist²) < L_lb − margin.
+__global__ void row_list_kernel(CullInfo cull, int32_t* __restrict__ tiles,
+                                int32_t* __restrict__ offset, int n_blocks,
+                                int32_t* __restrict__ done, const IterState* __restrict__ st) {
+  if (!st->active) return;
+  const float s2 = st->sx * st->sx;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b < n_blocks) {
+    const float4 lo = cull.xlo[b], hi = cull.xhi[b];
+    float l = -INFINITY;
+    for (int j = lane; j < cull.n_ytiles; j += 32)
+      l = fmaxf(l, cull.bminmax[j].x - s2 * box_maxdist2(lo, hi, cull.ylo[j], cull.yhi[j]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l = fmaxf(l, __shfl_xor_sync(0xffffffffu, l, o));
+    const float floor_l = l - cull.margin2;
+    int count = 0;
+    int32_t* out = tiles + static_cast<int64_t>(b) * cull.n_ytiles;
+    for (int j0 = 0; j0 < cull.n_ytiles; j0 += 32) {
+      const int j = j0 + lane;
+      const bool keep =
+          j < cull.n_ytiles &&
+          !(cull.bminmax[j].y - s2 * box_mindist2(lo, hi, cull.ylo[j], cull.yhi[j]) < floor_l);
+      const unsigned mask = __ballot_sync(0xffffffffu, keep);
+      if (keep) out[count + __popc(mask & ((1u << lane) - 1))] = j;
+      count += __popc(mask);
+    }
+    if (lane == 0) offset[b + 1] = count;
+  }
+  last_cta_scan(offset, n_blocks, done, cull.counters ? cull.counters + 1 : nullptr);
+}
+
+// ---------------------------------------------------------------------------
 // Row finalisation shared by the combine and the fallback.
 __device__ __forceinline__ void finalize_row(int64_t row, int64_t m, double log2p1, double s0,
                                              double sy0, double sy1, double sy2, double sv,
@@ -556,45 +835,41 @@ __device__ __forceinline__ void finalize_row(int64_t row, int64_t m, double log2
   }
 }
 
-__global__ void estep_row_combine_kernel(const double* __restrict__ part, int splits, int64_t m,
-                                         int64_t n, const double* __restrict__ xt64,
+__global__ void estep_row_combine_kernel(const double* __restrict__ seg, WorkList wl, int G,
+                                         int64_t m, int64_t n, const double* __restrict__ xt64,
                                          RowOut out, YStats ys, int32_t* __restrict__ flag_list,
-                                         int32_t* __restrict__ flag_count, IterState* st,
-                                         int64_t r0, int64_t r1) {
+                                         int32_t* __restrict__ flag_count, IterState* st) {
   if (!st->active) return;
-  // kCombineLanes lanes per row, lane j sums splits j, j+L, … then a fixed
-  // xor-tree combines the lanes: deterministic, and L× the memory-level
-  // parallelism of one thread per row.  Rows [r0, r1) of this launch.
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t row = r0 + gid / kCombineLanes;
+  const int64_t row = gid / kCombineLanes;
   const int lane = static_cast<int>(gid % kCombineLanes);
-  const bool live = row < r1;
-  double a0 = 0, ax = 0, ay = 0, az = 0, av = 0;
-  if (live) {
-    for (int sp = lane; sp < splits; sp += kCombineLanes) {
-      const double* p = part + static_cast<int64_t>(sp) * 5 * m;
-      a0 += p[row];
-      ax += p[m + row];
-      ay += p[2 * m + row];
-      az += p[3 * m + row];
-      av += p[4 * m + row];
-    }
-  }
-#pragma unroll
-  for (int o = kCombineLanes / 2; o > 0; o >>= 1) {
-    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-    ax += __shfl_xor_sync(0xffffffffu, ax, o);
-    ay += __shfl_xor_sync(0xffffffffu, ay, o);
-    az += __shfl_xor_sync(0xffffffffu, az, o);
-    av += __shfl_xor_sync(0xffffffffu, av, o);
-  }
-  if (!live || lane != 0) return;
-  if (!(a0 >= static_cast<double>(n) * 0x1p-76)) {
+  double a[5];
+  sum_segments<5>(wl, G, seg, static_cast<int>(row / kTile), static_cast<int>(row % kTile), lane,
+                  row < m, a);
+  if (row >= m || lane != 0) return;
+  if (!(a[0] >= static_cast<double>(n) * 0x1p-76)) {
     const int slot = atomicAdd(flag_count, 1);
     flag_list[slot] = static_cast<int32_t>(row);
     return;
   }
-  finalize_row(row, m, log2(a0), a0, ax, ay, az, av, xt64, derived_scale(st), out, ys, st);
+  finalize_row(row, m, log2(a[0]), a[0], a[1], a[2], a[3], a[4], xt64, derived_scale(st), out, ys,
+               st);
+}
+
+// distributed: AoS row sums [m_pad][5] of the local scene shard
+__global__ void row_seg_sum_kernel(const double* __restrict__ seg, WorkList wl, int G, int64_t m,
+                                   int64_t m_pad, double* __restrict__ out,
+                                   const IterState* __restrict__ st) {
+  if (!st->active) return;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t row = gid / kCombineLanes;
+  const int lane = static_cast<int>(gid % kCombineLanes);
+  double a[5];
+  sum_segments<5>(wl, G, seg, static_cast<int>(row / kTile), static_cast<int>(row % kTile), lane,
+                  row < m, a);
+  if (row < m_pad && lane == 0)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) out[row * 5 + k] = a[k];
 }
 
 // Exact row accumulation for flagged rows (tiny mass): warp per row,
@@ -646,65 +921,41 @@ __global__ void estep_row_fallback_kernel(const float4* __restrict__ xt4, int64_
 }
 
 // ---------------------------------------------------------------------------
-// Host-side launcher.
-
-// Split the reduction axis so the grid fills whole waves: CTAs are uniform,
-// so wave efficiency = T / (ceil(T/slots)·slots) with T = blocks × splits.
-// Take the fewest splits reaching ≥ 96 % (or the best found), keeping ≥ 128
-// reduction points per split.
-static int choose_splits(int blocks, int64_t len, int slots) {
-  const int max_s = static_cast<int>(std::max<int64_t>(1, len / 128));
-  int best = 1;
-  double best_eff = -1.0;
-  for (int s = 1; s <= max_s; ++s) {
-    const int64_t per = ceil_div(len, s);
-    const int real = ceil_div(len, per);  // splits actually produced
-    const int64_t t = static_cast<int64_t>(blocks) * real;
-    const double waves = std::ceil(static_cast<double>(t) / slots);
-    const double eff = static_cast<double>(t) / (waves * slots);
-    if (t < slots && s < max_s) continue;  // want at least one full wave
-    if (eff >= 0.96) return s;
-    if (eff > best_eff + 1e-9) {
-      best_eff = eff;
-      best = s;
-    }
-  }
-  return best;
-}
+// Host-side launchers.
 
 EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
   EStepPlan p;
+  if (const char* e = std::getenv("FCPD_ESTEP_FORM")) p.centred = std::strcmp(e, "diff") != 0;
   int occ_col = 0, occ_row = 0;
-  FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &occ_col, estep_col_kernel<kColsPerThread / 2>, 128, 0));
-  FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &occ_row, estep_row_kernel<kRowsPerThread / 2>, 128, 0));
-  p.col_blocks = ceil_div(n, 128 * kColsPerThread);
-  const int s1 = choose_splits(p.col_blocks, m, sm_count * std::max(occ_col, 1));
-  // splits on 256-point tile boundaries (culling tests whole tiles)
-  p.m_per_split = static_cast<int64_t>(ceil_div(ceil_div(m, s1), kTile)) * kTile;
-  p.col_splits = ceil_div(m, p.m_per_split);
-  p.row_blocks = ceil_div(m, 128 * kRowsPerThread);
-  const int s2 = choose_splits(p.row_blocks, n, sm_count * std::max(occ_row, 1));
-  p.n_per_split = static_cast<int64_t>(ceil_div(ceil_div(n, s2), kTile)) * kTile;
-  p.row_splits = ceil_div(n, p.n_per_split);
-  p.chunks = 1;
+  FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_col, estep_col_kernel, 128, 0));
+  FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_row, estep_row_kernel, 128, 0));
+  p.col_blocks = static_cast<int>(ceil_div(n, kTile));
+  p.row_blocks = static_cast<int>(ceil_div(m, kTile));
+  p.col_grid = sm_count * std::max(occ_col, 1);
+  p.row_grid = sm_count * std::max(occ_row, 1);
   return p;
 }
 
-void plan_row_chunks(EStepPlan& p, int64_t m, int64_t n, int sm_count, int chunks) {
-  int occ_row = 0;
-  FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &occ_row, estep_row_kernel<kRowsPerThread / 2>, 128, 0));
-  p.chunks = chunks;
-  for (int c = 0; c < chunks; ++c) {
-    const int rb = static_cast<int>(static_cast<int64_t>(p.row_blocks) * (c + 1) / chunks -
-                                    static_cast<int64_t>(p.row_blocks) * c / chunks);
-    const int s = choose_splits(std::max(rb, 1), n, sm_count * std::max(occ_row, 1));
-    p.chunk_nps[c] = static_cast<int64_t>(ceil_div(ceil_div(n, s), kTile)) * kTile;
-    p.chunk_splits[c] = ceil_div(n, p.chunk_nps[c]);
-  }
+namespace {
+WorkList pass1_list(const EStepPlan& p, const EStepBuffers& b, int64_t m) {
+  WorkList wl;
+  wl.implicit = b.cull.enabled ? 0 : 1;
+  wl.n_blocks = p.col_blocks;
+  wl.n_other = static_cast<int>(ceil_div(m, kTile));
+  wl.tiles = b.wl1.tiles;
+  wl.offset = b.wl1.offset;
+  return wl;
 }
+WorkList pass2_list(const EStepPlan& p, const EStepBuffers& b, int64_t n) {
+  WorkList wl;
+  wl.implicit = b.cull.enabled ? 0 : 1;
+  wl.n_blocks = p.row_blocks;
+  wl.n_other = static_cast<int>(ceil_div(n, kTile));
+  wl.tiles = b.wl2.tiles;
+  wl.offset = b.wl2.offset;
+  return wl;
+}
+}  // namespace
 
 void launch_estep_prologue(IterState* st, int64_t m, int64_t n_global, int d, double omega,
                            int32_t* flags_count, uint64_t* stamps, cudaStream_t stream) {
@@ -719,23 +970,23 @@ void launch_tile_bbox(const float4* pts, int64_t count, float4* lo, float4* hi,
 }
 
 // Pass 1 (column normalisers) + the culling geometry around it: model-tile
-// boxes of this iteration's x̃ and the per-block bounds before, scene-tile
-// b ranges and row bounds after (pass 2 reads them).
+// boxes of this iteration's x̃ and the pass-1 work list before, scene-tile
+// b ranges after (the pass-2 list reads them).
 void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
                         IterState* st, cudaStream_t stream) {
   const CullInfo& cu = b.cull;
+  const WorkList wl = pass1_list(p, b, m);
   if (cu.enabled) {
     launch_tile_bbox(b.xt4, m, b.cullw.xlo, b.cullw.xhi, st, stream);
-    col_bound_kernel<<<ceil_div(p.col_blocks, 8), 256, 0, stream>>>(cu, b.cullw.col_bound,
-                                                                    p.col_blocks, st);
+    col_list_kernel<<<ceil_div(p.col_blocks, 8), 256, 0, stream>>>(
+        cu, b.wl1.tiles, b.wl1.offset, p.col_blocks, b.wl1.done, st);
     FCPD_LAUNCH_CHECK();
   }
-  estep_col_kernel<kColsPerThread / 2>
-      <<<dim3(p.col_blocks, p.col_splits), 128, 0, stream>>>(b.xt4, m, b.y4b, n, p.m_per_split,
-                                                             st, b.col_part, cu);
+  estep_col_kernel<<<p.col_grid, 128, 0, stream>>>(b.xt4, m, b.y4b, n, st, wl, b.col_seg,
+                                                   p.centred);
   FCPD_LAUNCH_CHECK();
   estep_col_combine_kernel<<<ceil_div(n * kCombineLanes, 256), 256, 0, stream>>>(
-      b.col_part, p.col_splits, m, n, b.y4b, b.b2, b.pt1, b.col_flags, b.flags_count, st);
+      b.col_seg, wl, p.col_grid, m, n, b.y4b, b.b2, b.pt1, b.col_flags, b.flags_count, st);
   FCPD_LAUNCH_CHECK();
   estep_col_fallback_kernel<<<148, 256, 0, stream>>>(b.xt4, m, b.y4b, b.b2, b.pt1, b.col_flags,
                                                      b.flags_count, st);
@@ -743,17 +994,42 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
   if (cu.enabled) {
     tile_bminmax_kernel<<<ceil_div(n, kTile), kTile, 0, stream>>>(b.y4b, n, b.cullw.bminmax, st);
     FCPD_LAUNCH_CHECK();
-    row_bound_kernel<<<ceil_div(p.row_blocks, 8), 256, 0, stream>>>(cu, b.cullw.row_bound,
-                                                                    p.row_blocks, st);
-    FCPD_LAUNCH_CHECK();
   }
 }
 
 void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int64_t m,
                                  int64_t n, IterState* st, cudaStream_t stream) {
-  estep_row_kernel<kRowsPerThread / 2>
-      <<<dim3(p.row_blocks, p.row_splits), 128, 0, stream>>>(b.xt4, m, b.y4b, n, p.n_per_split,
-                                                             st, b.row_part, 0, b.cull);
+  const CullInfo& cu = b.cull;
+  const WorkList wl = pass2_list(p, b, n);
+  if (cu.enabled) {
+    row_list_kernel<<<ceil_div(p.row_blocks, 8), 256, 0, stream>>>(
+        cu, b.wl2.tiles, b.wl2.offset, p.row_blocks, b.wl2.done, st);
+    FCPD_LAUNCH_CHECK();
+  }
+  estep_row_kernel<<<p.row_grid, 128, 0, stream>>>(b.xt4, m, b.y4b, n, st, wl, b.row_seg,
+                                                   p.centred);
+  FCPD_LAUNCH_CHECK();
+}
+
+void launch_estep_pass2(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
+                        IterState* st, cudaStream_t stream) {
+  launch_estep_pass2_partials(p, b, m, n, st, stream);
+  const WorkList wl = pass2_list(p, b, n);
+  int32_t* list = b.row_flags;
+  int32_t* count = b.flags_count + 1;
+  estep_row_combine_kernel<<<ceil_div(m * kCombineLanes, 256), 256, 0, stream>>>(
+      b.row_seg, wl, p.row_grid, m, n, b.xt64, b.out, b.ystats, list, count, st);
+  FCPD_LAUNCH_CHECK();
+  estep_row_fallback_kernel<<<148, 256, 0, stream>>>(b.xt4, m, b.y4b, n, b.xt64, b.out,
+                                                     b.ystats, list, count, st);
+  FCPD_LAUNCH_CHECK();
+}
+
+void launch_row_seg_sum(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
+                        int64_t m_pad, double* out, const IterState* st, cudaStream_t stream) {
+  const WorkList wl = pass2_list(p, b, n);
+  row_seg_sum_kernel<<<ceil_div(m_pad * kCombineLanes, 256), 256, 0, stream>>>(
+      b.row_seg, wl, p.row_grid, m, m_pad, out, st);
   FCPD_LAUNCH_CHECK();
 }
 
@@ -764,40 +1040,7 @@ void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t 
   FCPD_LAUNCH_CHECK();
   launch_estep_pass1(p, b, m, n, st, stream);
   if (mid) FCPD_CUDA(cudaEventRecord(mid, stream));
-  launch_estep_pass2_chunk(p, b, m, n, st, stream, 0, 1);
-}
-
-RowChunk row_chunk(const EStepPlan& p, int64_t m, int c, int chunks) {
-  RowChunk r;
-  r.rb0 = static_cast<int>(static_cast<int64_t>(p.row_blocks) * c / chunks);
-  r.rb1 = static_cast<int>(static_cast<int64_t>(p.row_blocks) * (c + 1) / chunks);
-  r.r0 = std::min<int64_t>(m, static_cast<int64_t>(r.rb0) * 128 * kRowsPerThread);
-  r.r1 = std::min<int64_t>(m, static_cast<int64_t>(r.rb1) * 128 * kRowsPerThread);
-  return r;
-}
-
-// Pass 2 for the model rows of chunk c of `chunks`: partial sums, combine,
-// exact fallback for this chunk's flagged rows (its own list/counter), so
-// the rows' P̃Y / residual are final when the launch sequence returns and a
-// consumer (the Qᵀ·R stream of the same rows) can start on another stream.
-void launch_estep_pass2_chunk(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
-                              IterState* st, cudaStream_t stream, int c, int chunks) {
-  const RowChunk rc = row_chunk(p, m, c, chunks);
-  if (rc.rb1 <= rc.rb0) return;
-  const bool own = chunks > 1 && p.chunks == chunks;
-  const int splits = own ? p.chunk_splits[c] : p.row_splits;
-  const int64_t nps = own ? p.chunk_nps[c] : p.n_per_split;
-  estep_row_kernel<kRowsPerThread / 2><<<dim3(rc.rb1 - rc.rb0, splits), 128, 0, stream>>>(
-      b.xt4, m, b.y4b, n, nps, st, b.row_part, rc.rb0, b.cull);
-  FCPD_LAUNCH_CHECK();
-  int32_t* list = b.row_flags + rc.r0;
-  int32_t* count = b.flags_count + 1 + c;
-  estep_row_combine_kernel<<<ceil_div((rc.r1 - rc.r0) * kCombineLanes, 256), 256, 0, stream>>>(
-      b.row_part, splits, m, n, b.xt64, b.out, b.ystats, list, count, st, rc.r0, rc.r1);
-  FCPD_LAUNCH_CHECK();
-  estep_row_fallback_kernel<<<148, 256, 0, stream>>>(b.xt4, m, b.y4b, n, b.xt64, b.out,
-                                                     b.ystats, list, count, st);
-  FCPD_LAUNCH_CHECK();
+  launch_estep_pass2(p, b, m, n, st, stream);
 }
 
 }  // namespace fcpd

@@ -10,11 +10,7 @@
 
 namespace fcpd {
 
-// one column pair / row pair per thread: a 128-thread CTA covers exactly one
-// 256-point tile, the culling granularity
-constexpr int kColsPerThread = 2;
-constexpr int kRowsPerThread = 2;
-constexpr int kMaxRowChunks = 8;  // pass-2 row chunks (overlap with the Qᵀ·R stream)
+constexpr int kTilePts = 256;  // points per tile (a CTA's own block, a staged tile)
 
 // Fallback-path per-row outputs (all device pointers; SoA fp64 M×3).
 struct RowOut {
@@ -32,29 +28,46 @@ struct YStats {
   double sq_mean;
 };
 
-struct EStepPlan {
-  int col_blocks = 0, col_splits = 0;
-  int64_t m_per_split = 0;
-  int row_blocks = 0, row_splits = 0;
-  int64_t n_per_split = 0;
-  // per-chunk pass-2 splits when pass 2 runs as row chunks (overlap form):
-  // fewer row blocks per launch need more N-splits to fill the GPU
-  int chunks = 1;
-  int chunk_splits[kMaxRowChunks] = {};
-  int64_t chunk_nps[kMaxRowChunks] = {};
-  int max_row_splits() const {
-    int s = row_splits;
-    for (int c = 0; c < chunks; ++c) s = chunk_splits[c] > s ? chunk_splits[c] : s;
-    return s;
+// The work of one pass: for each of n_blocks own 256-point blocks (scene
+// tiles in pass 1, model tiles in pass 2), the list of tiles of the other
+// set whose pairs are evaluated.  Units = (block, tile) pairs in block-major
+// order; offset[b] = units before block b.  implicit = every tile of every
+// block (no culling): tiles/offset are not read.
+struct WorkList {
+  int implicit = 1;
+  int n_blocks = 0, n_other = 0;
+  const int32_t* tiles = nullptr;   // [n_blocks][n_other]
+  const int32_t* offset = nullptr;  // [n_blocks + 1]
+  __host__ __device__ int64_t off(int b) const {
+    return implicit ? static_cast<int64_t>(b) * n_other : static_cast<int64_t>(offset[b]);
+  }
+  __host__ __device__ int tile(int b, int64_t k) const {
+    return implicit ? static_cast<int>(k) : tiles[static_cast<int64_t>(b) * n_other + k];
   }
 };
-void plan_row_chunks(EStepPlan& p, int64_t m, int64_t n, int sm_count, int chunks);
 
-// Tile culling.  Points are Morton-sorted by the engine
-// so 256-point tiles are compact boxes; a (column block, model tile) or (row
-// block, scene tile) pair is skipped when every pair term in it is below
-// 2^-margin of the smallest possible column (row) total.  With margin =
-// 50 + log2(count) the skipped mass is ≤ 2^-50 relative: exact to fp32.
+struct WorkListBuffers {  // writable views (engine-owned)
+  int32_t* tiles = nullptr;
+  int32_t* offset = nullptr;
+  int32_t* done = nullptr;  // last-CTA counter of the list kernel (self-resetting)
+};
+
+// Persistent stream-K schedule of both passes (one CTA wave per pass).
+struct EStepPlan {
+  int centred = 1;  // tile-centred pair form where exact enough; FCPD_ESTEP_FORM=diff → off
+  int col_blocks = 0, row_blocks = 0;  // scene tiles (pass-1 blocks), model tiles (pass 2)
+  int col_grid = 0, row_grid = 0;      // persistent CTAs per pass
+  size_t col_seg_doubles() const { return static_cast<size_t>(col_grid + col_blocks) * kTilePts; }
+  size_t row_seg_doubles() const {
+    return static_cast<size_t>(row_grid + row_blocks) * 5 * kTilePts;
+  }
+};
+
+// Tile culling.  Points are Morton-sorted by the engine so
+// 256-point tiles are compact boxes; a (block, tile) pair is dropped from
+// the work list when every pair term in it is below 2^-margin of the
+// smallest possible column (row) total.  With margin = 50 + log2(count) the
+// skipped mass is ≤ 2^-50 relative: exact to fp32.
 struct CullInfo {
   int enabled = 0;
   int n_xtiles = 0, n_ytiles = 0;   // 256-point tiles
@@ -62,16 +75,13 @@ struct CullInfo {
   const float4* xhi = nullptr;
   const float4* ylo = nullptr;      // scene tiles (fixed)
   const float4* yhi = nullptr;
-  const float* col_bound = nullptr; // per scene tile: U (unscaled d²)
-  const float* row_bound = nullptr; // per model tile: lower bound of max L (log2)
   const float2* bminmax = nullptr;  // per scene tile: (min b, max b)
   float margin1 = 0.f, margin2 = 0.f;
-  unsigned long long* counters = nullptr;  // [0] pass-1 tiles, [1] pass-2 tiles evaluated
+  unsigned long long* counters = nullptr;  // [0] pass-1, [1] pass-2 tile pairs evaluated
 };
 
 struct CullBuffers {  // writable views of the CullInfo arrays (engine-owned)
   float4 *xlo, *xhi, *ylo, *yhi;
-  float *col_bound, *row_bound;
   float2* bminmax;
 };
 
@@ -81,15 +91,16 @@ struct EStepBuffers {
   float4* y4b;         // y fp32 (x,y,z,b2), N — .w written by pass 1
   double* b2;          // b_n fp64 (log2 units), N
   double* pt1;         // optional Σ_m P_mn, N
-  double* col_part;    // [col_splits][N]
-  double* row_part;    // [row_splits][5][M]
+  double* col_seg;     // pass-1 segment partials [col_grid + col_blocks][256]
+  double* row_seg;     // pass-2 segment partials [row_grid + row_blocks][5][256]
   int32_t* col_flags;  // N
   int32_t* row_flags;  // M
   int32_t* flags_count;  // 2
   RowOut out;
   YStats ystats;
-  CullInfo cull;      // cull.enabled = 0 → dense (every pair evaluated)
+  CullInfo cull;      // cull.enabled = 0 → implicit work lists (every pair evaluated)
   CullBuffers cullw;  // geometry buffers written each iteration
+  WorkListBuffers wl1, wl2;  // pass-1 / pass-2 work lists (used when culling)
 };
 
 // Scene-tile boxes (once per session; Y does not move).
@@ -103,16 +114,16 @@ void launch_estep_prologue(IterState* st, int64_t m, int64_t n_global, int d, do
                            int32_t* flags_count, uint64_t* stamps, cudaStream_t stream);
 void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
                         IterState* st, cudaStream_t stream);
+// pass-2 work list + segment partials (no combine)
 void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int64_t m,
                                  int64_t n, IterState* st, cudaStream_t stream);
-
-struct RowChunk {
-  int rb0 = 0, rb1 = 0;      // row blocks
-  int64_t r0 = 0, r1 = 0;    // model rows
-};
-RowChunk row_chunk(const EStepPlan& p, int64_t m, int c, int chunks);
-void launch_estep_pass2_chunk(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
-                              IterState* st, cudaStream_t stream, int c, int chunks);
+// pass 2 complete: partials, combine, exact fallback of flagged rows
+void launch_estep_pass2(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
+                        IterState* st, cudaStream_t stream);
+// distributed: per-row sums of the pass-2 segments as AoS [m_pad][5]
+// (rows ≥ m are zero) for the reduce-scatter
+void launch_row_seg_sum(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
+                        int64_t m_pad, double* out, const IterState* st, cudaStream_t stream);
 void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n, int d,
                   double omega, IterState* st, uint64_t* stamps, cudaStream_t stream,
                   cudaEvent_t mid = nullptr);

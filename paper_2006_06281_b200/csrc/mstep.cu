@@ -512,56 +512,6 @@ void launch_colsum(const ColsumPlan& p, const float* A, int64_t lda, const float
   FCPD_LAUNCH_CHECK();
 }
 
-struct ZChunks {
-  int n;
-  SkGeom g[kMaxChunkPlans];
-  const double* part[kMaxChunkPlans];
-};
-
-__global__ void zreduce_chunks_kernel(ZChunks zc, int64_t k, const double* __restrict__ lam,
-                                      const double* __restrict__ lam_num, double lambda_reg,
-                                      double* __restrict__ coef, float4* __restrict__ g4,
-                                      IterState* st) {
-  if (!st->active) return;
-  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t i = gid / kSkLanes;
-  const int lane = static_cast<int>(gid % kSkLanes);
-  double z0 = 0, z1 = 0, z2 = 0;
-  for (int c = 0; c < zc.n; ++c) {  // fixed chunk order
-    double a0, a1, a2;
-    sk_sum_lanes(zc.part[c], zc.g[c], i < k ? i : k - 1, lane, a0, a1, a2);
-    z0 += a0;
-    z1 += a1;
-    z2 += a2;
-  }
-  if (i >= k || lane) return;
-  const double diag = lam[i] + lambda_reg * st->sigma2;
-  if (!(diag > 0.0)) set_error(st, kDevSolveDiag, diag);
-  const double inv = 1.0 / diag;
-  coef[i] = z0 * inv;
-  coef[k + i] = z1 * inv;
-  coef[2 * k + i] = z2 * inv;
-  const double f = lam_num[i] * inv;
-  g4[i] = make_float4(static_cast<float>(z0 * f), static_cast<float>(z1 * f),
-                      static_cast<float>(z2 * f), 0.f);
-}
-
-void launch_zreduce_chunks(const ColsumPlan* plans, const double* const* parts, int chunks,
-                           const double* lam, const double* lam_num, double lambda_reg,
-                           double* coef, float4* g4, IterState* st, cudaStream_t stream) {
-  if (chunks < 1 || chunks > kMaxChunkPlans) throw Failure(FCPD_ERR_PARAMETER, "zreduce: chunks");
-  ZChunks zc{};
-  zc.n = chunks;
-  for (int c = 0; c < chunks; ++c) {
-    zc.g[c] = geom(plans[c]);
-    zc.part[c] = parts[c];
-  }
-  const int64_t k = plans[0].cols;
-  zreduce_chunks_kernel<<<ceil_div(k * kSkLanes, 256), 256, 0, stream>>>(zc, k, lam, lam_num,
-                                                                         lambda_reg, coef, g4, st);
-  FCPD_LAUNCH_CHECK();
-}
-
 void launch_zreduce(const ColsumPlan& p, const double* part, const double* lam,
                     const double* lam_num, double lambda_reg, double* coef, float4* g4,
                     IterState* st, cudaStream_t stream) {

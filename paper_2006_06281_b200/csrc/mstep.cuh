@@ -9,7 +9,6 @@
 namespace fcpd {
 
 constexpr int kColsumThreads = 256;
-constexpr int kMaxChunkPlans = 8;  // ≥ kMaxRowChunks (estep.cuh)
 constexpr int kColsPerBlock = 4 * kColsumThreads;  // 1024 columns per column block
 
 // Stream-K plan for "column sums of a row-major matrix weighted by a per-row
@@ -28,15 +27,8 @@ struct ColsumPlan {
   }
 };
 
-// ctas_per_sm: resident bulk CTAs per SM the grid assumes (2 = whole GPU;
-// 1 = leave room for concurrently running E-step CTAs).
+// ctas_per_sm: resident bulk CTAs per SM the grid assumes (2 = whole GPU).
 ColsumPlan make_colsum_plan(int64_t rows, int64_t cols, int sm_count, int ctas_per_sm = 2);
-
-// z over several row-chunk plans (each with its own partial buffer), summed
-// per column in chunk order, then the filter of launch_zreduce.
-void launch_zreduce_chunks(const ColsumPlan* plans, const double* const* parts, int chunks,
-                           const double* lam, const double* lam_num, double lambda_reg,
-                           double* coef, float4* g4, IterState* st, cudaStream_t stream);
 
 // part ← partials of Σ_r A[r][c]·v[r].d (d < 3); A row-major fp32, lda % 4 == 0.
 void launch_colsum(const ColsumPlan& p, const float* A, int64_t lda, const float4* v,

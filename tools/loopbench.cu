@@ -1,0 +1,206 @@
+// loopbench.cu — throughput of the E-step inner loops in isolation (B200).
+//
+// Each variant replays its pass's inner loop over 256 shared-memory points
+// R times (no syncs, no global traffic) at the real kernels' occupancy, and
+// reports cycles per point-warp (64 pairs): the achievable ceiling the
+// full kernels are compared against.
+//   row_diff / col_diff : difference form (estep_row_kernel / estep_col_kernel)
+//   row_ctr  / col_ctr  : centred form (estep_row_kernel_c / estep_col_kernel_c)
+//   *_nomufu            : same FP32 work, ex2 replaced by a register move
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/loopbench tools/loopbench.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int kPts = 256;
+constexpr int kReps = 64;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+template <bool M>
+__device__ __forceinline__ float2 ex2v(float2 v) {
+  if (M) return make_float2(ex2(v.x), ex2(v.y));
+  return make_float2(v.y, v.x);
+}
+
+template <int V, bool MUFU>
+__global__ void __launch_bounds__(128) loop_kernel(float* out, int occ_pad) {
+  __shared__ float4 sa[kPts];
+  __shared__ float4 sb[kPts];
+  __shared__ float2 sq[kPts];
+  extern __shared__ char pad[];  // occupancy control
+  for (int i = threadIdx.x; i < kPts; i += 128) {
+    const float f = 1e-3f * (i + 1);
+    sa[i] = make_float4(f, f, -f, -f);
+    sb[i] = make_float4(0.5f * f, 0.5f * f, -2.f * f, -2.f * f);
+    sq[i] = make_float2(f * f, f * f);
+  }
+  if (occ_pad < 0) pad[threadIdx.x] = 0;
+  __syncthreads();
+  const float t0 = 1e-4f * threadIdx.x;
+  const float2 ax = make_float2(t0, -t0), ay = make_float2(0.3f * t0, 0.7f), az = make_float2(t0, 0.1f);
+  const float2 n2 = make_float2(-t0 * t0, -0.5f), minus1 = make_float2(-1.f, -1.f);
+  float2 f0 = make_float2(0.f, 0.f), fx = f0, fy = f0, fz = f0, fq = f0;
+  float2 g0 = f0, gx = f0, gy = f0, gz = f0, gq = f0;
+  for (int r = 0; r < kReps; ++r) {
+    for (int j = 0; j < kPts; j += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float4 a = sa[j + u];
+        const float4 b = sb[j + u];
+        const float2 A = make_float2(a.x, a.y), B = make_float2(a.z, a.w);
+        const float2 C = make_float2(b.x, b.y), D = make_float2(b.z, b.w);
+        if (V == 0) {  // row_diff: 3 FADD2 + FMUL2 + 2 FFMA2 + FFMA2 + 2 MUFU + FADD2 + 4 FFMA2
+          const float2 dx = __fadd2_rn(A, ax), dy = __fadd2_rn(B, ay), dz = __fadd2_rn(C, az);
+          float2 t = __fmul2_rn(dx, dx);
+          t = __ffma2_rn(dy, dy, t);
+          t = __ffma2_rn(dz, dz, t);
+          const float2 L = __ffma2_rn(t, minus1, D);
+          const float2 w = ex2v<MUFU>(L);
+          f0 = __fadd2_rn(f0, w);
+          fx = __ffma2_rn(w, A, fx);
+          fy = __ffma2_rn(w, B, fy);
+          fz = __ffma2_rn(w, C, fz);
+          fq = __ffma2_rn(w, t, fq);
+        } else if (V == 1) {  // row_ctr: FADD2 + 3 FFMA2 + 2 MUFU + FADD2 + 4 FFMA2
+          const float2 Q = sq[j + u];
+          float2 L = __fadd2_rn(D, n2);
+          L = __ffma2_rn(A, ax, L);
+          L = __ffma2_rn(B, ay, L);
+          L = __ffma2_rn(C, az, L);
+          const float2 w = ex2v<MUFU>(L);
+          f0 = __fadd2_rn(f0, w);
+          fx = __ffma2_rn(w, A, fx);
+          fy = __ffma2_rn(w, B, fy);
+          fz = __ffma2_rn(w, C, fz);
+          fq = __ffma2_rn(w, Q, fq);
+        } else if (V == 2) {  // col_diff: 3 FADD2 + FMUL2 + 2 FFMA2 + 2 MUFU + FADD2
+          const float2 dx = __fadd2_rn(A, ax), dy = __fadd2_rn(B, ay), dz = __fadd2_rn(C, az);
+          float2 t = __fmul2_rn(dx, dx);
+          t = __ffma2_rn(dy, dy, t);
+          t = __ffma2_rn(dz, dz, t);
+          f0 = __fadd2_rn(f0, ex2v<MUFU>(make_float2(-t.x, -t.y)));
+        } else if (V == 4) {  // row_ctr with two row pairs per thread (operand reuse)
+          const float2 Q = sq[j + u];
+          float2 L = __fadd2_rn(D, n2);
+          float2 L2 = __fadd2_rn(D, ay);
+          L = __ffma2_rn(A, ax, L);
+          L2 = __ffma2_rn(A, az, L2);
+          L = __ffma2_rn(B, ay, L);
+          L2 = __ffma2_rn(B, n2, L2);
+          L = __ffma2_rn(C, az, L);
+          L2 = __ffma2_rn(C, ax, L2);
+          const float2 w = ex2v<MUFU>(L);
+          const float2 w2 = ex2v<MUFU>(L2);
+          f0 = __fadd2_rn(f0, w);
+          g0 = __fadd2_rn(g0, w2);
+          fx = __ffma2_rn(w, A, fx);
+          gx = __ffma2_rn(w2, A, gx);
+          fy = __ffma2_rn(w, B, fy);
+          gy = __ffma2_rn(w2, B, gy);
+          fz = __ffma2_rn(w, C, fz);
+          gz = __ffma2_rn(w2, C, gz);
+          fq = __ffma2_rn(w, Q, fq);
+          gq = __ffma2_rn(w2, Q, gq);
+        } else if (V == 5) {  // row_ctr, accumulations as scalar FFMA
+          const float2 Q = sq[j + u];
+          float2 L = __fadd2_rn(D, n2);
+          L = __ffma2_rn(A, ax, L);
+          L = __ffma2_rn(B, ay, L);
+          L = __ffma2_rn(C, az, L);
+          const float2 w = ex2v<MUFU>(L);
+          f0.x += w.x; f0.y += w.y;
+          fx.x = __fmaf_rn(w.x, A.x, fx.x); fx.y = __fmaf_rn(w.y, A.y, fx.y);
+          fy.x = __fmaf_rn(w.x, B.x, fy.x); fy.y = __fmaf_rn(w.y, B.y, fy.y);
+          fz.x = __fmaf_rn(w.x, C.x, fz.x); fz.y = __fmaf_rn(w.y, C.y, fz.y);
+          fq.x = __fmaf_rn(w.x, Q.x, fq.x); fq.y = __fmaf_rn(w.y, Q.y, fq.y);
+        } else if (V == 6) {  // 8 FFMA2 with three distinct varying operands each
+          fx = __ffma2_rn(A, B, fx);
+          fy = __ffma2_rn(C, D, fy);
+          fz = __ffma2_rn(B, C, fz);
+          fq = __ffma2_rn(D, A, fq);
+          f0 = __ffma2_rn(fx, fy, f0);
+          g0 = __ffma2_rn(fz, fq, g0);
+          gx = __ffma2_rn(A, C, gx);
+          gy = __ffma2_rn(B, D, gy);
+        } else if (V == 7) {  // 8 FFMA2, one varying operand + two reusable
+          fx = __ffma2_rn(A, ax, fx);
+          fy = __ffma2_rn(A, ay, fy);
+          fz = __ffma2_rn(A, az, fz);
+          fq = __ffma2_rn(A, n2, fq);
+          f0 = __ffma2_rn(B, ax, f0);
+          g0 = __ffma2_rn(B, ay, g0);
+          gx = __ffma2_rn(B, az, gx);
+          gy = __ffma2_rn(B, n2, gy);
+        } else {  // col_ctr: FADD2 + 3 FFMA2 + 2 MUFU + FADD2
+          float2 e = __fadd2_rn(n2, D);
+          e = __ffma2_rn(ax, A, e);
+          e = __ffma2_rn(ay, B, e);
+          e = __ffma2_rn(az, C, e);
+          f0 = __fadd2_rn(f0, ex2v<MUFU>(e));
+        }
+      }
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] =
+      f0.x + f0.y + fx.x + fx.y + fy.x + fy.y + fz.x + fz.y + fq.x + fq.y + g0.x + g0.y + gx.x +
+      gx.y + gy.x + gy.y + gz.x + gz.y + gq.x + gq.y;
+}
+
+template <int V, bool MUFU>
+void run(const char* name, int sms, int ctas_per_sm, float* out) {
+  auto k = loop_kernel<V, MUFU>;
+  int occ = 0;
+  // pad dynamic smem so exactly ctas_per_sm CTAs fit (228 KB per SM)
+  const int pad = 227 * 1024 / ctas_per_sm - 12 * 1024;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 128, pad);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int grid = sms * occ;
+  k<<<grid, 128, pad>>>(out, 0);
+  cudaDeviceSynchronize();
+  cudaEventRecord(a);
+  for (int r = 0; r < 3; ++r) k<<<grid, 128, pad>>>(out, 0);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  int clk_khz = 0;
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+  // point-warps per SMSP: (grid·4 warps)·kReps·kPts / (sms·4)
+  const double pw_per_smsp = double(grid) * 4 * kReps * kPts / (sms * 4.0);
+  const double cycles = (ms / 3) * 1e-3 * clk_khz * 1e3;
+  cudaError_t e = cudaGetLastError();
+  std::printf("%-14s occ=%2d CTAs/SM  %8.3f ms  %6.2f cycles/point-warp (@%d MHz attr)  %s\n",
+              name, occ, ms / 3, cycles / pw_per_smsp, clk_khz / 1000, cudaGetErrorString(e));
+}
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  float* out;
+  cudaMalloc(&out, sizeof(float) * sms * 32 * 128);
+  std::printf("-- extra variants at 8 CTAs/SM (row_ctr_rp2 = 128 pairs per point-warp; ffma2_* = 8 FFMA2 per point)\n");
+  run<4, true>("row_ctr_rp2", sms, 8, out);
+  run<4, false>("row_ctr_rp2_nm", sms, 8, out);
+  run<5, true>("row_ctr_sacc", sms, 8, out);
+  run<5, false>("row_ctr_sacc_nm", sms, 8, out);
+  run<6, false>("ffma2_3var", sms, 8, out);
+  run<7, false>("ffma2_1var", sms, 8, out);
+  for (int occ : {8}) {
+    std::printf("-- target %d CTAs/SM (%d warps/SMSP)\n", occ, occ);
+    run<0, true>("row_diff", sms, occ, out);
+    run<1, true>("row_ctr", sms, occ, out);
+    run<2, true>("col_diff", sms, occ, out);
+    run<3, true>("col_ctr", sms, occ, out);
+    run<0, false>("row_diff_nomufu", sms, occ, out);
+    run<1, false>("row_ctr_nomufu", sms, occ, out);
+    run<2, false>("col_diff_nomufu", sms, occ, out);
+    run<3, false>("col_ctr_nomufu", sms, occ, out);
+  }
+  return 0;
+}
