@@ -199,7 +199,8 @@ struct Session {
   DevBuf<float2> bminmax;
   DevBuf<unsigned long long> cull_counters;  // tiles evaluated (pass 1, pass 2), cumulative
   // per-iteration work lists of the two passes (culled tile pairs)
-  DevBuf<int32_t> wl1_tiles, wl1_off, wl2_tiles, wl2_off, wl_done;
+  DevBuf<int32_t> wl1_tiles, wl1_off, wl2_tiles, wl2_off, wl2_off_cc, wl_done;
+  DevBuf<double> row_seg_cc;  // tensor-core pass 2: the CUDA-core kernel's segments
 
   // ---- distributed (NCCL) sharding: scene N split over ranks, model rows
   // [m0, m0+mr) owned by this rank (m_pad = world·mr ≥ M).  In this mode
@@ -233,7 +234,9 @@ struct Session {
     for (auto* b : {&xlo, &xhi, &ylo, &yhi}) b->release();
     bminmax.release();
     cull_counters.release();
-    for (auto* b : {&wl1_tiles, &wl1_off, &wl2_tiles, &wl2_off, &wl_done}) b->release();
+    for (auto* b : {&wl1_tiles, &wl1_off, &wl2_tiles, &wl2_off, &wl2_off_cc, &wl_done})
+      b->release();
+    row_seg_cc.release();
   }
 };
 
@@ -394,6 +397,7 @@ bool cull_default(int64_t x_tiles, int64_t y_tiles) {
 void set_cull(Session& s, EStepBuffers& eb, int64_t m, int64_t n_local, int64_t n_global) {
   CullInfo& c = eb.cull;
   c.enabled = s.cull && s.xlo.p && s.ylo.p && s.wl1_tiles.p && s.wl2_tiles.p ? 1 : 0;
+  c.lists = (c.enabled || s.ep.tc) && s.wl2_tiles.p ? 1 : 0;
   c.n_xtiles = ceil_div(m, 256);
   c.n_ytiles = ceil_div(n_local, 256);
   c.xlo = s.xlo.p;
@@ -407,7 +411,8 @@ void set_cull(Session& s, EStepBuffers& eb, int64_t m, int64_t n_local, int64_t 
   c.counters = s.cull_counters.p;
   eb.cullw = CullBuffers{s.xlo.p, s.xhi.p, s.ylo.p, s.yhi.p, s.bminmax.p};
   eb.wl1 = WorkListBuffers{s.wl1_tiles.p, s.wl1_off.p, s.wl_done.p};
-  eb.wl2 = WorkListBuffers{s.wl2_tiles.p, s.wl2_off.p, s.wl_done.p ? s.wl_done.p + 1 : nullptr};
+  eb.wl2 = WorkListBuffers{s.wl2_tiles.p, s.wl2_off.p, s.wl_done.p ? s.wl_done.p + 1 : nullptr,
+                           s.wl2_off_cc.p};
 }
 
 // E-step buffers of the session (pt1: optional Σ_m P_mn output; resid:
@@ -421,6 +426,7 @@ EStepBuffers estep_buffers(Session& s, double* pt1, bool resid) {
   eb.pt1 = pt1;
   eb.col_seg = s.col_seg.p;
   eb.row_seg = s.row_seg.p;
+  eb.row_seg_cc = s.row_seg_cc.p;
   eb.col_flags = s.col_flags.p;
   eb.row_flags = s.row_flags.p;
   eb.flags_count = s.flags_count.p;
@@ -445,13 +451,17 @@ void alloc_estep(Session& s, int64_t m, int64_t n, cudaStream_t str) {
   s.bminmax.ensure(nyt);
   s.cull_counters.ensure(2);
   FCPD_CUDA(cudaMemsetAsync(s.cull_counters.p, 0, 2 * sizeof(unsigned long long), str));
-  if (s.cull) {
+  if (s.cull || s.ep.tc) {
     s.wl1_tiles.ensure(static_cast<size_t>(nyt) * nxt);
     s.wl1_off.ensure(nyt + 1);
     s.wl2_tiles.ensure(static_cast<size_t>(nxt) * nyt);
     s.wl2_off.ensure(nxt + 1);
     s.wl_done.ensure(2);
     FCPD_CUDA(cudaMemsetAsync(s.wl_done.p, 0, 2 * sizeof(int32_t), str));
+  }
+  if (s.ep.tc) {
+    s.wl2_off_cc.ensure(nxt + 1);
+    s.row_seg_cc.ensure(static_cast<size_t>(s.ep.row_grid + s.ep.row_blocks) * 5 * 256);
   }
   launch_tile_bbox(s.y4b.p, n, s.ylo.p, s.yhi.p, nullptr, str);
 }
@@ -1293,12 +1303,16 @@ int32_t fcpd_kernels_per_iteration(const fcpd_ctx* ctx) {
   // distributed: prologue, col, col-combine, col-fallback, row, row-sum,
   // finalize-own, fb-max, fb-sum, fb-finalize, Qᵀ·R, z-sum, z-filter, Q·g,
   // transform, σ²-local, σ²-final (+ 7 NCCL collectives).
-  // Tile culling adds 4: model-tile boxes, column bounds, scene-tile b range,
-  // row bounds.
+  // Tile culling adds 4: model-tile boxes, pass-1 list, scene-tile b range,
+  // pass-2 list.
   if (!ctx) return 0;
   const Session& s = ctx->sess;
-  const int cull = s.cull && s.xlo.p && s.ylo.p ? 4 : 0;
-  return (s.dist ? 17 : 12) + cull;
+  const bool culling = s.cull && s.xlo.p && s.ylo.p;
+  int extra = culling ? 4 : 0;
+  // tensor-core pass 2: its CUDA-core companion kernel (+ x̃ boxes and the
+  // routing list when culling is off)
+  if (s.ep.tc) extra += 1 + (culling ? 0 : 2);
+  return (s.dist ? 17 : 12) + extra;
 }
 
 int fcpd_register(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n,

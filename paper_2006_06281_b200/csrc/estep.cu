@@ -48,9 +48,6 @@ namespace {
 constexpr int kTile = kTilePts;  // points staged in shared memory per step
 constexpr int kCombineLanes = 8; // lanes cooperating on one row/column reduction
 constexpr float kPadCoord = 3.0e18f;  // padding point: t ≈ 1e37, 2^-t = 0
-// centred form only where its fp32 rounding stays ≤ ~4e-6 in log2 units:
-// squared half-diagonal of the CTA's own box in the scaled frame
-constexpr float kCentredMaxR2 = 16.f;
 
 __device__ __forceinline__ float sqdist(float4 a, float4 b) {
   // the fallbacks' pair term (difference form, as the main kernels' diff path)
@@ -688,19 +685,11 @@ __global__ void tile_bminmax_kernel(const float4* __restrict__ y4b, int64_t n,
   }
 }
 
-// The last CTA of a list kernel turns the per-block counts (offset[b+1])
-// into the exclusive prefix (in place), resets the done counter for the next
-// graph replay and adds the total to the evaluated-pairs counter.
-__device__ void last_cta_scan(int32_t* offset, int n_blocks, int32_t* done,
-                              unsigned long long* counter) {
-  __shared__ int is_last;
-  __shared__ int wsum[32];
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = atomicAdd(done, 1) == static_cast<int>(gridDim.x) - 1;
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
+// The last CTA of a list kernel turns the per-block counts (offset[b+1],
+// and offset2[b+1] when given) into exclusive prefixes (in place), resets
+// the done counter for the next graph replay and adds the total to the
+// evaluated-pairs counter.
+__device__ void scan_counts(int32_t* offset, int n_blocks, int* wsum) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int carry = 0;
   for (int base = 0; base < n_blocks; base += blockDim.x) {
@@ -722,10 +711,26 @@ __device__ void last_cta_scan(int32_t* offset, int n_blocks, int32_t* done,
     carry += total;
     __syncthreads();
   }
+  if (threadIdx.x == 0) offset[0] = 0;
+}
+
+__device__ void last_cta_scan(int32_t* offset, int32_t* offset2, int n_blocks, int32_t* done,
+                              unsigned long long* counter) {
+  __shared__ int is_last;
+  __shared__ int wsum[32];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(done, 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  scan_counts(offset, n_blocks, wsum);
+  if (offset2) scan_counts(offset2, n_blocks, wsum);
   if (threadIdx.x == 0) {
-    offset[0] = 0;
     *done = 0;
-    if (counter) *counter += static_cast<unsigned long long>(carry);
+    if (counter)
+      *counter += static_cast<unsigned long long>(offset[n_blocks]) +
+                  (offset2 ? static_cast<unsigned long long>(offset2[n_blocks]) : 0ull);
   }
 }
 
@@ -759,41 +764,58 @@ __global__ void col_list_kernel(CullInfo cull, int32_t* __restrict__ tiles,
     }
     if (lane == 0) offset[b + 1] = count;
   }
-  last_cta_scan(offset, n_blocks, done, cull.counters);
+  last_cta_scan(offset, nullptr, n_blocks, done, cull.counters);
 }
 
 // Pass-2 list: per model tile b, a lower bound on max_n L_mn of every row,
 // L_lb = max over scene tiles of (min b − s²·maxdist²); keep scene tile j
-// unless its largest possible L (max b − s²·mindist²) < L_lb − margin.
+// unless its largest possible L (max b − s²·mindist²) < L_lb − margin
+// (culling off: keep every tile).  With offset_cc (tensor-core pass 2), a
+// block whose scaled squared half-diagonal exceeds kCentredMaxR2 is routed
+// to the CUDA-core list (difference form) instead.
 __global__ void row_list_kernel(CullInfo cull, int32_t* __restrict__ tiles,
-                                int32_t* __restrict__ offset, int n_blocks,
-                                int32_t* __restrict__ done, const IterState* __restrict__ st) {
+                                int32_t* __restrict__ offset, int32_t* __restrict__ offset_cc,
+                                int n_blocks, int32_t* __restrict__ done,
+                                const IterState* __restrict__ st) {
   if (!st->active) return;
   const float s2 = st->sx * st->sx;
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (b < n_blocks) {
     const float4 lo = cull.xlo[b], hi = cull.xhi[b];
-    float l = -INFINITY;
-    for (int j = lane; j < cull.n_ytiles; j += 32)
-      l = fmaxf(l, cull.bminmax[j].x - s2 * box_maxdist2(lo, hi, cull.ylo[j], cull.yhi[j]));
+    float floor_l = -INFINITY;
+    if (cull.enabled) {
+      float l = -INFINITY;
+      for (int j = lane; j < cull.n_ytiles; j += 32)
+        l = fmaxf(l, cull.bminmax[j].x - s2 * box_maxdist2(lo, hi, cull.ylo[j], cull.yhi[j]));
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) l = fmaxf(l, __shfl_xor_sync(0xffffffffu, l, o));
-    const float floor_l = l - cull.margin2;
+      for (int o = 16; o > 0; o >>= 1) l = fmaxf(l, __shfl_xor_sync(0xffffffffu, l, o));
+      floor_l = l - cull.margin2;
+    }
     int count = 0;
     int32_t* out = tiles + static_cast<int64_t>(b) * cull.n_ytiles;
     for (int j0 = 0; j0 < cull.n_ytiles; j0 += 32) {
       const int j = j0 + lane;
       const bool keep =
           j < cull.n_ytiles &&
-          !(cull.bminmax[j].y - s2 * box_mindist2(lo, hi, cull.ylo[j], cull.yhi[j]) < floor_l);
+          (!cull.enabled ||
+           !(cull.bminmax[j].y - s2 * box_mindist2(lo, hi, cull.ylo[j], cull.yhi[j]) < floor_l));
       const unsigned mask = __ballot_sync(0xffffffffu, keep);
       if (keep) out[count + __popc(mask & ((1u << lane) - 1))] = j;
       count += __popc(mask);
     }
-    if (lane == 0) offset[b + 1] = count;
+    if (lane == 0) {
+      bool to_tc = true;
+      if (offset_cc) {
+        const float ex = hi.x - lo.x, ey = hi.y - lo.y, ez = hi.z - lo.z;
+        to_tc = 0.25f * s2 * (ex * ex + ey * ey + ez * ez) <= kCentredMaxR2;
+        offset_cc[b + 1] = to_tc ? 0 : count;
+      }
+      offset[b + 1] = to_tc ? count : 0;
+    }
   }
-  last_cta_scan(offset, n_blocks, done, cull.counters ? cull.counters + 1 : nullptr);
+  last_cta_scan(offset, offset_cc, n_blocks, done,
+                cull.enabled && cull.counters ? cull.counters + 1 : nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -835,17 +857,35 @@ __device__ __forceinline__ void finalize_row(int64_t row, int64_t m, double log2
   }
 }
 
-__global__ void estep_row_combine_kernel(const double* __restrict__ seg, WorkList wl, int G,
-                                         int64_t m, int64_t n, const double* __restrict__ xt64,
-                                         RowOut out, YStats ys, int32_t* __restrict__ flag_list,
+// One producer of pass-2 segments: its work list, grid and slots.
+struct SegSrc {
+  WorkList wl;
+  int G = 0;
+  const double* seg = nullptr;  // nullptr: absent
+};
+
+__device__ __forceinline__ void sum_row(const SegSrc& a, const SegSrc& b, int64_t row, int lane,
+                                        bool live, double (&s)[5]) {
+  const int blk = static_cast<int>(row / kTile), li = static_cast<int>(row % kTile);
+  sum_segments<5>(a.wl, a.G, a.seg, blk, li, lane, live, s);
+  if (b.seg) {  // each block's units are in exactly one of the two lists
+    double t[5];
+    sum_segments<5>(b.wl, b.G, b.seg, blk, li, lane, live, t);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) s[k] += t[k];
+  }
+}
+
+__global__ void estep_row_combine_kernel(SegSrc sa, SegSrc sb, int64_t m, int64_t n,
+                                         const double* __restrict__ xt64, RowOut out, YStats ys,
+                                         int32_t* __restrict__ flag_list,
                                          int32_t* __restrict__ flag_count, IterState* st) {
   if (!st->active) return;
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t row = gid / kCombineLanes;
   const int lane = static_cast<int>(gid % kCombineLanes);
   double a[5];
-  sum_segments<5>(wl, G, seg, static_cast<int>(row / kTile), static_cast<int>(row % kTile), lane,
-                  row < m, a);
+  sum_row(sa, sb, row, lane, row < m, a);
   if (row >= m || lane != 0) return;
   if (!(a[0] >= static_cast<double>(n) * 0x1p-76)) {
     const int slot = atomicAdd(flag_count, 1);
@@ -857,16 +897,14 @@ __global__ void estep_row_combine_kernel(const double* __restrict__ seg, WorkLis
 }
 
 // distributed: AoS row sums [m_pad][5] of the local scene shard
-__global__ void row_seg_sum_kernel(const double* __restrict__ seg, WorkList wl, int G, int64_t m,
-                                   int64_t m_pad, double* __restrict__ out,
-                                   const IterState* __restrict__ st) {
+__global__ void row_seg_sum_kernel(SegSrc sa, SegSrc sb, int64_t m, int64_t m_pad,
+                                   double* __restrict__ out, const IterState* __restrict__ st) {
   if (!st->active) return;
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t row = gid / kCombineLanes;
   const int lane = static_cast<int>(gid % kCombineLanes);
   double a[5];
-  sum_segments<5>(wl, G, seg, static_cast<int>(row / kTile), static_cast<int>(row % kTile), lane,
-                  row < m, a);
+  sum_row(sa, sb, row, lane, row < m, a);
   if (row < m_pad && lane == 0)
 #pragma unroll
     for (int k = 0; k < 5; ++k) out[row * 5 + k] = a[k];
@@ -933,6 +971,12 @@ EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
   p.row_blocks = static_cast<int>(ceil_div(m, kTile));
   p.col_grid = sm_count * std::max(occ_col, 1);
   p.row_grid = sm_count * std::max(occ_row, 1);
+  if (const char* e = std::getenv("FCPD_ESTEP_TC")) p.tc = std::atoi(e) != 0;
+  if (!p.centred) p.tc = 0;  // the tensor-core pass is the centred form
+  if (p.tc) {
+    estep_row_tc_prepare();
+    p.tc_grid = sm_count;  // one CTA per SM (all 512 TMEM columns)
+  }
   return p;
 }
 
@@ -946,14 +990,24 @@ WorkList pass1_list(const EStepPlan& p, const EStepBuffers& b, int64_t m) {
   wl.offset = b.wl1.offset;
   return wl;
 }
-WorkList pass2_list(const EStepPlan& p, const EStepBuffers& b, int64_t n) {
+WorkList pass2_list(const EStepPlan& p, const EStepBuffers& b, int64_t n, bool cc = false) {
   WorkList wl;
-  wl.implicit = b.cull.enabled ? 0 : 1;
+  wl.implicit = b.cull.lists ? 0 : 1;
   wl.n_blocks = p.row_blocks;
   wl.n_other = static_cast<int>(ceil_div(n, kTile));
   wl.tiles = b.wl2.tiles;
-  wl.offset = b.wl2.offset;
+  wl.offset = cc ? b.wl2.offset_cc : b.wl2.offset;
   return wl;
+}
+// pass-2 producers: (tensor cores, CUDA cores) or (CUDA cores, none)
+void pass2_sources(const EStepPlan& p, const EStepBuffers& b, int64_t n, SegSrc& a, SegSrc& c) {
+  if (p.tc) {
+    a = SegSrc{pass2_list(p, b, n), p.tc_grid, b.row_seg};
+    c = SegSrc{pass2_list(p, b, n, true), p.row_grid, b.row_seg_cc};
+  } else {
+    a = SegSrc{pass2_list(p, b, n), p.row_grid, b.row_seg};
+    c = SegSrc{};
+  }
 }
 }  // namespace
 
@@ -1000,25 +1054,36 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
 void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int64_t m,
                                  int64_t n, IterState* st, cudaStream_t stream) {
   const CullInfo& cu = b.cull;
-  const WorkList wl = pass2_list(p, b, n);
-  if (cu.enabled) {
+  if (cu.lists) {
+    if (!cu.enabled)  // x̃ tile boxes for the routing (pass 1 made them when culling)
+      launch_tile_bbox(b.xt4, m, b.cullw.xlo, b.cullw.xhi, st, stream);
     row_list_kernel<<<ceil_div(p.row_blocks, 8), 256, 0, stream>>>(
-        cu, b.wl2.tiles, b.wl2.offset, p.row_blocks, b.wl2.done, st);
+        cu, b.wl2.tiles, b.wl2.offset, p.tc ? b.wl2.offset_cc : nullptr, p.row_blocks,
+        b.wl2.done, st);
     FCPD_LAUNCH_CHECK();
   }
-  estep_row_kernel<<<p.row_grid, 128, 0, stream>>>(b.xt4, m, b.y4b, n, st, wl, b.row_seg,
-                                                   p.centred);
+  SegSrc a, c;
+  pass2_sources(p, b, n, a, c);
+  if (p.tc) {
+    launch_estep_row_tc(b.xt4, m, b.y4b, n, st, a.wl, b.row_seg, p.tc_grid, stream);
+    estep_row_kernel<<<p.row_grid, 128, 0, stream>>>(b.xt4, m, b.y4b, n, st, c.wl,
+                                                     b.row_seg_cc, p.centred);
+  } else {
+    estep_row_kernel<<<p.row_grid, 128, 0, stream>>>(b.xt4, m, b.y4b, n, st, a.wl, b.row_seg,
+                                                     p.centred);
+  }
   FCPD_LAUNCH_CHECK();
 }
 
 void launch_estep_pass2(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
                         IterState* st, cudaStream_t stream) {
   launch_estep_pass2_partials(p, b, m, n, st, stream);
-  const WorkList wl = pass2_list(p, b, n);
+  SegSrc a, c;
+  pass2_sources(p, b, n, a, c);
   int32_t* list = b.row_flags;
   int32_t* count = b.flags_count + 1;
   estep_row_combine_kernel<<<ceil_div(m * kCombineLanes, 256), 256, 0, stream>>>(
-      b.row_seg, wl, p.row_grid, m, n, b.xt64, b.out, b.ystats, list, count, st);
+      a, c, m, n, b.xt64, b.out, b.ystats, list, count, st);
   FCPD_LAUNCH_CHECK();
   estep_row_fallback_kernel<<<148, 256, 0, stream>>>(b.xt4, m, b.y4b, n, b.xt64, b.out,
                                                      b.ystats, list, count, st);
@@ -1027,9 +1092,10 @@ void launch_estep_pass2(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
 
 void launch_row_seg_sum(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
                         int64_t m_pad, double* out, const IterState* st, cudaStream_t stream) {
-  const WorkList wl = pass2_list(p, b, n);
-  row_seg_sum_kernel<<<ceil_div(m_pad * kCombineLanes, 256), 256, 0, stream>>>(
-      b.row_seg, wl, p.row_grid, m, m_pad, out, st);
+  SegSrc a, c;
+  pass2_sources(p, b, n, a, c);
+  row_seg_sum_kernel<<<ceil_div(m_pad * kCombineLanes, 256), 256, 0, stream>>>(a, c, m, m_pad,
+                                                                              out, st);
   FCPD_LAUNCH_CHECK();
 }
 

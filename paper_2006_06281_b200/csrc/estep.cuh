@@ -49,19 +49,33 @@ struct WorkList {
 struct WorkListBuffers {  // writable views (engine-owned)
   int32_t* tiles = nullptr;
   int32_t* offset = nullptr;
-  int32_t* done = nullptr;  // last-CTA counter of the list kernel (self-resetting)
+  int32_t* done = nullptr;     // last-CTA counter of the list kernel (self-resetting)
+  int32_t* offset_cc = nullptr;  // pass 2 with tensor cores: the CUDA-core share
 };
 
 // Persistent stream-K schedule of both passes (one CTA wave per pass).
+// Pass-2 blocks whose squared box half-diagonal in the scaled frame exceeds
+// this run on the CUDA cores in the difference form (the centred form's
+// rounding ≈ 4ε·R² in log2 units; 16 → ≤ 4e-6).
+constexpr float kCentredMaxR2 = 16.f;
+
 struct EStepPlan {
   int centred = 1;  // tile-centred pair form where exact enough; FCPD_ESTEP_FORM=diff → off
+  int tc = 0;       // pass 2 on tcgen05 (estep_tc.cu) for blocks within kCentredMaxR2
   int col_blocks = 0, row_blocks = 0;  // scene tiles (pass-1 blocks), model tiles (pass 2)
-  int col_grid = 0, row_grid = 0;      // persistent CTAs per pass
+  int col_grid = 0, row_grid = 0;      // persistent CTAs per pass (CUDA-core kernels)
+  int tc_grid = 0;                     // persistent CTAs of the tensor-core pass 2
   size_t col_seg_doubles() const { return static_cast<size_t>(col_grid + col_blocks) * kTilePts; }
   size_t row_seg_doubles() const {
-    return static_cast<size_t>(row_grid + row_blocks) * 5 * kTilePts;
+    return static_cast<size_t>(std::max(row_grid, tc_grid) + row_blocks) * 5 * kTilePts;
   }
 };
+
+// estep_tc.cu
+void estep_row_tc_prepare();
+void launch_estep_row_tc(const float4* xt4, int64_t m, const float4* y4b, int64_t n,
+                         const IterState* st, const WorkList& wl, double* seg, int grid,
+                         cudaStream_t stream);
 
 // Tile culling.  Points are Morton-sorted by the engine so
 // 256-point tiles are compact boxes; a (block, tile) pair is dropped from
@@ -69,7 +83,8 @@ struct EStepPlan {
 // smallest possible column (row) total.  With margin = 50 + log2(count) the
 // skipped mass is ≤ 2^-50 relative: exact to fp32.
 struct CullInfo {
-  int enabled = 0;
+  int enabled = 0;  // culling drops tile pairs from the work lists
+  int lists = 0;    // explicit work lists (culling, or pass-2 routing to tensor cores)
   int n_xtiles = 0, n_ytiles = 0;   // 256-point tiles
   const float4* xlo = nullptr;      // model tiles (x̃ of this iteration)
   const float4* xhi = nullptr;
@@ -92,7 +107,8 @@ struct EStepBuffers {
   double* b2;          // b_n fp64 (log2 units), N
   double* pt1;         // optional Σ_m P_mn, N
   double* col_seg;     // pass-1 segment partials [col_grid + col_blocks][256]
-  double* row_seg;     // pass-2 segment partials [row_grid + row_blocks][5][256]
+  double* row_seg;     // pass-2 segment partials [grid + row_blocks][5][256]
+  double* row_seg_cc;  // with tensor cores: the CUDA-core kernel's segments
   int32_t* col_flags;  // N
   int32_t* row_flags;  // M
   int32_t* flags_count;  // 2
