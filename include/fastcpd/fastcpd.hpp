@@ -18,9 +18,14 @@
 #pragma once
 
 #include <algorithm>
+#include <cerrno>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <fstream>
+#include <limits>
 #include <memory>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -302,6 +307,99 @@ inline double init_sigma2(const PointSet& x, const PointSet& y) {
   }
   const double v = (m * fy + n * fx - 2.0 * dot) / (static_cast<double>(x.dim()) * m * n);
   return v > 0.0 ? v : 0.0;
+}
+
+// ------------------------------------------- point files (pointset.hpp:45-119)
+// Text point files: one point per line, coordinates separated by whitespace
+// or commas, '#' starts a comment, blank lines ignored.  Same checks and
+// messages as the reference: unreadable file → IoError, a token that is not
+// a finite number → ParseError "path:line: malformed number 'tok'", a row
+// of another width → DimensionError, no points → ParseError.
+inline PointSet load_points(const std::string& path, Index expected_dim = -1) {
+  std::ifstream in(path);
+  if (!in) throw IoError("cannot open point file: " + path);
+  std::vector<double> vals;
+  Index dim = -1, rows = 0;
+  std::string line;
+  long lineno = 0;
+  while (std::getline(in, line)) {
+    ++lineno;
+    std::replace(line.begin(), line.end(), ',', ' ');
+    std::istringstream ss(line);
+    std::string tok;
+    Index width = 0;
+    while (ss >> tok) {
+      if (tok[0] == '#') break;
+      char* end = nullptr;
+      errno = 0;
+      const double v = std::strtod(tok.c_str(), &end);
+      if (end != tok.c_str() + tok.size() || !std::isfinite(v) || tok.empty())
+        throw ParseError(path + ":" + std::to_string(lineno) + ": malformed number '" + tok +
+                         "'");
+      vals.push_back(v);
+      ++width;
+    }
+    if (width == 0) continue;  // blank or comment-only line
+    if (dim < 0) dim = width;
+    else if (width != dim)
+      throw DimensionError(path + ":" + std::to_string(lineno) + ": expected " +
+                           std::to_string(dim) + " columns, got " + std::to_string(width));
+    ++rows;
+  }
+  if (rows == 0) throw ParseError(path + ": no points in file");
+  if (expected_dim >= 0 && dim != expected_dim)
+    throw DimensionError(path + ": expected dimension " + std::to_string(expected_dim) +
+                         ", got " + std::to_string(dim));
+  Matrix m(rows, dim);
+  for (Index i = 0; i < rows; ++i)
+    for (Index j = 0; j < dim; ++j) m(i, j) = vals[static_cast<size_t>(i * dim + j)];
+  return PointSet{std::move(m)};
+}
+
+// Full round-trip precision (max_digits10), one point per line.
+inline void write_points(const PointSet& ps, const std::string& path) {
+  std::ofstream out(path);
+  if (!out) throw IoError("cannot open for writing: " + path);
+  out.precision(std::numeric_limits<double>::max_digits10);
+  for (Index i = 0; i < ps.count(); ++i) {
+    for (Index j = 0; j < ps.dim(); ++j) out << (j ? " " : "") << ps.pts(i, j);
+    out << '\n';
+  }
+  if (!out) throw IoError("write failed: " + path);
+}
+
+// ------------------------------------------- run report (registration.hpp:178-204)
+// key=value lines (15 significant digits): the configuration, diagnostics,
+// timing breakdown and the σ² trace as sigma2[i]=….  The device run adds
+// t_setup (Gram + eigendecomposition) after t_total.
+inline void write_report(const std::string& path, const RegistrationConfig& cfg,
+                         const RegistrationResult& res) {
+  std::ofstream out(path);
+  if (!out) throw IoError("cannot write report: " + path);
+  out.precision(15);
+  const auto kv = [&](const char* k, auto v) { out << k << '=' << v << '\n'; };
+  kv("variant", to_string(cfg.variant));
+  kv("omega", cfg.omega);
+  kv("beta", cfg.beta);
+  kv("lambda", cfg.lambda_reg);
+  kv("iterations", cfg.iterations);
+  kv("rank_fraction", cfg.rank_fraction);
+  kv("seed", cfg.seed);
+  kv("normalize", cfg.normalize ? 1 : 0);
+  kv("baseline_solver", res.diagnostics.baseline_solver);
+  kv("sigma2_initial", res.sigma2_initial);
+  kv("degenerate_rows", res.diagnostics.degenerate_rows);
+  kv("sigma2_clamps", res.diagnostics.sigma2_clamps);
+  kv("t_c", res.timing.t_c);
+  kv("t_eig", res.timing.t_eig);
+  kv("t_iter", res.timing.t_iter);
+  kv("t_f", res.timing.t_f);
+  kv("t_o", res.timing.t_o);
+  kv("t_total", res.timing.t_total);
+  kv("t_setup", res.timing.t_setup);
+  for (size_t i = 0; i < res.sigma2_trace.size(); ++i)
+    out << "sigma2[" << i << "]=" << res.sigma2_trace[i] << '\n';
+  if (!out) throw IoError("report write failed: " + path);
 }
 
 }  // namespace fastcpd

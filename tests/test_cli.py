@@ -1,0 +1,75 @@
+"""Point-file I/O, the run report and the `fcpd register` CLI (SURVEY §8f
+rank 3; reference: pointset.hpp:45-119, registration.hpp:178-204,
+tools/fcpd.cpp:56-83, tests/test_pointset.cpp, tests/test_cli.cpp)."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.join(ROOT, "paper_2006_06281_b200")
+LIBDIR = os.path.join(PKG, "lib")
+CLI = os.path.join(PKG, "bin", "fcpd")
+
+
+def build():
+    subprocess.run(["make", "-s", "-j8", "-C", PKG], check=True)
+    return CLI
+
+
+def test_pointio_and_report_match_reference_tests(tmp_path):
+    """tests/test_pointset.cpp restated against the drop-in header (host only)."""
+    build()
+    src = os.path.join(ROOT, "tests", "cpp", "test_pointio.cpp")
+    exe = str(tmp_path / "test_pointio")
+    subprocess.run(["/usr/bin/g++", "-std=c++17", "-O2", "-Wall", "-Werror", "-I",
+                    os.path.join(ROOT, "include"), src, "-L", LIBDIR, "-lfcpd_b200",
+                    f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
+    r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=60)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "FAIL:" not in r.stdout
+
+
+def test_cli_usage_and_errors(tmp_path):
+    exe = build()
+    r = subprocess.run([exe, "--help"], capture_output=True, text=True)
+    assert r.returncode == 0 and "register MODEL SCENE" in r.stdout
+    r = subprocess.run([exe, "degrade", "x"], capture_output=True, text=True)
+    assert r.returncode == 2
+    # a missing scene file is reported by name before any device work
+    model = tmp_path / "model_only.txt"
+    np.savetxt(model, np.random.default_rng(201).uniform(-1, 1, (10, 2)))
+    r = subprocess.run([exe, "register", str(model), str(tmp_path / "no_such_scene.txt")],
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "no_such_scene.txt" in r.stderr
+    r = subprocess.run([exe, "register", str(model), str(model), "--variant", "bogus"],
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "unknown solver variant" in r.stderr
+
+
+@pytest.mark.gpu
+def test_cli_register_on_gpu(tmp_path, orc):
+    """tests/test_cli.cpp:39-63: register an identical torus pair, 20
+    iterations; the report's final σ² does not exceed the initial one and the
+    output equals the library call with the same configuration."""
+    import paper_2006_06281_b200 as fc
+
+    exe = build()
+    cloud = orc.make_torus(80, 200)
+    pts = tmp_path / "cloud.txt"
+    np.savetxt(pts, cloud, fmt="%.17g")
+    out, rep, svg = tmp_path / "reg_out.txt", tmp_path / "reg_report.txt", tmp_path / "reg.svg"
+    r = subprocess.run([exe, "register", str(pts), str(pts), "--iters", "20", "--out", str(out),
+                        "--report", str(rep), "--svg", str(svg)],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert out.exists() and svg.exists()
+    kv = dict(line.split("=", 1) for line in rep.read_text().splitlines())
+    initial, final = float(kv["sigma2_initial"]), float(kv["sigma2[19]"])
+    assert 0.0 <= final <= initial
+    assert kv["variant"] == "fast" and kv["iterations"] == "20"
+    got = np.loadtxt(out)
+    ref = fc.register_pointsets(cloud, cloud, fc.RegistrationConfig(iterations=20))
+    assert np.abs(got - ref.transformed).max() <= 1e-12
