@@ -15,6 +15,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -504,7 +505,6 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
                      const std::vector<double>& y_soa, int capacity, bool need_mstep) {
   const int64_t m = s.m, n = s.n;
   cudaStream_t str = ctx->stream;
-  s.release_graph();
   s.x0.ensure(3 * m);
   s.xt64.ensure(3 * m);
   s.xt_prev.ensure(3 * m);
@@ -630,22 +630,40 @@ std::vector<int64_t> morton_sort(std::vector<double>& soa, int64_t cnt) {
   double span = 0.0;
   for (int c = 0; c < 3; ++c) span = std::max(span, hi[c] - lo[c]);
   const double q = span > 0.0 ? 2097151.0 / span : 0.0;
-  std::vector<std::pair<uint64_t, int64_t>> keys(cnt);
+  std::vector<uint64_t> key(cnt), key2(cnt);
+  std::vector<int64_t> perm(cnt), perm2(cnt);
+  uint64_t all_or = 0, all_and = ~0ull;
   for (int64_t i = 0; i < cnt; ++i) {
-    uint64_t key = 0;
+    uint64_t k = 0;
     for (int c = 0; c < 3; ++c) {
       const uint64_t v = static_cast<uint64_t>((soa[c * cnt + i] - lo[c]) * q);
-      key |= morton_spread21(v) << c;
+      k |= morton_spread21(v) << c;
     }
-    keys[i] = {key, i};
+    key[i] = k;
+    perm[i] = i;
+    all_or |= k;
+    all_and &= k;
   }
-  std::sort(keys.begin(), keys.end());
-  std::vector<int64_t> perm(cnt);
+  // LSD radix sort, 8 bits per pass (passes whose byte is constant are
+  // skipped); stable, so equal keys keep index order — the same order as
+  // sorting (key, index) pairs, deterministic.  O(8n) instead of O(n log n):
+  // the host side of session setup at 200k points.
+  for (int shift = 0; shift < 64; shift += 8) {
+    if ((((all_or ^ all_and) >> shift) & 0xff) == 0) continue;
+    size_t count[257] = {};
+    for (int64_t i = 0; i < cnt; ++i) ++count[((key[i] >> shift) & 0xff) + 1];
+    for (int b = 0; b < 256; ++b) count[b + 1] += count[b];
+    for (int64_t i = 0; i < cnt; ++i) {
+      const size_t dst = count[(key[i] >> shift) & 0xff]++;
+      key2[dst] = key[i];
+      perm2[dst] = perm[i];
+    }
+    key.swap(key2);
+    perm.swap(perm2);
+  }
   std::vector<double> out(soa.size());
-  for (int64_t k = 0; k < cnt; ++k) {
-    perm[k] = keys[k].second;
-    for (int c = 0; c < 3; ++c) out[c * cnt + k] = soa[c * cnt + perm[k]];
-  }
+  for (int c = 0; c < 3; ++c)
+    for (int64_t k = 0; k < cnt; ++k) out[c * cnt + k] = soa[c * cnt + perm[k]];
   soa.swap(out);
   return perm;
 }
@@ -704,9 +722,13 @@ void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, i
   s.cfg = cfg;
   std::vector<double> xs, ys;
   normalize_pair_host(x, m, y, n, d, cfg.normalize != 0, xs, ys, s.center, &s.scale);
-  // internal order: Morton-sorted model and scene (undone on output)
-  s.perm_x = morton_sort(xs, m);
-  s.perm_y = morton_sort(ys, n);
+  // internal order: Morton-sorted model and scene (undone on output); the
+  // two sorts are independent
+  {
+    std::thread tx([&] { s.perm_x = morton_sort(xs, m); });
+    s.perm_y = morton_sort(ys, n);
+    tx.join();
+  }
   // x0 must be on the device before the Gram build
   s.x0.ensure(3 * m);
   FCPD_CUDA(cudaMemcpyAsync(s.x0.p, xs.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice,
@@ -732,11 +754,26 @@ void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, i
     throw;
   }
   FCPD_CUDA(cudaStreamEndCapture(ctx->stream, &g));
-  cudaGraphExec_t exec = nullptr;
-  const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
-  cudaGraphDestroy(g);
-  FCPD_CUDA(ie);
-  s.graph = exec;
+  // a repeated register call with the same shapes captures the same graph
+  // topology: update the existing executable instead of re-instantiating
+  bool updated = false;
+  if (s.graph) {
+    cudaGraphExecUpdateResultInfo info{};
+    updated = cudaGraphExecUpdate(s.graph, g, &info) == cudaSuccess;
+    if (!updated) {
+      cudaGetLastError();  // clear the update failure
+      s.release_graph();
+    }
+  }
+  if (!updated) {
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    FCPD_CUDA(ie);
+    s.graph = exec;
+  } else {
+    cudaGraphDestroy(g);
+  }
   FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
   s.t_setup_host = since(t0);
   s.launched = 0;
