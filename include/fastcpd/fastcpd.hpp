@@ -185,6 +185,7 @@ struct RegistrationConfig {
   bool early_stop = false;
   bool want_correspondence = false;  // extension: materialise P̃ (M×N) at the end
   int device = 0;                    // extension: CUDA device of the default context
+  double spectral_tau = 1e-10;       // extension: basis-stream filter threshold (0 = all K)
 };
 
 struct RegistrationDiagnostics {
@@ -235,6 +236,7 @@ class Context {
     c.seed = cfg.seed;
     c.normalize = cfg.normalize ? 1 : 0;
     c.early_stop = cfg.early_stop ? 1 : 0;
+    c.spectral_tau = cfg.spectral_tau;
     RegistrationResult res;
     res.transformed.pts.resize(m, d);
     res.coefficients.w.resize(m, d);

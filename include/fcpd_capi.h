@@ -61,6 +61,11 @@ typedef struct fcpd_config {
   uint64_t seed;        /* echoed only, as in the reference       (0)    */
   int32_t normalize;    /* normalize_pair before registering      (1)    */
   int32_t early_stop;   /* stop when |Δσ²| < 1e-10                 (0)    */
+  int32_t pad0;
+  double spectral_tau;  /* extension: the basis streams skip eigenpairs
+                           whose filter λnum/(λ+λ_reg σ²) < tau; their
+                           contribution to x̃ is far below the fp32 basis
+                           rounding (1e-10; 0 = stream all K)             */
 } fcpd_config;
 
 /* TimingBreakdown — registration.hpp:21-28, plus t_setup (Gram build +
@@ -93,6 +98,8 @@ typedef struct fcpd_result {
   int64_t tiles_evaluated[2]; /* E-step tile pairs computed since the
                                  session began (pass 1, pass 2); the rest
                                  were culled (≤ 2^-50 of any total)     */
+  int64_t spectral_rank;    /* eigenpairs the last iteration's basis
+                               streams used (filter ≥ tau; = K untruncated) */
 } fcpd_result;
 
 typedef struct fcpd_ctx fcpd_ctx;

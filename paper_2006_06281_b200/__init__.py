@@ -88,7 +88,8 @@ class _Config(C.Structure):
     _fields_ = [("omega", C.c_double), ("beta", C.c_double), ("lambda_reg", C.c_double),
                 ("iterations", C.c_int32), ("variant", C.c_int32),
                 ("rank_fraction", C.c_double), ("seed", C.c_uint64),
-                ("normalize", C.c_int32), ("early_stop", C.c_int32)]
+                ("normalize", C.c_int32), ("early_stop", C.c_int32), ("pad0", C.c_int32),
+                ("spectral_tau", C.c_double)]
 
 
 class _Timing(C.Structure):
@@ -106,7 +107,8 @@ class _Result(C.Structure):
                 ("sigma2_initial", C.c_double), ("degenerate_rows", C.c_int64),
                 ("sigma2_clamps", C.c_int64), ("timing", _Timing),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-                ("tiles_evaluated", C.c_int64 * 2)]
+                ("tiles_evaluated", C.c_int64 * 2),
+                ("spectral_rank", C.c_int64)]
 
 
 _lib = None
@@ -190,11 +192,15 @@ class RegistrationConfig:  # registration.hpp:30-40
     seed: int = 0
     normalize: bool = True
     early_stop: bool = False
+    # extension: skip eigenpairs whose spectral filter is below tau in the
+    # per-iteration basis streams (0 = stream all K)
+    spectral_tau: float = 1e-10
 
     def _c(self) -> _Config:
         return _Config(self.omega, self.beta, self.lambda_reg, int(self.iterations),
                        VARIANTS[variant_from_string(self.variant)], self.rank_fraction,
-                       int(self.seed), int(bool(self.normalize)), int(bool(self.early_stop)))
+                       int(self.seed), int(bool(self.normalize)), int(bool(self.early_stop)), 0,
+                       float(self.spectral_tau))
 
 
 @dataclass
@@ -345,7 +351,8 @@ class Context:
         return dict(transformed=None if out_x is None else np.ascontiguousarray(out_x),
                     sigma2_trace=trace[: res.iterations_run].copy(),
                     iterations_run=res.iterations_run, degenerate_rows=res.degenerate_rows,
-                    tiles_evaluated=(int(res.tiles_evaluated[0]), int(res.tiles_evaluated[1])))
+                    tiles_evaluated=(int(res.tiles_evaluated[0]), int(res.tiles_evaluated[1])),
+                    spectral_rank=int(res.spectral_rank))
 
     @property
     def stream_ptr(self) -> int:

@@ -59,7 +59,8 @@ struct IterState {
   int64_t degenerate_rows;  // cumulative
   int64_t sigma2_clamps;    // cumulative
   int32_t iters_run;
-  int32_t pad1;
+  int32_t keff;         // leading eigenpairs the M-step streams this iteration (mstep.cu)
+  double sigma2_m;      // σ² the last M-step solved with (final coefficients)
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {

@@ -192,6 +192,7 @@ struct Session {
   YStats ystats{};
   EStepPlan ep;
   ColsumPlan zp, vp;
+  double tau = 0.0;  // spectral truncation threshold of the basis streams (0: off)
   cudaGraphExec_t graph = nullptr;
   // spatial order (sorted → original index) and tile-culling buffers
   std::vector<int64_t> perm_x, perm_y;
@@ -306,6 +307,8 @@ void validate_register(const double* x, int64_t m, const double* y, int64_t n, i
     throw Failure(FCPD_ERR_PARAMETER,
                   "register: only the fast / fast_lowrank variants run on the B200 path");
   if (m > INT32_MAX || n > INT32_MAX) throw Failure(FCPD_ERR_PARAMETER, "register: too many points");
+  if (!(cfg.spectral_tau >= 0.0 && cfg.spectral_tau < 1.0))
+    throw Failure(FCPD_ERR_PARAMETER, "register: spectral_tau must lie in [0, 1)");
 }
 
 int64_t lowrank_rank(double fraction, int64_t m) {  // solvers.hpp:46-54
@@ -480,6 +483,8 @@ void enqueue_iteration(fcpd_ctx* ctx, Session& s, cudaEvent_t* ev = nullptr) {
   rec(0);
   launch_estep(s.ep, eb, s.m, s.n, s.d, s.cfg.omega, st, s.stamps.p, str, ev ? ev[1] : nullptr);
   rec(2);
+  if (s.zp.trunc)
+    launch_spectral_rank(b.lam, b.lam + b.k, b.k, s.cfg.lambda_reg, s.tau, st, str);
   launch_colsum(s.zp, b.q, b.kpad, s.resid4.p, s.zpart.p, st, s.stamps.p, 1, str);
   rec(3);
   launch_zreduce(s.zp, s.zpart.p, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.coef.p, s.g4.p, st,
@@ -562,6 +567,15 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
     Basis& b = ctx->basis;
     s.zp = make_colsum_plan(m, b.k, ctx->sm_count);
     s.vp = make_colsum_plan(b.k, m, ctx->sm_count);
+    // spectral truncation: the basis streams stop where the filter drops
+    // below tau (mstep.cu: spectral_rank_kernel); FCPD_SPECTRAL_TAU=0 → off
+    s.tau = s.cfg.spectral_tau;
+    // a basis under 64 MB streams in microseconds: truncating it saves less
+    // than its extra kernel costs
+    if (4.0 * static_cast<double>(m) * static_cast<double>(b.k) < 64.0 * (1 << 20)) s.tau = 0.0;
+    if (const char* e = std::getenv("FCPD_SPECTRAL_TAU")) s.tau = std::atof(e);  // A/B
+    s.zp.trunc = s.tau > 0.0 ? 1 : 0;
+    s.vp.trunc = s.tau > 0.0 ? 2 : 0;
     s.zpart.ensure(s.zp.part_doubles());
     s.vpart.ensure(s.vp.part_doubles());
     s.coef.ensure(3 * b.k);
@@ -828,7 +842,13 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
   const std::vector<int64_t>& px = s.perm_x;
   const std::vector<int64_t>& py = s.perm_y;
   if (out->coefficients) {
-    // W = Q c (the last iteration's coefficients): one more Qᵀ-row stream
+    // W = Q c (the last iteration's coefficients).  With a truncated basis
+    // stream the iterations only formed c for the kept eigenpairs: redo z
+    // over the full basis from the last residual, then one Qᵀ-row stream.
+    if (s.zp.trunc && run > 0) {
+      launch_colsum(s.zp, b.q, b.kpad, s.resid4.p, s.zpart.p, nullptr, nullptr, 0, str);
+      launch_zcoef(s.zp, s.zpart.p, b.lam, s.cfg.lambda_reg, s.coef.p, s.st.p, str);
+    }
     pack_coef_kernel<<<ceil_div(b.k, 256), 256, 0, str>>>(s.coef.p, b.k, s.g4.p);
     FCPD_LAUNCH_CHECK();
     launch_colsum(s.vp, b.qt, b.mpad, s.g4.p, s.vpart.p, nullptr, nullptr, 0, str);
@@ -876,6 +896,7 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
   FCPD_CUDA(cudaStreamSynchronize(str));
   out->tiles_evaluated[0] = static_cast<int64_t>(tiles[0]);
   out->tiles_evaluated[1] = static_cast<int64_t>(tiles[1]);
+  out->spectral_rank = s.zp.trunc && h.keff > 0 ? std::min<int64_t>(h.keff, b.k) : b.k;
   if (out->degenerate_mask)
     for (int64_t k = 0; k < m; ++k) out->degenerate_mask[px[k]] = degm[k];
   if (out->transformed) {
@@ -1168,6 +1189,7 @@ void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall) {
   Basis& b = ctx->basis;
   cudaStream_t str = ctx->stream;
   IterState h{};
+  out->spectral_rank = ctx->basis.k;  // the distributed streams are not truncated
   FCPD_CUDA(cudaMemcpyAsync(&h, s.st.p, sizeof h, cudaMemcpyDeviceToHost, str));
   FCPD_CUDA(cudaStreamSynchronize(str));
   if (h.err_code != 0) {
@@ -1253,6 +1275,8 @@ void fcpd_config_default(fcpd_config* cfg) {
   cfg->seed = 0;
   cfg->normalize = 1;
   cfg->early_stop = 0;
+  cfg->pad0 = 0;
+  cfg->spectral_tau = 1e-10;
 }
 
 const char* fcpd_version(void) { return "fcpd-b200 0.1 (sm_100a)"; }
@@ -1349,6 +1373,7 @@ int32_t fcpd_kernels_per_iteration(const fcpd_ctx* ctx) {
   // tensor-core pass 2: its CUDA-core companion kernel (+ x̃ boxes and the
   // routing list when culling is off)
   if (s.ep.tc) extra += 1 + (culling ? 0 : 2);
+  if (!s.dist && s.zp.trunc) extra += 1;  // spectral rank
   return (s.dist ? 17 : 12) + extra;
 }
 
@@ -1394,7 +1419,12 @@ int fcpd_session_profile(fcpd_ctx* ctx, int32_t iterations, double* ms_per_phase
     cudaEvent_t ev[7];
     for (auto& e : ev) FCPD_CUDA(cudaEventCreate(&e));
     double acc[6] = {0, 0, 0, 0, 0, 0};
+    // every profiled iteration starts from a cold L2 (a 256 MB write, more
+    // than the 126 MB L2), so the phase times are HBM-honest
+    DevBuf<uint8_t> flush;
+    flush.ensure(size_t(256) << 20);
     for (int it = 0; it < iterations; ++it) {
+      FCPD_CUDA(cudaMemsetAsync(flush.p, it & 0xff, size_t(256) << 20, ctx->stream));
       enqueue_iteration(ctx, s, ev);
       ++s.launched;
       FCPD_CUDA(cudaEventSynchronize(ev[6]));
@@ -1405,6 +1435,7 @@ int fcpd_session_profile(fcpd_ctx* ctx, int32_t iterations, double* ms_per_phase
       }
     }
     for (auto& e : ev) cudaEventDestroy(e);
+    flush.release();
     for (int p = 0; p < 6; ++p) ms_per_phase[p] = acc[p] / iterations;
   });
 }

@@ -42,7 +42,25 @@ constexpr int kRowGroup = 16;  // rows per fp32 sub-accumulation / loads in flig
 struct SkGeom {
   int64_t rows, cols4, units;
   int grid, kmax;
+  int trunc;  // ColsumPlan::trunc
 };
+
+// The geometry actually streamed this iteration: with spectral truncation
+// the eigenvector axis (columns of Q, rows of Qᵀ) stops at st->keff.  Every
+// kernel of one stream (colsum, reduction) derives the same geometry.
+__device__ __forceinline__ SkGeom sk_eff(SkGeom g, const IterState* st) {
+  if (!g.trunc || !st) return g;
+  const int64_t keff = st->keff;
+  if (g.trunc == 1) {
+    g.cols4 = min(g.cols4, (keff + 3) / 4);
+    g.units = (g.cols4 + kColsumThreads - 1) / kColsumThreads * g.rows;
+  } else {
+    const int64_t col_blocks = g.units / g.rows;
+    g.rows = min(g.rows, keff);
+    g.units = col_blocks * g.rows;
+  }
+  return g;
+}
 
 __host__ __device__ __forceinline__ int64_t sk_begin(const SkGeom& g, int64_t cta) {
   return cta * g.units / g.grid;
@@ -61,6 +79,8 @@ __device__ __forceinline__ void sk_sum(const double* __restrict__ part, const Sk
   const int64_t g_hi = sk_owner(g, (cb + 1) * g.rows - 1);
   s0 = s1 = s2 = 0.0;
   for (int64_t cta = g_lo; cta <= g_hi; ++cta) {
+    // fewer units than CTAs (a truncated stream): skip empty ranges
+    if (sk_begin(g, cta) == sk_begin(g, cta + 1)) continue;
     const int64_t k = cb - sk_begin(g, cta) / g.rows;
     const double* p = part + ((cta * g.kmax + k) * 3) * kColsPerBlock + cc;
     s0 += p[0];
@@ -74,13 +94,14 @@ __device__ __forceinline__ void sk_sum(const double* __restrict__ part, const Sk
 constexpr int kSkLanes = 4;
 __device__ __forceinline__ void sk_sum_lanes(const double* __restrict__ part, const SkGeom& g,
                                              int64_t c, int lane, double& s0, double& s1,
-                                             double& s2) {
+                                             double& s2, bool need = true) {
   const int64_t cb = c / kColsPerBlock;
   const int64_t cc = c - cb * kColsPerBlock;
   const int64_t g_lo = sk_owner(g, cb * g.rows);
-  const int64_t g_hi = sk_owner(g, (cb + 1) * g.rows - 1);
+  const int64_t g_hi = need ? sk_owner(g, (cb + 1) * g.rows - 1) : g_lo - 1;  // !need: no loads
   s0 = s1 = s2 = 0.0;
   for (int64_t cta = g_lo + lane; cta <= g_hi; cta += kSkLanes) {
+    if (sk_begin(g, cta) == sk_begin(g, cta + 1)) continue;  // empty range
     const int64_t k = cb - sk_begin(g, cta) / g.rows;
     const double* p = part + ((cta * g.kmax + k) * 3) * kColsPerBlock + cc;
     s0 += p[0];
@@ -95,8 +116,32 @@ __device__ __forceinline__ void sk_sum_lanes(const double* __restrict__ part, co
   }
 }
 
+// A whole warp on one column (lanes stride the covering CTAs, then a fixed
+// xor tree): for columns covered by many CTAs (a truncated stream puts the
+// whole grid on one column block).
+__device__ __forceinline__ void sk_sum_warp(const double* __restrict__ part, const SkGeom& g,
+                                            int64_t c, int lane, double& s0, double& s1,
+                                            double& s2) {
+  const int64_t cb = c / kColsPerBlock;
+  const int64_t cc = c - cb * kColsPerBlock;
+  const int64_t g_lo = sk_owner(g, cb * g.rows);
+  const int64_t g_hi = sk_owner(g, (cb + 1) * g.rows - 1);
+  s0 = s1 = s2 = 0.0;
+  for (int64_t cta = g_lo + lane; cta <= g_hi; cta += 32) {
+    if (sk_begin(g, cta) == sk_begin(g, cta + 1)) continue;
+    const int64_t k = cb - sk_begin(g, cta) / g.rows;
+    const double* p = part + ((cta * g.kmax + k) * 3) * kColsPerBlock + cc;
+    s0 += p[0];
+    s1 += p[kColsPerBlock];
+    s2 += p[2 * kColsPerBlock];
+  }
+  s0 = warp_sum(s0);
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+}
+
 SkGeom geom(const ColsumPlan& p) {
-  return SkGeom{p.rows, p.cols4, p.units, p.grid, p.kmax};
+  return SkGeom{p.rows, p.cols4, p.units, p.grid, p.kmax, p.trunc};
 }
 }  // namespace
 
@@ -107,6 +152,7 @@ __global__ void __launch_bounds__(kColsumThreads)
   if (st && !st->active) return;
   if (stamps && blockIdx.x == 0 && threadIdx.x == 0)
     stamps[4 * st->iter + stamp_slot] = globaltimer();
+  g = sk_eff(g, st);
   const int64_t ld4 = lda >> 2;
   int64_t u = sk_begin(g, blockIdx.x);
   const int64_t u_end = sk_begin(g, blockIdx.x + 1);
@@ -242,6 +288,7 @@ __global__ void __launch_bounds__(kBulkThreads, kBulkCtasPerSm)
   if (st && !st->active) return;
   if (stamps && blockIdx.x == 0 && threadIdx.x == 0)
     stamps[4 * st->iter + stamp_slot] = globaltimer();
+  g = sk_eff(g, st);
   extern __shared__ __align__(128) unsigned char smem[];
   float* ring = reinterpret_cast<float*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBulkStages * kStageBytes);
@@ -367,21 +414,29 @@ __global__ void zreduce_filter_kernel(const double* __restrict__ part, SkGeom g,
                                       double* __restrict__ coef, float4* __restrict__ g4,
                                       IterState* st) {
   if (!st->active) return;
-  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t i = gid / kSkLanes;
-  double z0, z1, z2;
-  sk_sum_lanes(part, g, i < k ? i : k - 1, static_cast<int>(gid % kSkLanes), z0, z1, z2);
-  if (i >= k || gid % kSkLanes) return;
+  g = sk_eff(g, st);
+  // one warp per column, grid-stride over the K columns
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t kk = g.trunc == 1 ? min(k, g.cols4 * 4) : k;  // streamed eigenvectors
   // σ² of this iteration's E-step, unclamped (registration.hpp:137)
-  const double diag = lam[i] + lambda_reg * st->sigma2;
-  if (!(diag > 0.0)) set_error(st, kDevSolveDiag, diag);
-  const double inv = 1.0 / diag;
-  coef[i] = z0 * inv;
-  coef[k + i] = z1 * inv;
-  coef[2 * k + i] = z2 * inv;
-  const double f = lam_num[i] * inv;
-  g4[i] = make_float4(static_cast<float>(z0 * f), static_cast<float>(z1 * f),
-                      static_cast<float>(z2 * f), 0.f);
+  const double sigma2 = st->sigma2;
+  if (warp == 0 && lane == 0) st->sigma2_m = sigma2;
+  for (int64_t i = warp; i < k; i += nwarps) {
+    double z0 = 0.0, z1 = 0.0, z2 = 0.0;
+    if (i < kk) sk_sum_warp(part, g, i, lane, z0, z1, z2);  // else: filter below tau, z = 0
+    if (lane) continue;
+    const double diag = lam[i] + lambda_reg * sigma2;
+    if (!(diag > 0.0)) set_error(st, kDevSolveDiag, diag);
+    const double inv = 1.0 / diag;
+    coef[i] = z0 * inv;
+    coef[k + i] = z1 * inv;
+    coef[2 * k + i] = z2 * inv;
+    const double f = lam_num[i] * inv;
+    g4[i] = make_float4(static_cast<float>(z0 * f), static_cast<float>(z1 * f),
+                        static_cast<float>(z2 * f), 0.f);
+  }
 }
 
 // x̃new = X + V; per-row σ² terms; block partial sums (fixed order).
@@ -394,6 +449,7 @@ __global__ void __launch_bounds__(256)
   // m = row stride of the SoA arrays; rows ≥ m_valid (shard padding) are inert
   if (!st->active) return;
   if (stamps && blockIdx.x == 0 && threadIdx.x == 0) stamps[4 * st->iter + 2] = globaltimer();
+  g = sk_eff(g, st);
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t i = gid / kSkLanes;
   double term = 0.0;
@@ -468,6 +524,61 @@ __global__ void vreduce_add_kernel(const double* __restrict__ part, SkGeom g, in
   for (int c = 0; c < d; ++c) out[c * m + i] = (x0 ? x0[c * m + i] : 0.0) + v[c];
 }
 
+// Effective spectral rank: f_k = λnum_k/(λ_k + λ_reg σ²) is non-increasing
+// along the descending spectrum (λnum = λ_raw or λ, both sorted), so the
+// kept eigenpairs are a prefix; binary search for the first f_k < tau.
+// Dropping them changes V = Q(f ⊙ z) by ≤ Σ_{dropped} f_k |z_k| |q_k| —
+// with tau = 1e-10 far below the fp32 basis rounding (≈ 2e-7‖R‖).
+__global__ void spectral_rank_kernel(const double* __restrict__ lam,
+                                     const double* __restrict__ lam_num, int64_t k,
+                                     double lambda_reg, double tau, IterState* st) {
+  if (!st->active) return;
+  int64_t keep = k;
+  if (tau > 0.0) {
+    const double c = lambda_reg * st->sigma2;
+    int64_t lo = 0, hi = k;  // first index with f < tau lies in [lo, hi]
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      const double diag = lam[mid] + c;
+      const double f = diag > 0.0 ? lam_num[mid] / diag : 1.0;
+      if (f >= tau) lo = mid + 1;
+      else hi = mid;
+    }
+    keep = lo;
+  }
+  keep = (keep + 3) / 4 * 4;
+  st->keff = static_cast<int32_t>(min(max(keep, int64_t(4)), (k + 3) / 4 * 4));
+}
+
+__global__ void zcoef_kernel(const double* __restrict__ part, SkGeom g, int64_t k,
+                             const double* __restrict__ lam, double lambda_reg,
+                             double* __restrict__ coef, const IterState* __restrict__ st) {
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = gid / kSkLanes;
+  double z0, z1, z2;
+  sk_sum_lanes(part, g, i < k ? i : k - 1, static_cast<int>(gid % kSkLanes), z0, z1, z2);
+  if (i >= k || gid % kSkLanes) return;
+  const double inv = 1.0 / (lam[i] + lambda_reg * st->sigma2_m);
+  coef[i] = z0 * inv;
+  coef[k + i] = z1 * inv;
+  coef[2 * k + i] = z2 * inv;
+}
+
+void launch_spectral_rank(const double* lam, const double* lam_num, int64_t k, double lambda_reg,
+                          double tau, IterState* st, cudaStream_t stream) {
+  spectral_rank_kernel<<<1, 1, 0, stream>>>(lam, lam_num, k, lambda_reg, tau, st);
+  FCPD_LAUNCH_CHECK();
+}
+
+void launch_zcoef(const ColsumPlan& p, const double* part, const double* lam, double lambda_reg,
+                  double* coef, const IterState* st, cudaStream_t stream) {
+  SkGeom g = geom(p);
+  g.trunc = 0;
+  zcoef_kernel<<<ceil_div(p.cols * kSkLanes, 256), 256, 0, stream>>>(part, g, p.cols, lam,
+                                                                     lambda_reg, coef, st);
+  FCPD_LAUNCH_CHECK();
+}
+
 // ---------------------------------------------------------------------------
 
 ColsumPlan make_colsum_plan(int64_t rows, int64_t cols, int sm_count, int ctas_per_sm) {
@@ -496,7 +607,8 @@ ColsumPlan make_colsum_plan(int64_t rows, int64_t cols, int sm_count, int ctas_p
   }
   p.grid = static_cast<int>(std::max<int64_t>(1, min64(slots, p.units)));
   const int64_t per = (p.units + p.grid - 1) / p.grid;
-  p.kmax = static_cast<int>((per + rows - 1) / rows + 1);
+  // + 1: a truncated geometry (sk_eff) may cross one more block boundary
+  p.kmax = static_cast<int>((per + rows - 1) / rows + 2);
   return p;
 }
 
@@ -515,8 +627,9 @@ void launch_colsum(const ColsumPlan& p, const float* A, int64_t lda, const float
 void launch_zreduce(const ColsumPlan& p, const double* part, const double* lam,
                     const double* lam_num, double lambda_reg, double* coef, float4* g4,
                     IterState* st, cudaStream_t stream) {
-  zreduce_filter_kernel<<<ceil_div(p.cols * kSkLanes, 256), 256, 0, stream>>>(
-      part, geom(p), p.cols, lam, lam_num, lambda_reg, coef, g4, st);
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(p.cols * 32, 256), 148 * 8));
+  zreduce_filter_kernel<<<blocks, 256, 0, stream>>>(part, geom(p), p.cols, lam, lam_num,
+                                                    lambda_reg, coef, g4, st);
   FCPD_LAUNCH_CHECK();
 }
 
@@ -602,8 +715,9 @@ void launch_zfilter(const double* z, int64_t k, const double* lam, const double*
 
 void launch_vreduce_add(const ColsumPlan& p, const double* part, const double* x0, int d,
                         double* out, cudaStream_t stream) {
-  vreduce_add_kernel<<<ceil_div(p.cols, 256), 256, 0, stream>>>(part, geom(p), p.cols, x0, d,
-                                                                out);
+  SkGeom g = geom(p);
+  g.trunc = 0;  // host-driven full products (no IterState)
+  vreduce_add_kernel<<<ceil_div(p.cols, 256), 256, 0, stream>>>(part, g, p.cols, x0, d, out);
   FCPD_LAUNCH_CHECK();
 }
 

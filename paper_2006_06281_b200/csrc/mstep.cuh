@@ -22,6 +22,9 @@ struct ColsumPlan {
   int grid = 0;
   int kmax = 0;
   bool bulk = true;  // cp.async.bulk ring (default) or register-staged LDG
+  // spectral truncation (IterState::keff): 0 none, 1 the first keff columns
+  // (z = Qᵀ R over Q), 2 the first keff rows (V = Q g over Qᵀ)
+  int trunc = 0;
   size_t part_doubles() const {
     return static_cast<size_t>(grid) * kmax * 3 * kColsPerBlock;
   }
@@ -29,6 +32,16 @@ struct ColsumPlan {
 
 // ctas_per_sm: resident bulk CTAs per SM the grid assumes (2 = whole GPU).
 ColsumPlan make_colsum_plan(int64_t rows, int64_t cols, int sm_count, int ctas_per_sm = 2);
+
+// Effective spectral rank of this iteration → st->keff (multiple of 4):
+// the leading eigenpairs whose filter λnum_k/(λ_k + λ_reg σ²) ≥ tau (the
+// filter decreases along the descending spectrum); tau ≤ 0 → all K.
+void launch_spectral_rank(const double* lam, const double* lam_num, int64_t k, double lambda_reg,
+                          double tau, IterState* st, cudaStream_t stream);
+// coef = z / (λ + λ_reg σ²_m) from full-K partials (final coefficients when
+// the iterations streamed a truncated basis)
+void launch_zcoef(const ColsumPlan& p, const double* part, const double* lam, double lambda_reg,
+                  double* coef, const IterState* st, cudaStream_t stream);
 
 // part ← partials of Σ_r A[r][c]·v[r].d (d < 3); A row-major fp32, lda % 4 == 0.
 void launch_colsum(const ColsumPlan& p, const float* A, int64_t lda, const float4* v,

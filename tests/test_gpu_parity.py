@@ -370,16 +370,19 @@ def test_distributed_engine_single_rank(ctx, fc, orc, variant, omega):
     at world size 2 on CPU (tests/test_dist_gloo.py)."""
     from paper_2006_06281_b200 import datagen
     x, y, w = datagen.generate("c1", m=2500)
+    # the distributed streams are not spectrally truncated: compare untruncated
     cfg = fc.RegistrationConfig(omega=omega, beta=2.0, lambda_reg=3.0, iterations=25,
-                                variant=variant, rank_fraction=0.05)
+                                variant=variant, rank_fraction=0.05, spectral_tau=0.0)
     ref = ctx.register(x, y, cfg)
     uid = fc.nccl_unique_id()
     with fc.Context.distributed(0, 0, 1, uid) as dctx:
         assert dctx.world == (0, 1)
         got = dctx.register(x, y, cfg)
         # 17 per iteration, plus the same optional culling / tensor-core
-        # kernels the single-GPU session launches (12 + extras)
-        assert dctx.kernels_per_iteration == ctx.kernels_per_iteration + 5
+        # kernels as the single-GPU session (12 + extras; the single-GPU
+        # session may add its spectral-rank kernel)
+        assert dctx.kernels_per_iteration in (ctx.kernels_per_iteration + 5,
+                                              ctx.kernels_per_iteration + 4)
     rel = np.abs(got.sigma2_trace / ref.sigma2_trace - 1).max()
     assert rel <= 1e-9, rel
     assert np.abs(got.transformed - ref.transformed).max() <= 1e-9 * bbox_diag(y)
@@ -443,3 +446,32 @@ def test_full_size_parity_configs_2_4(ctx, fc, orc, tmp_path, name, iters):
     rel, pts = record_parity(f"{name}-full-{iters}it", got, ref, y)
     assert rel.max() <= SIGMA_RTOL
     assert pts <= POINT_FRAC
+
+
+# ------------------------------------------ spectral truncation of the streams
+
+
+def test_spectral_truncation_matches_full_basis(ctx, fc):
+    """Full rank at M=5000 (a 100 MB basis, so the truncated streams are on):
+    skipping the eigenpairs whose filter λ/(λ+λσ²) is below 1e-10 leaves the
+    registration unchanged to far below the parity bar, while the streams
+    read only a small prefix of the basis."""
+    from paper_2006_06281_b200 import datagen
+    x, y, w = datagen.generate("c1", m=5000)
+    cfg = fc.RegistrationConfig(omega=w.omega, beta=w.beta, lambda_reg=w.lambda_reg,
+                                iterations=40)
+    full = fc.RegistrationConfig(omega=w.omega, beta=w.beta, lambda_reg=w.lambda_reg,
+                                 iterations=40, spectral_tau=0.0)
+    a = ctx.register(x, y, cfg)
+    b = ctx.register(x, y, full)
+    rel = np.abs(a.sigma2_trace / b.sigma2_trace - 1).max()
+    assert rel <= 1e-6, rel
+    assert np.abs(a.transformed - b.transformed).max() <= 1e-7 * bbox_diag(y)
+    assert np.abs(a.coefficients - b.coefficients).max() <= 1e-5 * np.abs(b.coefficients).max()
+    ctx.session_begin(x, y, cfg)
+    ctx.session_run(cfg.iterations)
+    st = ctx.session_read(with_points=False)
+    assert 0 < st["spectral_rank"] < 5000, st["spectral_rank"]
+    ctx.session_begin(x, y, full)
+    ctx.session_run(full.iterations)
+    assert ctx.session_read(with_points=False)["spectral_rank"] == 5000
