@@ -423,9 +423,12 @@ __global__ void zreduce_filter_kernel(const double* __restrict__ part, SkGeom g,
   // σ² of this iteration's E-step, unclamped (registration.hpp:137)
   const double sigma2 = st->sigma2;
   if (warp == 0 && lane == 0) st->sigma2_m = sigma2;
-  for (int64_t i = warp; i < k; i += nwarps) {
-    double z0 = 0.0, z1 = 0.0, z2 = 0.0;
-    if (i < kk) sk_sum_warp(part, g, i, lane, z0, z1, z2);  // else: filter below tau, z = 0
+  // columns ≥ kk (filter below tau) are neither streamed nor read this
+  // iteration: V stops at the same keff, and the final coefficients are
+  // recomputed over the full basis (launch_zcoef)
+  for (int64_t i = warp; i < kk; i += nwarps) {
+    double z0, z1, z2;
+    sk_sum_warp(part, g, i, lane, z0, z1, z2);
     if (lane) continue;
     const double diag = lam[i] + lambda_reg * sigma2;
     if (!(diag > 0.0)) set_error(st, kDevSolveDiag, diag);
@@ -627,7 +630,7 @@ void launch_colsum(const ColsumPlan& p, const float* A, int64_t lda, const float
 void launch_zreduce(const ColsumPlan& p, const double* part, const double* lam,
                     const double* lam_num, double lambda_reg, double* coef, float4* g4,
                     IterState* st, cudaStream_t stream) {
-  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(p.cols * 32, 256), 148 * 8));
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(p.cols * 32, 256), 148 * 2));
   zreduce_filter_kernel<<<blocks, 256, 0, stream>>>(part, geom(p), p.cols, lam, lam_num,
                                                     lambda_reg, coef, g4, st);
   FCPD_LAUNCH_CHECK();
