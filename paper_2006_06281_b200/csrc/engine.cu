@@ -831,6 +831,8 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
   out->basis_reused = s.basis_reused ? 1 : 0;
   out->sigma2_initial = s.sigma2_initial;
   out->degenerate_rows = h.degenerate_rows;
+  out->spectral_rank = s.zp.trunc && h.keff > 0 ? std::min<int64_t>(h.keff, ctx->basis.k)
+                                                 : ctx->basis.k;
   out->sigma2_clamps = h.sigma2_clamps;
   if (out->sigma2_trace && run > 0)
     FCPD_CUDA(cudaMemcpyAsync(out->sigma2_trace, s.trace.p, sizeof(double) * run,
@@ -967,6 +969,8 @@ void enqueue_iteration_dist(fcpd_ctx* ctx, Session& s) {
   launch_fallback_finalize_own(s.fsum_own.p, s.fmax_all.p + s.m0, s.mask_own.p, s.mr, s.xt64.p, o,
                                s.ystats, st, str);
   // M-step on the own row shard of the basis
+  if (s.zp.trunc)
+    launch_spectral_rank(b.lam, b.lam + b.k, b.k, s.cfg.lambda_reg, s.tau, st, str);
   launch_colsum(s.zp, b.q + s.m0 * b.kpad, b.kpad, s.resid4.p, s.zpart.p, st, s.stamps.p, 1, str);
   launch_zsum(s.zp, s.zpart.p, s.zfull.p, st, str);
   FCPD_NCCL(ncclAllReduce(s.zfull.p, s.zfull.p, 3 * b.k, ncclDouble, ncclSum, comm, str));
@@ -1129,6 +1133,13 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
                                 cudaMemcpyDeviceToDevice, str));
   s.zp = make_colsum_plan(s.m_valid_own, b.k, ctx->sm_count);
   s.vp = make_colsum_plan(b.k, mr, ctx->sm_count);
+  // spectral truncation as on one GPU (the cut is the same on every rank:
+  // it depends only on λ and the all-reduced σ²)
+  s.tau = s.cfg.spectral_tau;
+  if (4.0 * static_cast<double>(m) * static_cast<double>(b.k) < 64.0 * (1 << 20)) s.tau = 0.0;
+  if (const char* e = std::getenv("FCPD_SPECTRAL_TAU")) s.tau = std::atof(e);
+  s.zp.trunc = s.tau > 0.0 ? 1 : 0;
+  s.vp.trunc = s.tau > 0.0 ? 2 : 0;
   s.zpart.ensure(s.zp.part_doubles());
   s.vpart.ensure(s.vp.part_doubles());
   s.zfull.ensure(3 * b.k);
@@ -1189,7 +1200,6 @@ void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall) {
   Basis& b = ctx->basis;
   cudaStream_t str = ctx->stream;
   IterState h{};
-  out->spectral_rank = ctx->basis.k;  // the distributed streams are not truncated
   FCPD_CUDA(cudaMemcpyAsync(&h, s.st.p, sizeof h, cudaMemcpyDeviceToHost, str));
   FCPD_CUDA(cudaStreamSynchronize(str));
   if (h.err_code != 0) {
@@ -1224,6 +1234,14 @@ void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall) {
         out->transformed[c * s.m + px[k]] =
             s.cfg.normalize ? xt[c * s.m + k] * s.scale + s.center[c] : xt[c * s.m + k];
   if (out->coefficients) {
+    if (s.zp.trunc && run > 0) {  // the iterations streamed a truncated basis
+      launch_colsum(s.zp, b.q + s.m0 * b.kpad, b.kpad, s.resid4.p, s.zpart.p, nullptr, nullptr,
+                    0, str);
+      launch_zsum(s.zp, s.zpart.p, s.zfull.p, nullptr, str);
+      FCPD_NCCL(ncclAllReduce(s.zfull.p, s.zfull.p, 3 * b.k, ncclDouble, ncclSum, ctx->comm,
+                              str));
+      launch_zcoef_full(s.zfull.p, b.k, b.lam, s.cfg.lambda_reg, s.coef.p, s.st.p, str);
+    }
     pack_coef_kernel<<<ceil_div(b.k, 256), 256, 0, str>>>(s.coef.p, b.k, s.g4.p);
     FCPD_LAUNCH_CHECK();
     launch_colsum(s.vp, s.qt_own.p, s.mr4, s.g4.p, s.vpart.p, nullptr, nullptr, 0, str);
@@ -1373,7 +1391,7 @@ int32_t fcpd_kernels_per_iteration(const fcpd_ctx* ctx) {
   // tensor-core pass 2: its CUDA-core companion kernel (+ x̃ boxes and the
   // routing list when culling is off)
   if (s.ep.tc) extra += 1 + (culling ? 0 : 2);
-  if (!s.dist && s.zp.trunc) extra += 1;  // spectral rank
+  if (s.zp.trunc) extra += 1;  // spectral rank
   return (s.dist ? 17 : 12) + extra;
 }
 

@@ -669,18 +669,25 @@ void launch_sigma_final(const double* sig_part, int blocks, int64_t m_global, in
   FCPD_LAUNCH_CHECK();
 }
 
-// z (SoA 3×K) = Σ stream-K partials, no filter (distributed path: all-reduced next)
+// z (SoA 3×K) = Σ stream-K partials, no filter (distributed path: all-reduced
+// next).  One warp per column; columns outside this iteration's truncated
+// stream are zero so the all-reduce carries no stale values.
 __global__ void zsum_kernel(const double* __restrict__ part, SkGeom g, int64_t k,
                             double* __restrict__ z, const IterState* __restrict__ st) {
   if (st && !st->active) return;
-  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t i = gid / kSkLanes;
-  double z0, z1, z2;
-  sk_sum_lanes(part, g, i < k ? i : k - 1, static_cast<int>(gid % kSkLanes), z0, z1, z2);
-  if (i >= k || gid % kSkLanes) return;
-  z[i] = z0;
-  z[k + i] = z1;
-  z[2 * k + i] = z2;
+  g = sk_eff(g, st);
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t kk = g.trunc == 1 ? min(k, g.cols4 * 4) : k;
+  for (int64_t i = warp; i < k; i += nwarps) {
+    double z0 = 0.0, z1 = 0.0, z2 = 0.0;
+    if (i < kk) sk_sum_warp(part, g, i, lane, z0, z1, z2);
+    if (lane) continue;
+    z[i] = z0;
+    z[k + i] = z1;
+    z[2 * k + i] = z2;
+  }
 }
 
 __global__ void zfilter_kernel(const double* __restrict__ z, int64_t k,
@@ -690,6 +697,7 @@ __global__ void zfilter_kernel(const double* __restrict__ z, int64_t k,
   if (!st->active) return;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= k) return;
+  if (i == 0) st->sigma2_m = st->sigma2;
   const double diag = lam[i] + lambda_reg * st->sigma2;
   if (!(diag > 0.0)) set_error(st, kDevSolveDiag, diag);
   const double inv = 1.0 / diag;
@@ -704,7 +712,28 @@ __global__ void zfilter_kernel(const double* __restrict__ z, int64_t k,
 
 void launch_zsum(const ColsumPlan& p, const double* part, double* z, const IterState* st,
                  cudaStream_t stream) {
-  zsum_kernel<<<ceil_div(p.cols * kSkLanes, 256), 256, 0, stream>>>(part, geom(p), p.cols, z, st);
+  SkGeom g = geom(p);
+  if (!st) g.trunc = 0;  // host-driven full sum
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(p.cols * 32, 256), 148 * 2));
+  zsum_kernel<<<blocks, 256, 0, stream>>>(part, g, p.cols, z, st);
+  FCPD_LAUNCH_CHECK();
+}
+
+// coef = z / (λ + λ_reg σ²_m) from an assembled z (distributed final coefficients)
+__global__ void zcoef_full_kernel(const double* __restrict__ z, int64_t k,
+                                  const double* __restrict__ lam, double lambda_reg,
+                                  double* __restrict__ coef, const IterState* __restrict__ st) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= k) return;
+  const double inv = 1.0 / (lam[i] + lambda_reg * st->sigma2_m);
+  coef[i] = z[i] * inv;
+  coef[k + i] = z[k + i] * inv;
+  coef[2 * k + i] = z[2 * k + i] * inv;
+}
+
+void launch_zcoef_full(const double* z, int64_t k, const double* lam, double lambda_reg,
+                       double* coef, const IterState* st, cudaStream_t stream) {
+  zcoef_full_kernel<<<ceil_div(k, 256), 256, 0, stream>>>(z, k, lam, lambda_reg, coef, st);
   FCPD_LAUNCH_CHECK();
 }
 

@@ -43,6 +43,10 @@ void launch_spectral_rank(const double* lam, const double* lam_num, int64_t k, d
 void launch_zcoef(const ColsumPlan& p, const double* part, const double* lam, double lambda_reg,
                   double* coef, const IterState* st, cudaStream_t stream);
 
+// distributed final coefficients: coef = z / (λ + λ_reg σ²_m), z all-reduced
+void launch_zcoef_full(const double* z, int64_t k, const double* lam, double lambda_reg,
+                       double* coef, const IterState* st, cudaStream_t stream);
+
 // part ← partials of Σ_r A[r][c]·v[r].d (d < 3); A row-major fp32, lda % 4 == 0.
 void launch_colsum(const ColsumPlan& p, const float* A, int64_t lda, const float4* v,
                    double* part, const IterState* st, uint64_t* stamps, int stamp_slot,
