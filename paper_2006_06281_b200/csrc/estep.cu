@@ -286,10 +286,12 @@ __global__ void __launch_bounds__(128)
           for (int u = 0; u < 8; ++u) {
             const float4 va = xa[j + u];
             const float4 vb = xb[j + u];
-            float2 e = __fadd2_rn(on, make_float2(vb.z, vb.w));  // −|u|² − |v|²
-            e = __ffma2_rn(ox, make_float2(va.x, va.y), e);
+            // 2u·v − |v|² = |u|² − t: the column's own 2^{−|u|²} is factored
+            // out of its sum and applied once in fp64 (|u|² ≤ R² ≤ 16, so the
+            // shifted terms stay in range)
+            float2 e = __ffma2_rn(ox, make_float2(va.x, va.y), make_float2(vb.z, vb.w));
             e = __ffma2_rn(oy, make_float2(va.z, va.w), e);
-            e = __ffma2_rn(oz, make_float2(vb.x, vb.y), e);      // −t
+            e = __ffma2_rn(oz, make_float2(vb.x, vb.y), e);
             f = __fadd2_rn(f, ex2x2(e));
           }
         }
@@ -311,6 +313,10 @@ __global__ void __launch_bounds__(128)
       }
       d0 += static_cast<double>(f.x);
       d1 += static_cast<double>(f.y);
+    }
+    if (centred) {  // undo the factored-out 2^{|u|²}
+      d0 *= exp2(static_cast<double>(on.x));
+      d1 *= exp2(static_cast<double>(on.y));
     }
     double* out = seg + (g + rb) * kTile;
     out[2 * threadIdx.x] = d0;
@@ -538,10 +544,11 @@ __global__ void __launch_bounds__(128, 8)
             const float2 Q = yq[j + u];
             const float2 Ux = make_float2(A.x, A.y), Uy = make_float2(A.z, A.w);
             const float2 Uz = make_float2(B.x, B.y);
-            float2 L = __fadd2_rn(make_float2(B.z, B.w), on);  // b − |u|² − |v|²
-            L = __ffma2_rn(Ux, ox, L);
+            // b − |u|² + 2u·v = (b − t) + |v|²: the row's own 2^{|v|²} is
+            // factored out of its sums and undone once in fp64 (|v|² ≤ 16)
+            float2 L = __ffma2_rn(Ux, ox, make_float2(B.z, B.w));
             L = __ffma2_rn(Uy, oy, L);
-            L = __ffma2_rn(Uz, oz, L);                          // b − t
+            L = __ffma2_rn(Uz, oz, L);
             const float2 w = ex2x2(L);
             f0 = __fadd2_rn(f0, w);
             fx = __ffma2_rn(w, Ux, fx);
@@ -590,10 +597,16 @@ __global__ void __launch_bounds__(128, 8)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int li = 2 * t + h;
-      const double s0 = acc_s[0][h][t], s1 = acc_s[1][h][t], s2v = acc_s[2][h][t],
-                   s3 = acc_s[3][h][t], s4 = acc_s[4][h][t];
+      double s0 = acc_s[0][h][t], s1 = acc_s[1][h][t], s2v = acc_s[2][h][t],
+             s3 = acc_s[3][h][t], s4 = acc_s[4][h][t];
       if (centred) {
         const double vx = v[h][0], vy = v[h][1], vz = v[h][2], vq = v[h][3];
+        const double sc = exp2(-vq);  // undo the factored-out 2^{|v|²}
+        s0 *= sc;
+        s1 *= sc;
+        s2v *= sc;
+        s3 *= sc;
+        s4 *= sc;
         out[li] = s0;
         out[kTile + li] = s1 + static_cast<double>(bc.c.x) * s0;
         out[2 * kTile + li] = s2v + static_cast<double>(bc.c.y) * s0;
