@@ -60,9 +60,23 @@ struct DevBuf {
   }
 };
 
+// Basis-cache key of the (normalised, sorted) model: four independent
+// 64-bit multiply-xor lanes over 8-byte words (≈ 8× the byte-wise rate),
+// byte-wise FNV-1a for the tail, lanes folded at the end.
 uint64_t fnv1a(const void* data, size_t bytes, uint64_t h = 1469598103934665603ull) {
   const unsigned char* c = static_cast<const unsigned char*>(data);
-  for (size_t i = 0; i < bytes; ++i) {
+  constexpr uint64_t kMul = 0x9E3779B97F4A7C15ull;
+  uint64_t lane[4] = {h, h ^ 0x1ull, h ^ 0x2ull, h ^ 0x3ull};
+  size_t i = 0;
+  for (; i + 32 <= bytes; i += 32)
+    for (int l = 0; l < 4; ++l) {
+      uint64_t w;
+      std::memcpy(&w, c + i + 8 * l, 8);
+      lane[l] = (lane[l] ^ w) * kMul;
+      lane[l] ^= lane[l] >> 29;
+    }
+  for (int l = 0; l < 4; ++l) h = (h ^ lane[l]) * 1099511628211ull;
+  for (; i < bytes; ++i) {
     h ^= c[i];
     h *= 1099511628211ull;
   }
@@ -248,7 +262,6 @@ struct fcpd_ctx {
   int device = 0;
   int sm_count = 148;
   cudaStream_t stream = nullptr;
-  cudaStream_t side = nullptr;  // second stream forked inside the iteration graph
   cusolverDnHandle_t solver = nullptr;
   cublasHandle_t blas = nullptr;
   ncclComm_t comm = nullptr;  // set by fcpd_create_dist: scene-sharded EM over NCCL
@@ -734,8 +747,13 @@ void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, i
   s.n = n;
   s.d = d;
   s.cfg = cfg;
+  static const bool host_timing = std::getenv("FCPD_HOST_TIMING") != nullptr;
+  auto stamp = [&](const char* what) {
+    if (host_timing) std::fprintf(stderr, "[fcpd] begin %-12s %8.3f ms\n", what, 1e3 * since(t0));
+  };
   std::vector<double> xs, ys;
   normalize_pair_host(x, m, y, n, d, cfg.normalize != 0, xs, ys, s.center, &s.scale);
+  stamp("normalize");
   // internal order: Morton-sorted model and scene (undone on output); the
   // two sorts are independent
   {
@@ -743,13 +761,16 @@ void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, i
     s.perm_y = morton_sort(ys, n);
     tx.join();
   }
+  stamp("morton");
   // x0 must be on the device before the Gram build
   s.x0.ensure(3 * m);
   FCPD_CUDA(cudaMemcpyAsync(s.x0.p, xs.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice,
                             ctx->stream));
   ensure_basis(ctx, s, xs);
+  stamp("basis");
   ctx->basis.perm = s.perm_x;  // basis rows are in the session's sorted order
   prepare_buffers(ctx, s, xs, ys, cfg.iterations, true);
+  stamp("buffers");
   s.sigma2_initial = init_sigma2_host(xs, m, ys, n, d);
   if (cfg.iterations > 0 && !(cfg.omega >= 0.0 && cfg.omega < 1.0))
     throw Failure(FCPD_ERR_NUMERIC,
@@ -757,6 +778,7 @@ void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, i
   reset_state(ctx, s, s.sigma2_initial);
   FCPD_CUDA(cudaMemsetAsync(s.coef.p, 0, sizeof(double) * 3 * ctx->basis.k, ctx->stream));
 
+  stamp("state");
   // capture one EM iteration as a CUDA graph
   cudaGraph_t g = nullptr;
   FCPD_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
@@ -788,7 +810,9 @@ void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, i
   } else {
     cudaGraphDestroy(g);
   }
+  stamp("graph");
   FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
+  stamp("sync");
   s.t_setup_host = since(t0);
   s.launched = 0;
   s.ready = true;
@@ -1311,7 +1335,6 @@ int fcpd_create(fcpd_ctx** out, int device) {
     FCPD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     ctx->sm_count = sms;
     FCPD_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-    FCPD_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     if (cusolverDnCreate(&ctx->solver) != CUSOLVER_STATUS_SUCCESS)
       throw Failure(FCPD_ERR_CUDA, "cusolverDnCreate failed");
     if (cublasCreate(&ctx->blas) != CUBLAS_STATUS_SUCCESS)
@@ -1368,7 +1391,6 @@ void fcpd_destroy(fcpd_ctx* ctx) {
   if (ctx->solver) cusolverDnDestroy(ctx->solver);
   if (ctx->blas) cublasDestroy(ctx->blas);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
-  if (ctx->side) cudaStreamDestroy(ctx->side);
   delete ctx;
 }
 
