@@ -27,6 +27,13 @@ import sys
 import threading
 import time
 
+# stdout carries exactly one JSON line: NCCL's log goes to stderr, and its
+# VERSION level (a bare printf of the banner to stdout) is lowered to WARN
+if "NCCL_DEBUG_FILE" not in os.environ:
+    os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
+if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -181,7 +188,9 @@ def run_ours(args, world, rank, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     x, y_full, w = datagen.generate(args.workload)
-    sharded = world > 1 and not args.replicas
+    # --shard1: the NCCL-sharded engine path as a one-rank group (exercises
+    # the multi-GPU code path on one GPU; no rank waits on another)
+    sharded = (world > 1 and not args.replicas) or args.shard1
     prof_iters = 0 if sharded else 3
     total = args.warmup + args.steps + prof_iters
     cfg = datagen.config_for(w, iterations=total)
@@ -189,7 +198,8 @@ def run_ours(args, world, rank, local):
         # scene points sharded over ranks; the engine's own NCCL
         # communicator carries the per-iteration reductions
         obj = [fcpd.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
         ctx = fcpd.Context.distributed(local, rank, world, obj[0])
         n = y_full.shape[0]
         y = y_full[rank * n // world:(rank + 1) * n // world]
@@ -406,6 +416,8 @@ def main():
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas instead of the scene-sharded NCCL path")
     ap.add_argument("--watchdog-s", type=float, default=900.0)
+    ap.add_argument("--shard1", action="store_true",
+                    help="run the sharded (NCCL) engine path with a single rank")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: ≥ 3 warm-up steps

@@ -855,8 +855,6 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
   out->basis_reused = s.basis_reused ? 1 : 0;
   out->sigma2_initial = s.sigma2_initial;
   out->degenerate_rows = h.degenerate_rows;
-  out->spectral_rank = s.zp.trunc && h.keff > 0 ? std::min<int64_t>(h.keff, ctx->basis.k)
-                                                 : ctx->basis.k;
   out->sigma2_clamps = h.sigma2_clamps;
   if (out->sigma2_trace && run > 0)
     FCPD_CUDA(cudaMemcpyAsync(out->sigma2_trace, s.trace.p, sizeof(double) * run,
@@ -1245,6 +1243,8 @@ void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall) {
   out->basis_reused = s.basis_reused ? 1 : 0;
   out->sigma2_initial = s.sigma2_initial;
   out->degenerate_rows = static_cast<int64_t>(deg);
+  out->spectral_rank = s.zp.trunc && h.keff > 0 ? std::min<int64_t>(h.keff, ctx->basis.k)
+                                                 : ctx->basis.k;
   out->sigma2_clamps = h.sigma2_clamps;
   if (out->sigma2_trace && run > 0)
     FCPD_CUDA(cudaMemcpyAsync(out->sigma2_trace, s.trace.p, sizeof(double) * run,

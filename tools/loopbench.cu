@@ -134,6 +134,35 @@ __global__ void __launch_bounds__(128) loop_kernel(float* out, int occ_pad) {
           g0 = __ffma2_rn(B, ay, g0);
           gx = __ffma2_rn(B, az, gx);
           gy = __ffma2_rn(B, n2, gy);
+        } else if (V == 8) {  // tc_acc: L from registers (TMEM stand-in), 2 rows per V load
+          const float2 L0 = make_float2(A.x - t0, A.y), L1 = make_float2(B.x + t0, B.y);
+          const float2 w = ex2v<MUFU>(L0), w2 = ex2v<MUFU>(L1);
+          f0 = __fadd2_rn(f0, w);
+          g0 = __fadd2_rn(g0, w2);
+          fx = __ffma2_rn(w, A, fx);
+          gx = __ffma2_rn(w2, A, gx);
+          fy = __ffma2_rn(w, B, fy);
+          gy = __ffma2_rn(w2, B, gy);
+          fz = __ffma2_rn(w, C, fz);
+          gz = __ffma2_rn(w2, C, gz);
+          fq = __ffma2_rn(w, D, fq);
+          gq = __ffma2_rn(w2, D, gq);
+        } else if (V == 9) {  // col_fac: pass 1 with the factored constant (3 FFMA2 + FADD2)
+          float2 e = __ffma2_rn(ax, A, D);
+          e = __ffma2_rn(ay, B, e);
+          e = __ffma2_rn(az, C, e);
+          f0 = __fadd2_rn(f0, ex2v<MUFU>(e));
+        } else if (V == 10) {  // row_fac: pass 2 with the factored constant (3 + 5 packed)
+          const float2 Q = sq[j + u];
+          float2 L = __ffma2_rn(A, ax, D);
+          L = __ffma2_rn(B, ay, L);
+          L = __ffma2_rn(C, az, L);
+          const float2 w = ex2v<MUFU>(L);
+          f0 = __fadd2_rn(f0, w);
+          fx = __ffma2_rn(w, A, fx);
+          fy = __ffma2_rn(w, B, fy);
+          fz = __ffma2_rn(w, C, fz);
+          fq = __ffma2_rn(w, Q, fq);
         } else {  // col_ctr: FADD2 + 3 FFMA2 + 2 MUFU + FADD2
           float2 e = __fadd2_rn(n2, D);
           e = __ffma2_rn(ax, A, e);
@@ -184,6 +213,12 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   float* out;
   cudaMalloc(&out, sizeof(float) * sms * 32 * 128);
+  std::printf("-- current kernels' loops at 8 CTAs/SM (tc_acc = 128 pairs per point-warp)\n");
+  run<9, true>("col_fac", sms, 8, out);
+  run<10, true>("row_fac", sms, 8, out);
+  run<8, true>("tc_acc", sms, 8, out);
+  run<8, true>("tc_acc_occ4", sms, 4, out);
+  run<8, false>("tc_acc_nomufu", sms, 8, out);
   std::printf("-- extra variants at 8 CTAs/SM (row_ctr_rp2 = 128 pairs per point-warp; ffma2_* = 8 FFMA2 per point)\n");
   run<4, true>("row_ctr_rp2", sms, 8, out);
   run<4, false>("row_ctr_rp2_nm", sms, 8, out);
