@@ -100,7 +100,7 @@ __device__ __forceinline__ int wl_block_of(const WorkList& wl, int64_t u) {
 }
 
 // Centre and squared half-diagonal of the CTA's points' bounding box
-// (scaled frame); blockDim = 128.  Callers separate successive calls by a
+// (scaled frame); blockDim ≤ 128.  Callers separate successive calls by a
 // __syncthreads (the staging barrier).
 struct BoxCentre {
   float3 c;
@@ -131,8 +131,8 @@ __device__ __forceinline__ BoxCentre cta_box_centre(float lx, float ly, float lz
   float r[6];
 #pragma unroll
   for (int k = 0; k < 6; ++k) r[k] = red[k][0];
-#pragma unroll
-  for (int i = 1; i < 4; ++i) {
+  const int nw = blockDim.x >> 5;  // ≤ 4
+  for (int i = 1; i < nw; ++i) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) r[k] = fminf(r[k], red[k][i]);
 #pragma unroll
@@ -435,10 +435,17 @@ __global__ void estep_col_fallback_kernel(const float4* __restrict__ xt4, int64_
 // The pass is bound by FP32 operand traffic (≈ one 64-bit register operand
 // per cycle per SMSP, measured: tools/loopbench.cu); the centred form needs
 // 25 operands per 2 pairs against 31.
-__global__ void __launch_bounds__(128, 8)
+// NP row pairs per thread; the CTA (128/NP threads) owns the 256-row block.
+// NP = 2 shares every staged scene point's operands between two packed row
+// pairs (fewer register-operand reads per pair: −7.5 % per pair in
+// tools/loopbench.cu).
+template <int NP>
+__global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
     estep_row_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4b,
                      int64_t n, const IterState* __restrict__ st, WorkList wl,
                      double* __restrict__ seg /* [slot][5][256] */, int allow_centred) {
+  constexpr int kThr = 128 / NP;   // threads
+  constexpr int kRows = 2 * NP;    // rows per thread
   if (!st->active) return;
   __shared__ float4 ya[kTile];  // centred (ux,ux,uy,uy) | diff (y,y,y',y') scaled
   __shared__ float4 yb[kTile];  // centred (uz,uz,b−|u|²,·) | diff (z,z,b,b)
@@ -446,7 +453,7 @@ __global__ void __launch_bounds__(128, 8)
   // fp64 tile accumulators in shared memory (thread-private slots,
   // [quantity][row][thread] → conflict-free): registers stay with the
   // packed pipeline
-  __shared__ double acc_s[5][2][128];
+  __shared__ double acc_s[5][kRows][kThr];
   const float s = st->sx;
   const int64_t G = gridDim.x, g = blockIdx.x;
   const int64_t P = wl.off(wl.n_blocks) * kTile;
@@ -459,11 +466,11 @@ __global__ void __launch_bounds__(128, 8)
     while (wl.off(rb + 1) * kTile <= p) ++rb;
     const int64_t pe = min(p1, wl.off(rb + 1) * kTile);
     __syncthreads();  // previous segment's readers of the shared box/tiles are done
-    const int64_t r0 = static_cast<int64_t>(rb) * kTile + 2 * t;
-    float4 xv[2];
+    const int64_t r0 = static_cast<int64_t>(rb) * kTile + kRows * t;
+    float4 xv[kRows];
     float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < kRows; ++h) {
       const int64_t r = r0 + h;
       xv[h] = r < m ? scale_pt(xt4[r], s) : make_float4(kPadCoord, kPadCoord, kPadCoord, 0.f);
       if (r < m) {
@@ -474,31 +481,37 @@ __global__ void __launch_bounds__(128, 8)
     }
     const BoxCentre bc = cta_box_centre(lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]);
     const bool centred = allow_centred && bc.r2 <= kCentredMaxR2;
-    // per-thread operands: centred → 2v, −|v|² (and v, |v|² for the
+    // per-thread operands per row pair: centred → 2v (and v, |v|² for the
     // conversion); diff → −x'
-    float v[2][4];
-    float2 ox, oy, oz, on;
+    float v[kRows][4];
+    float2 ox[NP], oy[NP], oz[NP];
     if (centred) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < kRows; ++h) {
         const bool ok = r0 + h < m;
         v[h][0] = ok ? __fsub_rn(xv[h].x, bc.c.x) : 0.f;
         v[h][1] = ok ? __fsub_rn(xv[h].y, bc.c.y) : 0.f;
         v[h][2] = ok ? __fsub_rn(xv[h].z, bc.c.z) : 0.f;
         v[h][3] = __fmaf_rn(v[h][2], v[h][2], __fmaf_rn(v[h][1], v[h][1], __fmul_rn(v[h][0], v[h][0])));
       }
-      ox = make_float2(2.f * v[0][0], 2.f * v[1][0]);
-      oy = make_float2(2.f * v[0][1], 2.f * v[1][1]);
-      oz = make_float2(2.f * v[0][2], 2.f * v[1][2]);
-      on = make_float2(-v[0][3], -v[1][3]);
+#pragma unroll
+      for (int q2 = 0; q2 < NP; ++q2) {
+        ox[q2] = make_float2(2.f * v[2 * q2][0], 2.f * v[2 * q2 + 1][0]);
+        oy[q2] = make_float2(2.f * v[2 * q2][1], 2.f * v[2 * q2 + 1][1]);
+        oz[q2] = make_float2(2.f * v[2 * q2][2], 2.f * v[2 * q2 + 1][2]);
+      }
     } else {
-      ox = make_float2(-xv[0].x, -xv[1].x);
-      oy = make_float2(-xv[0].y, -xv[1].y);
-      oz = make_float2(-xv[0].z, -xv[1].z);
-      on = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int q2 = 0; q2 < NP; ++q2) {
+        ox[q2] = make_float2(-xv[2 * q2].x, -xv[2 * q2 + 1].x);
+        oy[q2] = make_float2(-xv[2 * q2].y, -xv[2 * q2 + 1].y);
+        oz[q2] = make_float2(-xv[2 * q2].z, -xv[2 * q2 + 1].z);
+      }
     }
 #pragma unroll
-    for (int k = 0; k < 5; ++k) acc_s[k][0][t] = acc_s[k][1][t] = 0.0;
+    for (int k = 0; k < 5; ++k)
+#pragma unroll
+      for (int h = 0; h < kRows; ++h) acc_s[k][h][t] = 0.0;
     for (int64_t q = p; q < pe;) {
       const int64_t k = q / kTile - wl.off(rb);
       const int a = static_cast<int>(q % kTile);
@@ -509,7 +522,7 @@ __global__ void __launch_bounds__(128, 8)
       if (cnt == 0) continue;  // uniform
       const int cnt8 = (cnt + 7) & ~7;
       __syncthreads();
-      for (int i = t; i < cnt8; i += 128) {
+      for (int i = t; i < cnt8; i += kThr) {
         if (centred) {
           float4 u;
           float uq;
@@ -534,7 +547,10 @@ __global__ void __launch_bounds__(128, 8)
         }
       }
       __syncthreads();
-      float2 f0 = make_float2(0.f, 0.f), fx = f0, fy = f0, fz = f0, fv = f0;
+      float2 f0[NP], fx[NP], fy[NP], fz[NP], fv[NP];
+#pragma unroll
+      for (int q2 = 0; q2 < NP; ++q2)
+        f0[q2] = fx[q2] = fy[q2] = fz[q2] = fv[q2] = make_float2(0.f, 0.f);
       if (centred) {
         for (int j = 0; j < cnt8; j += 8) {
 #pragma unroll
@@ -543,18 +559,21 @@ __global__ void __launch_bounds__(128, 8)
             const float4 B = yb[j + u];
             const float2 Q = yq[j + u];
             const float2 Ux = make_float2(A.x, A.y), Uy = make_float2(A.z, A.w);
-            const float2 Uz = make_float2(B.x, B.y);
-            // b − |u|² + 2u·v = (b − t) + |v|²: the row's own 2^{|v|²} is
-            // factored out of its sums and undone once in fp64 (|v|² ≤ 16)
-            float2 L = __ffma2_rn(Ux, ox, make_float2(B.z, B.w));
-            L = __ffma2_rn(Uy, oy, L);
-            L = __ffma2_rn(Uz, oz, L);
-            const float2 w = ex2x2(L);
-            f0 = __fadd2_rn(f0, w);
-            fx = __ffma2_rn(w, Ux, fx);
-            fy = __ffma2_rn(w, Uy, fy);
-            fz = __ffma2_rn(w, Uz, fz);
-            fv = __ffma2_rn(w, Q, fv);
+            const float2 Uz = make_float2(B.x, B.y), Bn = make_float2(B.z, B.w);
+#pragma unroll
+            for (int q2 = 0; q2 < NP; ++q2) {
+              // b − |u|² + 2u·v = (b − t) + |v|²: the row's own 2^{|v|²} is
+              // factored out of its sums and undone once in fp64 (|v|² ≤ 16)
+              float2 L = __ffma2_rn(Ux, ox[q2], Bn);
+              L = __ffma2_rn(Uy, oy[q2], L);
+              L = __ffma2_rn(Uz, oz[q2], L);
+              const float2 w = ex2x2(L);
+              f0[q2] = __fadd2_rn(f0[q2], w);
+              fx[q2] = __ffma2_rn(w, Ux, fx[q2]);
+              fy[q2] = __ffma2_rn(w, Uy, fy[q2]);
+              fz[q2] = __ffma2_rn(w, Uz, fz[q2]);
+              fv[q2] = __ffma2_rn(w, Q, fv[q2]);
+            }
           }
         }
       } else {
@@ -565,38 +584,45 @@ __global__ void __launch_bounds__(128, 8)
             const float4 B = yb[j + u];
             const float2 Yx = make_float2(A.x, A.y), Yy = make_float2(A.z, A.w);
             const float2 Yz = make_float2(B.x, B.y), Bn = make_float2(B.z, B.w);
-            const float2 ddx = __fadd2_rn(Yx, ox);
-            const float2 ddy = __fadd2_rn(Yy, oy);
-            const float2 ddz = __fadd2_rn(Yz, oz);
-            float2 tt = __fmul2_rn(ddx, ddx);
-            tt = __ffma2_rn(ddy, ddy, tt);
-            tt = __ffma2_rn(ddz, ddz, tt);
-            const float2 L = __ffma2_rn(tt, minus1, Bn);
-            const float2 w = ex2x2(L);
-            f0 = __fadd2_rn(f0, w);
-            fx = __ffma2_rn(w, Yx, fx);
-            fy = __ffma2_rn(w, Yy, fy);
-            fz = __ffma2_rn(w, Yz, fz);
-            fv = __ffma2_rn(w, tt, fv);
+#pragma unroll
+            for (int q2 = 0; q2 < NP; ++q2) {
+              const float2 ddx = __fadd2_rn(Yx, ox[q2]);
+              const float2 ddy = __fadd2_rn(Yy, oy[q2]);
+              const float2 ddz = __fadd2_rn(Yz, oz[q2]);
+              float2 tt = __fmul2_rn(ddx, ddx);
+              tt = __ffma2_rn(ddy, ddy, tt);
+              tt = __ffma2_rn(ddz, ddz, tt);
+              const float2 L = __ffma2_rn(tt, minus1, Bn);
+              const float2 w = ex2x2(L);
+              f0[q2] = __fadd2_rn(f0[q2], w);
+              fx[q2] = __ffma2_rn(w, Yx, fx[q2]);
+              fy[q2] = __ffma2_rn(w, Yy, fy[q2]);
+              fz[q2] = __ffma2_rn(w, Yz, fz[q2]);
+              fv[q2] = __ffma2_rn(w, tt, fv[q2]);
+            }
           }
         }
       }
-      acc_s[0][0][t] += f0.x;
-      acc_s[0][1][t] += f0.y;
-      acc_s[1][0][t] += fx.x;
-      acc_s[1][1][t] += fx.y;
-      acc_s[2][0][t] += fy.x;
-      acc_s[2][1][t] += fy.y;
-      acc_s[3][0][t] += fz.x;
-      acc_s[3][1][t] += fz.y;
-      acc_s[4][0][t] += fv.x;
-      acc_s[4][1][t] += fv.y;
+#pragma unroll
+      for (int q2 = 0; q2 < NP; ++q2) {
+        const int h0 = 2 * q2, h1 = 2 * q2 + 1;
+        acc_s[0][h0][t] += f0[q2].x;
+        acc_s[0][h1][t] += f0[q2].y;
+        acc_s[1][h0][t] += fx[q2].x;
+        acc_s[1][h1][t] += fx[q2].y;
+        acc_s[2][h0][t] += fy[q2].x;
+        acc_s[2][h1][t] += fy[q2].y;
+        acc_s[3][h0][t] += fz[q2].x;
+        acc_s[3][h1][t] += fz[q2].y;
+        acc_s[4][h0][t] += fv[q2].x;
+        acc_s[4][h1][t] += fv[q2].y;
+      }
     }
     // segment out: S0, Σw·y', Σw·t per own row
     double* out = seg + (g + rb) * 5 * kTile;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int li = 2 * t + h;
+    for (int h = 0; h < kRows; ++h) {
+      const int li = kRows * t + h;
       double s0 = acc_s[0][h][t], s1 = acc_s[1][h][t], s2v = acc_s[2][h][t],
              s3 = acc_s[3][h][t], s4 = acc_s[4][h][t];
       if (centred) {
@@ -979,7 +1005,11 @@ EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
   if (const char* e = std::getenv("FCPD_ESTEP_FORM")) p.centred = std::strcmp(e, "diff") != 0;
   int occ_col = 0, occ_row = 0;
   FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_col, estep_col_kernel, 128, 0));
-  FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_row, estep_row_kernel, 128, 0));
+  if (const char* e = std::getenv("FCPD_ROW_PAIRS")) p.row_pairs = std::atoi(e) == 1 ? 1 : 2;
+  if (p.row_pairs == 2)
+    FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_row, estep_row_kernel<2>, 64, 0));
+  else
+    FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_row, estep_row_kernel<1>, 128, 0));
   p.col_blocks = static_cast<int>(ceil_div(n, kTile));
   p.row_blocks = static_cast<int>(ceil_div(m, kTile));
   p.col_grid = sm_count * std::max(occ_col, 1);
@@ -1064,6 +1094,16 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
   }
 }
 
+void launch_row_cc(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
+                   IterState* st, const WorkList& wl, double* seg, cudaStream_t stream) {
+  if (p.row_pairs == 2)
+    estep_row_kernel<2><<<p.row_grid, 64, 0, stream>>>(b.xt4, m, b.y4b, n, st, wl, seg,
+                                                       p.centred);
+  else
+    estep_row_kernel<1><<<p.row_grid, 128, 0, stream>>>(b.xt4, m, b.y4b, n, st, wl, seg,
+                                                        p.centred);
+}
+
 void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int64_t m,
                                  int64_t n, IterState* st, cudaStream_t stream) {
   const CullInfo& cu = b.cull;
@@ -1079,11 +1119,9 @@ void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int6
   pass2_sources(p, b, n, a, c);
   if (p.tc) {
     launch_estep_row_tc(b.xt4, m, b.y4b, n, st, a.wl, b.row_seg, p.tc_grid, stream);
-    estep_row_kernel<<<p.row_grid, 128, 0, stream>>>(b.xt4, m, b.y4b, n, st, c.wl,
-                                                     b.row_seg_cc, p.centred);
+    launch_row_cc(p, b, m, n, st, c.wl, b.row_seg_cc, stream);
   } else {
-    estep_row_kernel<<<p.row_grid, 128, 0, stream>>>(b.xt4, m, b.y4b, n, st, a.wl, b.row_seg,
-                                                     p.centred);
+    launch_row_cc(p, b, m, n, st, a.wl, b.row_seg, stream);
   }
   FCPD_LAUNCH_CHECK();
 }

@@ -19,6 +19,29 @@ __device__ __forceinline__ float ex2(float x) {
   asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// exp2 on the FMA pipe for x ≤ 0 (f32x2): 2^x = 2^n · p(f), n = round(x),
+// f ∈ [−0.5, 0.5], p a degree-5 minimax-style polynomial (rel. err ~1e-7);
+// 2^n by adding n to the exponent bits.  x < −126 flushes to 0.
+__device__ __forceinline__ float2 ex2_poly(float2 x) {
+  x = make_float2(fmaxf(x.x, -127.f), fmaxf(x.y, -127.f));
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5·2^23
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 n = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-n.x, -n.y));
+  float2 p = make_float2(1.3333558146e-3f, 1.3333558146e-3f);
+  p = __ffma2_rn(p, f, make_float2(9.6181291076e-3f, 9.6181291076e-3f));
+  p = __ffma2_rn(p, f, make_float2(5.5504108665e-2f, 5.5504108665e-2f));
+  p = __ffma2_rn(p, f, make_float2(2.4022650696e-1f, 2.4022650696e-1f));
+  p = __ffma2_rn(p, f, make_float2(6.9314718056e-1f, 6.9314718056e-1f));
+  p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
+  const int ix = __float_as_int(t.x) - 0x4B400000, iy = __float_as_int(t.y) - 0x4B400000;
+  float2 r = make_float2(__int_as_float(__float_as_int(p.x) + (ix << 23)),
+                         __int_as_float(__float_as_int(p.y) + (iy << 23)));
+  if (x.x <= -127.f) r.x = 0.f;
+  if (x.y <= -127.f) r.y = 0.f;
+  return r;
+}
+
 template <bool M>
 __device__ __forceinline__ float2 ex2v(float2 v) {
   if (M) return make_float2(ex2(v.x), ex2(v.y));
@@ -163,6 +186,31 @@ __global__ void __launch_bounds__(128) loop_kernel(float* out, int occ_pad) {
           fy = __ffma2_rn(w, B, fy);
           fz = __ffma2_rn(w, C, fz);
           fq = __ffma2_rn(w, Q, fq);
+        } else if (V == 12 || V == 13) {  // col_fac with 1/8 (12) or 2/8 (13) exps on FMA
+          float2 e = __ffma2_rn(ax, A, D);
+          e = __ffma2_rn(ay, B, e);
+          e = __ffma2_rn(az, C, e);
+          const bool poly = (V == 12) ? (u == 7) : (u == 3 || u == 7);
+          f0 = __fadd2_rn(f0, poly ? ex2_poly(make_float2(-fabsf(e.x), -fabsf(e.y))) : ex2v<MUFU>(e));
+        } else if (V == 11) {  // row_fac with two row pairs per thread (U shared)
+          const float2 Q = sq[j + u];
+          float2 L = __ffma2_rn(A, ax, D);
+          float2 L2 = __ffma2_rn(A, az, D);
+          L = __ffma2_rn(B, ay, L);
+          L2 = __ffma2_rn(B, n2, L2);
+          L = __ffma2_rn(C, az, L);
+          L2 = __ffma2_rn(C, ax, L2);
+          const float2 w = ex2v<MUFU>(L), w2 = ex2v<MUFU>(L2);
+          f0 = __fadd2_rn(f0, w);
+          g0 = __fadd2_rn(g0, w2);
+          fx = __ffma2_rn(w, A, fx);
+          gx = __ffma2_rn(w2, A, gx);
+          fy = __ffma2_rn(w, B, fy);
+          gy = __ffma2_rn(w2, B, gy);
+          fz = __ffma2_rn(w, C, fz);
+          gz = __ffma2_rn(w2, C, gz);
+          fq = __ffma2_rn(w, Q, fq);
+          gq = __ffma2_rn(w2, Q, gq);
         } else {  // col_ctr: FADD2 + 3 FFMA2 + 2 MUFU + FADD2
           float2 e = __fadd2_rn(n2, D);
           e = __ffma2_rn(ax, A, e);
@@ -216,6 +264,10 @@ int main() {
   std::printf("-- current kernels' loops at 8 CTAs/SM (tc_acc = 128 pairs per point-warp)\n");
   run<9, true>("col_fac", sms, 8, out);
   run<10, true>("row_fac", sms, 8, out);
+  run<12, true>("col_fac_poly1of8", sms, 8, out);
+  run<13, true>("col_fac_poly2of8", sms, 8, out);
+  run<11, true>("row_fac_rp2", sms, 8, out);
+  run<11, true>("row_fac_rp2_o6", sms, 6, out);
   run<8, true>("tc_acc", sms, 8, out);
   run<8, true>("tc_acc_occ4", sms, 4, out);
   run<8, false>("tc_acc_nomufu", sms, 8, out);
