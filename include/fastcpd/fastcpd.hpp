@@ -22,9 +22,12 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <cstdio>
 #include <fstream>
 #include <limits>
+#include <map>
 #include <memory>
+#include <random>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -402,6 +405,234 @@ inline void write_report(const std::string& path, const RegistrationConfig& cfg,
   for (size_t i = 0; i < res.sigma2_trace.size(); ++i)
     out << "sigma2[" << i << "]=" << res.sigma2_trace[i] << '\n';
   if (!out) throw IoError("report write failed: " + path);
+}
+
+// ------------------------------------------- benchmark harness (metrics.hpp)
+// Ground truth: model row index → expected position (degradations.hpp:22).
+using Truth = std::map<Index, std::vector<double>>;
+
+struct DegradedPair {
+  PointSet model;
+  PointSet scene;
+  Truth truth;
+};
+
+// RMS distance of the transformed model rows that have a ground truth
+// (metrics.hpp:19-31).
+inline double rmse(const PointSet& transformed, const Truth& truth) {
+  if (truth.empty()) throw ParameterError("rmse: empty ground truth");
+  double sum = 0.0;
+  for (const auto& kv : truth) {
+    const Index i = kv.first;
+    if (i < 0 || i >= transformed.count()) throw ParameterError("rmse: truth index out of range");
+    if (static_cast<Index>(kv.second.size()) != transformed.dim())
+      throw DimensionError("rmse: truth dimension mismatch");
+    for (Index j = 0; j < transformed.dim(); ++j) {
+      const double e = transformed.pts(i, j) - kv.second[static_cast<size_t>(j)];
+      sum += e * e;
+    }
+  }
+  return std::sqrt(sum / static_cast<double>(truth.size()));
+}
+
+struct BenchRecord {
+  Index m = 0, n = 0;
+  SolverVariant variant = SolverVariant::fast;
+  TimingBreakdown timing;
+  double rmse = 0.0;
+  int iterations = 0;
+  bool failed = false;
+};
+
+// `size` rows drawn without replacement, kept in source order, deterministic
+// per seed (metrics.hpp:43-58).
+inline PointSet subsample(const PointSet& ps, Index size, unsigned long seed) {
+  if (size < 1 || size > ps.count()) throw ParameterError("subsample: size out of range");
+  std::vector<Index> idx(static_cast<size_t>(ps.count()));
+  for (size_t i = 0; i < idx.size(); ++i) idx[i] = static_cast<Index>(i);
+  std::mt19937_64 rng(seed);
+  std::shuffle(idx.begin(), idx.end(), rng);
+  idx.resize(static_cast<size_t>(size));
+  std::sort(idx.begin(), idx.end());
+  PointSet out;
+  out.pts.resize(size, ps.dim());
+  for (Index i = 0; i < size; ++i)
+    for (Index j = 0; j < ps.dim(); ++j) out.pts(i, j) = ps.pts(idx[static_cast<size_t>(i)], j);
+  return out;
+}
+
+// A mild random affine map (metrics.hpp:60-94): rotation ≤ 10° (about a
+// random axis in 3-D), per-axis scale in [0.9, 1.1], shift in [−0.1, 0.1].
+inline PointSet random_affine(const PointSet& ps, unsigned long seed) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unit(-1.0, 1.0);
+  const Index d = ps.dim();
+  const double max_angle = 10.0 * 3.14159265358979323846 / 180.0;
+  double rot[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+  if (d == 2) {
+    const double a = unit(rng) * max_angle;
+    rot[0][0] = std::cos(a), rot[0][1] = -std::sin(a);
+    rot[1][0] = std::sin(a), rot[1][1] = std::cos(a);
+  } else if (d == 3) {
+    double ax[3] = {unit(rng), unit(rng), unit(rng)};
+    double nrm = std::sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+    if (nrm < 1e-12) ax[0] = ax[1] = 0.0, ax[2] = 1.0, nrm = 1.0;
+    for (double& c : ax) c /= nrm;
+    const double a = unit(rng) * max_angle, sa = std::sin(a), ca = 1.0 - std::cos(a);
+    const double k[3][3] = {{0, -ax[2], ax[1]}, {ax[2], 0, -ax[0]}, {-ax[1], ax[0], 0}};
+    for (int i = 0; i < 3; ++i)  // Rodrigues: I + sin(a)·K + (1 − cos(a))·K²
+      for (int j = 0; j < 3; ++j) {
+        double k2 = 0.0;
+        for (int l = 0; l < 3; ++l) k2 += k[i][l] * k[l][j];
+        rot[i][j] = (i == j ? 1.0 : 0.0) + sa * k[i][j] + ca * k2;
+      }
+  }
+  std::vector<double> scale(static_cast<size_t>(d)), shift(static_cast<size_t>(d));
+  for (Index j = 0; j < d; ++j) {
+    scale[static_cast<size_t>(j)] = 1.0 + 0.1 * unit(rng);
+    shift[static_cast<size_t>(j)] = 0.1 * unit(rng);
+  }
+  PointSet out;
+  out.pts.resize(ps.count(), d);
+  for (Index i = 0; i < ps.count(); ++i)
+    for (Index j = 0; j < d; ++j) {
+      double v = 0.0;  // (p · Rᵀ)_j
+      for (Index l = 0; l < d && l < 3; ++l) v += ps.pts(i, l) * rot[j][l];
+      if (d > 3) v = ps.pts(i, j);
+      out.pts(i, j) = v * scale[static_cast<size_t>(j)] + shift[static_cast<size_t>(j)];
+    }
+  return out;
+}
+
+// Scene = the subsample rescaled to [−1, 1] (joint normalisation with
+// itself), model = its random-affine copy, truth row-to-row (metrics.hpp:96-106).
+inline DegradedPair make_bench_pair(const PointSet& source, Index size, unsigned long seed) {
+  const PointSet base = subsample(source, size, seed);
+  const Index m = base.count(), d = base.dim();
+  std::vector<double> ctr(static_cast<size_t>(d), 0.0);
+  for (Index j = 0; j < d; ++j) {
+    for (Index i = 0; i < m; ++i) ctr[static_cast<size_t>(j)] += 2.0 * base.pts(i, j);
+    ctr[static_cast<size_t>(j)] /= static_cast<double>(2 * m);
+  }
+  double sc = 0.0;
+  for (Index i = 0; i < m; ++i)
+    for (Index j = 0; j < d; ++j)
+      sc = std::max(sc, std::fabs(base.pts(i, j) - ctr[static_cast<size_t>(j)]));
+  if (sc <= 0.0) sc = 1.0;
+  DegradedPair pair;
+  pair.scene.pts.resize(m, d);
+  for (Index i = 0; i < m; ++i)
+    for (Index j = 0; j < d; ++j)
+      pair.scene.pts(i, j) = (base.pts(i, j) - ctr[static_cast<size_t>(j)]) / sc;
+  pair.model = random_affine(pair.scene, seed + 1);
+  for (Index i = 0; i < m; ++i) {
+    std::vector<double> row(static_cast<size_t>(d));
+    for (Index j = 0; j < d; ++j) row[static_cast<size_t>(j)] = pair.scene.pts(i, j);
+    pair.truth[i] = std::move(row);
+  }
+  return pair;
+}
+
+// One registration per (size, variant) cell, sequential, one discarded
+// 1-iteration warm-up per size; a failing cell is recorded (rmse −1 in the
+// CSV), not fatal (metrics.hpp:108-141).  On the device the cpd / cpd_lowrank
+// variants are such failing cells.
+inline std::vector<BenchRecord> run_benchmark(const PointSet& source,
+                                              const std::vector<Index>& sizes,
+                                              const std::vector<SolverVariant>& variants,
+                                              const RegistrationConfig& cfg, unsigned long seed) {
+  std::vector<BenchRecord> records;
+  for (Index size : sizes) {
+    const DegradedPair pair = make_bench_pair(source, size, seed + static_cast<unsigned long>(size));
+    {
+      RegistrationConfig warm = cfg;
+      warm.iterations = 1;
+      warm.variant = SolverVariant::fast;
+      register_pointsets(pair.model, pair.scene, warm);
+    }
+    for (SolverVariant v : variants) {
+      BenchRecord rec;
+      rec.m = pair.model.count();
+      rec.n = pair.scene.count();
+      rec.variant = v;
+      rec.iterations = cfg.iterations;
+      try {
+        RegistrationConfig run = cfg;
+        run.variant = v;
+        const RegistrationResult res = register_pointsets(pair.model, pair.scene, run);
+        rec.timing = res.timing;
+        rec.rmse = rmse(res.transformed, pair.truth);
+      } catch (const Error&) {
+        rec.failed = true;
+      }
+      records.push_back(rec);
+    }
+  }
+  return records;
+}
+
+inline constexpr const char* kBenchCsvHeader =
+    "M,N,variant,t_c,t_eig,t_iter,t_f,t_o,t_total,rmse,iterations";
+
+// Durations with 6 decimals; t_f and t_total re-derived from the rounded
+// parts so the timing identities hold exactly in the file (metrics.hpp:147-169).
+inline void write_bench_csv(const std::vector<BenchRecord>& records, const std::string& path) {
+  std::ofstream out(path);
+  if (!out) throw IoError("cannot write CSV: " + path);
+  out << kBenchCsvHeader << '\n';
+  const auto q = [](double v) { return std::round(v * 1e6) / 1e6; };
+  char buf[512];
+  for (const BenchRecord& r : records) {
+    const double tc = q(r.timing.t_c), te = q(r.timing.t_eig), ti = q(r.timing.t_iter),
+                 to = q(r.timing.t_o);
+    std::snprintf(buf, sizeof buf, "%lld,%lld,%s,%.6f,%.6f,%.6f,%.6f,%.6f,%.6f,%.9g,%d\n",
+                  static_cast<long long>(r.m), static_cast<long long>(r.n), to_string(r.variant),
+                  tc, te, ti, te + ti, to, tc + te + ti + to, r.failed ? -1.0 : r.rmse,
+                  r.iterations);
+    out << buf;
+  }
+  if (!out) throw IoError("CSV write failed: " + path);
+}
+
+inline std::vector<BenchRecord> load_bench_csv(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw IoError("cannot open CSV: " + path);
+  std::string line;
+  if (!std::getline(in, line) || line != kBenchCsvHeader)
+    throw ParseError(path + ": missing or unexpected CSV header");
+  std::vector<BenchRecord> records;
+  long lineno = 1;
+  while (std::getline(in, line)) {
+    ++lineno;
+    if (line.empty()) continue;
+    std::vector<std::string> cells;
+    std::stringstream ss(line);
+    std::string cell;
+    while (std::getline(ss, cell, ',')) cells.push_back(cell);
+    if (!line.empty() && line.back() == ',') cells.push_back("");
+    if (cells.size() != 11) throw ParseError(path + ":" + std::to_string(lineno) + ": bad CSV row");
+    BenchRecord r;
+    try {
+      r.m = std::stoll(cells[0]);
+      r.n = std::stoll(cells[1]);
+      r.variant = variant_from_string(cells[2]);
+      r.timing.t_c = std::stod(cells[3]);
+      r.timing.t_eig = std::stod(cells[4]);
+      r.timing.t_iter = std::stod(cells[5]);
+      r.timing.t_f = std::stod(cells[6]);
+      r.timing.t_o = std::stod(cells[7]);
+      r.timing.t_total = std::stod(cells[8]);
+      r.rmse = std::stod(cells[9]);
+      r.iterations = std::stoi(cells[10]);
+    } catch (const ParameterError&) {
+      throw ParseError(path + ":" + std::to_string(lineno) + ": bad CSV value");
+    } catch (const std::exception&) {
+      throw ParseError(path + ":" + std::to_string(lineno) + ": bad CSV value");
+    }
+    r.failed = r.rmse < 0.0;
+    records.push_back(r);
+  }
+  return records;
 }
 
 }  // namespace fastcpd

@@ -6,16 +6,20 @@
 // and the key=value run report.  Same flags and defaults (ω=0.7, β=2,
 // λ=10, 100 iterations, variant fast, rank fraction 0.1, seed 0).
 // --svg writes a plain scatter overlay of the first two coordinates
-// (registered model over scene).  Not provided: degrade / bench / plot.
+// (registered model over scene).  `bench` sweeps sizes × variants in the
+// reference's CSV schema.  Not provided: degrade / plot.
 //
 //   fcpd register MODEL SCENE [--omega W] [--beta B] [--lambda L] [--iters N]
 //        [--variant fast|fast-lowrank] [--rank-fraction F] [--seed S]
 //        [--no-normalize] [--swap] [--early-stop] [--out FILE] [--report FILE]
 //        [--svg FILE] [--device D]
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
+#include <random>
+#include <sstream>
 #include <string>
 #include <utility>
 #include <vector>
@@ -31,8 +35,10 @@ int usage(const char* prog, int code) {
                "usage: %s register MODEL SCENE [--omega W] [--beta B] [--lambda L] [--iters N]\n"
                "          [--variant fast|fast-lowrank] [--rank-fraction F] [--seed S]\n"
                "          [--no-normalize] [--swap] [--early-stop] [--out FILE]\n"
-               "          [--report FILE] [--svg FILE] [--device D]\n",
-               prog);
+               "          [--report FILE] [--svg FILE] [--device D]\n"
+               "       %s bench [SOURCE | --synthetic] --sizes M1,M2,... [--variants fast,...]\n"
+               "          [--iters N] [--seed S] [--csv FILE] [--device D]\n",
+               prog, prog);
   return code;
 }
 
@@ -130,6 +136,70 @@ int cmd_register(const std::vector<std::string>& args) {
   return 0;
 }
 
+// `fcpd bench` (proj/tools/fcpd.cpp:132-182): one registration per
+// (size, variant) cell through run_benchmark, written in the reference's CSV
+// schema.  --synthetic draws the reference's torus-like cloud.
+int cmd_bench(const std::vector<std::string>& args) {
+  std::vector<std::string> pos;
+  fc::RegistrationConfig cfg;
+  std::string sizes_arg, variants_arg = "fast,fast-lowrank", csv_path = "bench.csv";
+  bool synthetic = false;
+  for (size_t i = 0; i < args.size(); ++i) {
+    const std::string& a = args[i];
+    auto value = [&]() -> const std::string& {
+      if (i + 1 >= args.size()) throw fc::ParameterError(a + ": missing value");
+      return args[++i];
+    };
+    if (a == "--sizes") sizes_arg = value();
+    else if (a == "--variants") variants_arg = value();
+    else if (a == "--iters") cfg.iterations = static_cast<int>(to_long(a, value()));
+    else if (a == "--seed") cfg.seed = static_cast<unsigned long>(to_long(a, value()));
+    else if (a == "--omega") cfg.omega = to_double(a, value());
+    else if (a == "--beta") cfg.beta = to_double(a, value());
+    else if (a == "--lambda") cfg.lambda_reg = to_double(a, value());
+    else if (a == "--rank-fraction") cfg.rank_fraction = to_double(a, value());
+    else if (a == "--csv") csv_path = value();
+    else if (a == "--synthetic") synthetic = true;
+    else if (a == "--device") cfg.device = static_cast<int>(to_long(a, value()));
+    else if (!a.empty() && a[0] == '-') throw fc::ParameterError("unknown option: " + a);
+    else pos.push_back(a);
+  }
+  std::vector<fc::Index> sizes;
+  std::vector<fc::SolverVariant> variants;
+  {
+    std::stringstream ss(sizes_arg);
+    std::string tok;
+    while (std::getline(ss, tok, ',')) sizes.push_back(static_cast<fc::Index>(to_long("--sizes", tok)));
+    std::stringstream vs(variants_arg);
+    while (std::getline(vs, tok, ',')) variants.push_back(fc::variant_from_string(tok));
+  }
+  if (sizes.empty() || variants.empty())
+    throw fc::ParameterError("bench: --sizes and --variants must be non-empty");
+  fc::PointSet source;
+  if (synthetic) {  // torus-like 3-D cloud with enough points for the largest cell
+    const fc::Index m = *std::max_element(sizes.begin(), sizes.end());
+    source.pts.resize(m, 3);
+    std::mt19937_64 rng(cfg.seed);
+    std::uniform_real_distribution<double> u(0.0, 2.0 * 3.14159265358979323846);
+    for (fc::Index i = 0; i < m; ++i) {
+      const double a = u(rng), b = u(rng);
+      source.pts(i, 0) = (1.0 + 0.35 * std::cos(b)) * std::cos(a);
+      source.pts(i, 1) = (1.0 + 0.35 * std::cos(b)) * std::sin(a);
+      source.pts(i, 2) = 0.35 * std::sin(b);
+    }
+  } else {
+    if (pos.size() != 1) throw fc::ParameterError("bench: expected SOURCE or --synthetic");
+    source = fc::load_points(pos[0]);
+  }
+  const auto records = fc::run_benchmark(source, sizes, variants, cfg, cfg.seed);
+  fc::write_bench_csv(records, csv_path);
+  for (const auto& r : records)
+    std::printf("M=%lld %s t_iter=%.6f t_total=%.6f rmse=%.6g%s\n", static_cast<long long>(r.m),
+                fc::to_string(r.variant), r.timing.t_iter, r.timing.t_total, r.rmse,
+                r.failed ? " FAILED" : "");
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -140,13 +210,14 @@ int main(int argc, char** argv) {
     std::printf("%s\n", fcpd_version());
     return 0;
   }
-  if (cmd != "register") {
+  if (cmd != "register" && cmd != "bench") {
     std::fprintf(stderr, "%s: unknown or unsupported subcommand '%s' (this build provides "
-                         "'register')\n", argv[0], cmd.c_str());
+                         "'register' and 'bench')\n", argv[0], cmd.c_str());
     return 2;
   }
   try {
-    return cmd_register(std::vector<std::string>(argv + 2, argv + argc));
+    const std::vector<std::string> rest(argv + 2, argv + argc);
+    return cmd == "bench" ? cmd_bench(rest) : cmd_register(rest);
   } catch (const fc::Error& e) {
     std::fprintf(stderr, "error: %s\n", e.what());
     return 1;

@@ -18,11 +18,10 @@ def build():
     return CLI
 
 
-def test_pointio_and_report_match_reference_tests(tmp_path):
-    """tests/test_pointset.cpp restated against the drop-in header (host only)."""
+def _run_host_cpp(tmp_path, name):
     build()
-    src = os.path.join(ROOT, "tests", "cpp", "test_pointio.cpp")
-    exe = str(tmp_path / "test_pointio")
+    src = os.path.join(ROOT, "tests", "cpp", name + ".cpp")
+    exe = str(tmp_path / name)
     subprocess.run(["/usr/bin/g++", "-std=c++17", "-O2", "-Wall", "-Werror", "-I",
                     os.path.join(ROOT, "include"), src, "-L", LIBDIR, "-lfcpd_b200",
                     f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
@@ -32,12 +31,28 @@ def test_pointio_and_report_match_reference_tests(tmp_path):
     assert "FAIL:" not in r.stdout
 
 
+def test_pointio_and_report_match_reference_tests(tmp_path):
+    """tests/test_pointset.cpp restated against the drop-in header (host only)."""
+    _run_host_cpp(tmp_path, "test_pointio")
+
+
+def test_bench_harness_helpers(tmp_path):
+    """tests/test_metrics.cpp host cases: rmse, subsample, random_affine,
+    make_bench_pair and the byte-stable bench CSV (host only)."""
+    _run_host_cpp(tmp_path, "test_metrics")
+
+
 def test_cli_usage_and_errors(tmp_path):
     exe = build()
     r = subprocess.run([exe, "--help"], capture_output=True, text=True)
     assert r.returncode == 0 and "register MODEL SCENE" in r.stdout
     r = subprocess.run([exe, "degrade", "x"], capture_output=True, text=True)
     assert r.returncode == 2
+    r = subprocess.run([exe, "bench", "--sizes", "40"], capture_output=True, text=True)
+    assert r.returncode != 0 and "--synthetic" in r.stderr
+    r = subprocess.run([exe, "bench", "--synthetic", "--sizes", "40", "--frobnicate"],
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "unknown option" in r.stderr
     # a missing scene file is reported by name before any device work
     model = tmp_path / "model_only.txt"
     np.savetxt(model, np.random.default_rng(201).uniform(-1, 1, (10, 2)))
@@ -73,3 +88,31 @@ def test_cli_register_on_gpu(tmp_path, orc):
     got = np.loadtxt(out)
     ref = fc.register_pointsets(cloud, cloud, fc.RegistrationConfig(iterations=20))
     assert np.abs(got - ref.transformed).max() <= 1e-12
+
+
+@pytest.mark.gpu
+def test_cli_bench_on_gpu(tmp_path):
+    """tests/test_cli.cpp:108-116 and test_metrics.cpp:66-82: a synthetic
+    sweep over two sizes × two variants writes four CSV records in the
+    reference schema; every cell converges (rmse ≥ 0, small), the timing
+    identities hold in the file and the dense `cpd` variant, which the device
+    path does not provide, is recorded as a failed cell rather than aborting."""
+    exe = build()
+    csv = tmp_path / "bench.csv"
+    r = subprocess.run([exe, "bench", "--synthetic", "--sizes", "40,60", "--variants",
+                        "fast,fast-lowrank,cpd", "--iters", "30", "--csv", str(csv)],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    lines = csv.read_text().splitlines()
+    assert lines[0] == "M,N,variant,t_c,t_eig,t_iter,t_f,t_o,t_total,rmse,iterations"
+    rows = [ln.split(",") for ln in lines[1:]]
+    assert len(rows) == 6
+    assert [int(x[0]) for x in rows] == [40, 40, 40, 60, 60, 60]
+    for x in rows:
+        tc, te, ti, tf, to, tt, err = (float(v) for v in x[3:10])
+        assert abs(tf - (te + ti)) <= 1e-9 and abs(tt - (tc + tf + to)) <= 1e-9
+        assert int(x[10]) == 30
+        if x[2] == "cpd":
+            assert err == -1.0
+        else:
+            assert 0.0 <= err < 0.2, x

@@ -192,6 +192,15 @@ __global__ void __launch_bounds__(128) loop_kernel(float* out, int occ_pad) {
           e = __ffma2_rn(az, C, e);
           const bool poly = (V == 12) ? (u == 7) : (u == 3 || u == 7);
           f0 = __fadd2_rn(f0, poly ? ex2_poly(make_float2(-fabsf(e.x), -fabsf(e.y))) : ex2v<MUFU>(e));
+        } else if (V == 14) {  // col_fac with two column pairs per thread (staged v shared)
+          float2 e = __ffma2_rn(ax, A, D);
+          float2 e2 = __ffma2_rn(az, A, D);
+          e = __ffma2_rn(ay, B, e);
+          e2 = __ffma2_rn(ax, B, e2);
+          e = __ffma2_rn(az, C, e);
+          e2 = __ffma2_rn(ay, C, e2);
+          f0 = __fadd2_rn(f0, ex2v<MUFU>(e));
+          g0 = __fadd2_rn(g0, ex2v<MUFU>(e2));
         } else if (V == 11) {  // row_fac with two row pairs per thread (U shared)
           const float2 Q = sq[j + u];
           float2 L = __ffma2_rn(A, ax, D);
@@ -264,6 +273,9 @@ int main() {
   std::printf("-- current kernels' loops at 8 CTAs/SM (tc_acc = 128 pairs per point-warp)\n");
   run<9, true>("col_fac", sms, 8, out);
   run<10, true>("row_fac", sms, 8, out);
+  run<14, true>("col_fac_cp2", sms, 8, out);
+  run<14, true>("col_fac_cp2_o12", sms, 12, out);
+  run<14, false>("col_fac_cp2_nm", sms, 8, out);
   run<12, true>("col_fac_poly1of8", sms, 8, out);
   run<13, true>("col_fac_poly2of8", sms, 8, out);
   run<11, true>("row_fac_rp2", sms, 8, out);
