@@ -6,8 +6,10 @@ N=24,000 (20 % uniform outliers), D=3, ω=0.2, β=2, λ=3 — generated with the
 seeded synthetic stand-in generator (paper_2006_06281_b200/datagen.py).
 A "step" is one EM iteration (E-step + M-step + transform + σ²) replayed
 from the engine's CUDA graph; inputs are resident in HBM before timing.  The
-basis Q and Qᵀ (2 × 1.6 GB fp32) exceed the 126 MB L2, so every timed
-iteration streams from HBM without an explicit flush.
+K timed steps are the first K iterations of the configured run (default K =
+the config's iteration count, 100), each preceded by a 256 MB L2-flushing
+write outside its event pair; W warm-up iterations run in a separate session
+first.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -151,6 +153,8 @@ def run_reference(args, world, rank):
         return
     from paper_2006_06281_b200 import datagen
     x, y, w = datagen.generate(args.workload)
+    if args.steps is None:
+        args.steps = w.iterations
     # one untimed warm-up iteration (also sizes the sample), then a bounded
     # sample: at most args.steps iterations, capped by a time budget
     t_est = cpu_sample(x, y, w, 1)[2]
@@ -191,9 +195,16 @@ def run_ours(args, world, rank, local):
     # --shard1: the NCCL-sharded engine path as a one-rank group (exercises
     # the multi-GPU code path on one GPU; no rank waits on another)
     sharded = (world > 1 and not args.replicas) or args.shard1
-    prof_iters = 0 if sharded else 3
-    total = args.warmup + args.steps + prof_iters
-    cfg = datagen.config_for(w, iterations=total)
+    # A step is one EM iteration.  The K timed steps are the FIRST K
+    # iterations of the configured run (K defaults to the config's iteration
+    # count, so `value` = iterations / Σ per-iteration device time over the
+    # whole run); the W warm-up iterations run in a throwaway
+    # session before it.  The per-phase profile replays the same K-iteration
+    # trajectory, so the roofline describes exactly the timed iterations.
+    if args.steps is None:
+        args.steps = w.iterations
+    prof_iters = 0 if sharded else args.steps
+    cfg = datagen.config_for(w, iterations=args.steps)
     if sharded:
         # scene points sharded over ranks; the engine's own NCCL
         # communicator carries the per-iteration reductions
@@ -208,12 +219,13 @@ def run_ours(args, world, rank, local):
         y = y_full
     watchdog = Watchdog(args.watchdog_s)
     t0 = time.perf_counter()
-    ctx.session_begin(x, y, cfg)
+    ctx.session_begin(x, y, datagen.config_for(w, iterations=args.warmup))
     setup_s = time.perf_counter() - t0
 
     stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=torch.device("cuda", local))
     ctx.session_run(args.warmup)
     ctx.session_sync()
+    ctx.session_begin(x, y, cfg)  # the timed run (basis cached by the warm-up session)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -238,24 +250,26 @@ def run_ours(args, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
-    tiles0 = ctx.session_read(with_points=False)["tiles_evaluated"] if prof_iters else None
-    phases = ctx.session_profile(prof_iters) if prof_iters else None
     state = ctx.session_read(with_points=False)
+    phases, prof_tiles = None, (0, 0)
+    if prof_iters:  # the same trajectory again, eager, with per-phase events
+        ctx.session_begin(x, y, cfg)
+        tiles0 = ctx.session_read(with_points=False)["tiles_evaluated"]
+        phases = ctx.session_profile(prof_iters)
+        tiles1 = ctx.session_read(with_points=False)["tiles_evaluated"]
+        # tile pairs the two E-step passes evaluated (0 when culling is off)
+        prof_tiles = tuple(b - a for a, b in zip(tiles0, tiles1))
     # the basis-stream kernel over the FULL basis (no spectral truncation),
     # for its HBM roofline; the basis is cached in the context
     full_phases = None
     if prof_iters and (state.get("spectral_rank") or 0) < (x.shape[0] if w.variant == "fast"
                                                           else fcpd.lowrank_rank(w.rank_fraction,
                                                                                  x.shape[0])):
-        fcfg = datagen.config_for(w, iterations=1 + prof_iters)
+        fcfg = datagen.config_for(w, iterations=4)
         fcfg.spectral_tau = 0.0
         ctx.session_begin(x, y, fcfg)
         ctx.session_run(1)
-        full_phases = ctx.session_profile(prof_iters)
-    # tile pairs the two E-step passes evaluated during the profiled iterations
-    # (0 when culling is off: every pair evaluated)
-    prof_tiles = (tuple(b - a for a, b in zip(tiles0, state["tiles_evaluated"]))
-                  if prof_iters else (0, 0))
+        full_phases = ctx.session_profile(3)
     sigma_last = float(state["sigma2_trace"][-1])
 
     # e2e through the public API: host buffers in, results out, basis cached
@@ -405,7 +419,8 @@ def run_ours(args, world, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed EM iterations (default: the workload's iteration count)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c1")

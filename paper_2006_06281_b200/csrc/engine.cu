@@ -214,6 +214,7 @@ struct Session {
   DevBuf<float4> xlo, xhi, ylo, yhi;
   DevBuf<float2> bminmax;
   DevBuf<unsigned long long> cull_counters;  // tiles evaluated (pass 1, pass 2), cumulative
+  DevBuf<int32_t> probe_paid;                // culling probe outcome per block (both passes)
   // per-iteration work lists of the two passes (culled tile pairs)
   DevBuf<int32_t> wl1_tiles, wl1_off, wl2_tiles, wl2_off, wl2_off_cc, wl_done;
   DevBuf<double> row_seg_cc;  // tensor-core pass 2: the CUDA-core kernel's segments
@@ -250,6 +251,7 @@ struct Session {
     for (auto* b : {&xlo, &xhi, &ylo, &yhi}) b->release();
     bminmax.release();
     cull_counters.release();
+    probe_paid.release();
     for (auto* b : {&wl1_tiles, &wl1_off, &wl2_tiles, &wl2_off, &wl2_off_cc, &wl_done})
       b->release();
     row_seg_cc.release();
@@ -410,11 +412,22 @@ bool cull_default(int64_t x_tiles, int64_t y_tiles) {
 }
 
 // Wire the session's culling geometry into the E-step buffers.  margin =
-// 50 + log2(count) log2-units: skipped mass ≤ 2^-50 of any column/row total.
+// kCullMarginBits + log2(count) log2-units: the skipped mass is ≤ 2^-bits of
+// any column/row total.  32 bits (2.3e-10 relative) sits far below the fp32
+// pair terms' own rounding (≈ |t|·2^-24 per term) and the 1e-5 σ² parity
+// bar; FCPD_CULL_MARGIN overrides.
+constexpr float kCullMarginBits = 32.f;
+float cull_margin_bits() {
+  if (const char* e = std::getenv("FCPD_CULL_MARGIN")) return static_cast<float>(std::atof(e));
+  return kCullMarginBits;
+}
+
 void set_cull(Session& s, EStepBuffers& eb, int64_t m, int64_t n_local, int64_t n_global) {
   CullInfo& c = eb.cull;
   c.enabled = s.cull && s.xlo.p && s.ylo.p && s.wl1_tiles.p && s.wl2_tiles.p ? 1 : 0;
   c.lists = (c.enabled || s.ep.tc) && s.wl2_tiles.p ? 1 : 0;
+  const char* pe = std::getenv("FCPD_CULL_PROBE");
+  c.probe = pe ? (std::atoi(pe) != 0) : 1;
   c.n_xtiles = ceil_div(m, 256);
   c.n_ytiles = ceil_div(n_local, 256);
   c.xlo = s.xlo.p;
@@ -422,10 +435,13 @@ void set_cull(Session& s, EStepBuffers& eb, int64_t m, int64_t n_local, int64_t 
   c.ylo = s.ylo.p;
   c.yhi = s.yhi.p;
   c.bminmax = s.bminmax.p;
-  c.margin1 = 50.f + static_cast<float>(std::log2(static_cast<double>(std::max<int64_t>(m, 1))));
+  const float bits = cull_margin_bits();
+  c.margin1 = bits + static_cast<float>(std::log2(static_cast<double>(std::max<int64_t>(m, 1))));
   c.margin2 =
-      50.f + static_cast<float>(std::log2(static_cast<double>(std::max<int64_t>(n_global, 1))));
+      bits + static_cast<float>(std::log2(static_cast<double>(std::max<int64_t>(n_global, 1))));
   c.counters = s.cull_counters.p;
+  c.probe_paid1 = s.probe_paid.p;
+  c.probe_paid2 = s.probe_paid.p ? s.probe_paid.p + c.n_ytiles : nullptr;
   eb.cullw = CullBuffers{s.xlo.p, s.xhi.p, s.ylo.p, s.yhi.p, s.bminmax.p};
   eb.wl1 = WorkListBuffers{s.wl1_tiles.p, s.wl1_off.p, s.wl_done.p};
   eb.wl2 = WorkListBuffers{s.wl2_tiles.p, s.wl2_off.p, s.wl_done.p ? s.wl_done.p + 1 : nullptr,
@@ -468,6 +484,8 @@ void alloc_estep(Session& s, int64_t m, int64_t n, cudaStream_t str) {
   s.bminmax.ensure(nyt);
   s.cull_counters.ensure(2);
   FCPD_CUDA(cudaMemsetAsync(s.cull_counters.p, 0, 2 * sizeof(unsigned long long), str));
+  s.probe_paid.ensure(nxt + nyt);
+  FCPD_CUDA(cudaMemsetAsync(s.probe_paid.p, 1, (nxt + nyt) * sizeof(int32_t), str));  // ≠ 0
   if (s.cull || s.ep.tc) {
     s.wl1_tiles.ensure(static_cast<size_t>(nyt) * nxt);
     s.wl1_off.ensure(nyt + 1);

@@ -48,6 +48,16 @@ namespace {
 constexpr int kTile = kTilePts;  // points staged in shared memory per step
 constexpr int kCombineLanes = 8; // lanes cooperating on one row/column reduction
 constexpr float kPadCoord = 3.0e18f;  // padding point: t ≈ 1e37, 2^-t = 0
+constexpr int kListThreads = 256;     // list kernels: one CTA per own block
+static_assert(kListThreads == kTilePts, "list CTA: one thread per own point");
+constexpr int kProbeTiles = 2;        // other-set tiles probed for the exact culling bound
+// Probe policy (speed only; any probe decision keeps the bound exact): probe
+// a block when the tiles the box bound keeps but U = 0 would drop are ≥ 1/2
+// of the kept ones; keep probing it every iteration while the probe drops
+// ≥ 1/4 of them, else reconsider every 4th iteration.
+constexpr float kProbeMinShare = 2.f;
+constexpr float kProbePayShare = 4.f;
+constexpr int kProbeRetry = 3;
 
 __device__ __forceinline__ float sqdist(float4 a, float4 b) {
   // the fallbacks' pair term (difference form, as the main kernels' diff path)
@@ -773,85 +783,340 @@ __device__ void last_cta_scan(int32_t* offset, int32_t* offset2, int n_blocks, i
   }
 }
 
-// Pass-1 list: per scene tile b, U = min over model tiles of the largest
-// squared distance (every column has t_min ≤ s²·U, so its total is
-// ≥ 2^{−s²U}); keep model tile j unless s²·mindist²(b, j) > s²U + margin.
-__global__ void col_list_kernel(CullInfo cull, int32_t* __restrict__ tiles,
-                                int32_t* __restrict__ offset, int n_blocks,
-                                int32_t* __restrict__ done, const IterState* __restrict__ st) {
-  if (!st->active) return;
-  const float s2 = st->sx * st->sx;
-  const int lane = threadIdx.x & 31;
-  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (b < n_blocks) {
-    const float4 lo = cull.ylo[b], hi = cull.yhi[b];
-    float u = INFINITY;
-    for (int j = lane; j < cull.n_xtiles; j += 32)
-      u = fminf(u, box_maxdist2(lo, hi, cull.xlo[j], cull.xhi[j]));
+// CTA-wide reductions for the list kernels (kMax: max, else min; sums of
+// small counts are exact in fp32).
+template <bool kMax>
+__device__ __forceinline__ float cta_reduce(float v, float* sh) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) u = fminf(u, __shfl_xor_sync(0xffffffffu, u, o));
-    const float cut = s2 * u + cull.margin1;
-    int count = 0;
-    int32_t* out = tiles + static_cast<int64_t>(b) * cull.n_xtiles;
-    for (int j0 = 0; j0 < cull.n_xtiles; j0 += 32) {
-      const int j = j0 + lane;
-      const bool keep =
-          j < cull.n_xtiles && !(s2 * box_mindist2(lo, hi, cull.xlo[j], cull.xhi[j]) > cut);
-      const unsigned mask = __ballot_sync(0xffffffffu, keep);
-      if (keep) out[count + __popc(mask & ((1u << lane) - 1))] = j;
-      count += __popc(mask);
+  for (int o = 16; o > 0; o >>= 1) {
+    const float w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = kMax ? fmaxf(v, w) : fminf(v, w);
+  }
+  __syncthreads();  // sh may still be read by a previous reduction
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  v = sh[0];
+  for (int w = 1; w < kListThreads / 32; ++w) v = kMax ? fmaxf(v, sh[w]) : fminf(v, sh[w]);
+  return v;
+}
+__device__ __forceinline__ float2 cta_sum2(float2 v, float2* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float2 r = sh[0];
+  for (int w = 1; w < kListThreads / 32; ++w) r.x += sh[w].x, r.y += sh[w].y;
+  return r;
+}
+__device__ __forceinline__ unsigned long long cta_min_u64(unsigned long long v,
+                                                          unsigned long long* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  v = sh[0];
+  for (int w = 1; w < kListThreads / 32; ++w) v = sh[w] < v ? sh[w] : v;
+  return v;
+}
+
+// The kProbeTiles tiles of the other set whose box centres lie closest to
+// the block's box centre (distinct; fewer when the other set has fewer).
+__device__ __forceinline__ int probe_tiles(float4 lo, float4 hi, const float4* olo,
+                                           const float4* ohi, int n_other, int* sel,
+                                           unsigned long long* sh) {
+  const float cx = 0.5f * (lo.x + hi.x), cy = 0.5f * (lo.y + hi.y), cz = 0.5f * (lo.z + hi.z);
+  int count = 0;
+  for (int r = 0; r < kProbeTiles && r < n_other; ++r) {
+    unsigned long long best = ~0ull;
+    for (int j = threadIdx.x; j < n_other; j += kListThreads) {
+      bool taken = false;
+      for (int q = 0; q < r; ++q) taken |= sel[q] == j;
+      if (taken) continue;
+      const float4 a = olo[j], b = ohi[j];
+      const float dx = 0.5f * (a.x + b.x) - cx, dy = 0.5f * (a.y + b.y) - cy,
+                  dz = 0.5f * (a.z + b.z) - cz;
+      const float d2 = dx * dx + dy * dy + dz * dz;  // ≥ 0: bits order like the value
+      const unsigned long long key =
+          (static_cast<unsigned long long>(__float_as_uint(d2)) << 32) | static_cast<unsigned>(j);
+      best = key < best ? key : best;
     }
-    if (lane == 0) offset[b + 1] = count;
+    best = cta_min_u64(best, sh);
+    sel[r] = static_cast<int>(best & 0xffffffffu);  // uniform across the CTA
+    ++count;
+  }
+  return count;
+}
+
+// Append the kept tiles j (keep(j) uniform per j) to out[]; returns the count.
+template <typename Keep>
+__device__ __forceinline__ int cta_compact(int n_other, int32_t* out, int* wcount, Keep keep) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int count = 0;
+  for (int j0 = 0; j0 < n_other; j0 += kListThreads) {
+    const int j = j0 + threadIdx.x;
+    const bool k = j < n_other && keep(j);
+    const unsigned mask = __ballot_sync(0xffffffffu, k);
+    __syncthreads();  // previous chunk's wcount readers are done
+    if (lane == 0) wcount[warp] = __popc(mask);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < kListThreads / 32; ++w) {
+      before += w < warp ? wcount[w] : 0;
+      total += wcount[w];
+    }
+    if (k) out[count + before + __popc(mask & ((1u << lane) - 1))] = j;
+    count += total;
+  }
+  return count;
+}
+
+// Probe staging: candidate points centred on the own block's box centre,
+// pair-interleaved for f32x2 math: pa[k] = (x_2k, x_2k+1, y_2k, y_2k+1),
+// pb[k] = (z_2k, z_2k+1, q_2k, q_2k+1).
+__device__ __forceinline__ void probe_stage(float4* pa, float4* pb, int i, float vx, float vy,
+                                            float vz, float q) {
+  float* fa = reinterpret_cast<float*>(pa) + (i >> 1) * 4 + (i & 1);
+  float* fb = reinterpret_cast<float*>(pb) + (i >> 1) * 4 + (i & 1);
+  fa[0] = vx;
+  fa[2] = vy;
+  fb[0] = vz;
+  fb[2] = q;
+}
+// min (kMax: max) over the staged points of q_i + a·v_i: 3 FFMA2 per two
+// points, four independent chains
+template <bool kMax>
+__device__ __forceinline__ float probe_scan(const float4* pa, const float4* pb, int pairs,
+                                            float ax, float ay, float az) {
+  const float2 X = make_float2(ax, ax), Y = make_float2(ay, ay), Z = make_float2(az, az);
+  const float init = kMax ? -INFINITY : INFINITY;
+  float r[4] = {init, init, init, init};
+  for (int k = 0; k < pairs; k += 2) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float4 A = pa[k + h], B = pb[k + h];
+      float2 d = __ffma2_rn(X, make_float2(A.x, A.y), make_float2(B.z, B.w));
+      d = __ffma2_rn(Y, make_float2(A.z, A.w), d);
+      d = __ffma2_rn(Z, make_float2(B.x, B.y), d);
+      r[2 * h] = kMax ? fmaxf(r[2 * h], d.x) : fminf(r[2 * h], d.x);
+      r[2 * h + 1] = kMax ? fmaxf(r[2 * h + 1], d.y) : fminf(r[2 * h + 1], d.y);
+    }
+  }
+  return kMax ? fmaxf(fmaxf(r[0], r[1]), fmaxf(r[2], r[3]))
+              : fminf(fminf(r[0], r[1]), fminf(r[2], r[3]));
+}
+
+// Pass-1 list, one CTA per scene block b.  Every column n of the block has
+// total ≥ max(2^{−t_min(n)}, 2^{log2 c}); the bound uses U ≥ max_n
+// min_m ‖y_n − x̃_m‖², the smaller of
+//  * the box bound min over model tiles j of maxdist²(b, j), and
+//  * the probe: the exact nearest distance of every column to the points of
+//    the kProbeTiles model tiles nearest the block (padded up by 2^-16),
+// and model tile j is dropped when s²·mindist²(b, j) > min(s²U, −log2 c) +
+// margin (every pair term in it is then < 2^-margin of the column total).
+__global__ void __launch_bounds__(kListThreads)
+    col_list_kernel(CullInfo cull, const float4* __restrict__ xt4, int64_t m,
+                    const float4* __restrict__ y4, int64_t n, int32_t* __restrict__ tiles,
+                    int32_t* __restrict__ offset, int n_blocks, int32_t* __restrict__ done,
+                    const IterState* __restrict__ st) {
+  if (!st->active) return;
+  __shared__ float4 pa[kProbeTiles * kTile / 2], pb[kProbeTiles * kTile / 2];
+  __shared__ unsigned long long sh64[kListThreads / 32];
+  __shared__ float shf[kListThreads / 32];
+  __shared__ int sel[kProbeTiles];
+  __shared__ int wcount[kListThreads / 32];
+  __shared__ float2 sh2[kListThreads / 32];
+  const float s2 = st->sx * st->sx;
+  const int b = blockIdx.x;
+  const float4 lo = cull.ylo[b], hi = cull.yhi[b];
+  const float neg_log2c = static_cast<float>(-st->log2c);  // +inf when ω = 0
+  float u = INFINITY, far = 0.f;
+  for (int j = threadIdx.x; j < cull.n_xtiles; j += kListThreads) {
+    u = fminf(u, box_maxdist2(lo, hi, cull.xlo[j], cull.xhi[j]));
+    far = fmaxf(far, box_mindist2(lo, hi, cull.xlo[j], cull.xhi[j]));
+  }
+  u = cta_reduce<false>(u, shf);
+  far = cta_reduce<true>(far, shf);
+  // Probe only where it can pay (policy above): the tiles the box bound
+  // keeps but U = 0 would drop bound what the probe can drop.
+  bool useful = s2 * far > fminf(0.f, neg_log2c) + cull.margin1;
+  float kept_box = 0.f;
+  useful = useful && cull.probe &&
+           (!cull.probe_paid1 || cull.probe_paid1[b] || (st->iter & kProbeRetry) == 0);
+  if (useful) {
+    const float cut_box = fminf(s2 * u, neg_log2c) + cull.margin1;
+    const float cut_min = fminf(0.f, neg_log2c) + cull.margin1;
+    float2 k = make_float2(0.f, 0.f);  // (kept, contested)
+    for (int j = threadIdx.x; j < cull.n_xtiles; j += kListThreads) {
+      const float t = s2 * box_mindist2(lo, hi, cull.xlo[j], cull.xhi[j]);
+      k.x += t <= cut_box ? 1.f : 0.f;
+      k.y += t <= cut_box && t > cut_min ? 1.f : 0.f;
+    }
+    k = cta_sum2(k, sh2);
+    kept_box = k.x;
+    useful = k.y * kProbeMinShare >= k.x;
+  }
+  const int np = cull.probe && useful
+                     ? probe_tiles(lo, hi, cull.xlo, cull.xhi, cull.n_xtiles, sel, sh64)
+                     : 0;
+  // exact nearest distance of every column to the probed points, in the
+  // expanded form |u|² − 2u·v + |v|² about the block centre c
+  const float cx = 0.5f * (lo.x + hi.x), cy = 0.5f * (lo.y + hi.y), cz = 0.5f * (lo.z + hi.z);
+  float vmax = 0.f;  // max |v|² of the probed points
+  for (int i = threadIdx.x; i < np * kTile; i += kListThreads) {
+    const int64_t g = static_cast<int64_t>(sel[i / kTile]) * kTile + i % kTile;
+    if (g < m) {
+      const float4 x = xt4[g];
+      const float vx = x.x - cx, vy = x.y - cy, vz = x.z - cz;
+      const float q = vx * vx + vy * vy + vz * vz;
+      vmax = fmaxf(vmax, q);
+      probe_stage(pa, pb, i, vx, vy, vz, q);
+    } else {
+      probe_stage(pa, pb, i, 0.f, 0.f, 0.f, INFINITY);
+    }
+  }
+  vmax = cta_reduce<true>(vmax, shf);  // (its barrier also publishes the staging)
+  const int64_t c = static_cast<int64_t>(b) * kTile + threadIdx.x;
+  float nn = -INFINITY;  // invalid column: neutral for the max
+  if (c < n && np > 0) {
+    const float4 y = y4[c];
+    const float ux = y.x - cx, uy = y.y - cy, uz = y.z - cz;
+    const float uq = ux * ux + uy * uy + uz * uz;
+    nn = fmaxf(0.f, uq + probe_scan<false>(pa, pb, np * kTile / 2, -2.f * ux, -2.f * uy,
+                                            -2.f * uz));
+  }
+  // pad for the rounding of the expanded form (≤ a few ε·(|u|² + |v|²))
+  const float ex = hi.x - lo.x, ey = hi.y - lo.y, ez = hi.z - lo.z;
+  const float h2 = 0.25f * (ex * ex + ey * ey + ez * ez);
+  const float probe = cta_reduce<true>(nn, shf) * (1.f + 0x1p-16f) + 0x1p-20f * (h2 + vmax);
+  if (np > 0) u = fminf(u, probe);
+  const float floor_t = fminf(s2 * u, neg_log2c);
+  const float cut = floor_t + cull.margin1;
+  const int count = cta_compact(cull.n_xtiles, tiles + static_cast<int64_t>(b) * cull.n_xtiles,
+                                wcount, [&](int j) {
+                                  return !(s2 * box_mindist2(lo, hi, cull.xlo[j], cull.xhi[j]) >
+                                           cut);
+                                });
+  if (threadIdx.x == 0) {
+    offset[b + 1] = count;
+    if (np > 0 && cull.probe_paid1) cull.probe_paid1[b] = (kept_box - count) * kProbePayShare >= kept_box;
   }
   last_cta_scan(offset, nullptr, n_blocks, done, cull.counters);
 }
 
-// Pass-2 list: per model tile b, a lower bound on max_n L_mn of every row,
-// L_lb = max over scene tiles of (min b − s²·maxdist²); keep scene tile j
-// unless its largest possible L (max b − s²·mindist²) < L_lb − margin
-// (culling off: keep every tile).  With offset_cc (tensor-core pass 2), a
-// block whose scaled squared half-diagonal exceeds kCentredMaxR2 is routed
-// to the CUDA-core list (difference form) instead.
-__global__ void row_list_kernel(CullInfo cull, int32_t* __restrict__ tiles,
-                                int32_t* __restrict__ offset, int32_t* __restrict__ offset_cc,
-                                int n_blocks, int32_t* __restrict__ done,
-                                const IterState* __restrict__ st) {
+// Pass-2 list, one CTA per model block b.  Every row m of the block has
+// max_n L_mn ≥ L_lb, the larger of
+//  * the box bound max over scene tiles j of (min b − s²·maxdist²(b, j)),
+//  * the probe: min over the block's rows of the exact max of b_n − s²‖y_n −
+//    x̃_m‖² over the kProbeTiles scene tiles nearest the block (less a
+//    rounding slack);
+// scene tile j is dropped when its largest possible L (max b − s²·mindist²)
+// < L_lb − margin (culling off: every tile kept).  With offset_cc
+// (tensor-core pass 2), a block whose scaled squared half-diagonal exceeds
+// kCentredMaxR2 is routed to the CUDA-core list (difference form) instead.
+__global__ void __launch_bounds__(kListThreads)
+    row_list_kernel(CullInfo cull, const float4* __restrict__ xt4, int64_t m,
+                    const float4* __restrict__ y4b, int64_t n, int32_t* __restrict__ tiles,
+                    int32_t* __restrict__ offset, int32_t* __restrict__ offset_cc, int n_blocks,
+                    int32_t* __restrict__ done, const IterState* __restrict__ st) {
   if (!st->active) return;
+  __shared__ float4 pa[kProbeTiles * kTile / 2], pb[kProbeTiles * kTile / 2];
+  __shared__ unsigned long long sh64[kListThreads / 32];
+  __shared__ float shf[kListThreads / 32];
+  __shared__ int sel[kProbeTiles];
+  __shared__ int wcount[kListThreads / 32];
+  __shared__ float2 sh2[kListThreads / 32];
   const float s2 = st->sx * st->sx;
-  const int lane = threadIdx.x & 31;
-  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (b < n_blocks) {
-    const float4 lo = cull.xlo[b], hi = cull.xhi[b];
-    float floor_l = -INFINITY;
-    if (cull.enabled) {
-      float l = -INFINITY;
-      for (int j = lane; j < cull.n_ytiles; j += 32)
-        l = fmaxf(l, cull.bminmax[j].x - s2 * box_maxdist2(lo, hi, cull.ylo[j], cull.yhi[j]));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) l = fmaxf(l, __shfl_xor_sync(0xffffffffu, l, o));
-      floor_l = l - cull.margin2;
+  const int b = blockIdx.x;
+  const float4 lo = cull.xlo[b], hi = cull.xhi[b];
+  float floor_l = -INFINITY, kept_box = 0.f;
+  int np = 0;
+  if (cull.enabled) {
+    float l = -INFINITY, lmin = INFINITY;
+    for (int j = threadIdx.x; j < cull.n_ytiles; j += kListThreads) {
+      l = fmaxf(l, cull.bminmax[j].x - s2 * box_maxdist2(lo, hi, cull.ylo[j], cull.yhi[j]));
+      lmin = fminf(lmin,
+                   cull.bminmax[j].y - s2 * box_mindist2(lo, hi, cull.ylo[j], cull.yhi[j]));
     }
-    int count = 0;
-    int32_t* out = tiles + static_cast<int64_t>(b) * cull.n_ytiles;
-    for (int j0 = 0; j0 < cull.n_ytiles; j0 += 32) {
-      const int j = j0 + lane;
-      const bool keep =
-          j < cull.n_ytiles &&
-          (!cull.enabled ||
-           !(cull.bminmax[j].y - s2 * box_mindist2(lo, hi, cull.ylo[j], cull.yhi[j]) < floor_l));
-      const unsigned mask = __ballot_sync(0xffffffffu, keep);
-      if (keep) out[count + __popc(mask & ((1u << lane) - 1))] = j;
-      count += __popc(mask);
-    }
-    if (lane == 0) {
-      bool to_tc = true;
-      if (offset_cc) {
-        const float ex = hi.x - lo.x, ey = hi.y - lo.y, ez = hi.z - lo.z;
-        to_tc = 0.25f * s2 * (ex * ex + ey * ey + ez * ez) <= kCentredMaxR2;
-        offset_cc[b + 1] = to_tc ? 0 : count;
+    l = cta_reduce<true>(l, shf);
+    lmin = cta_reduce<false>(lmin, shf);
+    // L ≤ 0, so a tile can only be dropped if its bound is below −margin;
+    // probe policy as in pass 1, with L_lb = 0 as the optimistic bound
+    bool useful = lmin < -cull.margin2;
+    useful = useful && cull.probe &&
+             (!cull.probe_paid2 || cull.probe_paid2[b] || (st->iter & kProbeRetry) == 0);
+    if (useful) {
+      const float floor_box = l - cull.margin2;
+      float2 k = make_float2(0.f, 0.f);
+      for (int j = threadIdx.x; j < cull.n_ytiles; j += kListThreads) {
+        const float v =
+            cull.bminmax[j].y - s2 * box_mindist2(lo, hi, cull.ylo[j], cull.yhi[j]);
+        k.x += v >= floor_box ? 1.f : 0.f;
+        k.y += v >= floor_box && v < -cull.margin2 ? 1.f : 0.f;
       }
-      offset[b + 1] = to_tc ? count : 0;
+      k = cta_sum2(k, sh2);
+      kept_box = k.x;
+      useful = k.y * kProbeMinShare >= k.x;
     }
+    np = cull.probe && useful
+             ? probe_tiles(lo, hi, cull.ylo, cull.yhi, cull.n_ytiles, sel, sh64)
+             : 0;
+    // exact max over the probed columns of b_n − s²‖y_n − x̃_m‖² for every
+    // row, expanded about the block centre c: (b − s²|v|²) + 2s²u·v − s²|u|²
+    const float cx = 0.5f * (lo.x + hi.x), cy = 0.5f * (lo.y + hi.y),
+                cz = 0.5f * (lo.z + hi.z);
+    float vmax = 0.f;
+    for (int i = threadIdx.x; i < np * kTile; i += kListThreads) {
+      const int64_t g = static_cast<int64_t>(sel[i / kTile]) * kTile + i % kTile;
+      if (g < n) {
+        const float4 y = y4b[g];
+        const float vx = y.x - cx, vy = y.y - cy, vz = y.z - cz;
+        const float q = vx * vx + vy * vy + vz * vz;
+        vmax = fmaxf(vmax, q);
+        probe_stage(pa, pb, i, vx, vy, vz, y.w - s2 * q);
+      } else {
+        probe_stage(pa, pb, i, 0.f, 0.f, 0.f, -INFINITY);
+      }
+    }
+    vmax = cta_reduce<true>(vmax, shf);
+    const int64_t r = static_cast<int64_t>(b) * kTile + threadIdx.x;
+    float best = INFINITY;  // invalid row: neutral for the min
+    if (r < m && np > 0) {
+      const float4 x = xt4[r];
+      const float ux = x.x - cx, uy = x.y - cy, uz = x.z - cz;
+      const float uq = ux * ux + uy * uy + uz * uz;
+      const float t2 = 2.f * s2;
+      best = probe_scan<true>(pa, pb, np * kTile / 2, t2 * ux, t2 * uy, t2 * uz) - s2 * uq;
+    }
+    const float probe = cta_reduce<false>(best, shf);
+    const float ex = hi.x - lo.x, ey = hi.y - lo.y, ez = hi.z - lo.z;
+    const float h2 = 0.25f * (ex * ex + ey * ey + ez * ez);
+    // rounding slack of the fp32 bound (expanded form: ≲ a few ε·s²(|u|² + |v|²))
+    if (np > 0) l = fmaxf(l, probe - 1e-3f - 1e-5f * fabsf(probe) - 0x1p-20f * s2 * (h2 + vmax));
+    floor_l = l - cull.margin2;
+  }
+  const int count = cta_compact(
+      cull.n_ytiles, tiles + static_cast<int64_t>(b) * cull.n_ytiles, wcount, [&](int j) {
+        return !cull.enabled ||
+               !(cull.bminmax[j].y - s2 * box_mindist2(lo, hi, cull.ylo[j], cull.yhi[j]) <
+                 floor_l);
+      });
+  if (threadIdx.x == 0) {
+    bool to_tc = true;
+    if (offset_cc) {
+      const float ex = hi.x - lo.x, ey = hi.y - lo.y, ez = hi.z - lo.z;
+      to_tc = 0.25f * s2 * (ex * ex + ey * ey + ez * ez) <= kCentredMaxR2;
+      offset_cc[b + 1] = to_tc ? 0 : count;
+    }
+    offset[b + 1] = to_tc ? count : 0;
+    if (np > 0 && cull.probe_paid2) cull.probe_paid2[b] = (kept_box - count) * kProbePayShare >= kept_box;
   }
   last_cta_scan(offset, offset_cc, n_blocks, done,
                 cull.enabled && cull.counters ? cull.counters + 1 : nullptr);
@@ -1075,8 +1340,8 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
   const WorkList wl = pass1_list(p, b, m);
   if (cu.enabled) {
     launch_tile_bbox(b.xt4, m, b.cullw.xlo, b.cullw.xhi, st, stream);
-    col_list_kernel<<<ceil_div(p.col_blocks, 8), 256, 0, stream>>>(
-        cu, b.wl1.tiles, b.wl1.offset, p.col_blocks, b.wl1.done, st);
+    col_list_kernel<<<p.col_blocks, kListThreads, 0, stream>>>(
+        cu, b.xt4, m, b.y4b, n, b.wl1.tiles, b.wl1.offset, p.col_blocks, b.wl1.done, st);
     FCPD_LAUNCH_CHECK();
   }
   estep_col_kernel<<<p.col_grid, 128, 0, stream>>>(b.xt4, m, b.y4b, n, st, wl, b.col_seg,
@@ -1110,9 +1375,9 @@ void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int6
   if (cu.lists) {
     if (!cu.enabled)  // x̃ tile boxes for the routing (pass 1 made them when culling)
       launch_tile_bbox(b.xt4, m, b.cullw.xlo, b.cullw.xhi, st, stream);
-    row_list_kernel<<<ceil_div(p.row_blocks, 8), 256, 0, stream>>>(
-        cu, b.wl2.tiles, b.wl2.offset, p.tc ? b.wl2.offset_cc : nullptr, p.row_blocks,
-        b.wl2.done, st);
+    row_list_kernel<<<p.row_blocks, kListThreads, 0, stream>>>(
+        cu, b.xt4, m, b.y4b, n, b.wl2.tiles, b.wl2.offset, p.tc ? b.wl2.offset_cc : nullptr,
+        p.row_blocks, b.wl2.done, st);
     FCPD_LAUNCH_CHECK();
   }
   SegSrc a, c;

@@ -81,10 +81,13 @@ void launch_estep_row_tc(const float4* xt4, int64_t m, const float4* y4b, int64_
 // Tile culling.  Points are Morton-sorted by the engine so
 // 256-point tiles are compact boxes; a (block, tile) pair is dropped from
 // the work list when every pair term in it is below 2^-margin of the
-// smallest possible column (row) total.  With margin = 50 + log2(count) the
-// skipped mass is ≤ 2^-50 relative: exact to fp32.
+// smallest possible column (row) total.  With margin = bits + log2(count)
+// the skipped mass is ≤ 2^-bits relative (engine.cu: 32 bits).  The lower
+// bound on the totals comes from box geometry and, with `probe`, from exact
+// nearest-point distances to the two closest tiles (estep.cu list kernels).
 struct CullInfo {
   int enabled = 0;  // culling drops tile pairs from the work lists
+  int probe = 1;    // probe bound on (FCPD_CULL_PROBE=0 → box bound only)
   int lists = 0;    // explicit work lists (culling, or pass-2 routing to tensor cores)
   int n_xtiles = 0, n_ytiles = 0;   // 256-point tiles
   const float4* xlo = nullptr;      // model tiles (x̃ of this iteration)
@@ -94,6 +97,10 @@ struct CullInfo {
   const float2* bminmax = nullptr;  // per scene tile: (min b, max b)
   float margin1 = 0.f, margin2 = 0.f;
   unsigned long long* counters = nullptr;  // [0] pass-1, [1] pass-2 tile pairs evaluated
+  // per own block: did the last probe drop ≥ 1/4 of the box-kept tiles?
+  // (blocks whose probe does not pay reconsider it every 4th iteration)
+  int32_t* probe_paid1 = nullptr;  // [n_ytiles]
+  int32_t* probe_paid2 = nullptr;  // [n_xtiles]
 };
 
 struct CullBuffers {  // writable views of the CullInfo arrays (engine-owned)

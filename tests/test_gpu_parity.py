@@ -450,6 +450,42 @@ def test_full_size_parity_configs_2_4(ctx, fc, orc, tmp_path, name, iters):
     assert pts <= POINT_FRAC
 
 
+# ------------------------------------------------------------- tile culling
+
+
+@pytest.mark.parametrize("name,m,iters,late_frac", [("c2", 20000, 60, 0.5),
+                                                    ("c1", 12000, 60, 1.0)])
+def test_culling_matches_unculled(ctx, fc, monkeypatch, name, m, iters, late_frac):
+    """Tile culling (box + probe bounds, 32-bit margin) over a whole
+    trajectory: the σ² trace and the points equal the every-pair run (itself
+    pinned to the oracle above) far inside the parity bar.  On the C2 surface
+    σ² falls to ~1e-4 and the late iterations skip most tile pairs; C1's
+    uniform outliers keep σ² ≈ 1e-2, where little can be skipped."""
+    from paper_2006_06281_b200 import datagen
+    x, y, w = datagen.generate(name, m=m)
+    cfg = datagen.config_for(w, iterations=iters)
+    monkeypatch.setenv("FCPD_CULL", "0")
+    full = ctx.register(x, y, cfg)
+    monkeypatch.setenv("FCPD_CULL", "1")
+    got = ctx.register(x, y, cfg)
+    rel = np.abs(got.sigma2_trace / full.sigma2_trace - 1).max()
+    pts = np.abs(got.transformed - full.transformed).max() / bbox_diag(y)
+    print(f"{name}: σ² rel {rel:.3g}  points {pts:.3g} of the bbox diagonal, "
+          f"final σ² {full.sigma2_trace[-1]:.3g}")
+    assert rel <= 1e-6, rel
+    assert pts <= 1e-7, pts
+    # the last 10 iterations' share of tile pairs evaluated
+    ctx.session_begin(x, y, cfg)
+    ctx.session_run(iters - 10)
+    t0 = ctx.session_read(with_points=False)["tiles_evaluated"]
+    ctx.session_run(10)
+    t1 = ctx.session_read(with_points=False)["tiles_evaluated"]
+    total = 10 * -(-x.shape[0] // 256) * -(-y.shape[0] // 256)
+    frac = [(b - a) / total for a, b in zip(t0, t1)]
+    print(f"{name}: late tile-pair fraction evaluated {frac}")
+    assert 0.0 < max(frac) <= late_frac, frac
+
+
 # ------------------------------------------ spectral truncation of the streams
 
 

@@ -11,7 +11,7 @@ python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke
 timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_reference.json 2> $O/bench_reference.err
 for w in ${WORKLOADS:-c0 c2 c3 c4}; do
-  timeout 900 python bench.py --workload $w --steps 20 --warmup 5 --no-cpu --e2e-calls 1 > $O/bench_$w.json 2> $O/bench_$w.err
+  timeout 900 python bench.py --workload $w --warmup 5 --no-cpu --e2e-calls 1 > $O/bench_$w.json 2> $O/bench_$w.err
 done
 CMD="python bench.py --steps 5 --warmup 3 --no-cpu --e2e-calls 0"
 timeout 600 $CMD > $O/plain.log 2>&1 && \
