@@ -647,65 +647,46 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
                         int d, const fcpd_config& cfg);
 void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall);
 
-// ---- spatial (Morton / Z-order) sort: makes 256-point tiles compact boxes
-// for the E-step's tile culling.  The order depends only on the point set
-// itself (its own bounding box), is deterministic (ties by index), and is
-// undone on every output.
-uint64_t morton_spread21(uint64_t v) {
-  v &= 0x1fffffull;
-  v = (v | v << 32) & 0x1f00000000ffffull;
-  v = (v | v << 16) & 0x1f0000ff0000ffull;
-  v = (v | v << 8) & 0x100f00f00f00f00full;
-  v = (v | v << 4) & 0x10c30c30c30c30c3ull;
-  v = (v | v << 2) & 0x1249249249249249ull;
-  return v;
+// ---- spatial sort: makes every 256-point tile a compact box for the
+// E-step's tile culling and its centred pair form.  A k-d partition: split
+// the points at a multiple of 256 along the longest axis of their bounding
+// box, recursively, so every tile is one leaf with a bounded aspect ratio
+// (a Morton order lets some tiles straddle distant cells, and those tiles
+// lose both culling and the centred form).  Depth-first leaf order keeps
+// consecutive tiles near each other.  The order depends only on the point
+// set, is deterministic (ties by index), and is undone on every output.
+namespace {
+void kd_partition(const std::vector<double>& soa, int64_t cnt, int64_t* idx, int64_t len) {
+  constexpr int64_t kLeaf = 256;
+  while (len > kLeaf) {
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t k = 0; k < len; ++k)
+      for (int c = 0; c < 3; ++c) {
+        const double v = soa[c * cnt + idx[k]];
+        lo[c] = std::min(lo[c], v);
+        hi[c] = std::max(hi[c], v);
+      }
+    int axis = 0;
+    for (int c = 1; c < 3; ++c)
+      if (hi[c] - lo[c] > hi[axis] - lo[axis]) axis = c;
+    const int64_t leaves = (len + kLeaf - 1) / kLeaf;
+    const int64_t left = (leaves + 1) / 2 * kLeaf;  // a whole number of tiles
+    const double* key = soa.data() + axis * cnt;
+    std::nth_element(idx, idx + left, idx + len, [key](int64_t a, int64_t b) {
+      return key[a] < key[b] || (key[a] == key[b] && a < b);
+    });
+    kd_partition(soa, cnt, idx, left);
+    idx += left;
+    len -= left;
+  }
 }
+}  // namespace
 
 // perm[k] = original index of sorted position k; soa (SoA 3×cnt) is permuted.
-std::vector<int64_t> morton_sort(std::vector<double>& soa, int64_t cnt) {
-  double lo[3], hi[3];
-  for (int c = 0; c < 3; ++c) {
-    lo[c] = INFINITY;
-    hi[c] = -INFINITY;
-    for (int64_t i = 0; i < cnt; ++i) {
-      lo[c] = std::min(lo[c], soa[c * cnt + i]);
-      hi[c] = std::max(hi[c], soa[c * cnt + i]);
-    }
-  }
-  double span = 0.0;
-  for (int c = 0; c < 3; ++c) span = std::max(span, hi[c] - lo[c]);
-  const double q = span > 0.0 ? 2097151.0 / span : 0.0;
-  std::vector<uint64_t> key(cnt), key2(cnt);
-  std::vector<int64_t> perm(cnt), perm2(cnt);
-  uint64_t all_or = 0, all_and = ~0ull;
-  for (int64_t i = 0; i < cnt; ++i) {
-    uint64_t k = 0;
-    for (int c = 0; c < 3; ++c) {
-      const uint64_t v = static_cast<uint64_t>((soa[c * cnt + i] - lo[c]) * q);
-      k |= morton_spread21(v) << c;
-    }
-    key[i] = k;
-    perm[i] = i;
-    all_or |= k;
-    all_and &= k;
-  }
-  // LSD radix sort, 8 bits per pass (passes whose byte is constant are
-  // skipped); stable, so equal keys keep index order — the same order as
-  // sorting (key, index) pairs, deterministic.  O(8n) instead of O(n log n):
-  // the host side of session setup at 200k points.
-  for (int shift = 0; shift < 64; shift += 8) {
-    if ((((all_or ^ all_and) >> shift) & 0xff) == 0) continue;
-    size_t count[257] = {};
-    for (int64_t i = 0; i < cnt; ++i) ++count[((key[i] >> shift) & 0xff) + 1];
-    for (int b = 0; b < 256; ++b) count[b + 1] += count[b];
-    for (int64_t i = 0; i < cnt; ++i) {
-      const size_t dst = count[(key[i] >> shift) & 0xff]++;
-      key2[dst] = key[i];
-      perm2[dst] = perm[i];
-    }
-    key.swap(key2);
-    perm.swap(perm2);
-  }
+std::vector<int64_t> spatial_sort(std::vector<double>& soa, int64_t cnt) {
+  std::vector<int64_t> perm(cnt);
+  for (int64_t i = 0; i < cnt; ++i) perm[i] = i;
+  kd_partition(soa, cnt, perm.data(), cnt);
   std::vector<double> out(soa.size());
   for (int c = 0; c < 3; ++c)
     for (int64_t k = 0; k < cnt; ++k) out[c * cnt + k] = soa[c * cnt + perm[k]];
@@ -772,14 +753,14 @@ void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, i
   std::vector<double> xs, ys;
   normalize_pair_host(x, m, y, n, d, cfg.normalize != 0, xs, ys, s.center, &s.scale);
   stamp("normalize");
-  // internal order: Morton-sorted model and scene (undone on output); the
+  // internal order: spatially sorted model and scene (undone on output); the
   // two sorts are independent
   {
-    std::thread tx([&] { s.perm_x = morton_sort(xs, m); });
-    s.perm_y = morton_sort(ys, n);
+    std::thread tx([&] { s.perm_x = spatial_sort(xs, m); });
+    s.perm_y = spatial_sort(ys, n);
     tx.join();
   }
-  stamp("morton");
+  stamp("spatial_sort");
   // x0 must be on the device before the Gram build
   s.x0.ensure(3 * m);
   FCPD_CUDA(cudaMemcpyAsync(s.x0.p, xs.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice,
@@ -880,7 +861,7 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
   s.d2h += sizeof(double) * (run + 3 * m);
   std::vector<double> xt(3 * m);
   FCPD_CUDA(cudaMemcpyAsync(xt.data(), s.xt64.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, str));
-  // internal rows are Morton-sorted: sorted row k is original row perm_x[k]
+  // internal rows are spatially sorted: sorted row k is original row perm_x[k]
   const std::vector<int64_t>& px = s.perm_x;
   const std::vector<int64_t>& py = s.perm_y;
   if (out->coefficients) {
@@ -1100,9 +1081,9 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
         std::max((md * ystat[3] + ng * fx - 2.0 * dot) / (static_cast<double>(d) * md * ng), 0.0);
   }
   // internal spatial order: the full model (identical on all ranks) and the
-  // local scene shard are Morton-sorted; row shards are spatial slabs
-  s.perm_x = morton_sort(xs, m);
-  s.perm_y = morton_sort(ys, n);
+  // local scene shard are spatially sorted; row shards are spatial slabs
+  s.perm_x = spatial_sort(xs, m);
+  s.perm_y = spatial_sort(ys, n);
   // spectral basis (computed redundantly per rank; each keeps its row shard)
   s.x0.ensure(3 * m);
   FCPD_CUDA(cudaMemcpyAsync(s.x0.p, xs.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, str));
@@ -1519,8 +1500,8 @@ int fcpd_estep(fcpd_ctx* ctx, const double* xt, int64_t m, const double* y, int6
       std::memcpy(&ys[c * n], y + c * n, sizeof(double) * n);
     }
     s.dist = false;
-    s.perm_x = morton_sort(xs, m);  // internal spatial order (tile culling)
-    s.perm_y = morton_sort(ys, n);
+    s.perm_x = spatial_sort(xs, m);  // internal spatial order (tile culling)
+    s.perm_y = spatial_sort(ys, n);
     prepare_buffers(ctx, s, xs, ys, 1, false);
     reset_state(ctx, s, sigma2);
     const EStepBuffers eb = estep_buffers(s, s.pt1.p, false);
@@ -1650,7 +1631,7 @@ int fcpd_save_spectral_cache(fcpd_ctx* ctx, const char* path) {
     bool ok = std::fwrite("FCPD", 1, 4, f) == 4 && std::fwrite(&ver, 4, 1, f) == 1 &&
               std::fwrite(&mm, 8, 1, f) == 1 && std::fwrite(&kk, 8, 1, f) == 1 &&
               std::fwrite(&b.key_beta, 8, 1, f) == 1;
-    // rows in the caller's point order (the device keeps them Morton-sorted)
+    // rows in the caller's point order (the device keeps them spatially sorted)
     std::vector<int64_t> inv(b.m);
     for (int64_t k = 0; k < b.m; ++k) inv[b.perm.empty() ? k : b.perm[k]] = k;
     std::vector<double> row(b.k);
@@ -1705,7 +1686,7 @@ int fcpd_load_spectral_cache(fcpd_ctx* ctx, const char* path, const double* x, i
     std::vector<double> xs, ys;
     double center[3], scale;
     normalize_pair_host(x, m, y, n, d, cfg->normalize != 0, xs, ys, center, &scale);
-    std::vector<int64_t> perm = morton_sort(xs, m);  // the order register will use
+    std::vector<int64_t> perm = spatial_sort(xs, m);  // the order register will use
     uint64_t h = fnv1a(xs.data(), sizeof(double) * xs.size());
     h = fnv1a(&m, sizeof m, h);
     h = fnv1a(&rank, sizeof rank, h);

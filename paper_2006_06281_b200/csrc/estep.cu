@@ -22,7 +22,7 @@
 // correspondence.hpp:89-91) bit-for-bit in the decision.
 //
 // Schedule (both passes): the work is the list of (own block, other tile)
-// pairs — all of them, or the culled list (tile culling on Morton-sorted
+// pairs — all of them, or the culled list (tile culling on spatially sorted
 // points, list kernels below).  A persistent grid of exactly one CTA wave
 // splits the list's POINTS evenly (stream-K): CTA g gets the contiguous
 // range [g·P/G, (g+1)·P/G) of the P = 256·units point-units, cut into
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
 }
 
 // ---------------------------------------------------------------------------
-// Tile geometry and work lists for culling (points are Morton-sorted by the
+// Tile geometry and work lists for culling (points are k-d sorted by the
 // engine, so 256-point tiles are spatially compact).
 
 // per-tile axis-aligned box of the first three coordinates (unscaled)

@@ -78,7 +78,7 @@ void launch_estep_row_tc(const float4* xt4, int64_t m, const float4* y4b, int64_
                          const IterState* st, const WorkList& wl, double* seg, int grid,
                          cudaStream_t stream);
 
-// Tile culling.  Points are Morton-sorted by the engine so
+// Tile culling.  Points are k-d sorted by the engine so
 // 256-point tiles are compact boxes; a (block, tile) pair is dropped from
 // the work list when every pair term in it is below 2^-margin of the
 // smallest possible column (row) total.  With margin = bits + log2(count)

@@ -9,6 +9,7 @@
 //   *_nomufu            : same FP32 work, ex2 replaced by a register move
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/loopbench tools/loopbench.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 constexpr int kPts = 256;
@@ -235,6 +236,125 @@ __global__ void __launch_bounds__(128) loop_kernel(float* out, int occ_pad) {
       gx.y + gy.x + gy.y + gz.x + gz.y + gq.x + gq.y;
 }
 
+// Pass-2 accumulation on the legacy tensor path (mma.sync m16n8k8 tf32,
+// HMMA): logits by FFMA2 in the A-fragment layout (lane g,t4: rows g+16i,
+// g+8+16i; columns t4, t4+4 of each 8-column step), w split into tf32 hi/lo,
+// B = 8 column quantities (v hi, |v|² hi, v lo, |v|² lo), Σw by FADD2, the
+// MMA accumulators flushed into fp32 every 8 steps.  NB row blocks of 16 per
+// warp; reports cycles per 64 pairs (point-warp equivalent).
+template <int NB, bool MUFU, bool HM = true>
+__global__ void __launch_bounds__(128) mma_row_kernel(float* out, int occ_pad) {
+  __shared__ float4 sa[kPts];
+  __shared__ float4 sd1[kPts], sd2[kPts];  // pre-duplicated (vx,vx,vy,vy), (vz,vz,Bn,Bn)
+  __shared__ float sbf[kPts * 8];
+  extern __shared__ char pad[];
+  for (int i = threadIdx.x; i < kPts; i += 128) {
+    const float f = 1e-3f * (i + 1);
+    sa[i] = make_float4(f, -f, 0.5f * f, -2.f * f);
+    sd1[i] = make_float4(f, f, -f, -f);
+    sd2[i] = make_float4(0.5f * f, 0.5f * f, -2.f * f, -2.f * f);
+    for (int c = 0; c < 8; ++c) sbf[i * 8 + c] = f * (c + 1);
+  }
+  if (occ_pad < 0) pad[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  float2 ux[NB], uy[NB], uz[NB], s0[NB];
+  float c[NB][4], acc[NB][4];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const float t0 = 1e-4f * (threadIdx.x + i);
+    ux[i] = make_float2(t0, -t0);
+    uy[i] = make_float2(0.3f * t0, 0.7f);
+    uz[i] = make_float2(t0, 0.1f);
+    s0[i] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[i][q] = acc[i][q] = 0.f;
+  }
+  for (int r = 0; r < kReps; ++r) {
+    for (int j = 0; j < kPts; j += 64) {
+#pragma unroll
+      for (int st = 0; st < 8; ++st) {
+        const int k0 = j + 8 * st + t4, k1 = k0 + 4;
+        const float4 A1 = sd1[k0], A2 = sd2[k0], B1 = sd1[k1], B2 = sd2[k1];
+        const unsigned b0 = __float_as_uint(sbf[k0 * 8 + g]), b1 = __float_as_uint(sbf[k1 * 8 + g]);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          float2 L0 = __ffma2_rn(ux[i], make_float2(A1.x, A1.y), make_float2(A2.z, A2.w));
+          L0 = __ffma2_rn(uy[i], make_float2(A1.z, A1.w), L0);
+          L0 = __ffma2_rn(uz[i], make_float2(A2.x, A2.y), L0);
+          float2 L1 = __ffma2_rn(ux[i], make_float2(B1.x, B1.y), make_float2(B2.z, B2.w));
+          L1 = __ffma2_rn(uy[i], make_float2(B1.z, B1.w), L1);
+          L1 = __ffma2_rn(uz[i], make_float2(B2.x, B2.y), L1);
+          const float2 w0 = ex2v<MUFU>(L0), w1 = ex2v<MUFU>(L1);
+          s0[i] = __fadd2_rn(s0[i], __fadd2_rn(w0, w1));
+          const float2 h0 = make_float2(__uint_as_float(__float_as_uint(w0.x) & 0xffffe000u),
+                                        __uint_as_float(__float_as_uint(w0.y) & 0xffffe000u));
+          const float2 h1 = make_float2(__uint_as_float(__float_as_uint(w1.x) & 0xffffe000u),
+                                        __uint_as_float(__float_as_uint(w1.y) & 0xffffe000u));
+          const float2 l0 = __fadd2_rn(w0, make_float2(-h0.x, -h0.y));
+          const float2 l1 = __fadd2_rn(w1, make_float2(-h1.x, -h1.y));
+          if (!HM) {  // stand-in: the same operands consumed by FP32 adds
+            c[i][0] += h0.x + l0.x;
+            c[i][1] += h0.y + l0.y;
+            c[i][2] += h1.x + __uint_as_float(b0);
+            c[i][3] += h1.y + __uint_as_float(b1);
+            continue;
+          }
+          asm volatile(
+              "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+              "{%8,%9}, {%0,%1,%2,%3};\n"
+              : "+f"(c[i][0]), "+f"(c[i][1]), "+f"(c[i][2]), "+f"(c[i][3])
+              : "r"(__float_as_uint(h0.x)), "r"(__float_as_uint(h0.y)), "r"(__float_as_uint(h1.x)),
+                "r"(__float_as_uint(h1.y)), "r"(b0), "r"(b1));
+          asm volatile(
+              "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+              "{%8,%9}, {%0,%1,%2,%3};\n"
+              : "+f"(c[i][0]), "+f"(c[i][1]), "+f"(c[i][2]), "+f"(c[i][3])
+              : "r"(__float_as_uint(l0.x)), "r"(__float_as_uint(l0.y)), "r"(__float_as_uint(l1.x)),
+                "r"(__float_as_uint(l1.y)), "r"(b0), "r"(b1));
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] += c[i][q], c[i][q] = 0.f;
+    }
+  }
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) sum += s0[i].x + s0[i].y + acc[i][0] + acc[i][1] + acc[i][2] + acc[i][3];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = sum;
+}
+
+template <int NB, bool MUFU, bool HM = true>
+void run_mma(const char* name, int sms, int ctas_per_sm, float* out) {
+  auto k = mma_row_kernel<NB, MUFU, HM>;
+  int occ = 0;
+  const int pad = 227 * 1024 / ctas_per_sm - 21 * 1024;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 128, pad);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int grid = sms * occ;
+  k<<<grid, 128, pad>>>(out, 0);
+  cudaDeviceSynchronize();
+  cudaEventRecord(a);
+  for (int r = 0; r < 3; ++r) k<<<grid, 128, pad>>>(out, 0);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  int clk_khz = 0;
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+  // pairs per warp per rep = kPts columns × 16·NB rows; per SMSP
+  const double pairs_per_smsp = double(grid) * 4 * kReps * kPts * 16.0 * NB / (sms * 4.0);
+  const double cycles = (ms / 3) * 1e-3 * clk_khz * 1e3;
+  cudaError_t e = cudaGetLastError();
+  std::printf("%-14s occ=%2d CTAs/SM  %8.3f ms  %6.2f cycles/64 pairs (@%d MHz attr)  %s\n", name,
+              occ, ms / 3, 64.0 * cycles / pairs_per_smsp, clk_khz / 1000, cudaGetErrorString(e));
+}
+
 template <int V, bool MUFU>
 void run(const char* name, int sms, int ctas_per_sm, float* out) {
   auto k = loop_kernel<V, MUFU>;
@@ -270,6 +390,17 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   float* out;
   cudaMalloc(&out, sizeof(float) * sms * 32 * 128);
+  std::printf("-- pass-2 accumulation on HMMA (mma.sync tf32 hi/lo), cycles per 64 pairs\n");
+  run<10, true>("row_fac", sms, 8, out);
+  run_mma<1, true>("mma_nb1", sms, 8, out);
+  run_mma<2, true>("mma_nb2", sms, 8, out);
+  run_mma<2, true>("mma_nb2_o4", sms, 4, out);
+  run_mma<4, true>("mma_nb4", sms, 4, out);
+  run_mma<4, true>("mma_nb4_o6", sms, 6, out);
+  run_mma<2, false>("mma_nb2_nm", sms, 8, out);
+  run_mma<2, true, false>("mma_nb2_nohmma", sms, 8, out);
+  run_mma<2, false, false>("mma_nb2_nm_nohm", sms, 8, out);
+  if (std::getenv("LB_MMA_ONLY")) return 0;
   std::printf("-- current kernels' loops at 8 CTAs/SM (tc_acc = 128 pairs per point-warp)\n");
   run<9, true>("col_fac", sms, 8, out);
   run<10, true>("row_fac", sms, 8, out);
