@@ -207,6 +207,10 @@ struct Session {
   EStepPlan ep;
   ColsumPlan zp, vp;
   double tau = 0.0;  // spectral truncation threshold of the basis streams (0: off)
+  bool mfused = false;            // whole M-step as one cooperative kernel (mstep_fused.cu)
+  int mfused_grid = 0;
+  DevBuf<double> zpart_fused;     // [K][grid][3]
+  DevBuf<int32_t> mfused_done;    // its last-CTA counter
   cudaGraphExec_t graph = nullptr;
   // spatial order (sorted → original index) and tile-culling buffers
   std::vector<int64_t> perm_x, perm_y;
@@ -236,10 +240,10 @@ struct Session {
   void release() {
     release_graph();
     for (auto* b : {&x0, &xt64, &xt_prev, &y64, &b2, &pt1, &col_seg, &row_seg, &ptilde_y,
-                    &var, &log2p1, &zpart, &vpart, &coef, &sig_part, &trace})
+                    &var, &log2p1, &zpart, &vpart, &coef, &sig_part, &trace, &zpart_fused})
       b->release();
     for (auto* b : {&xt4, &y4b, &resid4, &g4}) b->release();
-    for (auto* b : {&col_flags, &row_flags, &flags_count, &degenerate}) b->release();
+    for (auto* b : {&col_flags, &row_flags, &flags_count, &degenerate, &mfused_done}) b->release();
     stamps.release();
     st.release();
     for (auto* b : {&rowsum_all, &rowsum_own, &fsum_all, &fsum_own, &zfull, &sig_local, &stage})
@@ -514,6 +518,15 @@ void enqueue_iteration(fcpd_ctx* ctx, Session& s, cudaEvent_t* ev = nullptr) {
   rec(0);
   launch_estep(s.ep, eb, s.m, s.n, s.d, s.cfg.omega, st, s.stamps.p, str, ev ? ev[1] : nullptr);
   rec(2);
+  if (s.mfused) {  // one cooperative kernel; its time is booked as the Qᵀ·R phase
+    MstepFusedArgs a{b.q, b.kpad, b.k, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.tau,
+                     s.zp.trunc, s.resid4.p, s.zpart_fused.p, s.coef.p, s.g4.p, s.x0.p,
+                     s.xt64.p, s.xt_prev.p, s.xt4.p, s.ptilde_y.p, s.var.p, s.sig_part.p,
+                     s.mfused_done.p, s.m, s.d, s.cfg.early_stop, s.trace.p, st, s.stamps.p};
+    launch_mstep_fused(a, s.mfused_grid, str);
+    for (int i = 3; i <= 6; ++i) rec(i);
+    return;
+  }
   if (s.zp.trunc)
     launch_spectral_rank(b.lam, b.lam + b.k, b.k, s.cfg.lambda_reg, s.tau, st, str);
   launch_colsum(s.zp, b.q, b.kpad, s.resid4.p, s.zpart.p, st, s.stamps.p, 1, str);
@@ -611,6 +624,19 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
     s.vpart.ensure(s.vp.part_doubles());
     s.coef.ensure(3 * b.k);
     s.g4.ensure(b.k);
+    // The fused M-step pays where the streamed basis is small enough that
+    // the two passes are latency-bound and its re-read of Q hits L2: a basis
+    // ≤ 64 MB, or a truncated one over M ≤ 32k rows (FCPD_MSTEP_FUSED=0/1).
+    const double qbytes = 4.0 * static_cast<double>(m) * static_cast<double>(b.k);
+    s.mfused = qbytes <= 64.0 * (1 << 20) || (s.zp.trunc && m <= 32768);
+    if (const char* e = std::getenv("FCPD_MSTEP_FUSED")) s.mfused = std::atoi(e) != 0;
+    if (s.mfused) {
+      s.mfused_grid = mstep_fused_grid(ctx->sm_count);
+      s.zpart_fused.ensure(static_cast<size_t>(b.k) * s.mfused_grid * 3);
+      s.mfused_done.ensure(1);
+      FCPD_CUDA(cudaMemsetAsync(s.mfused_done.p, 0, sizeof(int32_t), str));
+      s.sig_part.ensure(std::max(transform_sigma_blocks(m), s.mfused_grid));
+    }
   }
 }
 
@@ -1412,8 +1438,12 @@ int32_t fcpd_kernels_per_iteration(const fcpd_ctx* ctx) {
   // tensor-core pass 2: its CUDA-core companion kernel (+ x̃ boxes and the
   // routing list when culling is off)
   if (s.ep.tc) extra += 1 + (culling ? 0 : 2);
+  if (s.dist) return 17 + extra + (s.zp.trunc ? 1 : 0);
+  // fused M-step: one kernel instead of Qᵀ·R, z-reduce, Q·g, transform, σ²
+  // (and the spectral rank)
+  if (s.mfused) return 8 + extra;
   if (s.zp.trunc) extra += 1;  // spectral rank
-  return (s.dist ? 17 : 12) + extra;
+  return 12 + extra;
 }
 
 int fcpd_register(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n,

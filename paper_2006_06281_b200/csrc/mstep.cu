@@ -529,7 +529,8 @@ __global__ void vreduce_add_kernel(const double* __restrict__ part, SkGeom g, in
 
 // Effective spectral rank: f_k = λnum_k/(λ_k + λ_reg σ²) is non-increasing
 // along the descending spectrum (λnum = λ_raw or λ, both sorted), so the
-// kept eigenpairs are a prefix; binary search for the first f_k < tau.
+// kept eigenpairs are a prefix: cta_spectral_rank (mstep.cuh) finds the
+// first f_k < tau.
 // Dropping them changes V = Q(f ⊙ z) by ≤ Σ_{dropped} f_k |z_k| |q_k| —
 // with tau = 1e-10 far below the fp32 basis rounding (≈ 2e-7‖R‖).
 __global__ void spectral_rank_kernel(const double* __restrict__ lam,
@@ -537,18 +538,8 @@ __global__ void spectral_rank_kernel(const double* __restrict__ lam,
                                      double lambda_reg, double tau, IterState* st) {
   if (!st->active) return;
   int64_t keep = k;
-  if (tau > 0.0) {
-    const double c = lambda_reg * st->sigma2;
-    int64_t lo = 0, hi = k;  // first index with f < tau lies in [lo, hi]
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) / 2;
-      const double diag = lam[mid] + c;
-      const double f = diag > 0.0 ? lam_num[mid] / diag : 1.0;
-      if (f >= tau) lo = mid + 1;
-      else hi = mid;
-    }
-    keep = lo;
-  }
+  if (tau > 0.0) keep = cta_spectral_rank(lam, lam_num, k, lambda_reg * st->sigma2, tau);
+  if (threadIdx.x != 0) return;
   keep = (keep + 3) / 4 * 4;
   st->keff = static_cast<int32_t>(min(max(keep, int64_t(4)), (k + 3) / 4 * 4));
 }
@@ -569,7 +560,7 @@ __global__ void zcoef_kernel(const double* __restrict__ part, SkGeom g, int64_t 
 
 void launch_spectral_rank(const double* lam, const double* lam_num, int64_t k, double lambda_reg,
                           double tau, IterState* st, cudaStream_t stream) {
-  spectral_rank_kernel<<<1, 1, 0, stream>>>(lam, lam_num, k, lambda_reg, tau, st);
+  spectral_rank_kernel<<<1, 512, 0, stream>>>(lam, lam_num, k, lambda_reg, tau, st);
   FCPD_LAUNCH_CHECK();
 }
 

@@ -33,6 +33,41 @@ struct ColsumPlan {
 // ctas_per_sm: resident bulk CTAs per SM the grid assumes (2 = whole GPU).
 ColsumPlan make_colsum_plan(int64_t rows, int64_t cols, int sm_count, int ctas_per_sm = 2);
 
+// Effective spectral rank by a parallel two-round search, for a whole CTA
+// (every thread gets the result; all threads must call).  The filter
+// f_k = λnum_k/(λ_k + λ_reg σ²) is non-increasing along the descending
+// spectrum, so the kept eigenpairs are the prefix before the first f_k < tau:
+// round 1 samples blockDim.x evenly spaced k, round 2 scans the bracket that
+// holds the first failing sample — two dependent loads instead of log2 K.
+__device__ __forceinline__ int64_t cta_spectral_rank(const double* lam, const double* lam_num,
+                                                     int64_t k, double c, double tau) {
+  __shared__ int first_t;
+  __shared__ long long first_i;
+  const int t = threadIdx.x, T = blockDim.x;
+  auto fails = [&](int64_t i) {
+    const double diag = lam[i] + c;
+    const double f = diag > 0.0 ? lam_num[i] / diag : 1.0;
+    return !(f >= tau);
+  };
+  auto sample = [&](int64_t j) { return j * k / T; };  // i_0 = 0 < i_1 < … (k ≥ T) or repeats
+  if (t == 0) first_t = T;
+  __syncthreads();
+  if (sample(t) < k && fails(sample(t))) atomicMin(&first_t, t);
+  __syncthreads();
+  // failing indices form a suffix [first, k): first ∈ (i_{t*−1}, i_{t*}]
+  const int ts = first_t;
+  const int64_t lo = ts > 0 ? sample(ts - 1) + 1 : 0;
+  const int64_t hi = ts < T ? sample(ts) : k;
+  if (t == 0) first_i = hi;
+  __syncthreads();
+  for (int64_t i = lo + t; i < hi; i += T)
+    if (fails(i)) atomicMin(&first_i, static_cast<long long>(i));
+  __syncthreads();
+  const int64_t keep = first_i;
+  __syncthreads();  // first_* may be reused by a later call
+  return keep;
+}
+
 // Effective spectral rank of this iteration → st->keff (multiple of 4):
 // the leading eigenpairs whose filter λnum_k/(λ_k + λ_reg σ²) ≥ tau (the
 // filter decreases along the descending spectrum); tau ≤ 0 → all K.
@@ -80,6 +115,36 @@ void launch_zsum(const ColsumPlan& p, const double* part, double* z, const IterS
 void launch_zfilter(const double* z, int64_t k, const double* lam, const double* lam_num,
                     double lambda_reg, double* coef, float4* g4, IterState* st,
                     cudaStream_t stream);
+
+// The whole M-step (z, solve/filter, V, transform, σ²) as one cooperative
+// kernel (mstep_fused.cu): single GPU, for streamed bases that stay in L2.
+struct MstepFusedArgs {
+  const float* q;   // Q row-major, M × kpad fp32
+  int64_t kpad, k;  // row stride, eigenpairs
+  const double* lam;
+  const double* lam_num;
+  double lambda_reg, tau;
+  int trunc;  // spectral truncation on (keff from tau)
+  const float4* resid4;  // R = P̃Y − X
+  double* zpart;         // [k][grid][3]
+  double* coef;          // 3 × k SoA
+  float4* g4;            // k
+  const double* x0;
+  double* xt64;
+  double* xt_prev;
+  float4* xt4;
+  const double* ptilde_y;
+  const double* var;
+  double* sig_part;  // [grid]
+  int32_t* done;     // last-CTA counter (zero before the first launch; self-resetting)
+  int64_t m;
+  int d, early_stop;
+  double* trace;
+  IterState* st;
+  uint64_t* stamps;
+};
+int mstep_fused_grid(int sm_count);
+void launch_mstep_fused(const MstepFusedArgs& args, int grid, cudaStream_t stream);
 
 // out = (x0 or 0) + Σ partials, D columns.
 void launch_vreduce_add(const ColsumPlan& p, const double* part, const double* x0, int d,

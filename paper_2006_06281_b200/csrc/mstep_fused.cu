@@ -1,0 +1,297 @@
+// mstep_fused.cu — the whole M-step of one iteration (solvers.hpp:61-73,
+// :138-155, :160-176) as ONE cooperative persistent kernel, for bases whose
+// streamed part stays in L2 (single GPU).
+//
+// The streaming path (mstep.cu) is two HBM-bound passes over Q and Qᵀ plus
+// three small kernels.  When the streamed basis is small — the truncated
+// full-rank basis of C1 (keff ≈ 150–200 of 20 000 eigenpairs: 15 MB), the
+// K = 200 basis of C2 (40 MB), C0 — those passes are latency-bound and the
+// launch chain dominates.  One kernel does all of it with grid-wide syncs:
+//   phase 0  keff (spectral truncation; every CTA evaluates the same search)
+//   phase 1  z partials: CTA c sums Q[r][k]·R_r over its row slice r ∈ [r0, r1)
+//   phase 2  z_k = Σ_c partials (fixed order), c_k = z_k/(λ_k + λ_reg σ²),
+//            g_k = λnum_k·c_k                       — one warp per k
+//   phase 3  V_r = Σ_k Q[r][k]·g_k for the same row slice (Q rows re-read
+//            from L2, not Qᵀ), x̃new = X + V, per-row σ² terms (mstep.cu)
+//   phase 4  σ² = Σ terms / (D·M), checks, trace, early stop (the last CTA
+//            to finish phase 3; no grid barrier)
+// Every sum has a fixed order: bitwise reproducible.
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "mstep.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace fcpd {
+
+namespace {
+constexpr int kFusedThreads = 512;
+constexpr int kFusedWarps = kFusedThreads / 32;
+constexpr int kFusedSmem = kFusedThreads * 12 * 8;  // ≥ 8·kFusedThreads float3 (phase 3)
+static_assert(kFusedSmem >= 8 * kFusedThreads * 12, "phase-3 partials fit");
+
+// spectral_rank_kernel (mstep.cu), as a parallel CTA search
+__device__ __forceinline__ int64_t fused_keff(const MstepFusedArgs& a) {
+  int64_t keep = a.k;
+  if (a.trunc && a.tau > 0.0)
+    keep = cta_spectral_rank(a.lam, a.lam_num, a.k, a.lambda_reg * a.st->sigma2, a.tau);
+  keep = (keep + 3) / 4 * 4;
+  return min(max(keep, int64_t(4)), (a.k + 3) / 4 * 4);
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFusedArgs a) {
+  IterState* st = a.st;
+  if (!st->active) return;  // uniform: nothing below writes `active` before the last sync
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int it = st->iter;
+  if (a.stamps && c == 0 && tid == 0) a.stamps[4 * it + 1] = globaltimer();
+
+  // ---- phase 0: effective rank
+  const int64_t keff = fused_keff(a);
+  if (c == 0 && tid == 0) st->keff = static_cast<int32_t>(keff);
+  const int64_t m = a.m;
+  const int64_t r0 = c * m / G, r1 = (c + 1) * m / G;
+  const int nq = static_cast<int>(keff / 4);  // float4 quads of the streamed columns
+
+  // phases 1 and 3 share one dynamic shared-memory buffer (kFusedSmem)
+  extern __shared__ __align__(16) unsigned char fused_smem[];
+  // ---- phase 1: z partials over the CTA's rows.  Threads = (row group, quad).
+  double* red = reinterpret_cast<double*>(fused_smem);  // [thread][12]
+  {
+    const int ng = nq >= kFusedThreads ? 1 : kFusedThreads / nq;
+    const int grp = nq >= kFusedThreads ? 0 : tid / nq;
+    for (int qb = 0; qb < nq; qb += (nq >= kFusedThreads ? kFusedThreads : nq)) {
+      const int q = qb + (nq >= kFusedThreads ? tid : tid % nq);
+      const bool on = grp < ng && q < nq;
+      double acc[12];
+#pragma unroll
+      for (int i = 0; i < 12; ++i) acc[i] = 0.0;
+      if (on) {
+        const float4* col = reinterpret_cast<const float4*>(a.q) + q;
+        const int64_t ld4 = a.kpad / 4;
+        for (int64_t r = r0 + grp; r < r1; r += 8 * ng) {  // 8 rows in flight, fp32 over 8
+          float4 qv[8], rv[8];
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            const bool in = r + w * ng < r1;  // rows past the slice contribute 0
+            qv[w] = in ? __ldg(col + (r + w * ng) * ld4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            rv[w] = in ? __ldg(a.resid4 + r + w * ng) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          float f[12];
+#pragma unroll
+          for (int i = 0; i < 12; ++i) f[i] = 0.f;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            const float qq[4] = {qv[w].x, qv[w].y, qv[w].z, qv[w].w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              f[3 * i] = __fmaf_rn(qq[i], rv[w].x, f[3 * i]);
+              f[3 * i + 1] = __fmaf_rn(qq[i], rv[w].y, f[3 * i + 1]);
+              f[3 * i + 2] = __fmaf_rn(qq[i], rv[w].z, f[3 * i + 2]);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 12; ++i) acc[i] += f[i];
+        }
+      }
+      if (ng > 1) {  // combine the row groups in group order
+        __syncthreads();
+        if (on)
+#pragma unroll
+          for (int i = 0; i < 12; ++i) red[tid * 12 + i] = acc[i];
+        __syncthreads();
+        if (tid < nq) {
+          for (int i = 0; i < 12; ++i) acc[i] = red[tid * 12 + i];
+          for (int gg = 1; gg < ng; ++gg)
+#pragma unroll
+            for (int i = 0; i < 12; ++i) acc[i] += red[(gg * nq + tid) * 12 + i];
+        }
+      }
+      if ((ng > 1 && tid < nq) || (ng == 1 && on)) {
+        const int qq = ng > 1 ? tid : q;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double* p = a.zpart + ((static_cast<int64_t>(4 * qq + i) * G + c) * 3);
+          p[0] = acc[3 * i];
+          p[1] = acc[3 * i + 1];
+          p[2] = acc[3 * i + 2];
+        }
+      }
+    }
+  }
+  grid.sync();
+
+  // ---- phase 2: reduce + solve + filter, one warp per eigenpair
+  {
+    const double sigma2 = st->sigma2;  // this iteration's E-step σ² (registration.hpp:137)
+    const int64_t gw = static_cast<int64_t>(c) * kFusedWarps + warp, nw = int64_t(G) * kFusedWarps;
+    for (int64_t k = gw; k < keff; k += nw) {
+      double z0 = 0.0, z1 = 0.0, z2 = 0.0;
+      for (int cc = lane; cc < G; cc += 32) {
+        const double* p = a.zpart + (k * G + cc) * 3;  // written by other CTAs
+        z0 += __ldcg(p);
+        z1 += __ldcg(p + 1);
+        z2 += __ldcg(p + 2);
+      }
+      z0 = warp_sum(z0);
+      z1 = warp_sum(z1);
+      z2 = warp_sum(z2);
+      if (lane) continue;
+      const double diag = a.lam[k] + a.lambda_reg * sigma2;
+      if (!(diag > 0.0)) set_error(st, kDevSolveDiag, diag);
+      const double inv = 1.0 / diag;
+      a.coef[k] = z0 * inv;
+      a.coef[a.k + k] = z1 * inv;
+      a.coef[2 * a.k + k] = z2 * inv;
+      const double f = a.lam_num[k] * inv;
+      a.g4[k] = make_float4(static_cast<float>(z0 * f), static_cast<float>(z1 * f),
+                            static_cast<float>(z2 * f), 0.f);
+    }
+    if (c == 0 && tid == 0) st->sigma2_m = sigma2;
+  }
+  grid.sync();
+
+  // ---- phase 3: V = Q g on the row slice, transform, σ² terms.  Threads =
+  // (row group, slot) as in phase 1; the CTA walks its rows in chunks of
+  // 8·ng rows: every thread has 8 row loads in flight, writes its fp32
+  // partial dot products to shared memory, then one thread per row sums the
+  // slots in order (fp64) and finalises the row (transform_sigma_kernel).
+  if (a.stamps && c == 0 && tid == 0) a.stamps[4 * it + 2] = globaltimer();
+  float3* vp = reinterpret_cast<float3*>(fused_smem);  // [row in chunk][slot]
+  __shared__ double wsum[kFusedWarps];
+  {
+    const int S = nq < kFusedThreads ? nq : kFusedThreads;  // slots
+    const int ng = kFusedThreads / S;
+    const int grp = tid / S, slot = tid % S;
+    const bool on = grp < ng;
+    const int rc = 8 * ng;  // rows per chunk
+    const int64_t ld4 = a.kpad / 4;
+    const float4* qrow = reinterpret_cast<const float4*>(a.q);
+    double term_t = 0.0;  // this thread's σ² terms (rows it finalises), in row order
+    for (int64_t cb = r0; cb < r1; cb += rc) {
+      // the finalising thread's row data, loaded ahead of the dot products
+      const int64_t ri = cb + tid;
+      const bool fin_row = tid < rc && ri < r1;
+      double o0 = 0.0, o1 = 0.0, o2 = 0.0, x00 = 0.0, x01 = 0.0, x02 = 0.0;
+      double p0 = 0.0, p1 = 0.0, p2 = 0.0, vr = 0.0;
+      if (fin_row) {
+        o0 = a.xt64[ri], o1 = a.xt64[m + ri], o2 = a.xt64[2 * m + ri];
+        x00 = a.x0[ri], x01 = a.x0[m + ri], x02 = a.x0[2 * m + ri];
+        p0 = a.ptilde_y[ri], p1 = a.ptilde_y[m + ri], p2 = a.ptilde_y[2 * m + ri];
+        vr = a.var[ri];
+      }
+      if (on) {
+        float3 f[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) f[w] = make_float3(0.f, 0.f, 0.f);
+        for (int q = slot; q < nq; q += S) {
+          float4 qv[8];
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            const int64_t r = cb + grp + int64_t(w) * ng;
+            qv[w] = r < r1 ? __ldg(qrow + r * ld4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          float4 gk[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) gk[i] = __ldcg(a.g4 + 4 * q + i);  // written in phase 2
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            const float qq[4] = {qv[w].x, qv[w].y, qv[w].z, qv[w].w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              f[w].x = __fmaf_rn(qq[i], gk[i].x, f[w].x);
+              f[w].y = __fmaf_rn(qq[i], gk[i].y, f[w].y);
+              f[w].z = __fmaf_rn(qq[i], gk[i].z, f[w].z);
+            }
+          }
+        }
+#pragma unroll
+        for (int w = 0; w < 8; ++w) vp[(grp + w * ng) * S + slot] = f[w];
+      }
+      __syncthreads();
+      if (fin_row) {
+        const int64_t i = ri;
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+        for (int j = 0; j < S; ++j) {
+          const float3 f = vp[tid * S + j];
+          v0 += f.x;
+          v1 += f.y;
+          v2 += f.z;
+        }
+        const double n0 = x00 + v0, n1 = x01 + v1, n2 = x02 + v2;
+        const double e0 = n0 - o0, e1 = n1 - o1, e2 = n2 - o2;
+        const double b0 = p0 - o0, b1 = p1 - o1, b2 = p2 - o2;
+        term_t += vr - 2.0 * (e0 * b0 + e1 * b1 + e2 * b2) + (e0 * e0 + e1 * e1 + e2 * e2);
+        if (a.xt_prev) {
+          a.xt_prev[i] = o0;
+          a.xt_prev[m + i] = o1;
+          a.xt_prev[2 * m + i] = o2;
+        }
+        a.xt64[i] = n0;
+        a.xt64[m + i] = n1;
+        a.xt64[2 * m + i] = n2;
+        a.xt4[i] = make_float4(static_cast<float>(n0), static_cast<float>(n1),
+                               static_cast<float>(n2), 0.f);
+      }
+      __syncthreads();  // vp is rewritten by the next chunk
+    }
+    const double tw = warp_sum(term_t);  // fixed xor tree
+    if (lane == 0) wsum[warp] = tw;
+    __syncthreads();
+    __shared__ int is_last;
+    if (tid == 0) {
+      double sum = 0.0;
+      for (int w = 0; w < kFusedWarps; ++w) sum += wsum[w];
+      a.sig_part[c] = sum;
+      __threadfence();
+      is_last = atomicAdd(a.done, 1) == G - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+  }
+
+  // ---- phase 4 (the last CTA to finish phase 3): σ² (sigma_final_kernel)
+  if (tid == 0) *a.done = 0;  // self-resetting for the next replay
+  double s = 0.0;
+  for (int b = tid; b < G; b += kFusedThreads) s += __ldcg(a.sig_part + b);
+  s = warp_sum(s);
+  __shared__ double fin[kFusedWarps];
+  if (lane == 0) fin[warp] = s;
+  __syncthreads();
+  if (tid != 0) return;
+  double tot = 0.0;
+  for (int w = 0; w < kFusedWarps; ++w) tot += fin[w];
+  const double val = tot / (static_cast<double>(a.d) * static_cast<double>(m));
+  if (val < -1e-8) set_error(st, kDevNegVariance, val);
+  const double next = fmax(val, kSigma2Floor);
+  if (next <= kSigma2Floor) st->sigma2_clamps += 1;
+  a.trace[it] = next;
+  const double delta = fabs(next - st->sigma2);
+  st->sigma2 = next;
+  st->iters_run = it + 1;
+  st->iter = it + 1;
+  if (a.stamps) a.stamps[4 * it + 3] = globaltimer();
+  if (a.early_stop && delta < 1e-10) st->active = 0;
+}
+
+int mstep_fused_grid(int sm_count) { return sm_count; }
+
+void launch_mstep_fused(const MstepFusedArgs& args, int grid, cudaStream_t stream) {
+  // per launch: the attribute belongs to the current device
+  FCPD_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(&mstep_fused_kernel),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem));
+  MstepFusedArgs a = args;
+  void* params[] = {&a};
+  FCPD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&mstep_fused_kernel),
+                                        dim3(grid), dim3(kFusedThreads), params, kFusedSmem,
+                                        stream));
+}
+
+}  // namespace fcpd

@@ -365,12 +365,14 @@ def test_lowrank_register_via_topk_matches_dense_basis(ctx, fc, orc, monkeypatch
 @pytest.mark.parametrize("variant,omega,m,tau", [("fast", 0.2, 2500, 0.0),
                                                  ("fast_lowrank", 0.0, 2500, 0.0),
                                                  ("fast", 0.2, 5000, 1e-10)])
-def test_distributed_engine_single_rank(ctx, fc, orc, variant, omega, m, tau):
+def test_distributed_engine_single_rank(ctx, fc, orc, monkeypatch, variant, omega, m, tau):
     """The NCCL-sharded engine path (dist.cu kernels, reduce-scatter /
     all-reduce / all-gather inside the CUDA graph) run as a one-rank group
-    reproduces the single-GPU path; the decomposition itself is checked
-    at world size 2 on CPU (tests/test_dist_gloo.py)."""
+    reproduces the single-GPU path with the same (streaming) M-step; the
+    decomposition itself is checked at world size 2 on CPU
+    (tests/test_dist_gloo.py)."""
     from paper_2006_06281_b200 import datagen
+    monkeypatch.setenv("FCPD_MSTEP_FUSED", "0")
     x, y, w = datagen.generate("c1", m=m)
     # m=5000 full rank (100 MB basis) exercises the spectrally truncated
     # streams on both paths
@@ -389,6 +391,43 @@ def test_distributed_engine_single_rank(ctx, fc, orc, variant, omega, m, tau):
     assert rel <= 1e-9, rel
     assert np.abs(got.transformed - ref.transformed).max() <= 1e-9 * bbox_diag(y)
     assert np.abs(got.coefficients - ref.coefficients).max() <= 1e-6 * np.abs(ref.coefficients).max()
+
+
+# ------------------------------------------ fused M-step (mstep_fused.cu)
+
+
+@pytest.mark.parametrize("name,m,iters", [("c0", 2000, 50), ("c1", 5000, 60),
+                                          ("c2", 12000, 40)])
+def test_fused_mstep_matches_streaming(ctx, fc, monkeypatch, name, m, iters):
+    """The cooperative one-kernel M-step against the streaming one (two basis
+    passes + reduce/filter/transform/σ² kernels): full rank (C0), truncated
+    full rank (C1, 100 MB basis), low rank (C2).  Same σ² trace and points
+    inside the parity bar, and 4 fewer kernels per iteration (5 with the
+    spectral-rank kernel)."""
+    from paper_2006_06281_b200 import datagen
+    x, y, w = datagen.generate(name, m=m)
+    cfg = datagen.config_for(w, iterations=iters)
+    monkeypatch.setenv("FCPD_MSTEP_FUSED", "0")
+    ref = ctx.register(x, y, cfg)
+    k_stream = ctx.kernels_per_iteration
+    monkeypatch.setenv("FCPD_MSTEP_FUSED", "1")
+    got = ctx.register(x, y, cfg)
+    k_fused = ctx.kernels_per_iteration
+    rel = np.abs(got.sigma2_trace / ref.sigma2_trace - 1).max()
+    pts = np.abs(got.transformed - ref.transformed).max() / bbox_diag(y)
+    cf = np.abs(got.coefficients - ref.coefficients).max() / np.abs(ref.coefficients).max()
+    print(f"{name}: σ² rel {rel:.3g}  points {pts:.3g}  coefficients {cf:.3g}  "
+          f"kernels {k_stream} → {k_fused}")
+    # both are fp32-product / fp64-sum implementations with different
+    # summation orders: agreement at the fp32 rounding level, 10× inside the
+    # 1e-5 parity bar over the whole trajectory
+    assert rel <= 1e-6, rel
+    assert pts <= 1e-7, pts
+    assert cf <= 1e-5, cf
+    assert k_fused in (k_stream - 4, k_stream - 5)
+    again = ctx.register(x, y, cfg)  # bitwise reproducible
+    assert np.array_equal(again.sigma2_trace, got.sigma2_trace)
+    assert np.array_equal(again.transformed, got.transformed)
 
 
 # ------------------------------------------------ spectral cache (§8f rank 1)
