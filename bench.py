@@ -261,13 +261,20 @@ def run_ours(args, world, rank, local):
         prof_tiles = tuple(b - a for a, b in zip(tiles0, tiles1))
     # the basis-stream kernel over the FULL basis (no spectral truncation),
     # for its HBM roofline; the basis is cached in the context
+    # (the streaming kernel even where this run used the fused M-step)
     full_phases = None
-    if prof_iters and (state.get("spectral_rank") or 0) < (x.shape[0] if w.variant == "fast"
-                                                          else fcpd.lowrank_rank(w.rank_fraction,
-                                                                                 x.shape[0])):
+    if prof_iters:
         fcfg = datagen.config_for(w, iterations=4)
         fcfg.spectral_tau = 0.0
-        ctx.session_begin(x, y, fcfg)
+        saved = os.environ.get("FCPD_MSTEP_FUSED")
+        os.environ["FCPD_MSTEP_FUSED"] = "0"
+        try:
+            ctx.session_begin(x, y, fcfg)
+        finally:
+            if saved is None:
+                del os.environ["FCPD_MSTEP_FUSED"]
+            else:
+                os.environ["FCPD_MSTEP_FUSED"] = saved
         ctx.session_run(1)
         full_phases = ctx.session_profile(3)
     sigma_last = float(state["sigma2_trace"][-1])
@@ -341,7 +348,9 @@ def run_ours(args, world, rank, local):
             # The Q products (HBM-bound): as streamed in this run (spectral
             # truncation reads only `keff` eigenvectors) and, for the kernel's
             # bandwidth, over the full basis in a short untruncated session.
-            q_ms = phases["qt_r_stream"] + phases["q_g_stream"]
+            fused = bool(state.get("mstep_fused"))
+            # fused: the whole M-step is one kernel, booked as the Qᵀ·R phase
+            q_ms = phases["qt_r_stream"] + (0.0 if fused else phases["q_g_stream"])
             traffic = None
             prof_json = os.path.join(ROOT, "profiles", "ncu_summary.json")
             if os.path.exists(prof_json):
@@ -353,14 +362,14 @@ def run_ours(args, world, rank, local):
                             "peak_source": peak_kind,
                             "kernel": "colsum_bulk (Qᵀ·R and Q·g basis streams, "
                                       "cp.async.bulk ring)",
-                            "this_run": {"bytes_per_iteration": q_bytes,
-                                         "achieved": q_bytes / (q_ms / 1e3) / 1e9,
-                                         "share_of_iteration": q_ms / it_ms}}
-            if not full_phases:  # this run streamed the full basis
-                ach = q_bytes / (q_ms / 1e3) / 1e9
-                roofline_hbm.update({"achieved": ach, "frac": ach / peaks["hbm_gbs"],
-                                     "traffic": traffic})
-            else:
+                            "this_run": {
+                                "mstep": ("mstep_fused (one cooperative kernel: rank, Qᵀ·R, "
+                                          "filter, Q·g from L2, transform, σ²)" if fused else
+                                          "streaming (colsum_bulk ×2 + reduce/transform)"),
+                                "basis_bytes_per_iteration": (q_bytes / 2 if fused else q_bytes),
+                                "ms": q_ms,
+                                "share_of_iteration": q_ms / it_ms}}
+            if full_phases:
                 fk = (k + 3) // 4 * 4
                 fb = 4.0 * (m * fk + k * mpad)
                 fms = full_phases["qt_r_stream"] + full_phases["q_g_stream"]

@@ -97,9 +97,11 @@ typedef struct fcpd_result {
   int64_t d2h_bytes;        /* device→host bytes this call copied     */
   int64_t tiles_evaluated[2]; /* E-step tile pairs computed since the
                                  session began (pass 1, pass 2); the rest
-                                 were culled (≤ 2^-50 of any total)     */
+                                 were culled (≤ 2^-32 of any total)     */
   int64_t spectral_rank;    /* eigenpairs the last iteration's basis
                                streams used (filter ≥ tau; = K untruncated) */
+  int32_t mstep_fused;      /* 1 if the session ran the one-kernel M-step */
+  int32_t reserved0;
 } fcpd_result;
 
 typedef struct fcpd_ctx fcpd_ctx;

@@ -108,7 +108,8 @@ class _Result(C.Structure):
                 ("sigma2_clamps", C.c_int64), ("timing", _Timing),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("tiles_evaluated", C.c_int64 * 2),
-                ("spectral_rank", C.c_int64)]
+                ("spectral_rank", C.c_int64),
+                ("mstep_fused", C.c_int32), ("reserved0", C.c_int32)]
 
 
 _lib = None
@@ -352,7 +353,8 @@ class Context:
                     sigma2_trace=trace[: res.iterations_run].copy(),
                     iterations_run=res.iterations_run, degenerate_rows=res.degenerate_rows,
                     tiles_evaluated=(int(res.tiles_evaluated[0]), int(res.tiles_evaluated[1])),
-                    spectral_rank=int(res.spectral_rank))
+                    spectral_rank=int(res.spectral_rank),
+                    mstep_fused=bool(res.mstep_fused))
 
     @property
     def stream_ptr(self) -> int:

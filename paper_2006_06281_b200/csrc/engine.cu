@@ -946,6 +946,7 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
   out->tiles_evaluated[0] = static_cast<int64_t>(tiles[0]);
   out->tiles_evaluated[1] = static_cast<int64_t>(tiles[1]);
   out->spectral_rank = s.zp.trunc && h.keff > 0 ? std::min<int64_t>(h.keff, b.k) : b.k;
+  out->mstep_fused = s.mfused ? 1 : 0;
   if (out->degenerate_mask)
     for (int64_t k = 0; k < m; ++k) out->degenerate_mask[px[k]] = degm[k];
   if (out->transformed) {

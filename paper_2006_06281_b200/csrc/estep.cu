@@ -203,10 +203,16 @@ __global__ void estep_prologue_kernel(IterState* st, int64_t m, int64_t n, int d
 //    large (kCentredMaxR2).
 // f32x2 packing (FADD2/FMUL2/FFMA2, sm_100): each packed op evaluates two
 // (m, n) pairs; each lane rounds like the scalar op.
-__global__ void __launch_bounds__(128)
+// NC column pairs per thread; the CTA (128/NC threads) owns the 256-column
+// block.  NC = 2 shares every staged model point's shared-memory operands
+// between two packed column pairs (fewer LDS per pair).
+template <int NC>
+__global__ void __launch_bounds__(128 / NC)
     estep_col_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4,
                      int64_t n, const IterState* __restrict__ st, WorkList wl,
                      double* __restrict__ seg, int allow_centred) {
+  constexpr int kThr = 128 / NC;  // threads
+  constexpr int kCols = 2 * NC;   // columns per thread
   if (!st->active) return;
   __shared__ float4 xa[kTile];  // centred (vx,vx,vy,vy) | diff (−x,−x,−y,−y)
   __shared__ float4 xb[kTile];  // centred (vz,vz,−|v|²,−|v|²) | diff (−z,−z,·,·)
@@ -215,17 +221,18 @@ __global__ void __launch_bounds__(128)
   const int64_t P = wl.off(wl.n_blocks) * kTile;
   const int64_t p0 = sk_start(g, G, P), p1 = sk_start(g + 1, G, P);
   if (p0 >= p1) return;
+  const int t = threadIdx.x;
   int rb = wl_block_of(wl, p0 / kTile);
   for (int64_t p = p0; p < p1;) {
     while (wl.off(rb + 1) * kTile <= p) ++rb;
     const int64_t pe = min(p1, wl.off(rb + 1) * kTile);
     __syncthreads();  // previous segment's readers of the shared box/tiles are done
     // own columns of block rb
-    const int64_t c0 = static_cast<int64_t>(rb) * kTile + 2 * threadIdx.x;
-    float4 yv[2];
+    const int64_t c0 = static_cast<int64_t>(rb) * kTile + kCols * t;
+    float4 yv[kCols];
     float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < kCols; ++h) {
       const int64_t c = c0 + h;
       yv[h] = c < n ? scale_pt(y4[c], s) : make_float4(0.f, 0.f, 0.f, 0.f);
       if (c < n) {
@@ -236,28 +243,34 @@ __global__ void __launch_bounds__(128)
     }
     const BoxCentre bc = cta_box_centre(lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]);
     const bool centred = allow_centred && bc.r2 <= kCentredMaxR2;
-    // per-thread operands: centred → 2u, −|u|²; diff → y'
-    float2 ox, oy, oz, on;
-    if (centred) {
-      float ux[2], uy[2], uz[2], q[2];
+    // per-thread operands per column pair: centred → 2u, −|u|²; diff → y'
+    float2 ox[NC], oy[NC], oz[NC], on[NC];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        ux[h] = __fsub_rn(yv[h].x, bc.c.x);
-        uy[h] = __fsub_rn(yv[h].y, bc.c.y);
-        uz[h] = __fsub_rn(yv[h].z, bc.c.z);
-        q[h] = __fmaf_rn(uz[h], uz[h], __fmaf_rn(uy[h], uy[h], __fmul_rn(ux[h], ux[h])));
+    for (int q2 = 0; q2 < NC; ++q2) {
+      if (centred) {
+        float ux[2], uy[2], uz[2], q[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float4 y = yv[2 * q2 + h];
+          ux[h] = __fsub_rn(y.x, bc.c.x);
+          uy[h] = __fsub_rn(y.y, bc.c.y);
+          uz[h] = __fsub_rn(y.z, bc.c.z);
+          q[h] = __fmaf_rn(uz[h], uz[h], __fmaf_rn(uy[h], uy[h], __fmul_rn(ux[h], ux[h])));
+        }
+        ox[q2] = make_float2(2.f * ux[0], 2.f * ux[1]);
+        oy[q2] = make_float2(2.f * uy[0], 2.f * uy[1]);
+        oz[q2] = make_float2(2.f * uz[0], 2.f * uz[1]);
+        on[q2] = make_float2(-q[0], -q[1]);
+      } else {
+        ox[q2] = make_float2(yv[2 * q2].x, yv[2 * q2 + 1].x);
+        oy[q2] = make_float2(yv[2 * q2].y, yv[2 * q2 + 1].y);
+        oz[q2] = make_float2(yv[2 * q2].z, yv[2 * q2 + 1].z);
+        on[q2] = make_float2(0.f, 0.f);
       }
-      ox = make_float2(2.f * ux[0], 2.f * ux[1]);
-      oy = make_float2(2.f * uy[0], 2.f * uy[1]);
-      oz = make_float2(2.f * uz[0], 2.f * uz[1]);
-      on = make_float2(-q[0], -q[1]);
-    } else {
-      ox = make_float2(yv[0].x, yv[1].x);
-      oy = make_float2(yv[0].y, yv[1].y);
-      oz = make_float2(yv[0].z, yv[1].z);
-      on = make_float2(0.f, 0.f);
     }
-    double d0 = 0.0, d1 = 0.0;
+    double d[kCols];
+#pragma unroll
+    for (int h = 0; h < kCols; ++h) d[h] = 0.0;
     for (int64_t q = p; q < pe;) {
       const int64_t k = q / kTile - wl.off(rb);
       const int a = static_cast<int>(q % kTile);
@@ -268,7 +281,7 @@ __global__ void __launch_bounds__(128)
       if (cnt == 0) continue;  // uniform
       const int cnt8 = (cnt + 7) & ~7;
       __syncthreads();
-      for (int i = threadIdx.x; i < cnt8; i += 128) {
+      for (int i = t; i < cnt8; i += kThr) {
         if (centred) {
           float4 v;
           if (i < cnt) {
@@ -289,20 +302,25 @@ __global__ void __launch_bounds__(128)
         }
       }
       __syncthreads();
-      float2 f = make_float2(0.f, 0.f);
+      float2 f[NC];
+#pragma unroll
+      for (int q2 = 0; q2 < NC; ++q2) f[q2] = make_float2(0.f, 0.f);
       if (centred) {
         for (int j = 0; j < cnt8; j += 8) {
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const float4 va = xa[j + u];
             const float4 vb = xb[j + u];
-            // 2u·v − |v|² = |u|² − t: the column's own 2^{−|u|²} is factored
-            // out of its sum and applied once in fp64 (|u|² ≤ R² ≤ 16, so the
-            // shifted terms stay in range)
-            float2 e = __ffma2_rn(ox, make_float2(va.x, va.y), make_float2(vb.z, vb.w));
-            e = __ffma2_rn(oy, make_float2(va.z, va.w), e);
-            e = __ffma2_rn(oz, make_float2(vb.x, vb.y), e);
-            f = __fadd2_rn(f, ex2x2(e));
+#pragma unroll
+            for (int q2 = 0; q2 < NC; ++q2) {
+              // 2u·v − |v|² = |u|² − t: the column's own 2^{−|u|²} is
+              // factored out of its sum and applied once in fp64 (|u|² ≤ R²
+              // ≤ 16, so the shifted terms stay in range)
+              float2 e = __ffma2_rn(ox[q2], make_float2(va.x, va.y), make_float2(vb.z, vb.w));
+              e = __ffma2_rn(oy[q2], make_float2(va.z, va.w), e);
+              e = __ffma2_rn(oz[q2], make_float2(vb.x, vb.y), e);
+              f[q2] = __fadd2_rn(f[q2], ex2x2(e));
+            }
           }
         }
       } else {
@@ -311,26 +329,35 @@ __global__ void __launch_bounds__(128)
           for (int u = 0; u < 8; ++u) {
             const float4 va = xa[j + u];
             const float4 vb = xb[j + u];
-            const float2 dx = __fadd2_rn(ox, make_float2(va.x, va.y));
-            const float2 dy = __fadd2_rn(oy, make_float2(va.z, va.w));
-            const float2 dz = __fadd2_rn(oz, make_float2(vb.x, vb.y));
-            float2 t = __fmul2_rn(dx, dx);
-            t = __ffma2_rn(dy, dy, t);
-            t = __ffma2_rn(dz, dz, t);
-            f = __fadd2_rn(f, ex2x2(make_float2(-t.x, -t.y)));
+#pragma unroll
+            for (int q2 = 0; q2 < NC; ++q2) {
+              const float2 dx = __fadd2_rn(ox[q2], make_float2(va.x, va.y));
+              const float2 dy = __fadd2_rn(oy[q2], make_float2(va.z, va.w));
+              const float2 dz = __fadd2_rn(oz[q2], make_float2(vb.x, vb.y));
+              float2 tt = __fmul2_rn(dx, dx);
+              tt = __ffma2_rn(dy, dy, tt);
+              tt = __ffma2_rn(dz, dz, tt);
+              f[q2] = __fadd2_rn(f[q2], ex2x2(make_float2(-tt.x, -tt.y)));
+            }
           }
         }
       }
-      d0 += static_cast<double>(f.x);
-      d1 += static_cast<double>(f.y);
+#pragma unroll
+      for (int q2 = 0; q2 < NC; ++q2) {
+        d[2 * q2] += static_cast<double>(f[q2].x);
+        d[2 * q2 + 1] += static_cast<double>(f[q2].y);
+      }
     }
     if (centred) {  // undo the factored-out 2^{|u|²}
-      d0 *= exp2(static_cast<double>(on.x));
-      d1 *= exp2(static_cast<double>(on.y));
+#pragma unroll
+      for (int q2 = 0; q2 < NC; ++q2) {
+        d[2 * q2] *= exp2(static_cast<double>(on[q2].x));
+        d[2 * q2 + 1] *= exp2(static_cast<double>(on[q2].y));
+      }
     }
     double* out = seg + (g + rb) * kTile;
-    out[2 * threadIdx.x] = d0;
-    out[2 * threadIdx.x + 1] = d1;
+#pragma unroll
+    for (int h = 0; h < kCols; ++h) out[kCols * t + h] = d[h];
     p = pe;
   }
 }
@@ -1269,7 +1296,11 @@ EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
   EStepPlan p;
   if (const char* e = std::getenv("FCPD_ESTEP_FORM")) p.centred = std::strcmp(e, "diff") != 0;
   int occ_col = 0, occ_row = 0;
-  FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_col, estep_col_kernel, 128, 0));
+  if (const char* e = std::getenv("FCPD_COL_PAIRS")) p.col_pairs = std::atoi(e) == 1 ? 1 : 2;
+  if (p.col_pairs == 2)
+    FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_col, estep_col_kernel<2>, 64, 0));
+  else
+    FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_col, estep_col_kernel<1>, 128, 0));
   if (const char* e = std::getenv("FCPD_ROW_PAIRS")) p.row_pairs = std::atoi(e) == 1 ? 1 : 2;
   if (p.row_pairs == 2)
     FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_row, estep_row_kernel<2>, 64, 0));
@@ -1344,8 +1375,12 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
         cu, b.xt4, m, b.y4b, n, b.wl1.tiles, b.wl1.offset, p.col_blocks, b.wl1.done, st);
     FCPD_LAUNCH_CHECK();
   }
-  estep_col_kernel<<<p.col_grid, 128, 0, stream>>>(b.xt4, m, b.y4b, n, st, wl, b.col_seg,
-                                                   p.centred);
+  if (p.col_pairs == 2)
+    estep_col_kernel<2><<<p.col_grid, 64, 0, stream>>>(b.xt4, m, b.y4b, n, st, wl, b.col_seg,
+                                                       p.centred);
+  else
+    estep_col_kernel<1><<<p.col_grid, 128, 0, stream>>>(b.xt4, m, b.y4b, n, st, wl, b.col_seg,
+                                                        p.centred);
   FCPD_LAUNCH_CHECK();
   estep_col_combine_kernel<<<ceil_div(n * kCombineLanes, 256), 256, 0, stream>>>(
       b.col_seg, wl, p.col_grid, m, n, b.y4b, b.b2, b.pt1, b.col_flags, b.flags_count, st);

@@ -15,7 +15,7 @@ for w in ${WORKLOADS:-c0 c2 c3 c4}; do
 done
 CMD="python bench.py --steps 5 --warmup 3 --no-cpu --e2e-calls 0"
 timeout 600 $CMD > $O/plain.log 2>&1 && \
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"estep|colsum|zreduce|transform_sigma|sigma_final|list|bbox|bminmax" -c 80 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"estep|colsum|zreduce|transform_sigma|sigma_final|list|bbox|bminmax|mstep_fused|spectral_rank" -c 80 --csv \
    --log-file $O/launches.csv $CMD > $O/ncu_launch.log 2>&1
 echo "ncu exit $?" >> $O/ncu_launch.log
 tail -2 $O/pytest_gpu.txt; cat $O/smoke.txt | tail -1
