@@ -75,6 +75,37 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+// Programmatic dependent launch (PDL).  Hot-path kernels are launched with
+// launch_pdl: the next kernel in the stream (graph) may be scheduled while
+// its predecessor drains, hiding the launch gap.  Such a kernel must call
+// griddep_wait() before touching anything its predecessor writes — every
+// kernel launched this way does so as its first statement (a no-op when it
+// was launched normally).
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // let the next kernel be scheduled now: its CTAs become resident as ours
+  // retire and block in their own wait until this grid has completed
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();  // FCPD_PDL=0 → ordinary launches (engine.cu)
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  FCPD_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 __device__ __forceinline__ void set_error(IterState* st, int code, double value) {
   if (atomicCAS(&st->err_code, 0, code) == 0) {
     st->err_iter = st->iter;

@@ -278,6 +278,14 @@ struct fcpd_ctx {
 };
 
 namespace fcpd {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FCPD_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 namespace {
 
 int fail(fcpd_ctx* ctx, int code, const std::string& msg) {

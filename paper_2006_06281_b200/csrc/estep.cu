@@ -171,6 +171,7 @@ __device__ __forceinline__ float2 ex2x2(float2 v) {
 // registration.hpp:122), coordinate scale, outlier constant (:61-66).
 __global__ void estep_prologue_kernel(IterState* st, int64_t m, int64_t n, int d,
                                       double omega, int32_t* flags_count, uint64_t* stamps) {
+  griddep_wait();
   if (!st->active) return;
   if (stamps) stamps[4 * st->iter + 0] = globaltimer();
   flags_count[0] = flags_count[1] = 0;  // column and row fallback lists
@@ -211,6 +212,7 @@ __global__ void __launch_bounds__(128 / NC)
     estep_col_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4,
                      int64_t n, const IterState* __restrict__ st, WorkList wl,
                      double* __restrict__ seg, int allow_centred) {
+  griddep_wait();
   constexpr int kThr = 128 / NC;  // threads
   constexpr int kCols = 2 * NC;   // columns per thread
   if (!st->active) return;
@@ -396,6 +398,7 @@ __global__ void estep_col_combine_kernel(const double* __restrict__ seg, WorkLis
                                          int32_t* __restrict__ flag_list,
                                          int32_t* __restrict__ flag_count,
                                          const IterState* __restrict__ st) {
+  griddep_wait();
   if (!st->active) return;
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t col = gid / kCombineLanes;
@@ -429,6 +432,7 @@ __global__ void estep_col_fallback_kernel(const float4* __restrict__ xt4, int64_
                                           const int32_t* __restrict__ flag_list,
                                           const int32_t* __restrict__ flag_count,
                                           const IterState* __restrict__ st) {
+  griddep_wait();
   if (!st->active) return;
   const int count = *flag_count;
   const int lane = threadIdx.x & 31;
@@ -481,6 +485,7 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
     estep_row_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4b,
                      int64_t n, const IterState* __restrict__ st, WorkList wl,
                      double* __restrict__ seg /* [slot][5][256] */, int allow_centred) {
+  griddep_wait();
   constexpr int kThr = 128 / NP;   // threads
   constexpr int kRows = 2 * NP;    // rows per thread
   if (!st->active) return;
@@ -695,6 +700,7 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
 __global__ void tile_bbox_kernel(const float4* __restrict__ p, int64_t count,
                                  float4* __restrict__ lo, float4* __restrict__ hi,
                                  const IterState* __restrict__ st) {
+  griddep_wait();
   if (st && !st->active) return;
   __shared__ float red[6][8];
   const int64_t i = static_cast<int64_t>(blockIdx.x) * kTile + threadIdx.x;
@@ -735,6 +741,7 @@ __global__ void tile_bbox_kernel(const float4* __restrict__ p, int64_t count,
 // per scene tile: (min b_n, max b_n) after pass 1
 __global__ void tile_bminmax_kernel(const float4* __restrict__ y4b, int64_t n,
                                     float2* __restrict__ out, const IterState* __restrict__ st) {
+  griddep_wait();
   if (!st->active) return;
   __shared__ float red[2][8];
   const int64_t i = static_cast<int64_t>(blockIdx.x) * kTile + threadIdx.x;
@@ -953,6 +960,7 @@ __global__ void __launch_bounds__(kListThreads)
                     const float4* __restrict__ y4, int64_t n, int32_t* __restrict__ tiles,
                     int32_t* __restrict__ offset, int n_blocks, int32_t* __restrict__ done,
                     const IterState* __restrict__ st) {
+  griddep_wait();
   if (!st->active) return;
   __shared__ float4 pa[kProbeTiles * kTile / 2], pb[kProbeTiles * kTile / 2];
   __shared__ unsigned long long sh64[kListThreads / 32];
@@ -1033,7 +1041,8 @@ __global__ void __launch_bounds__(kListThreads)
                                 });
   if (threadIdx.x == 0) {
     offset[b + 1] = count;
-    if (np > 0 && cull.probe_paid1) cull.probe_paid1[b] = (kept_box - count) * kProbePayShare >= kept_box;
+    if (np > 0 && cull.probe_paid1)
+      cull.probe_paid1[b] = (kept_box - count) * kProbePayShare >= kept_box;
   }
   last_cta_scan(offset, nullptr, n_blocks, done, cull.counters);
 }
@@ -1053,6 +1062,7 @@ __global__ void __launch_bounds__(kListThreads)
                     const float4* __restrict__ y4b, int64_t n, int32_t* __restrict__ tiles,
                     int32_t* __restrict__ offset, int32_t* __restrict__ offset_cc, int n_blocks,
                     int32_t* __restrict__ done, const IterState* __restrict__ st) {
+  griddep_wait();
   if (!st->active) return;
   __shared__ float4 pa[kProbeTiles * kTile / 2], pb[kProbeTiles * kTile / 2];
   __shared__ unsigned long long sh64[kListThreads / 32];
@@ -1143,7 +1153,8 @@ __global__ void __launch_bounds__(kListThreads)
       offset_cc[b + 1] = to_tc ? 0 : count;
     }
     offset[b + 1] = to_tc ? count : 0;
-    if (np > 0 && cull.probe_paid2) cull.probe_paid2[b] = (kept_box - count) * kProbePayShare >= kept_box;
+    if (np > 0 && cull.probe_paid2)
+      cull.probe_paid2[b] = (kept_box - count) * kProbePayShare >= kept_box;
   }
   last_cta_scan(offset, offset_cc, n_blocks, done,
                 cull.enabled && cull.counters ? cull.counters + 1 : nullptr);
@@ -1211,6 +1222,7 @@ __global__ void estep_row_combine_kernel(SegSrc sa, SegSrc sb, int64_t m, int64_
                                          const double* __restrict__ xt64, RowOut out, YStats ys,
                                          int32_t* __restrict__ flag_list,
                                          int32_t* __restrict__ flag_count, IterState* st) {
+  griddep_wait();
   if (!st->active) return;
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t row = gid / kCombineLanes;
@@ -1230,6 +1242,7 @@ __global__ void estep_row_combine_kernel(SegSrc sa, SegSrc sb, int64_t m, int64_
 // distributed: AoS row sums [m_pad][5] of the local scene shard
 __global__ void row_seg_sum_kernel(SegSrc sa, SegSrc sb, int64_t m, int64_t m_pad,
                                    double* __restrict__ out, const IterState* __restrict__ st) {
+  griddep_wait();
   if (!st->active) return;
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t row = gid / kCombineLanes;
@@ -1249,6 +1262,7 @@ __global__ void estep_row_fallback_kernel(const float4* __restrict__ xt4, int64_
                                           const int32_t* __restrict__ flag_list,
                                           const int32_t* __restrict__ flag_count,
                                           IterState* st) {
+  griddep_wait();
   if (!st->active) return;
   const int count = *flag_count;
   const int lane = threadIdx.x & 31;
@@ -1296,6 +1310,10 @@ EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
   EStepPlan p;
   if (const char* e = std::getenv("FCPD_ESTEP_FORM")) p.centred = std::strcmp(e, "diff") != 0;
   int occ_col = 0, occ_row = 0;
+  // two column pairs per thread pay on large passes (fewer shared-memory
+  // loads per pair); small ones (C0: 64 tile pairs) are latency-bound and
+  // prefer more, lighter CTAs
+  p.col_pairs = ceil_div(m, kTile) * ceil_div(n, kTile) >= 1024 ? 2 : 1;
   if (const char* e = std::getenv("FCPD_COL_PAIRS")) p.col_pairs = std::atoi(e) == 1 ? 1 : 2;
   if (p.col_pairs == 2)
     FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_col, estep_col_kernel<2>, 64, 0));
@@ -1352,13 +1370,15 @@ void pass2_sources(const EStepPlan& p, const EStepBuffers& b, int64_t n, SegSrc&
 
 void launch_estep_prologue(IterState* st, int64_t m, int64_t n_global, int d, double omega,
                            int32_t* flags_count, uint64_t* stamps, cudaStream_t stream) {
-  estep_prologue_kernel<<<1, 1, 0, stream>>>(st, m, n_global, d, omega, flags_count, stamps);
+  launch_pdl(estep_prologue_kernel, dim3(1), dim3(1), 0, stream, st, m, n_global, d, omega,
+             flags_count, stamps);
   FCPD_LAUNCH_CHECK();
 }
 
 void launch_tile_bbox(const float4* pts, int64_t count, float4* lo, float4* hi,
                       const IterState* st, cudaStream_t stream) {
-  tile_bbox_kernel<<<ceil_div(count, kTile), kTile, 0, stream>>>(pts, count, lo, hi, st);
+  launch_pdl(tile_bbox_kernel, dim3(ceil_div(count, kTile)), dim3(kTile), 0, stream, pts, count, lo,
+             hi, st);
   FCPD_LAUNCH_CHECK();
 }
 
@@ -1371,25 +1391,26 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
   const WorkList wl = pass1_list(p, b, m);
   if (cu.enabled) {
     launch_tile_bbox(b.xt4, m, b.cullw.xlo, b.cullw.xhi, st, stream);
-    col_list_kernel<<<p.col_blocks, kListThreads, 0, stream>>>(
-        cu, b.xt4, m, b.y4b, n, b.wl1.tiles, b.wl1.offset, p.col_blocks, b.wl1.done, st);
+    launch_pdl(col_list_kernel, dim3(p.col_blocks), dim3(kListThreads), 0, stream, cu, b.xt4, m,
+               b.y4b, n, b.wl1.tiles, b.wl1.offset, p.col_blocks, b.wl1.done, st);
     FCPD_LAUNCH_CHECK();
   }
   if (p.col_pairs == 2)
-    estep_col_kernel<2><<<p.col_grid, 64, 0, stream>>>(b.xt4, m, b.y4b, n, st, wl, b.col_seg,
-                                                       p.centred);
+    launch_pdl(estep_col_kernel<2>, dim3(p.col_grid), dim3(64), 0, stream, b.xt4, m, b.y4b, n, st,
+               wl, b.col_seg, p.centred);
   else
-    estep_col_kernel<1><<<p.col_grid, 128, 0, stream>>>(b.xt4, m, b.y4b, n, st, wl, b.col_seg,
-                                                        p.centred);
+    launch_pdl(estep_col_kernel<1>, dim3(p.col_grid), dim3(128), 0, stream, b.xt4, m, b.y4b, n, st,
+               wl, b.col_seg, p.centred);
   FCPD_LAUNCH_CHECK();
-  estep_col_combine_kernel<<<ceil_div(n * kCombineLanes, 256), 256, 0, stream>>>(
-      b.col_seg, wl, p.col_grid, m, n, b.y4b, b.b2, b.pt1, b.col_flags, b.flags_count, st);
+  launch_pdl(estep_col_combine_kernel, dim3(ceil_div(n * kCombineLanes, 256)), dim3(256), 0, stream,
+             b.col_seg, wl, p.col_grid, m, n, b.y4b, b.b2, b.pt1, b.col_flags, b.flags_count, st);
   FCPD_LAUNCH_CHECK();
-  estep_col_fallback_kernel<<<148, 256, 0, stream>>>(b.xt4, m, b.y4b, b.b2, b.pt1, b.col_flags,
-                                                     b.flags_count, st);
+  launch_pdl(estep_col_fallback_kernel, dim3(148), dim3(256), 0, stream, b.xt4, m, b.y4b, b.b2,
+             b.pt1, b.col_flags, b.flags_count, st);
   FCPD_LAUNCH_CHECK();
   if (cu.enabled) {
-    tile_bminmax_kernel<<<ceil_div(n, kTile), kTile, 0, stream>>>(b.y4b, n, b.cullw.bminmax, st);
+    launch_pdl(tile_bminmax_kernel, dim3(ceil_div(n, kTile)), dim3(kTile), 0, stream, b.y4b, n,
+               b.cullw.bminmax, st);
     FCPD_LAUNCH_CHECK();
   }
 }
@@ -1397,11 +1418,11 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
 void launch_row_cc(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
                    IterState* st, const WorkList& wl, double* seg, cudaStream_t stream) {
   if (p.row_pairs == 2)
-    estep_row_kernel<2><<<p.row_grid, 64, 0, stream>>>(b.xt4, m, b.y4b, n, st, wl, seg,
-                                                       p.centred);
+    launch_pdl(estep_row_kernel<2>, dim3(p.row_grid), dim3(64), 0, stream, b.xt4, m, b.y4b, n, st,
+               wl, seg, p.centred);
   else
-    estep_row_kernel<1><<<p.row_grid, 128, 0, stream>>>(b.xt4, m, b.y4b, n, st, wl, seg,
-                                                        p.centred);
+    launch_pdl(estep_row_kernel<1>, dim3(p.row_grid), dim3(128), 0, stream, b.xt4, m, b.y4b, n, st,
+               wl, seg, p.centred);
 }
 
 void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int64_t m,
@@ -1410,9 +1431,9 @@ void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int6
   if (cu.lists) {
     if (!cu.enabled)  // x̃ tile boxes for the routing (pass 1 made them when culling)
       launch_tile_bbox(b.xt4, m, b.cullw.xlo, b.cullw.xhi, st, stream);
-    row_list_kernel<<<p.row_blocks, kListThreads, 0, stream>>>(
-        cu, b.xt4, m, b.y4b, n, b.wl2.tiles, b.wl2.offset, p.tc ? b.wl2.offset_cc : nullptr,
-        p.row_blocks, b.wl2.done, st);
+    launch_pdl(row_list_kernel, dim3(p.row_blocks), dim3(kListThreads), 0, stream, cu, b.xt4, m,
+               b.y4b, n, b.wl2.tiles, b.wl2.offset, p.tc ? b.wl2.offset_cc : nullptr, p.row_blocks,
+               b.wl2.done, st);
     FCPD_LAUNCH_CHECK();
   }
   SegSrc a, c;
@@ -1433,11 +1454,11 @@ void launch_estep_pass2(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
   pass2_sources(p, b, n, a, c);
   int32_t* list = b.row_flags;
   int32_t* count = b.flags_count + 1;
-  estep_row_combine_kernel<<<ceil_div(m * kCombineLanes, 256), 256, 0, stream>>>(
-      a, c, m, n, b.xt64, b.out, b.ystats, list, count, st);
+  launch_pdl(estep_row_combine_kernel, dim3(ceil_div(m * kCombineLanes, 256)), dim3(256), 0, stream,
+             a, c, m, n, b.xt64, b.out, b.ystats, list, count, st);
   FCPD_LAUNCH_CHECK();
-  estep_row_fallback_kernel<<<148, 256, 0, stream>>>(b.xt4, m, b.y4b, n, b.xt64, b.out,
-                                                     b.ystats, list, count, st);
+  launch_pdl(estep_row_fallback_kernel, dim3(148), dim3(256), 0, stream, b.xt4, m, b.y4b, n, b.xt64,
+             b.out, b.ystats, list, count, st);
   FCPD_LAUNCH_CHECK();
 }
 
@@ -1445,15 +1466,16 @@ void launch_row_seg_sum(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
                         int64_t m_pad, double* out, const IterState* st, cudaStream_t stream) {
   SegSrc a, c;
   pass2_sources(p, b, n, a, c);
-  row_seg_sum_kernel<<<ceil_div(m_pad * kCombineLanes, 256), 256, 0, stream>>>(a, c, m, m_pad,
-                                                                              out, st);
+  launch_pdl(row_seg_sum_kernel, dim3(ceil_div(m_pad * kCombineLanes, 256)), dim3(256), 0, stream,
+             a, c, m, m_pad, out, st);
   FCPD_LAUNCH_CHECK();
 }
 
 void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n, int d,
                   double omega, IterState* st, uint64_t* stamps, cudaStream_t stream,
                   cudaEvent_t mid) {
-  estep_prologue_kernel<<<1, 1, 0, stream>>>(st, m, n, d, omega, b.flags_count, stamps);
+  launch_pdl(estep_prologue_kernel, dim3(1), dim3(1), 0, stream, st, m, n, d, omega, b.flags_count,
+             stamps);
   FCPD_LAUNCH_CHECK();
   launch_estep_pass1(p, b, m, n, st, stream);
   if (mid) FCPD_CUDA(cudaEventRecord(mid, stream));

@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(kColsumThreads)
     colsum_kernel(const float* __restrict__ A, int64_t lda, const float4* __restrict__ v,
                   SkGeom g, double* __restrict__ part, const IterState* __restrict__ st,
                   uint64_t* stamps, int stamp_slot) {
+  griddep_wait();
   if (st && !st->active) return;
   if (stamps && blockIdx.x == 0 && threadIdx.x == 0)
     stamps[4 * st->iter + stamp_slot] = globaltimer();
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(kBulkThreads, kBulkCtasPerSm)
     colsum_bulk_kernel(const float* __restrict__ A, int64_t lda, const float4* __restrict__ v,
                        SkGeom g, double* __restrict__ part, const IterState* __restrict__ st,
                        uint64_t* stamps, int stamp_slot) {
+  griddep_wait();
   if (st && !st->active) return;
   if (stamps && blockIdx.x == 0 && threadIdx.x == 0)
     stamps[4 * st->iter + stamp_slot] = globaltimer();
@@ -413,6 +415,7 @@ __global__ void zreduce_filter_kernel(const double* __restrict__ part, SkGeom g,
                                       const double* __restrict__ lam_num, double lambda_reg,
                                       double* __restrict__ coef, float4* __restrict__ g4,
                                       IterState* st) {
+  griddep_wait();
   if (!st->active) return;
   g = sk_eff(g, st);
   // one warp per column, grid-stride over the K columns
@@ -449,6 +452,7 @@ __global__ void __launch_bounds__(256)
                            double* __restrict__ xt_prev, float4* __restrict__ xt4,
                            const double* __restrict__ ptilde_y, const double* __restrict__ var,
                            double* __restrict__ sig_part, IterState* st, uint64_t* stamps) {
+  griddep_wait();
   // m = row stride of the SoA arrays; rows ≥ m_valid (shard padding) are inert
   if (!st->active) return;
   if (stamps && blockIdx.x == 0 && threadIdx.x == 0) stamps[4 * st->iter + 2] = globaltimer();
@@ -492,6 +496,7 @@ __global__ void __launch_bounds__(256)
 __global__ void sigma_final_kernel(const double* __restrict__ sig_part, int blocks, int64_t m,
                                    int d, int early_stop, double* __restrict__ trace,
                                    IterState* st, uint64_t* stamps) {
+  griddep_wait();
   if (!st->active) return;
   __shared__ double red[32];
   double s = 0.0;
@@ -536,6 +541,7 @@ __global__ void vreduce_add_kernel(const double* __restrict__ part, SkGeom g, in
 __global__ void spectral_rank_kernel(const double* __restrict__ lam,
                                      const double* __restrict__ lam_num, int64_t k,
                                      double lambda_reg, double tau, IterState* st) {
+  griddep_wait();
   if (!st->active) return;
   int64_t keep = k;
   if (tau > 0.0) keep = cta_spectral_rank(lam, lam_num, k, lambda_reg * st->sigma2, tau);
@@ -560,7 +566,8 @@ __global__ void zcoef_kernel(const double* __restrict__ part, SkGeom g, int64_t 
 
 void launch_spectral_rank(const double* lam, const double* lam_num, int64_t k, double lambda_reg,
                           double tau, IterState* st, cudaStream_t stream) {
-  spectral_rank_kernel<<<1, 512, 0, stream>>>(lam, lam_num, k, lambda_reg, tau, st);
+  launch_pdl(spectral_rank_kernel, dim3(1), dim3(512), 0, stream, lam, lam_num, k, lambda_reg, tau,
+             st);
   FCPD_LAUNCH_CHECK();
 }
 
@@ -610,11 +617,11 @@ void launch_colsum(const ColsumPlan& p, const float* A, int64_t lda, const float
                    double* part, const IterState* st, uint64_t* stamps, int stamp_slot,
                    cudaStream_t stream) {
   if (p.bulk)
-    colsum_bulk_kernel<<<p.grid, kBulkThreads, kBulkSmem, stream>>>(A, lda, v, geom(p), part, st,
-                                                                     stamps, stamp_slot);
+    launch_pdl(colsum_bulk_kernel, dim3(p.grid), dim3(kBulkThreads), kBulkSmem, stream, A, lda, v,
+               geom(p), part, st, stamps, stamp_slot);
   else
-    colsum_kernel<<<p.grid, kColsumThreads, 0, stream>>>(A, lda, v, geom(p), part, st, stamps,
-                                                         stamp_slot);
+    launch_pdl(colsum_kernel, dim3(p.grid), dim3(kColsumThreads), 0, stream, A, lda, v, geom(p),
+               part, st, stamps, stamp_slot);
   FCPD_LAUNCH_CHECK();
 }
 
@@ -622,8 +629,8 @@ void launch_zreduce(const ColsumPlan& p, const double* part, const double* lam,
                     const double* lam_num, double lambda_reg, double* coef, float4* g4,
                     IterState* st, cudaStream_t stream) {
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(p.cols * 32, 256), 148 * 2));
-  zreduce_filter_kernel<<<blocks, 256, 0, stream>>>(part, geom(p), p.cols, lam, lam_num,
-                                                    lambda_reg, coef, g4, st);
+  launch_pdl(zreduce_filter_kernel, dim3(blocks), dim3(256), 0, stream, part, geom(p), p.cols, lam,
+             lam_num, lambda_reg, coef, g4, st);
   FCPD_LAUNCH_CHECK();
 }
 
@@ -646,8 +653,8 @@ int launch_transform_rows(const ColsumPlan& p, const double* part, int64_t m_val
                           IterState* st, uint64_t* stamps, cudaStream_t stream) {
   const int64_t m = p.cols;
   const int nb = transform_sigma_blocks(m);
-  transform_sigma_kernel<<<nb, 256, 0, stream>>>(part, geom(p), m, m_valid, x0, xt64, xt_prev,
-                                                 xt4, ptilde_y, var, sig_part, st, stamps);
+  launch_pdl(transform_sigma_kernel, dim3(nb), dim3(256), 0, stream, part, geom(p), m, m_valid, x0,
+             xt64, xt_prev, xt4, ptilde_y, var, sig_part, st, stamps);
   FCPD_LAUNCH_CHECK();
   return nb;
 }
@@ -655,8 +662,8 @@ int launch_transform_rows(const ColsumPlan& p, const double* part, int64_t m_val
 void launch_sigma_final(const double* sig_part, int blocks, int64_t m_global, int d,
                         int early_stop, double* trace, IterState* st, uint64_t* stamps,
                         cudaStream_t stream) {
-  sigma_final_kernel<<<1, 256, 0, stream>>>(sig_part, blocks, m_global, d, early_stop, trace, st,
-                                            stamps);
+  launch_pdl(sigma_final_kernel, dim3(1), dim3(256), 0, stream, sig_part, blocks, m_global, d,
+             early_stop, trace, st, stamps);
   FCPD_LAUNCH_CHECK();
 }
 

@@ -44,6 +44,7 @@ __device__ __forceinline__ int64_t fused_keff(const MstepFusedArgs& a) {
 }  // namespace
 
 __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFusedArgs a) {
+  griddep_wait();
   IterState* st = a.st;
   if (!st->active) return;  // uniform: nothing below writes `active` before the last sync
   cg::grid_group grid = cg::this_grid();
