@@ -971,6 +971,16 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
     tc += 1e-9 * static_cast<double>(st4[1] - st4[0]);
     ti += 1e-9 * static_cast<double>(st4[2] - st4[1]);
   }
+  if (std::getenv("FCPD_HOST_TIMING") && run > 1) {  // device phase split (diagnostic)
+    double t3 = 0.0, gap = 0.0;
+    for (int it = 0; it < run; ++it) t3 += 1e-9 * static_cast<double>(stamps[4 * it + 3] - stamps[4 * it + 2]);
+    for (int it = 0; it + 1 < run; ++it)
+      gap += 1e-9 * static_cast<double>(stamps[4 * (it + 1)] - stamps[4 * it + 3]);
+    std::fprintf(stderr,
+                 "[fcpd] per iteration: E-step %.2f us, M-step to V %.2f us, transform+σ² %.2f us, "
+                 "gap to next %.2f us\n",
+                 1e6 * tc / run, 1e6 * ti / run, 1e6 * t3 / run, 1e6 * gap / (run - 1));
+  }
   fcpd_timing& t = out->timing;
   t.t_c = tc;
   t.t_eig = s.t_eig;

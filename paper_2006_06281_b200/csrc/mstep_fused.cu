@@ -30,8 +30,15 @@ namespace fcpd {
 namespace {
 constexpr int kFusedThreads = 512;
 constexpr int kFusedWarps = kFusedThreads / 32;
-constexpr int kFusedSmem = kFusedThreads * 12 * 8;  // ≥ 8·kFusedThreads float3 (phase 3)
-static_assert(kFusedSmem >= 8 * kFusedThreads * 12, "phase-3 partials fit");
+constexpr int kRedLanes = 4;  // phase 3: threads per row in the slot reduction
+// phase 1: 12 doubles per thread; phase 3: 3 floats × S slots × (8·ng + 1)
+// padded rows, S·ng ≤ kFusedThreads
+constexpr int kFusedSmem = 3 * 9 * kFusedThreads * 4;
+static_assert(kFusedSmem >= kFusedThreads * 12 * 8, "phase-1 partials fit");
+// Phase 3 reads g (K float4) from shared memory: every CTA reading the same
+// few L2 lines directly is a hot spot (measured: +10 µs at C1).
+constexpr int kG4Max = 2048;
+constexpr int kFusedDynSmem = kFusedSmem + kG4Max * 16;
 
 // spectral_rank_kernel (mstep.cu), as a parallel CTA search
 __device__ __forceinline__ int64_t fused_keff(const MstepFusedArgs& a) {
@@ -53,6 +60,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
   const int it = st->iter;
   if (a.stamps && c == 0 && tid == 0) a.stamps[4 * it + 1] = globaltimer();
 
+  // phases 1 and 3 share the first kFusedSmem bytes; g (phase 3) follows
+  extern __shared__ __align__(16) unsigned char fused_smem[];
   // ---- phase 0: effective rank
   const int64_t keff = fused_keff(a);
   if (c == 0 && tid == 0) st->keff = static_cast<int32_t>(keff);
@@ -60,10 +69,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
   const int64_t r0 = c * m / G, r1 = (c + 1) * m / G;
   const int nq = static_cast<int>(keff / 4);  // float4 quads of the streamed columns
 
-  // phases 1 and 3 share one dynamic shared-memory buffer (kFusedSmem)
-  extern __shared__ __align__(16) unsigned char fused_smem[];
   // ---- phase 1: z partials over the CTA's rows.  Threads = (row group, quad).
-  double* red = reinterpret_cast<double*>(fused_smem);  // [thread][12]
+  double* red = reinterpret_cast<double*>(fused_smem);  // [12][thread]
   {
     const int ng = nq >= kFusedThreads ? 1 : kFusedThreads / nq;
     const int grp = nq >= kFusedThreads ? 0 : tid / nq;
@@ -84,6 +91,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
             qv[w] = in ? __ldg(col + (r + w * ng) * ld4) : make_float4(0.f, 0.f, 0.f, 0.f);
             rv[w] = in ? __ldg(a.resid4 + r + w * ng) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
+
           float f[12];
 #pragma unroll
           for (int i = 0; i < 12; ++i) f[i] = 0.f;
@@ -105,13 +113,13 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
         __syncthreads();
         if (on)
 #pragma unroll
-          for (int i = 0; i < 12; ++i) red[tid * 12 + i] = acc[i];
+          for (int i = 0; i < 12; ++i) red[i * kFusedThreads + tid] = acc[i];
         __syncthreads();
         if (tid < nq) {
-          for (int i = 0; i < 12; ++i) acc[i] = red[tid * 12 + i];
+          for (int i = 0; i < 12; ++i) acc[i] = red[i * kFusedThreads + tid];
           for (int gg = 1; gg < ng; ++gg)
 #pragma unroll
-            for (int i = 0; i < 12; ++i) acc[i] += red[(gg * nq + tid) * 12 + i];
+            for (int i = 0; i < 12; ++i) acc[i] += red[i * kFusedThreads + gg * nq + tid];
         }
       }
       if ((ng > 1 && tid < nq) || (ng == 1 && on)) {
@@ -163,8 +171,18 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
   // 8·ng rows: every thread has 8 row loads in flight, writes its fp32
   // partial dot products to shared memory, then one thread per row sums the
   // slots in order (fp64) and finalises the row (transform_sigma_kernel).
+  // [component][slot][row in chunk], rows padded to an odd stride: the
+  // per-row reduction reads consecutive words across threads
+  float* vp = reinterpret_cast<float*>(fused_smem);
   if (a.stamps && c == 0 && tid == 0) a.stamps[4 * it + 2] = globaltimer();
-  float3* vp = reinterpret_cast<float3*>(fused_smem);  // [row in chunk][slot]
+  // g in shared memory as [i][quad] (i = column within the quad): one L2 read
+  // per CTA, conflict-free reads across consecutive quads
+  float4* g4s = reinterpret_cast<float4*>(fused_smem + kFusedSmem);
+  const bool use_g4s = keff <= kG4Max;
+  if (use_g4s) {
+    for (int k = tid; k < keff; k += kFusedThreads) g4s[(k & 3) * nq + (k >> 2)] = __ldcg(a.g4 + k);
+    __syncthreads();
+  }
   __shared__ double wsum[kFusedWarps];
   {
     const int S = nq < kFusedThreads ? nq : kFusedThreads;  // slots
@@ -172,21 +190,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
     const int grp = tid / S, slot = tid % S;
     const bool on = grp < ng;
     const int rc = 8 * ng;  // rows per chunk
+    const int rcp = rc | 1;  // padded row stride of the partials
     const int64_t ld4 = a.kpad / 4;
     const float4* qrow = reinterpret_cast<const float4*>(a.q);
     double term_t = 0.0;  // this thread's σ² terms (rows it finalises), in row order
     for (int64_t cb = r0; cb < r1; cb += rc) {
-      // the finalising thread's row data, loaded ahead of the dot products
-      const int64_t ri = cb + tid;
-      const bool fin_row = tid < rc && ri < r1;
-      double o0 = 0.0, o1 = 0.0, o2 = 0.0, x00 = 0.0, x01 = 0.0, x02 = 0.0;
-      double p0 = 0.0, p1 = 0.0, p2 = 0.0, vr = 0.0;
-      if (fin_row) {
-        o0 = a.xt64[ri], o1 = a.xt64[m + ri], o2 = a.xt64[2 * m + ri];
-        x00 = a.x0[ri], x01 = a.x0[m + ri], x02 = a.x0[2 * m + ri];
-        p0 = a.ptilde_y[ri], p1 = a.ptilde_y[m + ri], p2 = a.ptilde_y[2 * m + ri];
-        vr = a.var[ri];
-      }
       if (on) {
         float3 f[8];
 #pragma unroll
@@ -200,7 +208,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
           }
           float4 gk[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) gk[i] = __ldcg(a.g4 + 4 * q + i);  // written in phase 2
+          for (int i = 0; i < 4; ++i)  // written in phase 2
+            gk[i] = use_g4s ? g4s[i * nq + q] : __ldcg(a.g4 + 4 * q + i);
 #pragma unroll
           for (int w = 0; w < 8; ++w) {
             const float qq[4] = {qv[w].x, qv[w].y, qv[w].z, qv[w].w};
@@ -213,18 +222,45 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
           }
         }
 #pragma unroll
-        for (int w = 0; w < 8; ++w) vp[(grp + w * ng) * S + slot] = f[w];
+        for (int w = 0; w < 8; ++w) {
+          float* v = vp + slot * rcp + grp + w * ng;
+          v[0] = f[w].x;
+          v[S * rcp] = f[w].y;
+          v[2 * S * rcp] = f[w].z;
+        }
       }
       __syncthreads();
-      if (fin_row) {
-        const int64_t i = ri;
-        double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-        for (int j = 0; j < S; ++j) {
-          const float3 f = vp[tid * S + j];
-          v0 += f.x;
-          v1 += f.y;
-          v2 += f.z;
+      // kRedLanes threads per row sum interleaved slots (fp64), combined by
+      // a fixed xor tree; the group's first lane finalises the row
+      constexpr int kRowsPerPass = kFusedThreads / kRedLanes;
+      for (int pass = 0; pass * kRowsPerPass < rc; ++pass) {  // uniform trip count
+        const int rr = pass * kRowsPerPass + tid / kRedLanes;
+        const int64_t i = cb + rr;
+        const bool live = rr < rc && i < r1;
+        const int sub = tid % kRedLanes;
+        double o0 = 0.0, o1 = 0.0, o2 = 0.0, x00 = 0.0, x01 = 0.0, x02 = 0.0;
+        double p0 = 0.0, p1 = 0.0, p2 = 0.0, vr = 0.0;
+        if (live && sub == 0) {  // row data, in flight during the reduction
+          o0 = a.xt64[i], o1 = a.xt64[m + i], o2 = a.xt64[2 * m + i];
+          x00 = a.x0[i], x01 = a.x0[m + i], x02 = a.x0[2 * m + i];
+          p0 = a.ptilde_y[i], p1 = a.ptilde_y[m + i], p2 = a.ptilde_y[2 * m + i];
+          vr = a.var[i];
         }
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+        if (live)
+          for (int j = sub; j < S; j += kRedLanes) {
+            const float* v = vp + j * rcp + rr;
+            v0 += v[0];
+            v1 += v[S * rcp];
+            v2 += v[2 * S * rcp];
+          }
+#pragma unroll
+        for (int o = 1; o < kRedLanes; o <<= 1) {
+          v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+          v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+          v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+        }
+        if (!live || sub != 0) continue;
         const double n0 = x00 + v0, n1 = x01 + v1, n2 = x02 + v2;
         const double e0 = n0 - o0, e1 = n1 - o1, e2 = n2 - o2;
         const double b0 = p0 - o0, b1 = p1 - o1, b2 = p2 - o2;
@@ -287,11 +323,11 @@ int mstep_fused_grid(int sm_count) { return sm_count; }
 void launch_mstep_fused(const MstepFusedArgs& args, int grid, cudaStream_t stream) {
   // per launch: the attribute belongs to the current device
   FCPD_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(&mstep_fused_kernel),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem));
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedDynSmem));
   MstepFusedArgs a = args;
   void* params[] = {&a};
   FCPD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&mstep_fused_kernel),
-                                        dim3(grid), dim3(kFusedThreads), params, kFusedSmem,
+                                        dim3(grid), dim3(kFusedThreads), params, kFusedDynSmem,
                                         stream));
 }
 
