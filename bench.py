@@ -118,6 +118,21 @@ class Watchdog:
         self._t.cancel()
 
 
+def estep_traffic():
+    """DRAM bytes per launch of the two E-step kernels (col + row) from the
+    committed ncu --set full summary, or None."""
+    try:
+        ks = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))["kernels"]
+        per = {}
+        for k in ks:
+            name = k["kernel"].replace("void ", "").split("<")[0]
+            if name in ("estep_col_kernel", "estep_row_kernel"):
+                per[name] = k["dram_read_B"] + k["dram_write_B"]
+        return sum(per.values()) if len(per) == 2 else None
+    except Exception:
+        return None
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -333,7 +348,8 @@ def run_ours(args, world, rank, local):
             evaluated_s = m * n * (f1 + f2) / 2 / (e_ms / 1e3)
             roofline = {"bound": "sfu+fp32", "achieved": evaluated_s / 1e9,
                         "peak": hz / ((f1 * c1 + f2 * c2) / ((f1 + f2) / 2)) / 1e9,
-                        "unit": "Gpairs/s", "frac": t_bound / (e_ms / 1e3), "traffic": None,
+                        "unit": "Gpairs/s", "frac": t_bound / (e_ms / 1e3),
+                        "traffic": estep_traffic(),
                         "kernel": "estep_col_kernel + estep_row_kernel (fused non-materialising "
                                   "E-step, both passes with their list/combine kernels)",
                         "share_of_iteration": e_ms / it_ms,
@@ -344,7 +360,8 @@ def run_ours(args, world, rank, local):
                                 "(12 lane-ops/pair at 128/clk/SM), over the pairs of the "
                                 "tile pairs not culled (evaluated_frac per pass); sampled "
                                 "SM clock; phase times include the geometry/combine/"
-                                "fallback kernels; memory traffic is negligible"}
+                                "fallback kernels; memory traffic is negligible (`traffic` = ncu DRAM "
+                                "bytes of one col + one row launch)"}
             # The Q products (HBM-bound): as streamed in this run (spectral
             # truncation reads only `keff` eigenvectors) and, for the kernel's
             # bandwidth, over the full basis in a short untruncated session.
