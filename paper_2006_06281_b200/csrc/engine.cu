@@ -265,6 +265,13 @@ struct Session {
 }  // namespace fcpd
 
 struct fcpd_ctx {
+  // last spatial order of each point set, keyed on its normalised content
+  // (repeated calls on the same clouds skip the k-d partition)
+  struct SortCache {
+    uint64_t hash = 0;
+    int64_t count = -1;
+    std::vector<int64_t> perm;
+  } sort_x, sort_y;
   int device = 0;
   int sm_count = 148;
   cudaStream_t stream = nullptr;
@@ -690,7 +697,8 @@ void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall);
 // consecutive tiles near each other.  The order depends only on the point
 // set, is deterministic (ties by index), and is undone on every output.
 namespace {
-void kd_partition(const std::vector<double>& soa, int64_t cnt, int64_t* idx, int64_t len) {
+void kd_partition(const std::vector<double>& soa, int64_t cnt, int64_t* idx, int64_t len,
+                  int par_depth = 2) {
   constexpr int64_t kLeaf = 256;
   while (len > kLeaf) {
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -709,7 +717,15 @@ void kd_partition(const std::vector<double>& soa, int64_t cnt, int64_t* idx, int
     std::nth_element(idx, idx + left, idx + len, [key](int64_t a, int64_t b) {
       return key[a] < key[b] || (key[a] == key[b] && a < b);
     });
-    kd_partition(soa, cnt, idx, left);
+    if (par_depth > 0 && len >= (int64_t(1) << 15)) {  // halves on separate threads
+      std::thread t([&soa, cnt, idx, left, par_depth] {
+        kd_partition(soa, cnt, idx, left, par_depth - 1);
+      });
+      kd_partition(soa, cnt, idx + left, len - left, par_depth - 1);
+      t.join();
+      return;
+    }
+    kd_partition(soa, cnt, idx, left, 0);
     idx += left;
     len -= left;
   }
@@ -725,6 +741,25 @@ std::vector<int64_t> spatial_sort(std::vector<double>& soa, int64_t cnt) {
   for (int c = 0; c < 3; ++c)
     for (int64_t k = 0; k < cnt; ++k) out[c * cnt + k] = soa[c * cnt + perm[k]];
   soa.swap(out);
+  return perm;
+}
+
+// spatial_sort through a content-keyed cache: a hit applies the cached
+// permutation (the same deterministic order the partition would produce).
+template <typename Cache>
+std::vector<int64_t> spatial_sort_cached(std::vector<double>& soa, int64_t cnt, Cache& c) {
+  const uint64_t h = fnv1a(soa.data(), sizeof(double) * soa.size());
+  if (c.count == cnt && c.hash == h && static_cast<int64_t>(c.perm.size()) == cnt) {
+    std::vector<double> out(soa.size());
+    for (int d = 0; d < 3; ++d)
+      for (int64_t k = 0; k < cnt; ++k) out[d * cnt + k] = soa[d * cnt + c.perm[k]];
+    soa.swap(out);
+    return c.perm;
+  }
+  std::vector<int64_t> perm = spatial_sort(soa, cnt);
+  c.hash = h;
+  c.count = cnt;
+  c.perm = perm;
   return perm;
 }
 
@@ -790,8 +825,8 @@ void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, i
   // internal order: spatially sorted model and scene (undone on output); the
   // two sorts are independent
   {
-    std::thread tx([&] { s.perm_x = spatial_sort(xs, m); });
-    s.perm_y = spatial_sort(ys, n);
+    std::thread tx([&] { s.perm_x = spatial_sort_cached(xs, m, ctx->sort_x); });
+    s.perm_y = spatial_sort_cached(ys, n, ctx->sort_y);
     tx.join();
   }
   stamp("spatial_sort");
@@ -1127,8 +1162,8 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
   }
   // internal spatial order: the full model (identical on all ranks) and the
   // local scene shard are spatially sorted; row shards are spatial slabs
-  s.perm_x = spatial_sort(xs, m);
-  s.perm_y = spatial_sort(ys, n);
+  s.perm_x = spatial_sort_cached(xs, m, ctx->sort_x);
+  s.perm_y = spatial_sort_cached(ys, n, ctx->sort_y);
   // spectral basis (computed redundantly per rank; each keeps its row shard)
   s.x0.ensure(3 * m);
   FCPD_CUDA(cudaMemcpyAsync(s.x0.p, xs.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, str));
