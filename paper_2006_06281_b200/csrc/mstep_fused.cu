@@ -37,7 +37,7 @@ constexpr int kFusedSmem = 3 * 9 * kFusedThreads * 4;
 static_assert(kFusedSmem >= kFusedThreads * 12 * 8, "phase-1 partials fit");
 // Phase 3 reads g (K float4) from shared memory: every CTA reading the same
 // few L2 lines directly is a hot spot (measured: +10 µs at C1).
-constexpr int kG4Max = 2048;
+constexpr int kG4Max = 8192;  // 128 KB: every fused-path basis up to K = 8192
 constexpr int kFusedDynSmem = kFusedSmem + kG4Max * 16;
 
 // spectral_rank_kernel (mstep.cu), as a parallel CTA search
