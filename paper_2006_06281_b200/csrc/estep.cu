@@ -211,7 +211,7 @@ template <int NC>
 __global__ void __launch_bounds__(128 / NC)
     estep_col_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4,
                      int64_t n, const IterState* __restrict__ st, WorkList wl,
-                     double* __restrict__ seg, int allow_centred) {
+                     double* __restrict__ seg, float centred_max_r2) {
   griddep_wait();
   constexpr int kThr = 128 / NC;  // threads
   constexpr int kCols = 2 * NC;   // columns per thread
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(128 / NC)
       }
     }
     const BoxCentre bc = cta_box_centre(lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]);
-    const bool centred = allow_centred && bc.r2 <= kCentredMaxR2;
+    const bool centred = bc.r2 <= centred_max_r2;  // < 0 → difference form only
     // per-thread operands per column pair: centred → 2u, −|u|²; diff → y'
     float2 ox[NC], oy[NC], oz[NC], on[NC];
 #pragma unroll
@@ -484,7 +484,7 @@ template <int NP>
 __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
     estep_row_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4b,
                      int64_t n, const IterState* __restrict__ st, WorkList wl,
-                     double* __restrict__ seg /* [slot][5][256] */, int allow_centred) {
+                     double* __restrict__ seg /* [slot][5][256] */, float centred_max_r2) {
   griddep_wait();
   constexpr int kThr = 128 / NP;   // threads
   constexpr int kRows = 2 * NP;    // rows per thread
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
       }
     }
     const BoxCentre bc = cta_box_centre(lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]);
-    const bool centred = allow_centred && bc.r2 <= kCentredMaxR2;
+    const bool centred = bc.r2 <= centred_max_r2;  // < 0 → difference form only
     // per-thread operands per row pair: centred → 2v (and v, |v|² for the
     // conversion); diff → −x'
     float v[kRows][4];
@@ -1309,6 +1309,9 @@ __global__ void estep_row_fallback_kernel(const float4* __restrict__ xt4, int64_
 EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
   EStepPlan p;
   if (const char* e = std::getenv("FCPD_ESTEP_FORM")) p.centred = std::strcmp(e, "diff") != 0;
+  p.centred_max_r2 = p.centred ? kCentredMaxR2 : -1.f;
+  if (const char* e = std::getenv("FCPD_CENTRED_MAX_R2"))  // precision/speed study
+    p.centred_max_r2 = p.centred ? static_cast<float>(std::atof(e)) : -1.f;
   int occ_col = 0, occ_row = 0;
   // two column pairs per thread pay on large passes (fewer shared-memory
   // loads per pair); small ones (C0: 64 tile pairs) are latency-bound and
@@ -1397,10 +1400,10 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
   }
   if (p.col_pairs == 2)
     launch_pdl(estep_col_kernel<2>, dim3(p.col_grid), dim3(64), 0, stream, b.xt4, m, b.y4b, n, st,
-               wl, b.col_seg, p.centred);
+               wl, b.col_seg, p.centred_max_r2);
   else
     launch_pdl(estep_col_kernel<1>, dim3(p.col_grid), dim3(128), 0, stream, b.xt4, m, b.y4b, n, st,
-               wl, b.col_seg, p.centred);
+               wl, b.col_seg, p.centred_max_r2);
   FCPD_LAUNCH_CHECK();
   launch_pdl(estep_col_combine_kernel, dim3(ceil_div(n * kCombineLanes, 256)), dim3(256), 0, stream,
              b.col_seg, wl, p.col_grid, m, n, b.y4b, b.b2, b.pt1, b.col_flags, b.flags_count, st);
@@ -1419,10 +1422,10 @@ void launch_row_cc(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t
                    IterState* st, const WorkList& wl, double* seg, cudaStream_t stream) {
   if (p.row_pairs == 2)
     launch_pdl(estep_row_kernel<2>, dim3(p.row_grid), dim3(64), 0, stream, b.xt4, m, b.y4b, n, st,
-               wl, seg, p.centred);
+               wl, seg, p.centred_max_r2);
   else
     launch_pdl(estep_row_kernel<1>, dim3(p.row_grid), dim3(128), 0, stream, b.xt4, m, b.y4b, n, st,
-               wl, seg, p.centred);
+               wl, seg, p.centred_max_r2);
 }
 
 void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int64_t m,

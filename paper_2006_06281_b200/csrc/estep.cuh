@@ -61,6 +61,7 @@ constexpr float kCentredMaxR2 = 16.f;
 
 struct EStepPlan {
   int centred = 1;  // tile-centred pair form where exact enough; FCPD_ESTEP_FORM=diff → off
+  float centred_max_r2 = kCentredMaxR2;  // per-segment guard (< 0: difference form only)
   int tc = 0;       // pass 2 on tcgen05 (estep_tc.cu) for blocks within kCentredMaxR2
   int row_pairs = 2;  // CUDA-core pass 2: packed row pairs per thread (FCPD_ROW_PAIRS=1 → 1)
   int col_pairs = 2;  // pass 1: packed column pairs per thread (FCPD_COL_PAIRS=1 → 1)
