@@ -635,4 +635,64 @@ inline std::vector<BenchRecord> load_bench_csv(const std::string& path) {
   return records;
 }
 
+// Log-log chart of t_iter against M, one path per variant, as an SVG string
+// (the reference's svg::bench_plot, svg.hpp:81-133): deterministic output,
+// failed cells and non-positive values skipped, an empty chart shell when
+// nothing is left.
+inline std::string bench_plot(const std::vector<BenchRecord>& records) {
+  constexpr double kW = 480, kH = 360, kLeft = 60, kRight = 20, kTop = 20, kBottom = 50;
+  static const char* kColors[] = {"#1f77b4", "#d62728", "#2ca02c", "#9467bd", "#ff7f0e",
+                                  "#8c564b"};
+  const auto num = [](double v) {
+    char b[32];
+    std::snprintf(b, sizeof b, "%.2f", v);
+    return std::string(b);
+  };
+  std::map<std::string, std::vector<std::pair<double, double>>> series;
+  double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+  for (const BenchRecord& r : records) {
+    if (r.failed || r.m <= 0 || !(r.timing.t_iter > 0.0)) continue;
+    const double x = std::log10(static_cast<double>(r.m)), y = std::log10(r.timing.t_iter);
+    series[to_string(r.variant)].emplace_back(x, y);
+    x0 = std::min(x0, x), x1 = std::max(x1, x);
+    y0 = std::min(y0, y), y1 = std::max(y1, y);
+  }
+  // data → pixel along one axis (a degenerate range maps to the middle)
+  const auto axis = [](double v, double lo, double hi, double p0, double p1) {
+    return hi > lo ? p0 + (v - lo) / (hi - lo) * (p1 - p0) : 0.5 * (p0 + p1);
+  };
+  std::string out = "<svg xmlns=\"http://www.w3.org/2000/svg\" width=\"" + num(kW) +
+                    "\" height=\"" + num(kH) + "\">\n";
+  out += "<rect x=\"" + num(kLeft) + "\" y=\"" + num(kTop) + "\" width=\"" +
+         num(kW - kLeft - kRight) + "\" height=\"" + num(kH - kTop - kBottom) +
+         "\" fill=\"none\" stroke=\"#000000\"/>\n";
+  out += "<text x=\"" + num(kW / 2) + "\" y=\"" + num(kH - 10) +
+         "\" text-anchor=\"middle\" font-size=\"14\">M (log scale)</text>\n";
+  out += "<text x=\"15\" y=\"" + num(kH / 2) +
+         "\" text-anchor=\"middle\" font-size=\"14\" transform=\"rotate(-90 15 " + num(kH / 2) +
+         ")\">t_iter seconds (log scale)</text>\n";
+  int k = 0;
+  for (auto& [name, pts] : series) {
+    std::sort(pts.begin(), pts.end());
+    std::string d;
+    for (size_t i = 0; i < pts.size(); ++i)
+      d += (i ? " L " : "M ") + num(axis(pts[i].first, x0, x1, kLeft, kW - kRight)) + " " +
+           num(axis(pts[i].second, y0, y1, kH - kBottom, kTop));
+    const char* col = kColors[k % 6];
+    ++k;
+    out += "<path d=\"" + d + "\" fill=\"none\" stroke=\"" + col + "\" stroke-width=\"2\"/>\n";
+    out += "<text x=\"" + num(kW - kRight - 5) + "\" y=\"" + num(kTop + 15.0 * k) +
+           "\" text-anchor=\"end\" font-size=\"12\" fill=\"" + col + "\">" + name + "</text>\n";
+  }
+  out += "</svg>\n";
+  return out;
+}
+
+inline void write_text_file(const std::string& content, const std::string& path) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw IoError("cannot write file: " + path);
+  out << content;
+  if (!out) throw IoError("write failed: " + path);
+}
+
 }  // namespace fastcpd

@@ -7,7 +7,8 @@
 // λ=10, 100 iterations, variant fast, rank fraction 0.1, seed 0).
 // --svg writes a plain scatter overlay of the first two coordinates
 // (registered model over scene).  `bench` sweeps sizes × variants in the
-// reference's CSV schema.  Not provided: degrade / plot.
+// reference's CSV schema (+ its t_iter chart); `plot` re-renders a CSV.
+// Not provided: degrade.
 //
 //   fcpd register MODEL SCENE [--omega W] [--beta B] [--lambda L] [--iters N]
 //        [--variant fast|fast-lowrank] [--rank-fraction F] [--seed S]
@@ -37,8 +38,9 @@ int usage(const char* prog, int code) {
                "          [--no-normalize] [--swap] [--early-stop] [--out FILE]\n"
                "          [--report FILE] [--svg FILE] [--device D]\n"
                "       %s bench [SOURCE | --synthetic] --sizes M1,M2,... [--variants fast,...]\n"
-               "          [--iters N] [--seed S] [--csv FILE] [--device D]\n",
-               prog, prog);
+               "          [--iters N] [--seed S] [--csv FILE] [--svg FILE] [--device D]\n"
+               "       %s plot BENCH_CSV [--out FILE]\n",
+               prog, prog, prog);
   return code;
 }
 
@@ -142,7 +144,8 @@ int cmd_register(const std::vector<std::string>& args) {
 int cmd_bench(const std::vector<std::string>& args) {
   std::vector<std::string> pos;
   fc::RegistrationConfig cfg;
-  std::string sizes_arg, variants_arg = "fast,fast-lowrank", csv_path = "bench.csv";
+  std::string sizes_arg, variants_arg = "fast,fast-lowrank", csv_path = "bench.csv",
+              svg_path = "bench.svg";
   bool synthetic = false;
   for (size_t i = 0; i < args.size(); ++i) {
     const std::string& a = args[i];
@@ -159,6 +162,7 @@ int cmd_bench(const std::vector<std::string>& args) {
     else if (a == "--lambda") cfg.lambda_reg = to_double(a, value());
     else if (a == "--rank-fraction") cfg.rank_fraction = to_double(a, value());
     else if (a == "--csv") csv_path = value();
+    else if (a == "--svg") svg_path = value();
     else if (a == "--synthetic") synthetic = true;
     else if (a == "--device") cfg.device = static_cast<int>(to_long(a, value()));
     else if (!a.empty() && a[0] == '-') throw fc::ParameterError("unknown option: " + a);
@@ -193,10 +197,35 @@ int cmd_bench(const std::vector<std::string>& args) {
   }
   const auto records = fc::run_benchmark(source, sizes, variants, cfg, cfg.seed);
   fc::write_bench_csv(records, csv_path);
+  fc::write_text_file(fc::bench_plot(records), svg_path);
   for (const auto& r : records)
     std::printf("M=%lld %s t_iter=%.6f t_total=%.6f rmse=%.6g%s\n", static_cast<long long>(r.m),
                 fc::to_string(r.variant), r.timing.t_iter, r.timing.t_total, r.rmse,
                 r.failed ? " FAILED" : "");
+  return 0;
+}
+
+// `fcpd plot CSV [--out FILE]` (proj/tools/fcpd.cpp:184-189): re-render a
+// bench CSV as the t_iter-vs-M chart.
+int cmd_plot(const std::vector<std::string>& args) {
+  std::string csv_path, out_path = "plot.svg";
+  for (size_t i = 0; i < args.size(); ++i) {
+    const std::string& a = args[i];
+    if (a == "--out") {
+      if (i + 1 >= args.size()) throw fc::ParameterError("--out: missing value");
+      out_path = args[++i];
+    } else if (!a.empty() && a[0] == '-') {
+      throw fc::ParameterError("unknown option: " + a);
+    } else if (csv_path.empty()) {
+      csv_path = a;
+    } else {
+      throw fc::ParameterError("plot: expected one CSV file");
+    }
+  }
+  if (csv_path.empty()) throw fc::ParameterError("plot: expected a bench CSV file");
+  const auto records = fc::load_bench_csv(csv_path);
+  fc::write_text_file(fc::bench_plot(records), out_path);
+  std::printf("wrote %s (%zu records)\n", out_path.c_str(), records.size());
   return 0;
 }
 
@@ -210,13 +239,14 @@ int main(int argc, char** argv) {
     std::printf("%s\n", fcpd_version());
     return 0;
   }
-  if (cmd != "register" && cmd != "bench") {
+  if (cmd != "register" && cmd != "bench" && cmd != "plot") {
     std::fprintf(stderr, "%s: unknown or unsupported subcommand '%s' (this build provides "
-                         "'register' and 'bench')\n", argv[0], cmd.c_str());
+                         "'register', 'bench' and 'plot')\n", argv[0], cmd.c_str());
     return 2;
   }
   try {
     const std::vector<std::string> rest(argv + 2, argv + argc);
+    if (cmd == "plot") return cmd_plot(rest);
     return cmd == "bench" ? cmd_bench(rest) : cmd_register(rest);
   } catch (const fc::Error& e) {
     std::fprintf(stderr, "error: %s\n", e.what());

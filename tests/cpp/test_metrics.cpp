@@ -1,6 +1,6 @@
 // Benchmark-harness helpers of the drop-in header (rmse, subsample,
-// random_affine, make_bench_pair, the bench CSV), restating the host-only
-// cases of the reference's proj/tests/test_metrics.cpp:12-109.  No GPU:
+// random_affine, make_bench_pair, the bench CSV, bench_plot), restating the
+// host-only cases of the reference's proj/tests/test_metrics.cpp:12-131.  No GPU:
 // BenchRecords are built by hand instead of through run_benchmark.
 #include <cmath>
 #include <cstdio>
@@ -173,6 +173,36 @@ int main(int argc, char** argv) {
     CHECK(throws_as<ParseError>([&] { load_bench_csv(dir + "/fcpd_bad2.csv"); }));
     CHECK(throws_as<IoError>([&] { load_bench_csv("/nonexistent/dir/b.csv"); }));
     CHECK(throws_as<IoError>([&] { write_bench_csv(recs, "/nonexistent/dir/b.csv"); }));
+  }
+
+  // bench_plot: deterministic, one path per variant with data, labelled axes,
+  // an empty shell without data (test_metrics.cpp:111-131)
+  {
+    std::vector<BenchRecord> recs;
+    const SolverVariant vs[3] = {SolverVariant::fast, SolverVariant::fast_lowrank,
+                                 SolverVariant::cpd};
+    for (int v = 0; v < 3; ++v)
+      for (Index m : {30, 50, 80}) {
+        BenchRecord r;
+        r.m = r.n = m;
+        r.variant = vs[v];
+        r.timing.t_iter = 1e-3 * m * (v + 1);
+        r.failed = (v == 2);  // the device path records cpd as failed cells
+        recs.push_back(r);
+      }
+    const std::string a = bench_plot(recs), b = bench_plot(recs);
+    CHECK(a == b);
+    size_t paths = 0;
+    for (size_t pos = a.find("<path d=\"M "); pos != std::string::npos;
+         pos = a.find("<path d=\"M ", pos + 1))
+      ++paths;
+    CHECK(paths == 2);
+    CHECK(a.find("M (log scale)") != std::string::npos);
+    CHECK(a.find("seconds") != std::string::npos);
+    CHECK(a.rfind("<svg", 0) == 0 && a.find("</svg>") != std::string::npos);
+    const std::string e = bench_plot({});
+    CHECK(e.find("<svg") != std::string::npos && e.find("<path d=\"M ") == std::string::npos);
+    CHECK(throws_as<IoError>([&] { write_text_file(a, "/nonexistent/dir/p.svg"); }));
   }
 
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "OK", g_fail);

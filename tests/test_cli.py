@@ -64,6 +64,32 @@ def test_cli_usage_and_errors(tmp_path):
     assert r.returncode != 0 and "unknown solver variant" in r.stderr
 
 
+def test_cli_plot_from_bench_csv(tmp_path):
+    """tests/test_cli.cpp:118-126: `plot` renders a bench CSV as a
+    deterministic SVG and rejects a file that is not a bench CSV (host only)."""
+    exe = build()
+    csv = tmp_path / "bench.csv"
+    rows = ["M,N,variant,t_c,t_eig,t_iter,t_f,t_o,t_total,rmse,iterations"]
+    for m, v, ti in [(40, "fast", 0.01), (60, "fast", 0.02), (40, "fast_lowrank", 0.012),
+                     (60, "fast_lowrank", 0.03), (40, "cpd", 0.0)]:
+        err = -1.0 if v == "cpd" else 1e-4
+        rows.append(f"{m},{m},{v},0.001000,0.002000,{ti:.6f},{0.002 + ti:.6f},0.000100,"
+                    f"{0.0031 + ti:.6f},{err},2")
+    csv.write_text("\n".join(rows) + "\n")
+    outs = []
+    for k in range(2):
+        svg = tmp_path / f"plot{k}.svg"
+        r = subprocess.run([exe, "plot", str(csv), "--out", str(svg)], capture_output=True,
+                           text=True, timeout=60)
+        assert r.returncode == 0, r.stderr
+        outs.append(svg.read_text())
+    assert outs[0] == outs[1] and outs[0].count('<path d="M ') == 2
+    bad = tmp_path / "bad.csv"
+    bad.write_text("1 2 3\n")
+    r = subprocess.run([exe, "plot", str(bad)], capture_output=True, text=True, timeout=60)
+    assert r.returncode != 0
+
+
 @pytest.mark.gpu
 def test_cli_register_on_gpu(tmp_path, orc):
     """tests/test_cli.cpp:39-63: register an identical torus pair, 20
@@ -99,10 +125,13 @@ def test_cli_bench_on_gpu(tmp_path):
     path does not provide, is recorded as a failed cell rather than aborting."""
     exe = build()
     csv = tmp_path / "bench.csv"
+    svg = tmp_path / "bench.svg"
     r = subprocess.run([exe, "bench", "--synthetic", "--sizes", "40,60", "--variants",
-                        "fast,fast-lowrank,cpd", "--iters", "30", "--csv", str(csv)],
+                        "fast,fast-lowrank,cpd", "--iters", "30", "--csv", str(csv),
+                        "--svg", str(svg)],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
+    assert svg.read_text().count('<path d="M ') == 2  # cpd cells failed: no path
     lines = csv.read_text().splitlines()
     assert lines[0] == "M,N,variant,t_c,t_eig,t_iter,t_f,t_o,t_total,rmse,iterations"
     rows = [ln.split(",") for ln in lines[1:]]
