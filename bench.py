@@ -339,9 +339,9 @@ def run_ours(args, world, rank, local):
             # (SASS-verified op counts): pass 1 = 1 ex2 + 7 FP32 lane-ops per
             # pair → MUFU-bound; pass 2 = 1 ex2 + 12 lane-ops → FP32-bound.
             # Only the pairs of evaluated (non-culled) tile pairs cost pipe time.
-            tiles_total = -(-m // 256) * -(-n // 256) * prof_iters
-            f1 = prof_tiles[0] / tiles_total if prof_tiles[0] else 1.0
-            f2 = prof_tiles[1] / tiles_total if prof_tiles[1] else 1.0
+            u1, u2 = fcpd.cull_units_total(m, n)
+            f1 = prof_tiles[0] / (u1 * prof_iters) if prof_tiles[0] else 1.0
+            f2 = prof_tiles[1] / (u2 * prof_iters) if prof_tiles[1] else 1.0
             c1, c2 = max(1 / 16, 7 / 128), max(1 / 16, 12 / 128)
             hz = 148 * f_mhz * 1e6
             t_bound = m * n * (f1 * c1 + f2 * c2) / hz

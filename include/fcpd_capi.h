@@ -95,9 +95,12 @@ typedef struct fcpd_result {
   fcpd_timing timing;
   int64_t h2d_bytes;        /* host→device bytes this call copied     */
   int64_t d2h_bytes;        /* device→host bytes this call copied     */
-  int64_t tiles_evaluated[2]; /* E-step tile pairs computed since the
-                                 session began (pass 1, pass 2); the rest
-                                 were culled (≤ 2^-32 of any total)     */
+  int64_t tiles_evaluated[2]; /* E-step (256-point block, 32-point
+                                 sub-tile) pairs computed since the
+                                 session began (pass 1: scene blocks ×
+                                 model sub-tiles; pass 2: model blocks ×
+                                 scene sub-tiles); the rest were culled
+                                 (≤ 2^-32 of any total)                 */
   int64_t spectral_rank;    /* eigenpairs the last iteration's basis
                                streams used (filter ≥ tau; = K untruncated) */
   int32_t mstep_fused;      /* 1 if the session ran the one-kernel M-step */

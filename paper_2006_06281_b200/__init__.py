@@ -79,6 +79,13 @@ def lowrank_rank(rank_fraction: float, m: int) -> int:  # solvers.hpp:46-54
     return max(1, min(_llround(rank_fraction * m), m))
 
 
+def cull_units_total(m: int, n: int) -> tuple[int, int]:
+    """Work-list entries of one unculled E-step iteration, the unit of
+    ``tiles_evaluated``: (256-point scene blocks × 32-point model sub-tiles,
+    256-point model blocks × 32-point scene sub-tiles)."""
+    return (-(-n // 256) * -(-m // 32), -(-m // 256) * -(-n // 32))
+
+
 def _llround(v: float) -> int:
     return int(np.floor(v + 0.5)) if v >= 0 else -int(np.floor(-v + 0.5))
 

@@ -215,11 +215,13 @@ struct Session {
   // spatial order (sorted → original index) and tile-culling buffers
   std::vector<int64_t> perm_x, perm_y;
   bool cull = true;
-  DevBuf<float4> xlo, xhi, ylo, yhi;
-  DevBuf<float2> bminmax;
-  DevBuf<unsigned long long> cull_counters;  // tiles evaluated (pass 1, pass 2), cumulative
+  DevBuf<float4> xlo, xhi, ylo, yhi;      // 256-point tile boxes
+  DevBuf<float4> sxlo, sxhi, sylo, syhi;  // 32-point sub-tile boxes (the culling units)
+  DevBuf<float2> bminmax, sbminmax;       // per scene tile / sub-tile: b range
+  // (block, sub-tile) pairs evaluated (pass 1, pass 2), cumulative
+  DevBuf<unsigned long long> cull_counters;
   DevBuf<int32_t> probe_paid;                // culling probe outcome per block (both passes)
-  // per-iteration work lists of the two passes (culled tile pairs)
+  // per-iteration work lists of the two passes (culled (block, sub-tile) pairs)
   DevBuf<int32_t> wl1_tiles, wl1_off, wl2_tiles, wl2_off, wl2_off_cc, wl_done;
   DevBuf<double> row_seg_cc;  // tensor-core pass 2: the CUDA-core kernel's segments
 
@@ -252,8 +254,9 @@ struct Session {
     mask_all.release();
     fmax_all.release();
     qt_own.release();
-    for (auto* b : {&xlo, &xhi, &ylo, &yhi}) b->release();
+    for (auto* b : {&xlo, &xhi, &ylo, &yhi, &sxlo, &sxhi, &sylo, &syhi}) b->release();
     bminmax.release();
+    sbminmax.release();
     cull_counters.release();
     probe_paid.release();
     for (auto* b : {&wl1_tiles, &wl1_off, &wl2_tiles, &wl2_off, &wl2_off_cc, &wl_done})
@@ -447,13 +450,20 @@ void set_cull(Session& s, EStepBuffers& eb, int64_t m, int64_t n_local, int64_t 
   c.lists = (c.enabled || s.ep.tc) && s.wl2_tiles.p ? 1 : 0;
   const char* pe = std::getenv("FCPD_CULL_PROBE");
   c.probe = pe ? (std::atoi(pe) != 0) : 1;
-  c.n_xtiles = ceil_div(m, 256);
-  c.n_ytiles = ceil_div(n_local, 256);
+  c.n_xtiles = ceil_div(m, kTilePts);
+  c.n_ytiles = ceil_div(n_local, kTilePts);
+  c.n_xsub = ceil_div(m, kSubPts);
+  c.n_ysub = ceil_div(n_local, kSubPts);
   c.xlo = s.xlo.p;
   c.xhi = s.xhi.p;
   c.ylo = s.ylo.p;
   c.yhi = s.yhi.p;
   c.bminmax = s.bminmax.p;
+  c.sxlo = s.sxlo.p;
+  c.sxhi = s.sxhi.p;
+  c.sylo = s.sylo.p;
+  c.syhi = s.syhi.p;
+  c.sbminmax = s.sbminmax.p;
   const float bits = cull_margin_bits();
   c.margin1 = bits + static_cast<float>(std::log2(static_cast<double>(std::max<int64_t>(m, 1))));
   c.margin2 =
@@ -461,7 +471,8 @@ void set_cull(Session& s, EStepBuffers& eb, int64_t m, int64_t n_local, int64_t 
   c.counters = s.cull_counters.p;
   c.probe_paid1 = s.probe_paid.p;
   c.probe_paid2 = s.probe_paid.p ? s.probe_paid.p + c.n_ytiles : nullptr;
-  eb.cullw = CullBuffers{s.xlo.p, s.xhi.p, s.ylo.p, s.yhi.p, s.bminmax.p};
+  eb.cullw = CullBuffers{s.xlo.p,  s.xhi.p,  s.ylo.p,  s.yhi.p,  s.bminmax.p,
+                         s.sxlo.p, s.sxhi.p, s.sylo.p, s.syhi.p, s.sbminmax.p};
   eb.wl1 = WorkListBuffers{s.wl1_tiles.p, s.wl1_off.p, s.wl_done.p};
   eb.wl2 = WorkListBuffers{s.wl2_tiles.p, s.wl2_off.p, s.wl_done.p ? s.wl_done.p + 1 : nullptr,
                            s.wl2_off_cc.p};
@@ -494,21 +505,27 @@ EStepBuffers estep_buffers(Session& s, double* pt1, bool resid) {
 void alloc_estep(Session& s, int64_t m, int64_t n, cudaStream_t str) {
   s.col_seg.ensure(s.ep.col_seg_doubles());
   s.row_seg.ensure(s.ep.row_seg_doubles());
-  const int64_t nxt = ceil_div(m, 256), nyt = ceil_div(n, 256);
+  const int64_t nxt = ceil_div(m, kTilePts), nyt = ceil_div(n, kTilePts);
+  const int64_t nxs = ceil_div(m, kSubPts), nys = ceil_div(n, kSubPts);
   s.cull = cull_default(nxt, nyt);
   s.xlo.ensure(nxt);
   s.xhi.ensure(nxt);
   s.ylo.ensure(nyt);
   s.yhi.ensure(nyt);
   s.bminmax.ensure(nyt);
+  s.sxlo.ensure(nxs);
+  s.sxhi.ensure(nxs);
+  s.sylo.ensure(nys);
+  s.syhi.ensure(nys);
+  s.sbminmax.ensure(nys);
   s.cull_counters.ensure(2);
   FCPD_CUDA(cudaMemsetAsync(s.cull_counters.p, 0, 2 * sizeof(unsigned long long), str));
   s.probe_paid.ensure(nxt + nyt);
   FCPD_CUDA(cudaMemsetAsync(s.probe_paid.p, 1, (nxt + nyt) * sizeof(int32_t), str));  // ≠ 0
   if (s.cull || s.ep.tc) {
-    s.wl1_tiles.ensure(static_cast<size_t>(nyt) * nxt);
+    s.wl1_tiles.ensure(static_cast<size_t>(nyt) * nxs);
     s.wl1_off.ensure(nyt + 1);
-    s.wl2_tiles.ensure(static_cast<size_t>(nxt) * nyt);
+    s.wl2_tiles.ensure(static_cast<size_t>(nxt) * nys);
     s.wl2_off.ensure(nxt + 1);
     s.wl_done.ensure(2);
     FCPD_CUDA(cudaMemsetAsync(s.wl_done.p, 0, 2 * sizeof(int32_t), str));
@@ -517,7 +534,7 @@ void alloc_estep(Session& s, int64_t m, int64_t n, cudaStream_t str) {
     s.wl2_off_cc.ensure(nxt + 1);
     s.row_seg_cc.ensure(static_cast<size_t>(s.ep.row_grid + s.ep.row_blocks) * 5 * 256);
   }
-  launch_tile_bbox(s.y4b.p, n, s.ylo.p, s.yhi.p, nullptr, str);
+  launch_tile_bbox(s.y4b.p, n, s.ylo.p, s.yhi.p, s.sylo.p, s.syhi.p, nullptr, str);
 }
 
 // ev (optional, 7 events): recorded before the iteration and after each of
@@ -691,15 +708,19 @@ void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall);
 // ---- spatial sort: makes every 256-point tile a compact box for the
 // E-step's tile culling and its centred pair form.  A k-d partition: split
 // the points at a multiple of 256 along the longest axis of their bounding
-// box, recursively, so every tile is one leaf with a bounded aspect ratio
+// box, recursively, so every tile is one leaf with a bounded aspect ratio,
+// then each tile the same way at multiples of 32 (the culling sub-tiles)
 // (a Morton order lets some tiles straddle distant cells, and those tiles
 // lose both culling and the centred form).  Depth-first leaf order keeps
 // consecutive tiles near each other.  The order depends only on the point
 // set, is deterministic (ties by index), and is undone on every output.
 namespace {
 void kd_partition(const std::vector<double>& soa, int64_t cnt, int64_t* idx, int64_t len,
-                  int par_depth = 2) {
-  constexpr int64_t kLeaf = 256;
+                  int par_depth = 2, int64_t kLeaf = kTilePts) {
+  if (len <= kLeaf) {  // a tile: split it the same way into 32-point sub-tiles
+    if (kLeaf == kTilePts && len > kSubPts) kd_partition(soa, cnt, idx, len, 0, kSubPts);
+    return;
+  }
   while (len > kLeaf) {
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int64_t k = 0; k < len; ++k)
@@ -718,17 +739,18 @@ void kd_partition(const std::vector<double>& soa, int64_t cnt, int64_t* idx, int
       return key[a] < key[b] || (key[a] == key[b] && a < b);
     });
     if (par_depth > 0 && len >= (int64_t(1) << 15)) {  // halves on separate threads
-      std::thread t([&soa, cnt, idx, left, par_depth] {
-        kd_partition(soa, cnt, idx, left, par_depth - 1);
+      std::thread t([&soa, cnt, idx, left, par_depth, kLeaf] {
+        kd_partition(soa, cnt, idx, left, par_depth - 1, kLeaf);
       });
-      kd_partition(soa, cnt, idx + left, len - left, par_depth - 1);
+      kd_partition(soa, cnt, idx + left, len - left, par_depth - 1, kLeaf);
       t.join();
       return;
     }
-    kd_partition(soa, cnt, idx, left, 0);
+    kd_partition(soa, cnt, idx, left, 0, kLeaf);
     idx += left;
     len -= left;
   }
+  if (kLeaf == kTilePts && len > kSubPts) kd_partition(soa, cnt, idx, len, 0, kSubPts);
 }
 }  // namespace
 

@@ -109,6 +109,13 @@ __device__ __forceinline__ int wl_block_of(const WorkList& wl, int64_t u) {
   return lo;
 }
 
+// Point index (in the other set) of list position e of block b: the units
+// are upts()-point runs of consecutive points.
+__device__ __forceinline__ int64_t wl_point(const WorkList& wl, int b, int64_t e) {
+  const int64_t k = e >> wl.ushift;
+  return (static_cast<int64_t>(wl.tile(b, k)) << wl.ushift) + (e - (k << wl.ushift));
+}
+
 // Centre and squared half-diagonal of the CTA's points' bounding box
 // (scaled frame); blockDim ≤ 128.  Callers separate successive calls by a
 // __syncthreads (the staging barrier).
@@ -220,14 +227,15 @@ __global__ void __launch_bounds__(128 / NC)
   __shared__ float4 xb[kTile];  // centred (vz,vz,−|v|²,−|v|²) | diff (−z,−z,·,·)
   const float s = st->sx;
   const int64_t G = gridDim.x, g = blockIdx.x;
-  const int64_t P = wl.off(wl.n_blocks) * kTile;
+  const int64_t P = wl.off(wl.n_blocks) << wl.ushift;
   const int64_t p0 = sk_start(g, G, P), p1 = sk_start(g + 1, G, P);
   if (p0 >= p1) return;
   const int t = threadIdx.x;
-  int rb = wl_block_of(wl, p0 / kTile);
+  int rb = wl_block_of(wl, p0 >> wl.ushift);
   for (int64_t p = p0; p < p1;) {
-    while (wl.off(rb + 1) * kTile <= p) ++rb;
-    const int64_t pe = min(p1, wl.off(rb + 1) * kTile);
+    while ((wl.off(rb + 1) << wl.ushift) <= p) ++rb;
+    const int64_t pe = min(p1, wl.off(rb + 1) << wl.ushift);
+    const int64_t ob = wl.off(rb) << wl.ushift;  // first point-unit of block rb
     __syncthreads();  // previous segment's readers of the shared box/tiles are done
     // own columns of block rb
     const int64_t c0 = static_cast<int64_t>(rb) * kTile + kCols * t;
@@ -274,20 +282,17 @@ __global__ void __launch_bounds__(128 / NC)
 #pragma unroll
     for (int h = 0; h < kCols; ++h) d[h] = 0.0;
     for (int64_t q = p; q < pe;) {
-      const int64_t k = q / kTile - wl.off(rb);
-      const int a = static_cast<int>(q % kTile);
-      const int b = static_cast<int>(min(static_cast<int64_t>(kTile), a + (pe - q)));
-      const int64_t base = static_cast<int64_t>(wl.tile(rb, k)) * kTile + a;
-      const int cnt = static_cast<int>(max(int64_t(0), min(static_cast<int64_t>(b - a), m - base)));
-      q += b - a;
-      if (cnt == 0) continue;  // uniform
+      // stage the next ≤ 256 points of the block's list (gathered from its
+      // units; points past m are padding)
+      const int cnt = static_cast<int>(min(static_cast<int64_t>(kTile), pe - q));
       const int cnt8 = (cnt + 7) & ~7;
       __syncthreads();
       for (int i = t; i < cnt8; i += kThr) {
+        const int64_t src = i < cnt ? wl_point(wl, rb, q + i - ob) : m;
         if (centred) {
           float4 v;
-          if (i < cnt) {
-            const float4 x = scale_pt(xt4[base + i], s);
+          if (src < m) {
+            const float4 x = scale_pt(xt4[src], s);
             v = make_float4(__fsub_rn(x.x, bc.c.x), __fsub_rn(x.y, bc.c.y),
                             __fsub_rn(x.z, bc.c.z), 0.f);
             v.w = -__fmaf_rn(v.z, v.z, __fmaf_rn(v.y, v.y, __fmul_rn(v.x, v.x)));
@@ -297,12 +302,13 @@ __global__ void __launch_bounds__(128 / NC)
           xa[i] = make_float4(v.x, v.x, v.y, v.y);
           xb[i] = make_float4(v.z, v.z, v.w, v.w);
         } else {
-          const float4 v = i < cnt ? scale_pt(xt4[base + i], s)
+          const float4 v = src < m ? scale_pt(xt4[src], s)
                                    : make_float4(kPadCoord, kPadCoord, kPadCoord, 0.f);
           xa[i] = make_float4(-v.x, -v.x, -v.y, -v.y);
           xb[i] = make_float4(-v.z, -v.z, 0.f, 0.f);
         }
       }
+      q += cnt;
       __syncthreads();
       float2 f[NC];
 #pragma unroll
@@ -372,8 +378,8 @@ __device__ __forceinline__ void sum_segments(const WorkList& wl, int64_t G, cons
 #pragma unroll
   for (int k = 0; k < NQ; ++k) a[k] = 0.0;
   if (live) {
-    const int64_t P = wl.off(wl.n_blocks) * kTile;
-    const int64_t ua = wl.off(b) * kTile, ub = wl.off(b + 1) * kTile;
+    const int64_t P = wl.off(wl.n_blocks) << wl.ushift;
+    const int64_t ua = wl.off(b) << wl.ushift, ub = wl.off(b + 1) << wl.ushift;
     if (ua < ub) {
       const int64_t g0 = sk_owner(ua, G, P), g1 = sk_owner(ub - 1, G, P);
       for (int64_t g = g0 + lane; g <= g1; g += kCombineLanes) {
@@ -498,15 +504,16 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
   __shared__ double acc_s[5][kRows][kThr];
   const float s = st->sx;
   const int64_t G = gridDim.x, g = blockIdx.x;
-  const int64_t P = wl.off(wl.n_blocks) * kTile;
+  const int64_t P = wl.off(wl.n_blocks) << wl.ushift;
   const int64_t p0 = sk_start(g, G, P), p1 = sk_start(g + 1, G, P);
   if (p0 >= p1) return;
   const float2 minus1 = make_float2(-1.f, -1.f);
   const int t = threadIdx.x;
-  int rb = wl_block_of(wl, p0 / kTile);
+  int rb = wl_block_of(wl, p0 >> wl.ushift);
   for (int64_t p = p0; p < p1;) {
-    while (wl.off(rb + 1) * kTile <= p) ++rb;
-    const int64_t pe = min(p1, wl.off(rb + 1) * kTile);
+    while ((wl.off(rb + 1) << wl.ushift) <= p) ++rb;
+    const int64_t pe = min(p1, wl.off(rb + 1) << wl.ushift);
+    const int64_t ob = wl.off(rb) << wl.ushift;  // first point-unit of block rb
     __syncthreads();  // previous segment's readers of the shared box/tiles are done
     const int64_t r0 = static_cast<int64_t>(rb) * kTile + kRows * t;
     float4 xv[kRows];
@@ -555,21 +562,16 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
 #pragma unroll
       for (int h = 0; h < kRows; ++h) acc_s[k][h][t] = 0.0;
     for (int64_t q = p; q < pe;) {
-      const int64_t k = q / kTile - wl.off(rb);
-      const int a = static_cast<int>(q % kTile);
-      const int b = static_cast<int>(min(static_cast<int64_t>(kTile), a + (pe - q)));
-      const int64_t base = static_cast<int64_t>(wl.tile(rb, k)) * kTile + a;
-      const int cnt = static_cast<int>(max(int64_t(0), min(static_cast<int64_t>(b - a), n - base)));
-      q += b - a;
-      if (cnt == 0) continue;  // uniform
+      const int cnt = static_cast<int>(min(static_cast<int64_t>(kTile), pe - q));
       const int cnt8 = (cnt + 7) & ~7;
       __syncthreads();
       for (int i = t; i < cnt8; i += kThr) {
+        const int64_t src = i < cnt ? wl_point(wl, rb, q + i - ob) : n;
         if (centred) {
           float4 u;
           float uq;
-          if (i < cnt) {
-            const float4 y = scale_pt(y4b[base + i], s);
+          if (src < n) {
+            const float4 y = scale_pt(y4b[src], s);
             u = make_float4(__fsub_rn(y.x, bc.c.x), __fsub_rn(y.y, bc.c.y),
                             __fsub_rn(y.z, bc.c.z), 0.f);
             uq = __fmaf_rn(u.z, u.z, __fmaf_rn(u.y, u.y, __fmul_rn(u.x, u.x)));
@@ -582,12 +584,13 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
           yb[i] = make_float4(u.z, u.z, u.w, u.w);
           yq[i] = make_float2(uq, uq);
         } else {
-          const float4 y = i < cnt ? scale_pt(y4b[base + i], s)
+          const float4 y = src < n ? scale_pt(y4b[src], s)
                                    : make_float4(kPadCoord, kPadCoord, kPadCoord, -INFINITY);
           ya[i] = make_float4(y.x, y.x, y.y, y.y);
           yb[i] = make_float4(y.z, y.z, y.w, y.w);
         }
       }
+      q += cnt;
       __syncthreads();
       float2 f0[NP], fx[NP], fy[NP], fz[NP], fv[NP];
 #pragma unroll
@@ -696,10 +699,13 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
 // Tile geometry and work lists for culling (points are k-d sorted by the
 // engine, so 256-point tiles are spatially compact).
 
-// per-tile axis-aligned box of the first three coordinates (unscaled)
+// per-tile and per-sub-tile axis-aligned boxes of the first three
+// coordinates (unscaled): one CTA per 256-point tile, one warp per sub-tile
 __global__ void tile_bbox_kernel(const float4* __restrict__ p, int64_t count,
                                  float4* __restrict__ lo, float4* __restrict__ hi,
+                                 float4* __restrict__ slo, float4* __restrict__ shi,
                                  const IterState* __restrict__ st) {
+  static_assert(kSubPts == 32, "one warp per sub-tile");
   griddep_wait();
   if (st && !st->active) return;
   __shared__ float red[6][8];
@@ -722,9 +728,15 @@ __global__ void tile_bbox_kernel(const float4* __restrict__ p, int64_t count,
       v[k] = k < 3 ? fminf(v[k], w) : fmaxf(v[k], w);
     }
   const int warp = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0)
+  if ((threadIdx.x & 31) == 0) {
 #pragma unroll
     for (int k = 0; k < 6; ++k) red[k][warp] = v[k];
+    const int64_t sub = static_cast<int64_t>(blockIdx.x) * kSubPerTile + warp;
+    if (slo && (sub << 5) < count) {
+      slo[sub] = make_float4(v[0], v[1], v[2], 0.f);
+      shi[sub] = make_float4(v[3], v[4], v[5], 0.f);
+    }
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     float r[6];
@@ -738,9 +750,10 @@ __global__ void tile_bbox_kernel(const float4* __restrict__ p, int64_t count,
   }
 }
 
-// per scene tile: (min b_n, max b_n) after pass 1
+// per scene tile and sub-tile: (min b_n, max b_n) after pass 1
 __global__ void tile_bminmax_kernel(const float4* __restrict__ y4b, int64_t n,
-                                    float2* __restrict__ out, const IterState* __restrict__ st) {
+                                    float2* __restrict__ out, float2* __restrict__ sout,
+                                    const IterState* __restrict__ st) {
   griddep_wait();
   if (!st->active) return;
   __shared__ float red[2][8];
@@ -755,6 +768,8 @@ __global__ void tile_bminmax_kernel(const float4* __restrict__ y4b, int64_t n,
   if ((threadIdx.x & 31) == 0) {
     red[0][threadIdx.x >> 5] = mn;
     red[1][threadIdx.x >> 5] = mx;
+    const int64_t sub = static_cast<int64_t>(blockIdx.x) * kSubPerTile + (threadIdx.x >> 5);
+    if ((sub << 5) < n) sout[sub] = make_float2(mn, mx);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -798,7 +813,7 @@ __device__ void scan_counts(int32_t* offset, int n_blocks, int* wsum) {
 }
 
 __device__ void last_cta_scan(int32_t* offset, int32_t* offset2, int n_blocks, int32_t* done,
-                              unsigned long long* counter) {
+                              unsigned long long* counter, int unit_mult = 1) {
   __shared__ int is_last;
   __shared__ int wsum[32];
   __threadfence();
@@ -812,8 +827,9 @@ __device__ void last_cta_scan(int32_t* offset, int32_t* offset2, int n_blocks, i
   if (threadIdx.x == 0) {
     *done = 0;
     if (counter)
-      *counter += static_cast<unsigned long long>(offset[n_blocks]) +
-                  (offset2 ? static_cast<unsigned long long>(offset2[n_blocks]) : 0ull);
+      *counter += (static_cast<unsigned long long>(offset[n_blocks]) +
+                   (offset2 ? static_cast<unsigned long long>(offset2[n_blocks]) : 0ull)) *
+                  static_cast<unsigned long long>(unit_mult);
   }
 }
 
@@ -950,11 +966,11 @@ __device__ __forceinline__ float probe_scan(const float4* pa, const float4* pb, 
 // Pass-1 list, one CTA per scene block b.  Every column n of the block has
 // total ≥ max(2^{−t_min(n)}, 2^{log2 c}); the bound uses U ≥ max_n
 // min_m ‖y_n − x̃_m‖², the smaller of
-//  * the box bound min over model tiles j of maxdist²(b, j), and
+//  * the box bound min over model sub-tiles j of maxdist²(b, j), and
 //  * the probe: the exact nearest distance of every column to the points of
 //    the kProbeTiles model tiles nearest the block (padded up by 2^-16),
-// and model tile j is dropped when s²·mindist²(b, j) > min(s²U, −log2 c) +
-// margin (every pair term in it is then < 2^-margin of the column total).
+// and model sub-tile j is dropped when s²·mindist²(b, j) > min(s²U, −log2 c)
+// + margin (every pair term in it is then < 2^-margin of the column total).
 __global__ void __launch_bounds__(kListThreads)
     col_list_kernel(CullInfo cull, const float4* __restrict__ xt4, int64_t m,
                     const float4* __restrict__ y4, int64_t n, int32_t* __restrict__ tiles,
@@ -973,9 +989,10 @@ __global__ void __launch_bounds__(kListThreads)
   const float4 lo = cull.ylo[b], hi = cull.yhi[b];
   const float neg_log2c = static_cast<float>(-st->log2c);  // +inf when ω = 0
   float u = INFINITY, far = 0.f;
-  for (int j = threadIdx.x; j < cull.n_xtiles; j += kListThreads) {
-    u = fminf(u, box_maxdist2(lo, hi, cull.xlo[j], cull.xhi[j]));
-    far = fmaxf(far, box_mindist2(lo, hi, cull.xlo[j], cull.xhi[j]));
+  for (int j = threadIdx.x; j < cull.n_xsub; j += kListThreads) {
+    const float4 jl = cull.sxlo[j], jh = cull.sxhi[j];
+    u = fminf(u, box_maxdist2(lo, hi, jl, jh));
+    far = fmaxf(far, box_mindist2(lo, hi, jl, jh));
   }
   u = cta_reduce<false>(u, shf);
   far = cta_reduce<true>(far, shf);
@@ -989,8 +1006,8 @@ __global__ void __launch_bounds__(kListThreads)
     const float cut_box = fminf(s2 * u, neg_log2c) + cull.margin1;
     const float cut_min = fminf(0.f, neg_log2c) + cull.margin1;
     float2 k = make_float2(0.f, 0.f);  // (kept, contested)
-    for (int j = threadIdx.x; j < cull.n_xtiles; j += kListThreads) {
-      const float t = s2 * box_mindist2(lo, hi, cull.xlo[j], cull.xhi[j]);
+    for (int j = threadIdx.x; j < cull.n_xsub; j += kListThreads) {
+      const float t = s2 * box_mindist2(lo, hi, cull.sxlo[j], cull.sxhi[j]);
       k.x += t <= cut_box ? 1.f : 0.f;
       k.y += t <= cut_box && t > cut_min ? 1.f : 0.f;
     }
@@ -1034,9 +1051,9 @@ __global__ void __launch_bounds__(kListThreads)
   if (np > 0) u = fminf(u, probe);
   const float floor_t = fminf(s2 * u, neg_log2c);
   const float cut = floor_t + cull.margin1;
-  const int count = cta_compact(cull.n_xtiles, tiles + static_cast<int64_t>(b) * cull.n_xtiles,
+  const int count = cta_compact(cull.n_xsub, tiles + static_cast<int64_t>(b) * cull.n_xsub,
                                 wcount, [&](int j) {
-                                  return !(s2 * box_mindist2(lo, hi, cull.xlo[j], cull.xhi[j]) >
+                                  return !(s2 * box_mindist2(lo, hi, cull.sxlo[j], cull.sxhi[j]) >
                                            cut);
                                 });
   if (threadIdx.x == 0) {
@@ -1047,13 +1064,14 @@ __global__ void __launch_bounds__(kListThreads)
   last_cta_scan(offset, nullptr, n_blocks, done, cull.counters);
 }
 
-// Pass-2 list, one CTA per model block b.  Every row m of the block has
-// max_n L_mn ≥ L_lb, the larger of
-//  * the box bound max over scene tiles j of (min b − s²·maxdist²(b, j)),
+// Pass-2 list, one CTA per model block b, over units of the scene (32-point
+// sub-tiles; 256-point tiles for the tensor-core pass: ulo/uhi/ubm, n_units).
+// Every row m of the block has max_n L_mn ≥ L_lb, the larger of
+//  * the box bound max over scene units j of (min b − s²·maxdist²(b, j)),
 //  * the probe: min over the block's rows of the exact max of b_n − s²‖y_n −
 //    x̃_m‖² over the kProbeTiles scene tiles nearest the block (less a
 //    rounding slack);
-// scene tile j is dropped when its largest possible L (max b − s²·mindist²)
+// scene unit j is dropped when its largest possible L (max b − s²·mindist²)
 // < L_lb − margin (culling off: every tile kept).  With offset_cc
 // (tensor-core pass 2), a block whose scaled squared half-diagonal exceeds
 // kCentredMaxR2 is routed to the CUDA-core list (difference form) instead.
@@ -1061,7 +1079,9 @@ __global__ void __launch_bounds__(kListThreads)
     row_list_kernel(CullInfo cull, const float4* __restrict__ xt4, int64_t m,
                     const float4* __restrict__ y4b, int64_t n, int32_t* __restrict__ tiles,
                     int32_t* __restrict__ offset, int32_t* __restrict__ offset_cc, int n_blocks,
-                    int32_t* __restrict__ done, const IterState* __restrict__ st) {
+                    int32_t* __restrict__ done, const float4* __restrict__ ulo,
+                    const float4* __restrict__ uhi, const float2* __restrict__ ubm, int n_units,
+                    int unit_mult, const IterState* __restrict__ st) {
   griddep_wait();
   if (!st->active) return;
   __shared__ float4 pa[kProbeTiles * kTile / 2], pb[kProbeTiles * kTile / 2];
@@ -1077,10 +1097,11 @@ __global__ void __launch_bounds__(kListThreads)
   int np = 0;
   if (cull.enabled) {
     float l = -INFINITY, lmin = INFINITY;
-    for (int j = threadIdx.x; j < cull.n_ytiles; j += kListThreads) {
-      l = fmaxf(l, cull.bminmax[j].x - s2 * box_maxdist2(lo, hi, cull.ylo[j], cull.yhi[j]));
-      lmin = fminf(lmin,
-                   cull.bminmax[j].y - s2 * box_mindist2(lo, hi, cull.ylo[j], cull.yhi[j]));
+    for (int j = threadIdx.x; j < n_units; j += kListThreads) {
+      const float4 jl = ulo[j], jh = uhi[j];
+      const float2 bm = ubm[j];
+      l = fmaxf(l, bm.x - s2 * box_maxdist2(lo, hi, jl, jh));
+      lmin = fminf(lmin, bm.y - s2 * box_mindist2(lo, hi, jl, jh));
     }
     l = cta_reduce<true>(l, shf);
     lmin = cta_reduce<false>(lmin, shf);
@@ -1092,9 +1113,8 @@ __global__ void __launch_bounds__(kListThreads)
     if (useful) {
       const float floor_box = l - cull.margin2;
       float2 k = make_float2(0.f, 0.f);
-      for (int j = threadIdx.x; j < cull.n_ytiles; j += kListThreads) {
-        const float v =
-            cull.bminmax[j].y - s2 * box_mindist2(lo, hi, cull.ylo[j], cull.yhi[j]);
+      for (int j = threadIdx.x; j < n_units; j += kListThreads) {
+        const float v = ubm[j].y - s2 * box_mindist2(lo, hi, ulo[j], uhi[j]);
         k.x += v >= floor_box ? 1.f : 0.f;
         k.y += v >= floor_box && v < -cull.margin2 ? 1.f : 0.f;
       }
@@ -1140,10 +1160,8 @@ __global__ void __launch_bounds__(kListThreads)
     floor_l = l - cull.margin2;
   }
   const int count = cta_compact(
-      cull.n_ytiles, tiles + static_cast<int64_t>(b) * cull.n_ytiles, wcount, [&](int j) {
-        return !cull.enabled ||
-               !(cull.bminmax[j].y - s2 * box_mindist2(lo, hi, cull.ylo[j], cull.yhi[j]) <
-                 floor_l);
+      n_units, tiles + static_cast<int64_t>(b) * n_units, wcount, [&](int j) {
+        return !cull.enabled || !(ubm[j].y - s2 * box_mindist2(lo, hi, ulo[j], uhi[j]) < floor_l);
       });
   if (threadIdx.x == 0) {
     bool to_tc = true;
@@ -1157,7 +1175,7 @@ __global__ void __launch_bounds__(kListThreads)
       cull.probe_paid2[b] = (kept_box - count) * kProbePayShare >= kept_box;
   }
   last_cta_scan(offset, offset_cc, n_blocks, done,
-                cull.enabled && cull.counters ? cull.counters + 1 : nullptr);
+                cull.enabled && cull.counters ? cull.counters + 1 : nullptr, unit_mult);
 }
 
 // ---------------------------------------------------------------------------
@@ -1345,16 +1363,19 @@ WorkList pass1_list(const EStepPlan& p, const EStepBuffers& b, int64_t m) {
   WorkList wl;
   wl.implicit = b.cull.enabled ? 0 : 1;
   wl.n_blocks = p.col_blocks;
-  wl.n_other = static_cast<int>(ceil_div(m, kTile));
+  wl.n_other = static_cast<int>(ceil_div(m, kSubPts));
   wl.tiles = b.wl1.tiles;
   wl.offset = b.wl1.offset;
   return wl;
 }
+// (the tensor-core pass 2 keeps 256-point units: its pieces are whole tiles)
 WorkList pass2_list(const EStepPlan& p, const EStepBuffers& b, int64_t n, bool cc = false) {
   WorkList wl;
   wl.implicit = b.cull.lists ? 0 : 1;
   wl.n_blocks = p.row_blocks;
-  wl.n_other = static_cast<int>(ceil_div(n, kTile));
+  wl.ushift = p.tc ? 8 : 5;
+  static_assert(kTilePts == 1 << 8 && kSubPts == 1 << 5, "unit shifts");
+  wl.n_other = static_cast<int>(ceil_div(n, int64_t(1) << wl.ushift));
   wl.tiles = b.wl2.tiles;
   wl.offset = cc ? b.wl2.offset_cc : b.wl2.offset;
   return wl;
@@ -1378,10 +1399,10 @@ void launch_estep_prologue(IterState* st, int64_t m, int64_t n_global, int d, do
   FCPD_LAUNCH_CHECK();
 }
 
-void launch_tile_bbox(const float4* pts, int64_t count, float4* lo, float4* hi,
-                      const IterState* st, cudaStream_t stream) {
+void launch_tile_bbox(const float4* pts, int64_t count, float4* lo, float4* hi, float4* slo,
+                      float4* shi, const IterState* st, cudaStream_t stream) {
   launch_pdl(tile_bbox_kernel, dim3(ceil_div(count, kTile)), dim3(kTile), 0, stream, pts, count, lo,
-             hi, st);
+             hi, slo, shi, st);
   FCPD_LAUNCH_CHECK();
 }
 
@@ -1393,7 +1414,7 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
   const CullInfo& cu = b.cull;
   const WorkList wl = pass1_list(p, b, m);
   if (cu.enabled) {
-    launch_tile_bbox(b.xt4, m, b.cullw.xlo, b.cullw.xhi, st, stream);
+    launch_tile_bbox(b.xt4, m, b.cullw.xlo, b.cullw.xhi, b.cullw.sxlo, b.cullw.sxhi, st, stream);
     launch_pdl(col_list_kernel, dim3(p.col_blocks), dim3(kListThreads), 0, stream, cu, b.xt4, m,
                b.y4b, n, b.wl1.tiles, b.wl1.offset, p.col_blocks, b.wl1.done, st);
     FCPD_LAUNCH_CHECK();
@@ -1413,7 +1434,7 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
   FCPD_LAUNCH_CHECK();
   if (cu.enabled) {
     launch_pdl(tile_bminmax_kernel, dim3(ceil_div(n, kTile)), dim3(kTile), 0, stream, b.y4b, n,
-               b.cullw.bminmax, st);
+               b.cullw.bminmax, b.cullw.sbminmax, st);
     FCPD_LAUNCH_CHECK();
   }
 }
@@ -1433,10 +1454,13 @@ void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int6
   const CullInfo& cu = b.cull;
   if (cu.lists) {
     if (!cu.enabled)  // x̃ tile boxes for the routing (pass 1 made them when culling)
-      launch_tile_bbox(b.xt4, m, b.cullw.xlo, b.cullw.xhi, st, stream);
+      launch_tile_bbox(b.xt4, m, b.cullw.xlo, b.cullw.xhi, b.cullw.sxlo, b.cullw.sxhi, st, stream);
+    // units of the scene: sub-tiles, or whole tiles for the tensor-core pass
+    const WorkList wl = pass2_list(p, b, n);
     launch_pdl(row_list_kernel, dim3(p.row_blocks), dim3(kListThreads), 0, stream, cu, b.xt4, m,
                b.y4b, n, b.wl2.tiles, b.wl2.offset, p.tc ? b.wl2.offset_cc : nullptr, p.row_blocks,
-               b.wl2.done, st);
+               b.wl2.done, p.tc ? cu.ylo : cu.sylo, p.tc ? cu.yhi : cu.syhi,
+               p.tc ? cu.bminmax : cu.sbminmax, wl.n_other, p.tc ? kSubPerTile : 1, st);
     FCPD_LAUNCH_CHECK();
   }
   SegSrc a, c;

@@ -10,7 +10,11 @@
 
 namespace fcpd {
 
-constexpr int kTilePts = 256;  // points per tile (a CTA's own block, a staged tile)
+constexpr int kTilePts = 256;  // points per tile (a CTA's own block, a staging chunk)
+// points per sub-tile: the culling unit of the other set (the engine's k-d
+// order makes every 32-point sub-tile of a 256-point tile a compact box)
+constexpr int kSubPts = 32;
+constexpr int kSubPerTile = kTilePts / kSubPts;
 
 // Fallback-path per-row outputs (all device pointers; SoA fp64 M×3).
 struct RowOut {
@@ -29,18 +33,22 @@ struct YStats {
 };
 
 // The work of one pass: for each of n_blocks own 256-point blocks (scene
-// tiles in pass 1, model tiles in pass 2), the list of tiles of the other
-// set whose pairs are evaluated.  Units = (block, tile) pairs in block-major
-// order; offset[b] = units before block b.  implicit = every tile of every
-// block (no culling): tiles/offset are not read.
+// tiles in pass 1, model tiles in pass 2), the list of units of the other
+// set whose pairs are evaluated.  A unit is upts() consecutive points of the
+// other set (a 32-point sub-tile; 256-point tiles for the tensor-core pass
+// 2).  Entries = (block, unit) pairs in block-major order; offset[b] =
+// entries before block b.  implicit = every unit of every block (no
+// culling): tiles/offset are not read.
 struct WorkList {
   int implicit = 1;
-  int n_blocks = 0, n_other = 0;
+  int n_blocks = 0, n_other = 0;  // n_other = units of the other set
+  int ushift = 5;                 // points per unit = 1 << ushift (kSubPts)
   const int32_t* tiles = nullptr;   // [n_blocks][n_other]
   const int32_t* offset = nullptr;  // [n_blocks + 1]
   __host__ __device__ int64_t off(int b) const {
     return implicit ? static_cast<int64_t>(b) * n_other : static_cast<int64_t>(offset[b]);
   }
+  __host__ __device__ int upts() const { return 1 << ushift; }
   __host__ __device__ int tile(int b, int64_t k) const {
     return implicit ? static_cast<int>(k) : tiles[static_cast<int64_t>(b) * n_other + k];
   }
@@ -81,8 +89,9 @@ void launch_estep_row_tc(const float4* xt4, int64_t m, const float4* y4b, int64_
                          cudaStream_t stream);
 
 // Tile culling.  Points are k-d sorted by the engine so
-// 256-point tiles are compact boxes; a (block, tile) pair is dropped from
-// the work list when every pair term in it is below 2^-margin of the
+// 256-point tiles and their 32-point sub-tiles are compact boxes; a (block,
+// sub-tile) pair is dropped from the work list when every pair term in it
+// is below 2^-margin of the
 // smallest possible column (row) total.  With margin = bits + log2(count)
 // the skipped mass is ≤ 2^-bits relative (engine.cu: 32 bits).  The lower
 // bound on the totals comes from box geometry and, with `probe`, from exact
@@ -91,14 +100,22 @@ struct CullInfo {
   int enabled = 0;  // culling drops tile pairs from the work lists
   int probe = 1;    // probe bound on (FCPD_CULL_PROBE=0 → box bound only)
   int lists = 0;    // explicit work lists (culling, or pass-2 routing to tensor cores)
-  int n_xtiles = 0, n_ytiles = 0;   // 256-point tiles
+  int n_xtiles = 0, n_ytiles = 0;   // 256-point tiles (own blocks; probe choice)
+  int n_xsub = 0, n_ysub = 0;       // 32-point sub-tiles (the culling units)
   const float4* xlo = nullptr;      // model tiles (x̃ of this iteration)
   const float4* xhi = nullptr;
   const float4* ylo = nullptr;      // scene tiles (fixed)
   const float4* yhi = nullptr;
   const float2* bminmax = nullptr;  // per scene tile: (min b, max b)
+  const float4* sxlo = nullptr;     // model sub-tiles
+  const float4* sxhi = nullptr;
+  const float4* sylo = nullptr;     // scene sub-tiles
+  const float4* syhi = nullptr;
+  const float2* sbminmax = nullptr;  // per scene sub-tile: (min b, max b)
   float margin1 = 0.f, margin2 = 0.f;
-  unsigned long long* counters = nullptr;  // [0] pass-1, [1] pass-2 tile pairs evaluated
+  // [0] pass-1, [1] pass-2 work-list entries evaluated, in (256-point block,
+  // 32-point sub-tile) pairs (a 256-point unit counts as 8)
+  unsigned long long* counters = nullptr;
   // per own block: did the last probe drop ≥ 1/4 of the box-kept tiles?
   // (blocks whose probe does not pay reconsider it every 4th iteration)
   int32_t* probe_paid1 = nullptr;  // [n_ytiles]
@@ -108,6 +125,8 @@ struct CullInfo {
 struct CullBuffers {  // writable views of the CullInfo arrays (engine-owned)
   float4 *xlo, *xhi, *ylo, *yhi;
   float2* bminmax;
+  float4 *sxlo, *sxhi, *sylo, *syhi;
+  float2* sbminmax;
 };
 
 struct EStepBuffers {
@@ -129,9 +148,9 @@ struct EStepBuffers {
   WorkListBuffers wl1, wl2;  // pass-1 / pass-2 work lists (used when culling)
 };
 
-// Scene-tile boxes (once per session; Y does not move).
-void launch_tile_bbox(const float4* pts, int64_t count, float4* lo, float4* hi,
-                      const IterState* st, cudaStream_t stream);
+// Tile and sub-tile boxes (scene: once per session, Y does not move).
+void launch_tile_bbox(const float4* pts, int64_t count, float4* lo, float4* hi, float4* slo,
+                      float4* shi, const IterState* st, cudaStream_t stream);
 
 EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count);
 // Pieces of launch_estep for the distributed path (n = local scene count;

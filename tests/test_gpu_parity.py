@@ -520,8 +520,8 @@ def test_culling_matches_unculled(ctx, fc, monkeypatch, name, m, iters, late_fra
     t0 = ctx.session_read(with_points=False)["tiles_evaluated"]
     ctx.session_run(10)
     t1 = ctx.session_read(with_points=False)["tiles_evaluated"]
-    total = 10 * -(-x.shape[0] // 256) * -(-y.shape[0] // 256)
-    frac = [(b - a) / total for a, b in zip(t0, t1)]
+    total = fc.cull_units_total(x.shape[0], y.shape[0])
+    frac = [(b - a) / (10 * u) for a, b, u in zip(t0, t1, total)]
     print(f"{name}: late tile-pair fraction evaluated {frac}")
     assert 0.0 < max(frac) <= late_frac, frac
 

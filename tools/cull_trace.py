@@ -24,7 +24,7 @@ def main():
     ctx.session_begin(x, y, cfg)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=torch.device("cuda", 0))
     flush = torch.empty(64 * 2**20, dtype=torch.float32, device="cuda")
-    tiles_total = -(-x.shape[0] // 256) * -(-y.shape[0] // 256)
+    tiles_total = fcpd.cull_units_total(x.shape[0], y.shape[0])
     prev = ctx.session_read(with_points=False)["tiles_evaluated"]
     rows = []
     for i in range(iters):
@@ -38,8 +38,8 @@ def main():
         st = ctx.session_read(with_points=False)
         t = st["tiles_evaluated"]
         rows.append({"it": i, "ms": e0.elapsed_time(e1), "sigma2": float(st["sigma2_trace"][-1]),
-                     "f1": (t[0] - prev[0]) / tiles_total or 1.0,
-                     "f2": (t[1] - prev[1]) / tiles_total or 1.0,
+                     "f1": (t[0] - prev[0]) / tiles_total[0] or 1.0,
+                     "f2": (t[1] - prev[1]) / tiles_total[1] or 1.0,
                      "keff": st["spectral_rank"]})
         prev = t
     tot = sum(r["ms"] for r in rows)
