@@ -51,6 +51,7 @@ constexpr float kPadCoord = 3.0e18f;  // padding point: t ≈ 1e37, 2^-t = 0
 constexpr int kListThreads = 256;     // list kernels: one CTA per own block
 static_assert(kListThreads == kTilePts, "list CTA: one thread per own point");
 constexpr int kProbeTiles = 2;        // other-set tiles probed for the exact culling bound
+constexpr int64_t kMinPtsPerCta = 256;  // stream-K grid: dense point-units per CTA, at least (one chunk)
 // Probe policy (speed only; any probe decision keeps the bound exact): probe
 // a block when the tiles the box bound keeps but U = 0 would drop are ≥ 1/2
 // of the kept ones; keep probing it every iteration while the probe drops
@@ -1347,8 +1348,18 @@ EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
     FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_row, estep_row_kernel<1>, 128, 0));
   p.col_blocks = static_cast<int>(ceil_div(n, kTile));
   p.row_blocks = static_cast<int>(ceil_div(m, kTile));
-  p.col_grid = sm_count * std::max(occ_col, 1);
-  p.row_grid = sm_count * std::max(occ_row, 1);
+  // One wave of CTAs, but at least kMinPtsPerCta point-units of the dense
+  // pass per CTA: on small passes (C0: 8 blocks × 2000 points) a full wave
+  // leaves each CTA a few points and each block's combine a long chain of
+  // segment slots to sum.
+  int64_t min_pts = kMinPtsPerCta;
+  if (const char* e = std::getenv("FCPD_ESTEP_MIN_PTS")) min_pts = std::max<int64_t>(1, std::atoll(e));
+  auto grid_for = [&](int64_t pts, int occ) {
+    const int64_t full = static_cast<int64_t>(sm_count) * std::max(occ, 1);
+    return static_cast<int>(std::min(full, std::max<int64_t>(sm_count, ceil_div(pts, min_pts))));
+  };
+  p.col_grid = grid_for(p.col_blocks * ceil_div(m, kSubPts) * kSubPts, occ_col);
+  p.row_grid = grid_for(p.row_blocks * ceil_div(n, kSubPts) * kSubPts, occ_row);
   if (const char* e = std::getenv("FCPD_ESTEP_TC")) p.tc = std::atoi(e) != 0;
   if (!p.centred) p.tc = 0;  // the tensor-core pass is the centred form
   if (p.tc) {

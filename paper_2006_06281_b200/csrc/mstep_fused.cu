@@ -30,7 +30,6 @@ namespace fcpd {
 namespace {
 constexpr int kFusedThreads = 512;
 constexpr int kFusedWarps = kFusedThreads / 32;
-constexpr int kRedLanes = 4;  // phase 3: threads per row in the slot reduction
 // phase 1: 12 doubles per thread; phase 3: 3 floats × S slots × (8·ng + 1)
 // padded rows, S·ng ≤ kFusedThreads
 constexpr int kFusedSmem = 3 * 9 * kFusedThreads * 4;
@@ -190,6 +189,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
     const int grp = tid / S, slot = tid % S;
     const bool on = grp < ng;
     const int rc = 8 * ng;  // rows per chunk
+    // lanes per row in the slot reduction: all the threads over the chunk's
+    // rows (a power of two ≤ 32: C1 4 lanes × 12 slots, C0 32 × 16)
+    int red_lanes = 1;
+    while (red_lanes < 32 && 2 * red_lanes * rc <= kFusedThreads) red_lanes *= 2;
     const int rcp = rc | 1;  // padded row stride of the partials
     const int64_t ld4 = a.kpad / 4;
     const float4* qrow = reinterpret_cast<const float4*>(a.q);
@@ -230,14 +233,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
         }
       }
       __syncthreads();
-      // kRedLanes threads per row sum interleaved slots (fp64), combined by
-      // a fixed xor tree; the group's first lane finalises the row
-      constexpr int kRowsPerPass = kFusedThreads / kRedLanes;
-      for (int pass = 0; pass * kRowsPerPass < rc; ++pass) {  // uniform trip count
-        const int rr = pass * kRowsPerPass + tid / kRedLanes;
+      // L threads per row sum interleaved slots (fp64), combined by a fixed
+      // xor tree; the group's first lane finalises the row
+      const int L = red_lanes, rows_per_pass = kFusedThreads / L;
+      for (int pass = 0; pass * rows_per_pass < rc; ++pass) {  // uniform trip count
+        const int rr = pass * rows_per_pass + tid / L;
         const int64_t i = cb + rr;
         const bool live = rr < rc && i < r1;
-        const int sub = tid % kRedLanes;
+        const int sub = tid % L;
         double o0 = 0.0, o1 = 0.0, o2 = 0.0, x00 = 0.0, x01 = 0.0, x02 = 0.0;
         double p0 = 0.0, p1 = 0.0, p2 = 0.0, vr = 0.0;
         if (live && sub == 0) {  // row data, in flight during the reduction
@@ -248,14 +251,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
         }
         double v0 = 0.0, v1 = 0.0, v2 = 0.0;
         if (live)
-          for (int j = sub; j < S; j += kRedLanes) {
+          for (int j = sub; j < S; j += L) {
             const float* v = vp + j * rcp + rr;
             v0 += v[0];
             v1 += v[S * rcp];
             v2 += v[2 * S * rcp];
           }
 #pragma unroll
-        for (int o = 1; o < kRedLanes; o <<= 1) {
+        for (int o = 1; o < L; o <<= 1) {
           v0 += __shfl_xor_sync(0xffffffffu, v0, o);
           v1 += __shfl_xor_sync(0xffffffffu, v1, o);
           v2 += __shfl_xor_sync(0xffffffffu, v2, o);
