@@ -1,0 +1,248 @@
+// Acceptance criteria 4-7 of the reference (proj/tests/acceptance.cpp:143-260)
+// run through the C++ drop-in header on the B200 engine.  The degradation
+// generators (degradations.hpp:17-137) are restated here as test-only
+// helpers, with the reference's RNG streams, so the inputs are the
+// reference's own.  Exit code 0 = all criteria passed; one line per check.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <numeric>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "fastcpd/fastcpd.hpp"
+
+using namespace fastcpd;
+
+static int g_fail = 0;
+static void report(const char* what, bool ok, const std::string& detail) {
+  std::printf("%s: %s — %s\n", ok ? "PASS" : "FAIL", what, detail.c_str());
+  if (!ok) ++g_fail;
+}
+
+// test_util.hpp:25-37
+static PointSet make_torus(Index m, unsigned long seed) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> u(0.0, 2.0 * M_PI);
+  PointSet ps;
+  ps.pts.resize(m, 3);
+  for (Index i = 0; i < m; ++i) {
+    const double a = u(rng), b = u(rng);
+    ps.pts(i, 0) = (1.0 + 0.35 * std::cos(b)) * std::cos(a);
+    ps.pts(i, 1) = (1.0 + 0.35 * std::cos(b)) * std::sin(a);
+    ps.pts(i, 2) = 0.35 * std::sin(b);
+  }
+  return ps;
+}
+
+// normalize_pair(p, p) (pointset.hpp:124-148): centroid and the largest
+// absolute coordinate deviation of the point set.
+static PointSet normalized(const PointSet& p) {
+  const Index m = p.count(), d = p.dim();
+  std::vector<double> c(static_cast<size_t>(d), 0.0);
+  for (Index i = 0; i < m; ++i)
+    for (Index j = 0; j < d; ++j) c[static_cast<size_t>(j)] += p.pts(i, j);
+  for (auto& v : c) v /= static_cast<double>(m);
+  double s = 0.0;
+  for (Index i = 0; i < m; ++i)
+    for (Index j = 0; j < d; ++j) s = std::max(s, std::fabs(p.pts(i, j) - c[static_cast<size_t>(j)]));
+  if (!(s > 0.0)) s = 1.0;
+  PointSet out = p;
+  for (Index i = 0; i < m; ++i)
+    for (Index j = 0; j < d; ++j) out.pts(i, j) = (p.pts(i, j) - c[static_cast<size_t>(j)]) / s;
+  return out;
+}
+
+// add_noise (degradations.hpp:17-27): i.i.d. Gaussian per coordinate, row order
+static PointSet noisy(const PointSet& p, double stddev, unsigned long seed) {
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> g(0.0, stddev);
+  PointSet out = p;
+  for (Index i = 0; i < out.count(); ++i)
+    for (Index j = 0; j < out.dim(); ++j) out.pts(i, j) += g(rng);
+  return out;
+}
+
+// add_outliers (degradations.hpp:31-53): floor(ratio·M) uniform draws from
+// the bounding box padded by 5 % per side, appended after the originals
+static PointSet with_outliers(const PointSet& p, double ratio, unsigned long seed) {
+  const Index m = p.count(), d = p.dim();
+  const Index extra = static_cast<Index>(std::floor(ratio * static_cast<double>(m)));
+  std::vector<double> lo(static_cast<size_t>(d), INFINITY), hi(static_cast<size_t>(d), -INFINITY);
+  for (Index i = 0; i < m; ++i)
+    for (Index j = 0; j < d; ++j) {
+      lo[static_cast<size_t>(j)] = std::min(lo[static_cast<size_t>(j)], p.pts(i, j));
+      hi[static_cast<size_t>(j)] = std::max(hi[static_cast<size_t>(j)], p.pts(i, j));
+    }
+  for (Index j = 0; j < d; ++j) {
+    const double pad = 0.05 * (hi[static_cast<size_t>(j)] - lo[static_cast<size_t>(j)]);
+    lo[static_cast<size_t>(j)] -= pad;
+    hi[static_cast<size_t>(j)] += pad;
+  }
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unit(0.0, 1.0);
+  PointSet out;
+  out.pts.resize(m + extra, d);
+  for (Index i = 0; i < m; ++i)
+    for (Index j = 0; j < d; ++j) out.pts(i, j) = p.pts(i, j);
+  for (Index i = 0; i < extra; ++i)
+    for (Index j = 0; j < d; ++j)
+      out.pts(m + i, j) = lo[static_cast<size_t>(j)] +
+                          unit(rng) * (hi[static_cast<size_t>(j)] - lo[static_cast<size_t>(j)]);
+  return out;
+}
+
+// occlude (degradations.hpp:58-84): drop the `count` points nearest a random
+// anchor (stable by distance), keep the rest in file order
+static PointSet occluded(const PointSet& p, Index count, unsigned long seed,
+                         std::vector<Index>& kept) {
+  const Index m = p.count(), d = p.dim();
+  std::mt19937_64 rng(seed);
+  std::uniform_int_distribution<Index> pick(0, m - 1);
+  const Index a = pick(rng);
+  std::vector<double> d2(static_cast<size_t>(m), 0.0);
+  for (Index i = 0; i < m; ++i)
+    for (Index j = 0; j < d; ++j) {
+      const double e = p.pts(i, j) - p.pts(a, j);
+      d2[static_cast<size_t>(i)] += e * e;
+    }
+  std::vector<Index> order(static_cast<size_t>(m));
+  std::iota(order.begin(), order.end(), Index(0));
+  std::stable_sort(order.begin(), order.end(), [&](Index x, Index y) {
+    return d2[static_cast<size_t>(x)] < d2[static_cast<size_t>(y)];
+  });
+  order.erase(order.begin(), order.begin() + count);
+  std::sort(order.begin(), order.end());
+  kept = order;
+  PointSet out;
+  out.pts.resize(static_cast<Index>(kept.size()), d);
+  for (size_t i = 0; i < kept.size(); ++i)
+    for (Index j = 0; j < d; ++j) out.pts(static_cast<Index>(i), j) = p.pts(kept[i], j);
+  return out;
+}
+
+// synth_deform (degradations.hpp:89-123): ceil(M/50) control points drawn
+// from the set, N(0, amplitude²) coefficients, Gaussian-RBF displacement
+static DegradedPair deformed(const PointSet& p, double amplitude, double warp_beta,
+                             unsigned long seed) {
+  const Index m = p.count(), d = p.dim(), nc = (m + 49) / 50;
+  std::mt19937_64 rng(seed);
+  std::uniform_int_distribution<Index> pick(0, m - 1);
+  std::normal_distribution<double> g(0.0, amplitude);
+  std::vector<Index> ctr(static_cast<size_t>(nc));
+  for (auto& c : ctr) c = pick(rng);
+  std::vector<double> coeff(static_cast<size_t>(nc * d));
+  for (Index c = 0; c < nc; ++c)
+    for (Index j = 0; j < d; ++j) coeff[static_cast<size_t>(c * d + j)] = g(rng);
+  DegradedPair pair;
+  pair.model = p;
+  pair.scene = p;
+  const double inv = 1.0 / (2.0 * warp_beta * warp_beta);
+  for (Index i = 0; i < m; ++i) {
+    for (Index c = 0; c < nc; ++c) {
+      double r2 = 0.0;
+      for (Index j = 0; j < d; ++j) {
+        const double e = p.pts(ctr[static_cast<size_t>(c)], j) - p.pts(i, j);
+        r2 += e * e;
+      }
+      const double k = std::exp(-r2 * inv);
+      for (Index j = 0; j < d; ++j) pair.scene.pts(i, j) += coeff[static_cast<size_t>(c * d + j)] * k;
+    }
+  }
+  for (Index i = 0; i < m; ++i) {
+    std::vector<double> t(static_cast<size_t>(d));
+    for (Index j = 0; j < d; ++j) t[static_cast<size_t>(j)] = pair.scene.pts(i, j);
+    pair.truth[i] = t;
+  }
+  return pair;
+}
+
+static double seconds_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+int main() {
+  char buf[256];
+  {  // criterion 4 (acceptance.cpp:143-157): affine-perturbed torus
+    const auto t0 = std::chrono::steady_clock::now();
+    const DegradedPair pair = make_bench_pair(make_torus(600, 42), 500, 42);
+    RegistrationConfig cfg;
+    cfg.iterations = 50;
+    const RegistrationResult res = register_pointsets(pair.model, pair.scene, cfg);
+    const double err = rmse(res.transformed, pair.truth), secs = seconds_since(t0);
+    std::snprintf(buf, sizeof buf, "rmse %.3g (< 5e-3), %.2f s", err, secs);
+    report("criterion 4: affine registration accuracy", err < 5e-3 && secs < 60.0, buf);
+  }
+  {  // criterion 5 (acceptance.cpp:159-198): deform + noise/outliers/occlusion
+    const PointSet base = normalized(make_torus(500, 77));
+    const DegradedPair def = deformed(base, 0.1, 2.0, 7);
+    struct Case {
+      const char* name;
+      PointSet model, scene;
+      Truth truth;
+    };
+    std::vector<Case> cases;
+    cases.push_back({"deform", def.model, def.scene, def.truth});
+    cases.push_back({"deform+noise", def.model, noisy(def.scene, 0.1, 8), def.truth});
+    cases.push_back({"deform+outliers", def.model, with_outliers(def.scene, 0.6, 9), def.truth});
+    {
+      std::vector<Index> kept;
+      PointSet occ = occluded(def.model, 100, 10, kept);  // 20 % of 500
+      Truth truth;
+      for (size_t i = 0; i < kept.size(); ++i) truth[static_cast<Index>(i)] = def.truth.at(kept[i]);
+      cases.push_back({"deform+occlusion", occ, def.scene, truth});
+    }
+    bool ok = true;
+    std::string detail;
+    for (const auto& c : cases) {
+      RegistrationConfig cfg;
+      cfg.iterations = 100;
+      const RegistrationResult res = register_pointsets(c.model, c.scene, cfg);
+      const double err = rmse(res.transformed, c.truth);
+      std::snprintf(buf, sizeof buf, "%s %.3g ", c.name, err);
+      detail += buf;
+      ok = ok && err < 0.05;
+    }
+    report("criterion 5: degradation robustness rmse < 0.05", ok, detail);
+  }
+  {  // criteria 6 + 7 (acceptance.cpp:200-260): the benchmark sweep.  The
+     // O(M³) cpd baseline is out of scope on the device path (its cells are
+     // recorded as failed), so criterion 6 checks the fast variants' order.
+    const auto t0 = std::chrono::steady_clock::now();
+    RegistrationConfig cfg;
+    cfg.iterations = 20;
+    const std::vector<Index> sizes = {500, 1000, 2000, 4000};
+    const std::vector<SolverVariant> variants = {SolverVariant::fast_lowrank, SolverVariant::fast,
+                                                 SolverVariant::cpd};
+    const std::vector<BenchRecord> recs = run_benchmark(make_torus(4000, 11), sizes, variants, cfg, 12);
+    const double secs = seconds_since(t0);
+    auto t_iter = [&](Index m, SolverVariant v) {
+      for (const auto& r : recs)
+        if (r.m == m && r.variant == v && !r.failed) return r.timing.t_iter;
+      return -1.0;
+    };
+    bool order = true, cpd_failed = true;
+    std::string detail;
+    for (Index m : sizes) {
+      const double fl = t_iter(m, SolverVariant::fast_lowrank), f = t_iter(m, SolverVariant::fast);
+      std::snprintf(buf, sizeof buf, "M=%lld fl %.3g s f %.3g s; ", static_cast<long long>(m), fl, f);
+      detail += buf;
+      if (m >= 1000) order = order && fl >= 0.0 && f >= 0.0 && fl <= f;
+      cpd_failed = cpd_failed && t_iter(m, SolverVariant::cpd) < 0.0;
+    }
+    std::snprintf(buf, sizeof buf, "(%.1f s)", secs);
+    report("criterion 6: t_iter(fast_lowrank) <= t_iter(fast) for M >= 1000",
+           order && cpd_failed && secs < 600.0, detail + buf);
+    bool ident = true;
+    for (const auto& r : recs) {
+      if (r.failed) continue;
+      const TimingBreakdown& t = r.timing;
+      ident = ident && t.t_f == t.t_eig + t.t_iter && t.t_total == t.t_c + t.t_f + t.t_o;
+    }
+    report("criterion 7: timing identities hold exactly", ident,
+           std::to_string(recs.size()) + " records");
+  }
+  return g_fail == 0 ? 0 : 1;
+}

@@ -7,20 +7,21 @@ import subprocess
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SRC = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
-OUT = os.path.join(ROOT, "tests", "cpp", "build", "test_dropin")
 LIBDIR = os.path.join(ROOT, "paper_2006_06281_b200", "lib")
 
 
-def build_dropin():
+def build_dropin(name="test_dropin"):
+    """Compile tests/cpp/<name>.cpp against the drop-in header and the engine."""
+    src = os.path.join(ROOT, "tests", "cpp", name + ".cpp")
+    out = os.path.join(ROOT, "tests", "cpp", "build", name)
     subprocess.run(["make", "-s", "-j8", "-C", os.path.join(ROOT, "paper_2006_06281_b200")],
                    check=True)
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
     subprocess.run([cxx, "-std=c++17", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
-                    SRC, "-L", LIBDIR, "-lfcpd_b200", f"-Wl,-rpath,{LIBDIR}", "-o", OUT],
+                    src, "-L", LIBDIR, "-lfcpd_b200", f"-Wl,-rpath,{LIBDIR}", "-o", out],
                    check=True)
-    return OUT
+    return out
 
 
 def test_dropin_header_compiles_and_links():
@@ -34,3 +35,20 @@ def test_dropin_reference_tests_pass_on_gpu():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "FAIL" not in r.stdout
+
+
+def test_acceptance_program_compiles_and_links():
+    assert os.path.exists(build_dropin("test_acceptance"))
+
+
+@pytest.mark.gpu
+def test_acceptance_criteria_4_to_7_on_gpu():
+    """acceptance.cpp:143-260 through the drop-in header: affine accuracy
+    (rmse < 5e-3), robustness under deform/noise/outliers/occlusion
+    (rmse < 0.05), t_iter(fast_lowrank) <= t_iter(fast) for M >= 1000, and
+    the exact timing identities of every benchmark record."""
+    exe = build_dropin("test_acceptance")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("PASS") == 4 and "FAIL" not in r.stdout
