@@ -51,6 +51,7 @@ constexpr float kPadCoord = 3.0e18f;  // padding point: t ≈ 1e37, 2^-t = 0
 constexpr int kListThreads = 256;     // list kernels: one CTA per own block
 static_assert(kListThreads == kTilePts, "list CTA: one thread per own point");
 constexpr int kProbeTiles = 2;        // other-set tiles probed for the exact culling bound
+constexpr int kFlush2 = 64;  // pass-2 fp32 run length (staged points; tools/gpu_flush.sh)
 constexpr int64_t kMinPtsPerCta = 256;  // stream-K grid: dense point-units per CTA, at least (one chunk)
 // Probe policy (speed only; any probe decision keeps the bound exact): probe
 // a block when the tiles the box bound keeps but U = 0 would drop are ≥ 1/2
@@ -491,7 +492,8 @@ template <int NP>
 __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
     estep_row_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4b,
                      int64_t n, const IterState* __restrict__ st, WorkList wl,
-                     double* __restrict__ seg /* [slot][5][256] */, float centred_max_r2) {
+                     double* __restrict__ seg /* [slot][5][256] */, float centred_max_r2,
+                     int flush) {
   griddep_wait();
   constexpr int kThr = 128 / NP;   // threads
   constexpr int kRows = 2 * NP;    // rows per thread
@@ -597,8 +599,30 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
 #pragma unroll
       for (int q2 = 0; q2 < NP; ++q2)
         f0[q2] = fx[q2] = fy[q2] = fz[q2] = fv[q2] = make_float2(0.f, 0.f);
+      // the fp32 sums go to fp64 every `flush` staged points (a power of
+      // two) and at the end of the chunk: the centred form's conversion to
+      // Σw·t cancels terms of size R², so the fp32 run length sets the
+      // precision of the σ² terms (EStepPlan::flush2)
+      auto flush_rows = [&]() {
+#pragma unroll
+        for (int q2 = 0; q2 < NP; ++q2) {
+          const int h0 = 2 * q2, h1 = 2 * q2 + 1;
+          acc_s[0][h0][t] += f0[q2].x;
+          acc_s[0][h1][t] += f0[q2].y;
+          acc_s[1][h0][t] += fx[q2].x;
+          acc_s[1][h1][t] += fx[q2].y;
+          acc_s[2][h0][t] += fy[q2].x;
+          acc_s[2][h1][t] += fy[q2].y;
+          acc_s[3][h0][t] += fz[q2].x;
+          acc_s[3][h1][t] += fz[q2].y;
+          acc_s[4][h0][t] += fv[q2].x;
+          acc_s[4][h1][t] += fv[q2].y;
+          f0[q2] = fx[q2] = fy[q2] = fz[q2] = fv[q2] = make_float2(0.f, 0.f);
+        }
+      };
       if (centred) {
         for (int j = 0; j < cnt8; j += 8) {
+          if (j > 0 && (j & (flush - 1)) == 0) flush_rows();  // uniform
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const float4 A = ya[j + u];
@@ -624,6 +648,7 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
         }
       } else {
         for (int j = 0; j < cnt8; j += 8) {
+          if (j > 0 && (j & (flush - 1)) == 0) flush_rows();  // uniform
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const float4 A = ya[j + u];
@@ -649,20 +674,7 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
           }
         }
       }
-#pragma unroll
-      for (int q2 = 0; q2 < NP; ++q2) {
-        const int h0 = 2 * q2, h1 = 2 * q2 + 1;
-        acc_s[0][h0][t] += f0[q2].x;
-        acc_s[0][h1][t] += f0[q2].y;
-        acc_s[1][h0][t] += fx[q2].x;
-        acc_s[1][h1][t] += fx[q2].y;
-        acc_s[2][h0][t] += fy[q2].x;
-        acc_s[2][h1][t] += fy[q2].y;
-        acc_s[3][h0][t] += fz[q2].x;
-        acc_s[3][h1][t] += fz[q2].y;
-        acc_s[4][h0][t] += fv[q2].x;
-        acc_s[4][h1][t] += fv[q2].y;
-      }
+      flush_rows();
     }
     // segment out: S0, Σw·y', Σw·t per own row
     double* out = seg + (g + rb) * 5 * kTile;
@@ -1360,6 +1372,15 @@ EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
   };
   p.col_grid = grid_for(p.col_blocks * ceil_div(m, kSubPts) * kSubPts, occ_col);
   p.row_grid = grid_for(p.row_blocks * ceil_div(n, kSubPts) * kSubPts, occ_row);
+  // fp32 run length of the pass-2 sums before they go to fp64
+  auto flush_env = [](const char* name, int def) {
+    const char* e = std::getenv(name);
+    const int v = e ? std::atoi(e) : def;
+    int f = 8;  // a power of two in [8, 256]
+    while (f < kTile && 2 * f <= v) f *= 2;
+    return f;
+  };
+  p.flush2 = flush_env("FCPD_FLUSH2", kFlush2);
   if (const char* e = std::getenv("FCPD_ESTEP_TC")) p.tc = std::atoi(e) != 0;
   if (!p.centred) p.tc = 0;  // the tensor-core pass is the centred form
   if (p.tc) {
@@ -1454,10 +1475,10 @@ void launch_row_cc(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t
                    IterState* st, const WorkList& wl, double* seg, cudaStream_t stream) {
   if (p.row_pairs == 2)
     launch_pdl(estep_row_kernel<2>, dim3(p.row_grid), dim3(64), 0, stream, b.xt4, m, b.y4b, n, st,
-               wl, seg, p.centred_max_r2);
+               wl, seg, p.centred_max_r2, p.flush2);
   else
     launch_pdl(estep_row_kernel<1>, dim3(p.row_grid), dim3(128), 0, stream, b.xt4, m, b.y4b, n, st,
-               wl, seg, p.centred_max_r2);
+               wl, seg, p.centred_max_r2, p.flush2);
 }
 
 void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int64_t m,

@@ -73,6 +73,7 @@ struct EStepPlan {
   int tc = 0;       // pass 2 on tcgen05 (estep_tc.cu) for blocks within kCentredMaxR2
   int row_pairs = 2;  // CUDA-core pass 2: packed row pairs per thread (FCPD_ROW_PAIRS=1 → 1)
   int col_pairs = 2;  // pass 1: packed column pairs per thread (FCPD_COL_PAIRS=1 → 1)
+  int flush2 = 64;  // fp32 run length of the pass-2 sums (FCPD_FLUSH2, power of two)
   int col_blocks = 0, row_blocks = 0;  // scene tiles (pass-1 blocks), model tiles (pass 2)
   int col_grid = 0, row_grid = 0;      // persistent CTAs per pass (CUDA-core kernels)
   int tc_grid = 0;                     // persistent CTAs of the tensor-core pass 2
