@@ -643,12 +643,20 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
     Basis& b = ctx->basis;
     s.zp = make_colsum_plan(m, b.k, ctx->sm_count);
     s.vp = make_colsum_plan(b.k, m, ctx->sm_count);
+    // The fused M-step pays where the streamed basis is small enough that
+    // the two passes are latency-bound and its re-read of Q hits L2: a basis
+    // ≤ 64 MB, or a truncated one over M ≤ 32k rows (FCPD_MSTEP_FUSED=0/1).
+    const double qbytes = 4.0 * static_cast<double>(m) * static_cast<double>(b.k);
+    s.mfused = qbytes <= 64.0 * (1 << 20) || (s.cfg.spectral_tau > 0.0 && m <= 32768);
+    if (const char* e = std::getenv("FCPD_MSTEP_FUSED")) s.mfused = std::atoi(e) != 0;
     // spectral truncation: the basis streams stop where the filter drops
-    // below tau (mstep.cu: spectral_rank_kernel); FCPD_SPECTRAL_TAU=0 → off
+    // below tau (mstep.cu: spectral_rank_kernel; phase 0 of the fused
+    // kernel).  A basis under 64 MB on the streaming path streams in
+    // microseconds, so there its extra kernel would cost more than it saves;
+    // the fused kernel's search is free (C0: 13.4k → 15.2k it/s).
+    // FCPD_SPECTRAL_TAU=0 → off
     s.tau = s.cfg.spectral_tau;
-    // a basis under 64 MB streams in microseconds: truncating it saves less
-    // than its extra kernel costs
-    if (4.0 * static_cast<double>(m) * static_cast<double>(b.k) < 64.0 * (1 << 20)) s.tau = 0.0;
+    if (!s.mfused && qbytes < 64.0 * (1 << 20)) s.tau = 0.0;
     if (const char* e = std::getenv("FCPD_SPECTRAL_TAU")) s.tau = std::atof(e);  // A/B
     s.zp.trunc = s.tau > 0.0 ? 1 : 0;
     s.vp.trunc = s.tau > 0.0 ? 2 : 0;
@@ -656,12 +664,6 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
     s.vpart.ensure(s.vp.part_doubles());
     s.coef.ensure(3 * b.k);
     s.g4.ensure(b.k);
-    // The fused M-step pays where the streamed basis is small enough that
-    // the two passes are latency-bound and its re-read of Q hits L2: a basis
-    // ≤ 64 MB, or a truncated one over M ≤ 32k rows (FCPD_MSTEP_FUSED=0/1).
-    const double qbytes = 4.0 * static_cast<double>(m) * static_cast<double>(b.k);
-    s.mfused = qbytes <= 64.0 * (1 << 20) || (s.zp.trunc && m <= 32768);
-    if (const char* e = std::getenv("FCPD_MSTEP_FUSED")) s.mfused = std::atoi(e) != 0;
     if (s.mfused) {
       s.mfused_grid = mstep_fused_grid(ctx->sm_count);
       s.zpart_fused.ensure(static_cast<size_t>(b.k) * s.mfused_grid * 3);

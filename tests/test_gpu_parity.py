@@ -396,16 +396,19 @@ def test_distributed_engine_single_rank(ctx, fc, orc, monkeypatch, variant, omeg
 # ------------------------------------------ fused M-step (mstep_fused.cu)
 
 
-@pytest.mark.parametrize("name,m,iters", [("c0", 2000, 50), ("c1", 5000, 60),
-                                          ("c1", 4000, 30), ("c2", 12000, 40)])
-def test_fused_mstep_matches_streaming(ctx, fc, monkeypatch, name, m, iters):
+@pytest.mark.parametrize("name,m,iters,tau", [("c0", 2000, 50, None), ("c1", 5000, 60, None),
+                                              ("c1", 4000, 30, "0"), ("c2", 12000, 40, None)])
+def test_fused_mstep_matches_streaming(ctx, fc, monkeypatch, name, m, iters, tau):
     """The cooperative one-kernel M-step against the streaming one (two basis
-    passes + reduce/filter/transform/σ² kernels): full rank (C0), truncated
+    passes + reduce/filter/transform/σ² kernels): full rank (C0; the fused
+    path truncates its 16 MB basis, the streaming one does not), truncated
     full rank (C1, 100 MB basis), untruncated K = 4000 (g staged in 64 KB of
     shared memory), low rank (C2).  Same σ² trace and points
     inside the parity bar, and 4 fewer kernels per iteration (5 with the
     spectral-rank kernel)."""
     from paper_2006_06281_b200 import datagen
+    if tau is not None:
+        monkeypatch.setenv("FCPD_SPECTRAL_TAU", tau)
     x, y, w = datagen.generate(name, m=m)
     cfg = datagen.config_for(w, iterations=iters)
     monkeypatch.setenv("FCPD_MSTEP_FUSED", "0")

@@ -4,7 +4,7 @@ import os, sys
 sys.path.insert(0, '/root/repo')
 import paper_2006_06281_b200 as fcpd
 from paper_2006_06281_b200 import datagen
-x, y, w = datagen.generate('c1')
+x, y, w = datagen.generate(sys.argv[1] if len(sys.argv) > 1 else 'c1')
 ctx = fcpd.Context(0)
 for fused in ('1', '0'):
     os.environ['FCPD_MSTEP_FUSED'] = fused
@@ -12,4 +12,4 @@ for fused in ('1', '0'):
     r = ctx.register(x, y, cfg)
     r = ctx.register(x, y, cfg)
     t = r.timing
-    print('fused' if fused == '1' else 'stream', {k: round(getattr(t, k) * 1e4, 2) for k in ('t_c', 't_iter', 't_o')}, '(us per iteration)')
+    print(w.name if hasattr(w, 'name') else '', 'fused' if fused == '1' else 'stream', {k: round(getattr(t, k) * 1e4, 2) for k in ('t_c', 't_iter', 't_o')}, '(us per iteration)')
