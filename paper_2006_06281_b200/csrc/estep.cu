@@ -918,14 +918,16 @@ __device__ __forceinline__ int probe_tiles(float4 lo, float4 hi, const float4* o
   return count;
 }
 
-// Append the kept tiles j (keep(j) uniform per j) to out[]; returns the count.
-template <typename Keep>
-__device__ __forceinline__ int cta_compact(int n_other, int32_t* out, int* wcount, Keep keep) {
+// Append entry(j) for j < n, in order, to out[], skipping those that are
+// −1 (entry(j) uniform per j); returns the count.
+template <typename Entry>
+__device__ __forceinline__ int cta_compact(int n, int32_t* out, int* wcount, Entry entry) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int count = 0;
-  for (int j0 = 0; j0 < n_other; j0 += kListThreads) {
+  for (int j0 = 0; j0 < n; j0 += kListThreads) {
     const int j = j0 + threadIdx.x;
-    const bool k = j < n_other && keep(j);
+    const int32_t e = j < n ? entry(j) : -1;
+    const bool k = e >= 0;
     const unsigned mask = __ballot_sync(0xffffffffu, k);
     __syncthreads();  // previous chunk's wcount readers are done
     if (lane == 0) wcount[warp] = __popc(mask);
@@ -935,10 +937,42 @@ __device__ __forceinline__ int cta_compact(int n_other, int32_t* out, int* wcoun
       before += w < warp ? wcount[w] : 0;
       total += wcount[w];
     }
-    if (k) out[count + before + __popc(mask & ((1u << lane) - 1))] = j;
+    if (k) out[count + before + __popc(mask & ((1u << lane) - 1))] = e;
     count += total;
   }
   return count;
+}
+
+// The units a list kernel visits after its tile-level screen: the units of
+// the surviving 256-point tiles (a tile's units are boxes inside its box,
+// so a bound that drops the tile drops them).  With few enough tiles the
+// survivors are compacted into shared memory and only their units are
+// visited; otherwise every unit is visited and screened by its tile.
+constexpr int kMaxCandTiles = 4096;
+struct UnitWalk {
+  const int32_t* cand;  // surviving tiles (shared memory), or nullptr
+  int n_work, upt, n_units;
+  // unit of work item i, or −1 (past the end / screened out)
+  template <typename TileIn>
+  __device__ __forceinline__ int unit(int i, TileIn tile_in) const {
+    if (cand) {
+      const int u = cand[i / upt] * upt + i % upt;
+      return u < n_units ? u : -1;
+    }
+    return tile_in(i / upt) ? i : -1;
+  }
+};
+template <typename TileIn>
+__device__ __forceinline__ UnitWalk unit_walk(int n_tiles, int upt, int n_units, int32_t* cand_s,
+                                              int* wcount, TileIn tile_in) {
+  UnitWalk w{nullptr, n_units, upt, n_units};
+  if (n_tiles <= kMaxCandTiles) {
+    const int nc = cta_compact(n_tiles, cand_s, wcount, [&](int j) { return tile_in(j) ? j : -1; });
+    __syncthreads();  // publish cand_s
+    w.cand = cand_s;
+    w.n_work = nc * upt;
+  }
+  return w;
 }
 
 // Probe staging: candidate points centred on the own block's box centre,
@@ -979,7 +1013,9 @@ __device__ __forceinline__ float probe_scan(const float4* pa, const float4* pb, 
 // Pass-1 list, one CTA per scene block b.  Every column n of the block has
 // total ≥ max(2^{−t_min(n)}, 2^{log2 c}); the bound uses U ≥ max_n
 // min_m ‖y_n − x̃_m‖², the smaller of
-//  * the box bound min over model sub-tiles j of maxdist²(b, j), and
+//  * the box bound min over model sub-tiles j of maxdist²(b, j) (taken over
+//    the sub-tiles of the tiles a first, tile-level bound keeps: the
+//    minimising sub-tile always lies in one), and
 //  * the probe: the exact nearest distance of every column to the points of
 //    the kProbeTiles model tiles nearest the block (padded up by 2^-16),
 // and model sub-tile j is dropped when s²·mindist²(b, j) > min(s²U, −log2 c)
@@ -1001,14 +1037,28 @@ __global__ void __launch_bounds__(kListThreads)
   const int b = blockIdx.x;
   const float4 lo = cull.ylo[b], hi = cull.yhi[b];
   const float neg_log2c = static_cast<float>(-st->log2c);  // +inf when ω = 0
-  float u = INFINITY, far = 0.f;
-  for (int j = threadIdx.x; j < cull.n_xsub; j += kListThreads) {
-    const float4 jl = cull.sxlo[j], jh = cull.sxhi[j];
-    u = fminf(u, box_maxdist2(lo, hi, jl, jh));
+  // tile level: U_t ≥ U and the cut it gives (≥ every later cut) screen
+  // the model tiles; only the survivors' sub-tiles are read below
+  float ut = INFINITY, far = 0.f;
+  for (int j = threadIdx.x; j < cull.n_xtiles; j += kListThreads) {
+    const float4 jl = cull.xlo[j], jh = cull.xhi[j];
+    ut = fminf(ut, box_maxdist2(lo, hi, jl, jh));
     far = fmaxf(far, box_mindist2(lo, hi, jl, jh));
   }
-  u = cta_reduce<false>(u, shf);
+  ut = cta_reduce<false>(ut, shf);
   far = cta_reduce<true>(far, shf);
+  const float cut_t = fminf(s2 * ut, neg_log2c) + cull.margin1;
+  auto tile_in = [&](int j) {
+    return !(s2 * box_mindist2(lo, hi, cull.xlo[j], cull.xhi[j]) > cut_t);
+  };
+  __shared__ int32_t cand_s[kMaxCandTiles];
+  const UnitWalk walk = unit_walk(cull.n_xtiles, kSubPerTile, cull.n_xsub, cand_s, wcount, tile_in);
+  float u = ut;
+  for (int i = threadIdx.x; i < walk.n_work; i += kListThreads) {
+    const int sj = walk.unit(i, tile_in);
+    if (sj >= 0) u = fminf(u, box_maxdist2(lo, hi, cull.sxlo[sj], cull.sxhi[sj]));
+  }
+  u = cta_reduce<false>(u, shf);
   // Probe only where it can pay (policy above): the tiles the box bound
   // keeps but U = 0 would drop bound what the probe can drop.
   bool useful = s2 * far > fminf(0.f, neg_log2c) + cull.margin1;
@@ -1018,9 +1068,11 @@ __global__ void __launch_bounds__(kListThreads)
   if (useful) {
     const float cut_box = fminf(s2 * u, neg_log2c) + cull.margin1;
     const float cut_min = fminf(0.f, neg_log2c) + cull.margin1;
-    float2 k = make_float2(0.f, 0.f);  // (kept, contested)
-    for (int j = threadIdx.x; j < cull.n_xsub; j += kListThreads) {
-      const float t = s2 * box_mindist2(lo, hi, cull.sxlo[j], cull.sxhi[j]);
+    float2 k = make_float2(0.f, 0.f);  // (kept, contested) sub-tiles
+    for (int i = threadIdx.x; i < walk.n_work; i += kListThreads) {
+      const int sj = walk.unit(i, tile_in);
+      if (sj < 0) continue;
+      const float t = s2 * box_mindist2(lo, hi, cull.sxlo[sj], cull.sxhi[sj]);
       k.x += t <= cut_box ? 1.f : 0.f;
       k.y += t <= cut_box && t > cut_min ? 1.f : 0.f;
     }
@@ -1064,11 +1116,13 @@ __global__ void __launch_bounds__(kListThreads)
   if (np > 0) u = fminf(u, probe);
   const float floor_t = fminf(s2 * u, neg_log2c);
   const float cut = floor_t + cull.margin1;
-  const int count = cta_compact(cull.n_xsub, tiles + static_cast<int64_t>(b) * cull.n_xsub,
-                                wcount, [&](int j) {
-                                  return !(s2 * box_mindist2(lo, hi, cull.sxlo[j], cull.sxhi[j]) >
-                                           cut);
-                                });
+  // (cut ≤ cut_t: the kept units lie in the walk's tiles)
+  const int count = cta_compact(
+      walk.n_work, tiles + static_cast<int64_t>(b) * cull.n_xsub, wcount, [&](int i) {
+        const int sj = walk.unit(i, tile_in);
+        return sj >= 0 && !(s2 * box_mindist2(lo, hi, cull.sxlo[sj], cull.sxhi[sj]) > cut) ? sj
+                                                                                          : -1;
+      });
   if (threadIdx.x == 0) {
     offset[b + 1] = count;
     if (np > 0 && cull.probe_paid1)
@@ -1080,7 +1134,8 @@ __global__ void __launch_bounds__(kListThreads)
 // Pass-2 list, one CTA per model block b, over units of the scene (32-point
 // sub-tiles; 256-point tiles for the tensor-core pass: ulo/uhi/ubm, n_units).
 // Every row m of the block has max_n L_mn ≥ L_lb, the larger of
-//  * the box bound max over scene units j of (min b − s²·maxdist²(b, j)),
+//  * the box bound max over scene units j of (min b − s²·maxdist²(b, j))
+//    (over the units of the tiles a first, tile-level bound keeps),
 //  * the probe: min over the block's rows of the exact max of b_n − s²‖y_n −
 //    x̃_m‖² over the kProbeTiles scene tiles nearest the block (less a
 //    rounding slack);
@@ -1105,19 +1160,36 @@ __global__ void __launch_bounds__(kListThreads)
   __shared__ float2 sh2[kListThreads / 32];
   const float s2 = st->sx * st->sx;
   const int b = blockIdx.x;
-  const float4 lo = cull.xlo[b], hi = cull.xhi[b];
+  const float4 lo = cull.xlo[b], hi = cull.xhi[b];  // (pass 2: the model block)
+  const int upt = kSubPerTile / unit_mult;  // units per scene tile (8, or 1: whole tiles)
+  // a scene tile's largest possible L (its units' are no larger)
+  auto tile_top = [&](int j) {
+    return cull.bminmax[j].y - s2 * box_mindist2(lo, hi, cull.ylo[j], cull.yhi[j]);
+  };
   float floor_l = -INFINITY, kept_box = 0.f;
+  float floor_t = -INFINITY;  // tile-level floor (≤ floor_l): screens the tiles
+  auto tile_in = [&](int j) { return !cull.enabled || !(tile_top(j) < floor_t); };
+  __shared__ int32_t cand_s[kMaxCandTiles];
+  UnitWalk walk{nullptr, n_units, upt, n_units};  // culling off: every unit
   int np = 0;
   if (cull.enabled) {
-    float l = -INFINITY, lmin = INFINITY;
-    for (int j = threadIdx.x; j < n_units; j += kListThreads) {
-      const float4 jl = ulo[j], jh = uhi[j];
-      const float2 bm = ubm[j];
-      l = fmaxf(l, bm.x - s2 * box_maxdist2(lo, hi, jl, jh));
+    float lt = -INFINITY, lmin = INFINITY;
+    for (int j = threadIdx.x; j < cull.n_ytiles; j += kListThreads) {
+      const float4 jl = cull.ylo[j], jh = cull.yhi[j];
+      const float2 bm = cull.bminmax[j];
+      lt = fmaxf(lt, bm.x - s2 * box_maxdist2(lo, hi, jl, jh));
       lmin = fminf(lmin, bm.y - s2 * box_mindist2(lo, hi, jl, jh));
     }
-    l = cta_reduce<true>(l, shf);
+    lt = cta_reduce<true>(lt, shf);
     lmin = cta_reduce<false>(lmin, shf);
+    floor_t = lt - cull.margin2;
+    walk = unit_walk(cull.n_ytiles, upt, n_units, cand_s, wcount, tile_in);
+    float l = lt;
+    for (int i = threadIdx.x; i < walk.n_work; i += kListThreads) {
+      const int u = walk.unit(i, tile_in);
+      if (u >= 0) l = fmaxf(l, ubm[u].x - s2 * box_maxdist2(lo, hi, ulo[u], uhi[u]));
+    }
+    l = cta_reduce<true>(l, shf);
     // L ≤ 0, so a tile can only be dropped if its bound is below −margin;
     // probe policy as in pass 1, with L_lb = 0 as the optimistic bound
     bool useful = lmin < -cull.margin2;
@@ -1126,8 +1198,10 @@ __global__ void __launch_bounds__(kListThreads)
     if (useful) {
       const float floor_box = l - cull.margin2;
       float2 k = make_float2(0.f, 0.f);
-      for (int j = threadIdx.x; j < n_units; j += kListThreads) {
-        const float v = ubm[j].y - s2 * box_mindist2(lo, hi, ulo[j], uhi[j]);
+      for (int i = threadIdx.x; i < walk.n_work; i += kListThreads) {
+        const int u = walk.unit(i, tile_in);
+        if (u < 0) continue;
+        const float v = ubm[u].y - s2 * box_mindist2(lo, hi, ulo[u], uhi[u]);
         k.x += v >= floor_box ? 1.f : 0.f;
         k.y += v >= floor_box && v < -cull.margin2 ? 1.f : 0.f;
       }
@@ -1172,9 +1246,14 @@ __global__ void __launch_bounds__(kListThreads)
     if (np > 0) l = fmaxf(l, probe - 1e-3f - 1e-5f * fabsf(probe) - 0x1p-20f * s2 * (h2 + vmax));
     floor_l = l - cull.margin2;
   }
+  // (floor_l ≥ floor_t: the kept units lie in the walk's tiles)
   const int count = cta_compact(
-      n_units, tiles + static_cast<int64_t>(b) * n_units, wcount, [&](int j) {
-        return !cull.enabled || !(ubm[j].y - s2 * box_mindist2(lo, hi, ulo[j], uhi[j]) < floor_l);
+      walk.n_work, tiles + static_cast<int64_t>(b) * n_units, wcount, [&](int i) {
+        const int u = walk.unit(i, tile_in);
+        return u >= 0 && (!cull.enabled ||
+                          !(ubm[u].y - s2 * box_mindist2(lo, hi, ulo[u], uhi[u]) < floor_l))
+                   ? u
+                   : -1;
       });
   if (threadIdx.x == 0) {
     bool to_tc = true;
