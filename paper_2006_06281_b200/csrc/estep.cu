@@ -46,7 +46,7 @@ namespace fcpd {
 namespace {
 
 constexpr int kTile = kTilePts;  // points staged in shared memory per step
-constexpr int kCombineLanes = 8; // lanes cooperating on one row/column reduction
+constexpr int kCombineLanes = 1; // lanes cooperating on one row/column reduction
 constexpr float kPadCoord = 3.0e18f;  // padding point: t ≈ 1e37, 2^-t = 0
 constexpr int kListThreads = 256;     // list kernels: one CTA per own block
 static_assert(kListThreads == kTilePts, "list CTA: one thread per own point");
@@ -385,7 +385,8 @@ __device__ __forceinline__ void sum_segments(const WorkList& wl, int64_t G, cons
     if (ua < ub) {
       const int64_t g0 = sk_owner(ua, G, P), g1 = sk_owner(ub - 1, G, P);
       for (int64_t g = g0 + lane; g <= g1; g += kCombineLanes) {
-        if (sk_start(g, G, P) == sk_start(g + 1, G, P)) continue;  // empty range
+        // an empty range needs P < G (a range holds ⌊P/G⌋ or ⌈P/G⌉ units)
+        if (P < G && sk_start(g, G, P) == sk_start(g + 1, G, P)) continue;
         const double* sp = seg + (g + b) * NQ * kTile + li;
 #pragma unroll
         for (int k = 0; k < NQ; ++k) a[k] += sp[k * kTile];
