@@ -1038,8 +1038,9 @@ __global__ void __launch_bounds__(kListThreads)
   const int b = blockIdx.x;
   const float4 lo = cull.ylo[b], hi = cull.yhi[b];
   const float neg_log2c = static_cast<float>(-st->log2c);  // +inf when ω = 0
-  // tile level: U_t ≥ U and the cut it gives (≥ every later cut) screen
-  // the model tiles; only the survivors' sub-tiles are read below
+  // tile level: U_t ≥ U (box bound over whole tiles), then the probe; the
+  // cut they give (≥ the final cut) screens the model tiles, and only the
+  // survivors' sub-tiles are read below
   float ut = INFINITY, far = 0.f;
   for (int j = threadIdx.x; j < cull.n_xtiles; j += kListThreads) {
     const float4 jl = cull.xlo[j], jh = cull.xhi[j];
@@ -1048,37 +1049,24 @@ __global__ void __launch_bounds__(kListThreads)
   }
   ut = cta_reduce<false>(ut, shf);
   far = cta_reduce<true>(far, shf);
-  const float cut_t = fminf(s2 * ut, neg_log2c) + cull.margin1;
-  auto tile_in = [&](int j) {
-    return !(s2 * box_mindist2(lo, hi, cull.xlo[j], cull.xhi[j]) > cut_t);
-  };
-  __shared__ int32_t cand_s[kMaxCandTiles];
-  const UnitWalk walk = unit_walk(cull.n_xtiles, kSubPerTile, cull.n_xsub, cand_s, wcount, tile_in);
-  float u = ut;
-  for (int i = threadIdx.x; i < walk.n_work; i += kListThreads) {
-    const int sj = walk.unit(i, tile_in);
-    if (sj >= 0) u = fminf(u, box_maxdist2(lo, hi, cull.sxlo[sj], cull.sxhi[sj]));
-  }
-  u = cta_reduce<false>(u, shf);
-  // Probe only where it can pay (policy above): the tiles the box bound
-  // keeps but U = 0 would drop bound what the probe can drop.
+  // Probe only where it can pay (policy above, counted over tiles): the
+  // tiles the box bound keeps but U = 0 would drop bound what the probe can
+  // drop.
   bool useful = s2 * far > fminf(0.f, neg_log2c) + cull.margin1;
-  float kept_box = 0.f;
+  float kept_box = 0.f;  // in sub-tiles
   useful = useful && cull.probe &&
            (!cull.probe_paid1 || cull.probe_paid1[b] || (st->iter & kProbeRetry) == 0);
   if (useful) {
-    const float cut_box = fminf(s2 * u, neg_log2c) + cull.margin1;
+    const float cut_box = fminf(s2 * ut, neg_log2c) + cull.margin1;
     const float cut_min = fminf(0.f, neg_log2c) + cull.margin1;
-    float2 k = make_float2(0.f, 0.f);  // (kept, contested) sub-tiles
-    for (int i = threadIdx.x; i < walk.n_work; i += kListThreads) {
-      const int sj = walk.unit(i, tile_in);
-      if (sj < 0) continue;
-      const float t = s2 * box_mindist2(lo, hi, cull.sxlo[sj], cull.sxhi[sj]);
+    float2 k = make_float2(0.f, 0.f);  // (kept, contested) tiles
+    for (int j = threadIdx.x; j < cull.n_xtiles; j += kListThreads) {
+      const float t = s2 * box_mindist2(lo, hi, cull.xlo[j], cull.xhi[j]);
       k.x += t <= cut_box ? 1.f : 0.f;
       k.y += t <= cut_box && t > cut_min ? 1.f : 0.f;
     }
     k = cta_sum2(k, sh2);
-    kept_box = k.x;
+    kept_box = k.x * kSubPerTile;
     useful = k.y * kProbeMinShare >= k.x;
   }
   const int np = cull.probe && useful
@@ -1114,9 +1102,21 @@ __global__ void __launch_bounds__(kListThreads)
   const float ex = hi.x - lo.x, ey = hi.y - lo.y, ez = hi.z - lo.z;
   const float h2 = 0.25f * (ex * ex + ey * ey + ez * ez);
   const float probe = cta_reduce<true>(nn, shf) * (1.f + 0x1p-16f) + 0x1p-20f * (h2 + vmax);
-  if (np > 0) u = fminf(u, probe);
-  const float floor_t = fminf(s2 * u, neg_log2c);
-  const float cut = floor_t + cull.margin1;
+  float u = np > 0 ? fminf(ut, probe) : ut;
+  const float cut_t = fminf(s2 * u, neg_log2c) + cull.margin1;
+  auto tile_in = [&](int j) {
+    return !(s2 * box_mindist2(lo, hi, cull.xlo[j], cull.xhi[j]) > cut_t);
+  };
+  __shared__ int32_t cand_s[kMaxCandTiles];
+  const UnitWalk walk = unit_walk(cull.n_xtiles, kSubPerTile, cull.n_xsub, cand_s, wcount, tile_in);
+  // the sub-tile box bound over the surviving tiles (the minimising sub-tile
+  // lies in one of them)
+  for (int i = threadIdx.x; i < walk.n_work; i += kListThreads) {
+    const int sj = walk.unit(i, tile_in);
+    if (sj >= 0) u = fminf(u, box_maxdist2(lo, hi, cull.sxlo[sj], cull.sxhi[sj]));
+  }
+  u = cta_reduce<false>(u, shf);
+  const float cut = fminf(s2 * u, neg_log2c) + cull.margin1;
   // (cut ≤ cut_t: the kept units lie in the walk's tiles)
   const int count = cta_compact(
       walk.n_work, tiles + static_cast<int64_t>(b) * cull.n_xsub, wcount, [&](int i) {
@@ -1183,31 +1183,22 @@ __global__ void __launch_bounds__(kListThreads)
     }
     lt = cta_reduce<true>(lt, shf);
     lmin = cta_reduce<false>(lmin, shf);
-    floor_t = lt - cull.margin2;
-    walk = unit_walk(cull.n_ytiles, upt, n_units, cand_s, wcount, tile_in);
     float l = lt;
-    for (int i = threadIdx.x; i < walk.n_work; i += kListThreads) {
-      const int u = walk.unit(i, tile_in);
-      if (u >= 0) l = fmaxf(l, ubm[u].x - s2 * box_maxdist2(lo, hi, ulo[u], uhi[u]));
-    }
-    l = cta_reduce<true>(l, shf);
     // L ≤ 0, so a tile can only be dropped if its bound is below −margin;
     // probe policy as in pass 1, with L_lb = 0 as the optimistic bound
     bool useful = lmin < -cull.margin2;
     useful = useful && cull.probe &&
              (!cull.probe_paid2 || cull.probe_paid2[b] || (st->iter & kProbeRetry) == 0);
-    if (useful) {
-      const float floor_box = l - cull.margin2;
+    if (useful) {  // counted over tiles
+      const float floor_box = lt - cull.margin2;
       float2 k = make_float2(0.f, 0.f);
-      for (int i = threadIdx.x; i < walk.n_work; i += kListThreads) {
-        const int u = walk.unit(i, tile_in);
-        if (u < 0) continue;
-        const float v = ubm[u].y - s2 * box_mindist2(lo, hi, ulo[u], uhi[u]);
+      for (int j = threadIdx.x; j < cull.n_ytiles; j += kListThreads) {
+        const float v = tile_top(j);
         k.x += v >= floor_box ? 1.f : 0.f;
         k.y += v >= floor_box && v < -cull.margin2 ? 1.f : 0.f;
       }
       k = cta_sum2(k, sh2);
-      kept_box = k.x;
+      kept_box = k.x * upt;
       useful = k.y * kProbeMinShare >= k.x;
     }
     np = cull.probe && useful
@@ -1245,6 +1236,15 @@ __global__ void __launch_bounds__(kListThreads)
     const float h2 = 0.25f * (ex * ex + ey * ey + ez * ez);
     // rounding slack of the fp32 bound (expanded form: ≲ a few ε·s²(|u|² + |v|²))
     if (np > 0) l = fmaxf(l, probe - 1e-3f - 1e-5f * fabsf(probe) - 0x1p-20f * s2 * (h2 + vmax));
+    // the tile-level floor screens the scene tiles; the unit box bound over
+    // the survivors (the maximising unit lies in one of them) tightens it
+    floor_t = l - cull.margin2;
+    walk = unit_walk(cull.n_ytiles, upt, n_units, cand_s, wcount, tile_in);
+    for (int i = threadIdx.x; i < walk.n_work; i += kListThreads) {
+      const int u = walk.unit(i, tile_in);
+      if (u >= 0) l = fmaxf(l, ubm[u].x - s2 * box_maxdist2(lo, hi, ulo[u], uhi[u]));
+    }
+    l = cta_reduce<true>(l, shf);
     floor_l = l - cull.margin2;
   }
   // (floor_l ≥ floor_t: the kept units lie in the walk's tiles)
