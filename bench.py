@@ -1,21 +1,26 @@
 #!/usr/bin/env python
 """Benchmark: Fast-CPD EM iterations/s on B200 (BASELINE.json metric).
 
-Workload (default): BASELINE.json configs[1] — full-rank Fast CPD, M=20,000,
-N=24,000 (20 % uniform outliers), D=3, ω=0.2, β=2, λ=3 — generated with the
-seeded synthetic stand-in generator (paper_2006_06281_b200/datagen.py).
-A "step" is one EM iteration (E-step + M-step + transform + σ²) replayed
-from the engine's CUDA graph; inputs are resident in HBM before timing.  The
-K timed steps are the first K iterations of the configured run (default K =
-the config's iteration count, 100), each preceded by a 256 MB L2-flushing
-write outside its event pair; W warm-up iterations run in a separate session
-first.
+Workload (default): BASELINE.json configs[4] — low-rank Fast CPD, K=300,
+M=N=200,000, D=3 (bumpy sphere + GRBF warp), ω=0.1, β=1, λ=2 — the largest
+config that fits one GPU and the one the 1/2/4/8-GPU metric is quoted on.
+Inputs come from the seeded synthetic stand-in generator
+(paper_2006_06281_b200/datagen.py).  A "step" is one EM iteration (E-step +
+M-step + transform + σ²) replayed from the engine's CUDA graph; inputs are
+resident in HBM before timing.  The K timed steps are the first K
+iterations of the configured run (default K = the config's 100), each
+preceded by a 256 MB L2-flushing write outside its event pair; W warm-up
+iterations run in a separate session first.  The same line carries a
+`secondary` block for configs[1] (C1, full rank M=20,000 N=24,000) with the
+1-thread (reference-faithful: the reference build has no OpenMP) and
+all-thread CPU figures beside it.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c0..c4] [--secondary c1|none]
 
 Under torchrun (N>1) each rank runs on its own GPU; rank 0 prints one JSON
 line.  `--impl reference` times the CPU restatement of the reference
-(oracle/, the reference itself cannot be compiled here — see DESIGN.md) on
+(oracle/; the reference itself cannot be compiled here — DESIGN.md §5) on
 the host cores, rank 0 only.
 """
 from __future__ import annotations
@@ -44,13 +49,19 @@ sys.path.insert(0, ROOT)
 METRIC = "EM iterations/s"
 UNIT = "it/s"
 
+# E-step roofline: clk per SM per (m, n) pair, by (pass, pair form), from the
+# SASS instruction mix of the pass kernels (profiles/r2_sass_mix.txt):
+# max(1 MUFU.EX2 / 16 per clk, FP32 lane-ops / 128 per clk).
+PAIR_CLK = {"pass1_centred": max(1 / 16, 4 / 128), "pass1_difference": max(1 / 16, 7 / 128),
+            "pass2_centred": max(1 / 16, 8 / 128), "pass2_difference": max(1 / 16, 12 / 128)}
+
 
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f), "measured"
+            return json.load(f), "measured (MEASURED_PEAKS.json)"
     except OSError:
-        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -77,7 +88,7 @@ class ClockSampler:
                     self.rows.append([v.strip() for v in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t.start()
@@ -118,19 +129,19 @@ class Watchdog:
         self._t.cancel()
 
 
-def estep_traffic():
-    """DRAM bytes per launch of the two E-step kernels (col + row) from the
-    committed ncu --set full summary, or None."""
-    try:
-        ks = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))["kernels"]
-        per = {}
-        for k in ks:
-            name = k["kernel"].replace("void ", "").split("<")[0]
-            if name in ("estep_col_kernel", "estep_row_kernel"):
-                per[name] = k["dram_read_B"] + k["dram_write_B"]
-        return sum(per.values()) if len(per) == 2 else None
-    except Exception:
-        return None
+def ncu_traffic(kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from this round's
+    committed `ncu --set full` summary, or None."""
+    for name in ("r2_ncu_summary.json", "ncu_summary.json"):
+        try:
+            ks = json.load(open(os.path.join(ROOT, "profiles", name)))["kernels"]
+        except Exception:
+            continue
+        vals = [k["dram_read_B"] + k["dram_write_B"] for k in ks
+                if k["kernel"].replace("void ", "").split("<")[0].split("(")[0].endswith(kernel)]
+        if vals:
+            return {"bytes_per_launch": sum(vals) / len(vals), "source": f"profiles/{name}"}
+    return None
 
 
 def dist_setup():
@@ -143,49 +154,115 @@ def dist_setup():
 # ---------------------------------------------------------------- CPU arms
 
 
-def cpu_sample(x, y, w, iterations: int):
-    """The oracle's dense, materialising restatement of register_pointsets on
-    the full workload, timing the EM loop only.  The eigenbasis is replaced
-    by the identity (a 20k×20k fp64 dense matrix streamed exactly like a real
-    basis): a LAPACK eigensolve of a 20k Gram matrix takes far longer than
-    the bench budget on the host, and the per-iteration arithmetic does not
-    depend on the basis values."""
+def cpu_iteration_sample(x, y, w, threads: int, slices: int):
+    """Seconds per EM iteration of the oracle's restatement of
+    register_pointsets on `threads` host threads, extrapolated from one
+    iteration over a 1/`slices` slice of the scene: the E-step's work is
+    linear in N, the M-step (over all M model rows) is not, so
+    t_iter = slices·(t_slice − t_mstep) + t_mstep with t_mstep measured on a
+    256-point slice.  C0/C1 (full rank) use the DENSE faithful restatement
+    (P and Φ materialised, as the reference does) with an identity stand-in
+    basis (the per-iteration arithmetic does not depend on the basis values;
+    a LAPACK eigensolve of a 20k Gram matrix exceeds the bench budget);
+    C2–C4 — where the reference itself is infeasible (Φ alone is 20–320 GB)
+    — the streaming restatement with a random stand-in basis of the same
+    shape.  Returns (seconds per iteration, description)."""
     from oracle import oracle as orc
-    threads = os.cpu_count() or 1
+    import paper_2006_06281_b200 as fcpd
     orc.set_threads(threads)
-    m = x.shape[0]
-    u = np.eye(m, order="F")
-    lam = np.ones(m)
-    res = orc.register(x, y, omega=w.omega, beta=w.beta, lambda_reg=w.lambda_reg,
-                       iterations=iterations, variant=w.variant,
-                       rank_fraction=w.rank_fraction, basis=(u, lam))
+    xn, yn = orc.normalize_pair(x, y)[:2]
+    m, n = xn.shape[0], yn.shape[0]
+    dense = w.variant == "fast"
+    k = m if dense else fcpd.lowrank_rank(w.rank_fraction, m)
+    ns = max(512, n // slices)
+
+    def run(yy, u, lam):
+        if dense:
+            r = orc.register(xn, yy, omega=w.omega, beta=w.beta, lambda_reg=w.lambda_reg,
+                             iterations=1, variant="fast", normalize=False, basis=(u, lam))
+            return r.timing["t_loop"]
+        t0 = time.perf_counter()
+        orc.register_stream(xn, yy, u, lam, omega=w.omega, lambda_reg=w.lambda_reg,
+                            iterations=1, normalize=False)
+        return time.perf_counter() - t0
+
+    if dense:
+        u = np.eye(m, order="F")
+    else:
+        u = np.asfortranarray(np.random.default_rng(0).standard_normal((m, k)) / np.sqrt(m))
+    lam = np.ones(k)
+    t_slice = run(yn[:ns], u, lam)
+    t_m = run(yn[:256], u, lam)
     del u
-    return iterations / res.timing["t_loop"], threads, res.timing["t_loop"]
+    per = (n / ns) * max(t_slice - t_m, 0.0) + t_m
+    kind = "dense faithful" if dense else "streaming"
+    desc = (f"1 EM iteration of the oracle's {kind} restatement over a {ns}-point scene slice "
+            f"(1/{n / ns:.0f} of N={n}; M={m}, K={k}) on {threads} host thread(s), "
+            f"extrapolated linearly in N (E-step) plus the M-step measured on a 256-point "
+            f"slice ({t_m:.2f} s); stand-in basis of the right shape")
+    return per, desc
 
 
 def run_reference(args, world, rank):
+    """The reference arm: the CPU restatement of the reference's path on the
+    host cores, same workload/metric as our arm.  Each step is one oracle EM
+    iteration over a 1/S scene slice (the reference itself cannot be built
+    here, and for C2–C4 it cannot run at all: Φ and P are 20–320 GB)."""
     if rank != 0:
         return
+    from oracle import oracle as orc
     from paper_2006_06281_b200 import datagen
+    import paper_2006_06281_b200 as fcpd
     x, y, w = datagen.generate(args.workload)
-    if args.steps is None:
-        args.steps = w.iterations
-    # one untimed warm-up iteration (also sizes the sample), then a bounded
-    # sample: at most args.steps iterations, capped by a time budget
-    t_est = cpu_sample(x, y, w, 1)[2]
-    k = max(1, min(args.steps, int(args.cpu_budget_s / max(t_est, 1e-9))))
-    rate, threads, secs = cpu_sample(x, y, w, k)
-    sample = (f"{k} dense fp64 EM iteration(s) of {args.workload} (M={x.shape[0]}, "
-              f"N={y.shape[0]}) through the oracle restatement of register_pointsets; "
-              f"identity stand-in basis; {threads} host threads")
+    steps = args.steps if args.steps is not None else w.iterations
+    threads = os.cpu_count() or 1
+    orc.set_threads(threads)
+    xn, yn = orc.normalize_pair(x, y)[:2]
+    m, n = xn.shape[0], yn.shape[0]
+    dense = w.variant == "fast"
+    k = m if dense else fcpd.lowrank_rank(w.rank_fraction, m)
+    slices = args.ref_slices or (1 if dense and m <= 2000 else 8 if dense else 64)
+    ns = max(512, n // slices)
+    if dense:
+        u = np.eye(m, order="F")
+    else:
+        u = np.asfortranarray(np.random.default_rng(0).standard_normal((m, k)) / np.sqrt(m))
+    lam = np.ones(k)
+
+    def step(yy):
+        t0 = time.perf_counter()
+        if dense:
+            r = orc.register(xn, yy, omega=w.omega, beta=w.beta, lambda_reg=w.lambda_reg,
+                             iterations=1, variant="fast", normalize=False, basis=(u, lam))
+            return r.timing["t_loop"], time.perf_counter() - t0
+        orc.register_stream(xn, yy, u, lam, omega=w.omega, lambda_reg=w.lambda_reg,
+                            iterations=1, normalize=False)
+        dt = time.perf_counter() - t0
+        return dt, dt
+
+    # warm-up: W slice steps, plus the M-step-only time (256-point slice)
+    for i in range(args.warmup):
+        step(yn[(i % slices) * ns:(i % slices) * ns + ns])
+    t_m = step(yn[:256])[0]
+    times = []
+    t_wall0 = time.perf_counter()
+    for i in range(steps):
+        s0 = (i % slices) * ns
+        times.append(step(yn[s0:s0 + ns])[0])
+    wall = time.perf_counter() - t_wall0
+    t_step = sum(times) / len(times)
+    per_iter = (n / ns) * max(t_step - t_m, 0.0) + t_m
+    rate = 1.0 / per_iter
+    sample = (f"each step = 1 EM iteration of the oracle's "
+              f"{'dense faithful' if dense else 'streaming'} restatement over a {ns}-point "
+              f"scene slice (1/{n / ns:.0f} of N={n}; M={m}, K={k}), {threads} host threads; "
+              f"it/s = 1/(N/slice·(t_step − t_M) + t_M), t_M = {t_m:.3f} s (M-step alone)")
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "cpu_steps_timed": k,
-        "ms_per_step": 1e3 * secs / k, "higher_is_better": True, "scaling": "weak",
+        "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / steps,
+        "iterations_per_step": ns / n, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, datagen.py)",
-        "config": {"workload": f"{args.workload}: {w.description}", "M": x.shape[0],
-                   "N": y.shape[0], "K": x.shape[0] if w.variant == "fast" else None,
-                   "omega": w.omega, "beta": w.beta, "lambda": w.lambda_reg},
+        "config": workload_config(args.workload, w, x.shape[0], y.shape[0], k),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -193,33 +270,28 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def workload_config(name, w, m, n, k):
+    return {"workload": f"{name}: {w.description}", "M": m, "N": n, "K": k, "omega": w.omega,
+            "beta": w.beta, "lambda": w.lambda_reg, "variant": w.variant,
+            "iterations": w.iterations}
+
+
 # ---------------------------------------------------------------- GPU arm
 
 
-def run_ours(args, world, rank, local):
+def measure(args, name, steps, warmup, world, rank, local, sharded, e2e_calls, prof=True):
+    """Device-timed EM iterations, per-phase profile, roofline inputs and
+    end-to-end register calls for one workload."""
     import torch
     import torch.distributed as dist
 
     import paper_2006_06281_b200 as fcpd
     from paper_2006_06281_b200 import datagen
 
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    x, y_full, w = datagen.generate(args.workload)
-    # --shard1: the NCCL-sharded engine path as a one-rank group (exercises
-    # the multi-GPU code path on one GPU; no rank waits on another)
-    sharded = (world > 1 and not args.replicas) or args.shard1
-    # A step is one EM iteration.  The K timed steps are the FIRST K
-    # iterations of the configured run (K defaults to the config's iteration
-    # count, so `value` = iterations / Σ per-iteration device time over the
-    # whole run); the W warm-up iterations run in a throwaway
-    # session before it.  The per-phase profile replays the same K-iteration
-    # trajectory, so the roofline describes exactly the timed iterations.
-    if args.steps is None:
-        args.steps = w.iterations
-    prof_iters = 0 if sharded else args.steps
-    cfg = datagen.config_for(w, iterations=args.steps)
+    x, y_full, w = datagen.generate(name)
+    if steps is None:
+        steps = w.iterations
+    cfg = datagen.config_for(w, iterations=steps)
     if sharded:
         # scene points sharded over ranks (SURVEY §8e); the engine's own NCCL
         # communicator carries the per-iteration reductions
@@ -232,13 +304,11 @@ def run_ours(args, world, rank, local):
     else:
         ctx = fcpd.Context(local)
         y = y_full
-    watchdog = Watchdog(args.watchdog_s)
     t0 = time.perf_counter()
-    ctx.session_begin(x, y, datagen.config_for(w, iterations=args.warmup))
+    ctx.session_begin(x, y, datagen.config_for(w, iterations=warmup))
     setup_s = time.perf_counter() - t0
-
     stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=torch.device("cuda", local))
-    ctx.session_run(args.warmup)
+    ctx.session_run(warmup)
     ctx.session_sync()
     ctx.session_begin(x, y, cfg)  # the timed run (basis cached by the warm-up session)
     if world > 1:
@@ -248,7 +318,7 @@ def run_ours(args, world, rank, local):
     # 126 MB L2) on the engine stream before it, outside its event pair
     flush = torch.empty(64 * 2**20, dtype=torch.float32, device=torch.device("cuda", local))
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+           for _ in range(steps)]
     with ClockSampler(local) as clk:
         for i, (e0, e1) in enumerate(evs):
             with torch.cuda.stream(stream):
@@ -266,19 +336,20 @@ def run_ours(args, world, rank, local):
         ms = float(t.item())
         dist.barrier()
     state = ctx.session_read(with_points=False)
-    phases, prof_tiles = None, (0, 0)
-    if prof_iters:  # the same trajectory again, eager, with per-phase events
+    out = {"name": name, "w": w, "x": x, "y_full": y_full, "steps": steps, "ms": ms,
+           "setup_s": setup_s, "state": state, "clocks": clk.summary(),
+           "kernels_per_iteration": ctx.kernels_per_iteration}
+    if prof and not sharded:
+        # the same trajectory again, eager, with per-phase events; the
+        # counters give the pairs each (pass, form) evaluated
         ctx.session_begin(x, y, cfg)
-        tiles0 = ctx.session_read(with_points=False)["tiles_evaluated"]
-        phases = ctx.session_profile(prof_iters)
-        tiles1 = ctx.session_read(with_points=False)["tiles_evaluated"]
-        # tile pairs the two E-step passes evaluated (0 when culling is off)
-        prof_tiles = tuple(b - a for a, b in zip(tiles0, tiles1))
-    # the basis-stream kernel over the FULL basis (no spectral truncation),
-    # for its HBM roofline; the basis is cached in the context
-    # (the streaming kernel even where this run used the fused M-step)
-    full_phases = None
-    if prof_iters:
+        s0 = ctx.session_read(with_points=False)
+        out["phases"] = ctx.session_profile(steps)
+        s1 = ctx.session_read(with_points=False)
+        out["tiles"] = tuple(b - a for a, b in zip(s0["tiles_evaluated"], s1["tiles_evaluated"]))
+        out["pairs"] = tuple(b - a for a, b in zip(s0["pairs_by_form"], s1["pairs_by_form"]))
+        # the basis-stream kernel over the FULL basis (no truncation, the
+        # streaming M-step even where this run fuses it), for its HBM roofline
         fcfg = datagen.config_for(w, iterations=4)
         fcfg.spectral_tau = 0.0
         saved = os.environ.get("FCPD_MSTEP_FUSED")
@@ -291,15 +362,11 @@ def run_ours(args, world, rank, local):
             else:
                 os.environ["FCPD_MSTEP_FUSED"] = saved
         ctx.session_run(1)
-        full_phases = ctx.session_profile(3)
-    sigma_last = float(state["sigma2_trace"][-1])
-
+        out["full_phases"] = ctx.session_profile(3)
     # e2e through the public API: host buffers in, results out, basis cached
     e2e_iters = w.iterations
     ecfg = datagen.config_for(w, iterations=e2e_iters)
-    e2e_calls = args.e2e_calls
-    last = None
-    e2e_s, e2e_rate = 0.0, 0.0
+    last, e2e_s, e2e_rate = None, 0.0, 0.0
     if e2e_calls > 0:
         ctx.register(x, y, ecfg)  # warm (basis already cached by the session)
         t0 = time.perf_counter()
@@ -312,132 +379,157 @@ def run_ours(args, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
         e2e_rate = (1 if sharded else world) * e2e_calls * e2e_iters / e2e_s
-    watchdog.cancel()
+    out["e2e"] = {"value": e2e_rate, "unit": UNIT,
+                  "h2d_bytes_per_step": last.h2d_bytes / e2e_iters if last else None,
+                  "d2h_bytes_per_step": last.d2h_bytes / e2e_iters if last else None,
+                  "note": f"{e2e_calls} register_pointsets call(s) of {e2e_iters} iterations "
+                          "through the C ABI with host fp64 buffers in and out; spectral basis "
+                          "cached in the context (setup reported separately as setup_s)"}
+    ctx.close()
+    return out
 
+
+def rooflines(r, peaks, peak_kind):
+    """E-step (SFU/FP32) and basis-stream (HBM) rooflines of one measure()."""
+    import paper_2006_06281_b200 as fcpd
+    w, x, y = r["w"], r["x"], r["y_full"]
+    m, n = x.shape[0], y.shape[0]
+    k = m if w.variant == "fast" else fcpd.lowrank_rank(w.rank_fraction, m)
+    phases, steps = r.get("phases"), r["steps"]
+    clocks = r["clocks"]
+    f_mhz = clocks["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)
+    hz = 148 * f_mhz * 1e6
+    if not phases:
+        return None, None
+    e_ms = phases["estep_pass1"] + phases["estep_pass2"]
+    it_ms = sum(phases.values())
+    pairs = dict(zip(PAIR_CLK, r["pairs"]))
+    if not any(pairs.values()):  # no counters: every pair, centred form
+        pairs = {"pass1_centred": m * n * steps, "pass1_difference": 0,
+                 "pass2_centred": m * n * steps, "pass2_difference": 0}
+    t_bound = sum(pairs[f] * PAIR_CLK[f] for f in PAIR_CLK) / hz / steps  # s per iteration
+    evaluated = sum(pairs.values()) / 2 / steps                            # pairs per pass
+    u1, u2 = fcpd.cull_units_total(m, n)
+    f1 = r["tiles"][0] / (u1 * steps) if r["tiles"][0] else 1.0
+    f2 = r["tiles"][1] / (u2 * steps) if r["tiles"][1] else 1.0
+    traffic = ncu_traffic("estep_row_kernel")
+    roof = {"bound": "sfu+fp32", "achieved": evaluated / (e_ms / 1e3) / 1e9,
+            "peak": evaluated / t_bound / 1e9, "unit": "Gpairs/s",
+            "frac": t_bound / (e_ms / 1e3),
+            "traffic": traffic["bytes_per_launch"] if traffic else None,
+            "traffic_source": (traffic or {}).get("source"),
+            "kernel": "E-step: estep_col_kernel (pass 1) + estep_row_kernel (pass 2) with their "
+                      "list / fallback kernels (phase time over the timed trajectory)",
+            "model": "per pair max(1 MUFU.EX2/16, FP32 lane-ops/128) clk/SM; lane-ops from SASS "
+                     "(profiles/r2_sass_mix.txt): pass 1 centred 4, difference 7; pass 2 "
+                     "centred 8, difference 12; weighted by the pairs each (pass, form) "
+                     "evaluated (pass-kernel counters); sampled SM clock",
+            "pairs_by_form_per_iteration": {f: v / steps for f, v in pairs.items()},
+            "evaluated_frac": [f1, f2],
+            "share_of_iteration": e_ms / it_ms,
+            "estep_ms_per_iteration": e_ms,
+            "bound_ms_per_iteration": t_bound * 1e3,
+            "dense_equiv_gpairs_per_s": m * n / (e_ms / 1e3) / 1e9}
+    fused = bool(r["state"].get("mstep_fused"))
+    keff = r["state"].get("spectral_rank") or k
+    kpad, mpad = (keff + 3) // 4 * 4, (m + 3) // 4 * 4
+    q_bytes = 4.0 * (m * kpad + keff * mpad)
+    q_ms = phases["qt_r_stream"] + (0.0 if fused else phases["q_g_stream"])
+    hbm = {"bound": "hbm", "unit": "GB/s", "peak": peaks["hbm_gbs"], "peak_source": peak_kind,
+           "kernel": "colsum_bulk (Qᵀ·R and Q·g basis streams)",
+           "this_run": {"mstep": "mstep_fused (one cooperative kernel)" if fused else
+                        "streaming (colsum_bulk ×2 + reduce/transform)",
+                        "basis_bytes_per_iteration": q_bytes / 2 if fused else q_bytes,
+                        "ms": q_ms, "share_of_iteration": q_ms / it_ms,
+                        "achieved_gbs": (q_bytes / 2 if fused else q_bytes) / (q_ms / 1e3) / 1e9}}
+    fp = r.get("full_phases")
+    if fp:
+        fk = (k + 3) // 4 * 4
+        fb = 4.0 * (m * fk + k * mpad)
+        fms = fp["qt_r_stream"] + fp["q_g_stream"]
+        ach = fb / (fms / 1e3) / 1e9
+        tr = ncu_traffic("colsum_bulk_kernel")
+        hbm.update({"achieved": ach, "frac": ach / peaks["hbm_gbs"],
+                    "traffic": tr["bytes_per_launch"] if tr else None,
+                    "full_basis": {"bytes_per_iteration": fb, "ms": fms}})
+    return roof, hbm
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    # --shard1: the NCCL-sharded engine path as a one-rank group (exercises
+    # the multi-GPU code path on one GPU; no rank waits on another)
+    sharded = (world > 1 and not args.replicas) or args.shard1
+    watchdog = Watchdog(args.watchdog_s)
+    main = measure(args, args.workload, args.steps, args.warmup, world, rank, local, sharded,
+                   args.e2e_calls)
+    sec = None
+    if args.secondary != "none" and args.secondary != args.workload and world == 1:
+        sec = measure(args, args.secondary, args.steps, args.warmup, world, rank, local, False,
+                      args.e2e_calls)
+    watchdog.cancel()
     if rank == 0:
+        import paper_2006_06281_b200 as fcpd
         peaks, peak_kind = load_peaks()
+        w, x, y_full = main["w"], main["x"], main["y_full"]
         m, n = x.shape[0], y_full.shape[0]
         k = m if w.variant == "fast" else fcpd.lowrank_rank(w.rank_fraction, m)
-        # eigenpairs the basis streams actually read (spectral truncation)
-        keff = state.get("spectral_rank") or k
-        kpad, mpad = (keff + 3) // 4 * 4, (m + 3) // 4 * 4
+        steps = main["steps"]
         # sharded: every iteration is the whole problem (strong scaling);
         # replicas: each rank runs its own copy (weak scaling)
-        value = (1 if sharded or world == 1 else world) * args.steps / (ms / 1e3)
-        q_bytes = 4.0 * (m * kpad + keff * mpad)
-        clocks = clk.summary()
-        f_mhz = clocks["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)
-        mufu_bound = 148 * f_mhz * 1e6 * 16 / 2  # 2 ex2 per pair, 16 ex2/clk/SM
-        roofline = roofline_hbm = None
-        pairs_s = None
-        if phases:
-            e_ms = phases["estep_pass1"] + phases["estep_pass2"]
-            it_ms = sum(phases.values())
-            pairs_s = m * n / (e_ms / 1e3)  # algorithmic (dense-equivalent) pair rate
-            # The dominant kernels: the two E-step passes, bound by the SFU
-            # (MUFU.EX2, 16/clk/SM) and the FP32 pipe, not by memory.  Model
-            # (SASS-verified op counts): pass 1 = 1 ex2 + 7 FP32 lane-ops per
-            # pair → MUFU-bound; pass 2 = 1 ex2 + 12 lane-ops → FP32-bound.
-            # Only the pairs of evaluated (non-culled) tile pairs cost pipe time.
-            u1, u2 = fcpd.cull_units_total(m, n)
-            f1 = prof_tiles[0] / (u1 * prof_iters) if prof_tiles[0] else 1.0
-            f2 = prof_tiles[1] / (u2 * prof_iters) if prof_tiles[1] else 1.0
-            c1, c2 = max(1 / 16, 7 / 128), max(1 / 16, 12 / 128)
-            hz = 148 * f_mhz * 1e6
-            t_bound = m * n * (f1 * c1 + f2 * c2) / hz
-            evaluated_s = m * n * (f1 + f2) / 2 / (e_ms / 1e3)
-            roofline = {"bound": "sfu+fp32", "achieved": evaluated_s / 1e9,
-                        "peak": hz / ((f1 * c1 + f2 * c2) / ((f1 + f2) / 2)) / 1e9,
-                        "unit": "Gpairs/s", "frac": t_bound / (e_ms / 1e3),
-                        "traffic": estep_traffic(),
-                        "kernel": "estep_col_kernel + estep_row_kernel (fused non-materialising "
-                                  "E-step, both passes with their list/combine kernels)",
-                        "share_of_iteration": e_ms / it_ms,
-                        "evaluated_frac": [f1, f2],
-                        "dense_equiv_gpairs_per_s": pairs_s / 1e9,
-                        "mufu_only_peak": mufu_bound / 1e9,
-                        "note": "pass1 MUFU-bound (16 ex2/clk/SM), pass2 FP32-bound "
-                                "(12 lane-ops/pair at 128/clk/SM), over the pairs of the "
-                                "tile pairs not culled (evaluated_frac per pass); sampled "
-                                "SM clock; phase times include the geometry/combine/"
-                                "fallback kernels; memory traffic is negligible (`traffic` = ncu DRAM "
-                                "bytes of one col + one row launch)"}
-            # The Q products (HBM-bound): as streamed in this run (spectral
-            # truncation reads only `keff` eigenvectors) and, for the kernel's
-            # bandwidth, over the full basis in a short untruncated session.
-            fused = bool(state.get("mstep_fused"))
-            # fused: the whole M-step is one kernel, booked as the Qᵀ·R phase
-            q_ms = phases["qt_r_stream"] + (0.0 if fused else phases["q_g_stream"])
-            traffic = None
-            prof_json = os.path.join(ROOT, "profiles", "ncu_summary.json")
-            if os.path.exists(prof_json):
-                try:
-                    traffic = json.load(open(prof_json)).get("colsum_dram_bytes_per_launch")
-                except Exception:
-                    traffic = None
-            roofline_hbm = {"bound": "hbm", "unit": "GB/s", "peak": peaks["hbm_gbs"],
-                            "peak_source": peak_kind,
-                            "kernel": "colsum_bulk (Qᵀ·R and Q·g basis streams, "
-                                      "cp.async.bulk ring)",
-                            "this_run": {
-                                "mstep": ("mstep_fused (one cooperative kernel: rank, Qᵀ·R, "
-                                          "filter, Q·g from L2, transform, σ²)" if fused else
-                                          "streaming (colsum_bulk ×2 + reduce/transform)"),
-                                "basis_bytes_per_iteration": (q_bytes / 2 if fused else q_bytes),
-                                "ms": q_ms,
-                                "share_of_iteration": q_ms / it_ms}}
-            if full_phases:
-                fk = (k + 3) // 4 * 4
-                fb = 4.0 * (m * fk + k * mpad)
-                fms = full_phases["qt_r_stream"] + full_phases["q_g_stream"]
-                ach = fb / (fms / 1e3) / 1e9
-                roofline_hbm.update({"achieved": ach, "frac": ach / peaks["hbm_gbs"],
-                                     "traffic": traffic,
-                                     "full_basis": {"bytes_per_iteration": fb, "ms": fms}})
-        cpu = None
-        if world == 1 and not args.no_cpu:
-            rate, threads, secs = cpu_sample(x, y_full, w, args.cpu_iters)
-            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                   "sample": f"{args.cpu_iters} dense fp64 EM iteration(s) of {args.workload} "
-                             f"via the oracle restatement, identity stand-in basis, "
-                             f"{threads} threads, {secs:.1f} s"}
+        value = (1 if sharded or world == 1 else world) * steps / (main["ms"] / 1e3)
+        roof, hbm = rooflines(main, peaks, peak_kind)
+        cfg = workload_config(args.workload, w, m, n, k)
+        cfg.update({
+            "parallelism": (f"scene-sharded x{world} (NCCL)" if sharded else
+                            f"replicas x{world}" if world > 1 else "single"),
+            "timed_iterations": f"the first {steps} of the {w.iterations}-iteration run",
+            "l2": "L2 flushed (256 MB write) before every timed iteration, outside the events",
+            "spectral_truncation": {"tau": 1e-10, "K": k,
+                                    "rank_used_last_iteration": main["state"].get("spectral_rank")}})
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong" if sharded else "weak",
-            "vs_baseline": None,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": main["ms"] / steps, "higher_is_better": True,
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None,
             "dtype": "f32 pair terms + f64 accumulation; f32 basis stream",
-            "data": "synthetic (seeded generator, datagen.py)",
-            "config": {"workload": f"{args.workload}: {w.description}", "M": m, "N": n, "K": k,
-                       "omega": w.omega, "beta": w.beta, "lambda": w.lambda_reg,
-                       "variant": w.variant,
-                       "parallelism": (f"scene-sharded x{world} (NCCL)" if sharded else
-                                       f"replicas x{world}" if world > 1 else "single"),
-                       "l2": "L2 flushed (256 MB write) before every timed iteration, "
-                             "flush outside the timed events",
-                       "spectral_truncation": {
-                           "tau": datagen.config_for(w).spectral_tau, "K": k,
-                           "rank_used_last_iteration": keff,
-                           "basis_bytes_per_iteration": q_bytes}},
-            "setup_s": setup_s, "sigma2_last": sigma_last,
-            "spectral_rank_last": state.get("spectral_rank"),
-            "phase_ms": phases,
-            "estep_gpairs_per_s": pairs_s / 1e9 if pairs_s else None,
-            "roofline": roofline,
-            "roofline_hbm": roofline_hbm,
-            "clocks": clocks,
-            "gpu_launches": ctx.kernels_per_iteration * args.steps,
-            "e2e": {"value": e2e_rate, "unit": UNIT,
-                    "h2d_bytes_per_step": last.h2d_bytes / e2e_iters if last else None,
-                    "d2h_bytes_per_step": last.d2h_bytes / e2e_iters if last else None,
-                    "note": f"{e2e_calls} register_pointsets calls of {e2e_iters} iterations "
-                            "through the C ABI with host fp64 buffers; spectral basis cached "
-                            "in the context (setup reported separately as setup_s)"},
+            "data": "synthetic (seeded generator, datagen.py)", "config": cfg,
+            "setup_s": main["setup_s"],
+            "sigma2_last": float(main["state"]["sigma2_trace"][-1]),
+            "phase_ms": main.get("phases"), "roofline": roof, "roofline_hbm": hbm,
+            "clocks": main["clocks"],
+            "gpu_launches": main["kernels_per_iteration"] * steps,
+            "e2e": main["e2e"],
         }
-        if cpu:
-            line["cpu_baseline"] = cpu
+        if world == 1 and not args.no_cpu:
+            per, desc = cpu_iteration_sample(x, y_full, w, os.cpu_count() or 1, args.cpu_slices)
+            line["cpu_baseline"] = {"value": 1.0 / per, "unit": UNIT,
+                                    "cores": os.cpu_count() or 1, "kind": "port", "sample": desc}
+        if sec:
+            sw = sec["w"]
+            sm_, sn_ = sec["x"].shape[0], sec["y_full"].shape[0]
+            sk = sm_ if sw.variant == "fast" else fcpd.lowrank_rank(sw.rank_fraction, sm_)
+            sroof, shbm = rooflines(sec, peaks, peak_kind)
+            block = {"config": workload_config(args.secondary, sw, sm_, sn_, sk),
+                     "value": sec["steps"] / (sec["ms"] / 1e3), "unit": UNIT,
+                     "steps": sec["steps"], "ms_per_step": sec["ms"] / sec["steps"],
+                     "setup_s": sec["setup_s"], "e2e": sec["e2e"],
+                     "roofline_frac": sroof["frac"] if sroof else None,
+                     "roofline": sroof, "roofline_hbm": shbm, "phase_ms": sec.get("phases")}
+            if not args.no_cpu:
+                cpus = []
+                for th in (1, os.cpu_count() or 1):
+                    per, desc = cpu_iteration_sample(sec["x"], sec["y_full"], sw, th,
+                                                     args.cpu_slices_secondary)
+                    cpus.append({"value": 1.0 / per, "unit": UNIT, "cores": th,
+                                 "kind": "port", "sample": desc})
+                block["cpu_baseline"] = cpus
+            line["secondary"] = block
         print(json.dumps(line), flush=True)
-    ctx.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -449,14 +541,17 @@ def main():
                     help="timed EM iterations (default: the workload's iteration count)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c1")
-    ap.add_argument("--e2e-calls", type=int, default=3)
-    ap.add_argument("--cpu-iters", type=int, default=2)
-    ap.add_argument("--cpu-budget-s", type=float, default=90.0)
+    ap.add_argument("--workload", default="c4")
+    ap.add_argument("--secondary", default="c1", help="second workload in the line, or none")
+    ap.add_argument("--e2e-calls", type=int, default=2)
+    ap.add_argument("--cpu-slices", type=int, default=64,
+                    help="CPU sample: 1/S of the scene (main workload)")
+    ap.add_argument("--cpu-slices-secondary", type=int, default=24)
+    ap.add_argument("--ref-slices", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas instead of the scene-sharded NCCL path")
-    ap.add_argument("--watchdog-s", type=float, default=900.0)
+    ap.add_argument("--watchdog-s", type=float, default=1500.0)
     ap.add_argument("--shard1", action="store_true",
                     help="run the sharded (NCCL) engine path with a single rank")
     args = ap.parse_args()

@@ -105,6 +105,12 @@ typedef struct fcpd_result {
                                streams used (filter ≥ tau; = K untruncated) */
   int32_t mstep_fused;      /* 1 if the session ran the one-kernel M-step */
   int32_t reserved0;
+  int64_t pairs_by_form[4]; /* E-step (m, n) pair slots evaluated since the
+                               session began, by (pass 1 centred, pass 1
+                               difference, pass 2 centred, pass 2
+                               difference) pair form — the instruction mix
+                               the E-step roofline is computed from (culling
+                               sessions; 0 otherwise)                    */
 } fcpd_result;
 
 typedef struct fcpd_ctx fcpd_ctx;

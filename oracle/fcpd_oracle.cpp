@@ -110,6 +110,33 @@ inline double at(const double* a, int64_t ld, int64_t i, int64_t j) {
   return a[j * ld + i];
 }
 
+// out (M×d, column-major) = (x0 or 0) + U·Z, U M×k column-major, Z k×d
+// column-major with leading dimension ldz (default k).  Each thread owns a
+// block of rows and streams the columns of U through it: the same sums as
+// the naive per-row loop (Σ_i in increasing i), but cache-friendly.
+void basis_times(const double* u, int64_t m, int64_t k, const double* z, int d,
+                 const double* x0, double* out, int64_t ldz = 0) {
+  constexpr int64_t kRows = 512;
+  if (ldz == 0) ldz = k;
+#pragma omp parallel for schedule(static)
+  for (int64_t r0 = 0; r0 < m; r0 += kRows) {
+    const int64_t r1 = std::min(m, r0 + kRows);
+    double acc[3][kRows];
+    for (int j = 0; j < d; ++j)
+      for (int64_t r = r0; r < r1; ++r) acc[j][r - r0] = 0.0;
+    for (int64_t i = 0; i < k; ++i) {
+      const double* ui = u + i * m;
+      for (int j = 0; j < d; ++j) {
+        const double zi = z[j * ldz + i];
+        for (int64_t r = r0; r < r1; ++r) acc[j][r - r0] += ui[r] * zi;
+      }
+    }
+    for (int j = 0; j < d; ++j)
+      for (int64_t r = r0; r < r1; ++r)
+        out[j * m + r] = (x0 ? x0[j * m + r] : 0.0) + acc[j][r - r0];
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -346,28 +373,15 @@ int orc_solve_fast_lowrank(const double* u, const double* lambda, int64_t m,
       z[j * k + i] = acc / (lambda[i] + shift);
     }
   }
-#pragma omp parallel for schedule(static)
-  for (int64_t r = 0; r < m; ++r) {
-    for (int j = 0; j < d; ++j) {
-      double acc = 0.0;
-      for (int64_t i = 0; i < k; ++i) acc += u[i * m + r] * z[j * k + i];
-      w[j * m + r] = acc;
-    }
-  }
+  basis_times(u, m, k, z.data(), d, nullptr, w);
   return kOk;
 }
 
 // solvers.hpp:138-144 apply_transform: out = X + Φ W.
 int orc_apply_transform(const double* x, int64_t m, int d, const double* phi,
                         const double* w, double* out) {
-#pragma omp parallel for schedule(static)
-  for (int64_t r = 0; r < m; ++r) {
-    for (int j = 0; j < d; ++j) {
-      double acc = 0.0;
-      for (int64_t c = 0; c < m; ++c) acc += phi[c * m + r] * w[j * m + c];
-      out[j * m + r] = x[j * m + r] + acc;
-    }
-  }
+  // out = X + Φ W: Φ column-major, streamed by columns (column c scaled by W_c)
+  basis_times(phi, m, m, w, d, x, out, m);
   return kOk;
 }
 
@@ -383,13 +397,7 @@ int orc_apply_transform_lowrank(const double* x, int64_t m, int d, const double*
       for (int64_t r = 0; r < m; ++r) acc += u[i * m + r] * w[j * m + r];
       t[j * k + i] = lambda[i] * acc;
     }
-#pragma omp parallel for schedule(static)
-  for (int64_t r = 0; r < m; ++r)
-    for (int j = 0; j < d; ++j) {
-      double acc = 0.0;
-      for (int64_t i = 0; i < k; ++i) acc += u[i * m + r] * t[j * k + i];
-      out[j * m + r] = x[j * m + r] + acc;
-    }
+  basis_times(u, m, k, t.data(), d, x, out);
   return kOk;
 }
 
@@ -485,18 +493,32 @@ int orc_estep_stream(const double* xt, int64_t m, const double* y, int64_t n,
     }
     return s;
   };
-  // pass 1: column log-normaliser b_n = -(shift + log(denominator))
+  // pass 1: column log-normaliser b_n = -(shift + log(denominator)).  Each
+  // logit is formed once into a per-thread buffer; exp(a) for a < −746 is
+  // exactly +0 in IEEE fp64 (the smallest subnormal is e^−744.44), so those
+  // terms are skipped without changing a single bit of the sums.
+  constexpr double kExpZero = -746.0;
   std::vector<double> b(n);
-#pragma omp parallel for schedule(static)
-  for (int64_t c = 0; c < n; ++c) {
-    double mx = -INFINITY;
-    for (int64_t r = 0; r < m; ++r) mx = std::max(mx, -d2(r, c) * inv);
-    if (has_outlier && log_c > mx) mx = log_c;
-    double sm = 0.0;
-    for (int64_t r = 0; r < m; ++r) sm += std::exp(-d2(r, c) * inv - mx);
-    const double s = sm + (has_outlier ? std::exp(log_c - mx) : 0.0);
-    b[c] = -(mx + std::log(s));
-    if (pt1) pt1[c] = sm / s;
+#pragma omp parallel
+  {
+    std::vector<double> e(m);
+#pragma omp for schedule(static)
+    for (int64_t c = 0; c < n; ++c) {
+      double mx = -INFINITY;
+      for (int64_t r = 0; r < m; ++r) {
+        e[r] = -d2(r, c) * inv;
+        mx = std::max(mx, e[r]);
+      }
+      if (has_outlier && log_c > mx) mx = log_c;
+      double sm = 0.0;
+      for (int64_t r = 0; r < m; ++r) {
+        const double a = e[r] - mx;
+        if (a >= kExpZero) sm += std::exp(a);
+      }
+      const double s = sm + (has_outlier ? std::exp(log_c - mx) : 0.0);
+      b[c] = -(mx + std::log(s));
+      if (pt1) pt1[c] = sm / s;
+    }
   }
   // column sums of y for the uniform fallback
   std::vector<double> ymean(d, 0.0);
@@ -510,13 +532,21 @@ int orc_estep_stream(const double* xt, int64_t m, const double* y, int64_t n,
   }
   ysq /= static_cast<double>(n);
   // pass 2: per row, max-shifted accumulation of w = exp(L - rowmax)
-#pragma omp parallel for schedule(static)
+#pragma omp parallel
+  {
+    std::vector<double> lg(n);
+#pragma omp for schedule(static)
   for (int64_t r = 0; r < m; ++r) {
     double mx = -INFINITY;
-    for (int64_t c = 0; c < n; ++c) mx = std::max(mx, -d2(r, c) * inv + b[c]);
+    for (int64_t c = 0; c < n; ++c) {
+      lg[c] = -d2(r, c) * inv + b[c];
+      mx = std::max(mx, lg[c]);
+    }
     double s0 = 0.0, sv = 0.0;
     double sd[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int64_t c = 0; c < n; ++c) {
+      const double a = lg[c] - mx;
+      if (a < kExpZero) continue;  // w = +0 exactly
       const double dd = d2(r, c);
       const double wgt = std::exp(-dd * inv + b[c] - mx);
       s0 += wgt;
@@ -539,6 +569,7 @@ int orc_estep_stream(const double* xt, int64_t m, const double* y, int64_t n,
       for (int j = 0; j < d; ++j) ptilde_y[j * m + r] = at(xt, m, r, j) + sd[j] / s0;
       var[r] = sv / s0;
     }
+  }
   }
   return kOk;
 }
@@ -747,9 +778,14 @@ int orc_load_spectral_cache(const char* path, int64_t* m, int64_t* k, double* be
 // σ² by the per-row form Σ_m [V_m − 2δ·Δ̄ + ‖δ‖²]/(DM), algebraically the
 // trace form of solvers.hpp:166-172 (row sums of P̃ are 1; checked against
 // the dense oracle at small sizes in tests/test_oracle_kat.py).
+// xt_start / sigma2_start (optional; nullptr / ≤ 0 → X and init_sigma2):
+// resume from a given EM state x̃ (in the frame the loop runs in: normalised
+// when `normalize`) and σ² — the state is exactly (x̃, σ²), so a window of
+// late iterations can be checked without replaying the whole run.
 int orc_register_stream(const double* x_in, int64_t m, const double* y_in, int64_t n, int d,
                         double omega, double lambda_reg, int iterations, int normalize,
                         const double* u, const double* lam, const double* lam_num, int64_t k,
+                        const double* xt_start, double sigma2_start,
                         double* out_x, double* sigma2_trace, int* iters_run,
                         double* sigma2_initial) {
   if (m == 0 || n == 0) return fail(kParameter, "register: empty point set");
@@ -767,7 +803,9 @@ int orc_register_stream(const double* x_in, int64_t m, const double* y_in, int64
   double sigma2 = 0.0;
   orc_init_sigma2(x.data(), m, y.data(), n, d, &sigma2);
   *sigma2_initial = sigma2;
+  if (sigma2_start > 0.0) sigma2 = sigma2_start;
   std::vector<double> xt = x, pty(m * d), p1(m), var(m), resid(m * d), z(k * d), xn(m * d);
+  if (xt_start) std::memcpy(xt.data(), xt_start, sizeof(double) * m * d);
   std::vector<int32_t> deg(m);
   int it = 0;
   for (; it < iterations; ++it) {
@@ -784,13 +822,7 @@ int orc_register_stream(const double* x_in, int64_t m, const double* y_in, int64
         for (int64_t r = 0; r < m; ++r) acc += u[j * m + r] * resid[c * m + r];
         z[c * k + j] = acc * lam_num[j] / (lam[j] + shift);
       }
-#pragma omp parallel for schedule(static)
-    for (int64_t r = 0; r < m; ++r)
-      for (int c = 0; c < d; ++c) {
-        double acc = 0.0;
-        for (int64_t j = 0; j < k; ++j) acc += u[j * m + r] * z[c * k + j];
-        xn[c * m + r] = x[c * m + r] + acc;
-      }
+    basis_times(u, m, k, z.data(), d, x.data(), xn.data());
     double tot = 0.0;
     for (int64_t r = 0; r < m; ++r) {
       double dd = 0.0, da = 0.0;
@@ -814,6 +846,30 @@ int orc_register_stream(const double* x_in, int64_t m, const double* y_in, int64
   for (int c = 0; c < d; ++c)
     for (int64_t r = 0; r < m; ++r)
       out_x[c * m + r] = normalize ? xt[c * m + r] * scale + center[c] : xt[c * m + r];
+  return kOk;
+}
+
+// Rows of Φ (kernel.hpp:31-47: exp(−max(|x_i|²+|x_j|²−2x_i·x_j, 0)/(2β²)),
+// unit diagonal) for the model rows rows[0..nrows), column-major
+// nrows × M.  The oracle's independent top-K basis (oracle.py topk_basis)
+// and the eigen-residual checks form Φ·V block by block from these rows.
+int orc_gram_rows(const double* x, int64_t m, int d, double beta, const int64_t* rows,
+                  int64_t nrows, double* out) {
+  if (beta <= 0.0) return fail(kParameter, "build_gram: beta must be positive");
+  const double inv = 1.0 / (2.0 * beta * beta);
+  std::vector<double> sq(m, 0.0);
+  for (int64_t i = 0; i < m; ++i)
+    for (int j = 0; j < d; ++j) sq[i] += at(x, m, i, j) * at(x, m, i, j);
+#pragma omp parallel for schedule(static)
+  for (int64_t c = 0; c < m; ++c) {
+    for (int64_t q = 0; q < nrows; ++q) {
+      const int64_t r = rows[q];
+      double xy = 0.0;
+      for (int j = 0; j < d; ++j) xy += at(x, m, r, j) * at(x, m, c, j);
+      const double d2 = sq[r] + sq[c] - 2.0 * xy;
+      out[c * nrows + q] = r == c ? 1.0 : std::exp(-std::max(d2, 0.0) * inv);
+    }
+  }
   return kOk;
 }
 

@@ -341,14 +341,17 @@ def load_spectral_cache(path: str):
 
 
 def register_stream(x, y, u, lam, lam_num=None, *, omega, lambda_reg, iterations,
-                    normalize=True) -> Result:
+                    normalize=True, xt_start=None, sigma2_start=None) -> Result:
     """Streaming-E-step restatement of register_pointsets with a given basis
-    (configs 2–4: no M×N matrix)."""
+    (configs 2–4: no M×N matrix).  ``xt_start``/``sigma2_start`` resume the
+    EM from a given state (x̃ in the loop's frame, σ²): a window of late
+    iterations is then checked without replaying the whole run."""
     x, y = _col(x), _col(y)
     u = np.asfortranarray(u, dtype=np.float64)
     lam = np.ascontiguousarray(lam, dtype=np.float64)
     lam_num = lam if lam_num is None else np.ascontiguousarray(lam_num, dtype=np.float64)
     m, d = x.shape
+    xs = None if xt_start is None else _col(xt_start)
     out_x = np.zeros((m, d), order="F")
     trace = np.zeros(max(iterations, 1))
     it = C.c_int()
@@ -356,7 +359,71 @@ def register_stream(x, y, u, lam, lam_num=None, *, omega, lambda_reg, iterations
     _check(lib().orc_register_stream(_ptr(x), _I64(m), _ptr(y), _I64(y.shape[0]), d,
                                      C.c_double(omega), C.c_double(lambda_reg), int(iterations),
                                      int(normalize), _ptr(u), _ptr(lam), _ptr(lam_num),
-                                     _I64(u.shape[1]), _ptr(out_x), _ptr(trace), C.byref(it),
-                                     C.byref(s0)))
+                                     _I64(u.shape[1]), _ptr(xs),
+                                     C.c_double(sigma2_start or 0.0), _ptr(out_x), _ptr(trace),
+                                     C.byref(it), C.byref(s0)))
     return Result(np.ascontiguousarray(out_x), np.zeros_like(out_x), trace[: it.value].copy(),
                   s0.value)
+
+
+# ------------------------------------------- top-K basis without forming Φ
+
+
+def gram_rows(x, beta: float, rows) -> np.ndarray:
+    """Rows ``rows`` of Φ (kernel.hpp:31-47) as a len(rows) × M array."""
+    x = _col(x)
+    m, d = x.shape
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.zeros((len(rows), m), order="F")
+    _check(lib().orc_gram_rows(_ptr(x), _I64(m), d, C.c_double(beta),
+                               rows.ctypes.data_as(C.POINTER(C.c_int64)), _I64(len(rows)),
+                               _ptr(out)))
+    return out
+
+
+def gram_apply(x, beta: float, v, rows=None, block: int = 2048) -> np.ndarray:
+    """Φ[rows]·V in fp64 without forming Φ (row blocks of Φ from the C
+    restatement, times V through BLAS)."""
+    m = np.asarray(x).shape[0]
+    rows = np.arange(m) if rows is None else np.asarray(rows, dtype=np.int64)
+    v = np.asarray(v, dtype=np.float64)
+    out = np.empty((len(rows), v.shape[1]))
+    for s in range(0, len(rows), block):
+        out[s:s + block] = gram_rows(x, beta, rows[s:s + block]) @ v
+    return out
+
+
+def topk_basis(x, beta: float, rank: int, *, power_iters: int = 4, oversample=None,
+               seed: int = 1234):
+    """Top-``rank`` eigenpairs of Φ (kernel.hpp:49-72 semantics: descending,
+    λ < 1e-12·λmax clamped to 0) by randomized block subspace iteration in
+    fp64 — an implementation independent of the device's (different start,
+    numpy QR / eigh, CPU Φ·V).  Returns (U, λ clamped, λ raw, residuals),
+    residuals[i] = ‖Φu_i − λ_i u_i‖ / λ_1."""
+    m = np.asarray(x).shape[0]
+    p = max(16, rank // 5) if oversample is None else oversample
+    b = min(m, rank + p)
+    rng = np.random.default_rng(seed)
+    q, _ = np.linalg.qr(gram_apply(x, beta, rng.standard_normal((m, b))))
+    for _ in range(power_iters):
+        q, _ = np.linalg.qr(gram_apply(x, beta, q))
+    z = gram_apply(x, beta, q)
+    bm = q.T @ z
+    theta, s = np.linalg.eigh(0.5 * (bm + bm.T))
+    order = np.argsort(theta)[::-1][:rank]
+    theta, s = theta[order], s[:, order]
+    u = q @ s
+    res = np.linalg.norm(z @ s - u * theta, axis=0) / max(theta[0], 1e-300)
+    lam_raw = theta.copy()
+    lam = theta.copy()
+    lam[lam < 1e-12 * max(lam[0], 0.0)] = 0.0  # kernel.hpp:68-70
+    return np.asfortranarray(u), lam, lam_raw, res
+
+
+def eigen_residuals(x, beta: float, u, lam, rows) -> np.ndarray:
+    """max over the sampled model rows of |(Φu_i)_r − λ_i u_ir| / λ_1 per
+    eigenpair: an independent fp64 check of a device basis at full size."""
+    u = np.asarray(u, dtype=np.float64)
+    rows = np.asarray(rows, dtype=np.int64)
+    pu = gram_apply(x, beta, u, rows=rows)
+    return np.abs(pu - u[rows] * np.asarray(lam)[None, :]).max(axis=0) / max(lam[0], 1e-300)

@@ -116,7 +116,8 @@ class _Result(C.Structure):
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("tiles_evaluated", C.c_int64 * 2),
                 ("spectral_rank", C.c_int64),
-                ("mstep_fused", C.c_int32), ("reserved0", C.c_int32)]
+                ("mstep_fused", C.c_int32), ("reserved0", C.c_int32),
+                ("pairs_by_form", C.c_int64 * 4)]
 
 
 _lib = None
@@ -360,6 +361,7 @@ class Context:
                     sigma2_trace=trace[: res.iterations_run].copy(),
                     iterations_run=res.iterations_run, degenerate_rows=res.degenerate_rows,
                     tiles_evaluated=(int(res.tiles_evaluated[0]), int(res.tiles_evaluated[1])),
+                    pairs_by_form=tuple(int(v) for v in res.pairs_by_form),
                     spectral_rank=int(res.spectral_rank),
                     mstep_fused=bool(res.mstep_fused))
 

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 #include <stdexcept>
@@ -44,7 +45,10 @@ enum DevErr : int {
 };
 
 // Per-iteration scalars living in device memory so a captured CUDA graph can
-// replay iterations without host round trips.
+// replay iterations without host round trips.  The E-step scalars of
+// iteration i+1 (σ² floor, coordinate scale, outlier constant) are set by the
+// last step of iteration i (estep_scalars_for_next), those of iteration 0 by
+// init_state_kernel — there is no per-iteration prologue launch.
 struct IterState {
   double sigma2;        // σ² entering this iteration (unclamped, as the reference)
   double sigma2_e;      // max(σ², 1e-10): the value the E-step uses
@@ -61,7 +65,47 @@ struct IterState {
   int32_t iters_run;
   int32_t keff;         // leading eigenpairs the M-step streams this iteration (mstep.cu)
   double sigma2_m;      // σ² the last M-step solved with (final coefficients)
+  double sigma2_e_last; // σ²_e of the last E-step that ran (dense correspondence output)
+  // E-step constants (set once by the host): ω, M, global N, D
+  double omega;
+  int64_t m_all, n_all;
+  int32_t dim;
+  int32_t flag_count[2];  // columns / rows queued for the exact fallback this iteration
+  int32_t cull_on;        // this iteration builds culled work lists (else: every pair)
+  int32_t cull_pays;      // the last lists dropped enough units to pay for themselves
+  int32_t pad1;
 };
+
+// Iterations between re-checks of a culling that did not pay (engine:
+// lists are skipped while the previous lists kept ≥ kCullKeepFrac of the
+// units, except every kCullRecheck-th iteration).
+constexpr int kCullRecheck = 8;
+constexpr double kCullKeepFrac = 0.94;
+
+// The E-step scalars for σ² (correspondence.hpp:43-47 floor + clamp flag,
+// :61-66 outlier constant in log2 units), the fallback queues emptied, and
+// the culling decision — run by ONE thread at the end of an iteration (for
+// the next one) and by init_state_kernel (iteration 0).
+__device__ __forceinline__ void estep_scalars_for_next(IterState* st, double sigma2, int next_iter) {
+  st->sigma2_e_last = st->sigma2_e;
+  double s2 = sigma2;
+  if (s2 < kSigma2Floor) {
+    s2 = kSigma2Floor;
+    st->sigma2_clamps += 1;
+  }
+  st->sigma2_e = s2;
+  st->sx = static_cast<float>(sqrt(kLog2e / (2.0 * s2)));
+  if (st->omega > 0.0) {
+    const double log_c = 0.5 * st->dim * log(2.0 * M_PI * s2) +
+                         log(st->omega / (1.0 - st->omega)) +
+                         log(static_cast<double>(st->m_all) / static_cast<double>(st->n_all));
+    st->log2c = log_c * kLog2e;
+  } else {
+    st->log2c = -INFINITY;
+  }
+  st->flag_count[0] = st->flag_count[1] = 0;
+  st->cull_on = next_iter == 0 || st->cull_pays || next_iter % kCullRecheck == 0;
+}
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;

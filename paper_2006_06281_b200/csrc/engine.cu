@@ -97,7 +97,7 @@ __global__ void dense_posterior_kernel(const double* __restrict__ xt64, int64_t 
   const int lane = threadIdx.x & 31;
   const int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (j >= n) return;
-  const double sigma2 = st->sigma2_e;
+  const double sigma2 = st->sigma2_e_last;  // the σ² (floored) of the last E-step
   const double inv = 1.0 / (2.0 * sigma2);
   const bool has_outlier = omega > 0.0;
   const double log_c = has_outlier ? 0.5 * d * log(2.0 * M_PI * sigma2) +
@@ -199,7 +199,7 @@ struct Session {
   DevBuf<float4> xt4, y4b, resid4, g4;
   DevBuf<double> b2, pt1, col_seg, row_seg, ptilde_y, var, log2p1, zpart, vpart, coef,
       sig_part, trace;
-  DevBuf<int32_t> col_flags, row_flags, flags_count, degenerate;
+  DevBuf<int32_t> col_flags, row_flags, col_done, row_done, degenerate;
   DevBuf<uint64_t> stamps;
   DevBuf<IterState> st;
 
@@ -222,8 +222,7 @@ struct Session {
   DevBuf<unsigned long long> cull_counters;
   DevBuf<int32_t> probe_paid;                // culling probe outcome per block (both passes)
   // per-iteration work lists of the two passes (culled (block, sub-tile) pairs)
-  DevBuf<int32_t> wl1_tiles, wl1_off, wl2_tiles, wl2_off, wl2_off_cc, wl_done;
-  DevBuf<double> row_seg_cc;  // tensor-core pass 2: the CUDA-core kernel's segments
+  DevBuf<int32_t> wl1_tiles, wl1_off, wl2_tiles, wl2_off, wl_done;
 
   // ---- distributed (NCCL) sharding: scene N split over ranks, model rows
   // [m0, m0+mr) owned by this rank (m_pad = world·mr ≥ M).  In this mode
@@ -245,7 +244,8 @@ struct Session {
                     &var, &log2p1, &zpart, &vpart, &coef, &sig_part, &trace, &zpart_fused})
       b->release();
     for (auto* b : {&xt4, &y4b, &resid4, &g4}) b->release();
-    for (auto* b : {&col_flags, &row_flags, &flags_count, &degenerate, &mfused_done}) b->release();
+    for (auto* b : {&col_flags, &row_flags, &col_done, &row_done, &degenerate, &mfused_done})
+      b->release();
     stamps.release();
     st.release();
     for (auto* b : {&rowsum_all, &rowsum_own, &fsum_all, &fsum_own, &zfull, &sig_local, &stage})
@@ -259,9 +259,7 @@ struct Session {
     sbminmax.release();
     cull_counters.release();
     probe_paid.release();
-    for (auto* b : {&wl1_tiles, &wl1_off, &wl2_tiles, &wl2_off, &wl2_off_cc, &wl_done})
-      b->release();
-    row_seg_cc.release();
+    for (auto* b : {&wl1_tiles, &wl1_off, &wl2_tiles, &wl2_off, &wl_done}) b->release();
   }
 };
 
@@ -447,7 +445,6 @@ float cull_margin_bits() {
 void set_cull(Session& s, EStepBuffers& eb, int64_t m, int64_t n_local, int64_t n_global) {
   CullInfo& c = eb.cull;
   c.enabled = s.cull && s.xlo.p && s.ylo.p && s.wl1_tiles.p && s.wl2_tiles.p ? 1 : 0;
-  c.lists = (c.enabled || s.ep.tc) && s.wl2_tiles.p ? 1 : 0;
   const char* pe = std::getenv("FCPD_CULL_PROBE");
   c.probe = pe ? (std::atoi(pe) != 0) : 1;
   c.n_xtiles = ceil_div(m, kTilePts);
@@ -469,18 +466,20 @@ void set_cull(Session& s, EStepBuffers& eb, int64_t m, int64_t n_local, int64_t 
   c.margin2 =
       bits + static_cast<float>(std::log2(static_cast<double>(std::max<int64_t>(n_global, 1))));
   c.counters = s.cull_counters.p;
+  c.wl1_offset = s.wl1_off.p;
+  c.wl1_units = static_cast<int64_t>(c.n_ytiles) * c.n_xsub;
+  c.wl2_units = static_cast<int64_t>(c.n_xtiles) * c.n_ysub;
   c.probe_paid1 = s.probe_paid.p;
   c.probe_paid2 = s.probe_paid.p ? s.probe_paid.p + c.n_ytiles : nullptr;
   eb.cullw = CullBuffers{s.xlo.p,  s.xhi.p,  s.ylo.p,  s.yhi.p,  s.bminmax.p,
                          s.sxlo.p, s.sxhi.p, s.sylo.p, s.syhi.p, s.sbminmax.p};
   eb.wl1 = WorkListBuffers{s.wl1_tiles.p, s.wl1_off.p, s.wl_done.p};
-  eb.wl2 = WorkListBuffers{s.wl2_tiles.p, s.wl2_off.p, s.wl_done.p ? s.wl_done.p + 1 : nullptr,
-                           s.wl2_off_cc.p};
+  eb.wl2 = WorkListBuffers{s.wl2_tiles.p, s.wl2_off.p, s.wl_done.p ? s.wl_done.p + 1 : nullptr};
 }
 
 // E-step buffers of the session (pt1: optional Σ_m P_mn output; resid:
-// write R = P̃Y − X for the M-step).
-EStepBuffers estep_buffers(Session& s, double* pt1, bool resid) {
+// write R = P̃Y − X for the M-step; row_aos: distributed row sums instead).
+EStepBuffers estep_buffers(Session& s, double* pt1, bool resid, double* row_aos = nullptr) {
   EStepBuffers eb{};
   eb.xt4 = s.xt4.p;
   eb.xt64 = s.xt64.p;
@@ -489,13 +488,15 @@ EStepBuffers estep_buffers(Session& s, double* pt1, bool resid) {
   eb.pt1 = pt1;
   eb.col_seg = s.col_seg.p;
   eb.row_seg = s.row_seg.p;
-  eb.row_seg_cc = s.row_seg_cc.p;
+  eb.col_done = s.col_done.p;
+  eb.row_done = s.row_done.p;
   eb.col_flags = s.col_flags.p;
   eb.row_flags = s.row_flags.p;
-  eb.flags_count = s.flags_count.p;
   eb.out = RowOut{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p,
                   resid ? s.resid4.p : nullptr, resid ? s.x0.p : nullptr};
   eb.ystats = s.ystats;
+  eb.row_aos = row_aos;
+  eb.stamps = s.stamps.p;
   set_cull(s, eb, s.m, s.n, s.dist ? s.n_global : s.n);
   return eb;
 }
@@ -505,6 +506,11 @@ EStepBuffers estep_buffers(Session& s, double* pt1, bool resid) {
 void alloc_estep(Session& s, int64_t m, int64_t n, cudaStream_t str) {
   s.col_seg.ensure(s.ep.col_seg_doubles());
   s.row_seg.ensure(s.ep.row_seg_doubles());
+  // block arrival counters of the pass fix-ups (self-resetting)
+  s.col_done.ensure(s.ep.col_blocks);
+  s.row_done.ensure(s.ep.row_blocks);
+  FCPD_CUDA(cudaMemsetAsync(s.col_done.p, 0, sizeof(int32_t) * s.ep.col_blocks, str));
+  FCPD_CUDA(cudaMemsetAsync(s.row_done.p, 0, sizeof(int32_t) * s.ep.row_blocks, str));
   const int64_t nxt = ceil_div(m, kTilePts), nyt = ceil_div(n, kTilePts);
   const int64_t nxs = ceil_div(m, kSubPts), nys = ceil_div(n, kSubPts);
   s.cull = cull_default(nxt, nyt);
@@ -518,21 +524,19 @@ void alloc_estep(Session& s, int64_t m, int64_t n, cudaStream_t str) {
   s.sylo.ensure(nys);
   s.syhi.ensure(nys);
   s.sbminmax.ensure(nys);
-  s.cull_counters.ensure(2);
-  FCPD_CUDA(cudaMemsetAsync(s.cull_counters.p, 0, 2 * sizeof(unsigned long long), str));
+  // [0..1] (block, sub-tile) units evaluated per pass, [2..5] pair slots by
+  // (pass, form) — cumulative over the session
+  s.cull_counters.ensure(6);
+  FCPD_CUDA(cudaMemsetAsync(s.cull_counters.p, 0, 6 * sizeof(unsigned long long), str));
   s.probe_paid.ensure(nxt + nyt);
   FCPD_CUDA(cudaMemsetAsync(s.probe_paid.p, 1, (nxt + nyt) * sizeof(int32_t), str));  // ≠ 0
-  if (s.cull || s.ep.tc) {
+  if (s.cull) {
     s.wl1_tiles.ensure(static_cast<size_t>(nyt) * nxs);
     s.wl1_off.ensure(nyt + 1);
     s.wl2_tiles.ensure(static_cast<size_t>(nxt) * nys);
     s.wl2_off.ensure(nxt + 1);
     s.wl_done.ensure(2);
     FCPD_CUDA(cudaMemsetAsync(s.wl_done.p, 0, 2 * sizeof(int32_t), str));
-  }
-  if (s.ep.tc) {
-    s.wl2_off_cc.ensure(nxt + 1);
-    s.row_seg_cc.ensure(static_cast<size_t>(s.ep.row_grid + s.ep.row_blocks) * 5 * 256);
   }
   launch_tile_bbox(s.y4b.p, n, s.ylo.p, s.yhi.p, s.sylo.p, s.syhi.p, nullptr, str);
 }
@@ -548,7 +552,7 @@ void enqueue_iteration(fcpd_ctx* ctx, Session& s, cudaEvent_t* ev = nullptr) {
     if (ev) FCPD_CUDA(cudaEventRecord(ev[i], str));
   };
   rec(0);
-  launch_estep(s.ep, eb, s.m, s.n, s.d, s.cfg.omega, st, s.stamps.p, str, ev ? ev[1] : nullptr);
+  launch_estep(s.ep, eb, s.m, s.n, st, str, ev ? ev[1] : nullptr);
   rec(2);
   if (s.mfused) {  // one cooperative kernel; its time is booked as the Qᵀ·R phase
     MstepFusedArgs a{b.q, b.kpad, b.k, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.tau,
@@ -601,7 +605,6 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
   s.degenerate.ensure(m);
   s.col_flags.ensure(n);
   s.row_flags.ensure(m);
-  s.flags_count.ensure(2);
   s.st.ensure(1);
   s.capacity = std::max(capacity, 1);
   s.trace.ensure(s.capacity);
@@ -663,7 +666,7 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
     s.zpart.ensure(s.zp.part_doubles());
     s.vpart.ensure(s.vp.part_doubles());
     s.coef.ensure(3 * b.k);
-    s.g4.ensure(b.k);
+    s.g4.ensure(b.kpad);  // the fused M-step streams whole quads (kpad ≥ K)
     if (s.mfused) {
       s.mfused_grid = mstep_fused_grid(ctx->sm_count);
       s.zpart_fused.ensure(static_cast<size_t>(b.k) * s.mfused_grid * 3);
@@ -674,13 +677,18 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
   }
 }
 
+// Iteration-0 state: σ², then the E-step scalars on the device (the code
+// every later iteration uses for its σ²); ω, M, global N, D.
 void reset_state(fcpd_ctx* ctx, Session& s, double sigma2) {
   IterState h{};
   h.sigma2 = sigma2;
   h.sigma2_e = sigma2;
   h.active = 1;
   FCPD_CUDA(cudaMemcpyAsync(s.st.p, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
-  FCPD_CUDA(cudaMemsetAsync(s.degenerate.p, 0, sizeof(int32_t) * s.m, ctx->stream));
+  launch_init_state(s.st.p, sigma2, s.cfg.omega, s.m, s.dist ? s.n_global : s.n, s.d,
+                    ctx->stream);
+  FCPD_CUDA(cudaMemsetAsync(s.degenerate.p, 0, sizeof(int32_t) * (s.dist ? s.mr : s.m),
+                            ctx->stream));
 }
 
 // registration.hpp:59-69 (host, fp64, same formula)
@@ -1006,12 +1014,13 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
     FCPD_CUDA(cudaMemcpyAsync(stamps.data(), s.stamps.p, sizeof(uint64_t) * 4 * run,
                               cudaMemcpyDeviceToHost, str));
   s.d2h += sizeof(uint64_t) * 4 * run;
-  unsigned long long tiles[2] = {0, 0};
+  unsigned long long tiles[6] = {0, 0, 0, 0, 0, 0};
   if (s.cull_counters.p)
     FCPD_CUDA(cudaMemcpyAsync(tiles, s.cull_counters.p, sizeof tiles, cudaMemcpyDeviceToHost, str));
   FCPD_CUDA(cudaStreamSynchronize(str));
   out->tiles_evaluated[0] = static_cast<int64_t>(tiles[0]);
   out->tiles_evaluated[1] = static_cast<int64_t>(tiles[1]);
+  for (int k = 0; k < 4; ++k) out->pairs_by_form[k] = static_cast<int64_t>(tiles[2 + k]);
   out->spectral_rank = s.zp.trunc && h.keff > 0 ? std::min<int64_t>(h.keff, b.k) : b.k;
   out->mstep_fused = s.mfused ? 1 : 0;
   if (out->degenerate_mask)
@@ -1073,11 +1082,9 @@ void enqueue_iteration_dist(fcpd_ctx* ctx, Session& s) {
   cudaStream_t str = ctx->stream;
   ncclComm_t comm = ctx->comm;
   const int64_t m = s.m, nl = s.n;
-  const EStepBuffers eb = estep_buffers(s, nullptr, false);
-  launch_estep_prologue(st, m, s.n_global, s.d, s.cfg.omega, s.flags_count.p, s.stamps.p, str);
+  const EStepBuffers eb = estep_buffers(s, nullptr, false, s.rowsum_all.p);
   launch_estep_pass1(s.ep, eb, m, nl, st, str);  // column-local: no communication
-  launch_estep_pass2_partials(s.ep, eb, m, nl, st, str);
-  launch_row_seg_sum(s.ep, eb, m, nl, s.m_pad, s.rowsum_all.p, st, str);
+  launch_estep_pass2(s.ep, eb, m, nl, st, str);  // row sums of the local columns (AoS)
   FCPD_NCCL(ncclReduceScatter(s.rowsum_all.p, s.rowsum_own.p, s.mr * 5, ncclDouble, ncclSum,
                               comm, str));
   const DistRowOut o{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p, s.resid4.p, s.x0.p};
@@ -1237,8 +1244,9 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
   s.pt1.ensure(n);
   s.col_flags.ensure(n);
   s.row_flags.ensure(m);
-  s.flags_count.ensure(2);
   s.rowsum_all.ensure(5 * s.m_pad);
+  // rows in [M, M_pad) are never written: zero once
+  FCPD_CUDA(cudaMemsetAsync(s.rowsum_all.p, 0, sizeof(double) * 5 * s.m_pad, str));
   s.rowsum_own.ensure(5 * mr);
   s.fsum_all.ensure(5 * s.m_pad);
   s.fsum_own.ensure(5 * mr);
@@ -1511,17 +1519,15 @@ int32_t fcpd_kernels_per_iteration(const fcpd_ctx* ctx) {
   // pass-2 list.
   if (!ctx) return 0;
   const Session& s = ctx->sess;
-  const bool culling = s.cull && s.xlo.p && s.ylo.p;
-  int extra = culling ? 4 : 0;
-  // tensor-core pass 2: its CUDA-core companion kernel (+ x̃ boxes and the
-  // routing list when culling is off)
-  if (s.ep.tc) extra += 1 + (culling ? 0 : 2);
-  if (s.dist) return 17 + extra + (s.zp.trunc ? 1 : 0);
-  // fused M-step: one kernel instead of Qᵀ·R, z-reduce, Q·g, transform, σ²
-  // (and the spectral rank)
-  if (s.mfused) return 8 + extra;
-  if (s.zp.trunc) extra += 1;  // spectral rank
-  return 12 + extra;
+  const bool culling = s.cull && s.xlo.p && s.ylo.p && s.wl1_tiles.p;
+  const int e = estep_kernels(culling, s.dist);
+  // distributed M-step: finalize-own, fb-max, fb-sum, fb-finalize, Qᵀ·R,
+  // z-sum, z-filter, Q·g, transform, σ²-local, σ²-final (+ the collectives)
+  if (s.dist) return e + 11 + (s.zp.trunc ? 1 : 0);
+  // fused M-step: one kernel for rank, Qᵀ·R, filter, Q·g, transform and σ²
+  if (s.mfused) return e + 1;
+  // streaming: (spectral rank,) Qᵀ·R, z-reduce/filter, Q·g, transform, σ²
+  return e + 5 + (s.zp.trunc ? 1 : 0);
 }
 
 int fcpd_register(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n,
@@ -1613,7 +1619,7 @@ int fcpd_estep(fcpd_ctx* ctx, const double* xt, int64_t m, const double* y, int6
     prepare_buffers(ctx, s, xs, ys, 1, false);
     reset_state(ctx, s, sigma2);
     const EStepBuffers eb = estep_buffers(s, s.pt1.p, false);
-    launch_estep(s.ep, eb, m, n, d, omega, s.st.p, nullptr, ctx->stream);
+    launch_estep(s.ep, eb, m, n, s.st.p, ctx->stream);
     std::vector<double> pty(3 * m), lp(m), vr(m), pc(n);
     std::vector<int32_t> dg(m);
     cudaStream_t str = ctx->stream;
@@ -1661,7 +1667,7 @@ int fcpd_posterior_dense(fcpd_ctx* ctx, const double* xt, int64_t m, const doubl
     st.ensure(1);
     IterState h{};
     h.sigma2 = sigma2;
-    h.sigma2_e = std::max(sigma2, kSigma2Floor);  // correspondence.hpp:43-47
+    h.sigma2_e_last = std::max(sigma2, kSigma2Floor);  // correspondence.hpp:43-47
     FCPD_CUDA(cudaMemcpyAsync(xd.p, xt, sizeof(double) * d * m, cudaMemcpyHostToDevice, str));
     FCPD_CUDA(cudaMemcpyAsync(yd.p, y, sizeof(double) * d * n, cudaMemcpyHostToDevice, str));
     FCPD_CUDA(cudaMemcpyAsync(st.p, &h, sizeof h, cudaMemcpyHostToDevice, str));

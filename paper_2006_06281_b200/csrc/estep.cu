@@ -29,8 +29,10 @@
 // segments at block boundaries.  Every CTA therefore does the same work to
 // within one point, independent of how culling thinned the list.  A segment
 // (CTA g, block b) writes its fp64 partial sums to slot g + b (slots are
-// strictly increasing along the schedule, so unique); the combine sums a
-// block's slots in CTA order: deterministic, bitwise reproducible.
+// strictly increasing along the schedule, so unique).  The CTA that
+// completes a block's last segment (an arrival counter per block) sums the
+// block's slots in CTA order and finalises the block: deterministic,
+// bitwise reproducible, and no separate combine launch.
 
 #include <cuda_runtime.h>
 #include <math.h>
@@ -46,7 +48,6 @@ namespace fcpd {
 namespace {
 
 constexpr int kTile = kTilePts;  // points staged in shared memory per step
-constexpr int kCombineLanes = 1; // lanes cooperating on one row/column reduction
 constexpr float kPadCoord = 3.0e18f;  // padding point: t ≈ 1e37, 2^-t = 0
 constexpr int kListThreads = 256;     // list kernels: one CTA per own block
 static_assert(kListThreads == kTilePts, "list CTA: one thread per own point");
@@ -176,28 +177,161 @@ __device__ __forceinline__ float2 ex2x2(float2 v) {
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// Iteration prologue: σ² floor + clamp count (correspondence.hpp:43-47,
-// registration.hpp:122), coordinate scale, outlier constant (:61-66).
-__global__ void estep_prologue_kernel(IterState* st, int64_t m, int64_t n, int d,
-                                      double omega, int32_t* flags_count, uint64_t* stamps) {
-  griddep_wait();
-  if (!st->active) return;
-  if (stamps) stamps[4 * st->iter + 0] = globaltimer();
-  flags_count[0] = flags_count[1] = 0;  // column and row fallback lists
-  double s2 = st->sigma2;
-  if (s2 < kSigma2Floor) {
-    s2 = kSigma2Floor;
-    st->sigma2_clamps += 1;
-  }
-  st->sigma2_e = s2;
-  st->sx = static_cast<float>(sqrt(kLog2e / (2.0 * s2)));
-  if (omega > 0.0) {
-    const double log_c = 0.5 * d * log(2.0 * M_PI * s2) + log(omega / (1.0 - omega)) +
-                         log(static_cast<double>(m) / static_cast<double>(n));
-    st->log2c = log_c * kLog2e;
+// Iteration-0 state (later iterations get theirs from the last step of the
+// previous one, estep_scalars_for_next).
+__global__ void init_state_kernel(IterState* st, double sigma2, double omega, int64_t m,
+                                  int64_t n, int d) {
+  st->omega = omega;
+  st->m_all = m;
+  st->n_all = n;
+  st->dim = d;
+  st->cull_pays = 0;
+  estep_scalars_for_next(st, sigma2, 0);
+  st->sigma2_e_last = st->sigma2_e;
+}
+
+// ---------------------------------------------------------------------------
+// Block fix-up shared by both passes.  A block's segments come from the CTAs
+// [g0, g1] of the stream-K range holding its point-units (those with a
+// non-empty range); each bumps the block's arrival counter after writing its
+// slot, and the one that arrives last sums the slots in CTA order.
+struct SegRange {
+  int64_t g0 = 0, g1 = -1;
+  int count = 0;
+};
+__device__ __forceinline__ bool sk_empty(int64_t g, int64_t G, int64_t P) {
+  // an empty range needs P < G (a range holds ⌊P/G⌋ or ⌈P/G⌉ units)
+  return P < G && sk_start(g, G, P) == sk_start(g + 1, G, P);
+}
+__device__ __forceinline__ SegRange seg_range(const WorkList& wl, int64_t G, int64_t P, int b) {
+  SegRange r;
+  const int64_t ua = wl.off(b) << wl.ushift, ub = wl.off(b + 1) << wl.ushift;
+  if (ua >= ub) return r;
+  r.g0 = sk_owner(ua, G, P);
+  r.g1 = sk_owner(ub - 1, G, P);
+  if (P >= G) {
+    r.count = static_cast<int>(r.g1 - r.g0 + 1);
   } else {
-    st->log2c = -INFINITY;
+    for (int64_t g = r.g0; g <= r.g1; ++g) r.count += sk_empty(g, G, P) ? 0 : 1;
   }
+  return r;
+}
+// Release this CTA's slot writes and count its arrival at block b; true in
+// the CTA that completes the block (which then sees every slot).
+__device__ __forceinline__ bool arrive_last(int32_t* done, int b, int count) {
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done + b, 1) == count - 1;
+  __syncthreads();
+  const bool l = last;
+  if (l) __threadfence();
+  return l;
+}
+// Culling sessions use the culled list only when this iteration built one;
+// otherwise every unit (counted into tiles_evaluated by CTA 0).
+__device__ __forceinline__ WorkList resolve_list(WorkList wl) {
+  if (wl.dyn_on && !*wl.dyn_on) {
+    wl.implicit = 1;
+    if (wl.implicit_counter && blockIdx.x == 0 && threadIdx.x == 0)
+      atomicAdd(wl.implicit_counter, static_cast<unsigned long long>(wl.n_blocks) *
+                                         static_cast<unsigned long long>(wl.n_other));
+  }
+  return wl;
+}
+
+// Pass-1 column finalisation (the block fix-up, and blocks a culled list
+// left empty): b_n = −log2(Σ_m 2^{−t_mn} + c), Σ_m P_mn — or the exact
+// fallback's queue when the mass is too small for the flush-to-zero fast
+// path (flushed terms are < 2^-126 each: ≤ M·2^-126 in total; need ≤ 2^-50
+// of the total).  Returns b as float, NaN when queued.
+struct ColFix {
+  int32_t* done;      // [col_blocks] arrival counters
+  float4* y4b;        // .w ← b_n
+  double* b2;
+  double* pt1;        // optional
+  int32_t* flag_list;
+  float2* bminmax;    // optional (culling): per scene tile / sub-tile b range
+  float2* sbminmax;
+};
+__device__ __forceinline__ float col_finalize(const ColFix& f, int64_t col, double sm, int64_t m,
+                                              IterState* st) {
+  const double c = exp2(st->log2c);  // 0 when ω = 0
+  const double total = sm + c;
+  if (!(total >= static_cast<double>(m) * 0x1p-76)) {
+    const int slot = atomicAdd(&st->flag_count[0], 1);
+    f.flag_list[slot] = static_cast<int32_t>(col);
+    return NAN;  // the fallback writes b2 / pt1
+  }
+  const double b2 = -log2(total);
+  f.b2[col] = b2;
+  f.y4b[col].w = static_cast<float>(b2);
+  if (f.pt1) f.pt1[col] = sm / total;
+  return static_cast<float>(b2);
+}
+
+// Per scene tile and 32-column sub-tile: (min b, max b) for the pass-2
+// list, kCols consecutive columns per thread.  Columns queued for the
+// fallback (b unknown yet) count as +inf for the max and are left out of
+// the min (no known b at all → −inf: no floor from that unit) — both
+// conservative for the culling bounds.
+template <int kCols>
+__device__ __forceinline__ void col_b_ranges(const ColFix& f, int rb, int64_t n, float lo,
+                                             float hi) {
+  constexpr int kPerSub = kSubPts / kCols;  // threads per sub-tile
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int o = 1; o < kPerSub; o <<= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  const int64_t sub = static_cast<int64_t>(rb) * kSubPerTile + t / kPerSub;
+  if (t % kPerSub == 0 && (sub << 5) < n)
+    f.sbminmax[sub] = make_float2(lo == INFINITY ? -INFINITY : lo, hi);
+#pragma unroll
+  for (int o = kPerSub; o < 32; o <<= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  __shared__ float2 red[8];
+  if ((t & 31) == 0) red[t >> 5] = make_float2(lo, hi);
+  __syncthreads();
+  if (t == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      lo = fminf(lo, red[w].x);
+      hi = fmaxf(hi, red[w].y);
+    }
+    f.bminmax[rb] = make_float2(lo == INFINITY ? -INFINITY : lo, hi);
+  }
+  __syncthreads();
+}
+
+// Pass-1 block fix-up: each column's sum over the block's slots in CTA
+// order, finalisation, b ranges.
+template <int kCols>
+__device__ void col_block_fixup(const ColFix& f, const double* seg, const SegRange& sr,
+                                int64_t G, int64_t P, int rb, int64_t m, int64_t n,
+                                IterState* st) {
+  const int t = threadIdx.x;
+  float lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+  for (int h = 0; h < kCols; ++h) {
+    const int li = kCols * t + h;
+    const int64_t col = static_cast<int64_t>(rb) * kTile + li;
+    double sm = 0.0;
+    for (int64_t g = sr.g0; g <= sr.g1; ++g)
+      if (!sk_empty(g, G, P)) sm += __ldcg(seg + (g + rb) * kTile + li);
+    if (col < n) {
+      const float b = col_finalize(f, col, sm, m, st);
+      if (b == b) {
+        lo = fminf(lo, b);
+        hi = fmaxf(hi, b);
+      } else {
+        hi = INFINITY;
+      }
+    }
+  }
+  if (f.bminmax) col_b_ranges<kCols>(f, rb, n, lo, hi);
 }
 
 // ---------------------------------------------------------------------------
@@ -217,14 +351,21 @@ __global__ void estep_prologue_kernel(IterState* st, int64_t m, int64_t n, int d
 // block.  NC = 2 shares every staged model point's shared-memory operands
 // between two packed column pairs (fewer LDS per pair).
 template <int NC>
-__global__ void __launch_bounds__(128 / NC)
+__global__ void __launch_bounds__(128 / NC, NC == 2 ? 16 : 8)
     estep_col_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4,
-                     int64_t n, const IterState* __restrict__ st, WorkList wl,
-                     double* __restrict__ seg, float centred_max_r2) {
+                     int64_t n, IterState* __restrict__ st, WorkList wl_in,
+                     double* __restrict__ seg, float centred_max_r2, ColFix fix,
+                     unsigned long long* form_pairs, uint64_t* stamps) {
   griddep_wait();
   constexpr int kThr = 128 / NC;  // threads
   constexpr int kCols = 2 * NC;   // columns per thread
   if (!st->active) return;
+  if (stamps && blockIdx.x == 0 && threadIdx.x == 0) stamps[4 * st->iter] = globaltimer();
+  const WorkList wl = resolve_list(wl_in);
+  // pair slots evaluated by form (centred, difference): thread 0's tally in
+  // shared memory (no registers held across the pair loops)
+  __shared__ unsigned long long form_tally[2];
+  if (threadIdx.x == 0) form_tally[0] = form_tally[1] = 0ull;
   __shared__ float4 xa[kTile];  // centred (vx,vx,vy,vy) | diff (−x,−x,−y,−y)
   __shared__ float4 xb[kTile];  // centred (vz,vz,−|v|²,−|v|²) | diff (−z,−z,·,·)
   const float s = st->sx;
@@ -368,69 +509,22 @@ __global__ void __launch_bounds__(128 / NC)
     double* out = seg + (g + rb) * kTile;
 #pragma unroll
     for (int h = 0; h < kCols; ++h) out[kCols * t + h] = d[h];
+    if (t == 0)
+      form_tally[centred ? 0 : 1] += static_cast<unsigned long long>(pe - p) *
+                                     static_cast<unsigned long long>(
+                                         min(int64_t(kTile), n - int64_t(rb) * kTile));
+    // the CTA completing block rb's last segment finalises the block
+    const SegRange sr = seg_range(wl, G, P, rb);
+    if (arrive_last(fix.done, rb, sr.count)) {
+      col_block_fixup<kCols>(fix, seg, sr, G, P, rb, m, n, st);
+      if (t == 0) fix.done[rb] = 0;  // self-resetting for the next replay
+    }
     p = pe;
   }
-}
-
-// Sum of the segments of block b at local index li (lane-strided over the
-// block's CTAs, then a fixed xor tree): deterministic.
-template <int NQ>
-__device__ __forceinline__ void sum_segments(const WorkList& wl, int64_t G, const double* seg,
-                                             int b, int li, int lane, bool live, double (&a)[NQ]) {
-#pragma unroll
-  for (int k = 0; k < NQ; ++k) a[k] = 0.0;
-  if (live) {
-    const int64_t P = wl.off(wl.n_blocks) << wl.ushift;
-    const int64_t ua = wl.off(b) << wl.ushift, ub = wl.off(b + 1) << wl.ushift;
-    if (ua < ub) {
-      const int64_t g0 = sk_owner(ua, G, P), g1 = sk_owner(ub - 1, G, P);
-      for (int64_t g = g0 + lane; g <= g1; g += kCombineLanes) {
-        // an empty range needs P < G (a range holds ⌊P/G⌋ or ⌈P/G⌉ units)
-        if (P < G && sk_start(g, G, P) == sk_start(g + 1, G, P)) continue;
-        const double* sp = seg + (g + b) * NQ * kTile + li;
-#pragma unroll
-        for (int k = 0; k < NQ; ++k) a[k] += sp[k * kTile];
-      }
-    }
+  if (form_pairs && t == 0) {
+    if (form_tally[0]) atomicAdd(form_pairs, form_tally[0]);
+    if (form_tally[1]) atomicAdd(form_pairs + 1, form_tally[1]);
   }
-#pragma unroll
-  for (int o = kCombineLanes / 2; o > 0; o >>= 1)
-#pragma unroll
-    for (int k = 0; k < NQ; ++k) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
-}
-
-// Pass 1 combine: column normaliser b_n.  Flags columns whose mass is too
-// small for the flush-to-zero fast path.
-__global__ void estep_col_combine_kernel(const double* __restrict__ seg, WorkList wl, int G,
-                                         int64_t m, int64_t n, float4* __restrict__ y4b,
-                                         double* __restrict__ b2_out, double* __restrict__ pt1,
-                                         int32_t* __restrict__ flag_list,
-                                         int32_t* __restrict__ flag_count,
-                                         const IterState* __restrict__ st) {
-  griddep_wait();
-  if (!st->active) return;
-  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t col = gid / kCombineLanes;
-  const int lane = static_cast<int>(gid % kCombineLanes);
-  double a[1];
-  sum_segments<1>(wl, G, seg, static_cast<int>(col / kTile), static_cast<int>(col % kTile), lane,
-                  col < n, a);
-  if (col >= n || lane != 0) return;
-  const double sm = a[0];
-  const double log2c = st->log2c;
-  const double c = exp2(log2c);  // 0 when ω = 0
-  const double total = sm + c;
-  // flushed terms are < 2^-126 each: ≤ M·2^-126 in total; need ≤ 2^-50·total
-  const bool flagged = !(total >= static_cast<double>(m) * 0x1p-76);
-  if (flagged) {
-    const int slot = atomicAdd(flag_count, 1);
-    flag_list[slot] = static_cast<int32_t>(col);
-    return;  // fallback writes b2 / pt1
-  }
-  const double b2 = -log2(total);
-  b2_out[col] = b2;
-  y4b[col].w = static_cast<float>(b2);
-  if (pt1) pt1[col] = sm / total;
 }
 
 // Exact column normaliser for flagged columns: warp per column, max-shifted
@@ -439,11 +533,10 @@ __global__ void estep_col_fallback_kernel(const float4* __restrict__ xt4, int64_
                                           float4* __restrict__ y4b, double* __restrict__ b2_out,
                                           double* __restrict__ pt1,
                                           const int32_t* __restrict__ flag_list,
-                                          const int32_t* __restrict__ flag_count,
                                           const IterState* __restrict__ st) {
   griddep_wait();
   if (!st->active) return;
-  const int count = *flag_count;
+  const int count = st->flag_count[0];
   const int lane = threadIdx.x & 31;
   const int warps = (blockDim.x >> 5) * gridDim.x;
   const float s = st->sx;
@@ -475,6 +568,92 @@ __global__ void estep_col_fallback_kernel(const float4* __restrict__ xt4, int64_
 }
 
 // ---------------------------------------------------------------------------
+// Row finalisation shared by the pass-2 block fix-up and the fallback.
+__device__ __forceinline__ void finalize_row(int64_t row, int64_t m, double log2p1, double s0,
+                                             double sy0, double sy1, double sy2, double sv,
+                                             const double* __restrict__ xt64, double s,
+                                             const RowOut& out, const YStats& ys,
+                                             IterState* st) {
+  const double x0 = xt64[row], x1 = xt64[m + row], x2 = xt64[2 * m + row];
+  double p0, p1, p2, var;
+  int deg = 0;
+  if (log2p1 < kLog2DegenerateRow) {  // uniform row, correspondence.hpp:89-91
+    deg = 1;
+    p0 = ys.mean[0];
+    p1 = ys.mean[1];
+    p2 = ys.mean[2];
+    var = ys.sq_mean - 2.0 * (x0 * p0 + x1 * p1 + x2 * p2) + (x0 * x0 + x1 * x1 + x2 * x2);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&st->degenerate_rows), 1ull);
+  } else {
+    const double inv = 1.0 / (s0 * s);
+    p0 = sy0 * inv;
+    p1 = sy1 * inv;
+    p2 = sy2 * inv;
+    var = sv / (s0 * s * s);
+  }
+  out.ptilde_y[row] = p0;
+  out.ptilde_y[m + row] = p1;
+  out.ptilde_y[2 * m + row] = p2;
+  out.var[row] = var;
+  out.log2p1[row] = log2p1;
+  out.degenerate[row] = deg;
+  if (out.resid4) {
+    // R = P̃Y − X (registration.hpp:136), fp32 for the Q product
+    const double* X = out.x0;
+    out.resid4[row] = make_float4(static_cast<float>(p0 - X[row]),
+                                  static_cast<float>(p1 - X[m + row]),
+                                  static_cast<float>(p2 - X[2 * m + row]), 0.f);
+  }
+}
+
+// Where the pass-2 block fix-up puts a row's five sums (S0, Σw·y' (3), Σw·t
+// in the scaled frame): single GPU → finalised (or queued for the exact
+// fallback when the mass is too small for the flush-to-zero fast path);
+// distributed → AoS row sums of this rank's columns for the reduce-scatter.
+struct RowFix {
+  int32_t* done;        // [row_blocks] arrival counters
+  const double* xt64;
+  RowOut out;
+  YStats ys;
+  int32_t* flag_list;
+  double* aos;          // distributed: [m_pad][5] (then out/flag_list unused)
+};
+__device__ __forceinline__ void row_finalize(const RowFix& f, int64_t row, int64_t m, int64_t n,
+                                             const double (&a)[5], IterState* st) {
+  if (f.aos) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) f.aos[row * 5 + k] = a[k];
+    return;
+  }
+  if (!(a[0] >= static_cast<double>(n) * 0x1p-76)) {
+    const int slot = atomicAdd(&st->flag_count[1], 1);
+    f.flag_list[slot] = static_cast<int32_t>(row);
+    return;
+  }
+  finalize_row(row, m, log2(a[0]), a[0], a[1], a[2], a[3], a[4], f.xt64, derived_scale(st), f.out,
+               f.ys, st);
+}
+template <int kRows>
+__device__ void row_block_fixup(const RowFix& f, const double* seg, const SegRange& sr,
+                                int64_t G, int64_t P, int rb, int64_t m, int64_t n,
+                                IterState* st) {
+  const int t = threadIdx.x;
+#pragma unroll 1
+  for (int h = 0; h < kRows; ++h) {
+    const int li = kRows * t + h;
+    const int64_t row = static_cast<int64_t>(rb) * kTile + li;
+    double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int64_t g = sr.g0; g <= sr.g1; ++g) {
+      if (sk_empty(g, G, P)) continue;
+      const double* sp = seg + (g + rb) * 5 * kTile + li;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) a[k] += __ldcg(sp + k * kTile);
+    }
+    if (row < m) row_finalize(f, row, m, n, a, st);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Pass 2: per-row sums over n: S0, Sy (3), SV.  Own block = 256 model points
 // (thread: row pair 2·tid, 2·tid+1); the staged tiles are scene points.
 //  * centred: L = (b − |u|²) − |v|² + 2u·v with u = y' − c, v = x' − c, and
@@ -492,13 +671,18 @@ __global__ void estep_col_fallback_kernel(const float4* __restrict__ xt4, int64_
 template <int NP>
 __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
     estep_row_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4b,
-                     int64_t n, const IterState* __restrict__ st, WorkList wl,
+                     int64_t n, IterState* __restrict__ st, WorkList wl_in,
                      double* __restrict__ seg /* [slot][5][256] */, float centred_max_r2,
-                     int flush) {
+                     int flush, RowFix fix, unsigned long long* form_pairs) {
   griddep_wait();
   constexpr int kThr = 128 / NP;   // threads
   constexpr int kRows = 2 * NP;    // rows per thread
   if (!st->active) return;
+  const WorkList wl = resolve_list(wl_in);
+  // pair slots evaluated by form (centred, difference): thread 0's tally in
+  // shared memory (no registers held across the pair loops)
+  __shared__ unsigned long long form_tally[2];
+  if (threadIdx.x == 0) form_tally[0] = form_tally[1] = 0ull;
   __shared__ float4 ya[kTile];  // centred (ux,ux,uy,uy) | diff (y,y,y',y') scaled
   __shared__ float4 yb[kTile];  // centred (uz,uz,b−|u|²,·) | diff (z,z,b,b)
   __shared__ float2 yq[kTile];  // centred (|u|², |u|²)
@@ -705,7 +889,21 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
         out[4 * kTile + li] = s4;
       }
     }
+    if (t == 0)
+      form_tally[centred ? 0 : 1] += static_cast<unsigned long long>(pe - p) *
+                                     static_cast<unsigned long long>(
+                                         min(int64_t(kTile), m - int64_t(rb) * kTile));
+    // the CTA completing block rb's last segment finalises its rows
+    const SegRange sr = seg_range(wl, G, P, rb);
+    if (arrive_last(fix.done, rb, sr.count)) {
+      row_block_fixup<kRows>(fix, seg, sr, G, P, rb, m, n, st);
+      if (t == 0) fix.done[rb] = 0;  // self-resetting for the next replay
+    }
     p = pe;
+  }
+  if (form_pairs && t == 0) {
+    if (form_tally[0]) atomicAdd(form_pairs, form_tally[0]);
+    if (form_tally[1]) atomicAdd(form_pairs + 1, form_tally[1]);
   }
 }
 
@@ -718,10 +916,13 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
 __global__ void tile_bbox_kernel(const float4* __restrict__ p, int64_t count,
                                  float4* __restrict__ lo, float4* __restrict__ hi,
                                  float4* __restrict__ slo, float4* __restrict__ shi,
-                                 const IterState* __restrict__ st) {
+                                 const IterState* __restrict__ st, uint64_t* stamps) {
   static_assert(kSubPts == 32, "one warp per sub-tile");
   griddep_wait();
   if (st && !st->active) return;
+  // the first kernel of a culling session's iteration stamps its start
+  if (stamps && blockIdx.x == 0 && threadIdx.x == 0) stamps[4 * st->iter] = globaltimer();
+  if (st && !st->cull_on) return;  // no lists this iteration: no x̃ boxes needed
   __shared__ float red[6][8];
   const int64_t i = static_cast<int64_t>(blockIdx.x) * kTile + threadIdx.x;
   float v[6];
@@ -764,39 +965,6 @@ __global__ void tile_bbox_kernel(const float4* __restrict__ p, int64_t count,
   }
 }
 
-// per scene tile and sub-tile: (min b_n, max b_n) after pass 1
-__global__ void tile_bminmax_kernel(const float4* __restrict__ y4b, int64_t n,
-                                    float2* __restrict__ out, float2* __restrict__ sout,
-                                    const IterState* __restrict__ st) {
-  griddep_wait();
-  if (!st->active) return;
-  __shared__ float red[2][8];
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * kTile + threadIdx.x;
-  float mn = INFINITY, mx = -INFINITY;
-  if (i < n) mn = mx = y4b[i].w;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  }
-  if ((threadIdx.x & 31) == 0) {
-    red[0][threadIdx.x >> 5] = mn;
-    red[1][threadIdx.x >> 5] = mx;
-    const int64_t sub = static_cast<int64_t>(blockIdx.x) * kSubPerTile + (threadIdx.x >> 5);
-    if ((sub << 5) < n) sout[sub] = make_float2(mn, mx);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < kTile / 32; ++w) {
-      mn = fminf(red[0][0], red[0][w]);
-      mx = fmaxf(red[1][0], red[1][w]);
-      red[0][0] = mn;
-      red[1][0] = mx;
-    }
-    out[blockIdx.x] = make_float2(red[0][0], red[1][0]);
-  }
-}
-
 // The last CTA of a list kernel turns the per-block counts (offset[b+1],
 // and offset2[b+1] when given) into exclusive prefixes (in place), resets
 // the done counter for the next graph replay and adds the total to the
@@ -826,25 +994,22 @@ __device__ void scan_counts(int32_t* offset, int n_blocks, int* wsum) {
   if (threadIdx.x == 0) offset[0] = 0;
 }
 
-__device__ void last_cta_scan(int32_t* offset, int32_t* offset2, int n_blocks, int32_t* done,
-                              unsigned long long* counter, int unit_mult = 1) {
+__device__ bool last_cta_scan(int32_t* offset, int n_blocks, int32_t* done,
+                              unsigned long long* counter) {
   __shared__ int is_last;
   __shared__ int wsum[32];
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) is_last = atomicAdd(done, 1) == static_cast<int>(gridDim.x) - 1;
   __syncthreads();
-  if (!is_last) return;
+  if (!is_last) return false;
   __threadfence();
   scan_counts(offset, n_blocks, wsum);
-  if (offset2) scan_counts(offset2, n_blocks, wsum);
   if (threadIdx.x == 0) {
     *done = 0;
-    if (counter)
-      *counter += (static_cast<unsigned long long>(offset[n_blocks]) +
-                   (offset2 ? static_cast<unsigned long long>(offset2[n_blocks]) : 0ull)) *
-                  static_cast<unsigned long long>(unit_mult);
+    if (counter) *counter += static_cast<unsigned long long>(offset[n_blocks]);
   }
+  return true;
 }
 
 // CTA-wide reductions for the list kernels (kMax: max, else min; sums of
@@ -1025,9 +1190,9 @@ __global__ void __launch_bounds__(kListThreads)
     col_list_kernel(CullInfo cull, const float4* __restrict__ xt4, int64_t m,
                     const float4* __restrict__ y4, int64_t n, int32_t* __restrict__ tiles,
                     int32_t* __restrict__ offset, int n_blocks, int32_t* __restrict__ done,
-                    const IterState* __restrict__ st) {
+                    ColFix fix, IterState* __restrict__ st) {
   griddep_wait();
-  if (!st->active) return;
+  if (!st->active || !st->cull_on) return;
   __shared__ float4 pa[kProbeTiles * kTile / 2], pb[kProbeTiles * kTile / 2];
   __shared__ unsigned long long sh64[kListThreads / 32];
   __shared__ float shf[kListThreads / 32];
@@ -1129,11 +1294,21 @@ __global__ void __launch_bounds__(kListThreads)
     if (np > 0 && cull.probe_paid1)
       cull.probe_paid1[b] = (kept_box - count) * kProbePayShare >= kept_box;
   }
-  last_cta_scan(offset, nullptr, n_blocks, done, cull.counters);
+  if (count == 0) {  // every model point is negligible for these columns (ω > 0)
+    const int64_t col = static_cast<int64_t>(b) * kTile + threadIdx.x;
+    float lo = INFINITY, hi = -INFINITY;
+    if (col < n) {
+      const float bv = col_finalize(fix, col, 0.0, m, st);
+      lo = bv == bv ? bv : INFINITY;
+      hi = bv == bv ? bv : INFINITY;
+    }
+    col_b_ranges<1>(fix, b, n, lo, hi);
+  }
+  last_cta_scan(offset, n_blocks, done, cull.counters);
 }
 
 // Pass-2 list, one CTA per model block b, over units of the scene (32-point
-// sub-tiles; 256-point tiles for the tensor-core pass: ulo/uhi/ubm, n_units).
+// sub-tiles: ulo/uhi/ubm, n_units).
 // Every row m of the block has max_n L_mn ≥ L_lb, the larger of
 //  * the box bound max over scene units j of (min b − s²·maxdist²(b, j))
 //    (over the units of the tiles a first, tile-level bound keeps),
@@ -1141,18 +1316,18 @@ __global__ void __launch_bounds__(kListThreads)
 //    x̃_m‖² over the kProbeTiles scene tiles nearest the block (less a
 //    rounding slack);
 // scene unit j is dropped when its largest possible L (max b − s²·mindist²)
-// < L_lb − margin (culling off: every tile kept).  With offset_cc
-// (tensor-core pass 2), a block whose scaled squared half-diagonal exceeds
-// kCentredMaxR2 is routed to the CUDA-core list (difference form) instead.
+// < L_lb − margin.  Its last CTA also decides whether the lists paid for
+// themselves this iteration (IterState::cull_pays).
 __global__ void __launch_bounds__(kListThreads)
     row_list_kernel(CullInfo cull, const float4* __restrict__ xt4, int64_t m,
                     const float4* __restrict__ y4b, int64_t n, int32_t* __restrict__ tiles,
-                    int32_t* __restrict__ offset, int32_t* __restrict__ offset_cc, int n_blocks,
-                    int32_t* __restrict__ done, const float4* __restrict__ ulo,
-                    const float4* __restrict__ uhi, const float2* __restrict__ ubm, int n_units,
-                    int unit_mult, const IterState* __restrict__ st) {
+                    int32_t* __restrict__ offset, int n_blocks, int32_t* __restrict__ done,
+                    const float4* __restrict__ ulo, const float4* __restrict__ uhi,
+                    const float2* __restrict__ ubm, int n_units, RowFix fix,
+                    IterState* __restrict__ st) {
+  constexpr int unit_mult = 1;
   griddep_wait();
-  if (!st->active) return;
+  if (!st->active || !st->cull_on) return;
   __shared__ float4 pa[kProbeTiles * kTile / 2], pb[kProbeTiles * kTile / 2];
   __shared__ unsigned long long sh64[kListThreads / 32];
   __shared__ float shf[kListThreads / 32];
@@ -1257,112 +1432,23 @@ __global__ void __launch_bounds__(kListThreads)
                    : -1;
       });
   if (threadIdx.x == 0) {
-    bool to_tc = true;
-    if (offset_cc) {
-      const float ex = hi.x - lo.x, ey = hi.y - lo.y, ez = hi.z - lo.z;
-      to_tc = 0.25f * s2 * (ex * ex + ey * ey + ez * ez) <= kCentredMaxR2;
-      offset_cc[b + 1] = to_tc ? 0 : count;
-    }
-    offset[b + 1] = to_tc ? count : 0;
+    offset[b + 1] = count;
     if (np > 0 && cull.probe_paid2)
       cull.probe_paid2[b] = (kept_box - count) * kProbePayShare >= kept_box;
   }
-  last_cta_scan(offset, offset_cc, n_blocks, done,
-                cull.enabled && cull.counters ? cull.counters + 1 : nullptr, unit_mult);
-}
-
-// ---------------------------------------------------------------------------
-// Row finalisation shared by the combine and the fallback.
-__device__ __forceinline__ void finalize_row(int64_t row, int64_t m, double log2p1, double s0,
-                                             double sy0, double sy1, double sy2, double sv,
-                                             const double* __restrict__ xt64, double s,
-                                             const RowOut& out, const YStats& ys,
-                                             IterState* st) {
-  const double x0 = xt64[row], x1 = xt64[m + row], x2 = xt64[2 * m + row];
-  double p0, p1, p2, var;
-  int deg = 0;
-  if (log2p1 < kLog2DegenerateRow) {  // uniform row, correspondence.hpp:89-91
-    deg = 1;
-    p0 = ys.mean[0];
-    p1 = ys.mean[1];
-    p2 = ys.mean[2];
-    var = ys.sq_mean - 2.0 * (x0 * p0 + x1 * p1 + x2 * p2) + (x0 * x0 + x1 * x1 + x2 * x2);
-    atomicAdd(reinterpret_cast<unsigned long long*>(&st->degenerate_rows), 1ull);
-  } else {
-    const double inv = 1.0 / (s0 * s);
-    p0 = sy0 * inv;
-    p1 = sy1 * inv;
-    p2 = sy2 * inv;
-    var = sv / (s0 * s * s);
+  if (count == 0) {  // (cannot happen: the unit setting the floor is kept) zero sums
+    const int64_t row = static_cast<int64_t>(b) * kTile + threadIdx.x;
+    const double zero[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (row < m) row_finalize(fix, row, m, n, zero, st);
   }
-  out.ptilde_y[row] = p0;
-  out.ptilde_y[m + row] = p1;
-  out.ptilde_y[2 * m + row] = p2;
-  out.var[row] = var;
-  out.log2p1[row] = log2p1;
-  out.degenerate[row] = deg;
-  if (out.resid4) {
-    // R = P̃Y − X (registration.hpp:136), fp32 for the Q product
-    const double* X = out.x0;
-    out.resid4[row] = make_float4(static_cast<float>(p0 - X[row]),
-                                  static_cast<float>(p1 - X[m + row]),
-                                  static_cast<float>(p2 - X[2 * m + row]), 0.f);
+  if (last_cta_scan(offset, n_blocks, done, cull.counters ? cull.counters + 1 : nullptr) &&
+      threadIdx.x == 0) {
+    // next iteration builds lists again only if these dropped enough units
+    const double kept1 = static_cast<double>(cull.wl1_offset[cull.n_ytiles]);
+    const double kept2 = static_cast<double>(offset[n_blocks]);
+    st->cull_pays = kept1 < kCullKeepFrac * static_cast<double>(cull.wl1_units) ||
+                    kept2 < kCullKeepFrac * static_cast<double>(cull.wl2_units);
   }
-}
-
-// One producer of pass-2 segments: its work list, grid and slots.
-struct SegSrc {
-  WorkList wl;
-  int G = 0;
-  const double* seg = nullptr;  // nullptr: absent
-};
-
-__device__ __forceinline__ void sum_row(const SegSrc& a, const SegSrc& b, int64_t row, int lane,
-                                        bool live, double (&s)[5]) {
-  const int blk = static_cast<int>(row / kTile), li = static_cast<int>(row % kTile);
-  sum_segments<5>(a.wl, a.G, a.seg, blk, li, lane, live, s);
-  if (b.seg) {  // each block's units are in exactly one of the two lists
-    double t[5];
-    sum_segments<5>(b.wl, b.G, b.seg, blk, li, lane, live, t);
-#pragma unroll
-    for (int k = 0; k < 5; ++k) s[k] += t[k];
-  }
-}
-
-__global__ void estep_row_combine_kernel(SegSrc sa, SegSrc sb, int64_t m, int64_t n,
-                                         const double* __restrict__ xt64, RowOut out, YStats ys,
-                                         int32_t* __restrict__ flag_list,
-                                         int32_t* __restrict__ flag_count, IterState* st) {
-  griddep_wait();
-  if (!st->active) return;
-  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t row = gid / kCombineLanes;
-  const int lane = static_cast<int>(gid % kCombineLanes);
-  double a[5];
-  sum_row(sa, sb, row, lane, row < m, a);
-  if (row >= m || lane != 0) return;
-  if (!(a[0] >= static_cast<double>(n) * 0x1p-76)) {
-    const int slot = atomicAdd(flag_count, 1);
-    flag_list[slot] = static_cast<int32_t>(row);
-    return;
-  }
-  finalize_row(row, m, log2(a[0]), a[0], a[1], a[2], a[3], a[4], xt64, derived_scale(st), out, ys,
-               st);
-}
-
-// distributed: AoS row sums [m_pad][5] of the local scene shard
-__global__ void row_seg_sum_kernel(SegSrc sa, SegSrc sb, int64_t m, int64_t m_pad,
-                                   double* __restrict__ out, const IterState* __restrict__ st) {
-  griddep_wait();
-  if (!st->active) return;
-  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t row = gid / kCombineLanes;
-  const int lane = static_cast<int>(gid % kCombineLanes);
-  double a[5];
-  sum_row(sa, sb, row, lane, row < m, a);
-  if (row < m_pad && lane == 0)
-#pragma unroll
-    for (int k = 0; k < 5; ++k) out[row * 5 + k] = a[k];
 }
 
 // Exact row accumulation for flagged rows (tiny mass): warp per row,
@@ -1371,11 +1457,10 @@ __global__ void estep_row_fallback_kernel(const float4* __restrict__ xt4, int64_
                                           const float4* __restrict__ y4b, int64_t n,
                                           const double* __restrict__ xt64, RowOut out, YStats ys,
                                           const int32_t* __restrict__ flag_list,
-                                          const int32_t* __restrict__ flag_count,
                                           IterState* st) {
   griddep_wait();
   if (!st->active) return;
-  const int count = *flag_count;
+  const int count = st->flag_count[1];
   const int lane = threadIdx.x & 31;
   const int warps = (blockDim.x >> 5) * gridDim.x;
   const float s = st->sx;
@@ -1442,7 +1527,7 @@ EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
   p.row_blocks = static_cast<int>(ceil_div(m, kTile));
   // One wave of CTAs, but at least kMinPtsPerCta point-units of the dense
   // pass per CTA: on small passes (C0: 8 blocks × 2000 points) a full wave
-  // leaves each CTA a few points and each block's combine a long chain of
+  // leaves each CTA a few points and each block's fix-up a long chain of
   // segment slots to sum.
   int64_t min_pts = kMinPtsPerCta;
   if (const char* e = std::getenv("FCPD_ESTEP_MIN_PTS")) min_pts = std::max<int64_t>(1, std::atoll(e));
@@ -1461,161 +1546,137 @@ EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
     return f;
   };
   p.flush2 = flush_env("FCPD_FLUSH2", kFlush2);
-  if (const char* e = std::getenv("FCPD_ESTEP_TC")) p.tc = std::atoi(e) != 0;
-  if (!p.centred) p.tc = 0;  // the tensor-core pass is the centred form
-  if (p.tc) {
-    estep_row_tc_prepare();
-    p.tc_grid = sm_count;  // one CTA per SM (all 512 TMEM columns)
-  }
   return p;
 }
 
 namespace {
-WorkList pass1_list(const EStepPlan& p, const EStepBuffers& b, int64_t m) {
+// A culling session's lists are used only in iterations that build them
+// (IterState::cull_on); the implicit fallback counts its units.
+WorkList pass1_list(const EStepPlan& p, const EStepBuffers& b, int64_t m, const IterState* st) {
   WorkList wl;
   wl.implicit = b.cull.enabled ? 0 : 1;
   wl.n_blocks = p.col_blocks;
   wl.n_other = static_cast<int>(ceil_div(m, kSubPts));
   wl.tiles = b.wl1.tiles;
   wl.offset = b.wl1.offset;
-  return wl;
-}
-// (the tensor-core pass 2 keeps 256-point units: its pieces are whole tiles)
-WorkList pass2_list(const EStepPlan& p, const EStepBuffers& b, int64_t n, bool cc = false) {
-  WorkList wl;
-  wl.implicit = b.cull.lists ? 0 : 1;
-  wl.n_blocks = p.row_blocks;
-  wl.ushift = p.tc ? 8 : 5;
-  static_assert(kTilePts == 1 << 8 && kSubPts == 1 << 5, "unit shifts");
-  wl.n_other = static_cast<int>(ceil_div(n, int64_t(1) << wl.ushift));
-  wl.tiles = b.wl2.tiles;
-  wl.offset = cc ? b.wl2.offset_cc : b.wl2.offset;
-  return wl;
-}
-// pass-2 producers: (tensor cores, CUDA cores) or (CUDA cores, none)
-void pass2_sources(const EStepPlan& p, const EStepBuffers& b, int64_t n, SegSrc& a, SegSrc& c) {
-  if (p.tc) {
-    a = SegSrc{pass2_list(p, b, n), p.tc_grid, b.row_seg};
-    c = SegSrc{pass2_list(p, b, n, true), p.row_grid, b.row_seg_cc};
-  } else {
-    a = SegSrc{pass2_list(p, b, n), p.row_grid, b.row_seg};
-    c = SegSrc{};
+  if (b.cull.enabled) {
+    wl.dyn_on = &st->cull_on;
+    wl.implicit_counter = b.cull.counters;
   }
+  return wl;
+}
+WorkList pass2_list(const EStepPlan& p, const EStepBuffers& b, int64_t n, const IterState* st) {
+  WorkList wl;
+  wl.implicit = b.cull.enabled ? 0 : 1;
+  wl.n_blocks = p.row_blocks;
+  wl.ushift = 5;
+  static_assert(kSubPts == 1 << 5, "unit shift");
+  wl.n_other = static_cast<int>(ceil_div(n, kSubPts));
+  wl.tiles = b.wl2.tiles;
+  wl.offset = b.wl2.offset;
+  if (b.cull.enabled) {
+    wl.dyn_on = &st->cull_on;
+    wl.implicit_counter = b.cull.counters ? b.cull.counters + 1 : nullptr;
+  }
+  return wl;
+}
+ColFix col_fix(const EStepBuffers& b) {
+  return ColFix{b.col_done, b.y4b, b.b2, b.pt1, b.col_flags,
+                b.cull.enabled ? b.cullw.bminmax : nullptr, b.cullw.sbminmax};
+}
+RowFix row_fix(const EStepBuffers& b) {
+  return RowFix{b.row_done, b.xt64, b.out, b.ystats, b.row_flags, b.row_aos};
 }
 }  // namespace
 
-void launch_estep_prologue(IterState* st, int64_t m, int64_t n_global, int d, double omega,
-                           int32_t* flags_count, uint64_t* stamps, cudaStream_t stream) {
-  launch_pdl(estep_prologue_kernel, dim3(1), dim3(1), 0, stream, st, m, n_global, d, omega,
-             flags_count, stamps);
+int estep_kernels(bool culling, bool dist) {
+  // pass 1 + column fallback + pass 2 (+ row fallback on one GPU); culling
+  // adds the x̃ tile boxes and the two list kernels (launched every
+  // iteration; they return at once when the iteration builds no lists)
+  return 3 + (dist ? 0 : 1) + (culling ? 3 : 0);
+}
+
+void launch_init_state(IterState* st, double sigma2, double omega, int64_t m, int64_t n_global,
+                       int d, cudaStream_t stream) {
+  init_state_kernel<<<1, 1, 0, stream>>>(st, sigma2, omega, m, n_global, d);
   FCPD_LAUNCH_CHECK();
 }
 
 void launch_tile_bbox(const float4* pts, int64_t count, float4* lo, float4* hi, float4* slo,
                       float4* shi, const IterState* st, cudaStream_t stream) {
   launch_pdl(tile_bbox_kernel, dim3(ceil_div(count, kTile)), dim3(kTile), 0, stream, pts, count, lo,
-             hi, slo, shi, st);
+             hi, slo, shi, st, static_cast<uint64_t*>(nullptr));
   FCPD_LAUNCH_CHECK();
 }
 
-// Pass 1 (column normalisers) + the culling geometry around it: model-tile
-// boxes of this iteration's x̃ and the pass-1 work list before, scene-tile
-// b ranges after (the pass-2 list reads them).
+// Pass 1 (column normalisers): with culling, the model-tile boxes of this
+// iteration's x̃ and the pass-1 work list before it; the column fallback
+// after.  Scene-tile b ranges are written by the pass-1 block fix-up.
 void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
                         IterState* st, cudaStream_t stream) {
   const CullInfo& cu = b.cull;
-  const WorkList wl = pass1_list(p, b, m);
+  const WorkList wl = pass1_list(p, b, m, st);
+  const ColFix fix = col_fix(b);
+  unsigned long long* forms = cu.counters ? cu.counters + 2 : nullptr;
   if (cu.enabled) {
-    launch_tile_bbox(b.xt4, m, b.cullw.xlo, b.cullw.xhi, b.cullw.sxlo, b.cullw.sxhi, st, stream);
+    // the first kernel of the iteration stamps its start
+    launch_pdl(tile_bbox_kernel, dim3(ceil_div(m, kTile)), dim3(kTile), 0, stream, b.xt4, m,
+               b.cullw.xlo, b.cullw.xhi, b.cullw.sxlo, b.cullw.sxhi,
+               static_cast<const IterState*>(st), b.stamps);
+    FCPD_LAUNCH_CHECK();
     launch_pdl(col_list_kernel, dim3(p.col_blocks), dim3(kListThreads), 0, stream, cu, b.xt4, m,
-               b.y4b, n, b.wl1.tiles, b.wl1.offset, p.col_blocks, b.wl1.done, st);
+               b.y4b, n, b.wl1.tiles, b.wl1.offset, p.col_blocks, b.wl1.done, fix, st);
     FCPD_LAUNCH_CHECK();
   }
+  uint64_t* stamps = cu.enabled ? nullptr : b.stamps;
   if (p.col_pairs == 2)
     launch_pdl(estep_col_kernel<2>, dim3(p.col_grid), dim3(64), 0, stream, b.xt4, m, b.y4b, n, st,
-               wl, b.col_seg, p.centred_max_r2);
+               wl, b.col_seg, p.centred_max_r2, fix, forms, stamps);
   else
     launch_pdl(estep_col_kernel<1>, dim3(p.col_grid), dim3(128), 0, stream, b.xt4, m, b.y4b, n, st,
-               wl, b.col_seg, p.centred_max_r2);
-  FCPD_LAUNCH_CHECK();
-  launch_pdl(estep_col_combine_kernel, dim3(ceil_div(n * kCombineLanes, 256)), dim3(256), 0, stream,
-             b.col_seg, wl, p.col_grid, m, n, b.y4b, b.b2, b.pt1, b.col_flags, b.flags_count, st);
+               wl, b.col_seg, p.centred_max_r2, fix, forms, stamps);
   FCPD_LAUNCH_CHECK();
   launch_pdl(estep_col_fallback_kernel, dim3(148), dim3(256), 0, stream, b.xt4, m, b.y4b, b.b2,
-             b.pt1, b.col_flags, b.flags_count, st);
-  FCPD_LAUNCH_CHECK();
-  if (cu.enabled) {
-    launch_pdl(tile_bminmax_kernel, dim3(ceil_div(n, kTile)), dim3(kTile), 0, stream, b.y4b, n,
-               b.cullw.bminmax, b.cullw.sbminmax, st);
-    FCPD_LAUNCH_CHECK();
-  }
-}
-
-void launch_row_cc(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
-                   IterState* st, const WorkList& wl, double* seg, cudaStream_t stream) {
-  if (p.row_pairs == 2)
-    launch_pdl(estep_row_kernel<2>, dim3(p.row_grid), dim3(64), 0, stream, b.xt4, m, b.y4b, n, st,
-               wl, seg, p.centred_max_r2, p.flush2);
-  else
-    launch_pdl(estep_row_kernel<1>, dim3(p.row_grid), dim3(128), 0, stream, b.xt4, m, b.y4b, n, st,
-               wl, seg, p.centred_max_r2, p.flush2);
-}
-
-void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int64_t m,
-                                 int64_t n, IterState* st, cudaStream_t stream) {
-  const CullInfo& cu = b.cull;
-  if (cu.lists) {
-    if (!cu.enabled)  // x̃ tile boxes for the routing (pass 1 made them when culling)
-      launch_tile_bbox(b.xt4, m, b.cullw.xlo, b.cullw.xhi, b.cullw.sxlo, b.cullw.sxhi, st, stream);
-    // units of the scene: sub-tiles, or whole tiles for the tensor-core pass
-    const WorkList wl = pass2_list(p, b, n);
-    launch_pdl(row_list_kernel, dim3(p.row_blocks), dim3(kListThreads), 0, stream, cu, b.xt4, m,
-               b.y4b, n, b.wl2.tiles, b.wl2.offset, p.tc ? b.wl2.offset_cc : nullptr, p.row_blocks,
-               b.wl2.done, p.tc ? cu.ylo : cu.sylo, p.tc ? cu.yhi : cu.syhi,
-               p.tc ? cu.bminmax : cu.sbminmax, wl.n_other, p.tc ? kSubPerTile : 1, st);
-    FCPD_LAUNCH_CHECK();
-  }
-  SegSrc a, c;
-  pass2_sources(p, b, n, a, c);
-  if (p.tc) {
-    launch_estep_row_tc(b.xt4, m, b.y4b, n, st, a.wl, b.row_seg, p.tc_grid, stream);
-    launch_row_cc(p, b, m, n, st, c.wl, b.row_seg_cc, stream);
-  } else {
-    launch_row_cc(p, b, m, n, st, a.wl, b.row_seg, stream);
-  }
+             b.pt1, static_cast<const int32_t*>(b.col_flags), static_cast<const IterState*>(st));
   FCPD_LAUNCH_CHECK();
 }
 
+// Pass 2: the work list (culling), the row accumulation with its block
+// fix-up (finalised rows, or AoS sums when distributed) and, on one GPU, the
+// exact fallback of the rows the fix-up queued.
 void launch_estep_pass2(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
                         IterState* st, cudaStream_t stream) {
-  launch_estep_pass2_partials(p, b, m, n, st, stream);
-  SegSrc a, c;
-  pass2_sources(p, b, n, a, c);
-  int32_t* list = b.row_flags;
-  int32_t* count = b.flags_count + 1;
-  launch_pdl(estep_row_combine_kernel, dim3(ceil_div(m * kCombineLanes, 256)), dim3(256), 0, stream,
-             a, c, m, n, b.xt64, b.out, b.ystats, list, count, st);
+  const CullInfo& cu = b.cull;
+  const WorkList wl = pass2_list(p, b, n, st);
+  const RowFix fix = row_fix(b);
+  unsigned long long* forms = cu.counters ? cu.counters + 4 : nullptr;
+  if (cu.enabled) {
+    launch_pdl(row_list_kernel, dim3(p.row_blocks), dim3(kListThreads), 0, stream, cu, b.xt4, m,
+               static_cast<const float4*>(b.y4b), n, b.wl2.tiles, b.wl2.offset, p.row_blocks,
+               b.wl2.done, static_cast<const float4*>(cu.sylo),
+               static_cast<const float4*>(cu.syhi), static_cast<const float2*>(cu.sbminmax),
+               wl.n_other, fix, st);
+    FCPD_LAUNCH_CHECK();
+  }
+  if (p.row_pairs == 2)
+    launch_pdl(estep_row_kernel<2>, dim3(p.row_grid), dim3(64), 0, stream, b.xt4, m,
+               static_cast<const float4*>(b.y4b), n, st, wl, b.row_seg, p.centred_max_r2,
+               p.flush2, fix, forms);
+  else
+    launch_pdl(estep_row_kernel<1>, dim3(p.row_grid), dim3(128), 0, stream, b.xt4, m,
+               static_cast<const float4*>(b.y4b), n, st, wl, b.row_seg, p.centred_max_r2,
+               p.flush2, fix, forms);
   FCPD_LAUNCH_CHECK();
-  launch_pdl(estep_row_fallback_kernel, dim3(148), dim3(256), 0, stream, b.xt4, m, b.y4b, n, b.xt64,
-             b.out, b.ystats, list, count, st);
-  FCPD_LAUNCH_CHECK();
+  if (!b.row_aos) {
+    launch_pdl(estep_row_fallback_kernel, dim3(148), dim3(256), 0, stream, b.xt4, m,
+               static_cast<const float4*>(b.y4b), n, b.xt64, b.out, b.ystats,
+               static_cast<const int32_t*>(b.row_flags), st);
+    FCPD_LAUNCH_CHECK();
+  }
 }
 
-void launch_row_seg_sum(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
-                        int64_t m_pad, double* out, const IterState* st, cudaStream_t stream) {
-  SegSrc a, c;
-  pass2_sources(p, b, n, a, c);
-  launch_pdl(row_seg_sum_kernel, dim3(ceil_div(m_pad * kCombineLanes, 256)), dim3(256), 0, stream,
-             a, c, m, m_pad, out, st);
-  FCPD_LAUNCH_CHECK();
-}
-
-void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n, int d,
-                  double omega, IterState* st, uint64_t* stamps, cudaStream_t stream,
-                  cudaEvent_t mid) {
-  launch_pdl(estep_prologue_kernel, dim3(1), dim3(1), 0, stream, st, m, n, d, omega, b.flags_count,
-             stamps);
-  FCPD_LAUNCH_CHECK();
+void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
+                  IterState* st, cudaStream_t stream, cudaEvent_t mid) {
   launch_estep_pass1(p, b, m, n, st, stream);
   if (mid) FCPD_CUDA(cudaEventRecord(mid, stream));
   launch_estep_pass2(p, b, m, n, st, stream);

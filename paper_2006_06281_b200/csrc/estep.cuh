@@ -45,6 +45,11 @@ struct WorkList {
   int ushift = 5;                 // points per unit = 1 << ushift (kSubPts)
   const int32_t* tiles = nullptr;   // [n_blocks][n_other]
   const int32_t* offset = nullptr;  // [n_blocks + 1]
+  // culling sessions: the list is used only when *dyn_on (IterState::cull_on,
+  // decided per iteration); otherwise the pass is implicit and adds its
+  // n_blocks·n_other units to *implicit_counter (tiles_evaluated)
+  const int32_t* dyn_on = nullptr;
+  unsigned long long* implicit_counter = nullptr;
   __host__ __device__ int64_t off(int b) const {
     return implicit ? static_cast<int64_t>(b) * n_other : static_cast<int64_t>(offset[b]);
   }
@@ -58,36 +63,27 @@ struct WorkListBuffers {  // writable views (engine-owned)
   int32_t* tiles = nullptr;
   int32_t* offset = nullptr;
   int32_t* done = nullptr;     // last-CTA counter of the list kernel (self-resetting)
-  int32_t* offset_cc = nullptr;  // pass 2 with tensor cores: the CUDA-core share
 };
 
 // Persistent stream-K schedule of both passes (one CTA wave per pass).
-// Pass-2 blocks whose squared box half-diagonal in the scaled frame exceeds
-// this run on the CUDA cores in the difference form (the centred form's
-// rounding ≈ 4ε·R² in log2 units; 16 → ≤ 4e-6).
+// Blocks whose squared box half-diagonal in the scaled frame exceeds this run
+// in the difference form (the centred form's rounding ≈ 4ε·R² in log2
+// units; 16 → ≤ 4e-6).
 constexpr float kCentredMaxR2 = 16.f;
 
 struct EStepPlan {
   int centred = 1;  // tile-centred pair form where exact enough; FCPD_ESTEP_FORM=diff → off
   float centred_max_r2 = kCentredMaxR2;  // per-segment guard (< 0: difference form only)
-  int tc = 0;       // pass 2 on tcgen05 (estep_tc.cu) for blocks within kCentredMaxR2
-  int row_pairs = 2;  // CUDA-core pass 2: packed row pairs per thread (FCPD_ROW_PAIRS=1 → 1)
+  int row_pairs = 2;  // pass 2: packed row pairs per thread (FCPD_ROW_PAIRS=1 → 1)
   int col_pairs = 2;  // pass 1: packed column pairs per thread (FCPD_COL_PAIRS=1 → 1)
   int flush2 = 64;  // fp32 run length of the pass-2 sums (FCPD_FLUSH2, power of two)
   int col_blocks = 0, row_blocks = 0;  // scene tiles (pass-1 blocks), model tiles (pass 2)
-  int col_grid = 0, row_grid = 0;      // persistent CTAs per pass (CUDA-core kernels)
-  int tc_grid = 0;                     // persistent CTAs of the tensor-core pass 2
+  int col_grid = 0, row_grid = 0;      // persistent CTAs per pass
   size_t col_seg_doubles() const { return static_cast<size_t>(col_grid + col_blocks) * kTilePts; }
   size_t row_seg_doubles() const {
-    return static_cast<size_t>(std::max(row_grid, tc_grid) + row_blocks) * 5 * kTilePts;
+    return static_cast<size_t>(row_grid + row_blocks) * 5 * kTilePts;
   }
 };
-
-// estep_tc.cu
-void estep_row_tc_prepare();
-void launch_estep_row_tc(const float4* xt4, int64_t m, const float4* y4b, int64_t n,
-                         const IterState* st, const WorkList& wl, double* seg, int grid,
-                         cudaStream_t stream);
 
 // Tile culling.  Points are k-d sorted by the engine so
 // 256-point tiles and their 32-point sub-tiles are compact boxes; a (block,
@@ -115,8 +111,13 @@ struct CullInfo {
   const float2* sbminmax = nullptr;  // per scene sub-tile: (min b, max b)
   float margin1 = 0.f, margin2 = 0.f;
   // [0] pass-1, [1] pass-2 work-list entries evaluated, in (256-point block,
-  // 32-point sub-tile) pairs (a 256-point unit counts as 8)
+  // 32-point sub-tile) pairs; [2..5] pairs evaluated by (pass 1 centred,
+  // pass 1 difference, pass 2 centred, pass 2 difference) form — the
+  // instruction mix the roofline is computed from
   unsigned long long* counters = nullptr;
+  // pass-1 list (read by the pass-2 list kernel for the "culling pays" test)
+  const int32_t* wl1_offset = nullptr;
+  int64_t wl1_units = 0, wl2_units = 0;  // units of the full (implicit) lists
   // per own block: did the last probe drop ≥ 1/4 of the box-kept tiles?
   // (blocks whose probe does not pay reconsider it every 4th iteration)
   int32_t* probe_paid1 = nullptr;  // [n_ytiles]
@@ -138,15 +139,17 @@ struct EStepBuffers {
   double* pt1;         // optional Σ_m P_mn, N
   double* col_seg;     // pass-1 segment partials [col_grid + col_blocks][256]
   double* row_seg;     // pass-2 segment partials [grid + row_blocks][5][256]
-  double* row_seg_cc;  // with tensor cores: the CUDA-core kernel's segments
-  int32_t* col_flags;  // N
+  int32_t* col_done;   // [col_blocks] segment arrival counters (self-resetting)
+  int32_t* row_done;   // [row_blocks]
+  int32_t* col_flags;  // N: columns queued for the exact fallback
   int32_t* row_flags;  // M
-  int32_t* flags_count;  // 2
   RowOut out;
   YStats ystats;
+  double* row_aos;     // distributed: row sums AoS [m_pad][5] instead of `out`
   CullInfo cull;      // cull.enabled = 0 → implicit work lists (every pair evaluated)
   CullBuffers cullw;  // geometry buffers written each iteration
   WorkListBuffers wl1, wl2;  // pass-1 / pass-2 work lists (used when culling)
+  uint64_t* stamps;   // device phase timestamps [iteration][4] (optional)
 };
 
 // Tile and sub-tile boxes (scene: once per session, Y does not move).
@@ -154,24 +157,21 @@ void launch_tile_bbox(const float4* pts, int64_t count, float4* lo, float4* hi, 
                       float4* shi, const IterState* st, cudaStream_t stream);
 
 EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count);
-// Pieces of launch_estep for the distributed path (n = local scene count;
-// the prologue's outlier constant uses the global N).
-void launch_estep_prologue(IterState* st, int64_t m, int64_t n_global, int d, double omega,
-                           int32_t* flags_count, uint64_t* stamps, cudaStream_t stream);
+// Iteration-0 state: E-step scalars of sigma2, ω, M, global N, D (device
+// math, the same code the iterations use for the next σ²).
+void launch_init_state(IterState* st, double sigma2, double omega, int64_t m, int64_t n_global,
+                       int d, cudaStream_t stream);
+// Pass 1 (column normalisers; each scene block finalised by the CTA that
+// completes it) + the column fallback.  n = local scene count.
 void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
                         IterState* st, cudaStream_t stream);
-// pass-2 work list + segment partials (no combine)
-void launch_estep_pass2_partials(const EStepPlan& p, const EStepBuffers& b, int64_t m,
-                                 int64_t n, IterState* st, cudaStream_t stream);
-// pass 2 complete: partials, combine, exact fallback of flagged rows
+// Pass 2: single GPU → finalised rows (b.out) + the exact row fallback;
+// distributed (b.row_aos) → per-row sums of the local columns, AoS [m_pad][5].
 void launch_estep_pass2(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
                         IterState* st, cudaStream_t stream);
-// distributed: per-row sums of the pass-2 segments as AoS [m_pad][5]
-// (rows ≥ m are zero) for the reduce-scatter
-void launch_row_seg_sum(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
-                        int64_t m_pad, double* out, const IterState* st, cudaStream_t stream);
-void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n, int d,
-                  double omega, IterState* st, uint64_t* stamps, cudaStream_t stream,
-                  cudaEvent_t mid = nullptr);
+void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
+                  IterState* st, cudaStream_t stream, cudaEvent_t mid = nullptr);
+// kernels one E-step launches (culling session or not; single GPU or not)
+int estep_kernels(bool culling, bool dist);
 
 }  // namespace fcpd

@@ -517,6 +517,7 @@ __global__ void sigma_final_kernel(const double* __restrict__ sig_part, int bloc
   st->sigma2 = next;
   st->iters_run = it + 1;
   st->iter = it + 1;
+  estep_scalars_for_next(st, next, it + 1);  // the next E-step's σ², scale, log c
   if (stamps) stamps[4 * it + 3] = globaltimer();
   if (early_stop && delta < 1e-10) st->active = 0;
 }

@@ -128,7 +128,7 @@ struct MstepFusedArgs {
   const float4* resid4;  // R = P̃Y − X
   double* zpart;         // [k][grid][3]
   double* coef;          // 3 × k SoA
-  float4* g4;            // k
+  float4* g4;            // kpad (the padding columns of the last quad get g = 0)
   const double* x0;
   double* xt64;
   double* xt_prev;

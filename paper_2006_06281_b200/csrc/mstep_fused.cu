@@ -125,6 +125,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
         const int qq = ng > 1 ? tid : q;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
+          // keff is a multiple of 4 and may exceed K (padding columns of Q,
+          // all zero): only real eigenpairs have partial slots
+          if (4 * qq + i >= a.k) break;
           double* p = a.zpart + ((static_cast<int64_t>(4 * qq + i) * G + c) * 3);
           p[0] = acc[3 * i];
           p[1] = acc[3 * i + 1];
@@ -140,6 +143,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
     const double sigma2 = st->sigma2;  // this iteration's E-step σ² (registration.hpp:137)
     const int64_t gw = static_cast<int64_t>(c) * kFusedWarps + warp, nw = int64_t(G) * kFusedWarps;
     for (int64_t k = gw; k < keff; k += nw) {
+      if (k >= a.k) {  // padding column of the last quad: g = 0 (Q's column is 0)
+        if (lane == 0) a.g4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        continue;
+      }
       double z0 = 0.0, z1 = 0.0, z2 = 0.0;
       for (int cc = lane; cc < G; cc += 32) {
         const double* p = a.zpart + (k * G + cc) * 3;  // written by other CTAs
@@ -317,6 +324,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
   st->sigma2 = next;
   st->iters_run = it + 1;
   st->iter = it + 1;
+  estep_scalars_for_next(st, next, it + 1);  // the next E-step's σ², scale, log c
   if (a.stamps) a.stamps[4 * it + 3] = globaltimer();
   if (a.early_stop && delta < 1e-10) st->active = 0;
 }

@@ -1,0 +1,25 @@
+#!/bin/bash
+# Round-2 pass B: the refactored E-step (block fix-ups, no prologue /
+# combine / bminmax kernels, per-iteration culling decision) — GPU suite,
+# smoke, default bench line, launch lists, one ncu --set full of the pass
+# kernels (C1), and the legacy-HMMA rate probe.
+O=gpurun_out/r2b
+mkdir -p $O
+rm -f $O/parity.jsonl
+FCPD_PARITY_LOG=$O/parity.jsonl timeout 2400 python -m pytest tests -q -m gpu -x -rA --durations=30 > $O/pytest_gpu.txt 2>&1
+echo "pytest exit $?" >> $O/pytest_gpu.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1
+timeout 1200 python bench.py --steps 20 --warmup 5 > $O/bench_default.json 2> $O/bench_default.err
+for w in c0 c2 c3; do
+  timeout 900 python bench.py --workload $w --secondary none --warmup 5 --no-cpu --e2e-calls 1 > $O/bench_$w.json 2> $O/bench_$w.err
+done
+timeout 300 python bench.py --workload c4 --secondary none --warmup 5 --no-cpu --e2e-calls 1 > $O/bench_c4_100.json 2> $O/bench_c4_100.err
+CMD1="python bench.py --workload c1 --secondary none --steps 5 --warmup 3 --no-cpu --e2e-calls 0"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file $O/launches_c1.csv $CMD1 > $O/ncu_launch_c1.log 2>&1
+CMD4="python bench.py --workload c4 --secondary none --steps 3 --warmup 3 --no-cpu --e2e-calls 0"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file $O/launches_c4.csv $CMD4 > $O/ncu_launch_c4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"estep_(row|col)_kernel|mstep_fused|colsum_bulk" -s 20 -c 4 -o $O/c1_full $CMD1 > $O/ncu_full_c1.log 2>&1
+./tools/hmma_rate > $O/hmma_rate.txt 2>&1
+tail -3 $O/pytest_gpu.txt; grep -E "^FAILED|Error" $O/pytest_gpu.txt | head -20; tail -1 $O/smoke.txt
+for f in $O/bench_*.json; do echo "== $f"; cut -c1-300 $f; done
+tail -2 $O/ncu_full_c1.log
