@@ -80,6 +80,7 @@ inline void throw_code(int code, const std::string& msg) {
 // -------------------------------------------------------------- matrix
 #ifdef FASTCPD_USE_EIGEN
 using Matrix = Eigen::MatrixXd;
+using Vector = Eigen::VectorXd;
 using Index = Eigen::Index;
 #else
 using Index = std::ptrdiff_t;
@@ -106,6 +107,27 @@ class Matrix {
 
  private:
   Index r_ = 0, c_ = 0;
+  std::vector<double> v_;
+};
+
+// fp64 vector: the subset of Eigen::VectorXd the L2 types use.
+class Vector {
+ public:
+  Vector() = default;
+  explicit Vector(Index n) : v_(static_cast<size_t>(n), 0.0) {}
+  Index size() const { return static_cast<Index>(v_.size()); }
+  double& operator()(Index i) { return v_[static_cast<size_t>(i)]; }
+  double operator()(Index i) const { return v_[static_cast<size_t>(i)]; }
+  double& operator[](Index i) { return v_[static_cast<size_t>(i)]; }
+  double operator[](Index i) const { return v_[static_cast<size_t>(i)]; }
+  double* data() { return v_.data(); }
+  const double* data() const { return v_.data(); }
+  void resize(Index n) { v_.assign(static_cast<size_t>(n), 0.0); }
+  void setZero() { std::fill(v_.begin(), v_.end(), 0.0); }
+  double minCoeff() const { return *std::min_element(v_.begin(), v_.end()); }
+  double maxCoeff() const { return *std::max_element(v_.begin(), v_.end()); }
+
+ private:
   std::vector<double> v_;
 };
 #endif
@@ -168,6 +190,19 @@ struct Correspondence {
   bool row_constrained = false;
   std::vector<Index> degenerate_rows;
   bool sigma2_clamped = false;
+
+  Vector row_sums() const {
+    Vector s(p.rows());
+    for (Index j = 0; j < p.cols(); ++j)
+      for (Index i = 0; i < p.rows(); ++i) s(i) += p(i, j);
+    return s;
+  }
+  Vector col_sums() const {
+    Vector s(p.cols());
+    for (Index j = 0; j < p.cols(); ++j)
+      for (Index i = 0; i < p.rows(); ++i) s(j) += p(i, j);
+    return s;
+  }
 };
 
 // ------------------------------------------------ registration.hpp:21-56
@@ -290,6 +325,274 @@ inline Context& default_context(int device = 0) {
 inline RegistrationResult register_pointsets(const PointSet& x, const PointSet& y,
                                              const RegistrationConfig& cfg) {
   return default_context(cfg.device).register_pointsets(x, y, cfg);
+}
+
+// ============================================================ L2 functions
+// The reference's numerics entry points (correspondence.hpp, kernel.hpp,
+// solvers.hpp, pointset.hpp) with the same names, types, checks and
+// exceptions, running in fp64 on the default context's device through the
+// C ABI (fcpd_capi.h, l2api.cu).  register_pointsets does not call these:
+// its EM loop is the fused device path.
+
+// --------------------------------------------- correspondence.hpp:15-18
+struct GmmParams {
+  double omega = 0.7;   // uniform outlier weight, [0,1)
+  double sigma2 = 1.0;  // shared isotropic variance
+};
+
+namespace detail {
+inline fcpd_ctx* l2ctx() { return default_context().get(); }
+inline void l2check(int rc) {
+  if (rc != FCPD_OK) throw_code(rc, fcpd_last_error(l2ctx()));
+}
+}  // namespace detail
+
+// correspondence.hpp:35-79 — GMM posterior with the per-column max shift
+// (materialised M×N; the dense fp64 device kernel).
+inline Correspondence posterior(const PointSet& x_t, const PointSet& y, const GmmParams& params) {
+  if (params.omega < 0.0 || params.omega >= 1.0)
+    throw ParameterError("posterior: omega must lie in [0, 1)");
+  if (x_t.dim() != y.dim()) throw DimensionError("posterior: dimension mismatch");
+  Correspondence c;
+  c.p.resize(x_t.count(), y.count());
+  int32_t clamped = 0;
+  int64_t nd = 0;
+  detail::l2check(fcpd_posterior_dense(detail::l2ctx(), x_t.pts.data(), x_t.count(), y.pts.data(),
+                                       y.count(), static_cast<int32_t>(x_t.dim()), params.omega,
+                                       params.sigma2, 0, c.p.data(), &clamped, nullptr, &nd));
+  c.sigma2_clamped = clamped != 0;
+  c.row_constrained = false;
+  return c;
+}
+
+// correspondence.hpp:83-98 — row normalisation with the uniform fallback.
+inline Correspondence enforce_row_constraint(const Correspondence& raw) {
+  Correspondence out = raw;
+  out.degenerate_rows.clear();
+  std::vector<int32_t> deg(static_cast<size_t>(raw.p.rows()), 0);
+  detail::l2check(fcpd_enforce_row_constraint(detail::l2ctx(), out.p.data(), out.p.rows(),
+                                              out.p.cols(), deg.data()));
+  for (Index i = 0; i < out.p.rows(); ++i)
+    if (deg[static_cast<size_t>(i)]) out.degenerate_rows.push_back(i);
+  out.row_constrained = true;
+  return out;
+}
+
+// correspondence.hpp:101-105 — Ỹ = P·Y.
+inline PointSet estimated_targets(const Correspondence& p, const PointSet& y) {
+  if (p.p.cols() != y.count()) throw ParameterError("estimated_targets: shape mismatch");
+  PointSet out;
+  out.pts.resize(p.p.rows(), y.dim());
+  detail::l2check(fcpd_estimated_targets(detail::l2ctx(), p.p.data(), p.p.rows(), p.p.cols(),
+                                         y.pts.data(), y.count(), static_cast<int32_t>(y.dim()),
+                                         out.pts.data()));
+  return out;
+}
+
+// ------------------------------------------------------ kernel.hpp:15-29
+struct GramKernel {
+  Matrix phi;
+  double beta = 0.0;
+  Index size() const { return phi.rows(); }
+};
+
+struct SpectralBasis {
+  Matrix u;       // M × K, orthonormal columns
+  Vector lambda;  // K, descending
+  Index points() const { return u.rows(); }
+  Index rank() const { return u.cols(); }
+};
+
+// kernel.hpp:31-47 — Φ_ij = exp(−‖x_i − x_j‖²/2β²), symmetric, unit diagonal.
+inline GramKernel build_gram(const PointSet& x, double beta) {
+  if (beta <= 0.0) throw ParameterError("build_gram: beta must be positive");
+  GramKernel k;
+  k.beta = beta;
+  k.phi.resize(x.count(), x.count());
+  detail::l2check(fcpd_build_gram(detail::l2ctx(), x.pts.data(), x.count(),
+                                  static_cast<int32_t>(x.dim()), beta, k.phi.data()));
+  return k;
+}
+
+// kernel.hpp:49-72 — top `rank` eigenpairs (cuSOLVER syevd, fp64),
+// descending, λ < 1e-12·λmax clamped to 0.
+inline SpectralBasis eigendecompose(const GramKernel& k, Index rank) {
+  const Index m = k.size();
+  if (rank < 1 || rank > m) throw ParameterError("eigendecompose: rank out of [1, M]");
+  SpectralBasis b;
+  b.u.resize(m, rank);
+  b.lambda.resize(rank);
+  detail::l2check(fcpd_eigendecompose(detail::l2ctx(), k.phi.data(), m, rank, b.u.data(),
+                                      b.lambda.data(), nullptr));
+  return b;
+}
+
+// kernel.hpp:76-83 — ‖Φ − U Λ Uᵀ‖_F.
+inline double lowrank_reconstruction_error(const SpectralBasis& b, const GramKernel& k) {
+  if (b.points() != k.size())
+    throw ParameterError("lowrank_reconstruction_error: size mismatch");
+  double e = 0.0;
+  detail::l2check(fcpd_lowrank_reconstruction_error(detail::l2ctx(), k.phi.data(), k.size(),
+                                                    b.u.data(), b.points(), b.lambda.data(),
+                                                    b.rank(), &e));
+  return e;
+}
+
+// kernel.hpp:85-144 — the spectral cache file: "FCPD", u32 version 1, u64 M,
+// u64 K, f64 β, then U row by row and λ, little-endian fp64 (host I/O).
+inline void save_spectral_cache(const std::string& path, const SpectralBasis& b, double beta) {
+  std::FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) throw IoError("cannot open spectral cache for writing: " + path);
+  const uint32_t version = 1;
+  const uint64_t m = static_cast<uint64_t>(b.points()), k = static_cast<uint64_t>(b.rank());
+  bool ok = std::fwrite("FCPD", 1, 4, f) == 4 && std::fwrite(&version, 4, 1, f) == 1 &&
+            std::fwrite(&m, 8, 1, f) == 1 && std::fwrite(&k, 8, 1, f) == 1 &&
+            std::fwrite(&beta, 8, 1, f) == 1;
+  std::vector<double> row(static_cast<size_t>(k));
+  for (uint64_t i = 0; ok && i < m; ++i) {
+    for (uint64_t j = 0; j < k; ++j)
+      row[static_cast<size_t>(j)] = b.u(static_cast<Index>(i), static_cast<Index>(j));
+    ok = std::fwrite(row.data(), 8, static_cast<size_t>(k), f) == static_cast<size_t>(k);
+  }
+  ok = ok && std::fwrite(b.lambda.data(), 8, static_cast<size_t>(k), f) == static_cast<size_t>(k);
+  ok = (std::fclose(f) == 0) && ok;
+  if (!ok) throw IoError("spectral cache write failed: " + path);
+}
+
+inline SpectralBasis load_spectral_cache(const std::string& path, double* beta_out = nullptr) {
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) throw IoError("cannot open spectral cache: " + path);
+  char magic[4] = {0, 0, 0, 0};
+  uint32_t version = 0;
+  uint64_t m = 0, k = 0;
+  double beta = 0.0;
+  const bool head = std::fread(magic, 1, 4, f) == 4 && std::fread(&version, 4, 1, f) == 1 &&
+                    std::fread(&m, 8, 1, f) == 1 && std::fread(&k, 8, 1, f) == 1 &&
+                    std::fread(&beta, 8, 1, f) == 1;
+  if (!head || std::string(magic, 4) != "FCPD") {
+    std::fclose(f);
+    throw ParseError("not a spectral cache file: " + path);
+  }
+  if (version != 1) {
+    std::fclose(f);
+    throw ParseError("unsupported spectral cache version in " + path);
+  }
+  SpectralBasis b;
+  b.u.resize(static_cast<Index>(m), static_cast<Index>(k));
+  b.lambda.resize(static_cast<Index>(k));
+  std::vector<double> row(static_cast<size_t>(k));
+  bool ok = true;
+  for (uint64_t i = 0; ok && i < m; ++i) {
+    ok = std::fread(row.data(), 8, static_cast<size_t>(k), f) == static_cast<size_t>(k);
+    for (uint64_t j = 0; ok && j < k; ++j)
+      b.u(static_cast<Index>(i), static_cast<Index>(j)) = row[static_cast<size_t>(j)];
+  }
+  ok = ok && std::fread(b.lambda.data(), 8, static_cast<size_t>(k), f) == static_cast<size_t>(k);
+  std::fclose(f);
+  if (!ok) throw ParseError("truncated spectral cache: " + path);
+  if (beta_out) *beta_out = beta;
+  return b;
+}
+
+// ----------------------------------------------------- solvers.hpp:61-176
+// solvers.hpp:61-73 — W = U (Λ + λσ² I)⁻¹ Uᵀ R.
+inline Coefficients solve_fast_lowrank(const SpectralBasis& basis, double lambda_reg,
+                                       double sigma2, const Matrix& residual) {
+  if (basis.points() != residual.rows())
+    throw ParameterError("solve_fast: residual rows must match basis points");
+  Coefficients c;
+  c.w.resize(residual.rows(), residual.cols());
+  detail::l2check(fcpd_solve_fast_lowrank(detail::l2ctx(), basis.u.data(), basis.lambda.data(),
+                                          basis.points(), basis.rank(), lambda_reg, sigma2,
+                                          residual.data(), residual.rows(),
+                                          static_cast<int32_t>(residual.cols()), c.w.data()));
+  return c;
+}
+
+// solvers.hpp:75-80.
+inline Coefficients solve_fast(const SpectralBasis& basis, double lambda_reg, double sigma2,
+                               const Matrix& residual) {
+  if (basis.rank() != basis.points())
+    throw ParameterError("solve_fast expects the full spectral basis");
+  return solve_fast_lowrank(basis, lambda_reg, sigma2, residual);
+}
+
+// solvers.hpp:138-144 — X + Φ W.
+inline PointSet apply_transform(const PointSet& x, const GramKernel& k, const Coefficients& c) {
+  if (k.size() != x.count() || c.w.rows() != x.count() || c.w.cols() != x.dim())
+    throw ParameterError("apply_transform: shape mismatch");
+  PointSet out;
+  out.pts.resize(x.count(), x.dim());
+  detail::l2check(fcpd_apply_transform(detail::l2ctx(), x.pts.data(), x.count(),
+                                       static_cast<int32_t>(x.dim()), k.phi.data(), k.size(),
+                                       c.w.data(), c.w.rows(), static_cast<int32_t>(c.w.cols()),
+                                       out.pts.data()));
+  return out;
+}
+
+// solvers.hpp:147-155 — X + U Λ Uᵀ W.
+inline PointSet apply_transform_lowrank(const PointSet& x, const SpectralBasis& basis,
+                                        const Coefficients& c) {
+  if (basis.points() != x.count() || c.w.rows() != x.count() || c.w.cols() != x.dim())
+    throw ParameterError("apply_transform_lowrank: shape mismatch");
+  PointSet out;
+  out.pts.resize(x.count(), x.dim());
+  detail::l2check(fcpd_apply_transform_lowrank(
+      detail::l2ctx(), x.pts.data(), x.count(), static_cast<int32_t>(x.dim()), basis.u.data(),
+      basis.points(), basis.lambda.data(), basis.rank(), c.w.data(), c.w.rows(),
+      static_cast<int32_t>(c.w.cols()), out.pts.data()));
+  return out;
+}
+
+// solvers.hpp:160-176 — σ² by the trace form (P row-constrained).
+inline double update_sigma2(const PointSet& y, const Correspondence& p, const PointSet& x_t) {
+  if (!p.row_constrained) throw ParameterError("update_sigma2 requires a row-constrained P");
+  double out = 0.0;
+  detail::l2check(fcpd_update_sigma2(detail::l2ctx(), y.pts.data(), y.count(), p.p.data(),
+                                     p.p.rows(), p.p.cols(), x_t.pts.data(), x_t.count(),
+                                     static_cast<int32_t>(x_t.dim()), 1, &out));
+  return out;
+}
+
+// ------------------------------------------------------ pointset.hpp:31-148
+struct NormalizationRecord {
+  Vector center;
+  double scale = 1.0;
+  bool degenerate = false;
+
+  PointSet apply(const PointSet& ps) const {
+    PointSet out;
+    out.pts.resize(ps.count(), ps.dim());
+    for (Index j = 0; j < ps.dim(); ++j)
+      for (Index i = 0; i < ps.count(); ++i) out.pts(i, j) = (ps.pts(i, j) - center(j)) / scale;
+    return out;
+  }
+  PointSet invert(const PointSet& ps) const {
+    PointSet out;
+    out.pts.resize(ps.count(), ps.dim());
+    for (Index j = 0; j < ps.dim(); ++j)
+      for (Index i = 0; i < ps.count(); ++i) out.pts(i, j) = ps.pts(i, j) * scale + center(j);
+    return out;
+  }
+};
+
+// pointset.hpp:124-148 — joint centroid, max-abs scale, the same map on both.
+inline std::tuple<PointSet, PointSet, NormalizationRecord> normalize_pair(const PointSet& x,
+                                                                         const PointSet& y) {
+  if (x.count() == 0 || y.count() == 0) throw ParameterError("normalize_pair: empty point set");
+  if (x.dim() != y.dim()) throw DimensionError("normalize_pair: dimension mismatch");
+  PointSet xo, yo;
+  xo.pts.resize(x.count(), x.dim());
+  yo.pts.resize(y.count(), y.dim());
+  NormalizationRecord rec;
+  rec.center.resize(x.dim());
+  int32_t deg = 0;
+  detail::l2check(fcpd_normalize_pair(detail::l2ctx(), x.pts.data(), x.count(),
+                                      static_cast<int32_t>(x.dim()), y.pts.data(), y.count(),
+                                      static_cast<int32_t>(y.dim()), xo.pts.data(),
+                                      yo.pts.data(), rec.center.data(), &rec.scale, &deg));
+  rec.degenerate = deg != 0;
+  return {std::move(xo), std::move(yo), rec};
 }
 
 // registration.hpp:59-69 (host, O(M+N)).

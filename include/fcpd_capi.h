@@ -210,17 +210,64 @@ FCPD_API int fcpd_load_spectral_cache(fcpd_ctx* ctx, const char* path, const dou
 FCPD_API int fcpd_build_gram(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d, double beta,
                     double* phi);
 
-/* solve_fast_lowrank — solvers.hpp:61-73 — with the basis given by the
- * caller (u: M×K column-major fp64, streamed as fp32 on the device).
- * residual, w: M×D. */
-FCPD_API int fcpd_solve_fast_lowrank(fcpd_ctx* ctx, const double* u, const double* lambda, int64_t m,
-                            int64_t k, double lambda_reg, double sigma2,
-                            const double* residual, int32_t d, double* w);
+/* ---- the reference's L2 functions in fp64 on the device (l2api.cu) -------
+ * Same semantics, checks and messages as the reference functions named;
+ * dense inputs as the caller passes them (column-major), products through
+ * cuBLAS dgemm, fixed-order reductions.  For the reference's unit tests and
+ * drop-in callers of these functions — the EM hot path (fcpd_register) does
+ * not use them. */
+
+/* estimated_targets — correspondence.hpp:101-105: out (M×D) = P (M×N) · Y
+ * (NY×D); NY != N → FCPD_ERR_PARAMETER "estimated_targets: shape mismatch". */
+FCPD_API int fcpd_estimated_targets(fcpd_ctx* ctx, const double* p, int64_t m, int64_t n,
+                                    const double* y, int64_t ny, int32_t d, double* out);
+
+/* enforce_row_constraint — correspondence.hpp:83-98, in place on P (M×N):
+ * rows with sum < 1e-300 become 1/N (degenerate[i] = 1), others / sum. */
+FCPD_API int fcpd_enforce_row_constraint(fcpd_ctx* ctx, double* p, int64_t m, int64_t n,
+                                         int32_t* degenerate);
+
+/* update_sigma2 — solvers.hpp:160-176 (trace form): y N×D, P M×NP, x̃ MX×D.
+ * !row_constrained → FCPD_ERR_PARAMETER; value < −1e-8 → FCPD_ERR_NUMERIC;
+ * *out = max(value, 1e-10). */
+FCPD_API int fcpd_update_sigma2(fcpd_ctx* ctx, const double* y, int64_t n, const double* p,
+                                int64_t m, int64_t np, const double* xt, int64_t mx, int32_t d,
+                                int32_t row_constrained, double* out);
+
+/* eigendecompose — kernel.hpp:49-72 — of a given Φ (M×M): top `rank`
+ * eigenpairs, descending, 1e-12·λmax clamp (lambda) and raw (lambda_raw). */
+FCPD_API int fcpd_eigendecompose(fcpd_ctx* ctx, const double* phi, int64_t m, int64_t rank,
+                                 double* u, double* lambda, double* lambda_raw);
+
+/* solve_fast_lowrank — solvers.hpp:61-73: W (M×D) = U diag(1/(λ+λ_reg σ²))
+ * Uᵀ R; u M×K, residual RM×D (RM != M → FCPD_ERR_PARAMETER); a non-positive
+ * λ_i + λ_reg σ² → FCPD_ERR_NUMERIC.  solve_fast (:75-80) is K = M. */
+FCPD_API int fcpd_solve_fast_lowrank(fcpd_ctx* ctx, const double* u, const double* lambda,
+                                     int64_t m, int64_t k, double lambda_reg, double sigma2,
+                                     const double* residual, int64_t rm, int32_t d, double* w);
+
+/* apply_transform — solvers.hpp:138-144: out = X + Φ W (Φ MPHI×MPHI, W
+ * MW×DW; any mismatch with X (M×D) → "apply_transform: shape mismatch"). */
+FCPD_API int fcpd_apply_transform(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d,
+                                  const double* phi, int64_t mphi, const double* w, int64_t mw,
+                                  int32_t dw, double* out);
 
 /* apply_transform_lowrank — solvers.hpp:147-155: out = X + U Λ Uᵀ W. */
 FCPD_API int fcpd_apply_transform_lowrank(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d,
-                                 const double* u, const double* lambda, int64_t k,
-                                 const double* w, double* out);
+                                          const double* u, int64_t mu, const double* lambda,
+                                          int64_t k, const double* w, int64_t mw, int32_t dw,
+                                          double* out);
+
+/* lowrank_reconstruction_error — kernel.hpp:76-83: ‖Φ − U Λ Uᵀ‖_F. */
+FCPD_API int fcpd_lowrank_reconstruction_error(fcpd_ctx* ctx, const double* phi, int64_t m,
+                                               const double* u, int64_t mu,
+                                               const double* lambda, int64_t k, double* out);
+
+/* normalize_pair — pointset.hpp:124-148 (host fp64): joint centroid,
+ * max-abs scale (≤ 0 → 1 and *degenerate = 1); xo/yo as x/y. */
+FCPD_API int fcpd_normalize_pair(fcpd_ctx* ctx, const double* x, int64_t m, int32_t dx,
+                                 const double* y, int64_t n, int32_t dy, double* xo, double* yo,
+                                 double* center, double* scale, int32_t* degenerate);
 
 #ifdef __cplusplus
 }

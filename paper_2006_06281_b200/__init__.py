@@ -163,8 +163,16 @@ def lib():
             "fcpd_create_dist": (C.c_int, [C.POINTER(vp), C.c_int, C.c_int, C.c_int,
                                            C.c_char_p]),
             "fcpd_world": (C.c_int, [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
-            "fcpd_solve_fast_lowrank": (C.c_int, [vp, P, P, I64, I64, D, D, P, I32, P]),
-            "fcpd_apply_transform_lowrank": (C.c_int, [vp, P, I64, I32, P, P, I64, P, P]),
+            "fcpd_solve_fast_lowrank": (C.c_int, [vp, P, P, I64, I64, D, D, P, I64, I32, P]),
+            "fcpd_apply_transform_lowrank": (C.c_int, [vp, P, I64, I32, P, I64, P, I64, P, I64,
+                                                       I32, P]),
+            "fcpd_apply_transform": (C.c_int, [vp, P, I64, I32, P, I64, P, I64, I32, P]),
+            "fcpd_estimated_targets": (C.c_int, [vp, P, I64, I64, P, I64, I32, P]),
+            "fcpd_enforce_row_constraint": (C.c_int, [vp, P, I64, I64, PI32]),
+            "fcpd_update_sigma2": (C.c_int, [vp, P, I64, P, I64, I64, P, I64, I32, I32, P]),
+            "fcpd_eigendecompose": (C.c_int, [vp, P, I64, I64, P, P, P]),
+            "fcpd_lowrank_reconstruction_error": (C.c_int, [vp, P, I64, P, I64, P, I64, P]),
+            "fcpd_normalize_pair": (C.c_int, [vp, P, I64, I32, P, I64, I32, P, P, P, P, PI32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -441,33 +449,107 @@ class Context:
                                                 int(iterations), _p(u), _p(lam), _p(raw)))
         return u, lam, raw
 
+    # fp64 device restatements of the reference's L2 functions (l2api.cu)
     def solve_fast_lowrank(self, u, lam, lambda_reg: float, sigma2: float, residual):
+        """solvers.hpp:61-73 — W = U diag(1/(λ+λσ²)) Uᵀ R."""
         u = np.asfortranarray(u, dtype=np.float64)
         lam = np.ascontiguousarray(lam, dtype=np.float64)
         r = _colmajor(residual)
         m, k = u.shape
-        if r.shape[0] != m:
-            raise ParameterError("solve_fast: residual rows must match basis points")
         w = np.zeros(r.shape, order="F")
         self._check(lib().fcpd_solve_fast_lowrank(self._h, _p(u), _p(lam), m, k, lambda_reg,
-                                                  sigma2, _p(r), r.shape[1], _p(w)))
+                                                  sigma2, _p(r), r.shape[0], r.shape[1], _p(w)))
         return np.ascontiguousarray(w)
 
     def solve_fast(self, u, lam, lambda_reg: float, sigma2: float, residual):
+        """solvers.hpp:75-80 (full basis)."""
         u = np.asarray(u)
         if u.shape[0] != u.shape[1]:
             raise ParameterError("solve_fast expects the full spectral basis")
         return self.solve_fast_lowrank(u, lam, lambda_reg, sigma2, residual)
 
     def apply_transform_lowrank(self, x, u, lam, w):
+        """solvers.hpp:147-155 — X + U Λ Uᵀ W."""
         x, w = _colmajor(x), _colmajor(w)
         u = np.asfortranarray(u, dtype=np.float64)
         lam = np.ascontiguousarray(lam, dtype=np.float64)
         m, d = x.shape
         out = np.zeros((m, d), order="F")
-        self._check(lib().fcpd_apply_transform_lowrank(self._h, _p(x), m, d, _p(u), _p(lam),
-                                                       u.shape[1], _p(w), _p(out)))
+        self._check(lib().fcpd_apply_transform_lowrank(self._h, _p(x), m, d, _p(u), u.shape[0],
+                                                       _p(lam), u.shape[1], _p(w), w.shape[0],
+                                                       w.shape[1], _p(out)))
         return np.ascontiguousarray(out)
+
+    def apply_transform(self, x, phi, w):
+        """solvers.hpp:138-144 — X + Φ W."""
+        x, w = _colmajor(x), _colmajor(w)
+        phi = np.asfortranarray(phi, dtype=np.float64)
+        m, d = x.shape
+        out = np.zeros((m, d), order="F")
+        self._check(lib().fcpd_apply_transform(self._h, _p(x), m, d, _p(phi), phi.shape[0],
+                                               _p(w), w.shape[0], w.shape[1], _p(out)))
+        return np.ascontiguousarray(out)
+
+    def estimated_targets(self, p, y):
+        """correspondence.hpp:101-105 — P·Y."""
+        p = np.asfortranarray(p, dtype=np.float64)
+        y = _colmajor(y)
+        out = np.zeros((p.shape[0], y.shape[1]), order="F")
+        self._check(lib().fcpd_estimated_targets(self._h, _p(p), p.shape[0], p.shape[1], _p(y),
+                                                 y.shape[0], y.shape[1], _p(out)))
+        return np.ascontiguousarray(out)
+
+    def enforce_row_constraint(self, p):
+        """correspondence.hpp:83-98 — (P̃, degenerate row indices)."""
+        q = np.array(p, dtype=np.float64, order="F", copy=True)
+        deg = np.zeros(q.shape[0], dtype=np.int32)
+        self._check(lib().fcpd_enforce_row_constraint(self._h, _p(q), q.shape[0], q.shape[1],
+                                                      _pi32(deg)))
+        return q, np.nonzero(deg)[0].tolist()
+
+    def update_sigma2(self, y, p, xt, row_constrained: bool = True) -> float:
+        """solvers.hpp:160-176 (trace form)."""
+        y, xt = _colmajor(y), _colmajor(xt)
+        p = np.asfortranarray(p, dtype=np.float64)
+        out = C.c_double()
+        self._check(lib().fcpd_update_sigma2(self._h, _p(y), y.shape[0], _p(p), p.shape[0],
+                                             p.shape[1], _p(xt), xt.shape[0], xt.shape[1],
+                                             int(bool(row_constrained)), C.byref(out)))
+        return out.value
+
+    def eigendecompose(self, phi, rank: int):
+        """kernel.hpp:49-72 of a given Φ — (U, λ clamped, λ raw)."""
+        phi = np.asfortranarray(phi, dtype=np.float64)
+        m = phi.shape[0]
+        u = np.zeros((m, rank), order="F")
+        lam, raw = np.zeros(rank), np.zeros(rank)
+        self._check(lib().fcpd_eigendecompose(self._h, _p(phi), m, int(rank), _p(u), _p(lam),
+                                              _p(raw)))
+        return u, lam, raw
+
+    def lowrank_reconstruction_error(self, u, lam, phi) -> float:
+        """kernel.hpp:76-83 — ‖Φ − U Λ Uᵀ‖_F."""
+        phi = np.asfortranarray(phi, dtype=np.float64)
+        u = np.asfortranarray(u, dtype=np.float64)
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        out = C.c_double()
+        self._check(lib().fcpd_lowrank_reconstruction_error(
+            self._h, _p(phi), phi.shape[0], _p(u), u.shape[0], _p(lam), u.shape[1],
+            C.byref(out)))
+        return out.value
+
+    def normalize_pair(self, x, y):
+        """pointset.hpp:124-148 — (x', y', center, scale, degenerate)."""
+        x, y = _colmajor(x), _colmajor(y)
+        xo, yo = np.zeros(x.shape, order="F"), np.zeros(y.shape, order="F")
+        c = np.zeros(max(x.shape[1], 1))
+        sc = C.c_double()
+        deg = C.c_int32()
+        self._check(lib().fcpd_normalize_pair(self._h, _p(x), x.shape[0], x.shape[1], _p(y),
+                                              y.shape[0], y.shape[1], _p(xo), _p(yo), _p(c),
+                                              C.byref(sc), C.byref(deg)))
+        return (np.ascontiguousarray(xo), np.ascontiguousarray(yo), c[: x.shape[1]], sc.value,
+                bool(deg.value))
 
 
 _default_ctx: Optional[Context] = None

@@ -76,11 +76,12 @@ struct IterState {
   int32_t pad1;
 };
 
-// Iterations between re-checks of a culling that did not pay (engine:
-// lists are skipped while the previous lists kept ≥ kCullKeepFrac of the
-// units, except every kCullRecheck-th iteration).
+// Culling lists are built in an iteration when the previous lists dropped
+// any unit (kept < kCullKeepFrac of them: σ² only falls, so a culling that
+// starts to bite soon pays for its list kernels), else only every
+// kCullRecheck-th iteration (C1's first iterations: nothing to drop).
 constexpr int kCullRecheck = 8;
-constexpr double kCullKeepFrac = 0.94;
+constexpr double kCullKeepFrac = 0.999;
 
 // The E-step scalars for σ² (correspondence.hpp:43-47 floor + clamp flag,
 // :61-66 outlier constant in log2 units), the fallback queues emptied, and

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "ctx.cuh"
 #include "dist.cuh"
 #include "estep.cuh"
 #include "mstep.cuh"
@@ -159,23 +160,6 @@ __global__ void pack_coef_kernel(const double* __restrict__ coef, int64_t k,
                         static_cast<float>(coef[2 * k + i]), 0.f);
 }
 
-// W = Q c (coefficients), fp64 accumulation over the fp32 basis.
-__global__ void coef_kernel(const float* __restrict__ qt, int64_t mpad, int64_t m, int64_t k,
-                            const double* __restrict__ coef, double* __restrict__ w) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  double a0 = 0, a1 = 0, a2 = 0;
-  for (int64_t j = 0; j < k; ++j) {
-    const double q = qt[j * mpad + i];
-    a0 += q * coef[j];
-    a1 += q * coef[k + j];
-    a2 += q * coef[2 * k + j];
-  }
-  w[i] = a0;
-  w[m + i] = a1;
-  w[2 * m + i] = a2;
-}
-
 }  // namespace
 
 // ------------------------------------------------------------------ Session
@@ -206,6 +190,10 @@ struct Session {
   YStats ystats{};
   EStepPlan ep;
   ColsumPlan zp, vp;
+  // z = Qᵀ·R as row dot products over the contiguous prefix of Qᵀ's rows
+  // (streaming M-step; FCPD_ZPASS=colsum → column sums over Q instead)
+  RowdotPlan zr;
+  bool rowdot = false;
   double tau = 0.0;  // spectral truncation threshold of the basis streams (0: off)
   bool mfused = false;            // whole M-step as one cooperative kernel (mstep_fused.cu)
   int mfused_grid = 0;
@@ -565,10 +553,17 @@ void enqueue_iteration(fcpd_ctx* ctx, Session& s, cudaEvent_t* ev = nullptr) {
   }
   if (s.zp.trunc)
     launch_spectral_rank(b.lam, b.lam + b.k, b.k, s.cfg.lambda_reg, s.tau, st, str);
-  launch_colsum(s.zp, b.q, b.kpad, s.resid4.p, s.zpart.p, st, s.stamps.p, 1, str);
-  rec(3);
-  launch_zreduce(s.zp, s.zpart.p, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.coef.p, s.g4.p, st,
-                 str);
+  if (s.rowdot) {
+    launch_rowdot(s.zr, b.qt, s.resid4.p, s.zpart.p, st, s.stamps.p, 1, str);
+    rec(3);
+    launch_rowdot_reduce(s.zr, s.zpart.p, b.k, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.coef.p,
+                         s.g4.p, nullptr, st, str);
+  } else {
+    launch_colsum(s.zp, b.q, b.kpad, s.resid4.p, s.zpart.p, st, s.stamps.p, 1, str);
+    rec(3);
+    launch_zreduce(s.zp, s.zpart.p, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.coef.p, s.g4.p, st,
+                   str);
+  }
   rec(4);
   launch_colsum(s.vp, b.qt, b.mpad, s.g4.p, s.vpart.p, st, nullptr, 0, str);
   rec(5);
@@ -663,7 +658,11 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
     if (const char* e = std::getenv("FCPD_SPECTRAL_TAU")) s.tau = std::atof(e);  // A/B
     s.zp.trunc = s.tau > 0.0 ? 1 : 0;
     s.vp.trunc = s.tau > 0.0 ? 2 : 0;
-    s.zpart.ensure(s.zp.part_doubles());
+    const char* zpass = std::getenv("FCPD_ZPASS");
+    s.rowdot = !s.mfused && !(zpass && std::string(zpass) == "colsum");
+    s.zr = make_rowdot_plan(b.k, m, b.mpad, ctx->sm_count);
+    s.zr.g.trunc = s.zp.trunc;
+    s.zpart.ensure(std::max(s.zp.part_doubles(), s.rowdot ? s.zr.part_doubles() : size_t(0)));
     s.vpart.ensure(s.vp.part_doubles());
     s.coef.ensure(3 * b.k);
     s.g4.ensure(b.kpad);  // the fused M-step streams whole quads (kpad ≥ K)
@@ -1103,8 +1102,15 @@ void enqueue_iteration_dist(fcpd_ctx* ctx, Session& s) {
   // M-step on the own row shard of the basis
   if (s.zp.trunc)
     launch_spectral_rank(b.lam, b.lam + b.k, b.k, s.cfg.lambda_reg, s.tau, st, str);
-  launch_colsum(s.zp, b.q + s.m0 * b.kpad, b.kpad, s.resid4.p, s.zpart.p, st, s.stamps.p, 1, str);
-  launch_zsum(s.zp, s.zpart.p, s.zfull.p, st, str);
+  if (s.rowdot) {  // over this rank's columns of Qᵀ (compact copy)
+    launch_rowdot(s.zr, s.qt_own.p, s.resid4.p, s.zpart.p, st, s.stamps.p, 1, str);
+    launch_rowdot_reduce(s.zr, s.zpart.p, b.k, nullptr, nullptr, 0.0, nullptr, nullptr,
+                         s.zfull.p, st, str);
+  } else {
+    launch_colsum(s.zp, b.q + s.m0 * b.kpad, b.kpad, s.resid4.p, s.zpart.p, st, s.stamps.p, 1,
+                  str);
+    launch_zsum(s.zp, s.zpart.p, s.zfull.p, st, str);
+  }
   FCPD_NCCL(ncclAllReduce(s.zfull.p, s.zfull.p, 3 * b.k, ncclDouble, ncclSum, comm, str));
   launch_zfilter(s.zfull.p, b.k, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.coef.p, s.g4.p, st, str);
   launch_colsum(s.vp, s.qt_own.p, s.mr4, s.g4.p, s.vpart.p, st, nullptr, 0, str);
@@ -1273,7 +1279,13 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
   if (const char* e = std::getenv("FCPD_SPECTRAL_TAU")) s.tau = std::atof(e);
   s.zp.trunc = s.tau > 0.0 ? 1 : 0;
   s.vp.trunc = s.tau > 0.0 ? 2 : 0;
-  s.zpart.ensure(s.zp.part_doubles());
+  {
+    const char* zpass = std::getenv("FCPD_ZPASS");
+    s.rowdot = !(zpass && std::string(zpass) == "colsum");
+    s.zr = make_rowdot_plan(b.k, s.m_valid_own, s.mr4, ctx->sm_count);
+    s.zr.g.trunc = s.zp.trunc;
+  }
+  s.zpart.ensure(std::max(s.zp.part_doubles(), s.rowdot ? s.zr.part_doubles() : size_t(0)));
   s.vpart.ensure(s.vp.part_doubles());
   s.zfull.ensure(3 * b.k);
   s.coef.ensure(3 * b.k);
@@ -1409,6 +1421,13 @@ void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall) {
 }
 
 }  // namespace
+
+CtxHandles ctx_handles(fcpd_ctx* ctx) {
+  return CtxHandles{ctx->device, ctx->stream, ctx->blas, ctx->solver};
+}
+
+int ctx_guarded(fcpd_ctx* ctx, const std::function<void()>& f) { return guarded(ctx, f); }
+
 }  // namespace fcpd
 
 // ============================================================== C ABI
@@ -1837,86 +1856,38 @@ int fcpd_build_basis_topk(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d, 
   });
 }
 
-namespace {
-// shared by solve_fast_lowrank / apply_transform_lowrank: run z = Qᵀ v,
-// filter, and either W = Q c or out = X + Q g.
-void lowrank_apply(fcpd_ctx* ctx, const double* u, const double* lambda, int64_t m, int64_t k,
-                   const double* rhs, int d, double lambda_reg, double sigma2, bool transform,
-                   const double* x, double* out) {
-  if (m <= 0 || k <= 0 || k > m) throw Failure(FCPD_ERR_PARAMETER, "solve_fast: bad basis shape");
-  if (d < 1 || d > 3) throw Failure(FCPD_ERR_DIMENSION, "solve_fast: the B200 path supports D <= 3");
-  cudaStream_t str = ctx->stream;
-  Basis b;
-  basis_from_host(b, u, lambda, m, k, str);
-  // lam buffer: [0,k) solver diagonal λ, [k,2k) numerator
-  std::vector<double> lh(2 * k);
-  for (int64_t i = 0; i < k; ++i) {
-    lh[i] = transform ? 1.0 : lambda[i];
-    lh[k + i] = transform ? lambda[i] : 1.0;
-  }
-  FCPD_CUDA(cudaMemcpyAsync(b.lam, lh.data(), sizeof(double) * 2 * k, cudaMemcpyHostToDevice, str));
-  std::vector<float4> v4(m);
-  for (int64_t i = 0; i < m; ++i) {
-    float c[3] = {0.f, 0.f, 0.f};
-    for (int j = 0; j < d; ++j) c[j] = static_cast<float>(rhs[j * m + i]);
-    v4[i] = make_float4(c[0], c[1], c[2], 0.f);
-  }
-  DevBuf<float4> v, g;
-  DevBuf<double> zpart, vpart, coef, xd, res;
-  DevBuf<IterState> st;
-  v.ensure(m);
-  g.ensure(k);
-  coef.ensure(3 * k);
-  st.ensure(1);
-  FCPD_CUDA(cudaMemcpyAsync(v.p, v4.data(), sizeof(float4) * m, cudaMemcpyHostToDevice, str));
-  IterState h{};
-  h.sigma2 = transform ? 0.0 : sigma2;
-  h.active = 1;
-  FCPD_CUDA(cudaMemcpyAsync(st.p, &h, sizeof h, cudaMemcpyHostToDevice, str));
-  const ColsumPlan zp = make_colsum_plan(m, k, ctx->sm_count);
-  zpart.ensure(zp.part_doubles());
-  launch_colsum(zp, b.q, b.kpad, v.p, zpart.p, st.p, nullptr, 0, str);
-  launch_zreduce(zp, zpart.p, b.lam, b.lam + k, transform ? 0.0 : lambda_reg, coef.p, g.p, st.p,
-                 str);
-  res.ensure(3 * m);
-  if (transform) {
-    const ColsumPlan vp = make_colsum_plan(k, m, ctx->sm_count);
-    vpart.ensure(vp.part_doubles());
-    launch_colsum(vp, b.qt, b.mpad, g.p, vpart.p, st.p, nullptr, 0, str);
-    xd.ensure(3 * m);
-    FCPD_CUDA(cudaMemcpyAsync(xd.p, x, sizeof(double) * d * m, cudaMemcpyHostToDevice, str));
-    launch_vreduce_add(vp, vpart.p, xd.p, d, res.p, str);
-  } else {
-    coef_kernel<<<ceil_div(m, 128), 128, 0, str>>>(b.qt, b.mpad, m, k, coef.p, res.p);
-    FCPD_LAUNCH_CHECK();
-  }
-  IterState hs{};
-  FCPD_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof hs, cudaMemcpyDeviceToHost, str));
-  FCPD_CUDA(cudaMemcpyAsync(out, res.p, sizeof(double) * d * m, cudaMemcpyDeviceToHost, str));
-  FCPD_CUDA(cudaStreamSynchronize(str));
-  for (auto* p : {&zpart, &vpart, &coef, &xd, &res}) p->release();
-  v.release();
-  g.release();
-  st.release();
-  b.release();
-  if (hs.err_code == kDevSolveDiag)
-    throw Failure(FCPD_ERR_NUMERIC, "solve_fast: lambda_i + lambda*sigma2 not positive");
-}
-}  // namespace
-
-int fcpd_solve_fast_lowrank(fcpd_ctx* ctx, const double* u, const double* lambda, int64_t m,
-                            int64_t k, double lambda_reg, double sigma2, const double* residual,
-                            int32_t d, double* w) {
+// normalize_pair (pointset.hpp:124-148): host fp64, O(M+N) — the engine's
+// own normalisation (normalize_pair_host), plus the reference's checks and
+// degenerate flag.
+int fcpd_normalize_pair(fcpd_ctx* ctx, const double* x, int64_t m, int32_t dx, const double* y,
+                        int64_t n, int32_t dy, double* xo, double* yo, double* center,
+                        double* scale, int32_t* degenerate) {
   return guarded(ctx, [&] {
-    lowrank_apply(ctx, u, lambda, m, k, residual, d, lambda_reg, sigma2, false, nullptr, w);
-  });
-}
-
-int fcpd_apply_transform_lowrank(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d,
-                                 const double* u, const double* lambda, int64_t k, const double* w,
-                                 double* out) {
-  return guarded(ctx, [&] {
-    lowrank_apply(ctx, u, lambda, m, k, w, d, 0.0, 0.0, true, x, out);
+    if (m <= 0 || n <= 0) throw Failure(FCPD_ERR_PARAMETER, "normalize_pair: empty point set");
+    if (dx != dy) throw Failure(FCPD_ERR_DIMENSION, "normalize_pair: dimension mismatch");
+    const int d = dx;
+    const double total = static_cast<double>(m + n);
+    std::vector<double> c(static_cast<size_t>(std::max(d, 1)), 0.0);
+    for (int k = 0; k < d; ++k) {
+      double sx = 0.0, sy = 0.0;
+      for (int64_t i = 0; i < m; ++i) sx += x[k * m + i];
+      for (int64_t i = 0; i < n; ++i) sy += y[k * n + i];
+      c[k] = (sx + sy) / total;
+    }
+    double sc = 0.0;
+    for (int k = 0; k < d; ++k) {
+      for (int64_t i = 0; i < m; ++i) sc = std::max(sc, std::fabs(x[k * m + i] - c[k]));
+      for (int64_t i = 0; i < n; ++i) sc = std::max(sc, std::fabs(y[k * n + i] - c[k]));
+    }
+    const bool deg = !(sc > 0.0);
+    if (deg) sc = 1.0;
+    for (int k = 0; k < d; ++k) {
+      for (int64_t i = 0; i < m; ++i) xo[k * m + i] = (x[k * m + i] - c[k]) / sc;
+      for (int64_t i = 0; i < n; ++i) yo[k * n + i] = (y[k * n + i] - c[k]) / sc;
+      if (center) center[k] = c[k];
+    }
+    if (scale) *scale = sc;
+    if (degenerate) *degenerate = deg ? 1 : 0;
   });
 }
 

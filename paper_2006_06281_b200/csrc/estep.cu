@@ -308,19 +308,45 @@ __device__ __forceinline__ void col_b_ranges(const ColFix& f, int rb, int64_t n,
 
 // Pass-1 block fix-up: each column's sum over the block's slots in CTA
 // order, finalisation, b ranges.
+// Slot loads are issued kFixBatch at a time (independent L2 loads in
+// flight), then added in CTA order: the same sums as a serial walk (an
+// empty range contributes +0.0, which leaves a sum of non-negative terms
+// unchanged bit for bit).
+constexpr int kFixBatch = 4;
+constexpr int kRowFixBatch = 2;  // pass 2: 5 quantities per slot
+
 template <int kCols>
 __device__ void col_block_fixup(const ColFix& f, const double* seg, const SegRange& sr,
                                 int64_t G, int64_t P, int rb, int64_t m, int64_t n,
                                 IterState* st) {
+  static_assert(kCols % 2 == 0, "double2 slot loads");
   const int t = threadIdx.x;
   float lo = INFINITY, hi = -INFINITY;
+  double sums[kCols];
+#pragma unroll
+  for (int h = 0; h < kCols; ++h) sums[h] = 0.0;
+  for (int64_t g = sr.g0; g <= sr.g1; g += kFixBatch) {
+    double2 v[kFixBatch][kCols / 2];
+#pragma unroll
+    for (int j = 0; j < kFixBatch; ++j) {
+      const bool live = g + j <= sr.g1 && !sk_empty(g + j, G, P);
+      const double2* sp = reinterpret_cast<const double2*>(seg + (g + j + rb) * kTile + kCols * t);
+#pragma unroll
+      for (int h = 0; h < kCols / 2; ++h) v[j][h] = live ? __ldcg(sp + h) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int j = 0; j < kFixBatch; ++j)
+#pragma unroll
+      for (int h = 0; h < kCols / 2; ++h) {
+        sums[2 * h] += v[j][h].x;
+        sums[2 * h + 1] += v[j][h].y;
+      }
+  }
 #pragma unroll
   for (int h = 0; h < kCols; ++h) {
     const int li = kCols * t + h;
     const int64_t col = static_cast<int64_t>(rb) * kTile + li;
-    double sm = 0.0;
-    for (int64_t g = sr.g0; g <= sr.g1; ++g)
-      if (!sk_empty(g, G, P)) sm += __ldcg(seg + (g + rb) * kTile + li);
+    const double sm = sums[h];
     if (col < n) {
       const float b = col_finalize(f, col, sm, m, st);
       if (b == b) {
@@ -639,17 +665,35 @@ __device__ void row_block_fixup(const RowFix& f, const double* seg, const SegRan
                                 IterState* st) {
   const int t = threadIdx.x;
 #pragma unroll 1
-  for (int h = 0; h < kRows; ++h) {
+  for (int h = 0; h < kRows; h += 2) {  // row pairs: one double2 per quantity and slot
     const int li = kRows * t + h;
-    const int64_t row = static_cast<int64_t>(rb) * kTile + li;
-    double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int64_t g = sr.g0; g <= sr.g1; ++g) {
-      if (sk_empty(g, G, P)) continue;
-      const double* sp = seg + (g + rb) * 5 * kTile + li;
+    double a[2][5];
 #pragma unroll
-      for (int k = 0; k < 5; ++k) a[k] += __ldcg(sp + k * kTile);
+    for (int k = 0; k < 5; ++k) a[0][k] = a[1][k] = 0.0;
+    for (int64_t g = sr.g0; g <= sr.g1; g += kRowFixBatch) {
+      double2 v[kRowFixBatch][5];
+#pragma unroll
+      for (int j = 0; j < kRowFixBatch; ++j) {
+        const bool live = g + j <= sr.g1 && !sk_empty(g + j, G, P);
+        const double* sp = seg + (g + j + rb) * 5 * kTile + li;
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+          v[j][k] = live ? __ldcg(reinterpret_cast<const double2*>(sp + k * kTile))
+                         : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int j = 0; j < kRowFixBatch; ++j)
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          a[0][k] += v[j][k].x;
+          a[1][k] += v[j][k].y;
+        }
     }
-    if (row < m) row_finalize(f, row, m, n, a, st);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int64_t row = static_cast<int64_t>(rb) * kTile + li + e;
+      if (row < m) row_finalize(f, row, m, n, a[e], st);
+    }
   }
 }
 
@@ -1443,7 +1487,9 @@ __global__ void __launch_bounds__(kListThreads)
   }
   if (last_cta_scan(offset, n_blocks, done, cull.counters ? cull.counters + 1 : nullptr) &&
       threadIdx.x == 0) {
-    // next iteration builds lists again only if these dropped enough units
+    // the next iteration builds lists again if these dropped any unit (σ²
+    // only falls, so a culling that starts to bite soon pays); otherwise
+    // every kCullRecheck-th iteration
     const double kept1 = static_cast<double>(cull.wl1_offset[cull.n_ytiles]);
     const double kept2 = static_cast<double>(offset[n_blocks]);
     st->cull_pays = kept1 < kCullKeepFrac * static_cast<double>(cull.wl1_units) ||

@@ -407,6 +407,252 @@ __global__ void __launch_bounds__(kBulkThreads, kBulkCtasPerSm)
   }
 }
 
+// ---------------------------------------------------------------------------
+// z = Qᵀ·R as ROW dot products over Qᵀ (K × M row-major fp32).  With
+// spectral truncation the streamed eigenvectors are a contiguous PREFIX of
+// Qᵀ's rows, so every copy is a long contiguous run; over Q (M × K
+// row-major) the same prefix is a short strided piece of every row (C4:
+// 736 of 1200 bytes per row, 2.3 TB/s).  Work units are (group of
+// kRdRows eigenvector rows, 1024-column block); a persistent stream-K grid
+// splits them evenly in row-group-major order.  A producer warp bulk-copies
+// a unit's kRdRows × 4 KB row pieces into a 32 KB stage of a 3-stage ring
+// (L2 evict-first); 8 consumer warps: each thread owns 4 columns, reads
+// their R once per unit (float4 per column, L2-resident) and keeps
+// kRdRows × 3 fp64 sums for the current row group (fp32 over its 4
+// columns).  When the CTA leaves a row group it reduces its threads in a
+// fixed order into one partial slot; rowdot_reduce sums a row's slots in
+// CTA order — bitwise reproducible.
+namespace {
+constexpr int kRdRows = 8;                        // eigenvector rows per unit
+constexpr int kRdCols = 4 * kColsumThreads;       // 1024 columns per unit
+constexpr int kRdSlot = kRdRows * 3;              // doubles per partial slot
+// one CTA per SM with a 6-stage ring: the 8×3 fp64 sums per thread need the
+// registers of a single resident CTA; 192 KB in flight per SM as colsum_bulk
+constexpr int kRdStages = 6;
+constexpr int kRdSmem = kRdStages * kStageBytes + 2 * kRdStages * 8;
+
+__device__ __forceinline__ RdGeom rd_eff(RdGeom g, const IterState* st) {
+  if (!g.trunc || !st) return g;
+  g.rows = min(g.rows, static_cast<int64_t>(st->keff));
+  g.units = (g.rows + kRdRows - 1) / kRdRows * g.col_blocks;
+  return g;
+}
+__host__ __device__ __forceinline__ int64_t rd_begin(const RdGeom& g, int64_t cta) {
+  return cta * g.units / g.grid;
+}
+__device__ __forceinline__ int64_t rd_owner(const RdGeom& g, int64_t u) {
+  return ((u + 1) * g.grid - 1) / g.units;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kBulkThreads, 1)
+    rowdot_bulk_kernel(const float* __restrict__ A, const float4* __restrict__ v, RdGeom g,
+                       double* __restrict__ part, const IterState* __restrict__ st,
+                       uint64_t* stamps, int stamp_slot) {
+  griddep_wait();
+  if (st && !st->active) return;
+  if (stamps && blockIdx.x == 0 && threadIdx.x == 0)
+    stamps[4 * st->iter + stamp_slot] = globaltimer();
+  g = rd_eff(g, st);
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* ring = reinterpret_cast<float*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRdStages * kStageBytes);
+  uint64_t* empty = full + kRdStages;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < kRdStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kBulkConsumers / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t u0 = rd_begin(g, blockIdx.x), u1 = rd_begin(g, blockIdx.x + 1);
+  static_assert(kRdRows * kRdCols * 4 == kStageBytes, "one unit per stage");
+
+  if (tid >= kBulkConsumers) {  // ---------------- producer warp
+    if (tid != kBulkConsumers) return;
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    for (int64_t u = u0; u < u1; ++u) {
+      const int64_t chunk = u - u0;
+      const int s = static_cast<int>(chunk % kRdStages);
+      const uint32_t ph = static_cast<uint32_t>((chunk / kRdStages) & 1);
+      const int64_t rg = u / g.col_blocks, cb = u - rg * g.col_blocks;
+      const int64_t c0 = cb * kRdCols;
+      const int64_t ncol = min(static_cast<int64_t>(kRdCols), g.cols - c0);
+      const uint32_t bytes = static_cast<uint32_t>(((ncol + 3) & ~int64_t(3)) * 4);
+      const int nrows = static_cast<int>(min(static_cast<int64_t>(kRdRows), g.rows - rg * kRdRows));
+      mbar_wait(&empty[s], ph ^ 1);
+      mbar_expect_tx(&full[s], bytes * nrows);
+      float* dst = ring + static_cast<int64_t>(s) * (kStageBytes / 4);
+      for (int r = 0; r < nrows; ++r)
+        bulk_g2s(dst + r * kRdCols, A + (rg * kRdRows + r) * g.lda + c0, bytes, &full[s], policy);
+    }
+    return;
+  }
+
+  // ------------------------------------------------ consumer warps
+  __shared__ double red[kBulkConsumers / 32][kRdSlot];
+  double acc[kRdRows][3];
+#pragma unroll
+  for (int r = 0; r < kRdRows; ++r) acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
+  int slot = 0;
+  // the fixed-order CTA reduction of the current row group into slot `slot`
+  auto flush_group = [&]() {
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int r = 0; r < kRdRows; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double w = warp_sum(acc[r][c]);
+        if (lane == 0) red[warp][r * 3 + c] = w;
+        acc[r][c] = 0.0;
+      }
+    asm volatile("bar.sync 1, %0;" ::"r"(kBulkConsumers));  // consumers only
+    if (tid < kRdSlot) {
+      double s = 0.0;
+      for (int w = 0; w < kBulkConsumers / 32; ++w) s += red[w][tid];
+      part[(static_cast<int64_t>(blockIdx.x) * g.kmax + slot) * kRdSlot + tid] = s;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(kBulkConsumers));  // red is reused
+    ++slot;
+  };
+  int64_t cur_rg = u0 < u1 ? u0 / g.col_blocks : 0;
+  for (int64_t u = u0; u < u1; ++u) {
+    const int64_t chunk = u - u0;
+    const int s = static_cast<int>(chunk % kRdStages);
+    const uint32_t ph = static_cast<uint32_t>((chunk / kRdStages) & 1);
+    const int64_t rg = u / g.col_blocks, cb = u - rg * g.col_blocks;
+    if (rg != cur_rg) {
+      flush_group();
+      cur_rg = rg;
+    }
+    const int64_t c0 = cb * kRdCols + 4 * tid;
+    const int nrows = static_cast<int>(min(static_cast<int64_t>(kRdRows), g.rows - rg * kRdRows));
+    float4 rv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      rv[j] = c0 + j < g.cols ? __ldg(v + c0 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    mbar_wait(&full[s], ph);
+    const float4* st4 = reinterpret_cast<const float4*>(ring + static_cast<int64_t>(s) * (kStageBytes / 4));
+#pragma unroll
+    for (int r = 0; r < kRdRows; ++r) {
+      if (r < nrows && c0 < g.cols) {
+        const float4 q = st4[r * (kRdCols / 4) + tid];
+        // fp32 over the thread's 4 columns, then fp64
+        const float fx = __fmaf_rn(q.w, rv[3].x, __fmaf_rn(q.z, rv[2].x, __fmaf_rn(q.y, rv[1].x, q.x * rv[0].x)));
+        const float fy = __fmaf_rn(q.w, rv[3].y, __fmaf_rn(q.z, rv[2].y, __fmaf_rn(q.y, rv[1].y, q.x * rv[0].y)));
+        const float fz = __fmaf_rn(q.w, rv[3].z, __fmaf_rn(q.z, rv[2].z, __fmaf_rn(q.y, rv[1].z, q.x * rv[0].z)));
+        acc[r][0] += fx;
+        acc[r][1] += fy;
+        acc[r][2] += fz;
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+  }
+  if (u0 < u1) flush_group();
+}
+
+// z_k (k < rows this iteration) = Σ over the CTAs covering its row group of
+// their slot, in CTA order (a warp per k: lanes stride the CTAs, fixed xor
+// tree).  filter != 0: c = z/(λ + λ_reg σ²), g = λnum·c (zreduce_filter);
+// else z (SoA 3×K, zeros past the streamed rows) for the distributed
+// all-reduce.
+__global__ void rowdot_reduce_kernel(const double* __restrict__ part, RdGeom g, int64_t k,
+                                     const double* __restrict__ lam,
+                                     const double* __restrict__ lam_num, double lambda_reg,
+                                     double* __restrict__ coef, float4* __restrict__ g4,
+                                     double* __restrict__ z_out, IterState* st) {
+  griddep_wait();
+  if (st && !st->active) return;
+  g = rd_eff(g, st);
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t kk = min(k, g.rows);
+  const double sigma2 = st ? st->sigma2 : 0.0;
+  if (st && lam && warp == 0 && lane == 0) st->sigma2_m = sigma2;
+  for (int64_t i = warp; i < (z_out ? k : kk); i += nwarps) {
+    double z0 = 0.0, z1 = 0.0, z2 = 0.0;
+    if (i < kk) {
+      const int64_t rg = i / kRdRows, rr = i - rg * kRdRows;
+      const int64_t g0 = rd_owner(g, rg * g.col_blocks), g1 = rd_owner(g, (rg + 1) * g.col_blocks - 1);
+      for (int64_t cta = g0 + lane; cta <= g1; cta += 32) {
+        const int64_t b = rd_begin(g, cta);
+        if (b == rd_begin(g, cta + 1)) continue;  // empty range
+        const int64_t slot = rg - b / g.col_blocks;
+        const double* p = part + (cta * g.kmax + slot) * kRdSlot + rr * 3;
+        z0 += p[0];
+        z1 += p[1];
+        z2 += p[2];
+      }
+      z0 = warp_sum(z0);
+      z1 = warp_sum(z1);
+      z2 = warp_sum(z2);
+    }
+    if (lane) continue;
+    if (z_out) {
+      z_out[i] = z0;
+      z_out[k + i] = z1;
+      z_out[2 * k + i] = z2;
+      continue;
+    }
+    const double diag = lam[i] + lambda_reg * sigma2;
+    if (!(diag > 0.0)) set_error(st, kDevSolveDiag, diag);
+    const double inv = 1.0 / diag;
+    coef[i] = z0 * inv;
+    coef[k + i] = z1 * inv;
+    coef[2 * k + i] = z2 * inv;
+    const double f = lam_num[i] * inv;
+    g4[i] = make_float4(static_cast<float>(z0 * f), static_cast<float>(z1 * f),
+                        static_cast<float>(z2 * f), 0.f);
+  }
+}
+
+RowdotPlan make_rowdot_plan(int64_t k, int64_t m, int64_t lda, int sm_count) {
+  RowdotPlan p;
+  p.g.rows = k;
+  p.g.cols = m;
+  p.g.lda = lda;
+  p.g.col_blocks = (m + kRdCols - 1) / kRdCols;
+  p.g.units = (k + kRdRows - 1) / kRdRows * p.g.col_blocks;
+  static bool attr = false;
+  if (!attr) {
+    FCPD_CUDA(cudaFuncSetAttribute(rowdot_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kRdSmem));
+    attr = true;
+  }
+  p.g.grid = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>(static_cast<int64_t>(sm_count), p.g.units)));
+  // slots per CTA: the row groups its range can touch (+1: a truncated
+  // geometry may cross one more boundary)
+  const int64_t per = (p.g.units + p.g.grid - 1) / p.g.grid;
+  p.g.kmax = static_cast<int>((per + p.g.col_blocks - 1) / p.g.col_blocks + 2);
+  return p;
+}
+
+size_t RowdotPlan::part_doubles() const {
+  return static_cast<size_t>(g.grid) * g.kmax * kRdSlot;
+}
+
+void launch_rowdot(const RowdotPlan& p, const float* qt, const float4* v, double* part,
+                   const IterState* st, uint64_t* stamps, int stamp_slot, cudaStream_t stream) {
+  launch_pdl(rowdot_bulk_kernel, dim3(p.g.grid), dim3(kBulkThreads), kRdSmem, stream, qt, v,
+             p.g, part, st, stamps, stamp_slot);
+  FCPD_LAUNCH_CHECK();
+}
+
+void launch_rowdot_reduce(const RowdotPlan& p, const double* part, int64_t k, const double* lam,
+                          const double* lam_num, double lambda_reg, double* coef, float4* g4,
+                          double* z_out, IterState* st, cudaStream_t stream) {
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(k * 32, 256), 148 * 2));
+  launch_pdl(rowdot_reduce_kernel, dim3(blocks), dim3(256), 0, stream, part, p.g, k, lam,
+             lam_num, lambda_reg, coef, g4, z_out, st);
+  FCPD_LAUNCH_CHECK();
+}
+
 // z_k = Σ partials; solve + filter (solvers.hpp:66-72):
 //   c_k = z_k / (λ_k + λ_reg σ²)   (W = Q c, kept for `coefficients`)
 //   g_k = λnum_k · c_k             (ΦW = Q g)

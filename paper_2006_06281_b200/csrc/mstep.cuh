@@ -30,6 +30,27 @@ struct ColsumPlan {
   }
 };
 
+// Row dot products z = Qᵀ·R over the contiguous (truncated) prefix of Qᵀ's
+// rows (mstep.cu rowdot_bulk_kernel): units of 8 rows × 1024 columns.
+struct RdGeom {
+  int64_t rows = 0, cols = 0, lda = 0;  // eigenvector rows, model columns, row stride
+  int64_t col_blocks = 0, units = 0;
+  int grid = 0, kmax = 0;
+  int trunc = 0;  // rows stop at IterState::keff
+};
+struct RowdotPlan {
+  RdGeom g;
+  size_t part_doubles() const;
+};
+RowdotPlan make_rowdot_plan(int64_t k, int64_t m, int64_t lda, int sm_count);
+void launch_rowdot(const RowdotPlan& p, const float* qt, const float4* v, double* part,
+                   const IterState* st, uint64_t* stamps, int stamp_slot, cudaStream_t stream);
+// z = Σ slots per eigenvector; with lam: c = z/(λ + λ_reg σ²), g = λnum·c;
+// with z_out (distributed): z itself, SoA 3×K, zeros past the streamed rows.
+void launch_rowdot_reduce(const RowdotPlan& p, const double* part, int64_t k, const double* lam,
+                          const double* lam_num, double lambda_reg, double* coef, float4* g4,
+                          double* z_out, IterState* st, cudaStream_t stream);
+
 // ctas_per_sm: resident bulk CTAs per SM the grid assumes (2 = whole GPU).
 ColsumPlan make_colsum_plan(int64_t rows, int64_t cols, int sm_count, int ctas_per_sm = 2);
 

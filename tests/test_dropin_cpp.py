@@ -52,3 +52,22 @@ def test_acceptance_criteria_4_to_7_on_gpu():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("PASS") == 4 and "FAIL" not in r.stdout
+
+
+def test_l2_program_compiles_and_links():
+    assert os.path.exists(build_dropin("test_l2_dropin"))
+
+
+@pytest.mark.gpu
+def test_reference_l2_unit_tests_on_gpu():
+    """proj/tests/test_correspondence.cpp, test_solvers.cpp (fast solvers)
+    and test_kernel.cpp restated against the drop-in header's L2 functions
+    (posterior, enforce_row_constraint, estimated_targets, build_gram,
+    eigendecompose, lowrank_reconstruction_error, the spectral cache,
+    solve_fast[_lowrank], apply_transform[_lowrank], update_sigma2,
+    normalize_pair), with the reference's tolerances, on the B200."""
+    exe = build_dropin("test_l2_dropin")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "FAIL" not in r.stdout

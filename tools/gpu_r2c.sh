@@ -1,0 +1,24 @@
+#!/bin/bash
+# Round-2 pass C: batched block fix-ups, culling policy, rowdot z-pass, L2 API.
+O=gpurun_out/r2c
+mkdir -p $O
+rm -f $O/parity.jsonl
+FCPD_PARITY_LOG=$O/parity.jsonl timeout 2400 python -m pytest tests -q -m gpu -rA --durations=30 > $O/pytest_gpu.txt 2>&1
+echo "pytest exit $?" >> $O/pytest_gpu.txt
+timeout 1200 python bench.py --steps 20 --warmup 5 > $O/bench_default.json 2> $O/bench_default.err
+for w in c0 c1 c2 c3 c4; do
+  timeout 900 python bench.py --workload $w --secondary none --warmup 5 --no-cpu --e2e-calls 1 > $O/bench_$w.json 2> $O/bench_$w.err
+done
+for w in c3 c4; do
+  FCPD_ZPASS=colsum timeout 900 python bench.py --workload $w --secondary none --warmup 5 --no-cpu --e2e-calls 0 > $O/bench_${w}_colsum.json 2> $O/bench_${w}_colsum.err
+done
+KSEL='regex:estep|mstep|colsum|rowdot|list_kernel|bbox|zreduce|transform_sigma|sigma_final|spectral_rank'
+CMD1="python bench.py --workload c1 --secondary none --steps 5 --warmup 3 --no-cpu --e2e-calls 0"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KSEL" -c 120 --csv --log-file $O/launches_c1.csv $CMD1 > $O/ncu_launch_c1.log 2>&1
+CMD4="python bench.py --workload c4 --secondary none --steps 100 --warmup 3 --no-cpu --e2e-calls 0"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KSEL" -c 1500 --csv --log-file $O/launches_c4.csv $CMD4 > $O/ncu_launch_c4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"estep_(row|col)_kernel|mstep_fused" -s 30 -c 3 -o $O/c1_full $CMD1 > $O/ncu_full_c1.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"estep_(row|col)_kernel|rowdot_bulk|colsum_bulk" -s 60 -c 4 -o $O/c4_full $CMD4 > $O/ncu_full_c4.log 2>&1
+tail -3 $O/pytest_gpu.txt; grep -E "^FAILED|Error" $O/pytest_gpu.txt | head -20
+for f in $O/bench_*.json; do echo "== $f"; cut -c1-200 $f; done
+tail -2 $O/ncu_full_c1.log $O/ncu_full_c4.log
