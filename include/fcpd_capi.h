@@ -136,6 +136,12 @@ FCPD_API int fcpd_nccl_unique_id(uint8_t* out128);
 FCPD_API int fcpd_create_dist(fcpd_ctx** out, int device, int rank, int world,
                               const uint8_t* id128);
 FCPD_API int fcpd_world(const fcpd_ctx* ctx, int32_t* rank, int32_t* world);
+/* A loopback group: `world` (≤ 8) virtual ranks on ONE device driven by one
+ * context — the scene-sharded data plane of fcpd_create_dist with the
+ * collectives as device kernels, for testing the multi-rank path on one GPU.
+ * fcpd_register / fcpd_session_begin on it take the FULL scene (split into
+ * `world` contiguous shards, rows [r·N/world, (r+1)·N/world)). */
+FCPD_API int fcpd_create_loopback(fcpd_ctx** out, int device, int world);
 
 /* register_pointsets — registration.hpp:79-175.  x: M×D model, y: N×D scene.
  * The spectral basis is cached in the context keyed by (normalised X, β,

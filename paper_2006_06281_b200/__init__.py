@@ -163,6 +163,7 @@ def lib():
             "fcpd_create_dist": (C.c_int, [C.POINTER(vp), C.c_int, C.c_int, C.c_int,
                                            C.c_char_p]),
             "fcpd_world": (C.c_int, [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+            "fcpd_create_loopback": (C.c_int, [C.POINTER(vp), C.c_int, C.c_int]),
             "fcpd_solve_fast_lowrank": (C.c_int, [vp, P, P, I64, I64, D, D, P, I64, I32, P]),
             "fcpd_apply_transform_lowrank": (C.c_int, [vp, P, I64, I32, P, I64, P, I64, P, I64,
                                                        I32, P]),
@@ -264,9 +265,13 @@ class Context:
     group (one process per GPU): register/session calls then take the full
     model and this rank's scene shard (see include/fcpd_capi.h)."""
 
-    def __init__(self, device: int = 0, *, _dist=None):
+    def __init__(self, device: int = 0, *, _dist=None, _loopback=None):
         self._h = C.c_void_p()
-        if _dist is None:
+        if _loopback is not None:
+            rc = lib().fcpd_create_loopback(C.byref(self._h), int(device), int(_loopback))
+            if rc != 0:
+                raise _CODES.get(rc, Error)(f"fcpd_create_loopback failed (code {rc})")
+        elif _dist is None:
             self._check(lib().fcpd_create(C.byref(self._h), int(device)))
         else:
             rank, world, uid = _dist
@@ -278,6 +283,13 @@ class Context:
     @classmethod
     def distributed(cls, device: int, rank: int, world: int, uid: bytes) -> "Context":
         return cls(device, _dist=(rank, world, uid))
+
+    @classmethod
+    def loopback(cls, device: int, world: int) -> "Context":
+        """`world` virtual ranks of the scene-sharded path on one device
+        (collectives as device kernels); register/session take the FULL
+        scene, split into contiguous shards."""
+        return cls(device, _loopback=world)
 
     @property
     def world(self):

@@ -17,11 +17,11 @@
 
 #include "common.cuh"
 #include "dist.cuh"
+#include "mstep.cuh"
 
 namespace fcpd {
 
 namespace {
-constexpr int kLanes = 8;
 
 __device__ __forceinline__ float sqdist_d(float4 a, float4 b) {
   const float dx = __fsub_rn(a.x, b.x);
@@ -85,7 +85,14 @@ __global__ void row_finalize_own_kernel(const double* __restrict__ sums_own, int
   const double* a = sums_own + i * 5;
   const bool flagged = !(a[0] >= static_cast<double>(n_global) * 0x1p-76);
   mask_own[i] = flagged ? 1 : 0;
-  if (flagged) return;
+  if (flagged) {
+    // the exact fallback fills this row later; until then it adds nothing
+    // to z (its contribution is the z correction), and it is counted for
+    // the group-wide "any row flagged" test
+    o.resid4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    atomicAdd(&st->flag_count[1], 1);
+    return;
+  }
   const double s = sqrt(kLog2e / (2.0 * st->sigma2_e));
   finalize_own(i, mr, log2(a[0]), a[0], a[1], a[2], a[3], a[4], xt64_own, s, o, ys, st);
 }
@@ -173,7 +180,8 @@ __global__ void fallback_finalize_own_kernel(const double* __restrict__ fsum_own
 
 // σ² block partials → one local double (fixed order).
 __global__ void sigma_local_sum_kernel(const double* __restrict__ sig_part, int blocks,
-                                       double* __restrict__ out, const IterState* st) {
+                                       double* __restrict__ out, float4* pack_dst,
+                                       const IterState* st) {
   if (!st->active) return;
   __shared__ double red[32];
   double s = 0.0;
@@ -184,8 +192,82 @@ __global__ void sigma_local_sum_kernel(const double* __restrict__ sig_part, int 
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < (blockDim.x >> 5); ++w) t += red[w];
-    out[0] = t;
+    if (out) out[0] = t;
+    if (pack_dst) {  // the rank's σ² partial rides in the unused .w of its first two x̃ rows
+      const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(t));
+      pack_dst[0].w = __uint_as_float(static_cast<unsigned>(b & 0xffffffffull));
+      pack_dst[1].w = __uint_as_float(static_cast<unsigned>(b >> 32));
+    }
   }
+}
+
+// σ² after the x̃ all-gather: the G rank partials (packed by
+// sigma_local_sum_kernel into .w of rows r·M_r, r·M_r + 1) summed in rank
+// order — the same value on every rank — then the iteration's last step.
+__global__ void sigma_final_gathered_kernel(const float4* __restrict__ xt4, int64_t mr, int world,
+                                            int64_t m_global, int d, int early_stop,
+                                            double* __restrict__ trace, IterState* st,
+                                            uint64_t* stamps) {
+  if (!st->active) return;
+  double tot = 0.0;
+  for (int r = 0; r < world; ++r) {
+    const unsigned lo = __float_as_uint(xt4[r * mr].w), hi = __float_as_uint(xt4[r * mr + 1].w);
+    tot += __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(hi) << 32) |
+                                                       lo));
+  }
+  finish_iteration_sigma(st, tot, m_global, d, early_stop, trace, stamps);
+}
+
+// z correction of the rows the exact fallback filled: Σ over flagged own
+// rows of Qᵀ_own[k][i]·R_i (one block per eigenvector, fixed-order tree).
+__global__ void zcorr_kernel(const float* __restrict__ qt_own, int64_t ld, int64_t k,
+                             const int32_t* __restrict__ mask_own, const float4* __restrict__ resid4,
+                             int64_t mr, double* __restrict__ zc, const IterState* st) {
+  if (!st->active) return;
+  __shared__ double red[3][32];
+  const int64_t kk = blockIdx.x;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int64_t i = threadIdx.x; i < mr; i += blockDim.x) {
+    if (!mask_own[i]) continue;
+    const double q = qt_own[kk * ld + i];
+    const float4 r = resid4[i];
+    a0 += q * r.x;
+    a1 += q * r.y;
+    a2 += q * r.z;
+  }
+  a0 = warp_sum(a0);
+  a1 = warp_sum(a1);
+  a2 = warp_sum(a2);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[0][w] = a0, red[1][w] = a1, red[2][w] = a2;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double s[3] = {0.0, 0.0, 0.0};
+  for (int c = 0; c < 3; ++c)
+    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) s[c] += red[c][i];
+  zc[kk] = s[0];
+  zc[k + kk] = s[1];
+  zc[2 * k + kk] = s[2];
+}
+
+__global__ void zadd_kernel(double* __restrict__ z, const double* __restrict__ zc, int64_t count,
+                            const IterState* st) {
+  if (!st->active) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count) z[i] += zc[i];
+}
+
+// the group-wide flagged-row count rides in z[3K] of the z all-reduce:
+// run the fallback exchange (a conditional graph node) only when nonzero
+__global__ void set_fallback_cond_kernel(cudaGraphConditionalHandle h,
+                                         const double* __restrict__ zfull, int64_t k,
+                                         const IterState* st) {
+  cudaGraphSetConditional(h, st->active && zfull[3 * k] > 0.5 ? 1u : 0u);
+}
+
+// rowdot_reduce's z all-reduce payload gets the local flagged-row count
+__global__ void put_flag_count_kernel(double* __restrict__ zfull, int64_t k, const IterState* st) {
+  zfull[3 * k] = st->active ? static_cast<double>(st->flag_count[1]) : 0.0;
 }
 
 // ------------------------------------------------------------------ launchers
@@ -217,9 +299,39 @@ void launch_fallback_finalize_own(const double* fsum_own, const float* gmax_own,
                                                                  xt64_own, o, ys, st);
   FCPD_LAUNCH_CHECK();
 }
-void launch_sigma_local_sum(const double* sig_part, int blocks, double* out, const IterState* st,
-                            cudaStream_t s) {
-  sigma_local_sum_kernel<<<1, 256, 0, s>>>(sig_part, blocks, out, st);
+void launch_sigma_local_sum(const double* sig_part, int blocks, double* out, float4* pack_dst,
+                            const IterState* st, cudaStream_t s) {
+  sigma_local_sum_kernel<<<1, 256, 0, s>>>(sig_part, blocks, out, pack_dst, st);
+  FCPD_LAUNCH_CHECK();
+}
+
+void launch_sigma_final_gathered(const float4* xt4, int64_t mr, int world, int64_t m_global, int d,
+                                 int early_stop, double* trace, IterState* st, uint64_t* stamps,
+                                 cudaStream_t s) {
+  sigma_final_gathered_kernel<<<1, 1, 0, s>>>(xt4, mr, world, m_global, d, early_stop, trace, st,
+                                              stamps);
+  FCPD_LAUNCH_CHECK();
+}
+
+void launch_zcorr(const float* qt_own, int64_t ld, int64_t k, const int32_t* mask_own,
+                  const float4* resid4, int64_t mr, double* zc, const IterState* st, cudaStream_t s) {
+  zcorr_kernel<<<static_cast<unsigned>(k), 256, 0, s>>>(qt_own, ld, k, mask_own, resid4, mr, zc, st);
+  FCPD_LAUNCH_CHECK();
+}
+
+void launch_zadd(double* z, const double* zc, int64_t count, const IterState* st, cudaStream_t s) {
+  zadd_kernel<<<ceil_div(count, 256), 256, 0, s>>>(z, zc, count, st);
+  FCPD_LAUNCH_CHECK();
+}
+
+void launch_set_fallback_cond(cudaGraphConditionalHandle h, const double* zfull, int64_t k,
+                              const IterState* st, cudaStream_t s) {
+  set_fallback_cond_kernel<<<1, 1, 0, s>>>(h, zfull, k, st);
+  FCPD_LAUNCH_CHECK();
+}
+
+void launch_put_flag_count(double* zfull, int64_t k, const IterState* st, cudaStream_t s) {
+  put_flag_count_kernel<<<1, 1, 0, s>>>(zfull, k, st);
   FCPD_LAUNCH_CHECK();
 }
 

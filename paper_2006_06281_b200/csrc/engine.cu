@@ -13,11 +13,13 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <thread>
 #include <vector>
 
+#include "comm.cuh"
 #include "common.cuh"
 #include "ctx.cuh"
 #include "dist.cuh"
@@ -218,7 +220,8 @@ struct Session {
   // (stride mr); xt4 holds all M_pad rows; y4b the local scene shard.
   bool dist = false;
   int64_t n_global = 0, m_pad = 0, mr = 0, m0 = 0, m_valid_own = 0, mr4 = 0;
-  DevBuf<double> rowsum_all, rowsum_own, fsum_all, fsum_own, zfull, sig_local, stage;
+  DevBuf<double> rowsum_all, rowsum_own, fsum_all, fsum_own, zfull, zcorr, sig_local, stage;
+  bool dist_conditional = false;  // the fallback exchange sits in a conditional graph node
   DevBuf<int32_t> mask_own, mask_all;
   DevBuf<float> fmax_all, qt_own;
 
@@ -236,7 +239,8 @@ struct Session {
       b->release();
     stamps.release();
     st.release();
-    for (auto* b : {&rowsum_all, &rowsum_own, &fsum_all, &fsum_own, &zfull, &sig_local, &stage})
+    for (auto* b : {&rowsum_all, &rowsum_own, &fsum_all, &fsum_own, &zfull, &zcorr, &sig_local,
+                    &stage})
       b->release();
     mask_own.release();
     mask_all.release();
@@ -268,12 +272,54 @@ struct fcpd_ctx {
   cublasHandle_t blas = nullptr;
   ncclComm_t comm = nullptr;  // set by fcpd_create_dist: scene-sharded EM over NCCL
   int rank = 0, world = 1;
+  // scene-sharded sessions: the collective backend (NCCL: this rank; loopback:
+  // every virtual rank) and, for a loopback group, its other ranks (owned)
+  std::unique_ptr<fcpd::Comm> comm_obj;
+  std::vector<fcpd_ctx*> loop_ranks;
   std::string err;
   fcpd::Basis basis;
   fcpd::Session sess;
 };
 
 namespace fcpd {
+namespace {
+// One rank per GPU (per process) over NCCL.
+struct NcclComm : Comm {
+  ncclComm_t c;
+  NcclComm(ncclComm_t cc, int w) : c(cc) { world = w; }
+  void reduce_scatter_sum(const std::vector<const double*>& send, const std::vector<double*>& recv,
+                          size_t count, cudaStream_t s) override {
+    FCPD_NCCL(ncclReduceScatter(send[0], recv[0], count, ncclDouble, ncclSum, c, s));
+  }
+  void all_reduce_sum(const std::vector<double*>& buf, size_t count, cudaStream_t s) override {
+    FCPD_NCCL(ncclAllReduce(buf[0], buf[0], count, ncclDouble, ncclSum, c, s));
+  }
+  void all_reduce_max(const std::vector<float*>& buf, size_t count, cudaStream_t s) override {
+    FCPD_NCCL(ncclAllReduce(buf[0], buf[0], count, ncclFloat, ncclMax, c, s));
+  }
+  void all_gather(const std::vector<const uint32_t*>& send, const std::vector<uint32_t*>& recv,
+                  size_t words, cudaStream_t s) override {
+    FCPD_NCCL(ncclAllGather(send[0], recv[0], words, ncclUint32, c, s));
+  }
+  void host_all_reduce(std::vector<std::vector<double>>& vals, bool max, cudaStream_t s) override {
+    std::vector<double>& v = vals[0];
+    double* d = nullptr;
+    FCPD_CUDA(cudaMalloc(&d, sizeof(double) * std::max<size_t>(v.size(), 1)));
+    FCPD_CUDA(cudaMemcpyAsync(d, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, s));
+    const ncclResult_t r = ncclAllReduce(d, d, v.size(), ncclDouble, max ? ncclMax : ncclSum, c, s);
+    cudaMemcpyAsync(v.data(), d, sizeof(double) * v.size(), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFree(d);
+    if (r != ncclSuccess)
+      throw Failure(FCPD_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+  }
+  // NCCL collectives are captured into the fallback's conditional node when
+  // the runtime accepts it (session_begin_group re-captures unconditionally
+  // otherwise)
+  bool conditional_ok() const override { return true; }
+};
+}  // namespace
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("FCPD_PDL");
@@ -832,7 +878,7 @@ void normalize_pair_host(const double* x, int64_t m, const double* y, int64_t n,
 
 void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n, int d,
                    const fcpd_config& cfg) {
-  if (ctx->comm) {
+  if (ctx->comm_obj) {
     session_begin_dist(ctx, x, m, y, n, d, cfg);
     return;
   }
@@ -1061,74 +1107,193 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
 }
 
 // ============================================================ distributed
-// One process per GPU; ctx->comm spans the ranks.  See dist.cu for the
-// sharding.  `y` passed to the dist session is this rank's scene shard;
-// `x` is the full model on every rank.
+// Scene-sharded EM.  A group is the ranks one process
+// drives: one rank per GPU over NCCL (ctx->comm_obj = NcclComm, the caller
+// passes the full model x and its scene shard y), or G virtual ranks on one
+// device (fcpd_create_loopback: LoopComm; the caller passes the full scene,
+// split here into G contiguous shards).  Every rank keeps the whole model
+// for the E-step, owns M_r = ⌈M/G⌉ model rows for the M-step, and its
+// scene shard.  Per iteration, in the common case, three collectives:
+//   reduce-scatter of the pass-2 row sums (5 doubles per row),
+//   all-reduce of z (3K doubles + the flagged-row count),
+//   all-gather of x̃ (float4 per row; the σ² partials ride in .w),
+// plus, only when some row's global mass is too small for the fp32 fast
+// path, the exact fallback exchange under a conditional graph node.
 
-void host_allreduce(fcpd_ctx* ctx, double* vals, int count, ncclRedOp_t op) {
-  DevBuf<double> d;
-  d.ensure(count);
-  FCPD_CUDA(cudaMemcpyAsync(d.p, vals, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
-  FCPD_NCCL(ncclAllReduce(d.p, d.p, count, ncclDouble, op, ctx->comm, ctx->stream));
-  FCPD_CUDA(cudaMemcpyAsync(vals, d.p, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
-  FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
-  d.release();
+std::vector<fcpd_ctx*> group_ranks(fcpd_ctx* lead) {
+  std::vector<fcpd_ctx*> r{lead};
+  for (fcpd_ctx* c : lead->loop_ranks) r.push_back(c);
+  return r;
 }
 
-void enqueue_iteration_dist(fcpd_ctx* ctx, Session& s) {
-  Basis& b = ctx->basis;
-  IterState* st = s.st.p;
-  cudaStream_t str = ctx->stream;
-  ncclComm_t comm = ctx->comm;
-  const int64_t m = s.m, nl = s.n;
-  const EStepBuffers eb = estep_buffers(s, nullptr, false, s.rowsum_all.p);
-  launch_estep_pass1(s.ep, eb, m, nl, st, str);  // column-local: no communication
-  launch_estep_pass2(s.ep, eb, m, nl, st, str);  // row sums of the local columns (AoS)
-  FCPD_NCCL(ncclReduceScatter(s.rowsum_all.p, s.rowsum_own.p, s.mr * 5, ncclDouble, ncclSum,
-                              comm, str));
-  const DistRowOut o{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p, s.resid4.p, s.x0.p};
-  launch_row_finalize_own(s.rowsum_own.p, s.mr, s.m_valid_own, s.n_global, s.xt64.p, o, s.ystats,
-                          s.mask_own.p, st, str);
-  // exact fallback for rows of tiny global mass (max + shifted sums)
-  FCPD_NCCL(ncclAllGather(s.mask_own.p, s.mask_all.p, s.mr, ncclInt32, comm, str));
-  launch_fallback_max(s.mask_all.p, s.m_pad, s.xt4.p, s.y4b.p, nl, s.fmax_all.p, st, str);
-  FCPD_NCCL(ncclAllReduce(s.fmax_all.p, s.fmax_all.p, s.m_pad, ncclFloat, ncclMax, comm, str));
-  launch_fallback_sum(s.mask_all.p, s.m_pad, s.fmax_all.p, s.xt4.p, s.y4b.p, nl, s.fsum_all.p, st,
-                      str);
-  FCPD_NCCL(ncclReduceScatter(s.fsum_all.p, s.fsum_own.p, s.mr * 5, ncclDouble, ncclSum, comm,
-                              str));
-  launch_fallback_finalize_own(s.fsum_own.p, s.fmax_all.p + s.m0, s.mask_own.p, s.mr, s.xt64.p, o,
-                               s.ystats, st, str);
-  // M-step on the own row shard of the basis
-  if (s.zp.trunc)
-    launch_spectral_rank(b.lam, b.lam + b.k, b.k, s.cfg.lambda_reg, s.tau, st, str);
-  if (s.rowdot) {  // over this rank's columns of Qᵀ (compact copy)
-    launch_rowdot(s.zr, s.qt_own.p, s.resid4.p, s.zpart.p, st, s.stamps.p, 1, str);
-    launch_rowdot_reduce(s.zr, s.zpart.p, b.k, nullptr, nullptr, 0.0, nullptr, nullptr,
-                         s.zfull.p, st, str);
-  } else {
-    launch_colsum(s.zp, b.q + s.m0 * b.kpad, b.kpad, s.resid4.p, s.zpart.p, st, s.stamps.p, 1,
-                  str);
-    launch_zsum(s.zp, s.zpart.p, s.zfull.p, st, str);
+// per-rank own-row views of the distributed E-step outputs
+DistRowOut dist_out(Session& s) {
+  return DistRowOut{s.ptilde_y.p, s.var.p, s.log2p1.p, s.degenerate.p, s.resid4.p, s.x0.p};
+}
+
+template <typename T, typename F>
+std::vector<T> per_rank(const std::vector<fcpd_ctx*>& R, F f) {
+  std::vector<T> v;
+  for (fcpd_ctx* c : R) v.push_back(f(c->sess));
+  return v;
+}
+
+// The exact fallback for rows of tiny global mass: the flagged rows' max L
+// over all columns (all-reduce MAX), the shifted fp64 sums over each rank's
+// columns (reduce-scatter), their finalisation, and their z contribution.
+void enqueue_fallback(const std::vector<fcpd_ctx*>& R, Comm& comm, cudaStream_t str) {
+  const int64_t k = R[0]->basis.k;
+  comm.all_gather(per_rank<const uint32_t*>(R, [](Session& s) {
+                    return reinterpret_cast<const uint32_t*>(s.mask_own.p); }),
+                  per_rank<uint32_t*>(R, [](Session& s) {
+                    return reinterpret_cast<uint32_t*>(s.mask_all.p); }),
+                  static_cast<size_t>(R[0]->sess.mr), str);
+  for (fcpd_ctx* c : R) {
+    Session& s = c->sess;
+    launch_fallback_max(s.mask_all.p, s.m_pad, s.xt4.p, s.y4b.p, s.n, s.fmax_all.p, s.st.p, str);
   }
-  FCPD_NCCL(ncclAllReduce(s.zfull.p, s.zfull.p, 3 * b.k, ncclDouble, ncclSum, comm, str));
-  launch_zfilter(s.zfull.p, b.k, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.coef.p, s.g4.p, st, str);
-  launch_colsum(s.vp, s.qt_own.p, s.mr4, s.g4.p, s.vpart.p, st, nullptr, 0, str);
-  const int nb = launch_transform_rows(s.vp, s.vpart.p, s.m_valid_own, s.x0.p, s.xt64.p,
-                                       s.xt_prev.p, s.xt4.p + s.m0, s.ptilde_y.p, s.var.p,
-                                       s.sig_part.p, st, s.stamps.p, str);
-  launch_sigma_local_sum(s.sig_part.p, nb, s.sig_local.p, st, str);
-  FCPD_NCCL(ncclAllReduce(s.sig_local.p, s.sig_local.p, 1, ncclDouble, ncclSum, comm, str));
-  launch_sigma_final(s.sig_local.p, 1, m, s.d, s.cfg.early_stop, s.trace.p, st, s.stamps.p, str);
-  FCPD_NCCL(ncclAllGather(s.xt4.p + s.m0, s.xt4.p, s.mr * 4, ncclFloat, comm, str));
+  comm.all_reduce_max(per_rank<float*>(R, [](Session& s) { return s.fmax_all.p; }),
+                      static_cast<size_t>(R[0]->sess.m_pad), str);
+  for (fcpd_ctx* c : R) {
+    Session& s = c->sess;
+    launch_fallback_sum(s.mask_all.p, s.m_pad, s.fmax_all.p, s.xt4.p, s.y4b.p, s.n, s.fsum_all.p,
+                        s.st.p, str);
+  }
+  comm.reduce_scatter_sum(per_rank<const double*>(R, [](Session& s) { return s.fsum_all.p; }),
+                          per_rank<double*>(R, [](Session& s) { return s.fsum_own.p; }),
+                          static_cast<size_t>(5 * R[0]->sess.mr), str);
+  for (fcpd_ctx* c : R) {
+    Session& s = c->sess;
+    launch_fallback_finalize_own(s.fsum_own.p, s.fmax_all.p + s.m0, s.mask_own.p, s.mr, s.xt64.p,
+                                 dist_out(s), s.ystats, s.st.p, str);
+    launch_zcorr(s.qt_own.p, s.mr4, k, s.mask_own.p, s.resid4.p, s.mr, s.zcorr.p, s.st.p, str);
+  }
+  comm.all_reduce_sum(per_rank<double*>(R, [](Session& s) { return s.zcorr.p; }),
+                      static_cast<size_t>(3 * k), str);
+  for (fcpd_ctx* c : R) launch_zadd(c->sess.zfull.p, c->sess.zcorr.p, 3 * k, c->sess.st.p, str);
 }
 
-void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n,
-                        int d, const fcpd_config& cfg) {
-  validate_register(x, m, y, n, d, cfg);
-  const auto t0 = Clock::now();
-  Session& s = ctx->sess;
-  cudaStream_t str = ctx->stream;
+// Enqueue `body` under a device-side predicate (a conditional IF node in the
+// graph being captured on `str`).  Throws if capture into the body fails;
+// the caller then re-captures with the body unconditional.
+void enqueue_if(cudaStream_t str, const std::function<void(cudaGraphConditionalHandle)>& set_pred,
+                const std::function<void(cudaStream_t)>& body) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t graph = nullptr;
+  FCPD_CUDA(cudaStreamGetCaptureInfo(str, &cs, nullptr, &graph, nullptr, nullptr));
+  if (cs != cudaStreamCaptureStatusActive) throw Failure(FCPD_ERR_CUDA, "enqueue_if: not capturing");
+  cudaGraphConditionalHandle h;
+  FCPD_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault));
+  set_pred(h);
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  FCPD_CUDA(cudaStreamGetCaptureInfo(str, &cs, nullptr, &graph, &deps, &ndeps));
+  cudaGraphNodeParams p{};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeIf;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  FCPD_CUDA(cudaGraphAddNode(&node, graph, deps, ndeps, &p));
+  cudaGraph_t body_graph = p.conditional.phGraph_out[0];
+  cudaStream_t bs = nullptr;
+  FCPD_CUDA(cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking));
+  try {
+    FCPD_CUDA(cudaStreamBeginCaptureToGraph(bs, body_graph, nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeRelaxed));
+    body(bs);
+    cudaGraph_t out = nullptr;
+    FCPD_CUDA(cudaStreamEndCapture(bs, &out));
+  } catch (...) {
+    cudaGraph_t out = nullptr;
+    cudaStreamEndCapture(bs, &out);
+    cudaStreamDestroy(bs);
+    throw;
+  }
+  cudaStreamDestroy(bs);
+  FCPD_CUDA(cudaStreamUpdateCaptureDependencies(str, &node, 1, cudaStreamSetCaptureDependencies));
+}
+
+void enqueue_iteration_group(fcpd_ctx* lead, cudaStream_t str, bool conditional) {
+  const std::vector<fcpd_ctx*> R = group_ranks(lead);
+  Comm& comm = *lead->comm_obj;
+  Session& s0 = lead->sess;
+  const int64_t k = lead->basis.k;
+  // E-step: pass 1 is column-local; pass 2 leaves per-row sums of the local
+  // columns (AoS [M_pad][5])
+  for (fcpd_ctx* c : R) {
+    Session& s = c->sess;
+    const EStepBuffers eb = estep_buffers(s, nullptr, false, s.rowsum_all.p);
+    launch_estep_pass1(s.ep, eb, s.m, s.n, s.st.p, str);
+    launch_estep_pass2(s.ep, eb, s.m, s.n, s.st.p, str);
+  }
+  comm.reduce_scatter_sum(per_rank<const double*>(R, [](Session& s) { return s.rowsum_all.p; }),
+                          per_rank<double*>(R, [](Session& s) { return s.rowsum_own.p; }),
+                          static_cast<size_t>(5 * s0.mr), str);
+  // own rows: finalise (flagged rows queued, zero residual), z partial over
+  // the own columns of Qᵀ, the local flagged count in z[3K]
+  for (fcpd_ctx* c : R) {
+    Session& s = c->sess;
+    Basis& b = c->basis;
+    IterState* st = s.st.p;
+    launch_row_finalize_own(s.rowsum_own.p, s.mr, s.m_valid_own, s.n_global, s.xt64.p,
+                            dist_out(s), s.ystats, s.mask_own.p, st, str);
+    if (s.zp.trunc)
+      launch_spectral_rank(b.lam, b.lam + b.k, b.k, s.cfg.lambda_reg, s.tau, st, str);
+    if (s.rowdot) {
+      launch_rowdot(s.zr, s.qt_own.p, s.resid4.p, s.zpart.p, st, s.stamps.p, 1, str);
+      launch_rowdot_reduce(s.zr, s.zpart.p, b.k, nullptr, nullptr, 0.0, nullptr, nullptr,
+                           s.zfull.p, st, str);
+    } else {
+      launch_colsum(s.zp, b.q + s.m0 * b.kpad, b.kpad, s.resid4.p, s.zpart.p, st, s.stamps.p, 1,
+                    str);
+      launch_zsum(s.zp, s.zpart.p, s.zfull.p, st, str);
+    }
+    launch_put_flag_count(s.zfull.p, b.k, st, str);
+  }
+  comm.all_reduce_sum(per_rank<double*>(R, [](Session& s) { return s.zfull.p; }),
+                      static_cast<size_t>(3 * k + 1), str);
+  if (conditional) {
+    enqueue_if(
+        str,
+        [&](cudaGraphConditionalHandle h) {
+          launch_set_fallback_cond(h, s0.zfull.p, k, s0.st.p, str);
+        },
+        [&](cudaStream_t bs) { enqueue_fallback(R, comm, bs); });
+  } else {
+    enqueue_fallback(R, comm, str);
+  }
+  // filter, V over the own rows, transform, σ² partial packed into x̃'s .w
+  for (fcpd_ctx* c : R) {
+    Session& s = c->sess;
+    Basis& b = c->basis;
+    IterState* st = s.st.p;
+    launch_zfilter(s.zfull.p, b.k, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.coef.p, s.g4.p, st, str);
+    launch_colsum(s.vp, s.qt_own.p, s.mr4, s.g4.p, s.vpart.p, st, nullptr, 0, str);
+    const int nb = launch_transform_rows(s.vp, s.vpart.p, s.m_valid_own, s.x0.p, s.xt64.p,
+                                         s.xt_prev.p, s.xt4.p + s.m0, s.ptilde_y.p, s.var.p,
+                                         s.sig_part.p, st, s.stamps.p, str);
+    launch_sigma_local_sum(s.sig_part.p, nb, nullptr, s.xt4.p + s.m0, st, str);
+  }
+  comm.all_gather(per_rank<const uint32_t*>(R, [](Session& s) {
+                    return reinterpret_cast<const uint32_t*>(s.xt4.p + s.m0); }),
+                  per_rank<uint32_t*>(R, [](Session& s) {
+                    return reinterpret_cast<uint32_t*>(s.xt4.p); }),
+                  static_cast<size_t>(4 * s0.mr), str);
+  for (fcpd_ctx* c : R) {
+    Session& s = c->sess;
+    launch_sigma_final_gathered(s.xt4.p, s.mr, comm.world, s.m, s.d, s.cfg.early_stop,
+                                s.trace.p, s.st.p, s.stamps.p, str);
+  }
+}
+
+// One rank's session state for its scene shard (normalised, SoA 3×n);
+// xs/y statistics are the group's.
+void prepare_rank(fcpd_ctx* c, int rank, int world, const std::vector<double>& xs_in, int64_t m,
+                  std::vector<double> ys, int64_t n, int64_t n_global, const YStats& ystats,
+                  int d, const fcpd_config& cfg, double sigma2_initial) {
+  Session& s = c->sess;
+  cudaStream_t str = c->stream;
   s.ready = false;
   s.dist = true;
   s.h2d = s.d2h = 0;
@@ -1136,89 +1301,33 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
   s.n = n;
   s.d = d;
   s.cfg = cfg;
-  const int G = ctx->world, R = ctx->rank;
-  if (m < G) throw Failure(FCPD_ERR_PARAMETER, "register: fewer model points than ranks");
-  // global scene size and normalize_pair statistics (pointset.hpp:124-148)
-  double red[5] = {static_cast<double>(n), 0, 0, 0, 0};
-  for (int c = 0; c < d; ++c)
-    for (int64_t i = 0; i < n; ++i) red[1 + c] += y[c * n + i];
-  host_allreduce(ctx, red, 4, ncclSum);
-  s.n_global = static_cast<int64_t>(red[0]);
-  std::vector<double> xs(3 * m, 0.0), ys(3 * n, 0.0);
-  s.center[0] = s.center[1] = s.center[2] = 0.0;
-  s.scale = 1.0;
-  if (cfg.normalize) {
-    const double total = static_cast<double>(m + s.n_global);
-    for (int c = 0; c < d; ++c) {
-      double sx = 0.0;
-      for (int64_t i = 0; i < m; ++i) sx += x[c * m + i];
-      s.center[c] = (sx + red[1 + c]) / total;
-    }
-    double sc = 0.0;
-    for (int c = 0; c < d; ++c) {
-      for (int64_t i = 0; i < m; ++i) sc = std::max(sc, std::fabs(x[c * m + i] - s.center[c]));
-      for (int64_t i = 0; i < n; ++i) sc = std::max(sc, std::fabs(y[c * n + i] - s.center[c]));
-    }
-    host_allreduce(ctx, &sc, 1, ncclMax);
-    if (sc <= 0.0) sc = 1.0;
-    s.scale = sc;
-    for (int c = 0; c < d; ++c) {
-      for (int64_t i = 0; i < m; ++i) xs[c * m + i] = (x[c * m + i] - s.center[c]) / sc;
-      for (int64_t i = 0; i < n; ++i) ys[c * n + i] = (y[c * n + i] - s.center[c]) / sc;
-    }
-  } else {
-    for (int c = 0; c < d; ++c) {
-      std::memcpy(&xs[c * m], x + c * m, sizeof(double) * m);
-      std::memcpy(&ys[c * n], y + c * n, sizeof(double) * n);
-    }
-  }
-  // global scene statistics of the normalised scene
-  double ystat[4] = {0, 0, 0, 0};
-  for (int c = 0; c < 3; ++c)
-    for (int64_t i = 0; i < n; ++i) ystat[c] += ys[c * n + i];
-  for (int64_t i = 0; i < n; ++i)
-    ystat[3] += ys[i] * ys[i] + ys[n + i] * ys[n + i] + ys[2 * n + i] * ys[2 * n + i];
-  host_allreduce(ctx, ystat, 4, ncclSum);
-  const double ng = static_cast<double>(s.n_global);
-  for (int c = 0; c < 3; ++c) s.ystats.mean[c] = ystat[c] / ng;
-  s.ystats.sq_mean = ystat[3] / ng;
-  // init_sigma2 (registration.hpp:59-69) from the global statistics
-  {
-    double fx = 0.0, dot = 0.0;
-    for (int c = 0; c < d; ++c) {
-      double sx = 0.0;
-      for (int64_t i = 0; i < m; ++i) {
-        fx += xs[c * m + i] * xs[c * m + i];
-        sx += xs[c * m + i];
-      }
-      dot += sx * ystat[c];
-    }
-    const double md = static_cast<double>(m);
-    s.sigma2_initial =
-        std::max((md * ystat[3] + ng * fx - 2.0 * dot) / (static_cast<double>(d) * md * ng), 0.0);
-  }
+  s.n_global = n_global;
+  s.ystats = ystats;
+  s.sigma2_initial = sigma2_initial;
+  if (m < world) throw Failure(FCPD_ERR_PARAMETER, "register: fewer model points than ranks");
   // internal spatial order: the full model (identical on all ranks) and the
-  // local scene shard are spatially sorted; row shards are spatial slabs
-  s.perm_x = spatial_sort_cached(xs, m, ctx->sort_x);
-  s.perm_y = spatial_sort_cached(ys, n, ctx->sort_y);
-  // spectral basis (computed redundantly per rank; each keeps its row shard)
+  // local scene shard; row shards are spatial slabs
+  std::vector<double> xs = xs_in;
+  s.perm_x = spatial_sort_cached(xs, m, c->sort_x);
+  s.perm_y = spatial_sort_cached(ys, n, c->sort_y);
+  // spectral basis (each rank keeps its row shard of it)
   s.x0.ensure(3 * m);
   FCPD_CUDA(cudaMemcpyAsync(s.x0.p, xs.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, str));
-  ensure_basis(ctx, s, xs);
-  ctx->basis.perm = s.perm_x;  // basis rows are in the session's sorted order
-  Basis& b = ctx->basis;
+  ensure_basis(c, s, xs);
+  c->basis.perm = s.perm_x;
+  Basis& b = c->basis;
   // shard geometry
-  s.mr = (m + G - 1) / G;
-  s.m_pad = s.mr * G;
-  s.m0 = s.mr * R;
+  s.mr = (m + world - 1) / world;
+  s.m_pad = s.mr * world;
+  s.m0 = s.mr * rank;
   s.m_valid_own = std::max<int64_t>(0, std::min<int64_t>(s.mr, m - s.m0));
   if (s.m_valid_own < 1) throw Failure(FCPD_ERR_PARAMETER, "register: empty model shard");
+  if (s.mr < 2) throw Failure(FCPD_ERR_PARAMETER, "register: fewer than 2 model rows per rank");
   s.mr4 = (s.mr + 3) / 4 * 4;
   const int64_t mr = s.mr;
-  // own-row SoA arrays (stride mr)
   std::vector<double> own(3 * mr, 0.0);
-  for (int c = 0; c < 3; ++c)
-    for (int64_t i = 0; i < s.m_valid_own; ++i) own[c * mr + i] = xs[c * m + s.m0 + i];
+  for (int cc = 0; cc < 3; ++cc)
+    for (int64_t i = 0; i < s.m_valid_own; ++i) own[cc * mr + i] = xs[cc * m + s.m0 + i];
   s.release_graph();
   s.x0.ensure(3 * mr);
   s.xt64.ensure(3 * mr);
@@ -1231,7 +1340,8 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
   FCPD_CUDA(cudaMemcpyAsync(s.x0.p, own.data(), sizeof(double) * 3 * mr, cudaMemcpyHostToDevice, str));
   FCPD_CUDA(cudaMemcpyAsync(s.xt64.p, s.x0.p, sizeof(double) * 3 * mr, cudaMemcpyDeviceToDevice, str));
   FCPD_CUDA(cudaMemcpyAsync(s.xt_prev.p, s.x0.p, sizeof(double) * 3 * mr, cudaMemcpyDeviceToDevice, str));
-  // full model (float4, padded) and local scene
+  FCPD_CUDA(cudaMemsetAsync(s.resid4.p, 0, sizeof(float4) * mr, str));
+  // full model (float4, padded far away) and the local scene
   std::vector<float4> x4(s.m_pad, make_float4(3.0e18f, 3.0e18f, 3.0e18f, 0.f)), y4(n);
   for (int64_t i = 0; i < m; ++i)
     x4[i] = make_float4(static_cast<float>(xs[i]), static_cast<float>(xs[m + i]),
@@ -1245,7 +1355,7 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
   FCPD_CUDA(cudaMemcpyAsync(s.y4b.p, y4.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, str));
   s.h2d += (sizeof(double) * 3 + sizeof(float4)) * (m + n);
   // E-step scratch over all M rows / local columns
-  s.ep = make_estep_plan(m, n, ctx->sm_count);
+  s.ep = make_estep_plan(m, n, c->sm_count);
   s.b2.ensure(n);
   s.pt1.ensure(n);
   s.col_flags.ensure(n);
@@ -1259,8 +1369,7 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
   s.mask_own.ensure(mr);
   s.mask_all.ensure(s.m_pad);
   s.fmax_all.ensure(s.m_pad);
-  // segment partials, work lists, culling geometry (model tiles over all M
-  // rows; local scene tiles)
+  FCPD_CUDA(cudaMemsetAsync(s.mask_own.p, 0, sizeof(int32_t) * mr, str));
   alloc_estep(s, m, n, str);
   // basis shard: Q rows [m0, m0+m_valid) in place; Qᵀ columns copied compact
   s.qt_own.ensure(static_cast<size_t>(b.k) * s.mr4);
@@ -1270,10 +1379,10 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
     FCPD_CUDA(cudaMemcpy2DAsync(s.qt_own.p, sizeof(float) * s.mr4, b.qt + s.m0,
                                 sizeof(float) * b.mpad, sizeof(float) * cols, b.k,
                                 cudaMemcpyDeviceToDevice, str));
-  s.zp = make_colsum_plan(s.m_valid_own, b.k, ctx->sm_count);
-  s.vp = make_colsum_plan(b.k, mr, ctx->sm_count);
-  // spectral truncation as on one GPU (the cut is the same on every rank:
-  // it depends only on λ and the all-reduced σ²)
+  s.zp = make_colsum_plan(s.m_valid_own, b.k, c->sm_count);
+  s.vp = make_colsum_plan(b.k, mr, c->sm_count);
+  // spectral truncation as on one GPU (the same cut on every rank: it
+  // depends only on λ and the σ² every rank computes identically)
   s.tau = s.cfg.spectral_tau;
   if (4.0 * static_cast<double>(m) * static_cast<double>(b.k) < 64.0 * (1 << 20)) s.tau = 0.0;
   if (const char* e = std::getenv("FCPD_SPECTRAL_TAU")) s.tau = std::atof(e);
@@ -1282,71 +1391,218 @@ void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double*
   {
     const char* zpass = std::getenv("FCPD_ZPASS");
     s.rowdot = !(zpass && std::string(zpass) == "colsum");
-    s.zr = make_rowdot_plan(b.k, s.m_valid_own, s.mr4, ctx->sm_count);
+    s.zr = make_rowdot_plan(b.k, s.m_valid_own, s.mr4, c->sm_count);
     s.zr.g.trunc = s.zp.trunc;
   }
   s.zpart.ensure(std::max(s.zp.part_doubles(), s.rowdot ? s.zr.part_doubles() : size_t(0)));
   s.vpart.ensure(s.vp.part_doubles());
-  s.zfull.ensure(3 * b.k);
+  s.zfull.ensure(3 * b.k + 1);
+  s.zcorr.ensure(3 * b.k);
   s.coef.ensure(3 * b.k);
-  s.g4.ensure(b.k);
+  s.g4.ensure(b.kpad);
   s.sig_part.ensure(transform_sigma_blocks(mr));
   s.sig_local.ensure(1);
   s.st.ensure(1);
   s.capacity = std::max(cfg.iterations, 1);
   s.trace.ensure(s.capacity);
   s.stamps.ensure(4 * static_cast<size_t>(s.capacity));
-  if (cfg.iterations > 0 && !(cfg.omega >= 0.0 && cfg.omega < 1.0))
-    throw Failure(FCPD_ERR_NUMERIC, "register: iteration 0: posterior: omega must lie in [0, 1)");
-  reset_state(ctx, s, s.sigma2_initial);
+  reset_state(c, s, sigma2_initial);
   FCPD_CUDA(cudaMemsetAsync(s.coef.p, 0, sizeof(double) * 3 * b.k, str));
   FCPD_CUDA(cudaStreamSynchronize(str));
-
-  cudaGraph_t g = nullptr;
-  FCPD_CUDA(cudaStreamBeginCapture(str, cudaStreamCaptureModeThreadLocal));
-  try {
-    enqueue_iteration_dist(ctx, s);
-  } catch (...) {
-    cudaStreamEndCapture(str, &g);
-    if (g) cudaGraphDestroy(g);
-    throw;
-  }
-  FCPD_CUDA(cudaStreamEndCapture(str, &g));
-  cudaGraphExec_t exec = nullptr;
-  const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
-  cudaGraphDestroy(g);
-  FCPD_CUDA(ie);
-  s.graph = exec;
-  s.t_setup_host = since(t0);
-  s.launched = 0;
-  s.ready = true;
 }
 
-// gather the own-row SoA blocks (stride mr) of every rank into a full SoA M×d
-void gather_rows(fcpd_ctx* ctx, Session& s, const double* own, double* out_full, int d) {
-  const int G = ctx->world;
-  s.stage.ensure(static_cast<size_t>(3) * s.mr * G);
-  FCPD_NCCL(ncclAllGather(own, s.stage.p, 3 * s.mr, ncclDouble, ctx->comm, ctx->stream));
-  std::vector<double> h(static_cast<size_t>(3) * s.mr * G);
-  FCPD_CUDA(cudaMemcpyAsync(h.data(), s.stage.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-  FCPD_CUDA(cudaStreamSynchronize(ctx->stream));
-  s.d2h += sizeof(double) * 3 * s.mr;
+// shards: per local rank, (pointer to its SoA scene shard, count)
+void session_begin_group(fcpd_ctx* lead, const double* x, int64_t m,
+                         const std::vector<std::pair<const double*, int64_t>>& shards, int d,
+                         const fcpd_config& cfg) {
+  const std::vector<fcpd_ctx*> R = group_ranks(lead);
+  Comm& comm = *lead->comm_obj;
+  const int G = comm.world;
+  const auto t0 = Clock::now();
+  for (size_t i = 0; i < R.size(); ++i)
+    validate_register(x, m, shards[i].first, shards[i].second, d, cfg);
+  // global scene size and normalize_pair statistics (pointset.hpp:124-148)
+  std::vector<std::vector<double>> red(R.size(), std::vector<double>(4, 0.0));
+  for (size_t i = 0; i < R.size(); ++i) {
+    const double* y = shards[i].first;
+    const int64_t n = shards[i].second;
+    red[i][0] = static_cast<double>(n);
+    for (int c = 0; c < d; ++c)
+      for (int64_t j = 0; j < n; ++j) red[i][1 + c] += y[c * n + j];
+  }
+  comm.host_all_reduce(red, false, lead->stream);
+  const int64_t n_global = static_cast<int64_t>(red[0][0]);
+  double center[3] = {0.0, 0.0, 0.0}, scale = 1.0;
+  if (cfg.normalize) {
+    const double total = static_cast<double>(m + n_global);
+    for (int c = 0; c < d; ++c) {
+      double sx = 0.0;
+      for (int64_t j = 0; j < m; ++j) sx += x[c * m + j];
+      center[c] = (sx + red[0][1 + c]) / total;
+    }
+    std::vector<std::vector<double>> sc(R.size(), std::vector<double>(1, 0.0));
+    for (size_t i = 0; i < R.size(); ++i) {
+      const double* y = shards[i].first;
+      const int64_t n = shards[i].second;
+      double v = 0.0;
+      for (int c = 0; c < d; ++c) {
+        for (int64_t j = 0; j < m; ++j) v = std::max(v, std::fabs(x[c * m + j] - center[c]));
+        for (int64_t j = 0; j < n; ++j) v = std::max(v, std::fabs(y[c * n + j] - center[c]));
+      }
+      sc[i][0] = v;
+    }
+    comm.host_all_reduce(sc, true, lead->stream);
+    scale = sc[0][0] > 0.0 ? sc[0][0] : 1.0;
+  }
+  auto norm = [&](const double* p, int64_t cnt) {
+    std::vector<double> o(3 * cnt, 0.0);
+    for (int c = 0; c < d; ++c)
+      for (int64_t j = 0; j < cnt; ++j)
+        o[c * cnt + j] = cfg.normalize ? (p[c * cnt + j] - center[c]) / scale : p[c * cnt + j];
+    return o;
+  };
+  const std::vector<double> xs = norm(x, m);
+  std::vector<std::vector<double>> ys(R.size());
+  std::vector<std::vector<double>> yst(R.size(), std::vector<double>(4, 0.0));
+  for (size_t i = 0; i < R.size(); ++i) {
+    ys[i] = norm(shards[i].first, shards[i].second);
+    const int64_t n = shards[i].second;
+    for (int c = 0; c < 3; ++c)
+      for (int64_t j = 0; j < n; ++j) yst[i][c] += ys[i][c * n + j];
+    for (int64_t j = 0; j < n; ++j)
+      yst[i][3] += ys[i][j] * ys[i][j] + ys[i][n + j] * ys[i][n + j] +
+                   ys[i][2 * n + j] * ys[i][2 * n + j];
+  }
+  comm.host_all_reduce(yst, false, lead->stream);
+  const double ng = static_cast<double>(n_global);
+  YStats ystats{};
+  for (int c = 0; c < 3; ++c) ystats.mean[c] = yst[0][c] / ng;
+  ystats.sq_mean = yst[0][3] / ng;
+  // init_sigma2 (registration.hpp:59-69) from the global statistics
+  double sigma2_initial = 0.0;
+  {
+    double fx = 0.0, dot = 0.0;
+    for (int c = 0; c < d; ++c) {
+      double sx = 0.0;
+      for (int64_t j = 0; j < m; ++j) {
+        fx += xs[c * m + j] * xs[c * m + j];
+        sx += xs[c * m + j];
+      }
+      dot += sx * yst[0][c];
+    }
+    const double md = static_cast<double>(m);
+    sigma2_initial = std::max((md * yst[0][3] + ng * fx - 2.0 * dot) / (static_cast<double>(d) * md * ng), 0.0);
+  }
+  if (cfg.iterations > 0 && !(cfg.omega >= 0.0 && cfg.omega < 1.0))
+    throw Failure(FCPD_ERR_NUMERIC, "register: iteration 0: posterior: omega must lie in [0, 1)");
+  for (size_t i = 0; i < R.size(); ++i) {
+    const int rank = lead->loop_ranks.empty() ? lead->rank : static_cast<int>(i);
+    prepare_rank(R[i], rank, G, xs, m, ys[i], shards[i].second, n_global, ystats, d, cfg,
+                 sigma2_initial);
+    Session& s = R[i]->sess;
+    for (int c = 0; c < 3; ++c) s.center[c] = center[c];
+    s.scale = scale;
+  }
+  // one EM iteration of the whole group as a CUDA graph on the lead stream;
+  // the fallback exchange behind a conditional node where the backend
+  // allows it (else, or if capturing into the node fails, unconditional)
+  cudaStream_t str = lead->stream;
+  bool conditional = comm.conditional_ok();
+  if (const char* e = std::getenv("FCPD_DIST_CONDITIONAL")) conditional = std::atoi(e) != 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    cudaGraph_t g = nullptr;
+    FCPD_CUDA(cudaStreamBeginCapture(str, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_iteration_group(lead, str, conditional);
+    } catch (const Failure&) {
+      cudaStreamEndCapture(str, &g);
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      if (!conditional) throw;
+      conditional = false;  // retry with the fallback exchange unconditional
+      continue;
+    }
+    FCPD_CUDA(cudaStreamEndCapture(str, &g));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {
+      cudaGetLastError();
+      if (!conditional) FCPD_CUDA(ie);
+      conditional = false;
+      continue;
+    }
+    lead->sess.graph = exec;
+    break;
+  }
+  lead->sess.dist_conditional = conditional;
+  lead->sess.t_setup_host = since(t0);
+  lead->sess.launched = 0;
+  lead->sess.ready = true;
+}
+
+void session_begin_dist(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, int64_t n,
+                        int d, const fcpd_config& cfg) {
+  std::vector<std::pair<const double*, int64_t>> shards;
+  std::vector<std::vector<double>> store;
+  if (ctx->loop_ranks.empty()) {
+    shards.push_back({y, n});  // NCCL: this rank's scene shard
+  } else {
+    // loopback group: the full scene, split into contiguous shards as the
+    // NCCL callers do (bench.py: rows [r·N/G, (r+1)·N/G))
+    const int G = ctx->comm_obj->world;
+    if (n < G) throw Failure(FCPD_ERR_PARAMETER, "register: fewer scene points than ranks");
+    for (int r = 0; r < G; ++r) {
+      const int64_t a = r * n / G, b = (r + 1) * n / G;
+      std::vector<double> sh(static_cast<size_t>(d) * (b - a));
+      for (int c = 0; c < d; ++c)
+        std::memcpy(&sh[c * (b - a)], y + c * n + a, sizeof(double) * (b - a));
+      store.push_back(std::move(sh));
+    }
+    for (int r = 0; r < G; ++r)
+      shards.push_back({store[r].data(), (r + 1) * n / G - r * n / G});
+  }
+  session_begin_group(ctx, x, m, shards, d, cfg);
+}
+
+// gather the own-row SoA blocks (stride mr) of every rank into a full SoA
+// M×d on the host (every rank of the group takes part)
+void gather_rows(fcpd_ctx* lead, const std::function<const double*(Session&)>& own,
+                 double* out_full, int d) {
+  const std::vector<fcpd_ctx*> R = group_ranks(lead);
+  Comm& comm = *lead->comm_obj;
+  const int G = comm.world;
+  Session& s0 = lead->sess;
+  for (fcpd_ctx* c : R) c->sess.stage.ensure(static_cast<size_t>(3) * c->sess.mr * G);
+  comm.all_gather(per_rank<const uint32_t*>(R, [&](Session& s) {
+                    return reinterpret_cast<const uint32_t*>(own(s)); }),
+                  per_rank<uint32_t*>(R, [](Session& s) {
+                    return reinterpret_cast<uint32_t*>(s.stage.p); }),
+                  static_cast<size_t>(3 * s0.mr * 2), lead->stream);
+  std::vector<double> h(static_cast<size_t>(3) * s0.mr * G);
+  FCPD_CUDA(cudaMemcpyAsync(h.data(), s0.stage.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost,
+                            lead->stream));
+  FCPD_CUDA(cudaStreamSynchronize(lead->stream));
+  s0.d2h += sizeof(double) * 3 * s0.mr;
   for (int r = 0; r < G; ++r)
     for (int c = 0; c < d; ++c)
-      for (int64_t i = 0; i < s.mr; ++i) {
-        const int64_t row = r * s.mr + i;
-        if (row < s.m) out_full[c * s.m + row] = h[(static_cast<size_t>(r) * 3 + c) * s.mr + i];
+      for (int64_t i = 0; i < s0.mr; ++i) {
+        const int64_t row = r * s0.mr + i;
+        if (row < s0.m) out_full[c * s0.m + row] = h[(static_cast<size_t>(r) * 3 + c) * s0.mr + i];
       }
 }
 
 void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall) {
+  const std::vector<fcpd_ctx*> R = group_ranks(ctx);
+  Comm& comm = *ctx->comm_obj;
   Session& s = ctx->sess;
-  Basis& b = ctx->basis;
   cudaStream_t str = ctx->stream;
-  IterState h{};
-  FCPD_CUDA(cudaMemcpyAsync(&h, s.st.p, sizeof h, cudaMemcpyDeviceToHost, str));
+  std::vector<IterState> hs(R.size());
+  for (size_t i = 0; i < R.size(); ++i)
+    FCPD_CUDA(cudaMemcpyAsync(&hs[i], R[i]->sess.st.p, sizeof(IterState), cudaMemcpyDeviceToHost,
+                              str));
   FCPD_CUDA(cudaStreamSynchronize(str));
+  const IterState& h = hs[0];
   if (h.err_code != 0) {
     char buf[64];
     std::snprintf(buf, sizeof buf, "%f", h.err_value);
@@ -1355,25 +1611,26 @@ void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall) {
                                  : std::string("update_sigma2: negative variance ") + buf;
     throw Failure(FCPD_ERR_NUMERIC, "register: iteration " + std::to_string(h.err_iter) + ": " + what);
   }
-  double deg = static_cast<double>(h.degenerate_rows);
-  host_allreduce(ctx, &deg, 1, ncclSum);  // own-row counts → global
+  std::vector<std::vector<double>> deg(R.size(), std::vector<double>(1, 0.0));
+  for (size_t i = 0; i < R.size(); ++i) deg[i][0] = static_cast<double>(hs[i].degenerate_rows);
+  comm.host_all_reduce(deg, false, str);  // own-row counts → global
   if (!out) return;
   if (out->correspondence)
     throw Failure(FCPD_ERR_PARAMETER, "register: correspondence output is single-GPU only");
   const int run = h.iters_run;
   const int d = s.d;
+  Basis& b = ctx->basis;
   out->iterations_run = run;
   out->basis_reused = s.basis_reused ? 1 : 0;
   out->sigma2_initial = s.sigma2_initial;
-  out->degenerate_rows = static_cast<int64_t>(deg);
-  out->spectral_rank = s.zp.trunc && h.keff > 0 ? std::min<int64_t>(h.keff, ctx->basis.k)
-                                                 : ctx->basis.k;
+  out->degenerate_rows = static_cast<int64_t>(deg[0][0]);
+  out->spectral_rank = s.zp.trunc && h.keff > 0 ? std::min<int64_t>(h.keff, b.k) : b.k;
   out->sigma2_clamps = h.sigma2_clamps;
   if (out->sigma2_trace && run > 0)
     FCPD_CUDA(cudaMemcpyAsync(out->sigma2_trace, s.trace.p, sizeof(double) * run,
                               cudaMemcpyDeviceToHost, str));
   std::vector<double> xt(3 * s.m, 0.0);
-  gather_rows(ctx, s, s.xt64.p, xt.data(), 3);
+  gather_rows(ctx, [](Session& q) { return static_cast<const double*>(q.xt64.p); }, xt.data(), 3);
   const std::vector<int64_t>& px = s.perm_x;  // sorted row k ↔ original row px[k]
   if (out->transformed)
     for (int c = 0; c < d; ++c)
@@ -1382,19 +1639,29 @@ void session_read_dist(fcpd_ctx* ctx, fcpd_result* out, double wall) {
             s.cfg.normalize ? xt[c * s.m + k] * s.scale + s.center[c] : xt[c * s.m + k];
   if (out->coefficients) {
     if (s.zp.trunc && run > 0) {  // the iterations streamed a truncated basis
-      launch_colsum(s.zp, b.q + s.m0 * b.kpad, b.kpad, s.resid4.p, s.zpart.p, nullptr, nullptr,
-                    0, str);
-      launch_zsum(s.zp, s.zpart.p, s.zfull.p, nullptr, str);
-      FCPD_NCCL(ncclAllReduce(s.zfull.p, s.zfull.p, 3 * b.k, ncclDouble, ncclSum, ctx->comm,
-                              str));
-      launch_zcoef_full(s.zfull.p, b.k, b.lam, s.cfg.lambda_reg, s.coef.p, s.st.p, str);
+      for (fcpd_ctx* c : R) {
+        Session& q = c->sess;
+        Basis& qb = c->basis;
+        launch_colsum(q.zp, qb.q + q.m0 * qb.kpad, qb.kpad, q.resid4.p, q.zpart.p, nullptr,
+                      nullptr, 0, str);
+        launch_zsum(q.zp, q.zpart.p, q.zfull.p, nullptr, str);
+      }
+      comm.all_reduce_sum(per_rank<double*>(R, [](Session& q) { return q.zfull.p; }),
+                          static_cast<size_t>(3 * b.k), str);
+      for (fcpd_ctx* c : R)
+        launch_zcoef_full(c->sess.zfull.p, c->basis.k, c->basis.lam, c->sess.cfg.lambda_reg,
+                          c->sess.coef.p, c->sess.st.p, str);
     }
-    pack_coef_kernel<<<ceil_div(b.k, 256), 256, 0, str>>>(s.coef.p, b.k, s.g4.p);
-    FCPD_LAUNCH_CHECK();
-    launch_colsum(s.vp, s.qt_own.p, s.mr4, s.g4.p, s.vpart.p, nullptr, nullptr, 0, str);
-    launch_vreduce_add(s.vp, s.vpart.p, nullptr, 3, s.ptilde_y.p, str);
+    for (fcpd_ctx* c : R) {
+      Session& q = c->sess;
+      pack_coef_kernel<<<ceil_div(c->basis.k, 256), 256, 0, str>>>(q.coef.p, c->basis.k, q.g4.p);
+      FCPD_LAUNCH_CHECK();
+      launch_colsum(q.vp, q.qt_own.p, q.mr4, q.g4.p, q.vpart.p, nullptr, nullptr, 0, str);
+      launch_vreduce_add(q.vp, q.vpart.p, nullptr, 3, q.ptilde_y.p, str);
+    }
     std::vector<double> w(3 * s.m, 0.0);
-    gather_rows(ctx, s, s.ptilde_y.p, w.data(), 3);
+    gather_rows(ctx, [](Session& q) { return static_cast<const double*>(q.ptilde_y.p); },
+                w.data(), 3);
     for (int c = 0; c < d; ++c)
       for (int64_t k = 0; k < s.m; ++k) out->coefficients[c * s.m + px[k]] = w[c * s.m + k];
   }
@@ -1502,6 +1769,30 @@ int fcpd_create_dist(fcpd_ctx** out, int device, int rank, int world, const uint
   }
   ctx->rank = rank;
   ctx->world = world;
+  ctx->comm_obj = std::make_unique<NcclComm>(ctx->comm, world);
+  return FCPD_OK;
+}
+
+int fcpd_create_loopback(fcpd_ctx** out, int device, int world) {
+  if (!out || world < 1 || world > kMaxLoopRanks) return FCPD_ERR_PARAMETER;
+  int rc = fcpd_create(out, device);
+  if (rc) return rc;
+  fcpd_ctx* lead = *out;
+  for (int r = 1; r < world; ++r) {
+    fcpd_ctx* c = nullptr;
+    rc = fcpd_create(&c, device);
+    if (rc) {
+      fcpd_destroy(lead);
+      *out = nullptr;
+      return rc;
+    }
+    c->rank = r;
+    c->world = world;
+    lead->loop_ranks.push_back(c);
+  }
+  lead->rank = 0;
+  lead->world = world;
+  lead->comm_obj = std::make_unique<LoopComm>(world);
   return FCPD_OK;
 }
 
@@ -1517,6 +1808,8 @@ void fcpd_destroy(fcpd_ctx* ctx) {
   cudaSetDevice(ctx->device);
   ctx->sess.release();
   ctx->basis.release();
+  for (fcpd_ctx* c : ctx->loop_ranks) fcpd_destroy(c);
+  ctx->loop_ranks.clear();
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->solver) cusolverDnDestroy(ctx->solver);
   if (ctx->blas) cublasDestroy(ctx->blas);
@@ -1540,9 +1833,16 @@ int32_t fcpd_kernels_per_iteration(const fcpd_ctx* ctx) {
   const Session& s = ctx->sess;
   const bool culling = s.cull && s.xlo.p && s.ylo.p && s.wl1_tiles.p;
   const int e = estep_kernels(culling, s.dist);
-  // distributed M-step: finalize-own, fb-max, fb-sum, fb-finalize, Qᵀ·R,
-  // z-sum, z-filter, Q·g, transform, σ²-local, σ²-final (+ the collectives)
-  if (s.dist) return e + 11 + (s.zp.trunc ? 1 : 0);
+  if (s.dist) {
+    // per rank: finalize-own, (spectral rank,) z pass + reduce, flag count,
+    // z filter, Q·g, transform, σ² partial, σ² final; the fallback exchange's
+    // fb-max, fb-sum, fb-finalize, z correction, z add only when it is not
+    // behind the conditional node (then its predicate kernel instead); a
+    // loopback group adds its three collective kernels
+    const int ranks = 1 + static_cast<int>(ctx->loop_ranks.size());
+    return ranks * (e + 9 + (s.zp.trunc ? 1 : 0) + (s.dist_conditional ? 0 : 5)) +
+           (s.dist_conditional ? 1 : 0) + (ctx->loop_ranks.empty() ? 0 : 3);
+  }
   // fused M-step: one kernel for rank, Qᵀ·R, filter, Q·g, transform and σ²
   if (s.mfused) return e + 1;
   // streaming: (spectral rank,) Qᵀ·R, z-reduce/filter, Q·g, transform, σ²

@@ -753,19 +753,7 @@ __global__ void sigma_final_kernel(const double* __restrict__ sig_part, int bloc
   if (threadIdx.x != 0) return;
   double tot = 0.0;
   for (int w = 0; w < (blockDim.x >> 5); ++w) tot += red[w];
-  const double val = tot / (static_cast<double>(d) * static_cast<double>(m));
-  if (val < -1e-8) set_error(st, kDevNegVariance, val);
-  const double next = fmax(val, kSigma2Floor);
-  if (next <= kSigma2Floor) st->sigma2_clamps += 1;
-  const int it = st->iter;
-  trace[it] = next;
-  const double delta = fabs(next - st->sigma2);
-  st->sigma2 = next;
-  st->iters_run = it + 1;
-  st->iter = it + 1;
-  estep_scalars_for_next(st, next, it + 1);  // the next E-step's σ², scale, log c
-  if (stamps) stamps[4 * it + 3] = globaltimer();
-  if (early_stop && delta < 1e-10) st->active = 0;
+  finish_iteration_sigma(st, tot, m, d, early_stop, trace, stamps);
 }
 
 // out = X + Σ partials  (apply_transform_lowrank epilogue, no σ² terms)

@@ -54,6 +54,29 @@ void launch_rowdot_reduce(const RowdotPlan& p, const double* part, int64_t k, co
 // ctas_per_sm: resident bulk CTAs per SM the grid assumes (2 = whole GPU).
 ColsumPlan make_colsum_plan(int64_t rows, int64_t cols, int sm_count, int ctas_per_sm = 2);
 
+// The last step of an iteration (one thread): σ² = tot/(D·M) with the
+// reference's checks (solvers.hpp:173-175), the clamp count
+// (registration.hpp:153), the trace, the next E-step's scalars, and the early
+// stop (:159-161).  Shared by sigma_final_kernel, the fused M-step's last CTA
+// and the distributed sigma_final_gathered_kernel.
+__device__ __forceinline__ void finish_iteration_sigma(IterState* st, double tot, int64_t m, int d,
+                                                       int early_stop, double* trace,
+                                                       uint64_t* stamps) {
+  const double val = tot / (static_cast<double>(d) * static_cast<double>(m));
+  if (val < -1e-8) set_error(st, kDevNegVariance, val);
+  const double next = fmax(val, kSigma2Floor);
+  if (next <= kSigma2Floor) st->sigma2_clamps += 1;
+  const int it = st->iter;
+  trace[it] = next;
+  const double delta = fabs(next - st->sigma2);
+  st->sigma2 = next;
+  st->iters_run = it + 1;
+  st->iter = it + 1;
+  estep_scalars_for_next(st, next, it + 1);  // the next E-step's σ², scale, log c
+  if (stamps) stamps[4 * it + 3] = globaltimer();
+  if (early_stop && delta < 1e-10) st->active = 0;
+}
+
 // Effective spectral rank by a parallel two-round search, for a whole CTA
 // (every thread gets the result; all threads must call).  The filter
 // f_k = λnum_k/(λ_k + λ_reg σ²) is non-increasing along the descending

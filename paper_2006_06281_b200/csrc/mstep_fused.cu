@@ -315,18 +315,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mstep_fused_kernel(MstepFuse
   if (tid != 0) return;
   double tot = 0.0;
   for (int w = 0; w < kFusedWarps; ++w) tot += fin[w];
-  const double val = tot / (static_cast<double>(a.d) * static_cast<double>(m));
-  if (val < -1e-8) set_error(st, kDevNegVariance, val);
-  const double next = fmax(val, kSigma2Floor);
-  if (next <= kSigma2Floor) st->sigma2_clamps += 1;
-  a.trace[it] = next;
-  const double delta = fabs(next - st->sigma2);
-  st->sigma2 = next;
-  st->iters_run = it + 1;
-  st->iter = it + 1;
-  estep_scalars_for_next(st, next, it + 1);  // the next E-step's σ², scale, log c
-  if (a.stamps) a.stamps[4 * it + 3] = globaltimer();
-  if (a.early_stop && delta < 1e-10) st->active = 0;
+  finish_iteration_sigma(st, tot, m, a.d, a.early_stop, a.trace, a.stamps);
 }
 
 int mstep_fused_grid(int sm_count) { return sm_count; }

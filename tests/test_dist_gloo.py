@@ -1,20 +1,29 @@
-"""World-size-2 CPU test of the multi-GPU decomposition.
+"""World-size-2 and -4 CPU tests of the multi-GPU decomposition.
 
-The device path (csrc/dist.cu + engine.cu enqueue_iteration_dist) splits one
-EM iteration into per-rank work and collectives:
+The device path (engine.cu enqueue_iteration_group + csrc/dist.cu) splits
+one EM iteration into per-rank work and, in the common case, THREE
+collectives:
 
   pass 1        column-local over the rank's scene shard (no communication)
   pass 2        per-row partial sums (S0, Σw·y, Σw·d²) over local columns
                 → reduce-scatter to the row-shard owners
-  M-step        z_r = Q_rᵀ R_r → all-reduce; V_r = Q_r (f⊙z) on own rows
-  σ²            per-row terms on own rows → all-reduce
-  x̃             all-gather
-  normalize     global centroid / max-abs / scene moments via all-reduce
+  own rows      finalised; rows whose global mass is too small for the fp32
+                fast path are flagged and get a zero residual for now
+  M-step        z_r = Q_rᵀ R_r → all-reduce, carrying the flagged-row count
+  fallback      only if the count is nonzero (a conditional graph node):
+                all-gather of the flags, all-reduce MAX of the flagged rows'
+                max log-posterior, reduce-scatter of the shifted sums, the
+                flagged rows' z correction → all-reduce
+  x̃             V_r = Q_r (f⊙z), x̃ own rows, σ² partial of the own rows;
+                all-gather of x̃ with the σ² partials riding along; every
+                rank sums the partials in rank order
+  normalize     global centroid / max-abs / scene moments (host all-reduce)
 
-This test runs exactly that decomposition in fp64 numpy on 2 gloo ranks and
+This test runs exactly that decomposition in fp64 numpy on gloo ranks and
 checks it against the unsharded oracle restatement of register_pointsets.
 (gloo has no reduce-scatter: all-reduce + taking the own rows is the same
-reduction.)
+reduction.)  `flag_below` forces the flagged path for rows whose mass is
+below it, so the fallback exchange is exercised.
 """
 import math
 import os
@@ -44,7 +53,7 @@ def _allreduce(a, op=dist.ReduceOp.SUM):
 
 
 def sharded_register(x, y_shard, rank, world, omega, beta, lam_reg, iters, u, lam_raw, lam_c,
-                     full_rank):
+                     full_rank, flag_below=0.0):
     m, d = x.shape
     n_loc = y_shard.shape[0]
     # normalize_pair with global statistics (pointset.hpp:124-148)
@@ -64,9 +73,11 @@ def sharded_register(x, y_shard, rank, world, omega, beta, lam_reg, iters, u, la
     mr = (m + world - 1) // world
     m0, m1 = rank * mr, min(m, rank * mr + mr)
     U = u[m0:m1]
+    k = U.shape[1]
     lam_num = lam_raw if full_rank else lam_c
     xt = X.copy()
     trace = []
+    fallbacks = 0
     for _ in range(iters):
         s2e = max(s2, 1e-10)
         d2 = ((Y[None, :, :] - xt[:, None, :]) ** 2).sum(-1)  # M × n_loc
@@ -79,31 +90,59 @@ def sharded_register(x, y_shard, rank, world, omega, beta, lam_reg, iters, u, la
         E = np.exp(e - shift)
         den = E.sum(0) + (np.exp(log_c - shift) if omega > 0 else 0.0)
         P = E / den                                          # pass 1: column-local
+        logP = e - shift - np.log(den)
         part = np.column_stack([P.sum(1), P @ Y, (P * d2).sum(1)])  # pass 2 partials
-        S = _allreduce(part)[m0:m1]                          # "reduce-scatter"
-        deg = S[:, 0] < 1e-300
-        pty = np.where(deg[:, None], ymean, S[:, 1:4] / np.where(deg, 1, S[:, 0])[:, None])
+        S = _allreduce(part)[m0:m1]                          # collective 1: "reduce-scatter"
+        flag = S[:, 0] < flag_below                          # mass too small: fallback
         xo = xt[m0:m1]
-        var = np.where(deg, ysq - 2 * xo @ ymean + (xo ** 2).sum(1),
-                       S[:, 4] / np.where(deg, 1, S[:, 0]))
+
+        def finalize(S, rows):
+            deg = S[:, 0] < 1e-300
+            pty = np.where(deg[:, None], ymean, S[:, 1:4] / np.where(deg, 1, S[:, 0])[:, None])
+            xr = xo[rows]
+            var = np.where(deg, ysq - 2 * xr @ ymean + (xr ** 2).sum(1),
+                           S[:, 4] / np.where(deg, 1, S[:, 0]))
+            return pty, var
+
+        pty, var = finalize(S, slice(None))
         R = pty - X[m0:m1]
-        z = _allreduce(U.T @ R)                              # all-reduce K×3
+        R[flag] = 0.0                                        # filled by the fallback
+        zc = np.concatenate([(U.T @ R).ravel(), [flag.sum()]])
+        zc = _allreduce(zc)                                  # collective 2: z + flagged count
+        z = zc[:-1].reshape(k, 3)
+        if zc[-1] > 0:                                       # the conditional fallback
+            fallbacks += 1
+            mask = np.zeros(world * mr)
+            mask[m0:m0 + (m1 - m0)] = flag
+            mask = _allreduce(mask)[:m] > 0                  # "all-gather" of the flags
+            lmax = np.where(mask, (logP.max(1) if n_loc else -np.inf), -np.inf)
+            lmax = _allreduce(lmax, dist.ReduceOp.MAX)       # max log P over all columns
+            W = np.exp(logP - np.where(mask, lmax, 0.0)[:, None]) * mask[:, None]
+            fs = np.column_stack([W.sum(1), W @ Y, (W * d2).sum(1)])
+            fs = _allreduce(fs)[m0:m1]                       # "reduce-scatter" shifted sums
+            fpty, fvar = finalize(fs, slice(None))
+            pty[flag], var[flag] = fpty[flag], fvar[flag]
+            R[flag] = pty[flag] - X[m0:m1][flag]
+            Rc = np.where(flag[:, None], R, 0.0)
+            z = z + _allreduce(U.T @ Rc)                     # z correction
         diag = lam_c + lam_reg * s2
         assert diag.min() > 0
         g = z * (lam_num / diag)[:, None]
         xn = X[m0:m1] + U @ g
         dlt = xn - xo
         term = (var - 2 * (dlt * (pty - xo)).sum(1) + (dlt ** 2).sum(1)).sum()
-        val = float(_allreduce(np.array([term]))[0]) / (d * m)
+        # collective 3: all-gather x̃ with the σ² partial riding along
+        own = torch.zeros(mr + 1, 3, dtype=torch.float64)
+        own[: m1 - m0] = torch.from_numpy(xn)
+        own[mr, 0] = term
+        gathered = [torch.zeros(mr + 1, 3, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(gathered, own)
+        val = sum(float(gv[mr, 0]) for gv in gathered) / (d * m)   # rank order
         nxt = max(val, 1e-10)
         trace.append(nxt)
         s2 = nxt
-        gathered = [torch.zeros(mr, 3, dtype=torch.float64) for _ in range(world)]
-        own = torch.zeros(mr, 3, dtype=torch.float64)
-        own[: m1 - m0] = torch.from_numpy(xn)
-        dist.all_gather(gathered, own)                       # all-gather x̃
-        xt = torch.cat(gathered).numpy()[:m]
-    return np.array(trace), xt * sc + center
+        xt = torch.cat([gv[:mr] for gv in gathered]).numpy()[:m]
+    return np.array(trace), xt * sc + center, fallbacks
 
 
 def _worker(rank, world, port, q, case):
@@ -121,18 +160,22 @@ def _worker(rank, world, port, q, case):
     u, lam_c, lam_raw = orc.eigendecompose(phi, k)
     n = y.shape[0]
     y_shard = y[rank * n // world:(rank + 1) * n // world]
-    trace, pts = sharded_register(x, y_shard, rank, world, case["omega"], case["beta"],
-                                  case["lam"], case["iters"], u, lam_raw, lam_c, case["full"])
-    q.put((rank, trace, pts))
+    trace, pts, fb = sharded_register(x, y_shard, rank, world, case["omega"], case["beta"],
+                                      case["lam"], case["iters"], u, lam_raw, lam_c, case["full"],
+                                      case.get("flag_below", 0.0))
+    q.put((rank, trace, pts, fb))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", [
-    dict(m=120, n=150, omega=0.0, beta=2.0, lam=3.0, iters=12, full=True, k=120),
-    dict(m=121, n=149, omega=0.3, beta=2.0, lam=3.0, iters=12, full=False, k=20),
+@pytest.mark.parametrize("world,case", [
+    (2, dict(m=120, n=150, omega=0.0, beta=2.0, lam=3.0, iters=12, full=True, k=120)),
+    (2, dict(m=121, n=149, omega=0.3, beta=2.0, lam=3.0, iters=12, full=False, k=20)),
+    (4, dict(m=122, n=151, omega=0.1, beta=2.0, lam=3.0, iters=10, full=False, k=24)),
+    # rows with mass below one point take the fallback exchange
+    (2, dict(m=120, n=150, omega=0.2, beta=2.0, lam=3.0, iters=10, full=True, k=120,
+             flag_below=1.0)),
 ])
-def test_two_rank_sharded_em_matches_oracle(orc, case):
-    world = 2
+def test_sharded_em_matches_oracle(orc, world, case):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -149,8 +192,10 @@ def test_two_rank_sharded_em_matches_oracle(orc, case):
                        iterations=case["iters"],
                        variant="fast" if case["full"] else "fast_lowrank",
                        rank_fraction=case["k"] / case["m"])
-    for _, trace, pts in res:
+    for _, trace, pts, fb in res:
         assert np.allclose(trace, ref.sigma2_trace, rtol=1e-10, atol=0)
         assert np.abs(pts - ref.transformed).max() <= 1e-10
+        assert (fb > 0) == (case.get("flag_below", 0.0) > 0)
     # every rank ends with the same full result
-    assert np.array_equal(res[0][2], res[1][2])
+    for r in res[1:]:
+        assert np.array_equal(res[0][2], r[2])

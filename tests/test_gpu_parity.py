@@ -383,10 +383,10 @@ def test_distributed_engine_single_rank(ctx, fc, orc, monkeypatch, variant, omeg
     with fc.Context.distributed(0, 0, 1, uid) as dctx:
         assert dctx.world == (0, 1)
         got = dctx.register(x, y, cfg)
-        # 17 per iteration, plus the same optional culling / tensor-core
-        # kernels as the single-GPU session (12 + extras; the single-GPU
-        # session may add its spectral-rank kernel)
-        assert dctx.kernels_per_iteration == ctx.kernels_per_iteration + 5
+        # the sharded iteration's extra kernels (finalize-own, flag count,
+        # z filter split, σ² partial packing, predicate of the conditional
+        # fallback node; +4 more when the fallback runs unconditionally)
+        assert dctx.kernels_per_iteration - ctx.kernels_per_iteration in (4, 8)
     rel = np.abs(got.sigma2_trace / ref.sigma2_trace - 1).max()
     assert rel <= 1e-9, rel
     assert np.abs(got.transformed - ref.transformed).max() <= 1e-9 * bbox_diag(y)
