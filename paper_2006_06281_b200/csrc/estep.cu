@@ -216,24 +216,12 @@ __device__ __forceinline__ SegRange seg_range(const WorkList& wl, int64_t G, int
   }
   return r;
 }
-// Release this CTA's slot writes and count its arrival at block b; true in
-// the CTA that completes the block (which then sees every slot).
-__device__ __forceinline__ bool arrive_last(int32_t* done, int b, int count) {
-  __shared__ int last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(done + b, 1) == count - 1;
-  __syncthreads();
-  const bool l = last;
-  if (l) __threadfence();
-  return l;
-}
 // Culling sessions use the culled list only when this iteration built one;
 // otherwise every unit (counted into tiles_evaluated by CTA 0).
-__device__ __forceinline__ WorkList resolve_list(WorkList wl) {
+__device__ __forceinline__ WorkList resolve_list(WorkList wl, bool count = true) {
   if (wl.dyn_on && !*wl.dyn_on) {
     wl.implicit = 1;
-    if (wl.implicit_counter && blockIdx.x == 0 && threadIdx.x == 0)
+    if (count && wl.implicit_counter && blockIdx.x == 0 && threadIdx.x == 0)
       atomicAdd(wl.implicit_counter, static_cast<unsigned long long>(wl.n_blocks) *
                                          static_cast<unsigned long long>(wl.n_other));
   }
@@ -308,58 +296,6 @@ __device__ __forceinline__ void col_b_ranges(const ColFix& f, int rb, int64_t n,
 
 // Pass-1 block fix-up: each column's sum over the block's slots in CTA
 // order, finalisation, b ranges.
-// Slot loads are issued kFixBatch at a time (independent L2 loads in
-// flight), then added in CTA order: the same sums as a serial walk (an
-// empty range contributes +0.0, which leaves a sum of non-negative terms
-// unchanged bit for bit).
-constexpr int kFixBatch = 4;
-constexpr int kRowFixBatch = 2;  // pass 2: 5 quantities per slot
-
-template <int kCols>
-__device__ void col_block_fixup(const ColFix& f, const double* seg, const SegRange& sr,
-                                int64_t G, int64_t P, int rb, int64_t m, int64_t n,
-                                IterState* st) {
-  static_assert(kCols % 2 == 0, "double2 slot loads");
-  const int t = threadIdx.x;
-  float lo = INFINITY, hi = -INFINITY;
-  double sums[kCols];
-#pragma unroll
-  for (int h = 0; h < kCols; ++h) sums[h] = 0.0;
-  for (int64_t g = sr.g0; g <= sr.g1; g += kFixBatch) {
-    double2 v[kFixBatch][kCols / 2];
-#pragma unroll
-    for (int j = 0; j < kFixBatch; ++j) {
-      const bool live = g + j <= sr.g1 && !sk_empty(g + j, G, P);
-      const double2* sp = reinterpret_cast<const double2*>(seg + (g + j + rb) * kTile + kCols * t);
-#pragma unroll
-      for (int h = 0; h < kCols / 2; ++h) v[j][h] = live ? __ldcg(sp + h) : make_double2(0.0, 0.0);
-    }
-#pragma unroll
-    for (int j = 0; j < kFixBatch; ++j)
-#pragma unroll
-      for (int h = 0; h < kCols / 2; ++h) {
-        sums[2 * h] += v[j][h].x;
-        sums[2 * h + 1] += v[j][h].y;
-      }
-  }
-#pragma unroll
-  for (int h = 0; h < kCols; ++h) {
-    const int li = kCols * t + h;
-    const int64_t col = static_cast<int64_t>(rb) * kTile + li;
-    const double sm = sums[h];
-    if (col < n) {
-      const float b = col_finalize(f, col, sm, m, st);
-      if (b == b) {
-        lo = fminf(lo, b);
-        hi = fmaxf(hi, b);
-      } else {
-        hi = INFINITY;
-      }
-    }
-  }
-  if (f.bminmax) col_b_ranges<kCols>(f, rb, n, lo, hi);
-}
-
 // ---------------------------------------------------------------------------
 // Pass 1: per-column sums Σ_m 2^{−t_mn}.  Own block = 256 scene points
 // (thread: column pair 2·tid, 2·tid+1); the staged tiles are model points.
@@ -380,7 +316,7 @@ template <int NC>
 __global__ void __launch_bounds__(128 / NC, NC == 2 ? 16 : 8)
     estep_col_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4,
                      int64_t n, IterState* __restrict__ st, WorkList wl_in,
-                     double* __restrict__ seg, float centred_max_r2, ColFix fix,
+                     double* __restrict__ seg, float centred_max_r2,
                      unsigned long long* form_pairs, uint64_t* stamps) {
   griddep_wait();
   constexpr int kThr = 128 / NC;  // threads
@@ -539,12 +475,6 @@ __global__ void __launch_bounds__(128 / NC, NC == 2 ? 16 : 8)
       form_tally[centred ? 0 : 1] += static_cast<unsigned long long>(pe - p) *
                                      static_cast<unsigned long long>(
                                          min(int64_t(kTile), n - int64_t(rb) * kTile));
-    // the CTA completing block rb's last segment finalises the block
-    const SegRange sr = seg_range(wl, G, P, rb);
-    if (arrive_last(fix.done, rb, sr.count)) {
-      col_block_fixup<kCols>(fix, seg, sr, G, P, rb, m, n, st);
-      if (t == 0) fix.done[rb] = 0;  // self-resetting for the next replay
-    }
     p = pe;
   }
   if (form_pairs && t == 0) {
@@ -555,19 +485,17 @@ __global__ void __launch_bounds__(128 / NC, NC == 2 ? 16 : 8)
 
 // Exact column normaliser for flagged columns: warp per column, max-shifted
 // log-sum-exp over all m in fp32 t_mn, fp64 accumulation.
-__global__ void estep_col_fallback_kernel(const float4* __restrict__ xt4, int64_t m,
-                                          float4* __restrict__ y4b, double* __restrict__ b2_out,
-                                          double* __restrict__ pt1,
-                                          const int32_t* __restrict__ flag_list,
-                                          const IterState* __restrict__ st) {
-  griddep_wait();
-  if (!st->active) return;
-  const int count = st->flag_count[0];
+// (run by the last CTA of the pass-1 combine: its warps take the queued
+// columns in turn)
+__device__ void col_fallback(const float4* __restrict__ xt4, int64_t m, float4* __restrict__ y4b,
+                             double* __restrict__ b2_out, double* __restrict__ pt1,
+                             const int32_t* __restrict__ flag_list, const IterState* st) {
+  const int count = *reinterpret_cast<const volatile int32_t*>(&st->flag_count[0]);
   const int lane = threadIdx.x & 31;
-  const int warps = (blockDim.x >> 5) * gridDim.x;
+  const int warps = blockDim.x >> 5;
   const float s = st->sx;
   const double log2c = st->log2c;
-  for (int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < count; w += warps) {
+  for (int w = threadIdx.x >> 5; w < count; w += warps) {
     const int64_t col = flag_list[w];
     const float4 yv = scale_pt(y4b[col], s);
     float tmin = INFINITY;
@@ -659,44 +587,6 @@ __device__ __forceinline__ void row_finalize(const RowFix& f, int64_t row, int64
   finalize_row(row, m, log2(a[0]), a[0], a[1], a[2], a[3], a[4], f.xt64, derived_scale(st), f.out,
                f.ys, st);
 }
-template <int kRows>
-__device__ void row_block_fixup(const RowFix& f, const double* seg, const SegRange& sr,
-                                int64_t G, int64_t P, int rb, int64_t m, int64_t n,
-                                IterState* st) {
-  const int t = threadIdx.x;
-#pragma unroll 1
-  for (int h = 0; h < kRows; h += 2) {  // row pairs: one double2 per quantity and slot
-    const int li = kRows * t + h;
-    double a[2][5];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) a[0][k] = a[1][k] = 0.0;
-    for (int64_t g = sr.g0; g <= sr.g1; g += kRowFixBatch) {
-      double2 v[kRowFixBatch][5];
-#pragma unroll
-      for (int j = 0; j < kRowFixBatch; ++j) {
-        const bool live = g + j <= sr.g1 && !sk_empty(g + j, G, P);
-        const double* sp = seg + (g + j + rb) * 5 * kTile + li;
-#pragma unroll
-        for (int k = 0; k < 5; ++k)
-          v[j][k] = live ? __ldcg(reinterpret_cast<const double2*>(sp + k * kTile))
-                         : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int j = 0; j < kRowFixBatch; ++j)
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
-          a[0][k] += v[j][k].x;
-          a[1][k] += v[j][k].y;
-        }
-    }
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int64_t row = static_cast<int64_t>(rb) * kTile + li + e;
-      if (row < m) row_finalize(f, row, m, n, a[e], st);
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Pass 2: per-row sums over n: S0, Sy (3), SV.  Own block = 256 model points
 // (thread: row pair 2·tid, 2·tid+1); the staged tiles are scene points.
@@ -717,7 +607,7 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
     estep_row_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4b,
                      int64_t n, IterState* __restrict__ st, WorkList wl_in,
                      double* __restrict__ seg /* [slot][5][256] */, float centred_max_r2,
-                     int flush, RowFix fix, unsigned long long* form_pairs) {
+                     int flush, unsigned long long* form_pairs) {
   griddep_wait();
   constexpr int kThr = 128 / NP;   // threads
   constexpr int kRows = 2 * NP;    // rows per thread
@@ -937,12 +827,6 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
       form_tally[centred ? 0 : 1] += static_cast<unsigned long long>(pe - p) *
                                      static_cast<unsigned long long>(
                                          min(int64_t(kTile), m - int64_t(rb) * kTile));
-    // the CTA completing block rb's last segment finalises its rows
-    const SegRange sr = seg_range(wl, G, P, rb);
-    if (arrive_last(fix.done, rb, sr.count)) {
-      row_block_fixup<kRows>(fix, seg, sr, G, P, rb, m, n, st);
-      if (t == 0) fix.done[rb] = 0;  // self-resetting for the next replay
-    }
     p = pe;
   }
   if (form_pairs && t == 0) {
@@ -1234,7 +1118,7 @@ __global__ void __launch_bounds__(kListThreads)
     col_list_kernel(CullInfo cull, const float4* __restrict__ xt4, int64_t m,
                     const float4* __restrict__ y4, int64_t n, int32_t* __restrict__ tiles,
                     int32_t* __restrict__ offset, int n_blocks, int32_t* __restrict__ done,
-                    ColFix fix, IterState* __restrict__ st) {
+                    IterState* __restrict__ st) {
   griddep_wait();
   if (!st->active || !st->cull_on) return;
   __shared__ float4 pa[kProbeTiles * kTile / 2], pb[kProbeTiles * kTile / 2];
@@ -1338,16 +1222,6 @@ __global__ void __launch_bounds__(kListThreads)
     if (np > 0 && cull.probe_paid1)
       cull.probe_paid1[b] = (kept_box - count) * kProbePayShare >= kept_box;
   }
-  if (count == 0) {  // every model point is negligible for these columns (ω > 0)
-    const int64_t col = static_cast<int64_t>(b) * kTile + threadIdx.x;
-    float lo = INFINITY, hi = -INFINITY;
-    if (col < n) {
-      const float bv = col_finalize(fix, col, 0.0, m, st);
-      lo = bv == bv ? bv : INFINITY;
-      hi = bv == bv ? bv : INFINITY;
-    }
-    col_b_ranges<1>(fix, b, n, lo, hi);
-  }
   last_cta_scan(offset, n_blocks, done, cull.counters);
 }
 
@@ -1367,7 +1241,7 @@ __global__ void __launch_bounds__(kListThreads)
                     const float4* __restrict__ y4b, int64_t n, int32_t* __restrict__ tiles,
                     int32_t* __restrict__ offset, int n_blocks, int32_t* __restrict__ done,
                     const float4* __restrict__ ulo, const float4* __restrict__ uhi,
-                    const float2* __restrict__ ubm, int n_units, RowFix fix,
+                    const float2* __restrict__ ubm, int n_units,
                     IterState* __restrict__ st) {
   constexpr int unit_mult = 1;
   griddep_wait();
@@ -1480,11 +1354,6 @@ __global__ void __launch_bounds__(kListThreads)
     if (np > 0 && cull.probe_paid2)
       cull.probe_paid2[b] = (kept_box - count) * kProbePayShare >= kept_box;
   }
-  if (count == 0) {  // (cannot happen: the unit setting the floor is kept) zero sums
-    const int64_t row = static_cast<int64_t>(b) * kTile + threadIdx.x;
-    const double zero[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    if (row < m) row_finalize(fix, row, m, n, zero, st);
-  }
   if (last_cta_scan(offset, n_blocks, done, cull.counters ? cull.counters + 1 : nullptr) &&
       threadIdx.x == 0) {
     // the next iteration builds lists again if these dropped any unit (σ²
@@ -1499,18 +1368,16 @@ __global__ void __launch_bounds__(kListThreads)
 
 // Exact row accumulation for flagged rows (tiny mass): warp per row,
 // max-shifted, fp64 accumulation.
-__global__ void estep_row_fallback_kernel(const float4* __restrict__ xt4, int64_t m,
-                                          const float4* __restrict__ y4b, int64_t n,
-                                          const double* __restrict__ xt64, RowOut out, YStats ys,
-                                          const int32_t* __restrict__ flag_list,
-                                          IterState* st) {
-  griddep_wait();
-  if (!st->active) return;
-  const int count = st->flag_count[1];
+// (run by the last CTA of the pass-2 combine)
+__device__ void row_fallback(const float4* __restrict__ xt4, int64_t m,
+                             const float4* __restrict__ y4b, int64_t n,
+                             const double* __restrict__ xt64, const RowOut& out, const YStats& ys,
+                             const int32_t* __restrict__ flag_list, IterState* st) {
+  const int count = *reinterpret_cast<const volatile int32_t*>(&st->flag_count[1]);
   const int lane = threadIdx.x & 31;
-  const int warps = (blockDim.x >> 5) * gridDim.x;
+  const int warps = blockDim.x >> 5;
   const float s = st->sx;
-  for (int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < count; w += warps) {
+  for (int w = threadIdx.x >> 5; w < count; w += warps) {
     const int64_t row = flag_list[w];
     const float4 xv = scale_pt(xt4[row], s);
     float lmax = -INFINITY;
@@ -1543,6 +1410,98 @@ __global__ void estep_row_fallback_kernel(const float4* __restrict__ xt4, int64_
       finalize_row(row, m, log2p1, a0, ax, ay, az, av, xt64, derived_scale(st), out, ys, st);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Combines: one thread per column (pass 1) / row (pass 2), one CTA per
+// 256-point block.  A point's segment slots are summed in CTA order with
+// kCombineBatch independent loads in flight (skipped slots add +0.0, which
+// leaves a sum of non-negative terms unchanged bit for bit), then finalised.
+// The combine's last CTA runs the exact fallback of everything queued.
+constexpr int kCombineBatch = 8;
+
+__device__ __forceinline__ bool last_cta(int32_t* done) {
+  __shared__ int is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(done, 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (!is_last) return false;
+  __threadfence();
+  if (threadIdx.x == 0) *done = 0;  // self-resetting for the next replay
+  return true;
+}
+
+// Pass-1 combine: b_n / Σ_m P_mn or the fallback queue, the tile's b ranges
+// (culling), then (last CTA) the exact fallback of the queued columns.
+__global__ void __launch_bounds__(kTile)
+    estep_col_combine_kernel(const double* __restrict__ seg, WorkList wl_in, int G, int64_t m,
+                             int64_t n, ColFix f, const float4* __restrict__ xt4,
+                             IterState* __restrict__ st, int32_t* __restrict__ done) {
+  griddep_wait();
+  if (!st->active) return;
+  const WorkList wl = resolve_list(wl_in, false);
+  const int64_t P = wl.off(wl.n_blocks) << wl.ushift;
+  const int b = blockIdx.x, li = threadIdx.x;
+  const int64_t col = static_cast<int64_t>(b) * kTile + li;
+  const SegRange sr = seg_range(wl, G, P, b);
+  double sm = 0.0;
+  for (int64_t g = sr.g0; g <= sr.g1; g += kCombineBatch) {
+    double v[kCombineBatch];
+#pragma unroll
+    for (int j = 0; j < kCombineBatch; ++j)
+      v[j] = g + j <= sr.g1 && !sk_empty(g + j, G, P) ? __ldcg(seg + (g + j + b) * kTile + li)
+                                                       : 0.0;
+#pragma unroll
+    for (int j = 0; j < kCombineBatch; ++j) sm += v[j];
+  }
+  float lo = INFINITY, hi = -INFINITY;
+  if (col < n) {
+    const float bv = col_finalize(f, col, sm, m, st);
+    if (bv == bv) {
+      lo = bv;
+      hi = bv;
+    } else {
+      hi = INFINITY;
+    }
+  }
+  if (f.bminmax) col_b_ranges<1>(f, b, n, lo, hi);
+  if (last_cta(done)) col_fallback(xt4, m, f.y4b, f.b2, f.pt1, f.flag_list, st);
+}
+
+// Pass-2 combine: finalised rows (or the fallback queue), or AoS row sums
+// of the local columns (distributed); then (last CTA, single GPU) the exact
+// fallback of the queued rows.
+__global__ void __launch_bounds__(kTile)
+    estep_row_combine_kernel(const double* __restrict__ seg, WorkList wl_in, int G, int64_t m,
+                             int64_t n, RowFix f, const float4* __restrict__ xt4,
+                             const float4* __restrict__ y4b, IterState* __restrict__ st,
+                             int32_t* __restrict__ done) {
+  griddep_wait();
+  if (!st->active) return;
+  const WorkList wl = resolve_list(wl_in, false);
+  const int64_t P = wl.off(wl.n_blocks) << wl.ushift;
+  const int b = blockIdx.x, li = threadIdx.x;
+  const int64_t row = static_cast<int64_t>(b) * kTile + li;
+  const SegRange sr = seg_range(wl, G, P, b);
+  double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int64_t g = sr.g0; g <= sr.g1; g += kCombineBatch) {
+    double v[kCombineBatch][5];
+#pragma unroll
+    for (int j = 0; j < kCombineBatch; ++j) {
+      const bool live = g + j <= sr.g1 && !sk_empty(g + j, G, P);
+      const double* sp = seg + (g + j + b) * 5 * kTile + li;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) v[j][k] = live ? __ldcg(sp + k * kTile) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kCombineBatch; ++j)
+#pragma unroll
+      for (int k = 0; k < 5; ++k) a[k] += v[j][k];
+  }
+  if (row < m) row_finalize(f, row, m, n, a, st);
+  if (!f.aos && last_cta(done))
+    row_fallback(xt4, m, y4b, n, f.xt64, f.out, f.ys, f.flag_list, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -1635,11 +1594,12 @@ RowFix row_fix(const EStepBuffers& b) {
 }
 }  // namespace
 
-int estep_kernels(bool culling, bool dist) {
-  // pass 1 + column fallback + pass 2 (+ row fallback on one GPU); culling
-  // adds the x̃ tile boxes and the two list kernels (launched every
-  // iteration; they return at once when the iteration builds no lists)
-  return 3 + (dist ? 0 : 1) + (culling ? 3 : 0);
+int estep_kernels(bool culling, bool) {
+  // pass 1 + its combine + pass 2 + its combine (the combines also run the
+  // exact fallbacks and the b ranges); culling adds the x̃ tile boxes and the
+  // two list kernels (launched every iteration; they return at once when the
+  // iteration builds no lists)
+  return 4 + (culling ? 3 : 0);
 }
 
 void launch_init_state(IterState* st, double sigma2, double omega, int64_t m, int64_t n_global,
@@ -1671,19 +1631,20 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
                static_cast<const IterState*>(st), b.stamps);
     FCPD_LAUNCH_CHECK();
     launch_pdl(col_list_kernel, dim3(p.col_blocks), dim3(kListThreads), 0, stream, cu, b.xt4, m,
-               b.y4b, n, b.wl1.tiles, b.wl1.offset, p.col_blocks, b.wl1.done, fix, st);
+               b.y4b, n, b.wl1.tiles, b.wl1.offset, p.col_blocks, b.wl1.done, st);
     FCPD_LAUNCH_CHECK();
   }
   uint64_t* stamps = cu.enabled ? nullptr : b.stamps;
   if (p.col_pairs == 2)
     launch_pdl(estep_col_kernel<2>, dim3(p.col_grid), dim3(64), 0, stream, b.xt4, m, b.y4b, n, st,
-               wl, b.col_seg, p.centred_max_r2, fix, forms, stamps);
+               wl, b.col_seg, p.centred_max_r2, forms, stamps);
   else
     launch_pdl(estep_col_kernel<1>, dim3(p.col_grid), dim3(128), 0, stream, b.xt4, m, b.y4b, n, st,
-               wl, b.col_seg, p.centred_max_r2, fix, forms, stamps);
+               wl, b.col_seg, p.centred_max_r2, forms, stamps);
   FCPD_LAUNCH_CHECK();
-  launch_pdl(estep_col_fallback_kernel, dim3(148), dim3(256), 0, stream, b.xt4, m, b.y4b, b.b2,
-             b.pt1, static_cast<const int32_t*>(b.col_flags), static_cast<const IterState*>(st));
+  launch_pdl(estep_col_combine_kernel, dim3(p.col_blocks), dim3(kTile), 0, stream,
+             static_cast<const double*>(b.col_seg), wl, p.col_grid, m, n, fix, b.xt4, st,
+             b.col_done);
   FCPD_LAUNCH_CHECK();
 }
 
@@ -1701,24 +1662,22 @@ void launch_estep_pass2(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
                static_cast<const float4*>(b.y4b), n, b.wl2.tiles, b.wl2.offset, p.row_blocks,
                b.wl2.done, static_cast<const float4*>(cu.sylo),
                static_cast<const float4*>(cu.syhi), static_cast<const float2*>(cu.sbminmax),
-               wl.n_other, fix, st);
+               wl.n_other, st);
     FCPD_LAUNCH_CHECK();
   }
   if (p.row_pairs == 2)
     launch_pdl(estep_row_kernel<2>, dim3(p.row_grid), dim3(64), 0, stream, b.xt4, m,
                static_cast<const float4*>(b.y4b), n, st, wl, b.row_seg, p.centred_max_r2,
-               p.flush2, fix, forms);
+               p.flush2, forms);
   else
     launch_pdl(estep_row_kernel<1>, dim3(p.row_grid), dim3(128), 0, stream, b.xt4, m,
                static_cast<const float4*>(b.y4b), n, st, wl, b.row_seg, p.centred_max_r2,
-               p.flush2, fix, forms);
+               p.flush2, forms);
   FCPD_LAUNCH_CHECK();
-  if (!b.row_aos) {
-    launch_pdl(estep_row_fallback_kernel, dim3(148), dim3(256), 0, stream, b.xt4, m,
-               static_cast<const float4*>(b.y4b), n, b.xt64, b.out, b.ystats,
-               static_cast<const int32_t*>(b.row_flags), st);
-    FCPD_LAUNCH_CHECK();
-  }
+  launch_pdl(estep_row_combine_kernel, dim3(p.row_blocks), dim3(kTile), 0, stream,
+             static_cast<const double*>(b.row_seg), wl, p.row_grid, m, n, fix, b.xt4,
+             static_cast<const float4*>(b.y4b), st, b.row_done);
+  FCPD_LAUNCH_CHECK();
 }
 
 void launch_estep(const EStepPlan& p, const EStepBuffers& b, int64_t m, int64_t n,
