@@ -73,14 +73,16 @@ struct IterState {
   int32_t flag_count[2];  // columns / rows queued for the exact fallback this iteration
   int32_t cull_on;        // this iteration builds culled work lists (else: every pair)
   int32_t cull_pays;      // the last lists dropped enough units to pay for themselves
-  int32_t pad1;
+  int32_t cull_recheck;   // iterations between list re-checks while they do not pay
 };
 
 // Culling lists are built in an iteration when the previous lists dropped
 // any unit (kept < kCullKeepFrac of them: σ² only falls, so a culling that
 // starts to bite soon pays for its list kernels), else only every
-// kCullRecheck-th iteration (C1's first iterations: nothing to drop).
-constexpr int kCullRecheck = 8;
+// IterState::cull_recheck-th iteration: 1 where the list kernels are a small
+// share of a pass (C3/C4: tens of ms of pairs), kCullRecheck otherwise (C1's
+// first iterations: nothing to drop, lists ≈ 3 % of an iteration).
+constexpr int kCullRecheck = 4;
 constexpr double kCullKeepFrac = 0.999;
 
 // The E-step scalars for σ² (correspondence.hpp:43-47 floor + clamp flag,
@@ -105,7 +107,8 @@ __device__ __forceinline__ void estep_scalars_for_next(IterState* st, double sig
     st->log2c = -INFINITY;
   }
   st->flag_count[0] = st->flag_count[1] = 0;
-  st->cull_on = next_iter == 0 || st->cull_pays || next_iter % kCullRecheck == 0;
+  st->cull_on = next_iter == 0 || st->cull_pays ||
+                next_iter % (st->cull_recheck > 0 ? st->cull_recheck : kCullRecheck) == 0;
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {

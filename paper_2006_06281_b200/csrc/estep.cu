@@ -186,6 +186,8 @@ __global__ void init_state_kernel(IterState* st, double sigma2, double omega, in
   st->n_all = n;
   st->dim = d;
   st->cull_pays = 0;
+  // re-check every iteration when the pair work dwarfs the list kernels
+  st->cull_recheck = static_cast<double>(m) * static_cast<double>(n) >= 2e9 ? 1 : kCullRecheck;
   estep_scalars_for_next(st, sigma2, 0);
   st->sigma2_e_last = st->sigma2_e;
 }

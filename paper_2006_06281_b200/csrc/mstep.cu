@@ -519,6 +519,17 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     ++slot;
   };
   int64_t cur_rg = u0 < u1 ? u0 / g.col_blocks : 0;
+  // R of the thread's 4 columns, one unit ahead (an L2 round trip per unit
+  // otherwise serialises the consumers)
+  auto load_r = [&](int64_t u, float4 (&r)[4]) {
+    const int64_t cb = u % g.col_blocks;
+    const int64_t c0 = cb * kRdCols + 4 * tid;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      r[j] = u < u1 && c0 + j < g.cols ? __ldg(v + c0 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  float4 rnext[4];
+  load_r(u0, rnext);
   for (int64_t u = u0; u < u1; ++u) {
     const int64_t chunk = u - u0;
     const int s = static_cast<int>(chunk % kRdStages);
@@ -532,8 +543,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     const int nrows = static_cast<int>(min(static_cast<int64_t>(kRdRows), g.rows - rg * kRdRows));
     float4 rv[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      rv[j] = c0 + j < g.cols ? __ldg(v + c0 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < 4; ++j) rv[j] = rnext[j];
+    load_r(u + 1, rnext);
     mbar_wait(&full[s], ph);
     const float4* st4 = reinterpret_cast<const float4*>(ring + static_cast<int64_t>(s) * (kStageBytes / 4));
 #pragma unroll
