@@ -389,7 +389,15 @@ int64_t lowrank_rank(double fraction, int64_t m) {  // solvers.hpp:46-54
 
 constexpr int64_t kDenseEigLimit = 46000;          // M×M fp64 + syevd workspace fit
 constexpr int64_t kDenseEigLimitLowrank = 16384;   // above: on-the-fly top-K solver
-constexpr int kTopkIterations = 4;
+// power steps of the top-K subspace iteration: the Gaussian spectrum decays
+// super-exponentially, and two steps leave every Ritz pair's residual at the
+// fp64 floor (≈ 1e-16·λ₁ at full C2/C4 size, tests/test_parity_full.py);
+// FCPD_TOPK_ITERS overrides
+constexpr int kTopkIterations = 2;
+int topk_iterations() {
+  if (const char* e = std::getenv("FCPD_TOPK_ITERS")) return std::max(0, std::atoi(e));
+  return kTopkIterations;
+}
 
 void ensure_basis(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa) {
   const bool lowrank = s.cfg.variant == FCPD_VARIANT_FAST_LOWRANK;
@@ -418,7 +426,7 @@ void ensure_basis(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa) {
   if (lowrank && s.m > topk_min) {
     const auto t1 = Clock::now();
     topk_eigensolve(ctx->solver, ctx->blas, s.x0.p, s.m, s.d, s.cfg.beta, rank,
-                    kTopkIterations, s.cfg.seed, b, ctx->stream);
+                    topk_iterations(), s.cfg.seed, b, ctx->stream);
     upload_lambda(b, false, ctx->stream);
     s.t_gram = 0.0;
     s.t_eig = since(t1);
@@ -2148,7 +2156,7 @@ int fcpd_build_basis_topk(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d, 
     FCPD_CUDA(cudaMemcpyAsync(xd.p, x, sizeof(double) * d * m, cudaMemcpyHostToDevice, ctx->stream));
     Basis b;
     topk_eigensolve(ctx->solver, ctx->blas, xd.p, m, d, beta, rank,
-                    iterations > 0 ? iterations : 4, 0, b, ctx->stream, u);
+                    iterations > 0 ? iterations : topk_iterations(), 0, b, ctx->stream, u);
     if (lambda) std::copy(b.lam_host.begin(), b.lam_host.end(), lambda);
     if (lambda_raw) std::copy(b.lam_raw_host.begin(), b.lam_raw_host.end(), lambda_raw);
     b.release();

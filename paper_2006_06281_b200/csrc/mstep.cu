@@ -418,8 +418,8 @@ __global__ void __launch_bounds__(kBulkThreads, kBulkCtasPerSm)
 // a unit's kRdRows × 4 KB row pieces into a 32 KB stage of a 3-stage ring
 // (L2 evict-first); 8 consumer warps: each thread owns 4 columns, reads
 // their R once per unit (float4 per column, L2-resident) and keeps
-// kRdRows × 3 fp64 sums for the current row group (fp32 over its 4
-// columns).  When the CTA leaves a row group it reduces its threads in a
+// kRdRows × 3 sums for the current row group (fp32 over 4 units' 16
+// products per column thread, then fp64).  When the CTA leaves a row group it reduces its threads in a
 // fixed order into one partial slot; rowdot_reduce sums a row's slots in
 // CTA order — bitwise reproducible.
 namespace {
@@ -494,12 +494,30 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
 
   // ------------------------------------------------ consumer warps
   __shared__ double red[kBulkConsumers / 32][kRdSlot];
+  // fp32 sums over kRdBatch units (16 products per column thread), then fp64
+  constexpr int kRdBatch = 4;
   double acc[kRdRows][3];
+  float accf[kRdRows][3];
 #pragma unroll
-  for (int r = 0; r < kRdRows; ++r) acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
+  for (int r = 0; r < kRdRows; ++r) {
+    acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
+    accf[r][0] = accf[r][1] = accf[r][2] = 0.f;
+  }
+  int in_batch = 0;
+  auto drain = [&]() {
+#pragma unroll
+    for (int r = 0; r < kRdRows; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        acc[r][c] += static_cast<double>(accf[r][c]);
+        accf[r][c] = 0.f;
+      }
+    in_batch = 0;
+  };
   int slot = 0;
   // the fixed-order CTA reduction of the current row group into slot `slot`
   auto flush_group = [&]() {
+    drain();
     const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int r = 0; r < kRdRows; ++r)
@@ -555,13 +573,14 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
         const float fx = __fmaf_rn(q.w, rv[3].x, __fmaf_rn(q.z, rv[2].x, __fmaf_rn(q.y, rv[1].x, q.x * rv[0].x)));
         const float fy = __fmaf_rn(q.w, rv[3].y, __fmaf_rn(q.z, rv[2].y, __fmaf_rn(q.y, rv[1].y, q.x * rv[0].y)));
         const float fz = __fmaf_rn(q.w, rv[3].z, __fmaf_rn(q.z, rv[2].z, __fmaf_rn(q.y, rv[1].z, q.x * rv[0].z)));
-        acc[r][0] += fx;
-        acc[r][1] += fy;
-        acc[r][2] += fz;
+        accf[r][0] += fx;
+        accf[r][1] += fy;
+        accf[r][2] += fz;
       }
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    if (++in_batch == kRdBatch) drain();
   }
   if (u0 < u1) flush_group();
 }

@@ -129,6 +129,26 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// Deterministic Gaussian start block on the device: a counter-based
+// generator (splitmix64 of (seed, index)) and Box–Muller — the same numbers
+// for a given seed on every run and every GPU, without a host RNG pass over
+// M·b values (72 M at C4).
+__global__ void gaussian_block_kernel(double* __restrict__ v, int64_t count, uint64_t seed) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  auto mix = [](uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  };
+  const uint64_t h1 = mix(seed ^ mix(static_cast<uint64_t>(i) * 2));
+  const uint64_t h2 = mix(seed ^ mix(static_cast<uint64_t>(i) * 2 + 1));
+  const double u1 = (static_cast<double>(h1 >> 11) + 0.5) * 0x1p-53;  // (0, 1)
+  const double u2 = static_cast<double>(h2 >> 11) * 0x1p-53;
+  v[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+
 void gram_matmul(const double* x, int64_t m, int d, double beta, const double* v, int64_t b,
                  double* y, cudaStream_t stream) {
   const double inv = 1.0 / (2.0 * beta * beta);
@@ -199,16 +219,10 @@ void topk_eigensolve(cusolverDnHandle_t solver, cublasHandle_t blas, const doubl
     FCPD_CUDA(cudaMalloc(&w, sizeof(double) * m * b));
     FCPD_CUDA(cudaMalloc(&t, sizeof(double) * b * b));
     FCPD_CUDA(cudaMalloc(&evals, sizeof(double) * b));
-    // deterministic Gaussian start block (seeded host RNG, uploaded once)
-    {
-      std::vector<double> h(static_cast<size_t>(m * b));
-      std::mt19937_64 rng(seed ^ 0x9E3779B97F4A7C15ull);
-      std::normal_distribution<double> nd(0.0, 1.0);
-      for (auto& e : h) e = nd(rng);
-      FCPD_CUDA(cudaMemcpyAsync(v, h.data(), sizeof(double) * m * b, cudaMemcpyHostToDevice,
-                                stream));
-      FCPD_CUDA(cudaStreamSynchronize(stream));
-    }
+    // deterministic Gaussian start block (device counter-based RNG)
+    gaussian_block_kernel<<<ceil_div(m * b, 256), 256, 0, stream>>>(v, m * b,
+                                                                    seed ^ 0x9E3779B97F4A7C15ull);
+    FCPD_LAUNCH_CHECK();
     Orth orth(solver, m, b, v);
     orth.run(v);
     for (int it = 0; it < iterations; ++it) {

@@ -38,8 +38,6 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], 
 }
 
 constexpr int kCols = 256;      // staged scene points per CTA (shared memory)
-constexpr int kRowTiles = 4;    // 16-row tiles per warp
-constexpr int kWarps = 4;
 constexpr int kReps = 64;       // passes over the staged points
 
 struct Feat {  // per column: B fragment words by t (k = t, t+4, 8+t, 12+t) and sums features
@@ -47,7 +45,8 @@ struct Feat {  // per column: B fragment words by t (k = t, t+4, 8+t, 12+t) and 
 };
 
 // rows: v (x,y,z) per row; cols: u (x,y,z), c per column
-__global__ void __launch_bounds__(kWarps * 32, 2)
+template <int kRowTiles, int kWarps, int kMinBlocks, int kUnroll>
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     pass2_hmma(const float4* __restrict__ rows, const float4* __restrict__ cols, int nrows,
                float* __restrict__ out, long long* cycles, float* __restrict__ logits_out) {
   __shared__ unsigned bfrag[kCols / 8][4][8][4];   // [tile][t][g][j]
@@ -108,7 +107,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       s0[rt][h] = sx[rt][h] = sy[rt][h] = sz[rt][h] = sv[rt][h] = make_float2(0.f, 0.f);
   const long long c0 = clock64();
   for (int rep = 0; rep < kReps; ++rep) {
-#pragma unroll 2
+#pragma unroll kUnroll
     for (int tile = 0; tile < kCols / 8; ++tile) {
       const uint4 bb = *reinterpret_cast<const uint4*>(&bfrag[tile][t][g][0]);
       const float4 f0 = feat[tile][2 * t], f1 = feat[tile][2 * t + 1];
@@ -148,10 +147,36 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
   if (tid == 0) cycles[blockIdx.x] = c1 - c0;
 }
 
+template <int RT, int W, int MB, int UN>
+void run(const char* name, int sms, const float4* dr, const float4* dc, int nrows, float* dout,
+         long long* dcyc) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass2_hmma<RT, W, MB, UN>, W * 32, 0);
+  const int blocks = sms * occ * 4;
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    pass2_hmma<RT, W, MB, UN><<<blocks, W * 32>>>(dr, dc, nrows, dout, dcyc, nullptr);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  const double pairs = double(blocks) * W * RT * 128.0 * (kCols / 8) * kReps;
+  const double ps = pairs / (best * 1e-3);
+  std::printf("%-22s occ=%d warps/SM=%2d  %.3f ms  %.3g pairs/s  %.1f cycles/64 pairs/SMSP @1965  %s\n",
+              name, occ, occ * W, best, ps, 64.0 / (ps / (sms * 4.0 * 1.965e9)),
+              cudaGetErrorString(cudaGetLastError()));
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int nrows = 4096;
+  const int nrows = 8192;
   std::mt19937 rng(1);
   std::uniform_real_distribution<float> U(-2.f, 2.f), B(-8.f, 0.f);
   std::vector<float4> hr(nrows), hc(kCols);
@@ -159,7 +184,7 @@ int main() {
   // c = b − |u|² chosen so that L' = 2v·u + c ranges over [-40, 0]
   for (auto& c : hc) {
     const float ux = U(rng), uy = U(rng), uz = U(rng);
-    c = make_float4(ux, uy, uz, B(rng) - 2.f * (std::fabs(ux) + std::fabs(uy) + std::fabs(uz)) * 2.f);
+    c = make_float4(ux, uy, uz, B(rng) - 4.f * (std::fabs(ux) + std::fabs(uy) + std::fabs(uz)));
   }
   float4 *dr, *dc;
   float *dout, *dlog;
@@ -168,22 +193,21 @@ int main() {
   cudaMalloc(&dc, sizeof(float4) * kCols);
   cudaMemcpy(dr, hr.data(), sizeof(float4) * nrows, cudaMemcpyHostToDevice);
   cudaMemcpy(dc, hc.data(), sizeof(float4) * kCols, cudaMemcpyHostToDevice);
-  const int blocks = sms * 2 * 4;
-  cudaMalloc(&dout, sizeof(float) * blocks * kWarps * 32);
-  cudaMalloc(&dcyc, sizeof(long long) * blocks);
-  const size_t nlog = static_cast<size_t>(blocks) * kWarps * kRowTiles * 16 * kCols;
+  cudaMalloc(&dout, sizeof(float) * sms * 64 * 1024);
+  cudaMalloc(&dcyc, sizeof(long long) * sms * 64);
+  constexpr int kWarps = 4, kRowTiles = 4;
+  const size_t nlog = static_cast<size_t>(kWarps) * kRowTiles * 16 * kCols;
   cudaMalloc(&dlog, sizeof(float) * nlog);
-  // precision run (first block's logits vs fp64)
-  pass2_hmma<<<1, kWarps * 32>>>(dr, dc, nrows, dout, dcyc, dlog);
+  // precision run (one block's logits vs fp64)
+  pass2_hmma<4, 4, 2, 2><<<1, 4 * 32>>>(dr, dc, nrows, dout, dcyc, dlog);
   cudaDeviceSynchronize();
-  std::vector<float> lg(static_cast<size_t>(kWarps) * kRowTiles * 16 * kCols);
+  std::vector<float> lg(nlog);
   cudaMemcpy(lg.data(), dlog, sizeof(float) * lg.size(), cudaMemcpyDeviceToHost);
   double maxerr = 0.0, maxerr_f32 = 0.0, bias = 0.0;
   for (int r = 0; r < kWarps * kRowTiles * 16; ++r)
     for (int n = 0; n < kCols; ++n) {
       const float4 v = hr[r % nrows], u = hc[n];
       const double ref = 2.0 * (double(v.x) * u.x + double(v.y) * u.y + double(v.z) * u.z) + u.w;
-      // the current kernel's fp32 FFMA chain for comparison
       float f = std::fmaf(2.f * v.x, u.x, u.w);
       f = std::fmaf(2.f * v.y, u.y, f);
       f = std::fmaf(2.f * v.z, u.z, f);
@@ -193,26 +217,14 @@ int main() {
       bias += e;
     }
   std::printf("logit |err| max: hmma %.3g  fp32-ffma %.3g  (log2 units; mean hmma err %.3g)\n",
-              maxerr, maxerr_f32, bias / (kWarps * kRowTiles * 16.0 * kCols));
-  for (int rep = 0; rep < 3; ++rep) {
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0);
-    pass2_hmma<<<blocks, kWarps * 32>>>(dr, dc, nrows, dout, dcyc, nullptr);
-    cudaEventRecord(e1);
-    cudaEventSynchronize(e1);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    long long cyc = 0;
-    cudaMemcpy(&cyc, dcyc, sizeof cyc, cudaMemcpyDeviceToHost);
-    const double pairs = double(blocks) * kWarps * kRowTiles * 128.0 * (kCols / 8) * kReps;
-    // per SMSP: pairs / (SMs·4) over the elapsed cycles of one CTA
-    const double per_smsp = pairs / (sms * 4.0);
-    std::printf("blocks=%d  %.3f ms  CTA0 %lld cycles  %.2f cycles/64 pairs/SMSP (by clock), "
-                "%.3g pairs/s  err=%s\n",
-                blocks, ms, cyc, cyc / (per_smsp / 64.0) / (blocks / (sms * 2.0)),
-                pairs / (ms * 1e-3), cudaGetErrorString(cudaGetLastError()));
-  }
+              maxerr, maxerr_f32, bias / (double(kWarps) * kRowTiles * 16.0 * kCols));
+  run<4, 4, 2, 2>("rt4 w4 mb2 un2", sms, dr, dc, nrows, dout, dcyc);
+  run<4, 4, 2, 1>("rt4 w4 mb2 un1", sms, dr, dc, nrows, dout, dcyc);
+  run<2, 4, 3, 2>("rt2 w4 mb3 un2", sms, dr, dc, nrows, dout, dcyc);
+  run<2, 8, 2, 2>("rt2 w8 mb2 un2", sms, dr, dc, nrows, dout, dcyc);
+  run<2, 8, 2, 4>("rt2 w8 mb2 un4", sms, dr, dc, nrows, dout, dcyc);
+  run<1, 8, 3, 4>("rt1 w8 mb3 un4", sms, dr, dc, nrows, dout, dcyc);
+  run<1, 16, 1, 4>("rt1 w16 mb1 un4", sms, dr, dc, nrows, dout, dcyc);
+  run<1, 4, 6, 8>("rt1 w4 mb6 un8", sms, dr, dc, nrows, dout, dcyc);
   return 0;
 }
