@@ -174,6 +174,30 @@ __device__ __forceinline__ float2 ex2x2(float2 v) {
   return make_float2(ex2_approx(v.x), ex2_approx(v.y));
 }
 
+// 2^x on the FMA pipe for two lanes (the MUFU-bound pass 1 leaves its FP32
+// pipe ~60 % idle): x = r + f with r = round(x) by the 1.5·2^23 trick and
+// f ∈ [−½, ½]; 2^f by a degree-5 polynomial (max relative error 3.5e-7 in
+// fp32 Horner; MUFU ex2.approx: ~2.4e-7); 2^r added to the exponent bits.
+// x is clamped to ≥ −125 (smaller terms are < 2^-125 — the flush-to-zero
+// MUFU returns 0 there; both are far below the column-total guard).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5·2^23
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
+  float2 p = __ffma2_rn(make_float2(0.0012915669940412045f, 0.0012915669940412045f), f,
+                        make_float2(0.009668530896306038f, 0.009668530896306038f));
+  p = __ffma2_rn(p, f, make_float2(0.055516887456178665f, 0.055516887456178665f));
+  p = __ffma2_rn(p, f, make_float2(0.24022264778614044f, 0.24022264778614044f));
+  p = __ffma2_rn(p, f, make_float2(0.6931464672088623f, 0.6931464672088623f));
+  p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
+  // t's low mantissa bits hold r (two's complement); << 23 moves it to the exponent
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -314,7 +338,9 @@ __device__ __forceinline__ void col_b_ranges(const ColFix& f, int rb, int64_t n,
 // NC column pairs per thread; the CTA (128/NC threads) owns the 256-column
 // block.  NC = 2 shares every staged model point's shared-memory operands
 // between two packed column pairs (fewer LDS per pair).
-template <int NC>
+// POLY of every 8 staged points take their ex2 on the FMA pipe (ex2_poly2)
+// in the centred form: MUFU and FP32 balance at 2 (1/16·¾ = (4 + 8·¼)/128).
+template <int NC, int POLY>
 __global__ void __launch_bounds__(128 / NC, NC == 2 ? 16 : 8)
     estep_col_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4,
                      int64_t n, IterState* __restrict__ st, WorkList wl_in,
@@ -434,7 +460,7 @@ __global__ void __launch_bounds__(128 / NC, NC == 2 ? 16 : 8)
               float2 e = __ffma2_rn(ox[q2], make_float2(va.x, va.y), make_float2(vb.z, vb.w));
               e = __ffma2_rn(oy[q2], make_float2(va.z, va.w), e);
               e = __ffma2_rn(oz[q2], make_float2(vb.x, vb.y), e);
-              f[q2] = __fadd2_rn(f[q2], ex2x2(e));
+              f[q2] = __fadd2_rn(f[q2], u < POLY ? ex2_poly2(e) : ex2x2(e));
             }
           }
         }
@@ -1521,10 +1547,11 @@ EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
   // prefer more, lighter CTAs
   p.col_pairs = ceil_div(m, kTile) * ceil_div(n, kTile) >= 1024 ? 2 : 1;
   if (const char* e = std::getenv("FCPD_COL_PAIRS")) p.col_pairs = std::atoi(e) == 1 ? 1 : 2;
+  if (const char* e = std::getenv("FCPD_EX2_POLY")) p.ex2_poly = std::max(0, std::min(3, std::atoi(e)));
   if (p.col_pairs == 2)
-    FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_col, estep_col_kernel<2>, 64, 0));
+    FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_col, estep_col_kernel<2, 0>, 64, 0));
   else
-    FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_col, estep_col_kernel<1>, 128, 0));
+    FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_col, estep_col_kernel<1, 0>, 128, 0));
   if (const char* e = std::getenv("FCPD_ROW_PAIRS")) p.row_pairs = std::atoi(e) == 1 ? 1 : 2;
   if (p.row_pairs == 2)
     FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_row, estep_row_kernel<2>, 64, 0));
@@ -1637,12 +1664,21 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
     FCPD_LAUNCH_CHECK();
   }
   uint64_t* stamps = cu.enabled ? nullptr : b.stamps;
-  if (p.col_pairs == 2)
-    launch_pdl(estep_col_kernel<2>, dim3(p.col_grid), dim3(64), 0, stream, b.xt4, m, b.y4b, n, st,
-               wl, b.col_seg, p.centred_max_r2, forms, stamps);
-  else
-    launch_pdl(estep_col_kernel<1>, dim3(p.col_grid), dim3(128), 0, stream, b.xt4, m, b.y4b, n, st,
-               wl, b.col_seg, p.centred_max_r2, forms, stamps);
+  auto col = [&](auto kernel, int threads) {
+    launch_pdl(kernel, dim3(p.col_grid), dim3(threads), 0, stream, b.xt4, m,
+               static_cast<const float4*>(b.y4b), n, st, wl, b.col_seg, p.centred_max_r2, forms,
+               stamps);
+  };
+  if (p.col_pairs == 2) {
+    switch (p.ex2_poly) {
+      case 1: col(estep_col_kernel<2, 1>, 64); break;
+      case 2: col(estep_col_kernel<2, 2>, 64); break;
+      case 3: col(estep_col_kernel<2, 3>, 64); break;
+      default: col(estep_col_kernel<2, 0>, 64); break;
+    }
+  } else {
+    col(estep_col_kernel<1, 0>, 128);
+  }
   FCPD_LAUNCH_CHECK();
   launch_pdl(estep_col_combine_kernel, dim3(p.col_blocks), dim3(kTile), 0, stream,
              static_cast<const double*>(b.col_seg), wl, p.col_grid, m, n, fix, b.xt4, st,

@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kBulkThreads, kBulkCtasPerSm)
 // a unit's kRdRows × 4 KB row pieces into a 32 KB stage of a 3-stage ring
 // (L2 evict-first); 8 consumer warps: each thread owns 4 columns, reads
 // their R once per unit (float4 per column, L2-resident) and keeps
-// kRdRows × 3 sums for the current row group (fp32 over 4 units' 16
+// kRdRows × 3 sums for the current row group (fp32 over the unit's 4
 // products per column thread, then fp64).  When the CTA leaves a row group it reduces its threads in a
 // fixed order into one partial slot; rowdot_reduce sums a row's slots in
 // CTA order — bitwise reproducible.
@@ -494,8 +494,9 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
 
   // ------------------------------------------------ consumer warps
   __shared__ double red[kBulkConsumers / 32][kRdSlot];
-  // fp32 sums over kRdBatch units (16 products per column thread), then fp64
-  constexpr int kRdBatch = 4;
+  // fp32 sums over kRdBatch units (4 products per column thread each), then
+  // fp64 (4 units: 1e-6 worse σ² agreement with the fused path at C0, no speed-up)
+  constexpr int kRdBatch = 1;
   double acc[kRdRows][3];
   float accf[kRdRows][3];
 #pragma unroll
