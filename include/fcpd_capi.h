@@ -194,7 +194,8 @@ FCPD_API int fcpd_build_basis(fcpd_ctx* ctx, const double* x, int64_t m, int32_t
 
 /* Top-K eigenpairs of Φ without forming it (configs 2–4): randomized block
  * subspace iteration with on-the-fly fp64 Φ·V products + Rayleigh–Ritz,
- * `iterations` power steps (0 → default 4).  Same outputs and clamp as
+ * `iterations` power steps; 0 → up to 4, stopping once every top-K Ritz
+ * residual ‖Φu − θu‖ ≤ 1e-11·θ₁.  Same outputs and clamp as
  * fcpd_build_basis. */
 FCPD_API int fcpd_build_basis_topk(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d,
                                    double beta, int64_t rank, int32_t iterations, double* u,

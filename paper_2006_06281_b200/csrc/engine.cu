@@ -389,14 +389,20 @@ int64_t lowrank_rank(double fraction, int64_t m) {  // solvers.hpp:46-54
 
 constexpr int64_t kDenseEigLimit = 46000;          // M×M fp64 + syevd workspace fit
 constexpr int64_t kDenseEigLimitLowrank = 16384;   // above: on-the-fly top-K solver
-// power steps of the top-K subspace iteration (FCPD_TOPK_ITERS overrides).
-// Two leave the full-size C2/C4 residuals at the fp64 floor but not the
-// eigenpairs near rank K at small M (K/M = 2 %: eigenvalues off by 2e-10·λ₁,
-// a top-K registration 2.7e-4 from the dense-basis one); four meet both
+// power steps of the top-K subspace iteration, at most (FCPD_TOPK_ITERS
+// overrides).  The solver stops early once every top-K Ritz residual is at
+// 1e-11·θ₁ (topk.cu; FCPD_TOPK_ADAPTIVE=0 runs all steps): two steps reach
+// the fp64 floor at full C2/C4 size but not the eigenpairs near rank K at
+// small M (K/M = 2 %: eigenvalues off by 2e-10·λ₁, a top-K registration
+// 2.7e-4 from the dense-basis one), which four meet
 constexpr int kTopkIterations = 4;
 int topk_iterations() {
   if (const char* e = std::getenv("FCPD_TOPK_ITERS")) return std::max(0, std::atoi(e));
   return kTopkIterations;
+}
+bool topk_adaptive() {
+  const char* e = std::getenv("FCPD_TOPK_ADAPTIVE");
+  return !(e && e[0] == '0');
 }
 
 void ensure_basis(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa) {
@@ -426,7 +432,7 @@ void ensure_basis(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa) {
   if (lowrank && s.m > topk_min) {
     const auto t1 = Clock::now();
     topk_eigensolve(ctx->solver, ctx->blas, s.x0.p, s.m, s.d, s.cfg.beta, rank,
-                    topk_iterations(), s.cfg.seed, b, ctx->stream);
+                    topk_iterations(), topk_adaptive(), s.cfg.seed, b, ctx->stream);
     upload_lambda(b, false, ctx->stream);
     s.t_gram = 0.0;
     s.t_eig = since(t1);
@@ -2156,7 +2162,8 @@ int fcpd_build_basis_topk(fcpd_ctx* ctx, const double* x, int64_t m, int32_t d, 
     FCPD_CUDA(cudaMemcpyAsync(xd.p, x, sizeof(double) * d * m, cudaMemcpyHostToDevice, ctx->stream));
     Basis b;
     topk_eigensolve(ctx->solver, ctx->blas, xd.p, m, d, beta, rank,
-                    iterations > 0 ? iterations : topk_iterations(), 0, b, ctx->stream, u);
+                    iterations > 0 ? iterations : topk_iterations(),
+                    iterations <= 0 && topk_adaptive(), 0, b, ctx->stream, u);
     if (lambda) std::copy(b.lam_host.begin(), b.lam_host.end(), lambda);
     if (lambda_raw) std::copy(b.lam_raw_host.begin(), b.lam_raw_host.end(), lambda_raw);
     b.release();

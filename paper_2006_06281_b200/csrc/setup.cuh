@@ -43,10 +43,18 @@ void pack_basis_from(Basis& b, const double* u_dev, int64_t m, int64_t k, int re
                      const std::vector<double>& lam_raw, cudaStream_t stream);
 
 // topk.cu — on-the-fly Gram products and the randomized block eigensolver.
+// Φ·V tile geometry: col_blocks blocks of 128 columns, Vᵀ padded to
+// m_pad × ldv
+struct GramPlan {
+  int64_t col_blocks = 1, ldv = 0, m_pad = 0;
+};
+GramPlan make_gram_plan(int64_t m, int64_t b);
+// Y = Φ V (V, Y: M×b column-major); vt: m_pad × ldv scratch
 void gram_matmul(const double* x, int64_t m, int d, double beta, const double* v, int64_t b,
-                 double* y, cudaStream_t stream);
+                 double* y, double* vt, const GramPlan& g, cudaStream_t stream);
 void topk_eigensolve(cusolverDnHandle_t solver, cublasHandle_t blas, const double* x_dev,
-                     int64_t m, int d, double beta, int64_t rank, int iterations, uint64_t seed,
-                     Basis& b_out, cudaStream_t stream, double* u_host_out = nullptr);
+                     int64_t m, int d, double beta, int64_t rank, int iterations, bool adaptive,
+                     uint64_t seed, Basis& b_out, cudaStream_t stream,
+                     double* u_host_out = nullptr, int* products_out = nullptr);
 
 }  // namespace fcpd
