@@ -1425,6 +1425,68 @@ void prepare_rank(fcpd_ctx* c, int rank, int world, const std::vector<double>& x
   FCPD_CUDA(cudaStreamSynchronize(str));
 }
 
+// The top-K basis of a low-rank rank group (configs 2–4 sharded): one
+// randomized eigensolve for the group with its Φ·V products row-sharded
+// over the ranks (topk.cu gram_matmul_sharded: each rank its M/G rows, an
+// all-gather), installed in every rank's context under the key
+// ensure_basis looks up, so prepare_rank finds it cached.  Returns the
+// solve's wall time (0: not this path, or already cached).
+double group_topk_basis(fcpd_ctx* lead, const std::vector<fcpd_ctx*>& R,
+                        const std::vector<double>& xs_in, int64_t m, int d,
+                        const fcpd_config& cfg) {
+  Comm& comm = *lead->comm_obj;
+  if (comm.world < 2 || cfg.variant != FCPD_VARIANT_FAST_LOWRANK) return 0.0;
+  int64_t topk_min = kDenseEigLimitLowrank;
+  if (const char* e = std::getenv("FCPD_TOPK_MIN_M")) topk_min = std::atoll(e);
+  if (m <= topk_min) return 0.0;
+  if (!(cfg.beta > 0.0)) throw Failure(FCPD_ERR_PARAMETER, "build_gram: beta must be positive");
+  const int64_t rank = lowrank_rank(cfg.rank_fraction, m);
+  std::vector<double> xs = xs_in;
+  spatial_sort_cached(xs, m, lead->sort_x);  // the order prepare_rank uses
+  uint64_t h = fnv1a(xs.data(), sizeof(double) * xs.size());
+  h = fnv1a(&m, sizeof m, h);
+  h = fnv1a(&rank, sizeof rank, h);
+  std::vector<std::vector<double>> need(R.size(), std::vector<double>(1, 0.0));
+  for (size_t i = 0; i < R.size(); ++i) {
+    const Basis& b = R[i]->basis;
+    const bool hit = b.q && b.key_hash == h && b.key_beta == cfg.beta && b.m == m &&
+                     b.k == rank && b.key_variant == cfg.variant;
+    need[i][0] = hit ? 0.0 : 1.0;
+  }
+  comm.host_all_reduce(need, true, lead->stream);  // every rank takes the same branch
+  if (need[0][0] == 0.0) return 0.0;
+  const auto t1 = Clock::now();
+  DevBuf<double> xd;
+  xd.ensure(3 * static_cast<size_t>(m));
+  FCPD_CUDA(cudaMemcpyAsync(xd.p, xs.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice,
+                            lead->stream));
+  GramShards sh;
+  sh.comm = &comm;
+  std::vector<Basis*> also;
+  for (size_t i = 0; i < R.size(); ++i) {
+    sh.ranks.push_back(lead->loop_ranks.empty() ? lead->rank : static_cast<int>(i));
+    R[i]->basis.release();
+    if (i > 0) also.push_back(&R[i]->basis);
+  }
+  topk_eigensolve(lead->solver, lead->blas, xd.p, m, d, cfg.beta, rank, topk_iterations(),
+                  topk_adaptive(), cfg.seed, lead->basis, lead->stream, nullptr, nullptr, &sh,
+                  &also);
+  FCPD_CUDA(cudaStreamSynchronize(lead->stream));
+  xd.release();
+  const double t = since(t1);
+  for (fcpd_ctx* c : R) {
+    Basis& b = c->basis;
+    upload_lambda(b, false, lead->stream);
+    b.key_hash = h;
+    b.key_beta = cfg.beta;
+    b.key_variant = cfg.variant;
+    b.t_gram = 0.0;
+    b.t_eig = t;
+  }
+  FCPD_CUDA(cudaStreamSynchronize(lead->stream));
+  return t;
+}
+
 // shards: per local rank, (pointer to its SoA scene shard, count)
 void session_begin_group(fcpd_ctx* lead, const double* x, int64_t m,
                          const std::vector<std::pair<const double*, int64_t>>& shards, int d,
@@ -1509,6 +1571,7 @@ void session_begin_group(fcpd_ctx* lead, const double* x, int64_t m,
   }
   if (cfg.iterations > 0 && !(cfg.omega >= 0.0 && cfg.omega < 1.0))
     throw Failure(FCPD_ERR_NUMERIC, "register: iteration 0: posterior: omega must lie in [0, 1)");
+  const double t_group_eig = group_topk_basis(lead, R, xs, m, d, cfg);
   for (size_t i = 0; i < R.size(); ++i) {
     const int rank = lead->loop_ranks.empty() ? lead->rank : static_cast<int>(i);
     prepare_rank(R[i], rank, G, xs, m, ys[i], shards[i].second, n_global, ystats, d, cfg,
@@ -1516,6 +1579,10 @@ void session_begin_group(fcpd_ctx* lead, const double* x, int64_t m,
     Session& s = R[i]->sess;
     for (int c = 0; c < 3; ++c) s.center[c] = center[c];
     s.scale = scale;
+    if (t_group_eig > 0.0) {  // built above for the group, not reused from a cache
+      s.basis_reused = false;
+      s.t_eig = t_group_eig;
+    }
   }
   // one EM iteration of the whole group as a CUDA graph on the lead stream;
   // the fallback exchange behind a conditional node where the backend

@@ -8,6 +8,8 @@
 
 #include <vector>
 
+#include "comm.cuh"
+
 namespace fcpd {
 
 // Device-resident spectral basis, packed for the streaming M-step.
@@ -43,6 +45,15 @@ void pack_basis_from(Basis& b, const double* u_dev, int64_t m, int64_t k, int re
                      const std::vector<double>& lam_raw, cudaStream_t stream);
 
 // topk.cu — on-the-fly Gram products and the randomized block eigensolver.
+// A rank group's products are row-sharded: `ranks` are the
+// global ranks this process drives (one for NCCL, all for a loopback group).
+struct GramShards {
+  Comm* comm = nullptr;
+  std::vector<int> ranks;
+  int64_t block_rows(int64_t m) const {
+    return ceil_div(ceil_div(m, static_cast<int64_t>(comm->world)), int64_t(64)) * 64;
+  }
+};
 // Φ·V tile geometry: col_blocks blocks of 128 columns, Vᵀ padded to
 // m_pad × ldv
 struct GramPlan {
@@ -55,6 +66,11 @@ void gram_matmul(const double* x, int64_t m, int d, double beta, const double* v
 void topk_eigensolve(cusolverDnHandle_t solver, cublasHandle_t blas, const double* x_dev,
                      int64_t m, int d, double beta, int64_t rank, int iterations, bool adaptive,
                      uint64_t seed, Basis& b_out, cudaStream_t stream,
-                     double* u_host_out = nullptr, int* products_out = nullptr);
+                     double* u_host_out = nullptr, int* products_out = nullptr,
+                     const GramShards* shards = nullptr,
+                     const std::vector<Basis*>* also_out = nullptr);
+void gram_matmul_sharded(const double* x, int64_t m, int d, double beta, const double* v,
+                         int64_t b, double* y, double* vt, const GramPlan& g, double* wpm,
+                         const GramShards& sh, cudaStream_t stream);
 
 }  // namespace fcpd

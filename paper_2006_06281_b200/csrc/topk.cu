@@ -175,11 +175,29 @@ __global__ void transpose_pad_kernel(const double* __restrict__ v, int64_t m, in
   }
 }
 
+// Wᵀ (point-major, ld ldv) → W (M×b column-major, ld m).
+__global__ void untranspose_kernel(const double* __restrict__ wt, int64_t ldv, int64_t m,
+                                   int64_t b, double* __restrict__ w) {
+  __shared__ double tile[32][33];
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * 32, c0 = static_cast<int64_t>(blockIdx.y) * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t j = j0 + r, c = c0 + threadIdx.x;
+    tile[r][threadIdx.x] = (j < m && c < b) ? wt[j * ldv + c] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t c = c0 + r, j = j0 + threadIdx.x;
+    if (c < b && j < m) w[c * m + j] = tile[threadIdx.x][r];
+  }
+}
+
 namespace {
 constexpr int kGdRows = 64;    // CTA rows (2 row warps × 32)
 constexpr int kGdChunk = 16;   // reduction points per pipeline stage
 constexpr int kGdPhiPitch = kGdChunk + 4;  // ≡ 4 (mod 16) doubles: A fragments in 2 wavefronts
 constexpr int kGdCols = 128;   // CTA columns (2 column warps × 64)
+constexpr size_t kGdSmem =
+    sizeof(double) * (2 * kGdRows * kGdPhiPitch + 2 * kGdChunk * (kGdCols + 8) + 2 * 4 * kGdChunk);
 
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -234,7 +252,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __global__ void __launch_bounds__(128, 3)
     gram_dmma_kernel(const double* __restrict__ x, const double* __restrict__ xq, int64_t m,
                      int d, double inv2b2, const double* __restrict__ vt, int64_t ldv,
-                     int64_t m_pad, int64_t b, double* __restrict__ y) {
+                     int64_t m_pad, int64_t b, int64_t row_begin, int64_t row_end,
+                     double* __restrict__ y, int point_major) {
   constexpr int kThreads = 128;
   constexpr int kCols = kGdCols;
   constexpr int kVPitch = kCols + 8;         // ≡ 8 (mod 16) doubles: B fragments in 2 wavefronts
@@ -247,9 +266,10 @@ __global__ void __launch_bounds__(128, 3)
   __shared__ double exp2_tab[64];                          // 2^(i/64)
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int wr = warp & 1, wc = warp >> 1;
-  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kGdRows;
+  const int64_t row0 = row_begin + static_cast<int64_t>(blockIdx.x) * kGdRows;
   const int64_t col0 = static_cast<int64_t>(blockIdx.y) * kCols;
   const int64_t nchunks = m_pad / kGdChunk;
+  const int64_t rows_end = min(row_end, m);
 
   // own rows as (2·inv·x_i, −inv·|x_i|²): a_ij = c_i + c_j + x_i'·x_j
   // (absolute error ≈ 1e-16·inv·(|x_i|² + |x_j|²) in a = relative in Φ_ij)
@@ -347,16 +367,23 @@ __global__ void __launch_bounds__(128, 3)
       __syncthreads();
     }
   }
-  // C fragment: row lane >> 2, columns 2·(lane & 3) + {0, 1}
+  // C fragment: row lane >> 2, columns 2·(lane & 3) + {0, 1}; column-major
+  // M×b (ld m), or point-major rows [row_begin, row_end) (ld ldv) for the
+  // row-sharded product's all-gather
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     const int64_t r = row0 + wr * 32 + 8 * a + (lane >> 2);
-    if (r >= m) continue;
+    if (r >= rows_end) continue;
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
       const int64_t c = col0 + wc * 64 + 8 * n + 2 * (lane & 3);
-      if (c < b) y[c * m + r] = acc[a][n][0];
-      if (c + 1 < b) y[(c + 1) * m + r] = acc[a][n][1];
+      if (point_major) {
+        *reinterpret_cast<double2*>(y + (r - row_begin) * ldv + c) =
+            make_double2(acc[a][n][0], acc[a][n][1]);
+      } else {
+        if (c < b) y[c * m + r] = acc[a][n][0];
+        if (c + 1 < b) y[(c + 1) * m + r] = acc[a][n][1];
+      }
     }
   }
 }
@@ -414,6 +441,37 @@ GramPlan make_gram_plan(int64_t m, int64_t b) {
   return g;
 }
 
+static void gram_prepare(const double* x, int64_t m, int d, double inv, const double* v,
+                         int64_t b, double* vt, const GramPlan& g, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    double tab[64];
+    for (int i = 0; i < 64; ++i) tab[i] = std::exp2(i / 64.0);
+    FCPD_CUDA(cudaMemcpyToSymbol(c_exp2_64, tab, sizeof tab));
+    FCPD_CUDA(cudaFuncSetAttribute(gram_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(kGdSmem)));
+    attr = true;
+  }
+  dim3 tg(static_cast<unsigned>(ceil_div(g.m_pad, 32)), static_cast<unsigned>(ceil_div(g.ldv, 32)));
+  transpose_pad_kernel<<<tg, dim3(32, 8), 0, stream>>>(v, m, b, vt, g.m_pad, g.ldv);
+  FCPD_LAUNCH_CHECK();
+  double* xq = vt + g.m_pad * g.ldv;  // scratch tail of vt (m_pad doubles)
+  gram_rownorm_kernel<<<static_cast<unsigned>(ceil_div(g.m_pad, 256)), 256, 0, stream>>>(
+      x, m, d, inv, g.m_pad, xq);
+  FCPD_LAUNCH_CHECK();
+}
+
+static void gram_rows(const double* x, int64_t m, int d, double inv, const double* vt,
+                      const GramPlan& g, int64_t b, int64_t r0, int64_t r1, double* y,
+                      int point_major, cudaStream_t stream) {
+  if (r1 <= r0) return;
+  const double* xq = vt + g.m_pad * g.ldv;
+  dim3 grid(static_cast<unsigned>(ceil_div(r1 - r0, kGdRows)), static_cast<unsigned>(g.col_blocks));
+  gram_dmma_kernel<<<grid, 128, kGdSmem, stream>>>(x, xq, m, d, inv, vt, g.ldv, g.m_pad, b, r0, r1,
+                                                   y, point_major);
+  FCPD_LAUNCH_CHECK();
+}
+
 void gram_matmul(const double* x, int64_t m, int d, double beta, const double* v, int64_t b,
                  double* y, double* vt, const GramPlan& g, cudaStream_t stream) {
   const double inv = 1.0 / (2.0 * beta * beta);
@@ -430,26 +488,32 @@ void gram_matmul(const double* x, int64_t m, int d, double beta, const double* v
     FCPD_LAUNCH_CHECK();
     return;
   }
-  dim3 tg(static_cast<unsigned>(ceil_div(g.m_pad, 32)), static_cast<unsigned>(ceil_div(g.ldv, 32)));
-  transpose_pad_kernel<<<tg, dim3(32, 8), 0, stream>>>(v, m, b, vt, g.m_pad, g.ldv);
-  FCPD_LAUNCH_CHECK();
-  constexpr size_t smem = sizeof(double) * (2 * kGdRows * kGdPhiPitch +
-                                            2 * kGdChunk * (kGdCols + 8) + 2 * 4 * kGdChunk);
-  static bool attr = false;
-  if (!attr) {
-    double tab[64];
-    for (int i = 0; i < 64; ++i) tab[i] = std::exp2(i / 64.0);
-    FCPD_CUDA(cudaMemcpyToSymbol(c_exp2_64, tab, sizeof tab));
-    FCPD_CUDA(cudaFuncSetAttribute(gram_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    attr = true;
+  gram_prepare(x, m, d, inv, v, b, vt, g, stream);
+  gram_rows(x, m, d, inv, vt, g, b, 0, m, y, 0, stream);
+}
+
+// Row-sharded W = Φ V over a rank group: each local rank q computes its
+// block of rows [q·rows, (q+1)·rows) point-major into its slice of wpm,
+// an all-gather completes wpm on every rank, and one transpose gives the
+// column-major W the orthonormalisation needs.
+void gram_matmul_sharded(const double* x, int64_t m, int d, double beta, const double* v,
+                         int64_t b, double* y, double* vt, const GramPlan& g, double* wpm,
+                         const GramShards& sh, cudaStream_t stream) {
+  const double inv = 1.0 / (2.0 * beta * beta);
+  const int64_t rows = sh.block_rows(m);
+  gram_prepare(x, m, d, inv, v, b, vt, g, stream);
+  std::vector<const uint32_t*> send;
+  std::vector<uint32_t*> recv;
+  for (int q : sh.ranks) {
+    double* blk = wpm + static_cast<int64_t>(q) * rows * g.ldv;
+    gram_rows(x, m, d, inv, vt, g, b, q * rows, std::min<int64_t>((q + 1) * rows, m), blk, 1,
+              stream);
+    send.push_back(reinterpret_cast<const uint32_t*>(blk));
+    recv.push_back(reinterpret_cast<uint32_t*>(wpm));
   }
-  dim3 grid(static_cast<unsigned>(ceil_div(m, kGdRows)), static_cast<unsigned>(g.col_blocks));
-  double* xq = vt + g.m_pad * g.ldv;  // scratch tail of vt (m_pad doubles)
-  gram_rownorm_kernel<<<static_cast<unsigned>(ceil_div(g.m_pad, 256)), 256, 0, stream>>>(
-      x, m, d, inv, g.m_pad, xq);
-  FCPD_LAUNCH_CHECK();
-  gram_dmma_kernel<<<grid, 128, smem, stream>>>(x, xq, m, d, inv, vt, g.ldv, g.m_pad, b, y);
+  sh.comm->all_gather(send, recv, static_cast<size_t>(rows * g.ldv * 2), stream);
+  dim3 tg(static_cast<unsigned>(ceil_div(m, 32)), static_cast<unsigned>(ceil_div(b, 32)));
+  untranspose_kernel<<<tg, dim3(32, 8), 0, stream>>>(wpm, g.ldv, m, b, y);
   FCPD_LAUNCH_CHECK();
 }
 
@@ -494,7 +558,8 @@ struct Orth {
 void topk_eigensolve(cusolverDnHandle_t solver, cublasHandle_t blas, const double* x_dev,
                      int64_t m, int d, double beta, int64_t rank, int iterations, bool adaptive,
                      uint64_t seed, Basis& b_out, cudaStream_t stream, double* u_host_out,
-                     int* products_out) {
+                     int* products_out, const GramShards* shards,
+                     const std::vector<Basis*>* also_out) {
   if (rank < 1 || rank > m) throw Failure(FCPD_ERR_PARAMETER, "eigendecompose: rank out of [1, M]");
   if (!(beta > 0.0)) throw Failure(FCPD_ERR_PARAMETER, "build_gram: beta must be positive");
   const int64_t over = std::max<int64_t>(16, rank / 5);
@@ -504,7 +569,7 @@ void topk_eigensolve(cusolverDnHandle_t solver, cublasHandle_t blas, const doubl
   FCPD_CUBLAS(cublasSetStream(blas, stream));
 
   double *v = nullptr, *w = nullptr, *t = nullptr, *evals = nullptr, *u = nullptr, *z = nullptr,
-         *res = nullptr, *dwork = nullptr, *vt = nullptr;
+         *res = nullptr, *dwork = nullptr, *vt = nullptr, *wpm = nullptr;
   int* info = nullptr;
   cusolverDnParams_t params = nullptr;
   auto release = [&] {
@@ -517,6 +582,7 @@ void topk_eigensolve(cusolverDnHandle_t solver, cublasHandle_t blas, const doubl
     cudaFree(res);
     cudaFree(dwork);
     cudaFree(vt);
+    cudaFree(wpm);
     cudaFree(info);
     if (params) cusolverDnDestroyParams(params);
   };
@@ -529,6 +595,11 @@ void topk_eigensolve(cusolverDnHandle_t solver, cublasHandle_t blas, const doubl
     FCPD_CUDA(cudaMalloc(&info, sizeof(int)));
     const GramPlan gp = make_gram_plan(m, b);
     FCPD_CUDA(cudaMalloc(&vt, sizeof(double) * gp.m_pad * (gp.ldv + 1)));  // + xq
+    if (shards && shards->comm && shards->comm->world > 1)
+      FCPD_CUDA(cudaMalloc(&wpm, sizeof(double) * shards->block_rows(m) * shards->comm->world *
+                                     gp.ldv));
+    else
+      shards = nullptr;
     // symmetric eigensolver workspace for the b×b Rayleigh quotient
     FCPD_CUSOLVER2(cusolverDnCreateParams(&params));
     size_t dbytes = 0, hbytes = 0;
@@ -548,7 +619,10 @@ void topk_eigensolve(cusolverDnHandle_t solver, cublasHandle_t blas, const doubl
     std::vector<double> hres(rank), hev(b);
     int products = 0;
     for (int step = 0;; ++step) {
-      gram_matmul(x_dev, m, d, beta, v, b, w, vt, gp, stream);  // W = G V
+      if (shards)  // W = G V
+        gram_matmul_sharded(x_dev, m, d, beta, v, b, w, vt, gp, wpm, *shards, stream);
+      else
+        gram_matmul(x_dev, m, d, beta, v, b, w, vt, gp, stream);
       ++products;
       const bool last = step >= iterations;
       if (!last && !(adaptive && step >= 1)) {
@@ -595,7 +669,12 @@ void topk_eigensolve(cusolverDnHandle_t solver, cublasHandle_t blas, const doubl
                                 stream));
       FCPD_CUDA(cudaStreamSynchronize(stream));
       const double tol = kTopkResidualTol * std::fabs(hev[b - 1]);
-      const double worst = *std::max_element(hres.begin(), hres.end());
+      double worst = *std::max_element(hres.begin(), hres.end());
+      if (shards) {  // every rank takes the same decision (the collectives stay in step)
+        std::vector<std::vector<double>> wv(shards->ranks.size(), std::vector<double>(1, worst));
+        shards->comm->host_all_reduce(wv, true, stream);
+        worst = wv[0][0];
+      }
       if (std::getenv("FCPD_TOPK_LOG"))
         std::fprintf(stderr, "topk: M=%lld K=%lld product %d residual %.3e·θ₁\n",
                      static_cast<long long>(m), static_cast<long long>(rank), products,
@@ -620,6 +699,8 @@ void topk_eigensolve(cusolverDnHandle_t solver, cublasHandle_t blas, const doubl
       FCPD_CUDA(cudaStreamSynchronize(stream));
     }
     pack_basis_from(b_out, u, m, rank, /*reverse=*/1, lam_raw, stream);
+    if (also_out)
+      for (Basis* bo : *also_out) pack_basis_from(*bo, u, m, rank, /*reverse=*/1, lam_raw, stream);
   } catch (...) {
     release();
     throw;

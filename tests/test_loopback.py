@@ -53,6 +53,46 @@ def test_loopback_matches_single_gpu(fc, orc, monkeypatch, world, variant, name,
     assert got.sigma2_initial == pytest.approx(ref.sigma2_initial, rel=1e-12)
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_loopback_sharded_topk_basis(fc, monkeypatch, tmp_path, world):
+    """The group's top-K setup with row-sharded Φ·V products (each rank its
+    M/G rows, an all-gather; kernel.hpp:49-72): every output row is summed
+    in the same order as on one GPU, so the basis is the single-GPU one up
+    to the last bits of the group's normalisation statistics, and the
+    registration matches as in the test above."""
+    from paper_2006_06281_b200 import datagen
+    monkeypatch.setenv("FCPD_TOPK_MIN_M", "1000")  # force the top-K path at M = 6000
+    monkeypatch.setenv("FCPD_MSTEP_FUSED", "0")
+    x, y, w = datagen.generate("c2", m=6000)
+    cfg = datagen.config_for(w, iterations=20)
+    cfg.rank_fraction = 0.02
+    with fc.Context(0) as one:
+        ref = one.register(x, y, cfg)
+        one.save_spectral_cache(str(tmp_path / "one.bin"))
+    with fc.Context.loopback(0, world) as grp:
+        got = grp.register(x, y, cfg)
+        grp.save_spectral_cache(str(tmp_path / "grp.bin"))
+    assert got.timing.t_eig > 0.0 and not got.basis_reused
+    def read(path):  # kernel.hpp:85-144 layout
+        raw = path.read_bytes()
+        m, k = np.frombuffer(raw[8:24], dtype=np.uint64)
+        u = np.frombuffer(raw[32:32 + 8 * m * k], dtype=np.float64).reshape(m, k)
+        lam = np.frombuffer(raw[32 + 8 * m * k:32 + 8 * m * k + 8 * k], dtype=np.float64)
+        return u, lam
+    ua, la = read(tmp_path / "one.bin")
+    ub, lb = read(tmp_path / "grp.bin")
+    assert ua.shape == ub.shape
+    assert np.abs(la - lb).max() <= 1e-12 * la[0]
+    z = np.random.default_rng(5).standard_normal((ua.shape[0], 4))
+    pa, pb = ua @ (la[:, None] * (ua.T @ z)), ub @ (lb[:, None] * (ub.T @ z))
+    assert np.abs(pa - pb).max() <= 1e-9 * np.abs(pa).max()
+    rel = np.abs(got.sigma2_trace / ref.sigma2_trace - 1).max()
+    pts = np.abs(got.transformed - ref.transformed).max() / bbox_diag(y)
+    print(f"world {world} sharded top-K: σ² rel {rel:.3g} points {pts:.3g} "
+          f"t_eig group {got.timing.t_eig:.3f} s single {ref.timing.t_eig:.3f} s")
+    assert rel <= 1e-6 and pts <= 1e-7
+
+
 def test_loopback_fallback_rows_match(fc, orc):
     """Model points far from every scene point (their fp32 row mass
     underflows): the group-wide flagged count turns on the conditional
