@@ -233,7 +233,8 @@ constexpr int kStageBytes = 32 * 1024;
 constexpr int kBulkConsumers = kColsumThreads;         // 8 warps
 constexpr int kBulkThreads = kBulkConsumers + 32;      // + producer warp
 constexpr int kBulkMaxChunkRows = 64;
-constexpr int kBulkSmem = kBulkStages * kStageBytes + 2 * kBulkStages * 8;
+constexpr int kBulkVBytes = kBulkMaxChunkRows * 16;   // the chunk's v rows (float4)
+constexpr int kBulkSmem = kBulkStages * (kStageBytes + kBulkVBytes) + 2 * kBulkStages * 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -293,7 +294,8 @@ __global__ void __launch_bounds__(kBulkThreads, kBulkCtasPerSm)
   g = sk_eff(g, st);
   extern __shared__ __align__(128) unsigned char smem[];
   float* ring = reinterpret_cast<float*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBulkStages * kStageBytes);
+  float4* vring = reinterpret_cast<float4*>(smem + kBulkStages * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBulkStages * (kStageBytes + kBulkVBytes));
   uint64_t* empty = full + kBulkStages;
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -309,8 +311,9 @@ __global__ void __launch_bounds__(kBulkThreads, kBulkCtasPerSm)
 
   if (tid >= kBulkConsumers) {  // ---------------- producer warp
     if (tid != kBulkConsumers) return;
-    uint64_t policy;
+    uint64_t policy, policy_v;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy_v));
     SegCursor c{u0, u1, 0, 0, 0};
     int64_t chunk = 0;
     while (c.next_segment(g)) {
@@ -323,7 +326,10 @@ __global__ void __launch_bounds__(kBulkThreads, kBulkCtasPerSm)
         const int s = static_cast<int>(chunk % kBulkStages);
         const uint32_t ph = static_cast<uint32_t>((chunk / kBulkStages) & 1);
         mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], seg_bytes * nr);
+        mbar_expect_tx(&full[s], seg_bytes * nr + 16u * nr);
+        // the chunk's v rows ride along (a broadcast LDG per row stalled the
+        // consumers on an L2 round trip)
+        bulk_g2s(vring + s * kBulkMaxChunkRows, v + r, 16u * nr, &full[s], policy_v);
         float* dst = ring + static_cast<int64_t>(s) * (kStageBytes / 4);
         const float* src = A + r * lda + c.cb * (4 * kColsumThreads);
         if (contiguous) {
@@ -378,18 +384,19 @@ __global__ void __launch_bounds__(kBulkThreads, kBulkCtasPerSm)
             f[j][0] = f[j][1] = f[j][2] = 0.f;
           }
         };
+        const float4* vs = vring + s * kBulkMaxChunkRows;
         int i = 0;
-        for (; i + 8 <= nr; i += 8) {  // 8 independent LDS + 8 broadcast LDG in flight
+        for (; i + 8 <= nr; i += 8) {  // 8 independent LDS + 8 broadcast LDS
           float4 vv[8], q[8];
 #pragma unroll
-          for (int w = 0; w < 8; ++w) vv[w] = __ldg(v + r + i + w);
+          for (int w = 0; w < 8; ++w) vv[w] = vs[i + w];
 #pragma unroll
           for (int w = 0; w < 8; ++w) q[w] = row[(i + w) * stride4];
 #pragma unroll
           for (int w = 0; w < 8; ++w) fma_row(q[w], vv[w]);
           flush();
         }
-        for (; i < nr; ++i) fma_row(row[i * stride4], __ldg(v + r + i));
+        for (; i < nr; ++i) fma_row(row[i * stride4], vs[i]);
         flush();
       }
       __syncwarp();
@@ -415,9 +422,9 @@ __global__ void __launch_bounds__(kBulkThreads, kBulkCtasPerSm)
 // 736 of 1200 bytes per row, 2.3 TB/s).  Work units are (group of
 // kRdRows eigenvector rows, 1024-column block); a persistent stream-K grid
 // splits them evenly in row-group-major order.  A producer warp bulk-copies
-// a unit's kRdRows × 4 KB row pieces into a 32 KB stage of a 3-stage ring
-// (L2 evict-first); 8 consumer warps: each thread owns 4 columns, reads
-// their R once per unit (float4 per column, L2-resident) and keeps
+// a unit's kRdRows × 4 KB row pieces (L2 evict-first) and its 16 KB of R
+// into a stage of a 4-stage ring; 8 consumer warps: each thread owns 4
+// columns, reads their R from the stage and keeps
 // kRdRows × 3 sums for the current row group (fp32 over the unit's 4
 // products per column thread, then fp64).  When the CTA leaves a row group it reduces its threads in a
 // fixed order into one partial slot; rowdot_reduce sums a row's slots in
@@ -426,10 +433,12 @@ namespace {
 constexpr int kRdRows = 8;                        // eigenvector rows per unit
 constexpr int kRdCols = 4 * kColsumThreads;       // 1024 columns per unit
 constexpr int kRdSlot = kRdRows * 3;              // doubles per partial slot
-// one CTA per SM with a 6-stage ring: the 8×3 fp64 sums per thread need the
-// registers of a single resident CTA; 192 KB in flight per SM as colsum_bulk
-constexpr int kRdStages = 6;
-constexpr int kRdSmem = kRdStages * kStageBytes + 2 * kRdStages * 8;
+// one CTA per SM with a 4-stage ring of (32 KB of Qᵀ + the unit's 16 KB of
+// R): the 8×3 fp64 sums per thread need the registers of a single resident
+// CTA; 128 KB of the basis in flight per SM
+constexpr int kRdStages = 4;
+constexpr int kRdRBytes = kRdCols * 16;           // the unit's R columns (float4)
+constexpr int kRdSmem = kRdStages * (kStageBytes + kRdRBytes) + 2 * kRdStages * 8;
 
 __device__ __forceinline__ RdGeom rd_eff(RdGeom g, const IterState* st) {
   if (!g.trunc || !st) return g;
@@ -456,7 +465,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   g = rd_eff(g, st);
   extern __shared__ __align__(128) unsigned char smem[];
   float* ring = reinterpret_cast<float*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRdStages * kStageBytes);
+  float4* rring = reinterpret_cast<float4*>(smem + kRdStages * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRdStages * (kStageBytes + kRdRBytes));
   uint64_t* empty = full + kRdStages;
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -472,8 +482,9 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
 
   if (tid >= kBulkConsumers) {  // ---------------- producer warp
     if (tid != kBulkConsumers) return;
-    uint64_t policy;
+    uint64_t policy, policy_r;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy_r));
     for (int64_t u = u0; u < u1; ++u) {
       const int64_t chunk = u - u0;
       const int s = static_cast<int>(chunk % kRdStages);
@@ -484,7 +495,9 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
       const uint32_t bytes = static_cast<uint32_t>(((ncol + 3) & ~int64_t(3)) * 4);
       const int nrows = static_cast<int>(min(static_cast<int64_t>(kRdRows), g.rows - rg * kRdRows));
       mbar_wait(&empty[s], ph ^ 1);
-      mbar_expect_tx(&full[s], bytes * nrows);
+      const uint32_t rbytes = static_cast<uint32_t>(ncol * 16);
+      mbar_expect_tx(&full[s], bytes * nrows + rbytes);
+      bulk_g2s(rring + s * kRdCols, v + c0, rbytes, &full[s], policy_r);  // R of the unit
       float* dst = ring + static_cast<int64_t>(s) * (kStageBytes / 4);
       for (int r = 0; r < nrows; ++r)
         bulk_g2s(dst + r * kRdCols, A + (rg * kRdRows + r) * g.lda + c0, bytes, &full[s], policy);
@@ -538,17 +551,6 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     ++slot;
   };
   int64_t cur_rg = u0 < u1 ? u0 / g.col_blocks : 0;
-  // R of the thread's 4 columns, one unit ahead (an L2 round trip per unit
-  // otherwise serialises the consumers)
-  auto load_r = [&](int64_t u, float4 (&r)[4]) {
-    const int64_t cb = u % g.col_blocks;
-    const int64_t c0 = cb * kRdCols + 4 * tid;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      r[j] = u < u1 && c0 + j < g.cols ? __ldg(v + c0 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-  };
-  float4 rnext[4];
-  load_r(u0, rnext);
   for (int64_t u = u0; u < u1; ++u) {
     const int64_t chunk = u - u0;
     const int s = static_cast<int>(chunk % kRdStages);
@@ -560,11 +562,14 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     }
     const int64_t c0 = cb * kRdCols + 4 * tid;
     const int nrows = static_cast<int>(min(static_cast<int64_t>(kRdRows), g.rows - rg * kRdRows));
-    float4 rv[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) rv[j] = rnext[j];
-    load_r(u + 1, rnext);
     mbar_wait(&full[s], ph);
+    // R of the thread's 4 columns, staged with the unit (a per-unit L2
+    // round trip otherwise serialises the consumers)
+    float4 rv[4];
+    const float4* rs = rring + s * kRdCols + 4 * tid;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      rv[j] = c0 + j < g.cols ? rs[j] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float4* st4 = reinterpret_cast<const float4*>(ring + static_cast<int64_t>(s) * (kStageBytes / 4));
 #pragma unroll
     for (int r = 0; r < kRdRows; ++r) {
