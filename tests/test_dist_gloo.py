@@ -199,3 +199,88 @@ def test_sharded_em_matches_oracle(orc, world, case):
     # every rank ends with the same full result
     for r in res[1:]:
         assert np.array_equal(res[0][2], r[2])
+
+
+# ---------------------------------------------------------------------------
+# The group's top-K setup (engine.cu group_topk_basis, topk.cu
+# gram_matmul_sharded): every Φ·V product is row-sharded — rank r forms rows
+# [r·M_b, (r+1)·M_b) — and all-gathered; the b×b / M×b algebra and the
+# adaptive stop (every top-K Ritz residual ≤ 1e-11·θ₁, max-reduced over the
+# ranks) are replicated.  kernel.hpp:49-72.
+
+def topk_adaptive(x, beta, rank, product, max_steps=4, tol=1e-11, seed=7, agree=None):
+    """The device's adaptive randomized subspace iteration in fp64 numpy;
+    `product(V)` returns Φ·V; `agree(worst)` makes the stop decision common."""
+    m = x.shape[0]
+    b = min(m, rank + max(16, rank // 5))
+    v, _ = np.linalg.qr(np.random.default_rng(seed).standard_normal((m, b)))
+    products = 0
+    for step in range(max_steps + 1):
+        w = product(v)
+        products += 1
+        if step < 1 and step < max_steps:
+            v, _ = np.linalg.qr(w)
+            continue
+        t = v.T @ w
+        theta, s = np.linalg.eigh(0.5 * (t + t.T))
+        s_top, th = s[:, -rank:], theta[-rank:]
+        u = v @ s_top
+        if step >= max_steps:
+            break
+        res = np.linalg.norm(w @ s_top - u * th, axis=0).max()
+        worst = agree(res) if agree else res
+        if worst <= tol * abs(theta[-1]):
+            break
+        v, _ = np.linalg.qr(w)
+    return u[:, ::-1], th[::-1], products
+
+
+def _topk_worker(rank, world, port, q, m, k):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as orc
+    x = orc.normalize_pair(orc.make_torus(m, 21), orc.make_torus(m, 22))[0]
+    rows = -(-m // world)  # block rows per rank
+
+    def product(v):
+        mine = np.arange(rank * rows, min((rank + 1) * rows, m))
+        blk = np.zeros((rows, v.shape[1]))
+        blk[:len(mine)] = orc.gram_apply(x, 2.0, v, rows=mine)
+        out = [torch.zeros(rows, v.shape[1], dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(out, torch.from_numpy(blk))
+        return torch.cat(out).numpy()[:m]
+
+    def agree(worst):
+        return float(_allreduce(np.array([worst]), op=dist.ReduceOp.MAX)[0])
+
+    u, lam, products = topk_adaptive(x, 2.0, k, product, agree=agree)
+    q.put((rank, u, lam, products))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_topk_setup_matches_unsharded(orc, world):
+    m, k = 900, 40
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_topk_worker, args=(r, world, port, q, m, k)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    x = orc.normalize_pair(orc.make_torus(m, 21), orc.make_torus(m, 22))[0]
+    u1, lam1, p1 = topk_adaptive(x, 2.0, k, lambda v: orc.gram_apply(x, 2.0, v))
+    for _, u, lam, products in res:
+        # row-sharded products are the unsharded rows: the same basis, bit for bit
+        assert products == p1
+        assert np.array_equal(lam, lam1) and np.array_equal(u, u1)
+    # and it is the top-K eigenbasis of Φ (LAPACK on the dense Gram matrix)
+    phi = orc.build_gram(x, 2.0)
+    _, _, raw = orc.eigendecompose(phi, k)
+    assert np.abs(lam1 - raw).max() <= 1e-10 * raw[0]
