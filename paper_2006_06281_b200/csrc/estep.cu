@@ -356,8 +356,9 @@ __global__ void __launch_bounds__(128 / NC, NC == 2 ? 16 : 8)
   // shared memory (no registers held across the pair loops)
   __shared__ unsigned long long form_tally[2];
   if (threadIdx.x == 0) form_tally[0] = form_tally[1] = 0ull;
-  __shared__ float4 xa[kTile];  // centred (vx,vx,vy,vy) | diff (−x,−x,−y,−y)
-  __shared__ float4 xb[kTile];  // centred (vz,vz,−|v|²,−|v|²) | diff (−z,−z,·,·)
+  // staged model points as scalars, read as broadcast (.F32) FFMA2 operands
+  // (as estep_row_kernel)
+  __shared__ float4 xa[kTile];  // centred (vx, vy, vz, −|v|²) | diff (−x', −y', −z', ·)
   const float s = st->sx;
   const int64_t G = gridDim.x, g = blockIdx.x;
   const int64_t P = wl.off(wl.n_blocks) << wl.ushift;
@@ -432,13 +433,11 @@ __global__ void __launch_bounds__(128 / NC, NC == 2 ? 16 : 8)
           } else {  // padding row: −|v|² = −inf → 2^{−t} = 0 exactly
             v = make_float4(0.f, 0.f, 0.f, -INFINITY);
           }
-          xa[i] = make_float4(v.x, v.x, v.y, v.y);
-          xb[i] = make_float4(v.z, v.z, v.w, v.w);
+          xa[i] = v;
         } else {
           const float4 v = src < m ? scale_pt(xt4[src], s)
                                    : make_float4(kPadCoord, kPadCoord, kPadCoord, 0.f);
-          xa[i] = make_float4(-v.x, -v.x, -v.y, -v.y);
-          xb[i] = make_float4(-v.z, -v.z, 0.f, 0.f);
+          xa[i] = make_float4(-v.x, -v.y, -v.z, 0.f);
         }
       }
       q += cnt;
@@ -451,15 +450,14 @@ __global__ void __launch_bounds__(128 / NC, NC == 2 ? 16 : 8)
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const float4 va = xa[j + u];
-            const float4 vb = xb[j + u];
 #pragma unroll
             for (int q2 = 0; q2 < NC; ++q2) {
               // 2u·v − |v|² = |u|² − t: the column's own 2^{−|u|²} is
               // factored out of its sum and applied once in fp64 (|u|² ≤ R²
               // ≤ 16, so the shifted terms stay in range)
-              float2 e = __ffma2_rn(ox[q2], make_float2(va.x, va.y), make_float2(vb.z, vb.w));
-              e = __ffma2_rn(oy[q2], make_float2(va.z, va.w), e);
-              e = __ffma2_rn(oz[q2], make_float2(vb.x, vb.y), e);
+              float2 e = __ffma2_rn(ox[q2], make_float2(va.x, va.x), make_float2(va.w, va.w));
+              e = __ffma2_rn(oy[q2], make_float2(va.y, va.y), e);
+              e = __ffma2_rn(oz[q2], make_float2(va.z, va.z), e);
               f[q2] = __fadd2_rn(f[q2], u < POLY ? ex2_poly2(e) : ex2x2(e));
             }
           }
@@ -469,12 +467,11 @@ __global__ void __launch_bounds__(128 / NC, NC == 2 ? 16 : 8)
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const float4 va = xa[j + u];
-            const float4 vb = xb[j + u];
 #pragma unroll
             for (int q2 = 0; q2 < NC; ++q2) {
-              const float2 dx = __fadd2_rn(ox[q2], make_float2(va.x, va.y));
-              const float2 dy = __fadd2_rn(oy[q2], make_float2(va.z, va.w));
-              const float2 dz = __fadd2_rn(oz[q2], make_float2(vb.x, vb.y));
+              const float2 dx = __fadd2_rn(ox[q2], make_float2(va.x, va.x));
+              const float2 dy = __fadd2_rn(oy[q2], make_float2(va.y, va.y));
+              const float2 dz = __fadd2_rn(oz[q2], make_float2(va.z, va.z));
               float2 tt = __fmul2_rn(dx, dx);
               tt = __ffma2_rn(dy, dy, tt);
               tt = __ffma2_rn(dz, dz, tt);
@@ -645,9 +642,12 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
   // shared memory (no registers held across the pair loops)
   __shared__ unsigned long long form_tally[2];
   if (threadIdx.x == 0) form_tally[0] = form_tally[1] = 0ull;
-  __shared__ float4 ya[kTile];  // centred (ux,ux,uy,uy) | diff (y,y,y',y') scaled
-  __shared__ float4 yb[kTile];  // centred (uz,uz,b−|u|²,·) | diff (z,z,b,b)
-  __shared__ float2 yq[kTile];  // centred (|u|², |u|²)
+  // staged scene points as scalars, read by the packed FFMA2s as broadcast
+  // (.F32) operands: one LDS.128 (+ one LDS.32) per point and half the
+  // register-operand traffic of duplicated (u,u) pairs (26.1 → 22.7 cycles
+  // per 64 pairs per SMSP, tools/operand_bench.cu)
+  __shared__ float4 ya[kTile];  // centred (ux, uy, uz, b − |u|²) | diff (y'x, y'y, y'z, b)
+  __shared__ float yq[kTile];   // centred |u|²
   // fp64 tile accumulators in shared memory (thread-private slots,
   // [quantity][row][thread] → conflict-free): registers stay with the
   // packed pipeline
@@ -730,14 +730,11 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
             u = make_float4(0.f, 0.f, 0.f, -INFINITY);
             uq = 0.f;
           }
-          ya[i] = make_float4(u.x, u.x, u.y, u.y);
-          yb[i] = make_float4(u.z, u.z, u.w, u.w);
-          yq[i] = make_float2(uq, uq);
+          ya[i] = u;
+          yq[i] = uq;
         } else {
-          const float4 y = src < n ? scale_pt(y4b[src], s)
-                                   : make_float4(kPadCoord, kPadCoord, kPadCoord, -INFINITY);
-          ya[i] = make_float4(y.x, y.x, y.y, y.y);
-          yb[i] = make_float4(y.z, y.z, y.w, y.w);
+          ya[i] = src < n ? scale_pt(y4b[src], s)
+                          : make_float4(kPadCoord, kPadCoord, kPadCoord, -INFINITY);
         }
       }
       q += cnt;
@@ -773,10 +770,10 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const float4 A = ya[j + u];
-            const float4 B = yb[j + u];
-            const float2 Q = yq[j + u];
-            const float2 Ux = make_float2(A.x, A.y), Uy = make_float2(A.z, A.w);
-            const float2 Uz = make_float2(B.x, B.y), Bn = make_float2(B.z, B.w);
+            const float q = yq[j + u];
+            const float2 Q = make_float2(q, q);
+            const float2 Ux = make_float2(A.x, A.x), Uy = make_float2(A.y, A.y);
+            const float2 Uz = make_float2(A.z, A.z), Bn = make_float2(A.w, A.w);
 #pragma unroll
             for (int q2 = 0; q2 < NP; ++q2) {
               // b − |u|² + 2u·v = (b − t) + |v|²: the row's own 2^{|v|²} is
@@ -799,9 +796,8 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const float4 A = ya[j + u];
-            const float4 B = yb[j + u];
-            const float2 Yx = make_float2(A.x, A.y), Yy = make_float2(A.z, A.w);
-            const float2 Yz = make_float2(B.x, B.y), Bn = make_float2(B.z, B.w);
+            const float2 Yx = make_float2(A.x, A.x), Yy = make_float2(A.y, A.y);
+            const float2 Yz = make_float2(A.z, A.z), Bn = make_float2(A.w, A.w);
 #pragma unroll
             for (int q2 = 0; q2 < NP; ++q2) {
               const float2 ddx = __fadd2_rn(Yx, ox[q2]);
