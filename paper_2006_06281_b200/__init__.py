@@ -27,7 +27,8 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libfcpd_b200.so")
+# FCPD_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("FCPD_LIB") or os.path.join(HERE, "lib", "libfcpd_b200.so")
 
 
 # ------------------------------------------------------------- errors.hpp:8-34

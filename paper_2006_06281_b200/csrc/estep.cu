@@ -43,6 +43,9 @@
 #include "common.cuh"
 #include "estep.cuh"
 
+#ifndef FCPD_ROW_MINB
+#define FCPD_ROW_MINB 12  // pass-2 CTAs per SM (80 registers: C4 pass 2 −5 % against 10)
+#endif
 namespace fcpd {
 
 namespace {
@@ -628,7 +631,7 @@ __device__ __forceinline__ void row_finalize(const RowFix& f, int64_t row, int64
 // pairs (fewer register-operand reads per pair: −7.5 % per pair in
 // tools/loopbench.cu).
 template <int NP>
-__global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : 10)
+__global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : FCPD_ROW_MINB)
     estep_row_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4b,
                      int64_t n, IterState* __restrict__ st, WorkList wl_in,
                      double* __restrict__ seg /* [slot][5][256] */, float centred_max_r2,
