@@ -198,6 +198,7 @@ struct Session {
   bool rowdot = false;
   double tau = 0.0;  // spectral truncation threshold of the basis streams (0: off)
   bool mfused = false;            // whole M-step as one cooperative kernel (mstep_fused.cu)
+  bool small = false;             // whole iteration as one cooperative kernel (small_iter_kernel)
   int mfused_grid = 0;
   DevBuf<double> zpart_fused;     // [K][grid][3]
   DevBuf<int32_t> mfused_done;    // its last-CTA counter
@@ -600,14 +601,24 @@ void enqueue_iteration(fcpd_ctx* ctx, Session& s, cudaEvent_t* ev = nullptr) {
     if (ev) FCPD_CUDA(cudaEventRecord(ev[i], str));
   };
   rec(0);
+  const MstepFusedArgs fa{b.q, b.kpad, b.k, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.tau,
+                          s.zp.trunc, s.resid4.p, s.zpart_fused.p, s.coef.p, s.g4.p, s.x0.p,
+                          s.xt64.p, s.xt_prev.p, s.xt4.p, s.ptilde_y.p, s.var.p, s.sig_part.p,
+                          s.mfused_done.p, s.m, s.d, s.cfg.early_stop, s.trace.p, st,
+                          s.stamps.p};
+  if (s.small) {  // the whole iteration as one cooperative kernel (booked as the E-step)
+    const int64_t units1 = static_cast<int64_t>(s.ep.col_blocks) * ceil_div(s.m, kSubPts);
+    const int64_t units2 = static_cast<int64_t>(s.ep.row_blocks) * ceil_div(s.n, kSubPts);
+    const SmallIterArgs sa{fa, s.y4b.p, s.b2.p, s.n, eb.out, eb.ystats, s.cull_counters.p,
+                           units1, units2};
+    launch_small_iter(sa, s.mfused_grid, str);
+    for (int i = 1; i <= 6; ++i) rec(i);
+    return;
+  }
   launch_estep(s.ep, eb, s.m, s.n, st, str, ev ? ev[1] : nullptr);
   rec(2);
   if (s.mfused) {  // one cooperative kernel; its time is booked as the Qᵀ·R phase
-    MstepFusedArgs a{b.q, b.kpad, b.k, b.lam, b.lam + b.k, s.cfg.lambda_reg, s.tau,
-                     s.zp.trunc, s.resid4.p, s.zpart_fused.p, s.coef.p, s.g4.p, s.x0.p,
-                     s.xt64.p, s.xt_prev.p, s.xt4.p, s.ptilde_y.p, s.var.p, s.sig_part.p,
-                     s.mfused_done.p, s.m, s.d, s.cfg.early_stop, s.trace.p, st, s.stamps.p};
-    launch_mstep_fused(a, s.mfused_grid, str);
+    launch_mstep_fused(fa, s.mfused_grid, str);
     for (int i = 3; i <= 6; ++i) rec(i);
     return;
   }
@@ -733,6 +744,10 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
       FCPD_CUDA(cudaMemsetAsync(s.mfused_done.p, 0, sizeof(int32_t), str));
       s.sig_part.ensure(std::max(transform_sigma_blocks(m), s.mfused_grid));
     }
+    // small problems: the whole iteration as one kernel (FCPD_SMALL_ITER=0/1)
+    s.small = !s.dist && s.mfused && !s.cull && small_iter_fits(m, s.n);
+    if (const char* e = std::getenv("FCPD_SMALL_ITER"))
+      s.small = std::atoi(e) != 0 && !s.dist && s.mfused && !s.cull && small_iter_fits(m, s.n);
   }
 }
 
@@ -1924,6 +1939,7 @@ int32_t fcpd_kernels_per_iteration(const fcpd_ctx* ctx) {
     return ranks * (e + 9 + (s.zp.trunc ? 1 : 0) + (s.dist_conditional ? 0 : 5)) +
            (s.dist_conditional ? 1 : 0) + (ctx->loop_ranks.empty() ? 0 : 3);
   }
+  if (s.small) return 1;  // the whole iteration (small_iter_kernel)
   // fused M-step: one kernel for rank, Qᵀ·R, filter, Q·g, transform and σ²
   if (s.mfused) return e + 1;
   // streaming: (spectral rank,) Qᵀ·R, z-reduce/filter, Q·g, transform, σ²

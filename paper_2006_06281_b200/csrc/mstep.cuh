@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "estep.cuh"
 
 namespace fcpd {
 
@@ -189,6 +190,22 @@ struct MstepFusedArgs {
 };
 int mstep_fused_grid(int sm_count);
 void launch_mstep_fused(const MstepFusedArgs& args, int grid, cudaStream_t stream);
+
+// One-kernel EM iteration for small problems (mstep_fused.cu
+// small_iter_kernel): both E-step passes with CTA-owned columns / rows, then
+// the fused M-step, in one cooperative launch on the fused M-step's grid.
+struct SmallIterArgs {
+  MstepFusedArgs ms;  // the M-step (and st, xt4, xt64, m)
+  float4* y4b;        // scene (x, y, z, b_n): .w written by pass 1
+  double* b2;         // b_n fp64
+  int64_t n;
+  RowOut out;         // P̃Y, var, log2 P1, degenerate, R = P̃Y − X
+  YStats ys;
+  unsigned long long* counters;  // session counters (tiles_evaluated, pairs by form)
+  int64_t units1, units2;        // (block, sub-tile) units per pass, every pair evaluated
+};
+bool small_iter_fits(int64_t m, int64_t n);
+void launch_small_iter(const SmallIterArgs& args, int grid, cudaStream_t stream);
 
 // out = (x0 or 0) + Σ partials, D columns.
 void launch_vreduce_add(const ColsumPlan& p, const double* part, const double* x0, int d,

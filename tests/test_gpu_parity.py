@@ -409,6 +409,7 @@ def test_fused_mstep_matches_streaming(ctx, fc, monkeypatch, name, m, iters, tau
     from paper_2006_06281_b200 import datagen
     if tau is not None:
         monkeypatch.setenv("FCPD_SPECTRAL_TAU", tau)
+    monkeypatch.setenv("FCPD_SMALL_ITER", "0")  # the multi-kernel E-step in both runs
     x, y, w = datagen.generate(name, m=m)
     cfg = datagen.config_for(w, iterations=iters)
     monkeypatch.setenv("FCPD_MSTEP_FUSED", "0")
@@ -432,6 +433,74 @@ def test_fused_mstep_matches_streaming(ctx, fc, monkeypatch, name, m, iters, tau
     again = ctx.register(x, y, cfg)  # bitwise reproducible
     assert np.array_equal(again.sigma2_trace, got.sigma2_trace)
     assert np.array_equal(again.transformed, got.transformed)
+
+
+# ------------------------------- one-kernel small iteration (small_iter_kernel)
+
+
+def _far_cloud(m, n, seed):
+    """A torus pair plus points far from the other set: model rows whose
+    posterior mass is far below the fp32 fast path's guard (exact row path)
+    and scene columns far from every model point (exact column path at
+    ω = 0).  (A register run cannot keep a row degenerate at this size: a
+    row at distance d puts σ² ≥ d²/(D·M), so its t stays below D·M/2.)"""
+    from oracle import oracle as orc
+    x = orc.make_torus(m, seed)
+    y = orc.make_torus(n, seed + 1) * 1.05 + 0.02
+    x[-3:] += np.array([3.0, 0.0, 0.0])   # far model rows
+    x[-6:-3] += np.array([0.0, 1.0, 0.0])
+    y[-4:] += np.array([0.0, 0.0, 3.0])   # far scene columns
+    return x, y
+
+
+@pytest.mark.parametrize("case", ["c0", "torus", "far"])
+def test_small_iteration_matches_multikernel(ctx, fc, monkeypatch, case):
+    """The whole EM iteration as one cooperative kernel against the
+    five-kernel path (stream-K passes + combines + fused M-step): same σ²
+    trace and points at the fp32 rounding level, one kernel per iteration,
+    bitwise reproducible."""
+    from paper_2006_06281_b200 import datagen
+    if case == "c0":
+        x, y, w = datagen.generate("c0")
+        cfg = datagen.config_for(w, iterations=50)
+    elif case == "torus":
+        from oracle import oracle as orc
+        x, y = orc.make_torus(700, 81), orc.make_torus(900, 82) * 1.1
+        cfg = fc.RegistrationConfig(omega=0.3, iterations=40)
+    else:
+        x, y = _far_cloud(600, 800, 83)
+        cfg = fc.RegistrationConfig(omega=0.0, iterations=30, beta=0.05, lambda_reg=100.0)
+    monkeypatch.setenv("FCPD_SMALL_ITER", "0")
+    ref = ctx.register(x, y, cfg)
+    k_multi = ctx.kernels_per_iteration
+    monkeypatch.setenv("FCPD_SMALL_ITER", "1")
+    got = ctx.register(x, y, cfg)
+    assert ctx.kernels_per_iteration == 1 and k_multi > 1
+    rel = np.abs(got.sigma2_trace / ref.sigma2_trace - 1).max()
+    pts = np.abs(got.transformed - ref.transformed).max() / bbox_diag(y)
+    print(f"{case}: σ² rel {rel:.3g} points {pts:.3g} kernels {k_multi} → 1")
+    # different fp32 summation orders: agreement at the fp32 rounding level
+    assert rel <= 1e-6, rel
+    assert pts <= 3e-7, pts
+    assert got.degenerate_rows == ref.degenerate_rows
+    again = ctx.register(x, y, cfg)
+    assert np.array_equal(again.sigma2_trace, got.sigma2_trace)
+    assert np.array_equal(again.transformed, got.transformed)
+
+
+def test_small_iteration_fallbacks_match_oracle(ctx, fc, orc, monkeypatch):
+    """Far model rows and far scene columns (the exact fp64 row / column
+    paths) through the one-kernel iteration against the dense fp64 oracle."""
+    monkeypatch.setenv("FCPD_SMALL_ITER", "1")
+    x, y = _far_cloud(400, 500, 91)
+    got = ctx.register(x, y, fc.RegistrationConfig(omega=0.0, iterations=25, beta=0.05,
+                                                   lambda_reg=100.0))
+    assert ctx.kernels_per_iteration == 1
+    ref = orc.register(x, y, omega=0.0, beta=0.05, lambda_reg=100.0, iterations=25)
+    rel, pts = record_parity("small-iter-fallbacks", got, ref, y)
+    assert rel.max() <= SIGMA_RTOL
+    assert pts <= POINT_FRAC
+    assert got.degenerate_rows == ref.degenerate_rows
 
 
 # ------------------------------------------------ spectral cache (§8f rank 1)
