@@ -339,8 +339,10 @@ class Context:
         self._check(lib().fcpd_register(self._h, _p(x), m, _p(y), n, d, C.byref(c),
                                         C.byref(res)))
         t = res.timing
+        # (M, D) results as filled by the C ABI (column-major, like the input
+        # it was given); a C-order copy would cost a transpose per call
         return RegistrationResult(
-            np.ascontiguousarray(out_x), np.ascontiguousarray(out_w),
+            out_x, out_w,
             trace[: res.iterations_run].copy(), res.sigma2_initial,
             TimingBreakdown(t.t_c, t.t_eig, t.t_iter, t.t_f, t.t_o, t.t_total, t.t_setup),
             int(res.degenerate_rows), int(res.sigma2_clamps), corr, mask.astype(bool),

@@ -63,6 +63,18 @@ struct DevBuf {
   }
 };
 
+// Run f(0..tasks-1) on `tasks` host threads (the caller's included).  Used
+// for the O(M+N) host passes of a register call, each task a fixed slice
+// (coordinate × point set), so every result is the same as the serial one.
+template <typename F>
+void parallel_for(int tasks, F f) {
+  std::vector<std::thread> th;
+  th.reserve(tasks > 1 ? tasks - 1 : 0);
+  for (int i = 1; i < tasks; ++i) th.emplace_back(f, i);
+  if (tasks > 0) f(0);
+  for (auto& t : th) t.join();
+}
+
 // Basis-cache key of the (normalised, sorted) model: four independent
 // 64-bit multiply-xor lanes over 8-byte words (≈ 8× the byte-wise rate),
 // byte-wise FNV-1a for the tail, lanes folded at the end.
@@ -265,7 +277,13 @@ struct fcpd_ctx {
     uint64_t hash = 0;
     int64_t count = -1;
     std::vector<int64_t> perm;
+    std::vector<double> scratch;  // the gather's target, reused (no page faults per call)
   } sort_x, sort_y;
+  // host staging of a register call, reused across calls: normalised points,
+  // their float4 packing, the read-back (a fresh 5 MB vector per call costs
+  // ~1 ms of page faults at C4)
+  std::vector<double> host_xs, host_ys, host_xt, host_w;
+  std::vector<float4> host_x4, host_y4;
   int device = 0;
   int sm_count = 148;
   cudaStream_t stream = nullptr;
@@ -653,7 +671,8 @@ namespace {
 // Upload points, plan kernels, allocate per-session device buffers.
 // x_soa/y_soa are fp64 SoA(3) host arrays already normalised.
 void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa,
-                     const std::vector<double>& y_soa, int capacity, bool need_mstep) {
+                     const std::vector<double>& y_soa, int capacity, bool need_mstep,
+                     bool x0_on_device = false) {
   const int64_t m = s.m, n = s.n;
   cudaStream_t str = ctx->stream;
   s.x0.ensure(3 * m);
@@ -678,14 +697,36 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
   s.ep = make_estep_plan(m, n, ctx->sm_count);
   s.sig_part.ensure(transform_sigma_blocks(m));  // one σ² partial per transform block
 
-  std::vector<float4> x4(m), y4(n);
-  for (int64_t i = 0; i < m; ++i)
-    x4[i] = make_float4(static_cast<float>(x_soa[i]), static_cast<float>(x_soa[m + i]),
-                        static_cast<float>(x_soa[2 * m + i]), 0.f);
-  for (int64_t i = 0; i < n; ++i)
-    y4[i] = make_float4(static_cast<float>(y_soa[i]), static_cast<float>(y_soa[n + i]),
-                        static_cast<float>(y_soa[2 * n + i]), 0.f);
-  FCPD_CUDA(cudaMemcpyAsync(s.x0.p, x_soa.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, str));
+  std::vector<float4>& x4 = ctx->host_x4;
+  std::vector<float4>& y4 = ctx->host_y4;
+  x4.resize(m);
+  y4.resize(n);
+  YStats ys{};
+  parallel_for(m + n >= 65536 ? 2 : 1, [&](int t) {
+    for (int k = t; k < 2; k += (m + n >= 65536 ? 2 : 1)) {
+      if (k == 0) {
+        for (int64_t i = 0; i < m; ++i)
+          x4[i] = make_float4(static_cast<float>(x_soa[i]), static_cast<float>(x_soa[m + i]),
+                              static_cast<float>(x_soa[2 * m + i]), 0.f);
+      } else {
+        for (int64_t i = 0; i < n; ++i)
+          y4[i] = make_float4(static_cast<float>(y_soa[i]), static_cast<float>(y_soa[n + i]),
+                              static_cast<float>(y_soa[2 * n + i]), 0.f);
+        // scene statistics for the uniform-row fallback (fp64, fixed order)
+        for (int c = 0; c < 3; ++c) {
+          double acc = 0.0;
+          for (int64_t i = 0; i < n; ++i) acc += y_soa[c * n + i];
+          ys.mean[c] = acc / static_cast<double>(n);
+        }
+        double sq = 0.0;
+        for (int64_t i = 0; i < n; ++i)
+          sq += y_soa[i] * y_soa[i] + y_soa[n + i] * y_soa[n + i] + y_soa[2 * n + i] * y_soa[2 * n + i];
+        ys.sq_mean = sq / static_cast<double>(n);
+      }
+    }
+  });
+  if (!x0_on_device)  // (session_begin uploads X before the basis build)
+    FCPD_CUDA(cudaMemcpyAsync(s.x0.p, x_soa.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, str));
   FCPD_CUDA(cudaMemcpyAsync(s.xt64.p, s.x0.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, str));
   FCPD_CUDA(cudaMemcpyAsync(s.xt_prev.p, s.x0.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, str));
   FCPD_CUDA(cudaMemcpyAsync(s.y64.p, y_soa.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice, str));
@@ -693,17 +734,6 @@ void prepare_buffers(fcpd_ctx* ctx, Session& s, const std::vector<double>& x_soa
   FCPD_CUDA(cudaMemcpyAsync(s.y4b.p, y4.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, str));
   s.h2d += (sizeof(double) * 3 + sizeof(float4)) * (m + n);
 
-  // scene statistics for the uniform-row fallback (fp64, fixed order)
-  YStats ys{};
-  for (int c = 0; c < 3; ++c) {
-    double acc = 0.0;
-    for (int64_t i = 0; i < n; ++i) acc += y_soa[c * n + i];
-    ys.mean[c] = acc / static_cast<double>(n);
-  }
-  double sq = 0.0;
-  for (int64_t i = 0; i < n; ++i)
-    sq += y_soa[i] * y_soa[i] + y_soa[n + i] * y_soa[n + i] + y_soa[2 * n + i] * y_soa[2 * n + i];
-  ys.sq_mean = sq / static_cast<double>(n);
   s.ystats = ys;
 
   alloc_estep(s, m, n, str);  // scene tiles are fixed for the session
@@ -856,9 +886,12 @@ template <typename Cache>
 std::vector<int64_t> spatial_sort_cached(std::vector<double>& soa, int64_t cnt, Cache& c) {
   const uint64_t h = fnv1a(soa.data(), sizeof(double) * soa.size());
   if (c.count == cnt && c.hash == h && static_cast<int64_t>(c.perm.size()) == cnt) {
-    std::vector<double> out(soa.size());
-    for (int d = 0; d < 3; ++d)
-      for (int64_t k = 0; k < cnt; ++k) out[d * cnt + k] = soa[d * cnt + c.perm[k]];
+    std::vector<double>& out = c.scratch;
+    out.resize(soa.size());
+    parallel_for(cnt >= 65536 ? 3 : 1, [&](int t) {
+      for (int d = t; d < 3; d += (cnt >= 65536 ? 3 : 1))
+        for (int64_t k = 0; k < cnt; ++k) out[d * cnt + k] = soa[d * cnt + c.perm[k]];
+    });
     soa.swap(out);
     return c.perm;
   }
@@ -879,24 +912,42 @@ void normalize_pair_host(const double* x, int64_t m, const double* y, int64_t n,
   center[0] = center[1] = center[2] = 0.0;
   *scale = 1.0;
   if (normalize) {
+    // one task per (coordinate, point set); each sum / max / write runs in
+    // the serial order, so the result does not depend on the threading
+    const int tasks = (m + n) >= 65536 ? 2 * d : 1;
     const double total = static_cast<double>(m + n);
-    for (int c = 0; c < d; ++c) {
-      double sx = 0.0, sy = 0.0;
-      for (int64_t i = 0; i < m; ++i) sx += x[c * m + i];
-      for (int64_t i = 0; i < n; ++i) sy += y[c * n + i];
-      center[c] = (sx + sy) / total;
-    }
+    double part[6] = {0, 0, 0, 0, 0, 0};
+    auto slice = [&](int t, auto&& body) {
+      for (int k = t; k < 2 * d; k += tasks) {
+        const int c = k >> 1;
+        const bool is_y = k & 1;
+        body(k, c, is_y ? y + c * n : x + c * m, is_y ? n : m, is_y ? &ys[c * n] : &xs[c * m]);
+      }
+    };
+    parallel_for(tasks, [&](int t) {
+      slice(t, [&](int k, int, const double* src, int64_t cnt, double*) {
+        double acc = 0.0;
+        for (int64_t i = 0; i < cnt; ++i) acc += src[i];
+        part[k] = acc;
+      });
+    });
+    for (int c = 0; c < d; ++c) center[c] = (part[2 * c] + part[2 * c + 1]) / total;
+    parallel_for(tasks, [&](int t) {
+      slice(t, [&](int k, int c, const double* src, int64_t cnt, double*) {
+        double mx = 0.0;
+        for (int64_t i = 0; i < cnt; ++i) mx = std::max(mx, std::fabs(src[i] - center[c]));
+        part[k] = mx;
+      });
+    });
     double sc = 0.0;
-    for (int c = 0; c < d; ++c) {
-      for (int64_t i = 0; i < m; ++i) sc = std::max(sc, std::fabs(x[c * m + i] - center[c]));
-      for (int64_t i = 0; i < n; ++i) sc = std::max(sc, std::fabs(y[c * n + i] - center[c]));
-    }
+    for (int k = 0; k < 2 * d; ++k) sc = std::max(sc, part[k]);
     if (sc <= 0.0) sc = 1.0;
     *scale = sc;
-    for (int c = 0; c < d; ++c) {
-      for (int64_t i = 0; i < m; ++i) xs[c * m + i] = (x[c * m + i] - center[c]) / sc;
-      for (int64_t i = 0; i < n; ++i) ys[c * n + i] = (y[c * n + i] - center[c]) / sc;
-    }
+    parallel_for(tasks, [&](int t) {
+      slice(t, [&](int, int c, const double* src, int64_t cnt, double* dst) {
+        for (int64_t i = 0; i < cnt; ++i) dst[i] = (src[i] - center[c]) / sc;
+      });
+    });
   } else {
     for (int c = 0; c < d; ++c) {
       std::memcpy(&xs[c * m], x + c * m, sizeof(double) * m);
@@ -925,7 +976,8 @@ void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, i
   auto stamp = [&](const char* what) {
     if (host_timing) std::fprintf(stderr, "[fcpd] begin %-12s %8.3f ms\n", what, 1e3 * since(t0));
   };
-  std::vector<double> xs, ys;
+  std::vector<double>& xs = ctx->host_xs;
+  std::vector<double>& ys = ctx->host_ys;
   normalize_pair_host(x, m, y, n, d, cfg.normalize != 0, xs, ys, s.center, &s.scale);
   stamp("normalize");
   // internal order: spatially sorted model and scene (undone on output); the
@@ -943,7 +995,7 @@ void session_begin(fcpd_ctx* ctx, const double* x, int64_t m, const double* y, i
   ensure_basis(ctx, s, xs);
   stamp("basis");
   ctx->basis.perm = s.perm_x;  // basis rows are in the session's sorted order
-  prepare_buffers(ctx, s, xs, ys, cfg.iterations, true);
+  prepare_buffers(ctx, s, xs, ys, cfg.iterations, true, /*x0_on_device=*/true);
   stamp("buffers");
   s.sigma2_initial = init_sigma2_host(xs, m, ys, n, d);
   if (cfg.iterations > 0 && !(cfg.omega >= 0.0 && cfg.omega < 1.0))
@@ -1034,7 +1086,8 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
     FCPD_CUDA(cudaMemcpyAsync(out->sigma2_trace, s.trace.p, sizeof(double) * run,
                               cudaMemcpyDeviceToHost, str));
   s.d2h += sizeof(double) * (run + 3 * m);
-  std::vector<double> xt(3 * m);
+  std::vector<double>& xt = ctx->host_xt;
+  xt.resize(3 * m);
   FCPD_CUDA(cudaMemcpyAsync(xt.data(), s.xt64.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, str));
   // internal rows are spatially sorted: sorted row k is original row perm_x[k]
   const std::vector<int64_t>& px = s.perm_x;
@@ -1051,12 +1104,15 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
     FCPD_LAUNCH_CHECK();
     launch_colsum(s.vp, b.qt, b.mpad, s.g4.p, s.vpart.p, nullptr, nullptr, 0, str);
     launch_vreduce_add(s.vp, s.vpart.p, nullptr, d, s.ptilde_y.p, str);
-    std::vector<double> w(static_cast<size_t>(d) * m);
+    std::vector<double>& w = ctx->host_w;
+    w.resize(static_cast<size_t>(d) * m);
     FCPD_CUDA(cudaMemcpyAsync(w.data(), s.ptilde_y.p, sizeof(double) * d * m,
                               cudaMemcpyDeviceToHost, str));
     FCPD_CUDA(cudaStreamSynchronize(str));
-    for (int c = 0; c < d; ++c)
-      for (int64_t k = 0; k < m; ++k) out->coefficients[c * m + px[k]] = w[c * m + k];
+    parallel_for(m >= 65536 ? d : 1, [&](int t) {
+      for (int c = t; c < d; c += (m >= 65536 ? d : 1))
+        for (int64_t k = 0; k < m; ++k) out->coefficients[c * m + px[k]] = w[c * m + k];
+    });
     s.d2h += sizeof(double) * d * m;
   }
   if (out->correspondence && run > 0) {
@@ -1100,10 +1156,12 @@ void session_read(fcpd_ctx* ctx, fcpd_result* out, double wall) {
   if (out->degenerate_mask)
     for (int64_t k = 0; k < m; ++k) out->degenerate_mask[px[k]] = degm[k];
   if (out->transformed) {
-    for (int c = 0; c < d; ++c)
-      for (int64_t k = 0; k < m; ++k)
-        out->transformed[c * m + px[k]] =
-            s.cfg.normalize ? xt[c * m + k] * s.scale + s.center[c] : xt[c * m + k];
+    parallel_for(m >= 65536 ? d : 1, [&](int t) {
+      for (int c = t; c < d; c += (m >= 65536 ? d : 1))
+        for (int64_t k = 0; k < m; ++k)
+          out->transformed[c * m + px[k]] =
+              s.cfg.normalize ? xt[c * m + k] * s.scale + s.center[c] : xt[c * m + k];
+    });
   }
   // phases (registration.hpp:120-147): t_c = E-step; t_iter = residual +
   // solve (Qᵀ R, filter, Q g); t_o = transform epilogue + σ² + everything else
