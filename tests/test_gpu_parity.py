@@ -453,7 +453,7 @@ def _far_cloud(m, n, seed):
     return x, y
 
 
-@pytest.mark.parametrize("case", ["c0", "torus", "far"])
+@pytest.mark.parametrize("case", ["c0", "torus", "far", "edge_m", "edge_n"])
 def test_small_iteration_matches_multikernel(ctx, fc, monkeypatch, case):
     """The whole EM iteration as one cooperative kernel against the
     five-kernel path (stream-K passes + combines + fused M-step): same σ²
@@ -467,9 +467,14 @@ def test_small_iteration_matches_multikernel(ctx, fc, monkeypatch, case):
         from oracle import oracle as orc
         x, y = orc.make_torus(700, 81), orc.make_torus(900, 82) * 1.1
         cfg = fc.RegistrationConfig(omega=0.3, iterations=40)
-    else:
+    elif case == "far":
         x, y = _far_cloud(600, 800, 83)
         cfg = fc.RegistrationConfig(omega=0.0, iterations=30, beta=0.05, lambda_reg=100.0)
+    else:  # the size limits of the one-kernel path: 8192 staged points, M·N = 2^24
+        from oracle import oracle as orc
+        big, small = orc.make_torus(8192, 84), orc.make_torus(2047, 85) * 1.05
+        x, y = (big, small) if case == "edge_m" else (small, big)
+        cfg = fc.RegistrationConfig(omega=0.1, iterations=15)
     monkeypatch.setenv("FCPD_SMALL_ITER", "0")
     ref = ctx.register(x, y, cfg)
     k_multi = ctx.kernels_per_iteration
