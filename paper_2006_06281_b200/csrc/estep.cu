@@ -66,7 +66,6 @@ constexpr float kProbeMinShare = 2.f;
 constexpr float kProbePayShare = 4.f;
 constexpr int kProbeRetry = 3;
 
-
 // smallest squared distance between two boxes (0 if they overlap)
 __device__ __forceinline__ float box_mindist2(float4 alo, float4 ahi, float4 blo, float4 bhi) {
   const float dx = fmaxf(0.f, fmaxf(alo.x - bhi.x, blo.x - ahi.x));
@@ -568,11 +567,11 @@ __device__ __forceinline__ void row_finalize(const RowFix& f, int64_t row, int64
 //  * centred: L = (b − |u|²) − |v|² + 2u·v with u = y' − c, v = x' − c, and
 //    the sums kept as Σw, Σw·u, Σw·|u|²; converted per segment in fp64:
 //      Σw·y' = Σw·u + c·Σw,  Σw·t = Σw·|u|² + |v|²·Σw − 2v·Σw·u.
-//    Per packed pair of pairs: FADD2 + 3 FFMA2 (L) + FADD2 + 4 FFMA2 (sums).
+//    Per packed pair of pairs: 3 FFMA2 (L) + FADD2 + 4 FFMA2 (sums).
 //  * difference: t = ‖y' − x'‖², L = b − t; sums Σw, Σw·y', Σw·t directly.
-// The pass is bound by FP32 operand traffic (≈ one 64-bit register operand
-// per cycle per SMSP, measured: tools/loopbench.cu); the centred form needs
-// 25 operands per 2 pairs against 31.
+// MUFU and FP32 are co-bound (8 lane-ops per ex2); the staged scene values
+// are broadcast (.F32) FFMA2 operands, which took the inner loop from 26.1
+// to 22.7 cycles per 64 pairs per SMSP (tools/operand_bench.cu).
 // NP row pairs per thread; the CTA (128/NP threads) owns the 256-row block.
 // NP = 2 shares every staged scene point's operands between two packed row
 // pairs (fewer register-operand reads per pair: −7.5 % per pair in
