@@ -329,7 +329,10 @@ __device__ __forceinline__ void col_b_ranges(const ColFix& f, int rb, int64_t n,
 // POLY of every 8 staged points take their ex2 on the FMA pipe (ex2_poly2)
 // in the centred form: MUFU and FP32 balance at 2 (1/16·¾ = (4 + 8·¼)/128).
 template <int NC, int POLY>
-__global__ void __launch_bounds__(128 / NC, NC == 2 ? 16 : 8)
+#ifndef FCPD_COL_MINB
+#define FCPD_COL_MINB 24  // pass-1 CTAs per SM (40 registers: C4 pass 1 −2.7 % against 16)
+#endif
+__global__ void __launch_bounds__(128 / NC, NC == 2 ? FCPD_COL_MINB : 8)
     estep_col_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4,
                      int64_t n, IterState* __restrict__ st, WorkList wl_in,
                      double* __restrict__ seg, float centred_max_r2,
