@@ -443,6 +443,16 @@ def rooflines(r, peaks, peak_kind):
                         "basis_bytes_per_iteration": q_bytes / 2 if fused else q_bytes,
                         "ms": q_ms, "share_of_iteration": q_ms / it_ms,
                         "achieved_gbs": (q_bytes / 2 if fused else q_bytes) / (q_ms / 1e3) / 1e9}}
+    t_iter = r["state"].get("t_iter") or 0.0
+    if not fused and t_iter > 0:
+        g_ms = 1e3 * t_iter / steps
+        hbm["this_run"]["in_graph"] = {
+            "ms": g_ms, "achieved_gbs": q_bytes / (g_ms / 1e3) / 1e9,
+            "frac": q_bytes / (g_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+            "source": "device globaltimer stamps at the z-pass and transform kernel starts in "
+                      "the timed graph replays: z pass + z reduce/filter + V pass with PDL-"
+                      "overlapped launches (the per-phase CUDA events of `ms` bracket each "
+                      "kernel's launch latency too)"}
     fp = r.get("full_phases")
     if fp:
         fk = (k + 3) // 4 * 4

@@ -386,7 +386,10 @@ class Context:
                     tiles_evaluated=(int(res.tiles_evaluated[0]), int(res.tiles_evaluated[1])),
                     pairs_by_form=tuple(int(v) for v in res.pairs_by_form),
                     spectral_rank=int(res.spectral_rank),
-                    mstep_fused=bool(res.mstep_fused))
+                    mstep_fused=bool(res.mstep_fused),
+                    # device-stamped phase sums over the run (s): E-step, and
+                    # the M-step from the z pass to the transform
+                    t_c=float(res.timing.t_c), t_iter=float(res.timing.t_iter))
 
     @property
     def stream_ptr(self) -> int:
