@@ -432,6 +432,11 @@ __global__ void __launch_bounds__(kBulkThreads, kBulkCtasPerSm)
 namespace {
 constexpr int kRdRows = 8;                        // eigenvector rows per unit
 constexpr int kRdCols = 4 * kColsumThreads;       // 1024 columns per unit
+// columns per consumer thread (2, with 16 consumer warps: 46 µs against 44
+// at C4 — register-capped with spills)
+constexpr int kRdCpt = 4;
+constexpr int kRdConsumers = kRdCols / kRdCpt;    // consumer threads
+constexpr int kRdThreads = kRdConsumers + 32;     // + producer warp
 constexpr int kRdSlot = kRdRows * 3;              // doubles per partial slot
 // one CTA per SM with a 4-stage ring of (32 KB of Qᵀ + the unit's 16 KB of
 // R): the 8×3 fp64 sums per thread need the registers of a single resident
@@ -454,7 +459,7 @@ __device__ __forceinline__ int64_t rd_owner(const RdGeom& g, int64_t u) {
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kBulkThreads, 1)
+__global__ void __launch_bounds__(kRdThreads, 1)
     rowdot_bulk_kernel(const float* __restrict__ A, const float4* __restrict__ v, RdGeom g,
                        double* __restrict__ part, const IterState* __restrict__ st,
                        uint64_t* stamps, int stamp_slot) {
@@ -472,7 +477,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < kRdStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kBulkConsumers / 32);
+      mbar_init(&empty[s], kRdConsumers / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -480,8 +485,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   const int64_t u0 = rd_begin(g, blockIdx.x), u1 = rd_begin(g, blockIdx.x + 1);
   static_assert(kRdRows * kRdCols * 4 == kStageBytes, "one unit per stage");
 
-  if (tid >= kBulkConsumers) {  // ---------------- producer warp
-    if (tid != kBulkConsumers) return;
+  if (tid >= kRdConsumers) {  // ---------------- producer warp
+    if (tid != kRdConsumers) return;
     uint64_t policy, policy_r;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy_r));
@@ -506,32 +511,16 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   }
 
   // ------------------------------------------------ consumer warps
-  __shared__ double red[kBulkConsumers / 32][kRdSlot];
-  // fp32 sums over kRdBatch units (4 products per column thread each), then
-  // fp64 (4 units: 1e-6 worse σ² agreement with the fused path at C0, no speed-up)
-  constexpr int kRdBatch = 1;
+  __shared__ double red[kRdConsumers / 32][kRdSlot];
+  // per row and unit: an fp32 dot product over the thread's kRdCpt columns,
+  // then fp64 (fp32 over several units: 1e-6 worse σ² agreement with the
+  // fused path at C0, no speed-up)
   double acc[kRdRows][3];
-  float accf[kRdRows][3];
 #pragma unroll
-  for (int r = 0; r < kRdRows; ++r) {
-    acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
-    accf[r][0] = accf[r][1] = accf[r][2] = 0.f;
-  }
-  int in_batch = 0;
-  auto drain = [&]() {
-#pragma unroll
-    for (int r = 0; r < kRdRows; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        acc[r][c] += static_cast<double>(accf[r][c]);
-        accf[r][c] = 0.f;
-      }
-    in_batch = 0;
-  };
+  for (int r = 0; r < kRdRows; ++r) acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
   int slot = 0;
   // the fixed-order CTA reduction of the current row group into slot `slot`
   auto flush_group = [&]() {
-    drain();
     const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int r = 0; r < kRdRows; ++r)
@@ -541,13 +530,13 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
         if (lane == 0) red[warp][r * 3 + c] = w;
         acc[r][c] = 0.0;
       }
-    asm volatile("bar.sync 1, %0;" ::"r"(kBulkConsumers));  // consumers only
+    asm volatile("bar.sync 1, %0;" ::"r"(kRdConsumers));  // consumers only
     if (tid < kRdSlot) {
       double s = 0.0;
-      for (int w = 0; w < kBulkConsumers / 32; ++w) s += red[w][tid];
+      for (int w = 0; w < kRdConsumers / 32; ++w) s += red[w][tid];
       part[(static_cast<int64_t>(blockIdx.x) * g.kmax + slot) * kRdSlot + tid] = s;
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(kBulkConsumers));  // red is reused
+    asm volatile("bar.sync 1, %0;" ::"r"(kRdConsumers));  // red is reused
     ++slot;
   };
   int64_t cur_rg = u0 < u1 ? u0 / g.col_blocks : 0;
@@ -560,33 +549,38 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
       flush_group();
       cur_rg = rg;
     }
-    const int64_t c0 = cb * kRdCols + 4 * tid;
+    const int64_t c0 = cb * kRdCols + kRdCpt * tid;
     const int nrows = static_cast<int>(min(static_cast<int64_t>(kRdRows), g.rows - rg * kRdRows));
     mbar_wait(&full[s], ph);
-    // R of the thread's 4 columns, staged with the unit (a per-unit L2
+    // R of the thread's kRdCpt columns, staged with the unit (a per-unit L2
     // round trip otherwise serialises the consumers)
-    float4 rv[4];
-    const float4* rs = rring + s * kRdCols + 4 * tid;
+    float4 rv[kRdCpt];
+    const float4* rs = rring + s * kRdCols + kRdCpt * tid;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < kRdCpt; ++j)
       rv[j] = c0 + j < g.cols ? rs[j] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4* st4 = reinterpret_cast<const float4*>(ring + static_cast<int64_t>(s) * (kStageBytes / 4));
+    const float* stf = ring + static_cast<int64_t>(s) * (kStageBytes / 4);
 #pragma unroll
     for (int r = 0; r < kRdRows; ++r) {
       if (r < nrows && c0 < g.cols) {
-        const float4 q = st4[r * (kRdCols / 4) + tid];
-        // fp32 over the thread's 4 columns, then fp64
-        const float fx = __fmaf_rn(q.w, rv[3].x, __fmaf_rn(q.z, rv[2].x, __fmaf_rn(q.y, rv[1].x, q.x * rv[0].x)));
-        const float fy = __fmaf_rn(q.w, rv[3].y, __fmaf_rn(q.z, rv[2].y, __fmaf_rn(q.y, rv[1].y, q.x * rv[0].y)));
-        const float fz = __fmaf_rn(q.w, rv[3].z, __fmaf_rn(q.z, rv[2].z, __fmaf_rn(q.y, rv[1].z, q.x * rv[0].z)));
-        accf[r][0] += fx;
-        accf[r][1] += fy;
-        accf[r][2] += fz;
+        // fp32 over the thread's kRdCpt columns, then fp64
+        static_assert(kRdCpt == 4, "one float4 of the basis row per thread");
+        const float4 q4 = reinterpret_cast<const float4*>(stf)[r * (kRdCols / 4) + tid];
+        const float q[kRdCpt] = {q4.x, q4.y, q4.z, q4.w};
+        float fx = q[0] * rv[0].x, fy = q[0] * rv[0].y, fz = q[0] * rv[0].z;
+#pragma unroll
+        for (int j = 1; j < kRdCpt; ++j) {
+          fx = __fmaf_rn(q[j], rv[j].x, fx);
+          fy = __fmaf_rn(q[j], rv[j].y, fy);
+          fz = __fmaf_rn(q[j], rv[j].z, fz);
+        }
+        acc[r][0] += static_cast<double>(fx);
+        acc[r][1] += static_cast<double>(fy);
+        acc[r][2] += static_cast<double>(fz);
       }
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[s]);
-    if (++in_batch == kRdBatch) drain();
   }
   if (u0 < u1) flush_group();
 }
@@ -675,7 +669,7 @@ size_t RowdotPlan::part_doubles() const {
 
 void launch_rowdot(const RowdotPlan& p, const float* qt, const float4* v, double* part,
                    const IterState* st, uint64_t* stamps, int stamp_slot, cudaStream_t stream) {
-  launch_pdl(rowdot_bulk_kernel, dim3(p.g.grid), dim3(kBulkThreads), kRdSmem, stream, qt, v,
+  launch_pdl(rowdot_bulk_kernel, dim3(p.g.grid), dim3(kRdThreads), kRdSmem, stream, qt, v,
              p.g, part, st, stamps, stamp_slot);
   FCPD_LAUNCH_CHECK();
 }
