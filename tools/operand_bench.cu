@@ -122,6 +122,9 @@ __global__ void __launch_bounds__(128) loop_kernel(float* out, int occ_pad) {
     f0[p] = fx[p] = fy[p] = fz[p] = fq[p] = make_float2(0.f, 0.f);
   }
   const int steps = (V == 2) ? kPts / 2 : kPts;  // col: two columns per step
+  float2 Lp[NP];  // V == 3: the next point's logits
+#pragma unroll
+  for (int p = 0; p < NP; ++p) Lp[p] = make_float2(-1.f, -2.f);
   for (int r = 0; r < kReps; ++r) {
     for (int j = 0; j < steps; j += 8) {
 #pragma unroll
@@ -161,6 +164,29 @@ __global__ void __launch_bounds__(128) loop_kernel(float* out, int occ_pad) {
             fz[p] = __ffma2_rn(w, Uz, fz[p]);
             fq[p] = __ffma2_rn(w, Q, fq[p]);
           }
+        } else if (V == 3) {
+          // bc with the logits of the next staged point computed before this
+          // point's ex2/sums (software-pipelined by one point)
+          const int jn = (j + u + 1) & (kPts - 1);
+          const float4 An = sa[jn];
+          const float4 A = sa[j + u];
+          const float q = sq[j + u].x;
+          const float2 Q = make_float2(q, q);
+          const float2 Ux = make_float2(A.x, A.x), Uy = make_float2(A.y, A.y);
+          const float2 Uz = make_float2(A.z, A.z);
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            const float2 w = ex2v<MUFU>(Lp[p]);
+            float2 Ln = __ffma2_rn(make_float2(An.x, An.x), ox[p], make_float2(An.w, An.w));
+            Ln = __ffma2_rn(make_float2(An.y, An.y), oy[p], Ln);
+            Ln = __ffma2_rn(make_float2(An.z, An.z), oz[p], Ln);
+            Lp[p] = Ln;
+            f0[p] = __fadd2_rn(f0[p], w);
+            fx[p] = __ffma2_rn(w, Ux, fx[p]);
+            fy[p] = __ffma2_rn(w, Uy, fy[p]);
+            fz[p] = __ffma2_rn(w, Uz, fz[p]);
+            fq[p] = __ffma2_rn(w, Q, fq[p]);
+          }
         } else {
           const float4 A = sa[j + u], B = sb[j + u];
           const float2 Q = sq[j + u];
@@ -186,7 +212,7 @@ __global__ void __launch_bounds__(128) loop_kernel(float* out, int occ_pad) {
   float s = 0.f;
 #pragma unroll
   for (int p = 0; p < NP; ++p)
-    s += f0[p].x + f0[p].y + fx[p].x + fx[p].y + fy[p].x + fy[p].y + fz[p].x + fz[p].y + fq[p].x +
+    s += Lp[p].x + f0[p].x + f0[p].y + fx[p].x + fx[p].y + fy[p].x + fy[p].y + fz[p].x + fz[p].y + fq[p].x +
          fq[p].y;
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
@@ -243,6 +269,8 @@ int main() {
     run_loop<1, 1, true>("bc np1", sms, occ, out);
     run_loop<1, 2, true>("bc np2", sms, occ, out);
     run_loop<1, 3, true>("bc np3", sms, occ, out);
+    run_loop<3, 2, true>("bc np2 pipelined", sms, occ, out);
+    run_loop<3, 2, false>("bc np2 pipe nomufu", sms, occ, out);
     run_loop<2, 2, true>("col np2", sms, occ, out);
     run_loop<2, 4, true>("col np4", sms, occ, out);
     run_loop<0, 2, false>("dup np2 nomufu", sms, occ, out);
