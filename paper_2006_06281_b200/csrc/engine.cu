@@ -625,10 +625,7 @@ void enqueue_iteration(fcpd_ctx* ctx, Session& s, cudaEvent_t* ev = nullptr) {
                           s.mfused_done.p, s.m, s.d, s.cfg.early_stop, s.trace.p, st,
                           s.stamps.p};
   if (s.small) {  // the whole iteration as one cooperative kernel (booked as the E-step)
-    const int64_t units1 = static_cast<int64_t>(s.ep.col_blocks) * ceil_div(s.m, kSubPts);
-    const int64_t units2 = static_cast<int64_t>(s.ep.row_blocks) * ceil_div(s.n, kSubPts);
-    const SmallIterArgs sa{fa, s.y4b.p, s.b2.p, s.n, eb.out, eb.ystats, s.cull_counters.p,
-                           units1, units2};
+    const SmallIterArgs sa{fa, s.y4b.p, s.b2.p, s.n, eb.out, eb.ystats, s.cull_counters.p};
     launch_small_iter(sa, s.mfused_grid, str);
     for (int i = 1; i <= 6; ++i) rec(i);
     return;

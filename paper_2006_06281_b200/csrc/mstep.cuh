@@ -201,8 +201,7 @@ struct SmallIterArgs {
   int64_t n;
   RowOut out;         // P̃Y, var, log2 P1, degenerate, R = P̃Y − X
   YStats ys;
-  unsigned long long* counters;  // session counters (tiles_evaluated, pairs by form)
-  int64_t units1, units2;        // (block, sub-tile) units per pass, every pair evaluated
+  unsigned long long* counters;  // session counters (pairs by form)
 };
 bool small_iter_fits(int64_t m, int64_t n);
 void launch_small_iter(const SmallIterArgs& args, int grid, cudaStream_t stream);

@@ -572,8 +572,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) small_iter_kernel(SmallIterA
     }
   }
   if (c == 0 && tid == 0 && a.counters) {  // every pair evaluated, difference form
-    atomicAdd(a.counters, static_cast<unsigned long long>(a.units1));
-    atomicAdd(a.counters + 1, static_cast<unsigned long long>(a.units2));
+    // (tile pairs are counted by culling sessions only, as on the pass kernels)
     const unsigned long long pairs = static_cast<unsigned long long>(m) * n;
     atomicAdd(a.counters + 3, pairs);
     atomicAdd(a.counters + 5, pairs);

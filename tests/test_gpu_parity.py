@@ -603,6 +603,37 @@ def test_culling_matches_unculled(ctx, fc, monkeypatch, name, m, iters, late_fra
     assert 0.0 < max(frac) <= late_frac, frac
 
 
+@pytest.mark.parametrize("small", ["0", "1"])
+def test_roofline_pair_counters(ctx, fc, monkeypatch, small):
+    """The per-(pass, form) pair counters bench.py computes the E-step
+    roofline from: with every pair evaluated (no culling) they add up to the
+    pairs each pass evaluates — M × (N rounded up to 32-point units) for
+    pass 2 and N × (M rounded up) for pass 1 on the stream-K pass kernels
+    (centred + difference), M × N per pass in the difference form on the
+    one-kernel small iteration.  Tile pairs are counted by culling sessions
+    only (bench.py reads no count as "every unit")."""
+    from oracle import oracle as orc
+    monkeypatch.setenv("FCPD_SMALL_ITER", small)
+    monkeypatch.setenv("FCPD_CULL", "0")
+    x, y = orc.make_torus(1500, 71), orc.make_torus(1700, 72) * 1.05
+    cfg = fc.RegistrationConfig(omega=0.1, iterations=7)
+    ctx.session_begin(x, y, cfg)
+    s0 = ctx.session_read(with_points=False)
+    ctx.session_run(7)
+    s1 = ctx.session_read(with_points=False)
+    pairs = [b - a for a, b in zip(s0["pairs_by_form"], s1["pairs_by_form"])]
+    tiles = [b - a for a, b in zip(s0["tiles_evaluated"], s1["tiles_evaluated"])]
+    m, n, it = x.shape[0], y.shape[0], 7
+    assert (ctx.kernels_per_iteration == 1) == (small == "1")
+    if small == "1":
+        assert pairs == [0, m * n * it, 0, m * n * it], pairs
+    else:
+        up = lambda v: -(-v // 32) * 32
+        assert pairs[0] + pairs[1] == n * up(m) * it, pairs
+        assert pairs[2] + pairs[3] == m * up(n) * it, pairs
+    assert tiles == [0, 0], tiles
+
+
 # ------------------------------------------ spectral truncation of the streams
 
 
