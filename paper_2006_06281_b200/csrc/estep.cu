@@ -328,11 +328,12 @@ __device__ __forceinline__ void col_b_ranges(const ColFix& f, int rb, int64_t n,
 // between two packed column pairs (fewer LDS per pair).
 // POLY of every 8 staged points take their ex2 on the FMA pipe (ex2_poly2)
 // in the centred form: MUFU and FP32 balance at 2 (1/16·¾ = (4 + 8·¼)/128).
-template <int NC, int POLY>
-#ifndef FCPD_COL_MINB
-#define FCPD_COL_MINB 24  // pass-1 CTAs per SM (40 registers: C4 pass 1 −2.7 % against 16)
-#endif
-__global__ void __launch_bounds__(128 / NC, NC == 2 ? FCPD_COL_MINB : 8)
+// MINB: CTAs per SM (NC = 2).  Large passes (C3, C4) run 32 (32 registers;
+// the spills sit outside the inner loop): C4 pass 1 1.660 → 1.570 ms against
+// 16, C3 3.14 → 3.00; on short ones (C1: < 2 staged chunks per CTA) 16 is
+// the fastest (profiles/r2_pass_ab.txt).
+template <int NC, int POLY, int MINB = 16>
+__global__ void __launch_bounds__(128 / NC, NC == 2 ? MINB : 8)
     estep_col_kernel(const float4* __restrict__ xt4, int64_t m, const float4* __restrict__ y4,
                      int64_t n, IterState* __restrict__ st, WorkList wl_in,
                      double* __restrict__ seg, float centred_max_r2,
@@ -1496,7 +1497,16 @@ EStepPlan make_estep_plan(int64_t m, int64_t n, int sm_count) {
   p.col_pairs = ceil_div(m, kTile) * ceil_div(n, kTile) >= 1024 ? 2 : 1;
   if (const char* e = std::getenv("FCPD_COL_PAIRS")) p.col_pairs = std::atoi(e) == 1 ? 1 : 2;
   if (const char* e = std::getenv("FCPD_EX2_POLY")) p.ex2_poly = std::max(0, std::min(3, std::atoi(e)));
-  if (p.col_pairs == 2)
+  // 32 CTAs per SM where each still gets ≥ 8 staged 256-point chunks of the
+  // dense pass (point-units of the implicit list over 32·SMs CTAs)
+  {
+    const int64_t units = static_cast<int64_t>(ceil_div(n, kTile)) * ceil_div(m, kSubPts) * kSubPts;
+    p.col_minb = units / (static_cast<int64_t>(sm_count) * 32) >= 8 * kTile ? 32 : 16;
+    if (const char* e = std::getenv("FCPD_COL_MINB")) p.col_minb = std::atoi(e) == 32 ? 32 : 16;
+  }
+  if (p.col_pairs == 2 && p.col_minb == 32)
+    FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_col, estep_col_kernel<2, 0, 32>, 64, 0));
+  else if (p.col_pairs == 2)
     FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_col, estep_col_kernel<2, 0>, 64, 0));
   else
     FCPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_col, estep_col_kernel<1, 0>, 128, 0));
@@ -1617,7 +1627,14 @@ void launch_estep_pass1(const EStepPlan& p, const EStepBuffers& b, int64_t m, in
                static_cast<const float4*>(b.y4b), n, st, wl, b.col_seg, p.centred_max_r2, forms,
                stamps);
   };
-  if (p.col_pairs == 2) {
+  if (p.col_pairs == 2 && p.col_minb == 32) {
+    switch (p.ex2_poly) {
+      case 1: col(estep_col_kernel<2, 1, 32>, 64); break;
+      case 2: col(estep_col_kernel<2, 2, 32>, 64); break;
+      case 3: col(estep_col_kernel<2, 3, 32>, 64); break;
+      default: col(estep_col_kernel<2, 0, 32>, 64); break;
+    }
+  } else if (p.col_pairs == 2) {
     switch (p.ex2_poly) {
       case 1: col(estep_col_kernel<2, 1>, 64); break;
       case 2: col(estep_col_kernel<2, 2>, 64); break;

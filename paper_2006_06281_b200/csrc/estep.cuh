@@ -78,6 +78,7 @@ struct EStepPlan {
   int col_pairs = 2;  // pass 1: packed column pairs per thread (FCPD_COL_PAIRS=1 → 1)
   int flush2 = 64;  // fp32 run length of the pass-2 sums (FCPD_FLUSH2, power of two)
   int ex2_poly = 1;  // pass 1: of every 8 staged points, this many take ex2 on the FMA pipe (FCPD_EX2_POLY)
+  int col_minb = 16;  // pass 1: CTAs per SM, 16 or 32 (large passes; FCPD_COL_MINB)
   int col_blocks = 0, row_blocks = 0;  // scene tiles (pass-1 blocks), model tiles (pass 2)
   int col_grid = 0, row_grid = 0;      // persistent CTAs per pass
   size_t col_seg_doubles() const { return static_cast<size_t>(col_grid + col_blocks) * kTilePts; }
