@@ -633,6 +633,15 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : FCPD_ROW_MINB)
     }
     const BoxCentre bc = cta_box_centre(lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]);
     const bool centred = bc.r2 <= centred_max_r2;  // < 0 → difference form only
+    // fp32 run length of the centred sums: the conversion to Σw·t cancels
+    // terms of size R², so the rounding bound scales with run × R²; `flush`
+    // is the run for the largest radius the form allows (R² = 16), and a
+    // smaller block radius (the dense, large-σ² iterations) takes
+    // proportionally longer runs, up to a whole staged chunk, under the same
+    // bound
+    int run = flush;
+    if (centred)
+      while (run < kTile && bc.r2 * static_cast<float>(2 * run) <= kCentredMaxR2 * flush) run *= 2;
     // per-thread operands per row pair: centred → 2v (and v, |v|² for the
     // conversion); diff → −x'
     float v[kRows][4];
@@ -719,7 +728,7 @@ __global__ void __launch_bounds__(128 / NP, NP == 1 ? 8 : FCPD_ROW_MINB)
       };
       if (centred) {
         for (int j = 0; j < cnt8; j += 8) {
-          if (j > 0 && (j & (flush - 1)) == 0) flush_rows();  // uniform
+          if (j > 0 && (j & (run - 1)) == 0) flush_rows();  // uniform
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const float4 A = ya[j + u];
